@@ -1,0 +1,37 @@
+# Top-level build. `make` builds the product library and the oracle checker;
+# `make ref` additionally compiles the unmodified reference (needs
+# /root/reference, i.e. only in the build container).
+#
+#   paper_1108_1785_b200/lib/libgnetmon.so   product: sm_100a kernels + C-ABI
+#   paper_1108_1785_b200/lib/libgnm_synth.so synthetic flow generator (bench/tests)
+#   oracle/lib/liborc.so                     C restatement (test infrastructure)
+#   oracle/_ref/libflowmon_ref.so            unmodified reference (test infrastructure)
+
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
+           -Xptxas -v -cudart static -Iinclude
+PKG := paper_1108_1785_b200
+SRCS := $(PKG)/csrc/capi.cu $(PKG)/csrc/kernels.cu $(PKG)/csrc/registry.cpp
+HDRS := include/gnetmon.h $(PKG)/csrc/kernels.cuh $(PKG)/csrc/registry.hpp
+
+.PHONY: all ref clean oracle
+all: $(PKG)/lib/libgnetmon.so $(PKG)/lib/libgnm_synth.so oracle
+
+$(PKG)/lib/libgnetmon.so: $(SRCS) $(HDRS)
+	@mkdir -p $(PKG)/lib
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) 2> $(PKG)/lib/ptxas.log || (cat $(PKG)/lib/ptxas.log; false)
+
+$(PKG)/lib/libgnm_synth.so: $(PKG)/csrc/synth.c
+	@mkdir -p $(PKG)/lib
+	gcc -std=c11 -O2 -fPIC -shared -fopenmp -Wall -Wextra -o $@ $< -lm
+
+oracle:
+	$(MAKE) -C oracle all
+
+ref:
+	$(MAKE) -C oracle ref
+
+clean:
+	rm -rf $(PKG)/lib
+	$(MAKE) -C oracle clean

@@ -1,0 +1,259 @@
+/*
+ * gnetmon.h — C-ABI boundary of the B200-native G-NetMon flow-analysis hot path.
+ *
+ * This is the drop-in boundary for the reference's analytics layer
+ * (flowmon, /root/reference/proj). Every entry point below names the
+ * reference interface it replaces (file:line relative to
+ * /root/reference/proj/core). No C++ types, no exceptions and no torch types
+ * cross this boundary: plain pointers, sizes and an int status, plus a
+ * thread-local last-error string (gnm_last_error).
+ *
+ * Hot path:  classify -> attribute -> rate -> per-site
+ * aggregate (K2, sm_100a) -> per-site median/avg/flag (K3, sm_100a) ->
+ * streak rule (host).
+ */
+#ifndef GNETMON_H
+#define GNETMON_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GNM_ABI_VERSION 1
+
+/* rate_engine.hpp:18-20 */
+#define GNM_BUCKET_COUNT 10001
+#define GNM_BUCKET_WIDTH_BPS 10000.0
+#define GNM_RATE_CAP_BPS 100000000.0
+/* monitor.hpp:15 */
+#define GNM_DEFAULT_WARN_THRESHOLD_BPS 1000000.0
+
+#define GNM_NO_SITE 0xFFFFFFFFu
+
+/* Status codes. The reference throws; these map its exception kinds. */
+typedef enum gnm_status {
+    GNM_OK = 0,
+    GNM_ERR_INVALID_ARGUMENT = 1,
+    GNM_ERR_OVERLAP = 2,        /* CatalogError::Kind::Overlap      site_catalog.hpp:18 */
+    GNM_ERR_INVALID_CIDR = 3,   /* CatalogError::Kind::InvalidCidr  site_catalog.hpp:18 */
+    GNM_ERR_CUDA = 4,           /* any CUDA runtime error */
+    GNM_ERR_OUT_OF_MEMORY = 5,  /* std::bad_alloc / cudaErrorMemoryAllocation */
+    GNM_ERR_ZERO_DURATION = 6,  /* RateError::Kind::ZeroDuration    rate_engine.hpp:37 */
+    GNM_ERR_EMPTY_HISTOGRAM = 7,/* RateError::Kind::EmptyHistogram  rate_engine.hpp:37 */
+    GNM_ERR_NO_DEVICE = 8,      /* no CUDA device: there is no CPU fallback */
+    GNM_ERR_CAPACITY = 9        /* caller buffer too small */
+} gnm_status;
+
+/* FlowClass (rate_engine.hpp:31), same ordinal values. */
+typedef enum gnm_flow_class {
+    GNM_FORWARD = 0,
+    GNM_PURE_ACK = 1,
+    GNM_ADMINISTRATIVE = 2,
+    GNM_UNMATCHED = 3
+} gnm_flow_class;
+
+/* Thread-local message of the last failing call on this thread. */
+const char* gnm_last_error(void);
+int gnm_abi_version(void);
+
+/* ---- FilterParams (rate_engine.hpp:22-29) ------------------------------- */
+typedef struct gnm_filter_params {
+    uint32_t ack_avg_size_max; /* default 96  */
+    uint32_t min_packets;      /* default 20  */
+    uint32_t min_duration_ms;  /* default 100 */
+    uint32_t workers;          /* accepted, ignored: the GPU grid is the worker pool */
+} gnm_filter_params;
+
+void gnm_filter_params_default(gnm_filter_params* out);
+
+/* ---- Site registry: replaces SiteCatalog (site_catalog.hpp:50-97) -------- */
+typedef struct gnm_cidr {
+    uint32_t addr;      /* host byte order, as Cidr::addr (site_catalog.hpp:32) */
+    int32_t prefix_len; /* 1..32 */
+} gnm_cidr;
+
+typedef struct gnm_registry gnm_registry;
+
+/* Cidr::parse (site_catalog.cpp:48-66). GNM_ERR_INVALID_CIDR on bad text. */
+int gnm_cidr_parse(const char* text, gnm_cidr* out);
+/* parse_ipv4 (site_catalog.cpp:10-40). */
+int gnm_ipv4_parse(const char* text, uint32_t* out);
+
+int gnm_registry_create(gnm_registry** out);
+void gnm_registry_destroy(gnm_registry* reg);
+/* SiteCatalog::register_site (site_catalog.cpp:90-121): expands each CIDR
+ * into /24 tiles (longer prefixes round up to the enclosing /24), rejects
+ * overlap with GNM_ERR_OVERLAP and leaves the registry unchanged on error.
+ * Site ids are dense registration indices. */
+int gnm_registry_register_site(gnm_registry* reg, const char* name, const gnm_cidr* cidrs,
+                               size_t n_cidrs, uint32_t* out_site_id);
+/* SiteCatalog::lookup (site_catalog.hpp:99-112); GNM_NO_SITE when absent. */
+uint32_t gnm_registry_lookup(const gnm_registry* reg, uint32_t ip);
+/* SiteCatalog::sequential_lookup (site_catalog.hpp:114-122). */
+uint32_t gnm_registry_sequential_lookup(const gnm_registry* reg, uint32_t ip);
+size_t gnm_registry_site_count(const gnm_registry* reg);
+size_t gnm_registry_entry_count(const gnm_registry* reg);
+/* SiteCatalog::entries (site_catalog.hpp:77): (prefix24, site) in insertion
+ * order. Writes min(cap, entry_count) pairs. */
+size_t gnm_registry_entries(const gnm_registry* reg, uint32_t* prefix24, uint32_t* site,
+                            size_t cap);
+/* SiteCatalog::site(id).name; NULL when out of range. */
+const char* gnm_registry_site_name(const gnm_registry* reg, uint32_t site);
+/* Bumped by every successful registration (device copies re-upload lazily). */
+uint64_t gnm_registry_version(const gnm_registry* reg);
+
+/* ---- Flow batches ---------------------------------------------------------
+ * The hot columns of flowmon::FlowRecord (netflow.hpp:59-67): src_addr@0,
+ * dst_addr@4, d_pkts@16, d_octets@20, start_ms@48, end_ms@56. */
+typedef enum gnm_mem { GNM_MEM_HOST = 0, GNM_MEM_DEVICE = 1 } gnm_mem;
+
+typedef struct gnm_batch_soa {
+    const uint32_t* src_addr;
+    const uint32_t* dst_addr;
+    const uint32_t* d_pkts;
+    const uint32_t* d_octets;
+    const uint64_t* start_ms;
+    const uint64_t* end_ms;
+    uint64_t n;
+    int32_t mem; /* gnm_mem */
+} gnm_batch_soa;
+
+/* 64-byte records in the exact flowmon::FlowRecord layout (netflow.hpp:59-67). */
+typedef struct gnm_batch_aos {
+    const void* records;
+    uint64_t n;
+    int32_t mem; /* gnm_mem */
+} gnm_batch_aos;
+
+#define GNM_FLOW_RECORD_BYTES 64
+
+/* ---- Results: replaces AnalysisResult's site level (rate_engine.hpp:76-119) */
+typedef struct gnm_site_stats {
+    uint64_t flow_count;    /* RateStats::flow_count; 0 => site absent from result.sites */
+    uint64_t octets;        /* sum of d_octets over Forward flows (north_star byte sum) */
+    uint64_t rate_ubps_lo;  /* exact u128 sum of per-flow micro-bps (RateHistogram::sum_ubps_) */
+    uint64_t rate_ubps_hi;
+    double min_bps;         /* RateStats, rate_engine.cpp:242-253 */
+    double max_bps;
+    double avg_bps;         /* double(u128 sum) / 1e6 / count, host-converted like libgcc */
+    double median_bps;      /* bucket-midpoint lower median, clamped into [min,max] */
+    uint32_t below_threshold; /* median_bps < threshold_bps (K3 flag), 0 when empty */
+    uint32_t reserved;
+} gnm_site_stats;
+
+typedef struct gnm_tallies { /* ClassTallies rate_engine.hpp:101-110 */
+    uint64_t forward;
+    uint64_t pure_ack;
+    uint64_t administrative;
+    uint64_t unmatched;
+} gnm_tallies;
+
+typedef struct gnm_result {
+    /* inputs */
+    uint64_t window_start_ms; /* copied through, no filtering (rate_engine.cpp:257-258) */
+    uint64_t window_end_ms;
+    double threshold_bps;     /* for below_threshold; GNM_DEFAULT_WARN_THRESHOLD_BPS */
+    uint32_t sites_capacity;  /* rows available in sites[] (and histograms[]) */
+    gnm_site_stats* sites;    /* caller-owned host array; row = SiteId */
+    uint32_t* histograms;     /* optional caller-owned host [capacity * 10001]; NULL skips */
+    /* outputs */
+    uint32_t n_sites;         /* registry site count at call time (rows written) */
+    gnm_tallies tallies;
+} gnm_result;
+
+/* ---- Device context -------------------------------------------------------- */
+typedef struct gnm_ctx gnm_ctx;
+
+/* One context per host thread and GPU; calls on a context are serialized. */
+int gnm_ctx_create(int device, gnm_ctx** out);
+void gnm_ctx_destroy(gnm_ctx* ctx);
+/* Use an external cudaStream_t (NULL = the context's own stream). */
+int gnm_ctx_set_stream(gnm_ctx* ctx, void* cuda_stream);
+void* gnm_ctx_stream(gnm_ctx* ctx);
+/* Host-batch loader chunk (records per pinned double-buffer half). */
+int gnm_ctx_set_chunk_records(gnm_ctx* ctx, uint64_t records);
+
+/* aggregate() (rate_engine.cpp:335-347) + the K3 site synthesis
+ * (finalize/stats_from, rate_engine.cpp:242-292) in one synchronous call.
+ * Results are identical for any batch split (commutative monoid). */
+int gnm_analyze(gnm_ctx* ctx, const gnm_registry* reg, const gnm_filter_params* params,
+                const gnm_batch_soa* batch, gnm_result* result);
+int gnm_analyze_aos(gnm_ctx* ctx, const gnm_registry* reg, const gnm_filter_params* params,
+                    const gnm_batch_aos* batch, gnm_result* result);
+
+/* Split form, for streaming and multi-GPU: accumulate any number of batches
+ * into the context's device partials (K2, asynchronous on the context
+ * stream), optionally all-reduce the partials across GPUs, then finalize
+ * (K3 + result D2H + partial reset; synchronous). */
+int gnm_accumulate(gnm_ctx* ctx, const gnm_registry* reg, const gnm_filter_params* params,
+                   const gnm_batch_soa* batch);
+int gnm_accumulate_aos(gnm_ctx* ctx, const gnm_registry* reg, const gnm_filter_params* params,
+                       const gnm_batch_aos* batch);
+int gnm_finalize(gnm_ctx* ctx, const gnm_registry* reg, gnm_result* result);
+/* Drop accumulated partials without producing a result. */
+int gnm_reset(gnm_ctx* ctx);
+
+/* Device partials of the current accumulation, for a cross-GPU all-reduce
+ * (SURVEY.md §8e). All are device pointers on the context's device.
+ *   sums:  uint64 [n_sites*4 + 4]  reduce SUM  (per site: octets, ubps limb0,
+ *          limb1, limb2 (32-bit limbs); then tallies fwd, ack, admin, unmatched)
+ *   min:   float64 [n_sites]       reduce MIN  (+inf when empty)
+ *   max:   float64 [n_sites]       reduce MAX  (0 when empty)
+ *   hist:  uint32 [n_sites*10001]  reduce SUM */
+typedef struct gnm_partials {
+    uint64_t* sums;
+    double* min_bps;
+    double* max_bps;
+    uint32_t* hist;
+    uint64_t n_sites;
+    uint64_t sums_count;
+    uint64_t hist_count;
+} gnm_partials;
+int gnm_get_partials(gnm_ctx* ctx, const gnm_registry* reg, gnm_partials* out);
+
+/* Per-record classification (classify/attribute, rate_engine.cpp:71-86,
+ * 127-146): out[i] = class << 30 | (site & 0x3FFFFFFF), site = 0x3FFFFFFF
+ * unless Forward. `out` is a host or device pointer per out_mem. */
+int gnm_classify(gnm_ctx* ctx, const gnm_registry* reg, const gnm_filter_params* params,
+                 const gnm_batch_soa* batch, uint32_t* out, int32_t out_mem);
+
+/* Device time of the last analyze/accumulate/finalize, from CUDA events on
+ * the context stream. */
+typedef struct gnm_timing {
+    double accumulate_ms; /* K2 (sum over launches since the last finalize) */
+    double finalize_ms;   /* K3 */
+    double h2d_ms;        /* loader copies (host batches) */
+    uint64_t k2_launches;
+    uint64_t kernel_launches; /* every kernel this library launched since ctx creation */
+    uint64_t records;         /* records accumulated since the last finalize */
+} gnm_timing;
+int gnm_ctx_timing(gnm_ctx* ctx, gnm_timing* out);
+/* 1 = record CUDA events around every kernel (default 0). */
+int gnm_ctx_enable_timing(gnm_ctx* ctx, int enable);
+
+/* ---- Warning rule: evaluate_warnings (monitor.cpp:13-34) ----------------- */
+typedef struct gnm_warning_state gnm_warning_state;
+typedef struct gnm_warning {
+    uint32_t site;
+    uint32_t consecutive_bad_hours;
+    double median_bps;
+} gnm_warning;
+
+int gnm_warning_state_create(gnm_warning_state** out);
+void gnm_warning_state_destroy(gnm_warning_state* st);
+uint32_t gnm_warning_state_streak(const gnm_warning_state* st, uint32_t site);
+/* For every site with flow_count > 0 (ascending SiteId, as std::map
+ * iteration): median < threshold extends the streak, else resets it; every
+ * site at streak >= 2 warns. Zero-flow sites are frozen. Writes up to cap
+ * warnings and the total count to *n_out. */
+int gnm_evaluate_warnings(const gnm_result* result, gnm_warning_state* st, double threshold_bps,
+                          gnm_warning* out, size_t cap, size_t* n_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GNETMON_H */

@@ -1,0 +1,792 @@
+// capi.cu — the extern "C" boundary (include/gnetmon.h): registry, device
+// context, pinned double-buffered loader, K2/K3 orchestration and the
+// host-side streak rule. No exceptions cross the ABI; every entry point
+// returns a gnm_status and leaves a thread-local message on failure.
+//
+// There is no CPU fallback: without a CUDA device gnm_ctx_create fails with
+// GNM_ERR_NO_DEVICE and nothing else can run.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "gnetmon.h"
+#include "kernels.cuh"
+#include "registry.hpp"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+struct CudaError : std::runtime_error {
+    explicit CudaError(const std::string& m) : std::runtime_error(m) {}
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        if (e == cudaErrorMemoryAllocation) throw std::bad_alloc();
+        throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        return f();
+    } catch (const CudaError& e) {
+        return fail(GNM_ERR_CUDA, e.what());
+    } catch (const std::bad_alloc&) {
+        return fail(GNM_ERR_OUT_OF_MEMORY, "out of memory");
+    } catch (const std::exception& e) {
+        return fail(GNM_ERR_INVALID_ARGUMENT, e.what());
+    }
+}
+
+} // namespace
+
+struct gnm_registry {
+    gnm::Registry r;
+};
+
+struct gnm_warning_state {
+    std::map<uint32_t, uint32_t> streaks; // WarningState (monitor.hpp:20-37)
+};
+
+struct EventPair {
+    cudaEvent_t a = nullptr, b = nullptr;
+};
+
+struct gnm_ctx {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;
+
+    // registry cache (device table)
+    const gnm_registry* reg = nullptr;
+    uint64_t reg_version = ~0ull;
+    uint32_t* d_table = nullptr;
+    size_t table_cap_words = 0;
+    uint32_t table_words = 0;
+
+    // partials
+    gnm::DevPartials P{};
+    uint32_t partial_cap = 0;
+    bool accumulating = false;
+    const gnm_registry* acc_reg = nullptr;
+    uint64_t acc_version = 0;
+
+    // finalize output staging: n_sites rows + 32 B of tallies
+    gnm_site_stats* d_out = nullptr;
+    gnm_site_stats* h_out = nullptr;
+    size_t out_cap_rows = 0;
+
+    // loader: two device slots of `chunk` records, pinned host staging
+    uint64_t chunk = 1ull << 22;
+    unsigned char* d_stage[2] = {nullptr, nullptr};
+    unsigned char* h_stage[2] = {nullptr, nullptr};
+    size_t stage_bytes = 0;
+    size_t h_stage_bytes = 0;
+    cudaEvent_t ev_h2d[2] = {nullptr, nullptr};
+    cudaEvent_t ev_k2[2] = {nullptr, nullptr};
+
+    // timing
+    bool timing = false;
+    std::vector<EventPair> pool;
+    std::vector<EventPair> k2_pairs, k3_pairs, h2d_pairs;
+    double acc_ms = 0, fin_ms = 0, h2d_ms = 0;
+    uint64_t k2_launches = 0, kernel_launches = 0, records = 0;
+};
+
+namespace {
+
+EventPair take_pair(gnm_ctx* c) {
+    if (!c->pool.empty()) {
+        EventPair p = c->pool.back();
+        c->pool.pop_back();
+        return p;
+    }
+    EventPair p;
+    ck(cudaEventCreate(&p.a), "cudaEventCreate");
+    ck(cudaEventCreate(&p.b), "cudaEventCreate");
+    return p;
+}
+
+double drain_pairs(gnm_ctx* c, std::vector<EventPair>& v) {
+    double total = 0;
+    for (EventPair& p : v) {
+        float ms = 0;
+        ck(cudaEventSynchronize(p.b), "cudaEventSynchronize");
+        ck(cudaEventElapsedTime(&ms, p.a, p.b), "cudaEventElapsedTime");
+        total += ms;
+        c->pool.push_back(p);
+    }
+    v.clear();
+    return total;
+}
+
+gnm::DevParams dev_params(const gnm_filter_params* p) {
+    gnm_filter_params d;
+    gnm_filter_params_default(&d);
+    if (!p) p = &d;
+    gnm::DevParams q;
+    q.ack_plus1 = static_cast<uint64_t>(p->ack_avg_size_max) + 1;
+    q.min_packets = p->min_packets;
+    q.min_duration_ms = p->min_duration_ms;
+    return q;
+}
+
+// Upload the registry's device table when the context has not seen this
+// registry version (the catalog is rebuilt on update).
+void ensure_table(gnm_ctx* c, const gnm_registry* reg) {
+    if (c->reg == reg && c->reg_version == reg->r.version() && c->d_table) return;
+    gnm::DeviceTable t = reg->r.compile_device_table();
+    while (t.words.size() % 4) t.words.push_back(0); // uint4 smem copy
+    if (t.words.size() > c->table_cap_words) {
+        if (c->d_table) ck(cudaFree(c->d_table), "cudaFree");
+        c->d_table = nullptr;
+        ck(cudaMalloc(&c->d_table, t.words.size() * 4), "cudaMalloc(table)");
+        c->table_cap_words = t.words.size();
+    }
+    // The previous table may still be read by queued kernels.
+    ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    ck(cudaMemcpy(c->d_table, t.words.data(), t.words.size() * 4, cudaMemcpyHostToDevice),
+       "cudaMemcpy(table)");
+    c->table_words = static_cast<uint32_t>(t.words.size());
+    c->reg = reg;
+    c->reg_version = reg->r.version();
+}
+
+// Partials sized for the registry's site count; all-zero (min=+inf) at rest.
+void ensure_partials(gnm_ctx* c, uint32_t n_sites) {
+    if (n_sites > c->partial_cap || !c->P.sums) {
+        ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+        if (c->P.sums) {
+            cudaFree(c->P.sums);
+            cudaFree(c->P.mn);
+            cudaFree(c->P.mx);
+            cudaFree(c->P.hist);
+        }
+        c->P = gnm::DevPartials{};
+        const uint32_t cap = std::max<uint32_t>(n_sites, 1);
+        ck(cudaMalloc(&c->P.sums, (static_cast<size_t>(cap) * 4 + 4) * 8), "cudaMalloc(sums)");
+        ck(cudaMalloc(&c->P.mn, static_cast<size_t>(cap) * 8), "cudaMalloc(min)");
+        ck(cudaMalloc(&c->P.mx, static_cast<size_t>(cap) * 8), "cudaMalloc(max)");
+        ck(cudaMalloc(&c->P.hist, static_cast<size_t>(cap) * gnm::kBuckets * 4), "cudaMalloc(hist)");
+        c->P.n_sites = cap;
+        ck(gnm::launch_init_partials(c->P, c->stream), "init partials");
+        c->kernel_launches += 1;
+        c->partial_cap = cap;
+    }
+    if (c->P.n_sites != n_sites) {
+        // Tallies live after the last site row: move them (zero at rest).
+        c->P.n_sites = n_sites;
+        ck(cudaMemsetAsync(c->P.sums + static_cast<size_t>(n_sites) * 4, 0, 32, c->stream),
+           "cudaMemsetAsync");
+    }
+}
+
+void ensure_out(gnm_ctx* c, uint32_t n_sites) {
+    const size_t rows = static_cast<size_t>(n_sites) + 1; // + tallies
+    if (rows <= c->out_cap_rows) return;
+    ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    if (c->d_out) cudaFree(c->d_out);
+    if (c->h_out) cudaFreeHost(c->h_out);
+    c->d_out = nullptr;
+    c->h_out = nullptr;
+    ck(cudaMalloc(&c->d_out, rows * sizeof(gnm_site_stats)), "cudaMalloc(out)");
+    ck(cudaMallocHost(&c->h_out, rows * sizeof(gnm_site_stats)), "cudaMallocHost(out)");
+    c->out_cap_rows = rows;
+}
+
+void ensure_stage(gnm_ctx* c, size_t bytes_per_slot, bool need_host) {
+    if (bytes_per_slot > c->stage_bytes) {
+        ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+        ck(cudaStreamSynchronize(c->copy_stream), "cudaStreamSynchronize");
+        for (int i = 0; i < 2; ++i) {
+            if (c->d_stage[i]) cudaFree(c->d_stage[i]);
+            c->d_stage[i] = nullptr;
+        }
+        for (int i = 0; i < 2; ++i) ck(cudaMalloc(&c->d_stage[i], bytes_per_slot), "cudaMalloc(stage)");
+        c->stage_bytes = bytes_per_slot;
+    }
+    if (need_host && bytes_per_slot > c->h_stage_bytes) {
+        ck(cudaStreamSynchronize(c->copy_stream), "cudaStreamSynchronize");
+        for (int i = 0; i < 2; ++i) {
+            if (c->h_stage[i]) cudaFreeHost(c->h_stage[i]);
+            c->h_stage[i] = nullptr;
+        }
+        for (int i = 0; i < 2; ++i)
+            ck(cudaMallocHost(&c->h_stage[i], bytes_per_slot), "cudaMallocHost(stage)");
+        c->h_stage_bytes = bytes_per_slot;
+    }
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+int begin_accumulate(gnm_ctx* c, const gnm_registry* reg) {
+    if (c->accumulating && (c->acc_reg != reg || c->acc_version != reg->r.version()))
+        return fail(GNM_ERR_INVALID_ARGUMENT,
+                    "registry changed during an accumulation; finalize or reset first");
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    ensure_table(c, reg);
+    ensure_partials(c, static_cast<uint32_t>(reg->r.sites().size()));
+    if (!c->accumulating) {
+        c->accumulating = true;
+        c->acc_reg = reg;
+        c->acc_version = reg->r.version();
+        c->records = 0;
+    }
+    return GNM_OK;
+}
+
+void launch_k2_timed(gnm_ctx* c, bool aos, const gnm::DevSoA& soa, const void* aos_ptr,
+                     uint64_t n, const gnm::DevParams& p) {
+    if (n == 0) return;
+    const gnm::LaunchCfg cfg = gnm::k2_config(c->device, n, c->table_words, aos);
+    EventPair ev;
+    if (c->timing) {
+        ev = take_pair(c);
+        ck(cudaEventRecord(ev.a, c->stream), "cudaEventRecord");
+    }
+    if (aos) ck(gnm::launch_k2_aos(cfg, aos_ptr, n, c->d_table, c->table_words, p, c->P, c->stream), "K2 launch");
+    else ck(gnm::launch_k2_soa(cfg, soa, c->d_table, c->table_words, p, c->P, c->stream), "K2 launch");
+    if (c->timing) {
+        ck(cudaEventRecord(ev.b, c->stream), "cudaEventRecord");
+        c->k2_pairs.push_back(ev);
+    }
+    c->k2_launches += 1;
+    c->kernel_launches += 1;
+    c->records += n;
+}
+
+// Host batches: pinned, double-buffered H2D on the copy stream overlapped
+// with K2 on the compute stream, chunk by chunk (SURVEY.md §8 loader L1).
+// Columns already in pinned memory DMA straight from the caller's buffers;
+// pageable columns go through the context's pinned staging slots.
+void load_and_run(gnm_ctx* c, bool aos, const void* const* cols, const size_t* widths, int ncols,
+                  uint64_t n, const gnm::DevParams& p) {
+    size_t rec_bytes = 0;
+    bool pinned = true;
+    for (int i = 0; i < ncols; ++i) {
+        rec_bytes += widths[i];
+        pinned = pinned && is_pinned(cols[i]);
+    }
+    const uint64_t chunk = std::max<uint64_t>(1024, std::min<uint64_t>(c->chunk, n));
+    ensure_stage(c, chunk * rec_bytes, !pinned);
+    for (uint64_t base = 0, k = 0; base < n; base += chunk, ++k) {
+        const int slot = static_cast<int>(k & 1);
+        const uint64_t m = std::min<uint64_t>(chunk, n - base);
+        // The device slot is free once the K2 that last read it finished.
+        ck(cudaStreamWaitEvent(c->copy_stream, c->ev_k2[slot], 0), "cudaStreamWaitEvent");
+        EventPair ev;
+        if (c->timing) {
+            ev = take_pair(c);
+            ck(cudaEventRecord(ev.a, c->copy_stream), "cudaEventRecord");
+        }
+        unsigned char* dslot = c->d_stage[slot];
+        size_t off = 0;
+        const void* dcols[6];
+        if (!pinned) {
+            // The pinned slot is free once its previous H2D completed.
+            ck(cudaEventSynchronize(c->ev_h2d[slot]), "cudaEventSynchronize");
+            size_t hoff = 0;
+            for (int i = 0; i < ncols; ++i) {
+                std::memcpy(c->h_stage[slot] + hoff,
+                            static_cast<const unsigned char*>(cols[i]) + base * widths[i], m * widths[i]);
+                hoff += m * widths[i];
+            }
+            ck(cudaMemcpyAsync(dslot, c->h_stage[slot], hoff, cudaMemcpyHostToDevice, c->copy_stream),
+               "cudaMemcpyAsync(H2D)");
+            for (int i = 0; i < ncols; ++i) {
+                dcols[i] = dslot + off;
+                off += m * widths[i];
+            }
+        } else {
+            for (int i = 0; i < ncols; ++i) {
+                ck(cudaMemcpyAsync(dslot + off, static_cast<const unsigned char*>(cols[i]) + base * widths[i],
+                                   m * widths[i], cudaMemcpyHostToDevice, c->copy_stream),
+                   "cudaMemcpyAsync(H2D)");
+                dcols[i] = dslot + off;
+                off += m * widths[i];
+            }
+        }
+        if (c->timing) {
+            ck(cudaEventRecord(ev.b, c->copy_stream), "cudaEventRecord");
+            c->h2d_pairs.push_back(ev);
+        }
+        ck(cudaEventRecord(c->ev_h2d[slot], c->copy_stream), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(c->stream, c->ev_h2d[slot], 0), "cudaStreamWaitEvent");
+        if (aos) {
+            launch_k2_timed(c, true, gnm::DevSoA{}, dcols[0], m, p);
+        } else {
+            gnm::DevSoA b{static_cast<const uint32_t*>(dcols[0]), static_cast<const uint32_t*>(dcols[1]),
+                          static_cast<const uint32_t*>(dcols[2]), static_cast<const uint32_t*>(dcols[3]),
+                          static_cast<const uint64_t*>(dcols[4]), static_cast<const uint64_t*>(dcols[5]), m};
+            launch_k2_timed(c, false, b, nullptr, m, p);
+        }
+        ck(cudaEventRecord(c->ev_k2[slot], c->stream), "cudaEventRecord");
+    }
+    // The caller's host buffers may be reused once their copies are done.
+    ck(cudaStreamSynchronize(c->copy_stream), "cudaStreamSynchronize");
+}
+
+int check_soa(const gnm_batch_soa* b) {
+    if (!b) return fail(GNM_ERR_INVALID_ARGUMENT, "null batch");
+    if (b->n && (!b->src_addr || !b->dst_addr || !b->d_pkts || !b->d_octets || !b->start_ms || !b->end_ms))
+        return fail(GNM_ERR_INVALID_ARGUMENT, "null column in a non-empty batch");
+    if (b->mem != GNM_MEM_HOST && b->mem != GNM_MEM_DEVICE)
+        return fail(GNM_ERR_INVALID_ARGUMENT, "batch.mem must be GNM_MEM_HOST or GNM_MEM_DEVICE");
+    return GNM_OK;
+}
+
+int accumulate_soa(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* params,
+                   const gnm_batch_soa* b) {
+    if (int e = check_soa(b)) return e;
+    if (int e = begin_accumulate(c, reg)) return e;
+    const gnm::DevParams p = dev_params(params);
+    if (b->n == 0) return GNM_OK;
+    if (b->mem == GNM_MEM_DEVICE) {
+        gnm::DevSoA d{b->src_addr, b->dst_addr, b->d_pkts, b->d_octets, b->start_ms, b->end_ms, b->n};
+        launch_k2_timed(c, false, d, nullptr, b->n, p);
+    } else {
+        const void* cols[6] = {b->src_addr, b->dst_addr, b->d_pkts, b->d_octets, b->start_ms, b->end_ms};
+        const size_t widths[6] = {4, 4, 4, 4, 8, 8};
+        load_and_run(c, false, cols, widths, 6, b->n, p);
+    }
+    return GNM_OK;
+}
+
+int accumulate_aos(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* params,
+                   const gnm_batch_aos* b) {
+    if (!b) return fail(GNM_ERR_INVALID_ARGUMENT, "null batch");
+    if (b->n && !b->records) return fail(GNM_ERR_INVALID_ARGUMENT, "null records");
+    if (int e = begin_accumulate(c, reg)) return e;
+    const gnm::DevParams p = dev_params(params);
+    if (b->n == 0) return GNM_OK;
+    if (b->mem == GNM_MEM_DEVICE) {
+        launch_k2_timed(c, true, gnm::DevSoA{}, b->records, b->n, p);
+    } else {
+        const void* cols[1] = {b->records};
+        const size_t widths[1] = {GNM_FLOW_RECORD_BYTES};
+        load_and_run(c, true, cols, widths, 1, b->n, p);
+    }
+    return GNM_OK;
+}
+
+int finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* r) {
+    if (!r) return fail(GNM_ERR_INVALID_ARGUMENT, "null result");
+    const uint32_t n_sites = static_cast<uint32_t>(reg->r.sites().size());
+    if (r->sites_capacity < n_sites || (n_sites && !r->sites))
+        return fail(GNM_ERR_CAPACITY, "result.sites holds " + std::to_string(r->sites_capacity) +
+                                          " rows, registry has " + std::to_string(n_sites) + " sites");
+    if (int e = begin_accumulate(c, reg)) return e; // no-op when already accumulating
+    ensure_out(c, n_sites);
+    EventPair ev;
+    if (c->timing) {
+        ev = take_pair(c);
+        ck(cudaEventRecord(ev.a, c->stream), "cudaEventRecord");
+    }
+    const double thr = r->threshold_bps;
+    const bool export_hist = r->histograms != nullptr;
+    ck(gnm::launch_k3(c->device, c->P, thr, c->d_out, export_hist ? 0 : 1, c->stream), "K3 launch");
+    c->kernel_launches += 1;
+    if (c->timing) {
+        ck(cudaEventRecord(ev.b, c->stream), "cudaEventRecord");
+        c->k3_pairs.push_back(ev);
+    }
+    ck(cudaMemcpyAsync(c->h_out, c->d_out, (static_cast<size_t>(n_sites) + 1) * sizeof(gnm_site_stats),
+                       cudaMemcpyDeviceToHost, c->stream),
+       "cudaMemcpyAsync(D2H)");
+    if (export_hist) {
+        ck(cudaMemcpyAsync(r->histograms, c->P.hist, static_cast<size_t>(n_sites) * gnm::kBuckets * 4,
+                           cudaMemcpyDeviceToHost, c->stream),
+           "cudaMemcpyAsync(D2H hist)");
+        ck(gnm::launch_reset(c->device, c->P, c->stream), "reset launch");
+        c->kernel_launches += 1;
+    }
+    ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    for (uint32_t s = 0; s < n_sites; ++s) {
+        gnm_site_stats o = c->h_out[s];
+        // stats_from (rate_engine.cpp:250): avg = (double(u128)/1e6)/count,
+        // converted on the host exactly as the reference (libgcc RNE).
+        if (o.flow_count) {
+            const unsigned __int128 u =
+                static_cast<unsigned __int128>(o.rate_ubps_hi) << 64 | o.rate_ubps_lo;
+            o.avg_bps = (static_cast<double>(u) / 1e6) / static_cast<double>(o.flow_count);
+        }
+        r->sites[s] = o;
+    }
+    const auto* t = reinterpret_cast<const uint64_t*>(c->h_out + n_sites);
+    r->tallies.forward = t[0];
+    r->tallies.pure_ack = t[1];
+    r->tallies.administrative = t[2];
+    r->tallies.unmatched = t[3];
+    r->n_sites = n_sites;
+    if (c->timing) {
+        c->acc_ms = drain_pairs(c, c->k2_pairs);
+        c->fin_ms = drain_pairs(c, c->k3_pairs);
+        c->h2d_ms = drain_pairs(c, c->h2d_pairs);
+    }
+    c->accumulating = false;
+    return GNM_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+const char* gnm_last_error(void) { return g_last_error.c_str(); }
+int gnm_abi_version(void) { return GNM_ABI_VERSION; }
+
+void gnm_filter_params_default(gnm_filter_params* out) {
+    if (!out) return;
+    out->ack_avg_size_max = 96;
+    out->min_packets = 20;
+    out->min_duration_ms = 100;
+    out->workers = 1;
+}
+
+// ---- registry ----------------------------------------------------------------
+int gnm_cidr_parse(const char* text, gnm_cidr* out) {
+    if (!text || !out) return fail(GNM_ERR_INVALID_ARGUMENT, "null argument");
+    gnm::Cidr c;
+    std::string err;
+    if (!gnm::parse_cidr(text, &c, &err)) return fail(GNM_ERR_INVALID_CIDR, err);
+    out->addr = c.addr;
+    out->prefix_len = c.prefix_len;
+    return GNM_OK;
+}
+
+int gnm_ipv4_parse(const char* text, uint32_t* out) {
+    if (!text || !out) return fail(GNM_ERR_INVALID_ARGUMENT, "null argument");
+    std::string err;
+    if (!gnm::parse_ipv4(text, out, &err)) return fail(GNM_ERR_INVALID_CIDR, err);
+    return GNM_OK;
+}
+
+int gnm_registry_create(gnm_registry** out) {
+    if (!out) return fail(GNM_ERR_INVALID_ARGUMENT, "null out");
+    return guarded([&] {
+        *out = new gnm_registry();
+        return GNM_OK;
+    });
+}
+
+void gnm_registry_destroy(gnm_registry* reg) { delete reg; }
+
+int gnm_registry_register_site(gnm_registry* reg, const char* name, const gnm_cidr* cidrs,
+                               size_t n_cidrs, uint32_t* out_site_id) {
+    if (!reg || !name || (n_cidrs && !cidrs)) return fail(GNM_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        std::vector<gnm::Cidr> list(n_cidrs);
+        for (size_t i = 0; i < n_cidrs; ++i) list[i] = gnm::Cidr{cidrs[i].addr, cidrs[i].prefix_len};
+        std::string err;
+        uint32_t id = 0;
+        const int rc = reg->r.register_site(name, list, &id, &err);
+        if (rc == 2) return fail(GNM_ERR_OVERLAP, err);
+        if (rc == 3) return fail(GNM_ERR_INVALID_CIDR, err);
+        if (rc) return fail(GNM_ERR_CAPACITY, err);
+        if (out_site_id) *out_site_id = id;
+        return static_cast<int>(GNM_OK);
+    });
+}
+
+uint32_t gnm_registry_lookup(const gnm_registry* reg, uint32_t ip) {
+    return reg ? reg->r.lookup(ip) : GNM_NO_SITE;
+}
+uint32_t gnm_registry_sequential_lookup(const gnm_registry* reg, uint32_t ip) {
+    return reg ? reg->r.sequential_lookup(ip) : GNM_NO_SITE;
+}
+size_t gnm_registry_site_count(const gnm_registry* reg) { return reg ? reg->r.sites().size() : 0; }
+size_t gnm_registry_entry_count(const gnm_registry* reg) { return reg ? reg->r.entries().size() : 0; }
+size_t gnm_registry_entries(const gnm_registry* reg, uint32_t* prefix24, uint32_t* site, size_t cap) {
+    if (!reg) return 0;
+    const auto& e = reg->r.entries();
+    const size_t n = std::min(cap, e.size());
+    for (size_t i = 0; i < n; ++i) {
+        if (prefix24) prefix24[i] = e[i].first;
+        if (site) site[i] = e[i].second;
+    }
+    return e.size();
+}
+const char* gnm_registry_site_name(const gnm_registry* reg, uint32_t site) {
+    if (!reg || site >= reg->r.sites().size()) return nullptr;
+    return reg->r.sites()[site].name.c_str();
+}
+uint64_t gnm_registry_version(const gnm_registry* reg) { return reg ? reg->r.version() : 0; }
+
+// ---- context -------------------------------------------------------------------
+int gnm_ctx_create(int device, gnm_ctx** out) {
+    if (!out) return fail(GNM_ERR_INVALID_ARGUMENT, "null out");
+    *out = nullptr;
+    int count = 0;
+    const cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return fail(GNM_ERR_NO_DEVICE, std::string("no CUDA device (") + cudaGetErrorString(e) +
+                                           "): gnetmon has no CPU fallback");
+    }
+    if (device < 0 || device >= count)
+        return fail(GNM_ERR_INVALID_ARGUMENT, "device ordinal out of range");
+    return guarded([&] {
+        auto* c = new gnm_ctx();
+        try {
+            c->device = device;
+            ck(cudaSetDevice(device), "cudaSetDevice");
+            ck(gnm::init_kernel_attributes(), "kernel attributes");
+            ck(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+            ck(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+            c->stream = c->own_stream;
+            for (int i = 0; i < 2; ++i) {
+                ck(cudaEventCreateWithFlags(&c->ev_h2d[i], cudaEventDisableTiming), "cudaEventCreate");
+                ck(cudaEventCreateWithFlags(&c->ev_k2[i], cudaEventDisableTiming), "cudaEventCreate");
+            }
+        } catch (...) {
+            gnm_ctx_destroy(c);
+            throw;
+        }
+        *out = c;
+        return static_cast<int>(GNM_OK);
+    });
+}
+
+void gnm_ctx_destroy(gnm_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+    cudaFree(c->d_table);
+    cudaFree(c->P.sums);
+    cudaFree(c->P.mn);
+    cudaFree(c->P.mx);
+    cudaFree(c->P.hist);
+    cudaFree(c->d_out);
+    if (c->h_out) cudaFreeHost(c->h_out);
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(c->d_stage[i]);
+        if (c->h_stage[i]) cudaFreeHost(c->h_stage[i]);
+        if (c->ev_h2d[i]) cudaEventDestroy(c->ev_h2d[i]);
+        if (c->ev_k2[i]) cudaEventDestroy(c->ev_k2[i]);
+    }
+    for (auto* v : {&c->pool, &c->k2_pairs, &c->k3_pairs, &c->h2d_pairs})
+        for (EventPair& p : *v) {
+            cudaEventDestroy(p.a);
+            cudaEventDestroy(p.b);
+        }
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    delete c;
+}
+
+int gnm_ctx_set_stream(gnm_ctx* c, void* s) {
+    if (!c) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx");
+    return guarded([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+        c->stream = s ? static_cast<cudaStream_t>(s) : c->own_stream;
+        return static_cast<int>(GNM_OK);
+    });
+}
+
+void* gnm_ctx_stream(gnm_ctx* c) { return c ? c->stream : nullptr; }
+
+int gnm_ctx_set_chunk_records(gnm_ctx* c, uint64_t records) {
+    if (!c || records == 0) return fail(GNM_ERR_INVALID_ARGUMENT, "bad chunk");
+    c->chunk = records;
+    return GNM_OK;
+}
+
+int gnm_ctx_enable_timing(gnm_ctx* c, int enable) {
+    if (!c) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx");
+    c->timing = enable != 0;
+    return GNM_OK;
+}
+
+int gnm_ctx_timing(gnm_ctx* c, gnm_timing* out) {
+    if (!c || !out) return fail(GNM_ERR_INVALID_ARGUMENT, "null argument");
+    out->accumulate_ms = c->acc_ms;
+    out->finalize_ms = c->fin_ms;
+    out->h2d_ms = c->h2d_ms;
+    out->k2_launches = c->k2_launches;
+    out->kernel_launches = c->kernel_launches;
+    out->records = c->records;
+    return GNM_OK;
+}
+
+// ---- analysis ----------------------------------------------------------------
+int gnm_accumulate(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* params,
+                   const gnm_batch_soa* batch) {
+    if (!c || !reg) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx/registry");
+    return guarded([&] { return accumulate_soa(c, reg, params, batch); });
+}
+
+int gnm_accumulate_aos(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* params,
+                       const gnm_batch_aos* batch) {
+    if (!c || !reg) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx/registry");
+    return guarded([&] { return accumulate_aos(c, reg, params, batch); });
+}
+
+int gnm_finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* result) {
+    if (!c || !reg) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx/registry");
+    return guarded([&] { return finalize(c, reg, result); });
+}
+
+int gnm_reset(gnm_ctx* c) {
+    if (!c) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx");
+    return guarded([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        if (c->P.sums) {
+            ck(gnm::launch_reset(c->device, c->P, c->stream), "reset launch");
+            c->kernel_launches += 1;
+            ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+        }
+        drain_pairs(c, c->k2_pairs);
+        drain_pairs(c, c->k3_pairs);
+        drain_pairs(c, c->h2d_pairs);
+        c->accumulating = false;
+        return static_cast<int>(GNM_OK);
+    });
+}
+
+int gnm_analyze(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* params,
+                const gnm_batch_soa* batch, gnm_result* result) {
+    if (!c || !reg) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx/registry");
+    if (c->accumulating) return fail(GNM_ERR_INVALID_ARGUMENT, "an accumulation is in progress");
+    return guarded([&] {
+        if (int e = accumulate_soa(c, reg, params, batch)) return e;
+        return finalize(c, reg, result);
+    });
+}
+
+int gnm_analyze_aos(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* params,
+                    const gnm_batch_aos* batch, gnm_result* result) {
+    if (!c || !reg) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx/registry");
+    if (c->accumulating) return fail(GNM_ERR_INVALID_ARGUMENT, "an accumulation is in progress");
+    return guarded([&] {
+        if (int e = accumulate_aos(c, reg, params, batch)) return e;
+        return finalize(c, reg, result);
+    });
+}
+
+int gnm_get_partials(gnm_ctx* c, const gnm_registry* reg, gnm_partials* out) {
+    if (!c || !reg || !out) return fail(GNM_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        if (int e = begin_accumulate(c, reg)) return e;
+        out->sums = reinterpret_cast<uint64_t*>(c->P.sums);
+        out->min_bps = reinterpret_cast<double*>(c->P.mn);
+        out->max_bps = reinterpret_cast<double*>(c->P.mx);
+        out->hist = c->P.hist;
+        out->n_sites = c->P.n_sites;
+        out->sums_count = static_cast<uint64_t>(c->P.n_sites) * 4 + 4;
+        out->hist_count = static_cast<uint64_t>(c->P.n_sites) * gnm::kBuckets;
+        return static_cast<int>(GNM_OK);
+    });
+}
+
+int gnm_classify(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* params,
+                 const gnm_batch_soa* b, uint32_t* out, int32_t out_mem) {
+    if (!c || !reg || !out) return fail(GNM_ERR_INVALID_ARGUMENT, "null argument");
+    if (int e = check_soa(b)) return e;
+    return guarded([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        ensure_table(c, reg);
+        if (b->n == 0) return static_cast<int>(GNM_OK);
+        const gnm::DevParams p = dev_params(params);
+        std::vector<void*> temps;
+        auto dev_copy = [&](const void* h, size_t bytes) -> const void* {
+            void* d = nullptr;
+            ck(cudaMalloc(&d, bytes), "cudaMalloc");
+            temps.push_back(d);
+            ck(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream), "cudaMemcpyAsync");
+            return d;
+        };
+        int rc = GNM_OK;
+        try {
+            gnm::DevSoA d{b->src_addr, b->dst_addr, b->d_pkts, b->d_octets, b->start_ms, b->end_ms, b->n};
+            if (b->mem == GNM_MEM_HOST) {
+                d.src = static_cast<const uint32_t*>(dev_copy(b->src_addr, b->n * 4));
+                d.dst = static_cast<const uint32_t*>(dev_copy(b->dst_addr, b->n * 4));
+                d.pkts = static_cast<const uint32_t*>(dev_copy(b->d_pkts, b->n * 4));
+                d.octets = static_cast<const uint32_t*>(dev_copy(b->d_octets, b->n * 4));
+                d.start = static_cast<const uint64_t*>(dev_copy(b->start_ms, b->n * 8));
+                d.end = static_cast<const uint64_t*>(dev_copy(b->end_ms, b->n * 8));
+            }
+            uint32_t* dout = out;
+            if (out_mem == GNM_MEM_HOST) {
+                void* t = nullptr;
+                ck(cudaMalloc(&t, b->n * 4), "cudaMalloc");
+                temps.push_back(t);
+                dout = static_cast<uint32_t*>(t);
+            }
+            const gnm::LaunchCfg cfg = gnm::k2_config(c->device, b->n, c->table_words, false);
+            ck(gnm::launch_classify(cfg, d, c->d_table, c->table_words, p, dout, c->stream), "classify launch");
+            c->kernel_launches += 1;
+            if (out_mem == GNM_MEM_HOST)
+                ck(cudaMemcpyAsync(out, dout, b->n * 4, cudaMemcpyDeviceToHost, c->stream), "cudaMemcpyAsync");
+            ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+        } catch (...) {
+            for (void* t : temps) cudaFree(t);
+            throw;
+        }
+        for (void* t : temps) cudaFree(t);
+        return rc;
+    });
+}
+
+// ---- warnings -------------------------------------------------------------------
+int gnm_warning_state_create(gnm_warning_state** out) {
+    if (!out) return fail(GNM_ERR_INVALID_ARGUMENT, "null out");
+    return guarded([&] {
+        *out = new gnm_warning_state();
+        return static_cast<int>(GNM_OK);
+    });
+}
+void gnm_warning_state_destroy(gnm_warning_state* st) { delete st; }
+uint32_t gnm_warning_state_streak(const gnm_warning_state* st, uint32_t site) {
+    if (!st) return 0;
+    auto it = st->streaks.find(site);
+    return it == st->streaks.end() ? 0 : it->second;
+}
+
+// evaluate_warnings, monitor.cpp:13-34.
+int gnm_evaluate_warnings(const gnm_result* r, gnm_warning_state* st, double threshold,
+                          gnm_warning* out, size_t cap, size_t* n_out) {
+    if (!r || !st) return fail(GNM_ERR_INVALID_ARGUMENT, "null argument");
+    if (r->n_sites && !r->sites) return fail(GNM_ERR_INVALID_ARGUMENT, "null sites");
+    return guarded([&] {
+        size_t n = 0;
+        for (uint32_t s = 0; s < r->n_sites; ++s) {
+            const gnm_site_stats& ss = r->sites[s];
+            if (ss.flow_count == 0) continue; // frozen (monitor.cpp:18-20)
+            uint32_t& streak = st->streaks[s];
+            if (ss.median_bps < threshold) ++streak;
+            else streak = 0;
+            if (streak >= 2) {
+                if (n < cap && out) out[n] = gnm_warning{s, streak, ss.median_bps};
+                ++n;
+            }
+        }
+        if (n_out) *n_out = n;
+        return static_cast<int>(GNM_OK);
+    });
+}
+
+} // extern "C"

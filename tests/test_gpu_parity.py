@@ -1,0 +1,158 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the CPU oracle,
+bit-exact on every output of the site-level AnalysisResult."""
+import numpy as np
+import pytest
+
+import parity
+from paper_1108_1785_b200 import (FilterParams, FlowBatch, FlowRecords, SiteCatalog,
+                                  aggregate_partitioned, synth)
+
+pytestmark = pytest.mark.gpu
+
+
+def catalog_of(sites):
+    cat = SiteCatalog()
+    for i, cidrs in enumerate(sites):
+        cat.register_site(f"site{i}", cidrs)
+    return cat
+
+
+def layout_catalog(layout):
+    cat = SiteCatalog()
+    layout.register(cat)
+    return cat
+
+
+@pytest.mark.parametrize("on_device", [False, True])
+def test_engine_stress_set_bit_exact(engine, orc, on_device):
+    sites, cols = parity.engine_stress_set()
+    cat = catalog_of(sites)
+    batch = FlowBatch(*cols)
+    if on_device:
+        batch = batch.to_device()
+    res = engine.aggregate(batch, cat, histograms=True)
+    parity.assert_matches_oracle(res, parity.oracle_reference(orc, cat, cols))
+    assert res.tallies.total() == len(cols[0])
+
+
+def test_edge_set_bit_exact(engine, orc):
+    sites, cols = parity.edge_set()
+    cat = catalog_of(sites)
+    res = engine.aggregate(FlowBatch(*cols), cat, histograms=True)
+    parity.assert_matches_oracle(res, parity.oracle_reference(orc, cat, cols))
+
+
+def test_tiny_durations_third_limb(engine, orc):
+    sites, cols = parity.tiny_duration_set()
+    cat = catalog_of(sites)
+    params = FilterParams(min_duration_ms=0, min_packets=1)
+    res = engine.aggregate(FlowBatch(*cols), cat, params, histograms=True)
+    acc = parity.oracle_reference(orc, cat, cols, (96, 1, 0))
+    assert acc["ubps_hi"].max() > 0  # the quotient really exceeded 2^64
+    parity.assert_matches_oracle(res, acc)
+
+
+@pytest.mark.parametrize("name,n", [("D1", 100_000), ("D2", 300_000), ("D3", 400_000)])
+def test_workload_shapes_bit_exact(engine, orc, name, n):
+    w = synth.workload(name)
+    cols = synth.generate(w, n)
+    cat = layout_catalog(w.sites)
+    res = engine.aggregate(FlowBatch(*cols).to_device(), cat, histograms=(name != "D3"))
+    parity.assert_matches_oracle(res, parity.oracle_reference(orc, cat, cols))
+
+
+@pytest.mark.parametrize("params", [FilterParams(), FilterParams(ack_avg_size_max=200),
+                                    FilterParams(min_packets=50, min_duration_ms=500),
+                                    FilterParams(ack_avg_size_max=0xFFFFFFFF)])
+def test_filter_params(engine, orc, params):
+    sites, cols = parity.engine_stress_set(20_000, seed=17)
+    cat = catalog_of(sites)
+    res = engine.aggregate(FlowBatch(*cols), cat, params)
+    acc = parity.oracle_reference(orc, cat, cols, (params.ack_avg_size_max, params.min_packets,
+                                                   params.min_duration_ms))
+    parity.assert_matches_oracle(res, acc)
+
+
+def test_classify_matches_oracle(engine, orc):
+    sites, cols = parity.engine_stress_set()
+    cat = catalog_of(sites)
+    got = engine.classify(FlowBatch(*cols), cat)
+    p, s = cat.entries_arrays()
+    want = orc.classify(cols, orc.catalog(p, s))
+    np.testing.assert_array_equal(got, want)
+
+
+def test_classify_d2_mixed_prefixes(engine, orc):
+    w = synth.workload("D2")
+    cols = synth.generate(w, 200_000)
+    cat = layout_catalog(w.sites)
+    got = engine.classify(FlowBatch(*cols).to_device(), cat)
+    p, s = cat.entries_arrays()
+    np.testing.assert_array_equal(got, orc.classify(cols, orc.catalog(p, s)))
+
+
+def test_aos_equals_soa(engine):
+    w = synth.workload("D2")
+    cols = synth.generate(w, 100_000)
+    cat = layout_catalog(w.sites)
+    soa = engine.aggregate(FlowBatch(*cols), cat, histograms=True)
+    aos_host = engine.aggregate(FlowRecords(synth.to_aos(cols)), cat, histograms=True)
+    import torch
+    aos_dev = engine.aggregate(FlowRecords(torch.from_numpy(synth.to_aos(cols)).cuda()), cat,
+                               histograms=True)
+    for r in (aos_host, aos_dev):
+        np.testing.assert_array_equal(r.table, soa.table)
+        np.testing.assert_array_equal(r.histograms, soa.histograms)
+        assert r.tallies == soa.tallies
+
+
+def test_partition_and_chunk_independence(engine):
+    """acceptance.cpp:328-362 / engine_test.cpp:282-305 on the GPU: any batch
+    split and any loader chunking gives the identical result."""
+    sites, cols = parity.engine_stress_set(20_000, seed=41)
+    cat = catalog_of(sites)
+    batch = FlowBatch(*cols)
+    whole = engine.aggregate(batch, cat, histograms=True)
+    rng = np.random.default_rng(6)
+    for _ in range(5):
+        cuts = sorted(rng.integers(0, len(batch) + 1, rng.integers(1, 8)).tolist())
+        part = aggregate_partitioned(batch, cat, FilterParams(), cuts, histograms=True)
+        np.testing.assert_array_equal(part.table, whole.table)
+        np.testing.assert_array_equal(part.histograms, whole.histograms)
+    engine.set_chunk_records(1500)
+    try:
+        chunked = engine.aggregate(batch, cat, histograms=True)
+    finally:
+        engine.set_chunk_records(1 << 22)
+    np.testing.assert_array_equal(chunked.table, whole.table)
+
+
+def test_empty_and_no_forward(engine):
+    cat = catalog_of([["10.1.2.0/24"]])
+    empty = parity.make_cols([], [], [], [], [])
+    r = engine.aggregate(FlowBatch(*empty), cat)
+    assert r.sites == {} and r.tallies.total() == 0
+    # engine_test.cpp:330-342: ack, admin, unmatched, no forward flow.
+    cols = parity.make_cols([0x0A010203, 0x0A010203, 0xC0000001], [0, 0, 0xC0000002],
+                            [100, 5, 100], [4000, 4000, 1_000_000], [1000, 50, 1000])
+    r = engine.aggregate(FlowBatch(*cols), cat)
+    assert r.sites == {}
+    assert (r.tallies.pure_ack, r.tallies.administrative, r.tallies.unmatched,
+            r.tallies.forward) == (1, 1, 1, 0)
+
+
+def test_state_resets_between_calls(engine, orc):
+    """The device partials are all-zero at rest: back-to-back calls on
+    different data and registries do not leak into each other."""
+    sites, cols = parity.engine_stress_set(10_000, seed=3)
+    cat = catalog_of(sites)
+    for _ in range(3):
+        r = engine.aggregate(FlowBatch(*cols), cat)
+    parity.assert_matches_oracle(r, parity.oracle_reference(orc, cat, cols))
+    w = synth.workload("D1")
+    c2 = synth.generate(w, 50_000)
+    cat2 = layout_catalog(w.sites)
+    r2 = engine.aggregate(FlowBatch(*c2), cat2)
+    parity.assert_matches_oracle(r2, parity.oracle_reference(orc, cat2, c2))
+    r3 = engine.aggregate(FlowBatch(*cols), cat)
+    np.testing.assert_array_equal(r3.table, r.table)
