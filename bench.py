@@ -292,7 +292,7 @@ def main():
         ev0.record(stream)
         for _ in range(steps):
             res = step(batch)
-            k2_ms.append(eng.timing()["accumulate_ms"])
+            k2_ms.append(eng.timing())
         ev1.record(stream)
         barrier()
         ms = ev0.elapsed_time(ev1)
@@ -312,7 +312,9 @@ def main():
     total = n * world
     value = total * args.steps / (ms / 1e3)
     e2e_value = total * e2e_steps / (e2e_ms / 1e3)
-    k2_avg = statistics.mean(k2_ms)
+    k2_avg = statistics.mean(t["accumulate_ms"] for t in k2_ms)
+    plan_avg = statistics.mean(t["plan_ms"] for t in k2_ms)
+    k3_avg = statistics.mean(t["finalize_ms"] for t in k2_ms)
     peak, peak_kind = load_peaks()
     achieved = n * ALG_BYTES_PER_RECORD / (k2_avg / 1e3) / 1e9
     traffic = load_traffic(args.workload)
@@ -344,6 +346,8 @@ def main():
         "gpu_launches": launches,
         "clocks": clk,
         "kernel_share": k2_avg / (ms / args.steps),
+        "breakdown_ms": {"k1_plan": plan_avg, "k2": k2_avg, "k3_finalize": k3_avg,
+                         "step": ms / args.steps},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

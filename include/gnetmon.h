@@ -175,6 +175,15 @@ int gnm_ctx_set_stream(gnm_ctx* ctx, void* cuda_stream);
 void* gnm_ctx_stream(gnm_ctx* ctx);
 /* Host-batch loader chunk (records per pinned double-buffer half). */
 int gnm_ctx_set_chunk_records(gnm_ctx* ctx, uint64_t records);
+/* Block-private accumulation of hot (heavily hit) sites:
+ * GNM_HOT_AUTO (default) plans it per batch from a 1/64 sample when the batch
+ * is large and skewed enough; GNM_HOT_OFF never; GNM_HOT_FORCE always (every
+ * sampled site up to the slot capacity; a test hook). Results are identical
+ * in every mode. */
+#define GNM_HOT_OFF 0
+#define GNM_HOT_AUTO 1
+#define GNM_HOT_FORCE 2
+int gnm_ctx_set_hot_mode(gnm_ctx* ctx, int mode);
 
 /* aggregate() (rate_engine.cpp:335-347) + the K3 site synthesis
  * (finalize/stats_from, rate_engine.cpp:242-292) in one synchronous call.
@@ -229,6 +238,7 @@ typedef struct gnm_timing {
     uint64_t k2_launches;
     uint64_t kernel_launches; /* every kernel this library launched since ctx creation */
     uint64_t records;         /* records accumulated since the last finalize */
+    double plan_ms;           /* K1 hot-site planning (sample, assign, table slots) */
 } gnm_timing;
 int gnm_ctx_timing(gnm_ctx* ctx, gnm_timing* out);
 /* 1 = record CUDA events around every kernel (default 0). */

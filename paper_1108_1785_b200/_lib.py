@@ -32,6 +32,10 @@ ERR_EMPTY_HISTOGRAM = 7
 ERR_NO_DEVICE = 8
 ERR_CAPACITY = 9
 
+HOT_OFF = 0
+HOT_AUTO = 1
+HOT_FORCE = 2
+
 MEM_HOST = 0
 MEM_DEVICE = 1
 
@@ -76,7 +80,8 @@ class gnm_partials(C.Structure):
 class gnm_timing(C.Structure):
     _fields_ = [("accumulate_ms", C.c_double), ("finalize_ms", C.c_double),
                 ("h2d_ms", C.c_double), ("k2_launches", C.c_uint64),
-                ("kernel_launches", C.c_uint64), ("records", C.c_uint64)]
+                ("kernel_launches", C.c_uint64), ("records", C.c_uint64),
+                ("plan_ms", C.c_double)]
 
 
 class gnm_warning(C.Structure):
@@ -127,6 +132,7 @@ _SIGS = [
     ("gnm_ctx_set_stream", C.c_int, [_P, _P]),
     ("gnm_ctx_stream", _P, [_P]),
     ("gnm_ctx_set_chunk_records", C.c_int, [_P, C.c_uint64]),
+    ("gnm_ctx_set_hot_mode", C.c_int, [_P, C.c_int]),
     ("gnm_analyze", C.c_int,
      [_P, _P, C.POINTER(gnm_filter_params), C.POINTER(gnm_batch_soa), C.POINTER(gnm_result)]),
     ("gnm_analyze_aos", C.c_int,

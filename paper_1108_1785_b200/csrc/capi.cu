@@ -77,10 +77,12 @@ struct gnm_ctx {
     uint64_t reg_version = ~0ull;
     uint32_t* d_table = nullptr;
     size_t table_cap_words = 0;
-    uint32_t table_words = 0;
+    gnm::DevTable table{};
+    int hot_mode = GNM_HOT_AUTO;
 
     // partials
     gnm::DevPartials P{};
+    uint32_t* d_scratch = nullptr; // hot-site plan: counts, site->slot, slot->site, counter
     uint32_t partial_cap = 0;
     bool accumulating = false;
     const gnm_registry* acc_reg = nullptr;
@@ -103,8 +105,9 @@ struct gnm_ctx {
     // timing
     bool timing = false;
     std::vector<EventPair> pool;
-    std::vector<EventPair> k2_pairs, k3_pairs, h2d_pairs;
-    double acc_ms = 0, fin_ms = 0, h2d_ms = 0;
+    std::vector<EventPair> k2_pairs, k3_pairs, h2d_pairs, plan_pairs;
+    double acc_ms = 0, fin_ms = 0, h2d_ms = 0, plan_ms = 0;
+    int occ[2] = {0, 0}; // K2 blocks/SM (cold, hot) for the current table size
     uint64_t k2_launches = 0, kernel_launches = 0, records = 0;
 };
 
@@ -135,7 +138,7 @@ double drain_pairs(gnm_ctx* c, std::vector<EventPair>& v) {
     return total;
 }
 
-gnm::DevParams dev_params(const gnm_filter_params* p) {
+gnm::DevParams dev_params(const gnm_ctx* c, const gnm_filter_params* p) {
     gnm_filter_params d;
     gnm_filter_params_default(&d);
     if (!p) p = &d;
@@ -143,6 +146,7 @@ gnm::DevParams dev_params(const gnm_filter_params* p) {
     q.ack_plus1 = static_cast<uint64_t>(p->ack_avg_size_max) + 1;
     q.min_packets = p->min_packets;
     q.min_duration_ms = p->min_duration_ms;
+    q.site_mask = c->table.packed ? gnm::kPackedSiteMask : 0x7FFFFFFFu;
     return q;
 }
 
@@ -162,7 +166,12 @@ void ensure_table(gnm_ctx* c, const gnm_registry* reg) {
     ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
     ck(cudaMemcpy(c->d_table, t.words.data(), t.words.size() * 4, cudaMemcpyHostToDevice),
        "cudaMemcpy(table)");
-    c->table_words = static_cast<uint32_t>(t.words.size());
+    c->table.words = c->d_table;
+    c->table.n_words = static_cast<uint32_t>(t.words.size());
+    c->table.node_begin = t.node_begin;
+    c->table.leaf_begin = t.leaf_begin;
+    c->table.packed = t.packed;
+    c->occ[0] = c->occ[1] = 0;
     c->reg = reg;
     c->reg_version = reg->r.version();
 }
@@ -176,6 +185,8 @@ void ensure_partials(gnm_ctx* c, uint32_t n_sites) {
             cudaFree(c->P.mn);
             cudaFree(c->P.mx);
             cudaFree(c->P.hist);
+            cudaFree(c->d_scratch);
+            c->d_scratch = nullptr;
         }
         c->P = gnm::DevPartials{};
         const uint32_t cap = std::max<uint32_t>(n_sites, 1);
@@ -183,6 +194,9 @@ void ensure_partials(gnm_ctx* c, uint32_t n_sites) {
         ck(cudaMalloc(&c->P.mn, static_cast<size_t>(cap) * 8), "cudaMalloc(min)");
         ck(cudaMalloc(&c->P.mx, static_cast<size_t>(cap) * 8), "cudaMalloc(max)");
         ck(cudaMalloc(&c->P.hist, static_cast<size_t>(cap) * gnm::kBuckets * 4), "cudaMalloc(hist)");
+        const size_t scratch_words = 2 * static_cast<size_t>(cap) + gnm::kHotStride + 1;
+        ck(cudaMalloc(&c->d_scratch, scratch_words * 4), "cudaMalloc(scratch)");
+        ck(cudaMemsetAsync(c->d_scratch, 0, scratch_words * 4, c->stream), "cudaMemsetAsync");
         c->P.n_sites = cap;
         ck(gnm::launch_init_partials(c->P, c->stream), "init partials");
         c->kernel_launches += 1;
@@ -257,24 +271,56 @@ int begin_accumulate(gnm_ctx* c, const gnm_registry* reg) {
     return GNM_OK;
 }
 
-void launch_k2_timed(gnm_ctx* c, bool aos, const gnm::DevSoA& soa, const void* aos_ptr,
-                     uint64_t n, const gnm::DevParams& p) {
-    if (n == 0) return;
-    const gnm::LaunchCfg cfg = gnm::k2_config(c->device, n, c->table_words, aos);
-    EventPair ev;
+void launch_k2_timed(gnm_ctx* c, const gnm::DevBatch& b, const gnm::DevParams& p) {
+    if (b.n == 0) return;
+    EventPair pe, ev;
     if (c->timing) {
+        pe = take_pair(c);
+        ck(cudaEventRecord(pe.a, c->stream), "cudaEventRecord");
+    }
+    // K1: hot-site plan for this batch (skipped when no site can be hot).
+    const gnm::LaunchCfg cold = gnm::k2_config(c->device, b.n, c->table.n_words, false, c->occ);
+    bool hot = false;
+    if (c->hot_mode != GNM_HOT_OFF) {
+        cudaError_t e;
+        hot = gnm::plan_hot(c->device, b, c->table, p, c->P.n_sites, c->d_scratch, cold.grid,
+                            c->hot_mode == GNM_HOT_FORCE, c->stream, &c->kernel_launches, &e);
+        ck(e, "hot-site plan");
+    }
+    const gnm::LaunchCfg cfg = hot ? gnm::k2_config(c->device, b.n, c->table.n_words, true, c->occ) : cold;
+    gnm::DevHot h{c->d_scratch + 2 * static_cast<size_t>(c->P.n_sites), hot ? gnm::kHotSlots : 0u};
+    if (c->timing) {
+        ck(cudaEventRecord(pe.b, c->stream), "cudaEventRecord");
+        c->plan_pairs.push_back(pe);
         ev = take_pair(c);
         ck(cudaEventRecord(ev.a, c->stream), "cudaEventRecord");
     }
-    if (aos) ck(gnm::launch_k2_aos(cfg, aos_ptr, n, c->d_table, c->table_words, p, c->P, c->stream), "K2 launch");
-    else ck(gnm::launch_k2_soa(cfg, soa, c->d_table, c->table_words, p, c->P, c->stream), "K2 launch");
+    ck(gnm::launch_k2(cfg, b, c->table, p, c->P, h, c->stream), "K2 launch");
     if (c->timing) {
         ck(cudaEventRecord(ev.b, c->stream), "cudaEventRecord");
         c->k2_pairs.push_back(ev);
     }
     c->k2_launches += 1;
     c->kernel_launches += 1;
-    c->records += n;
+    c->records += b.n;
+}
+
+gnm::DevBatch soa_batch(const void* const* cols, uint64_t n) {
+    gnm::DevBatch b{};
+    b.aos = false;
+    b.soa = gnm::DevSoA{static_cast<const uint32_t*>(cols[0]), static_cast<const uint32_t*>(cols[1]),
+                        static_cast<const uint32_t*>(cols[2]), static_cast<const uint32_t*>(cols[3]),
+                        static_cast<const uint64_t*>(cols[4]), static_cast<const uint64_t*>(cols[5]), n};
+    b.n = n;
+    return b;
+}
+
+gnm::DevBatch aos_batch(const void* rec, uint64_t n) {
+    gnm::DevBatch b{};
+    b.aos = true;
+    b.rec = rec;
+    b.n = n;
+    return b;
 }
 
 // Host batches: pinned, double-buffered H2D on the copy stream overlapped
@@ -334,14 +380,7 @@ void load_and_run(gnm_ctx* c, bool aos, const void* const* cols, const size_t* w
         }
         ck(cudaEventRecord(c->ev_h2d[slot], c->copy_stream), "cudaEventRecord");
         ck(cudaStreamWaitEvent(c->stream, c->ev_h2d[slot], 0), "cudaStreamWaitEvent");
-        if (aos) {
-            launch_k2_timed(c, true, gnm::DevSoA{}, dcols[0], m, p);
-        } else {
-            gnm::DevSoA b{static_cast<const uint32_t*>(dcols[0]), static_cast<const uint32_t*>(dcols[1]),
-                          static_cast<const uint32_t*>(dcols[2]), static_cast<const uint32_t*>(dcols[3]),
-                          static_cast<const uint64_t*>(dcols[4]), static_cast<const uint64_t*>(dcols[5]), m};
-            launch_k2_timed(c, false, b, nullptr, m, p);
-        }
+        launch_k2_timed(c, aos ? aos_batch(dcols[0], m) : soa_batch(dcols, m), p);
         ck(cudaEventRecord(c->ev_k2[slot], c->stream), "cudaEventRecord");
     }
     // The caller's host buffers may be reused once their copies are done.
@@ -361,11 +400,11 @@ int accumulate_soa(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params*
                    const gnm_batch_soa* b) {
     if (int e = check_soa(b)) return e;
     if (int e = begin_accumulate(c, reg)) return e;
-    const gnm::DevParams p = dev_params(params);
+    const gnm::DevParams p = dev_params(c, params);
     if (b->n == 0) return GNM_OK;
     if (b->mem == GNM_MEM_DEVICE) {
-        gnm::DevSoA d{b->src_addr, b->dst_addr, b->d_pkts, b->d_octets, b->start_ms, b->end_ms, b->n};
-        launch_k2_timed(c, false, d, nullptr, b->n, p);
+        const void* cols[6] = {b->src_addr, b->dst_addr, b->d_pkts, b->d_octets, b->start_ms, b->end_ms};
+        launch_k2_timed(c, soa_batch(cols, b->n), p);
     } else {
         const void* cols[6] = {b->src_addr, b->dst_addr, b->d_pkts, b->d_octets, b->start_ms, b->end_ms};
         const size_t widths[6] = {4, 4, 4, 4, 8, 8};
@@ -379,10 +418,10 @@ int accumulate_aos(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params*
     if (!b) return fail(GNM_ERR_INVALID_ARGUMENT, "null batch");
     if (b->n && !b->records) return fail(GNM_ERR_INVALID_ARGUMENT, "null records");
     if (int e = begin_accumulate(c, reg)) return e;
-    const gnm::DevParams p = dev_params(params);
+    const gnm::DevParams p = dev_params(c, params);
     if (b->n == 0) return GNM_OK;
     if (b->mem == GNM_MEM_DEVICE) {
-        launch_k2_timed(c, true, gnm::DevSoA{}, b->records, b->n, p);
+        launch_k2_timed(c, aos_batch(b->records, b->n), p);
     } else {
         const void* cols[1] = {b->records};
         const size_t widths[1] = {GNM_FLOW_RECORD_BYTES};
@@ -442,6 +481,7 @@ int finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* r) {
     r->n_sites = n_sites;
     if (c->timing) {
         c->acc_ms = drain_pairs(c, c->k2_pairs);
+        c->plan_ms = drain_pairs(c, c->plan_pairs);
         c->fin_ms = drain_pairs(c, c->k3_pairs);
         c->h2d_ms = drain_pairs(c, c->h2d_pairs);
     }
@@ -578,6 +618,7 @@ void gnm_ctx_destroy(gnm_ctx* c) {
     cudaFree(c->P.mn);
     cudaFree(c->P.mx);
     cudaFree(c->P.hist);
+    cudaFree(c->d_scratch);
     cudaFree(c->d_out);
     if (c->h_out) cudaFreeHost(c->h_out);
     for (int i = 0; i < 2; ++i) {
@@ -586,7 +627,7 @@ void gnm_ctx_destroy(gnm_ctx* c) {
         if (c->ev_h2d[i]) cudaEventDestroy(c->ev_h2d[i]);
         if (c->ev_k2[i]) cudaEventDestroy(c->ev_k2[i]);
     }
-    for (auto* v : {&c->pool, &c->k2_pairs, &c->k3_pairs, &c->h2d_pairs})
+    for (auto* v : {&c->pool, &c->k2_pairs, &c->k3_pairs, &c->h2d_pairs, &c->plan_pairs})
         for (EventPair& p : *v) {
             cudaEventDestroy(p.a);
             cudaEventDestroy(p.b);
@@ -614,6 +655,12 @@ int gnm_ctx_set_chunk_records(gnm_ctx* c, uint64_t records) {
     return GNM_OK;
 }
 
+int gnm_ctx_set_hot_mode(gnm_ctx* c, int mode) {
+    if (!c || mode < GNM_HOT_OFF || mode > GNM_HOT_FORCE) return fail(GNM_ERR_INVALID_ARGUMENT, "bad hot mode");
+    c->hot_mode = mode;
+    return GNM_OK;
+}
+
 int gnm_ctx_enable_timing(gnm_ctx* c, int enable) {
     if (!c) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx");
     c->timing = enable != 0;
@@ -623,6 +670,7 @@ int gnm_ctx_enable_timing(gnm_ctx* c, int enable) {
 int gnm_ctx_timing(gnm_ctx* c, gnm_timing* out) {
     if (!c || !out) return fail(GNM_ERR_INVALID_ARGUMENT, "null argument");
     out->accumulate_ms = c->acc_ms;
+    out->plan_ms = c->plan_ms;
     out->finalize_ms = c->fin_ms;
     out->h2d_ms = c->h2d_ms;
     out->k2_launches = c->k2_launches;
@@ -659,6 +707,7 @@ int gnm_reset(gnm_ctx* c) {
             ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
         }
         drain_pairs(c, c->k2_pairs);
+        drain_pairs(c, c->plan_pairs);
         drain_pairs(c, c->k3_pairs);
         drain_pairs(c, c->h2d_pairs);
         c->accumulating = false;
@@ -709,7 +758,7 @@ int gnm_classify(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* p
         ck(cudaSetDevice(c->device), "cudaSetDevice");
         ensure_table(c, reg);
         if (b->n == 0) return static_cast<int>(GNM_OK);
-        const gnm::DevParams p = dev_params(params);
+        const gnm::DevParams p = dev_params(c, params);
         std::vector<void*> temps;
         auto dev_copy = [&](const void* h, size_t bytes) -> const void* {
             void* d = nullptr;
@@ -736,8 +785,8 @@ int gnm_classify(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* p
                 temps.push_back(t);
                 dout = static_cast<uint32_t*>(t);
             }
-            const gnm::LaunchCfg cfg = gnm::k2_config(c->device, b->n, c->table_words, false);
-            ck(gnm::launch_classify(cfg, d, c->d_table, c->table_words, p, dout, c->stream), "classify launch");
+            const gnm::LaunchCfg cfg = gnm::k2_config(c->device, b->n, c->table.n_words, false, c->occ);
+            ck(gnm::launch_classify(cfg, d, c->table, p, dout, c->stream), "classify launch");
             c->kernel_launches += 1;
             if (out_mem == GNM_MEM_HOST)
                 ck(cudaMemcpyAsync(out, dout, b->n * 4, cudaMemcpyDeviceToHost, c->stream), "cudaMemcpyAsync");

@@ -1,6 +1,8 @@
 // kernels.cu — sm_100a kernels of the flow-analysis hot path.
 //
-//   K2  k2_soa / k2_aos   classify -> attribute -> rate -> per-site aggregate
+//   K1  k_sample, k_hot_assign, k_table_slots
+//                         hot-site plan for skewed batches (see plan_hot)
+//   K2  k2                classify -> attribute -> rate -> per-site aggregate
 //                         (reduce_slice, rate_engine.cpp:197-240 + add :9-23)
 //   K3  k3_finalize       per-site count / median / clamp / flag
 //                         (finalize + stats_from + median_bps,
@@ -13,8 +15,15 @@
 // record, no tensor cores. K2 streams the six SoA columns with 128-bit
 // non-allocating loads (4 records per thread per iteration), probes a
 // shared-memory-resident radix table (registry.hpp), and reduces into
-// order-independent integer/min/max accumulators in HBM/L2, so the result is
+// order-independent integer/min/max accumulators, so the result is
 // bit-identical to the reference for any grid, partitioning or GPU count.
+//
+// Contention: with Zipf-distributed sites the hottest site receives ~10% of
+// all Forward flows, and same-address L2 atomics serialise (~1 ns each). The
+// scalar sums of the hot sites (chosen per call by K1 from a 1/64 sample) are
+// therefore accumulated in block-private shared memory with native 32-bit
+// atomics and explicit carry propagation, and flushed once per CTA; cold
+// sites and every histogram bucket go straight to L2 with RED.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -26,6 +35,9 @@ namespace {
 
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr int kK2Block = 512;
+constexpr size_t kHotBytes = kHotStride * (5 * 4 + 2 * 8);
+constexpr size_t kSmemMax = 227 * 1024;
+constexpr size_t kSmemTableMax = kSmemMax - kHotBytes - 1024;
 
 extern __shared__ __align__(16) uint32_t g_smem[];
 
@@ -58,7 +70,8 @@ __device__ __forceinline__ uint2 table_pair(const uint32_t* __restrict__ gt, uin
 }
 
 // SiteCatalog::lookup (site_catalog.hpp:99-112) over the radix table:
-// one LDS.64 for a miss, three dependent LDS for a /24 hit.
+// one LDS.64 for a miss, three dependent LDS for a /24 hit. Returns the
+// packed (slot << 20 | site) value, or kNone.
 template <bool kSmem>
 __device__ __forceinline__ uint32_t lookup(const uint32_t* __restrict__ gt, uint32_t ip) {
     const uint32_t d = ip >> 16;
@@ -76,7 +89,42 @@ __device__ __forceinline__ void load_table(const uint32_t* __restrict__ gt, uint
         const uint4* g4 = reinterpret_cast<const uint4*>(gt);
         uint4* s4 = reinterpret_cast<uint4*>(g_smem);
         for (uint32_t i = threadIdx.x; i < words / 4; i += blockDim.x) s4[i] = __ldg(g4 + i);
-        __syncthreads();
+    }
+}
+
+// ---- block-private hot-site accumulators ---------------------------------
+struct HotSmem {
+    uint32_t* oct_lo;          // octets, 64-bit as two u32 with carry
+    uint32_t* oct_hi;
+    uint32_t* u0;              // micro-bps, 96-bit as three u32 with carries
+    uint32_t* u1;
+    uint32_t* u2;
+    unsigned long long* mn;    // f64 bits
+    unsigned long long* mx;
+};
+
+__device__ __forceinline__ HotSmem hot_smem(uint32_t table_words_in_smem) {
+    uint32_t* base = g_smem + table_words_in_smem;
+    HotSmem h;
+    h.oct_lo = base;
+    h.oct_hi = base + kHotStride;
+    h.u0 = base + 2 * kHotStride;
+    h.u1 = base + 3 * kHotStride;
+    h.u2 = base + 4 * kHotStride;
+    h.mn = reinterpret_cast<unsigned long long*>(base + 5 * kHotStride);
+    h.mx = h.mn + kHotStride;
+    return h;
+}
+
+__device__ __forceinline__ void hot_init(const HotSmem& h) {
+    for (uint32_t i = threadIdx.x; i < kHotStride; i += blockDim.x) {
+        h.oct_lo[i] = 0;
+        h.oct_hi[i] = 0;
+        h.u0[i] = 0;
+        h.u1[i] = 0;
+        h.u2[i] = 0;
+        h.mn[i] = kMinInitBits;
+        h.mx[i] = kMaxInitBits;
     }
 }
 
@@ -93,13 +141,14 @@ struct Tally {
 
 // RateHistogram::add (rate_engine.cpp:9-23) for one Forward flow, as
 // order-independent reductions:
-//   hist[site][bucket] += 1                       (u32, as the reference)
-//   octets, ubps limbs (32-bit limbs in u64 lanes) += ...   exact, carry-free
-//   min/max of the f64 rate via u64 atomics on the bit pattern (rates > 0,
+//   hist[site][bucket] += 1                              (u32, as the reference)
+//   octets and micro-bps sums                            exact integers
+//   min/max of the f64 rate via u64 min/max on the bit pattern (rates > 0,
 //   SURVEY.md §8a' #8); a cached read skips the atomic when it cannot win
 //   (a stale value is never below the current min / above the current max).
-__device__ __forceinline__ void accumulate(uint32_t site, uint32_t oct, uint64_t dur,
-                                           const DevPartials& P) {
+template <bool kHot>
+__device__ __forceinline__ void accumulate(uint32_t site, uint32_t slot, uint32_t oct,
+                                           uint64_t dur, const DevPartials& P, const HotSmem& h) {
     // flow_rate (rate_engine.cpp:88-94): exact product, one IEEE division.
     const double rate = __ddiv_rn(8000.0 * static_cast<double>(oct), __ull2double_rn(dur));
     const uint32_t bucket = bucket_of(rate);
@@ -113,23 +162,43 @@ __device__ __forceinline__ void accumulate(uint32_t site, uint32_t oct, uint64_t
         hi = static_cast<uint64_t>(q >> 64);
     }
     atomicAdd(P.hist + static_cast<size_t>(site) * kBuckets + bucket, 1u);
-    unsigned long long* s = P.sums + static_cast<size_t>(site) * 4;
-    atomicAdd(s + 0, static_cast<unsigned long long>(oct));
-    atomicAdd(s + 1, lo & 0xFFFFFFFFull);
-    atomicAdd(s + 2, lo >> 32);
-    if (hi) atomicAdd(s + 3, hi);
     const unsigned long long rb = static_cast<unsigned long long>(__double_as_longlong(rate));
-    if (rb < P.mn[site]) atomicMin(P.mn + site, rb);
-    if (rb > P.mx[site]) atomicMax(P.mx + site, rb);
+    if (kHot && slot) {
+        // 32-bit shared atomics with exact carry propagation.
+        const uint32_t o = atomicAdd(h.oct_lo + slot, oct);
+        if (o + oct < o) atomicAdd(h.oct_hi + slot, 1u);
+        const uint32_t vl = static_cast<uint32_t>(lo), vh = static_cast<uint32_t>(lo >> 32);
+        const uint32_t a = atomicAdd(h.u0 + slot, vl);
+        uint32_t c2 = 0;
+        if (vh) {
+            const uint32_t b = atomicAdd(h.u1 + slot, vh);
+            c2 = b + vh < b;
+        }
+        if (a + vl < a) {
+            const uint32_t b = atomicAdd(h.u1 + slot, 1u);
+            c2 += b == 0xFFFFFFFFu;
+        }
+        if (c2 | hi) atomicAdd(h.u2 + slot, c2 + static_cast<uint32_t>(hi));
+        if (rb < h.mn[slot]) atomicMin(h.mn + slot, rb);
+        if (rb > h.mx[slot]) atomicMax(h.mx + slot, rb);
+    } else {
+        unsigned long long* s = P.sums + static_cast<size_t>(site) * 4;
+        atomicAdd(s + 0, static_cast<unsigned long long>(oct));
+        atomicAdd(s + 1, lo & 0xFFFFFFFFull);
+        atomicAdd(s + 2, lo >> 32);
+        if (hi) atomicAdd(s + 3, hi);
+        if (rb < P.mn[site]) atomicMin(P.mn + site, rb);
+        if (rb > P.mx[site]) atomicMax(P.mx + site, rb);
+    }
 }
 
 // reduce_slice's per-record body (rate_engine.cpp:199-239), fixed order:
 // zero packets, pure ACK, administrative, src-first attribution.
-template <bool kSmem>
+template <bool kSmem, bool kHot>
 __device__ __forceinline__ void process(uint32_t src, uint32_t dst, uint32_t pkts, uint32_t oct,
                                         uint64_t start, uint64_t end, const DevParams& p,
                                         const uint32_t* __restrict__ gt, const DevPartials& P,
-                                        Tally& t) {
+                                        const HotSmem& h, Tally& t) {
     if (pkts == 0) {
         ++t.admin;
         return;
@@ -143,23 +212,21 @@ __device__ __forceinline__ void process(uint32_t src, uint32_t dst, uint32_t pkt
         ++t.admin;
         return;
     }
-    uint32_t site = lookup<kSmem>(gt, src);
-    if (site == kNone) site = lookup<kSmem>(gt, dst);
-    if (site == kNone) {
+    uint32_t v = lookup<kSmem>(gt, src);
+    if (v == kNone) v = lookup<kSmem>(gt, dst);
+    if (v == kNone) {
         ++t.unm;
         return;
     }
     ++t.fwd;
-    accumulate(site, oct, dur, P);
-}
-
-__device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
-    return __reduce_add_sync(0xFFFFFFFFu, v);
+    accumulate<kHot>(v & p.site_mask, kHot ? v >> 20 : 0u, oct, dur, P, h);
 }
 
 __device__ __forceinline__ void flush_tallies(const Tally& t, unsigned long long* out) {
-    const uint32_t f = warp_sum_u32(t.fwd), a = warp_sum_u32(t.ack), d = warp_sum_u32(t.admin),
-                   u = warp_sum_u32(t.unm);
+    const uint32_t f = __reduce_add_sync(0xFFFFFFFFu, t.fwd);
+    const uint32_t a = __reduce_add_sync(0xFFFFFFFFu, t.ack);
+    const uint32_t d = __reduce_add_sync(0xFFFFFFFFu, t.admin);
+    const uint32_t u = __reduce_add_sync(0xFFFFFFFFu, t.unm);
     if ((threadIdx.x & 31u) == 0) {
         if (f) atomicAdd(out + 0, static_cast<unsigned long long>(f));
         if (a) atomicAdd(out + 1, static_cast<unsigned long long>(a));
@@ -168,63 +235,161 @@ __device__ __forceinline__ void flush_tallies(const Tally& t, unsigned long long
     }
 }
 
-// ---- K2 over SoA columns ----------------------------------------------------
-template <bool kSmem, bool kVec>
-__global__ void __launch_bounds__(kK2Block) k2_soa(DevSoA b, const uint32_t* __restrict__ gt,
-                                                    uint32_t table_words, DevParams p,
-                                                    DevPartials P) {
-    load_table<kSmem>(gt, table_words);
-    Tally t;
-    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    uint64_t done = 0;
-    if constexpr (kVec) {
-        const uint64_t n4 = b.n / 4;
-        for (uint64_t g = tid; g < n4; g += stride) {
-            const uint4 s = ld_stream_u4(b.src + 4 * g);
-            const uint4 d = ld_stream_u4(b.dst + 4 * g);
-            const uint4 k = ld_stream_u4(b.pkts + 4 * g);
-            const uint4 o = ld_stream_u4(b.octets + 4 * g);
-            const ulonglong2 t0 = ld_stream_u64x2(b.start + 4 * g);
-            const ulonglong2 t1 = ld_stream_u64x2(b.start + 4 * g + 2);
-            const ulonglong2 e0 = ld_stream_u64x2(b.end + 4 * g);
-            const ulonglong2 e1 = ld_stream_u64x2(b.end + 4 * g + 2);
-            process<kSmem>(s.x, d.x, k.x, o.x, t0.x, e0.x, p, gt, P, t);
-            process<kSmem>(s.y, d.y, k.y, o.y, t0.y, e0.y, p, gt, P, t);
-            process<kSmem>(s.z, d.z, k.z, o.z, t1.x, e1.x, p, gt, P, t);
-            process<kSmem>(s.w, d.w, k.w, o.w, t1.y, e1.y, p, gt, P, t);
-        }
-        done = n4 * 4;
+__device__ __forceinline__ void hot_flush(const HotSmem& h, const DevHot& hot, const DevPartials& P) {
+    for (uint32_t slot = 1 + threadIdx.x; slot <= hot.n_slots; slot += blockDim.x) {
+        const uint64_t oct = static_cast<uint64_t>(h.oct_hi[slot]) << 32 | h.oct_lo[slot];
+        if (oct == 0) continue; // untouched: every Forward flow has >= 97 octets
+        const uint32_t site = __ldg(hot.hot_site + slot);
+        unsigned long long* s = P.sums + static_cast<size_t>(site) * 4;
+        atomicAdd(s + 0, oct);
+        atomicAdd(s + 1, static_cast<unsigned long long>(h.u0[slot]));
+        if (h.u1[slot]) atomicAdd(s + 2, static_cast<unsigned long long>(h.u1[slot]));
+        if (h.u2[slot]) atomicAdd(s + 3, static_cast<unsigned long long>(h.u2[slot]));
+        atomicMin(P.mn + site, h.mn[slot]);
+        atomicMax(P.mx + site, h.mx[slot]);
     }
-    for (uint64_t i = done + tid; i < b.n; i += stride)
-        process<kSmem>(b.src[i], b.dst[i], b.pkts[i], b.octets[i], b.start[i], b.end[i], p, gt, P, t);
-    flush_tallies(t, P.sums + static_cast<size_t>(P.n_sites) * 4);
 }
 
-// ---- K2 over 64-byte flowmon::FlowRecord AoS (netflow.hpp:59-67) -----------
-template <bool kSmem, bool kVec>
-__global__ void __launch_bounds__(kK2Block) k2_aos(const unsigned char* __restrict__ rec,
-                                                    uint64_t n, const uint32_t* __restrict__ gt,
-                                                    uint32_t table_words, DevParams p,
-                                                    DevPartials P) {
+// ---- K2 ----------------------------------------------------------------------
+// kLayout 0: SoA, 128-bit vector loads (all columns 16-byte aligned)
+//         1: SoA, scalar loads
+//         2: AoS 64-byte rows, 128-bit loads
+//         3: AoS, scalar loads
+template <int kLayout, bool kSmem, bool kHot>
+__global__ void __launch_bounds__(kK2Block) k2(DevBatch b, const uint32_t* __restrict__ gt,
+                                                uint32_t table_words, DevParams p, DevPartials P,
+                                                DevHot hot) {
     load_table<kSmem>(gt, table_words);
+    HotSmem h{};
+    if constexpr (kHot) {
+        h = hot_smem(kSmem ? table_words : 0u);
+        hot_init(h);
+    }
+    if constexpr (kSmem || kHot) __syncthreads();
     Tally t;
     const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t i = tid; i < n; i += stride) {
-        const unsigned char* r = rec + i * 64;
-        if constexpr (kVec) {
-            const uint4 a = __ldg(reinterpret_cast<const uint4*>(r));        // src dst nexthop ifs
-            const uint4 c = __ldg(reinterpret_cast<const uint4*>(r + 16));   // pkts octets first last
-            const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(r + 48)); // start end
-            process<kSmem>(a.x, a.y, c.x, c.y, e.x, e.y, p, gt, P, t);
-        } else {
-            const uint32_t* w = reinterpret_cast<const uint32_t*>(r);
-            const uint64_t* q = reinterpret_cast<const uint64_t*>(r + 48);
-            process<kSmem>(w[0], w[1], w[4], w[5], q[0], q[1], p, gt, P, t);
+    if constexpr (kLayout == 0 || kLayout == 1) {
+        const DevSoA& c = b.soa;
+        uint64_t done = 0;
+        if constexpr (kLayout == 0) {
+            const uint64_t n4 = c.n / 4;
+            for (uint64_t g = tid; g < n4; g += stride) {
+                const uint4 s = ld_stream_u4(c.src + 4 * g);
+                const uint4 d = ld_stream_u4(c.dst + 4 * g);
+                const uint4 k = ld_stream_u4(c.pkts + 4 * g);
+                const uint4 o = ld_stream_u4(c.octets + 4 * g);
+                const ulonglong2 t0 = ld_stream_u64x2(c.start + 4 * g);
+                const ulonglong2 t1 = ld_stream_u64x2(c.start + 4 * g + 2);
+                const ulonglong2 e0 = ld_stream_u64x2(c.end + 4 * g);
+                const ulonglong2 e1 = ld_stream_u64x2(c.end + 4 * g + 2);
+                process<kSmem, kHot>(s.x, d.x, k.x, o.x, t0.x, e0.x, p, gt, P, h, t);
+                process<kSmem, kHot>(s.y, d.y, k.y, o.y, t0.y, e0.y, p, gt, P, h, t);
+                process<kSmem, kHot>(s.z, d.z, k.z, o.z, t1.x, e1.x, p, gt, P, h, t);
+                process<kSmem, kHot>(s.w, d.w, k.w, o.w, t1.y, e1.y, p, gt, P, h, t);
+            }
+            done = n4 * 4;
+        }
+        for (uint64_t i = done + tid; i < c.n; i += stride)
+            process<kSmem, kHot>(c.src[i], c.dst[i], c.pkts[i], c.octets[i], c.start[i], c.end[i],
+                                 p, gt, P, h, t);
+    } else {
+        const unsigned char* rec = static_cast<const unsigned char*>(b.rec);
+        for (uint64_t i = tid; i < b.n; i += stride) {
+            const unsigned char* r = rec + i * 64;
+            if constexpr (kLayout == 2) {
+                const uint4 a = __ldg(reinterpret_cast<const uint4*>(r));       // src dst nexthop ifs
+                const uint4 c = __ldg(reinterpret_cast<const uint4*>(r + 16));  // pkts octets first last
+                const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(r + 48)); // start end
+                process<kSmem, kHot>(a.x, a.y, c.x, c.y, e.x, e.y, p, gt, P, h, t);
+            } else {
+                const uint32_t* w = reinterpret_cast<const uint32_t*>(r);
+                const uint64_t* q = reinterpret_cast<const uint64_t*>(r + 48);
+                process<kSmem, kHot>(w[0], w[1], w[4], w[5], q[0], q[1], p, gt, P, h, t);
+            }
         }
     }
     flush_tallies(t, P.sums + static_cast<size_t>(P.n_sites) * 4);
+    if constexpr (kHot) {
+        __syncthreads();
+        hot_flush(h, hot, P);
+    }
+}
+
+// ---- K1: hot-site plan ------------------------------------------------------
+// Each block classifies one contiguous chunk of the batch and counts Forward
+// flows per site.
+template <bool kSmem>
+__global__ void __launch_bounds__(kK2Block) k_sample(DevBatch b, const uint32_t* __restrict__ gt,
+                                                      uint32_t table_words, DevParams p,
+                                                      uint64_t chunk_stride, uint32_t chunk_len,
+                                                      uint32_t* __restrict__ cnt) {
+    load_table<kSmem>(gt, table_words);
+    if constexpr (kSmem) __syncthreads();
+    const uint64_t base = static_cast<uint64_t>(blockIdx.x) * chunk_stride;
+    for (uint32_t j = threadIdx.x; j < chunk_len; j += blockDim.x) {
+        const uint64_t i = base + j;
+        uint32_t src, dst, pkts, oct;
+        uint64_t start, end;
+        if (b.aos) {
+            const unsigned char* r = static_cast<const unsigned char*>(b.rec) + i * 64;
+            const uint32_t* w = reinterpret_cast<const uint32_t*>(r);
+            const uint64_t* q = reinterpret_cast<const uint64_t*>(r + 48);
+            src = w[0], dst = w[1], pkts = w[4], oct = w[5], start = q[0], end = q[1];
+        } else {
+            src = b.soa.src[i], dst = b.soa.dst[i], pkts = b.soa.pkts[i], oct = b.soa.octets[i];
+            start = b.soa.start[i], end = b.soa.end[i];
+        }
+        const uint64_t dur = end - start;
+        if (pkts == 0 || static_cast<uint64_t>(oct) < p.ack_plus1 * pkts || pkts < p.min_packets ||
+            dur < p.min_duration_ms || dur == 0)
+            continue;
+        uint32_t v = lookup<kSmem>(gt, src);
+        if (v == kNone) v = lookup<kSmem>(gt, dst);
+        if (v != kNone) atomicAdd(cnt + (v & p.site_mask), 1u);
+    }
+}
+
+// Sites with at least `thr` sampled Forward flows get a slot (first come,
+// first served up to kHotSlots; the numbering does not affect results).
+// Resets the counts for the next call.
+__global__ void k_hot_assign(uint32_t* __restrict__ cnt, uint32_t n_sites, uint32_t thr,
+                             uint32_t* __restrict__ site_slot, uint32_t* __restrict__ hot_site,
+                             uint32_t* __restrict__ next) {
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n_sites; s += gridDim.x * blockDim.x) {
+        const uint32_t c = cnt[s];
+        cnt[s] = 0;
+        uint32_t slot = 0;
+        if (c >= thr) {
+            const uint32_t k = atomicAdd(next, 1u);
+            if (k < kHotSlots) {
+                slot = k + 1;
+                hot_site[slot] = s;
+            }
+        }
+        site_slot[s] = slot;
+    }
+}
+
+// Rewrites the slot bits of every site value in the table (nodes flagged
+// uniform and leaf entries) and resets the slot counter.
+__global__ void k_table_slots(uint32_t* __restrict__ words, uint32_t node_begin,
+                              uint32_t leaf_begin, uint32_t end,
+                              const uint32_t* __restrict__ site_slot, uint32_t* __restrict__ next) {
+    const uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i0 == 0) *next = 0;
+    for (uint32_t i = node_begin + i0; i < end; i += gridDim.x * blockDim.x) {
+        const uint32_t w = words[i];
+        if (i < leaf_begin) {
+            if (w & 0x80000000u) {
+                const uint32_t site = w & 0xFFFFFu;
+                words[i] = 0x80000000u | site_slot[site] << 20 | site;
+            }
+        } else if (w != kNone) {
+            const uint32_t site = w & 0xFFFFFu;
+            words[i] = site_slot[site] << 20 | site;
+        }
+    }
 }
 
 // ---- per-record classification --------------------------------------------
@@ -233,6 +398,7 @@ __global__ void __launch_bounds__(kK2Block) k_classify(DevSoA b, const uint32_t*
                                                         uint32_t table_words, DevParams p,
                                                         uint32_t* __restrict__ out) {
     load_table<kSmem>(gt, table_words);
+    if constexpr (kSmem) __syncthreads();
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < b.n;
          i += stride) {
@@ -243,12 +409,12 @@ __global__ void __launch_bounds__(kK2Block) k_classify(DevSoA b, const uint32_t*
         else if (static_cast<uint64_t>(oct) < p.ack_plus1 * pkts) cls = GNM_PURE_ACK;
         else if (pkts < p.min_packets || dur < p.min_duration_ms || dur == 0) cls = GNM_ADMINISTRATIVE;
         else {
-            uint32_t s = lookup<kSmem>(gt, b.src[i]);
-            if (s == kNone) s = lookup<kSmem>(gt, b.dst[i]);
-            if (s == kNone) cls = GNM_UNMATCHED;
+            uint32_t v = lookup<kSmem>(gt, b.src[i]);
+            if (v == kNone) v = lookup<kSmem>(gt, b.dst[i]);
+            if (v == kNone) cls = GNM_UNMATCHED;
             else {
                 cls = GNM_FORWARD;
-                site = s & 0x3FFFFFFFu;
+                site = (v & p.site_mask) & 0x3FFFFFFFu;
             }
         }
         out[i] = cls << 30 | site;
@@ -358,9 +524,13 @@ __global__ void k_fill_u64(unsigned long long* p, size_t n, unsigned long long v
 }
 
 int sm_count(int device) {
+    static int cached[64] = {0};
+    if (device >= 0 && device < 64 && cached[device]) return cached[device];
     int n = 0;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
-    return n > 0 ? n : 1;
+    if (n <= 0) n = 1;
+    if (device >= 0 && device < 64) cached[device] = n;
+    return n;
 }
 
 template <typename K>
@@ -370,79 +540,136 @@ int occupancy(K kernel, int block, size_t smem) {
     return blocks > 0 ? blocks : 1;
 }
 
-constexpr size_t kSmemTableMax = 200 * 1024;
-
 template <typename K>
 cudaError_t allow_smem(K kernel) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(kSmemTableMax));
+                                static_cast<int>(kSmemMax));
 }
+
+template <int L>
+cudaError_t allow_layout() {
+    cudaError_t e;
+    if ((e = allow_smem(k2<L, true, true>))) return e;
+    if ((e = allow_smem(k2<L, true, false>))) return e;
+    if ((e = allow_smem(k2<L, false, true>))) return e;
+    return allow_smem(k2<L, false, false>);
+}
+
+template <int L, bool kS, bool kH>
+void launch_k2_t(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t, const DevParams& p,
+                 const DevPartials& P, const DevHot& hot, cudaStream_t s) {
+    k2<L, kS, kH><<<cfg.grid, cfg.block, cfg.smem, s>>>(b, t.words, t.n_words, p, P, hot);
+}
+
+template <int L>
+void launch_k2_l(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t, const DevParams& p,
+                 const DevPartials& P, const DevHot& hot, cudaStream_t s) {
+    const bool hh = hot.n_slots > 0;
+    if (cfg.table_in_smem) {
+        if (hh) launch_k2_t<L, true, true>(cfg, b, t, p, P, hot, s);
+        else launch_k2_t<L, true, false>(cfg, b, t, p, P, hot, s);
+    } else {
+        if (hh) launch_k2_t<L, false, true>(cfg, b, t, p, P, hot, s);
+        else launch_k2_t<L, false, false>(cfg, b, t, p, P, hot, s);
+    }
+}
+
+size_t table_smem_bytes(uint32_t table_words) { return static_cast<size_t>(table_words) * 4; }
 
 } // namespace
 
 cudaError_t init_kernel_attributes() {
     cudaError_t e;
-    if ((e = allow_smem(k2_soa<true, true>))) return e;
-    if ((e = allow_smem(k2_soa<true, false>))) return e;
-    if ((e = allow_smem(k2_aos<true, true>))) return e;
-    if ((e = allow_smem(k2_aos<true, false>))) return e;
+    if ((e = allow_layout<0>())) return e;
+    if ((e = allow_layout<1>())) return e;
+    if ((e = allow_layout<2>())) return e;
+    if ((e = allow_layout<3>())) return e;
+    if ((e = allow_smem(k_sample<true>))) return e;
     return allow_smem(k_classify<true>);
 }
 
-LaunchCfg k2_config(int device, uint64_t n, uint32_t table_words, bool aos) {
+LaunchCfg k2_config(int device, uint64_t n, uint32_t table_words, bool hot, int* occ_cache) {
     LaunchCfg c;
     c.block = kK2Block;
-    const size_t bytes = static_cast<size_t>(table_words) * 4;
-    c.table_in_smem = bytes <= kSmemTableMax;
-    c.smem = c.table_in_smem ? bytes : 0;
-    int per_sm;
-    if (aos)
-        per_sm = c.table_in_smem ? occupancy(k2_aos<true, true>, c.block, c.smem)
-                                 : occupancy(k2_aos<false, true>, c.block, 0);
+    const size_t tbytes = table_smem_bytes(table_words);
+    c.table_in_smem = tbytes <= kSmemTableMax;
+    c.smem = (c.table_in_smem ? tbytes : 0) + (hot ? kHotBytes : 0);
+    int per_sm = occ_cache ? occ_cache[hot ? 1 : 0] : 0;
+    if (per_sm > 0) {
+    } else if (c.table_in_smem)
+        per_sm = hot ? occupancy(k2<0, true, true>, c.block, c.smem)
+                     : occupancy(k2<0, true, false>, c.block, c.smem);
     else
-        per_sm = c.table_in_smem ? occupancy(k2_soa<true, true>, c.block, c.smem)
-                                 : occupancy(k2_soa<false, true>, c.block, 0);
+        per_sm = hot ? occupancy(k2<0, false, true>, c.block, c.smem)
+                     : occupancy(k2<0, false, false>, c.block, c.smem);
+    if (occ_cache) occ_cache[hot ? 1 : 0] = per_sm;
     const uint64_t resident = static_cast<uint64_t>(per_sm) * sm_count(device);
     // At least 16 records per thread so the per-CTA table load amortises.
-    const uint64_t want = (n + static_cast<uint64_t>(c.block) * 16 - 1) / (static_cast<uint64_t>(c.block) * 16);
+    const uint64_t per_block = static_cast<uint64_t>(c.block) * 16;
+    const uint64_t want = (n + per_block - 1) / per_block;
     c.grid = static_cast<int>(std::max<uint64_t>(1, std::min(resident, want)));
     return c;
 }
 
-cudaError_t launch_k2_soa(const LaunchCfg& cfg, const DevSoA& b, const uint32_t* table,
-                          uint32_t table_words, const DevParams& p, const DevPartials& P,
-                          cudaStream_t s) {
-    const bool vec = ((reinterpret_cast<uintptr_t>(b.src) | reinterpret_cast<uintptr_t>(b.dst) |
-                       reinterpret_cast<uintptr_t>(b.pkts) | reinterpret_cast<uintptr_t>(b.octets) |
-                       reinterpret_cast<uintptr_t>(b.start) | reinterpret_cast<uintptr_t>(b.end)) &
-                      15u) == 0;
-    if (cfg.table_in_smem) {
-        if (vec) {
-            k2_soa<true, true><<<cfg.grid, cfg.block, cfg.smem, s>>>(b, table, table_words, p, P);
-        } else {
-            k2_soa<true, false><<<cfg.grid, cfg.block, cfg.smem, s>>>(b, table, table_words, p, P);
-        }
+bool plan_hot(int device, const DevBatch& b, const DevTable& t, const DevParams& p,
+              uint32_t n_sites, uint32_t* scratch, int k2_grid, bool force, cudaStream_t s,
+              uint64_t* launches, cudaError_t* err) {
+    (void)device;
+    *err = cudaSuccess;
+    if (!t.packed || n_sites == 0 || b.n == 0) return false;
+    // Sample 1/64 of the batch (at most 256k records) in 64 contiguous chunks.
+    const uint32_t chunks = 64;
+    uint64_t sample = std::min<uint64_t>(262144, b.n / 64);
+    uint32_t chunk_len = static_cast<uint32_t>(sample / chunks);
+    uint32_t thr;
+    if (force) {
+        chunk_len = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(4096, b.n / chunks)));
+        thr = 1;
     } else {
-        if (vec) k2_soa<false, true><<<cfg.grid, cfg.block, 0, s>>>(b, table, table_words, p, P);
-        else k2_soa<false, false><<<cfg.grid, cfg.block, 0, s>>>(b, table, table_words, p, P);
+        if (chunk_len < 256) return false;
+        // A site is hot when it is expected to see >= 32 Forward flows per
+        // K2 CTA, so its block-private accumulator amortises the flush.
+        const double thr_d =
+            32.0 * k2_grid * static_cast<double>(chunk_len) * chunks / static_cast<double>(b.n);
+        thr = static_cast<uint32_t>(std::max(2.0, thr_d));
+        if (thr > chunk_len * chunks) return false;
     }
-    return cudaGetLastError();
+    uint32_t* cnt = scratch;
+    uint32_t* site_slot = scratch + n_sites;
+    uint32_t* hot_site = site_slot + n_sites;
+    uint32_t* next = hot_site + kHotStride;
+    const uint64_t stride = std::max<uint64_t>(b.n / chunks, chunk_len);
+    const uint32_t nchunks = static_cast<uint32_t>(std::min<uint64_t>(chunks, b.n / chunk_len));
+    const size_t tbytes = table_smem_bytes(t.n_words);
+    if (tbytes <= kSmemTableMax)
+        k_sample<true><<<nchunks, kK2Block, tbytes, s>>>(b, t.words, t.n_words, p, stride, chunk_len, cnt);
+    else
+        k_sample<false><<<nchunks, kK2Block, 0, s>>>(b, t.words, t.n_words, p, stride, chunk_len, cnt);
+    const uint32_t ag = std::min<uint32_t>((n_sites + 255) / 256, 1024);
+    k_hot_assign<<<ag, 256, 0, s>>>(cnt, n_sites, thr, site_slot, hot_site, next);
+    const uint32_t span = t.n_words - t.node_begin;
+    const uint32_t rg = std::max<uint32_t>(1, std::min<uint32_t>((span + 255) / 256, 1024));
+    k_table_slots<<<rg, 256, 0, s>>>(t.words, t.node_begin, t.leaf_begin, t.n_words, site_slot, next);
+    *launches += 3;
+    *err = cudaGetLastError();
+    return *err == cudaSuccess;
 }
 
-cudaError_t launch_k2_aos(const LaunchCfg& cfg, const void* records, uint64_t n,
-                          const uint32_t* table, uint32_t table_words, const DevParams& p,
-                          const DevPartials& P, cudaStream_t s) {
-    const auto* r = static_cast<const unsigned char*>(records);
-    const bool vec = (reinterpret_cast<uintptr_t>(records) & 15u) == 0;
-    if (cfg.table_in_smem) {
-        if (vec) {
-            k2_aos<true, true><<<cfg.grid, cfg.block, cfg.smem, s>>>(r, n, table, table_words, p, P);
-        } else {
-            k2_aos<true, false><<<cfg.grid, cfg.block, cfg.smem, s>>>(r, n, table, table_words, p, P);
-        }
+cudaError_t launch_k2(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t,
+                      const DevParams& p, const DevPartials& P, const DevHot& hot,
+                      cudaStream_t s) {
+    if (b.aos) {
+        const bool vec = (reinterpret_cast<uintptr_t>(b.rec) & 15u) == 0;
+        if (vec) launch_k2_l<2>(cfg, b, t, p, P, hot, s);
+        else launch_k2_l<3>(cfg, b, t, p, P, hot, s);
     } else {
-        if (vec) k2_aos<false, true><<<cfg.grid, cfg.block, 0, s>>>(r, n, table, table_words, p, P);
-        else k2_aos<false, false><<<cfg.grid, cfg.block, 0, s>>>(r, n, table, table_words, p, P);
+        const DevSoA& c = b.soa;
+        const bool vec = ((reinterpret_cast<uintptr_t>(c.src) | reinterpret_cast<uintptr_t>(c.dst) |
+                           reinterpret_cast<uintptr_t>(c.pkts) | reinterpret_cast<uintptr_t>(c.octets) |
+                           reinterpret_cast<uintptr_t>(c.start) | reinterpret_cast<uintptr_t>(c.end)) &
+                          15u) == 0;
+        if (vec) launch_k2_l<0>(cfg, b, t, p, P, hot, s);
+        else launch_k2_l<1>(cfg, b, t, p, P, hot, s);
     }
     return cudaGetLastError();
 }
@@ -472,18 +699,19 @@ cudaError_t launch_init_partials(const DevPartials& P, cudaStream_t s) {
     if ((e = cudaMemsetAsync(P.sums, 0, (static_cast<size_t>(P.n_sites) * 4 + 4) * 8, s))) return e;
     if ((e = cudaMemsetAsync(P.mx, 0, static_cast<size_t>(P.n_sites) * 8, s))) return e;
     if ((e = cudaMemsetAsync(P.hist, 0, static_cast<size_t>(P.n_sites) * kBuckets * 4, s))) return e;
-    if (P.n_sites) k_fill_u64<<<std::min<uint32_t>((P.n_sites + 255) / 256, 1024), 256, 0, s>>>(P.mn, P.n_sites, kMinInitBits);
+    if (P.n_sites)
+        k_fill_u64<<<std::min<uint32_t>((P.n_sites + 255) / 256, 1024), 256, 0, s>>>(P.mn, P.n_sites,
+                                                                                     kMinInitBits);
     return cudaGetLastError();
 }
 
-cudaError_t launch_classify(const LaunchCfg& cfg, const DevSoA& b, const uint32_t* table,
-                            uint32_t table_words, const DevParams& p, uint32_t* out,
-                            cudaStream_t s) {
-    if (cfg.table_in_smem) {
-        k_classify<true><<<cfg.grid, cfg.block, cfg.smem, s>>>(b, table, table_words, p, out);
-    } else {
-        k_classify<false><<<cfg.grid, cfg.block, 0, s>>>(b, table, table_words, p, out);
-    }
+cudaError_t launch_classify(const LaunchCfg& cfg, const DevSoA& b, const DevTable& t,
+                            const DevParams& p, uint32_t* out, cudaStream_t s) {
+    const size_t tbytes = table_smem_bytes(t.n_words);
+    if (tbytes <= kSmemTableMax)
+        k_classify<true><<<cfg.grid, cfg.block, tbytes, s>>>(b, t.words, t.n_words, p, out);
+    else
+        k_classify<false><<<cfg.grid, cfg.block, 0, s>>>(b, t.words, t.n_words, p, out);
     return cudaGetLastError();
 }
 

@@ -11,11 +11,14 @@ namespace gnm {
 constexpr uint32_t kBuckets = 10001;
 constexpr uint64_t kMinInitBits = 0x7FF0000000000000ull; // +inf: empty min
 constexpr uint64_t kMaxInitBits = 0;                     // +0.0: empty max (rates are > 0)
+constexpr uint32_t kHotSlots = 512;   // block-private accumulators for hot sites
+constexpr uint32_t kHotStride = 520;  // kHotSlots + 1 (slot 0 = cold), padded
 
 struct DevParams {
     uint64_t ack_plus1;       // ack_avg_size_max + 1, u64 (rate_engine.cpp:78)
     uint32_t min_packets;
     uint32_t min_duration_ms;
+    uint32_t site_mask;       // kPackedSiteMask, or 0x7FFFFFFF for wide tables
 };
 
 // Device partial accumulators of one context (layout in gnetmon.h, gnm_partials).
@@ -25,6 +28,12 @@ struct DevPartials {
     unsigned long long* mx;   // f64 bits
     unsigned int* hist;       // [n_sites * 10001]
     uint32_t n_sites;
+};
+
+// Per-call hot-site plan: slot -> site (slots 1..n_slots), 0 slots = off.
+struct DevHot {
+    const uint32_t* hot_site;
+    uint32_t n_slots;
 };
 
 struct DevSoA {
@@ -37,6 +46,22 @@ struct DevSoA {
     uint64_t n;
 };
 
+// A batch is SoA columns or 64-byte flowmon::FlowRecord AoS rows.
+struct DevBatch {
+    bool aos;
+    DevSoA soa;
+    const void* rec;
+    uint64_t n;
+};
+
+struct DevTable {
+    uint32_t* words;
+    uint32_t n_words;     // padded to a multiple of 4
+    uint32_t node_begin;
+    uint32_t leaf_begin;
+    bool packed;
+};
+
 struct LaunchCfg {
     int grid;
     int block;
@@ -44,26 +69,31 @@ struct LaunchCfg {
     bool table_in_smem;
 };
 
-// Once per device: opt the shared-memory-table kernels into > 48 KB smem.
+// Once per device: opt the shared-memory kernels into large dynamic smem.
 cudaError_t init_kernel_attributes();
 
-// Occupancy-derived launch configuration for K2 over n records with a table
-// of `table_words` u32.
-LaunchCfg k2_config(int device, uint64_t n, uint32_t table_words, bool aos);
+// Occupancy-derived launch configuration for K2 over n records.
+// occ_cache[hot] memoises blocks/SM (0 = unknown) for this table size.
+LaunchCfg k2_config(int device, uint64_t n, uint32_t table_words, bool hot, int* occ_cache);
 
-cudaError_t launch_k2_soa(const LaunchCfg& cfg, const DevSoA& b, const uint32_t* table,
-                          uint32_t table_words, const DevParams& p, const DevPartials& P,
-                          cudaStream_t s);
-cudaError_t launch_k2_aos(const LaunchCfg& cfg, const void* records, uint64_t n,
-                          const uint32_t* table, uint32_t table_words, const DevParams& p,
-                          const DevPartials& P, cudaStream_t s);
+// K1 (optional, skewed batches): sample the batch, pick the hot sites and
+// write their slots into the table words. Returns false when the batch is
+// too small for block-private accumulation to pay; `scratch` holds
+// n_sites u32 counts (zero at rest), n_sites u32 site->slot, kHotStride u32
+// slot->site and one u32 counter.
+bool plan_hot(int device, const DevBatch& b, const DevTable& t, const DevParams& p,
+              uint32_t n_sites, uint32_t* scratch, int k2_grid, bool force, cudaStream_t s,
+              uint64_t* launches, cudaError_t* err);
+
+cudaError_t launch_k2(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t,
+                      const DevParams& p, const DevPartials& P, const DevHot& hot,
+                      cudaStream_t s);
 // K3: per-site count/median/flag; reset != 0 also clears the partials.
 cudaError_t launch_k3(int device, const DevPartials& P, double threshold, gnm_site_stats* out,
                       int reset, cudaStream_t s);
 cudaError_t launch_reset(int device, const DevPartials& P, cudaStream_t s);
 cudaError_t launch_init_partials(const DevPartials& P, cudaStream_t s);
-cudaError_t launch_classify(const LaunchCfg& cfg, const DevSoA& b, const uint32_t* table,
-                            uint32_t table_words, const DevParams& p, uint32_t* out,
-                            cudaStream_t s);
+cudaError_t launch_classify(const LaunchCfg& cfg, const DevSoA& b, const DevTable& t,
+                            const DevParams& p, uint32_t* out, cudaStream_t s);
 
 } // namespace gnm

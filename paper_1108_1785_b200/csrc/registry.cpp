@@ -144,6 +144,9 @@ DeviceTable Registry::compile_device_table() const {
         }
     }
     const uint32_t leaf_base = kDirWords + static_cast<uint32_t>(nodes.size());
+    t.node_begin = kDirWords;
+    t.leaf_begin = leaf_base;
+    t.packed = sites_.size() <= kPackedSiteMask;
     for (uint32_t& n : nodes)
         if (!(n & 0x80000000u)) n += leaf_base;
     t.words.assign(kDirWords, 0);

@@ -53,16 +53,27 @@ std::string format_ipv4(uint32_t ip);
 //                              0xFFFFFFFF.
 // lookup(ip): d = ip>>16; {bits,rank} = words[2*(d>>5)..]; miss unless bit
 // d&31 is set; node = words[4096 + rank + popc(bits & below)];
-// site = uniform ? node&0x7FFFFFFF : words[node + ((ip>>8)&255)].
+// value = uniform ? node&0x7FFFFFFF : words[node + ((ip>>8)&255)].
+//
+// Site values are PACKED when the registry has fewer than 2^20 sites:
+// bits 0..19 hold the SiteId and bits 20..30 a per-call hot slot (0 = cold),
+// rewritten on the device before each accumulation (kernels.cu,
+// k_table_slots). Larger registries store the plain 31-bit SiteId and run
+// without hot slots (`packed` false).
 struct DeviceTable {
     std::vector<uint32_t> words;
     uint32_t n_blocks16 = 0;
     uint32_t n_leaves = 0;
+    uint32_t node_begin = 4096;  // first node word
+    uint32_t leaf_begin = 4096;  // first leaf word
+    bool packed = true;
 };
 
 constexpr uint32_t kNoSite = 0xFFFFFFFFu;
 constexpr uint32_t kDirWords = 4096;
 constexpr uint32_t kMaxSites = 0x3FFFFFFFu; // gnm_classify's 30-bit site field
+constexpr uint32_t kPackedSiteBits = 20;
+constexpr uint32_t kPackedSiteMask = (1u << kPackedSiteBits) - 1;
 
 class Registry {
 public:

@@ -373,15 +373,51 @@ class ClassTallies:
         return self.forward + self.pure_ack + self.administrative + self.unmatched
 
 
-@dataclass
 class AnalysisResult:
-    window_start_ms: int = 0
-    window_end_ms: int = 0
-    sites: dict = field(default_factory=dict)      # SiteId -> SiteResult, flow_count > 0
-    tallies: ClassTallies = field(default_factory=ClassTallies)
-    table: Optional[np.ndarray] = None             # raw gnm_site_stats rows, all sites
-    histograms: Optional[np.ndarray] = None        # (n_sites, 10001) when requested
-    threshold_bps: float = kDefaultWarnThresholdBps
+    """rate_engine.hpp:112-119 at site level. ``sites`` (SiteId -> SiteResult,
+    only sites with Forward flows, as the reference's map) is built lazily
+    from ``table``, the raw gnm_site_stats rows of every registered site."""
+
+    def __init__(self, window_start_ms: int = 0, window_end_ms: int = 0, sites: Optional[dict] = None,
+                 tallies: Optional[ClassTallies] = None, table: Optional[np.ndarray] = None,
+                 histograms: Optional[np.ndarray] = None,
+                 threshold_bps: float = kDefaultWarnThresholdBps):
+        self.window_start_ms = window_start_ms
+        self.window_end_ms = window_end_ms
+        self.tallies = tallies or ClassTallies()
+        self.table = table
+        self.histograms = histograms
+        self.threshold_bps = threshold_bps
+        self._sites = sites
+
+    @property
+    def sites(self) -> dict:
+        if self._sites is None:
+            self._sites = {}
+            t = self.table
+            if t is not None:
+                for s in np.nonzero(t["flow_count"])[0].tolist():
+                    row = t[s].tolist()  # one conversion per row
+                    (cnt, octs, lo, hi, mn, mx, avg, med, below, _) = row
+                    self._sites[s] = SiteResult(
+                        stats=RateStats(max_bps=mx, min_bps=mn, avg_bps=avg, median_bps=med,
+                                        flow_count=cnt),
+                        octets=octs, rate_ubps_sum=hi << 64 | lo, below_threshold=bool(below),
+                        histogram=None if self.histograms is None else self.histograms[s])
+        return self._sites
+
+    @staticmethod
+    def from_site_stats(n_sites: int, stats: dict, window_end_ms: int = 0) -> "AnalysisResult":
+        """A result holding the given per-site RateStats (tests of the
+        warning rule build results directly, monitor_test.cpp:23-47)."""
+        t = np.zeros(n_sites, SITE_STATS_DTYPE)
+        for s, st in stats.items():
+            t[s]["flow_count"] = st.flow_count
+            t[s]["median_bps"] = st.median_bps
+            t[s]["min_bps"] = st.min_bps
+            t[s]["max_bps"] = st.max_bps
+            t[s]["avg_bps"] = st.avg_bps
+        return AnalysisResult(window_end_ms=window_end_ms, table=t)
 
     def _c(self) -> gnm_result:
         t = self.table if self.table is not None else np.zeros(0, SITE_STATS_DTYPE)
@@ -396,22 +432,10 @@ class AnalysisResult:
 
 
 def _build_result(r: gnm_result, table: np.ndarray, hist: Optional[np.ndarray]) -> AnalysisResult:
-    res = AnalysisResult(window_start_ms=r.window_start_ms, window_end_ms=r.window_end_ms,
-                         table=table, histograms=hist, threshold_bps=r.threshold_bps)
-    res.tallies = ClassTallies(r.tallies.forward, r.tallies.pure_ack, r.tallies.administrative,
-                               r.tallies.unmatched)
-    present = np.nonzero(table["flow_count"])[0]
-    for s in present.tolist():
-        row = table[s]
-        res.sites[s] = SiteResult(
-            stats=RateStats(max_bps=float(row["max_bps"]), min_bps=float(row["min_bps"]),
-                            avg_bps=float(row["avg_bps"]), median_bps=float(row["median_bps"]),
-                            flow_count=int(row["flow_count"])),
-            octets=int(row["octets"]),
-            rate_ubps_sum=int(row["rate_ubps_hi"]) << 64 | int(row["rate_ubps_lo"]),
-            below_threshold=bool(row["below_threshold"]),
-            histogram=None if hist is None else hist[s])
-    return res
+    return AnalysisResult(window_start_ms=r.window_start_ms, window_end_ms=r.window_end_ms,
+                          tallies=ClassTallies(r.tallies.forward, r.tallies.pure_ack,
+                                               r.tallies.administrative, r.tallies.unmatched),
+                          table=table, histograms=hist, threshold_bps=r.threshold_bps)
 
 
 # ---- the device engine -----------------------------------------------------------
@@ -455,6 +479,11 @@ class Engine:
     def set_chunk_records(self, n: int) -> None:
         _check(lib.gnm_ctx_set_chunk_records(self._h, n))
 
+    def set_hot_mode(self, mode: str) -> None:
+        """"auto" (default), "off" or "force" block-private hot-site accumulation."""
+        m = {"off": _lib.HOT_OFF, "auto": _lib.HOT_AUTO, "force": _lib.HOT_FORCE}[mode]
+        _check(lib.gnm_ctx_set_hot_mode(self._h, m))
+
     def enable_timing(self, on: bool = True) -> None:
         _check(lib.gnm_ctx_enable_timing(self._h, 1 if on else 0))
 
@@ -463,7 +492,8 @@ class Engine:
         _check(lib.gnm_ctx_timing(self._h, C.byref(t)))
         return {"accumulate_ms": t.accumulate_ms, "finalize_ms": t.finalize_ms,
                 "h2d_ms": t.h2d_ms, "k2_launches": t.k2_launches,
-                "kernel_launches": t.kernel_launches, "records": t.records}
+                "kernel_launches": t.kernel_launches, "records": t.records,
+                "plan_ms": t.plan_ms}
 
     @staticmethod
     def _params(params: Optional[FilterParams]) -> gnm_filter_params:

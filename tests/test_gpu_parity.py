@@ -141,6 +141,41 @@ def test_empty_and_no_forward(engine):
             r.tallies.forward) == (1, 1, 1, 0)
 
 
+@pytest.mark.parametrize("mode", ["off", "force", "auto"])
+def test_hot_site_modes_bit_exact(engine, orc, mode):
+    """Block-private (shared-memory) accumulation of hot sites with 32-bit
+    carry chains must equal the oracle: full-range octets overflow every
+    limb of the per-block accumulators."""
+    sites, cols = parity.engine_stress_set(200_000, seed=11)
+    cat = catalog_of(sites)
+    engine.set_hot_mode(mode)
+    try:
+        res = engine.aggregate(FlowBatch(*cols).to_device(), cat, histograms=True)
+        res3 = engine.aggregate(FlowBatch(*parity.tiny_duration_set()[1]).to_device(),
+                                catalog_of(parity.tiny_duration_set()[0]),
+                                FilterParams(min_duration_ms=0, min_packets=1))
+    finally:
+        engine.set_hot_mode("auto")
+    parity.assert_matches_oracle(res, parity.oracle_reference(orc, cat, cols))
+    tcat = catalog_of(parity.tiny_duration_set()[0])
+    parity.assert_matches_oracle(res3, parity.oracle_reference(orc, tcat, parity.tiny_duration_set()[1],
+                                                               (96, 1, 0)))
+
+
+@pytest.mark.parametrize("mode", ["off", "force", "auto"])
+def test_zipf_d3_hot_modes(engine, orc, mode):
+    """D3 shape (10k Zipf sites) large enough for the auto planner to engage."""
+    w = synth.workload("D3")
+    cols = synth.generate(w, 2_000_000)
+    cat = layout_catalog(w.sites)
+    engine.set_hot_mode(mode)
+    try:
+        res = engine.aggregate(FlowBatch(*cols).to_device(), cat)
+    finally:
+        engine.set_hot_mode("auto")
+    parity.assert_matches_oracle(res, parity.oracle_reference(orc, cat, cols))
+
+
 def test_state_resets_between_calls(engine, orc):
     """The device partials are all-zero at rest: back-to-back calls on
     different data and registries do not leak into each other."""
