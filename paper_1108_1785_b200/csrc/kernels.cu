@@ -37,7 +37,8 @@ constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr int kK2Block = 512;
 constexpr size_t kHotBytes = kHotStride * (5 * 4 + 2 * 8);
 constexpr size_t kSmemMax = 227 * 1024;
-constexpr size_t kSmemTableMax = kSmemMax - kHotBytes - 1024;
+constexpr size_t kQueueBytes = (kK2Block / 32) * 64 * 16; // per-warp FwdItem queues
+constexpr size_t kSmemTableMax = kSmemMax - kHotBytes - kQueueBytes - 1024;
 
 extern __shared__ __align__(16) uint32_t g_smem[];
 
@@ -139,6 +140,56 @@ struct Tally {
     uint32_t fwd = 0, ack = 0, admin = 0, unm = 0;
 };
 
+// Exact micro-bps of one flow, rate_ubps_of (rate_engine.cpp:100-107):
+// floor(octets * 8e9 / dur) as a 128-bit value (hi is non-zero only when
+// dur is a few ms and octets are huge). Fast path: the f64 rate already
+// approximates the quotient to ~2^-51 relative, so q0 = rz(rate * 1e6)
+// lands within a few units of it; the exact integer residual then fixes
+// it up. Preconditions of the fast path (product fits in u64, dur <= 2^40,
+// quotient < 2^62) bound the estimate error by < 2^12 units and therefore
+// the true residual by < 2^52 * 2^0 < 2^63, so the wrapped u64 residual is
+// the real one; any estimate the fix-up loop cannot settle falls back to
+// the exact division.
+__device__ __forceinline__ void ubps_of(uint32_t oct, uint64_t dur, double rate, uint64_t& lo,
+                                        uint64_t& hi) {
+    hi = 0;
+    if (oct <= 2305843009u) {
+        const uint64_t p = static_cast<uint64_t>(oct) * 8000000000ull;
+        if (dur <= (1ull << 40) && rate < 4.0e12) {
+            uint64_t q = static_cast<uint64_t>(__dmul_rz(rate, 1.0e6));
+            int64_t r = static_cast<int64_t>(p - q * dur);
+            const int64_t d = static_cast<int64_t>(dur);
+#pragma unroll 1
+            for (int i = 0; i < 4 && r < 0; ++i) {
+                --q;
+                r += d;
+            }
+#pragma unroll 1
+            for (int i = 0; i < 4 && r >= d; ++i) {
+                ++q;
+                r -= d;
+            }
+            if (r >= 0 && r < d) {
+                lo = q;
+                return;
+            }
+        }
+        lo = p / dur;
+        return;
+    }
+    const unsigned __int128 q = static_cast<unsigned __int128>(oct) * 8000000000ull / dur;
+    lo = static_cast<uint64_t>(q);
+    hi = static_cast<uint64_t>(q >> 64);
+}
+
+// A Forward flow waiting in a warp's queue: packed (slot << 20 | site), octets, duration.
+struct FwdItem {
+    uint32_t packed;
+    uint32_t oct;
+    uint64_t dur;
+};
+constexpr uint32_t kQueue = 64; // per-warp FwdItem capacity (< 32 left + 32 pushed)
+
 // RateHistogram::add (rate_engine.cpp:9-23) for one Forward flow, as
 // order-independent reductions:
 //   hist[site][bucket] += 1                              (u32, as the reference)
@@ -146,24 +197,28 @@ struct Tally {
 //   min/max of the f64 rate via u64 min/max on the bit pattern (rates > 0,
 //   SURVEY.md §8a' #8); a cached read skips the atomic when it cannot win
 //   (a stale value is never below the current min / above the current max).
+// Called on warp-compacted items, so the arithmetic runs with full warps.
 template <bool kHot>
-__device__ __forceinline__ void accumulate(uint32_t site, uint32_t slot, uint32_t oct,
-                                           uint64_t dur, const DevPartials& P, const HotSmem& h) {
-    // flow_rate (rate_engine.cpp:88-94): exact product, one IEEE division.
-    const double rate = __ddiv_rn(8000.0 * static_cast<double>(oct), __ull2double_rn(dur));
-    const uint32_t bucket = bucket_of(rate);
-    // rate_ubps_of (rate_engine.cpp:100-107).
-    uint64_t lo, hi = 0;
-    if (oct <= 2305843009u) {
-        lo = static_cast<uint64_t>(oct) * 8000000000ull / dur;
-    } else {
-        const unsigned __int128 q = static_cast<unsigned __int128>(oct) * 8000000000ull / dur;
-        lo = static_cast<uint64_t>(q);
-        hi = static_cast<uint64_t>(q >> 64);
+__device__ __forceinline__ void accumulate(const FwdItem& it, uint32_t site_mask,
+                                           const DevPartials& P, const HotSmem& h) {
+    const uint32_t site = it.packed & site_mask;
+    const uint32_t slot = kHot ? it.packed >> 20 : 0u;
+    const bool hot = kHot && slot;
+    // Cold sites: fetch the current min/max first; the loads overlap the math.
+    unsigned long long cur_mn = 0, cur_mx = 0;
+    if (!hot) {
+        cur_mn = __ldcg(P.mn + site);
+        cur_mx = __ldcg(P.mx + site);
     }
+    const uint32_t oct = it.oct;
+    // flow_rate (rate_engine.cpp:88-94): exact product, one IEEE division.
+    const double rate = __ddiv_rn(8000.0 * static_cast<double>(oct), __ull2double_rn(it.dur));
+    const uint32_t bucket = bucket_of(rate);
+    uint64_t lo, hi;
+    ubps_of(oct, it.dur, rate, lo, hi);
     atomicAdd(P.hist + static_cast<size_t>(site) * kBuckets + bucket, 1u);
     const unsigned long long rb = static_cast<unsigned long long>(__double_as_longlong(rate));
-    if (kHot && slot) {
+    if (hot) {
         // 32-bit shared atomics with exact carry propagation.
         const uint32_t o = atomicAdd(h.oct_lo + slot, oct);
         if (o + oct < o) atomicAdd(h.oct_hi + slot, 1u);
@@ -185,41 +240,63 @@ __device__ __forceinline__ void accumulate(uint32_t site, uint32_t slot, uint32_
         unsigned long long* s = P.sums + static_cast<size_t>(site) * 4;
         atomicAdd(s + 0, static_cast<unsigned long long>(oct));
         atomicAdd(s + 1, lo & 0xFFFFFFFFull);
-        atomicAdd(s + 2, lo >> 32);
+        if (lo >> 32) atomicAdd(s + 2, lo >> 32);
         if (hi) atomicAdd(s + 3, hi);
-        if (rb < P.mn[site]) atomicMin(P.mn + site, rb);
-        if (rb > P.mx[site]) atomicMax(P.mx + site, rb);
+        if (rb < cur_mn) atomicMin(P.mn + site, rb);
+        if (rb > cur_mx) atomicMax(P.mx + site, rb);
     }
 }
 
-// reduce_slice's per-record body (rate_engine.cpp:199-239), fixed order:
-// zero packets, pure ACK, administrative, src-first attribution.
-template <bool kSmem, bool kHot>
-__device__ __forceinline__ void process(uint32_t src, uint32_t dst, uint32_t pkts, uint32_t oct,
-                                        uint64_t start, uint64_t end, const DevParams& p,
-                                        const uint32_t* __restrict__ gt, const DevPartials& P,
-                                        const HotSmem& h, Tally& t) {
+// reduce_slice's per-record filter + attribution (rate_engine.cpp:199-233),
+// fixed order: zero packets, pure ACK, administrative, src-first
+// attribution. Returns true (and the packed site value) for Forward flows.
+template <bool kSmem>
+__device__ __forceinline__ bool classify(bool valid, uint32_t src, uint32_t dst, uint32_t pkts,
+                                         uint32_t oct, uint64_t dur, const DevParams& p,
+                                         const uint32_t* __restrict__ gt, Tally& t,
+                                         uint32_t& packed) {
+    if (!valid) return false;
     if (pkts == 0) {
         ++t.admin;
-        return;
+        return false;
     }
     if (static_cast<uint64_t>(oct) < p.ack_plus1 * pkts) {
         ++t.ack;
-        return;
+        return false;
     }
-    const uint64_t dur = end - start;
     if (pkts < p.min_packets || dur < p.min_duration_ms || dur == 0) {
         ++t.admin;
-        return;
+        return false;
     }
     uint32_t v = lookup<kSmem>(gt, src);
     if (v == kNone) v = lookup<kSmem>(gt, dst);
     if (v == kNone) {
         ++t.unm;
-        return;
+        return false;
     }
     ++t.fwd;
-    accumulate<kHot>(v & p.site_mask, kHot ? v >> 20 : 0u, oct, dur, P, h);
+    packed = v;
+    return true;
+}
+
+// Warp-level stream compaction of Forward flows: lanes append their item to
+// the warp's shared queue (ballot + popc), and every time 32 are queued the
+// whole warp drains one item per lane, so accumulate() never runs with the
+// ~40% lane occupancy the class mix would otherwise leave it.
+template <bool kHot>
+__device__ __forceinline__ void push(bool fwd, const FwdItem& it, FwdItem* q, uint32_t& qn,
+                                     uint32_t lane, uint32_t site_mask, const DevPartials& P,
+                                     const HotSmem& h) {
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, fwd);
+    if (fwd) q[qn + __popc(m & ((1u << lane) - 1u))] = it;
+    qn += __popc(m);
+    if (qn >= 32) {
+        __syncwarp();
+        const FwdItem x = q[qn - 32 + lane];
+        qn -= 32;
+        __syncwarp();
+        accumulate<kHot>(x, site_mask, P, h);
+    }
 }
 
 __device__ __forceinline__ void flush_tallies(const Tally& t, unsigned long long* out) {
@@ -255,60 +332,103 @@ __device__ __forceinline__ void hot_flush(const HotSmem& h, const DevHot& hot, c
 //         1: SoA, scalar loads
 //         2: AoS 64-byte rows, 128-bit loads
 //         3: AoS, scalar loads
+// Loops are warp-uniform (each warp walks whole 32- or 128-record tiles with
+// a per-lane validity flag) so the queue's warp collectives stay converged.
 template <int kLayout, bool kSmem, bool kHot>
-__global__ void __launch_bounds__(kK2Block) k2(DevBatch b, const uint32_t* __restrict__ gt,
+__global__ void __launch_bounds__(kK2Block, 2) k2(DevBatch b, const uint32_t* __restrict__ gt,
                                                 uint32_t table_words, DevParams p, DevPartials P,
                                                 DevHot hot) {
     load_table<kSmem>(gt, table_words);
     HotSmem h{};
+    const uint32_t smem_words = kSmem ? table_words : 0u;
     if constexpr (kHot) {
-        h = hot_smem(kSmem ? table_words : 0u);
+        h = hot_smem(smem_words);
         hot_init(h);
     }
-    if constexpr (kSmem || kHot) __syncthreads();
+    const uint32_t lane = threadIdx.x & 31u;
+    FwdItem* q = reinterpret_cast<FwdItem*>(g_smem + smem_words + (kHot ? kHotBytes / 4 : 0u)) +
+                 (threadIdx.x >> 5) * kQueue;
+    uint32_t qn = 0;
+    __syncthreads();
     Tally t;
-    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    if constexpr (kLayout == 0 || kLayout == 1) {
+    const uint64_t warp_gid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    const uint32_t mask = p.site_mask;
+    FwdItem it;
+    if constexpr (kLayout == 0) {
         const DevSoA& c = b.soa;
-        uint64_t done = 0;
-        if constexpr (kLayout == 0) {
-            const uint64_t n4 = c.n / 4;
-            for (uint64_t g = tid; g < n4; g += stride) {
-                const uint4 s = ld_stream_u4(c.src + 4 * g);
-                const uint4 d = ld_stream_u4(c.dst + 4 * g);
-                const uint4 k = ld_stream_u4(c.pkts + 4 * g);
-                const uint4 o = ld_stream_u4(c.octets + 4 * g);
-                const ulonglong2 t0 = ld_stream_u64x2(c.start + 4 * g);
-                const ulonglong2 t1 = ld_stream_u64x2(c.start + 4 * g + 2);
-                const ulonglong2 e0 = ld_stream_u64x2(c.end + 4 * g);
-                const ulonglong2 e1 = ld_stream_u64x2(c.end + 4 * g + 2);
-                process<kSmem, kHot>(s.x, d.x, k.x, o.x, t0.x, e0.x, p, gt, P, h, t);
-                process<kSmem, kHot>(s.y, d.y, k.y, o.y, t0.y, e0.y, p, gt, P, h, t);
-                process<kSmem, kHot>(s.z, d.z, k.z, o.z, t1.x, e1.x, p, gt, P, h, t);
-                process<kSmem, kHot>(s.w, d.w, k.w, o.w, t1.y, e1.y, p, gt, P, h, t);
+        const uint64_t n4 = c.n / 4;
+        for (uint64_t base = warp_gid * 32; base < n4; base += nwarps * 32) {
+            const uint64_t g = base + lane;
+            const bool ok = g < n4;
+            uint4 s{}, d{}, k{}, o{};
+            ulonglong2 t0{}, t1{}, e0{}, e1{};
+            if (ok) {
+                s = ld_stream_u4(c.src + 4 * g);
+                d = ld_stream_u4(c.dst + 4 * g);
+                k = ld_stream_u4(c.pkts + 4 * g);
+                o = ld_stream_u4(c.octets + 4 * g);
+                t0 = ld_stream_u64x2(c.start + 4 * g);
+                t1 = ld_stream_u64x2(c.start + 4 * g + 2);
+                e0 = ld_stream_u64x2(c.end + 4 * g);
+                e1 = ld_stream_u64x2(c.end + 4 * g + 2);
             }
-            done = n4 * 4;
+            bool f;
+            it = FwdItem{0, o.x, e0.x - t0.x};
+            f = classify<kSmem>(ok, s.x, d.x, k.x, o.x, it.dur, p, gt, t, it.packed);
+            push<kHot>(f, it, q, qn, lane, mask, P, h);
+            it = FwdItem{0, o.y, e0.y - t0.y};
+            f = classify<kSmem>(ok, s.y, d.y, k.y, o.y, it.dur, p, gt, t, it.packed);
+            push<kHot>(f, it, q, qn, lane, mask, P, h);
+            it = FwdItem{0, o.z, e1.x - t1.x};
+            f = classify<kSmem>(ok, s.z, d.z, k.z, o.z, it.dur, p, gt, t, it.packed);
+            push<kHot>(f, it, q, qn, lane, mask, P, h);
+            it = FwdItem{0, o.w, e1.y - t1.y};
+            f = classify<kSmem>(ok, s.w, d.w, k.w, o.w, it.dur, p, gt, t, it.packed);
+            push<kHot>(f, it, q, qn, lane, mask, P, h);
         }
-        for (uint64_t i = done + tid; i < c.n; i += stride)
-            process<kSmem, kHot>(c.src[i], c.dst[i], c.pkts[i], c.octets[i], c.start[i], c.end[i],
-                                 p, gt, P, h, t);
+        // The n % 4 tail records: the first warp of the grid.
+        if (warp_gid == 0) {
+            const uint64_t i = n4 * 4 + lane;
+            const bool ok = i < c.n;
+            it = FwdItem{0, ok ? c.octets[i] : 0u, ok ? c.end[i] - c.start[i] : 0ull};
+            const bool f = classify<kSmem>(ok, ok ? c.src[i] : 0u, ok ? c.dst[i] : 0u,
+                                           ok ? c.pkts[i] : 0u, it.oct, it.dur, p, gt, t, it.packed);
+            push<kHot>(f, it, q, qn, lane, mask, P, h);
+        }
     } else {
-        const unsigned char* rec = static_cast<const unsigned char*>(b.rec);
-        for (uint64_t i = tid; i < b.n; i += stride) {
-            const unsigned char* r = rec + i * 64;
-            if constexpr (kLayout == 2) {
-                const uint4 a = __ldg(reinterpret_cast<const uint4*>(r));       // src dst nexthop ifs
-                const uint4 c = __ldg(reinterpret_cast<const uint4*>(r + 16));  // pkts octets first last
-                const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(r + 48)); // start end
-                process<kSmem, kHot>(a.x, a.y, c.x, c.y, e.x, e.y, p, gt, P, h, t);
-            } else {
-                const uint32_t* w = reinterpret_cast<const uint32_t*>(r);
-                const uint64_t* q = reinterpret_cast<const uint64_t*>(r + 48);
-                process<kSmem, kHot>(w[0], w[1], w[4], w[5], q[0], q[1], p, gt, P, h, t);
+        const uint64_t n = b.n;
+        for (uint64_t base = warp_gid * 32; base < n; base += nwarps * 32) {
+            const uint64_t i = base + lane;
+            const bool ok = i < n;
+            uint32_t src = 0, dst = 0, pkts = 0, oct = 0;
+            uint64_t start = 0, end = 0;
+            if (ok) {
+                if constexpr (kLayout == 1) {
+                    const DevSoA& c = b.soa;
+                    src = c.src[i], dst = c.dst[i], pkts = c.pkts[i], oct = c.octets[i];
+                    start = c.start[i], end = c.end[i];
+                } else if constexpr (kLayout == 2) {
+                    const unsigned char* r = static_cast<const unsigned char*>(b.rec) + i * 64;
+                    const uint4 a = __ldg(reinterpret_cast<const uint4*>(r));        // src dst nexthop ifs
+                    const uint4 cc = __ldg(reinterpret_cast<const uint4*>(r + 16));  // pkts octets first last
+                    const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(r + 48)); // start end
+                    src = a.x, dst = a.y, pkts = cc.x, oct = cc.y, start = e.x, end = e.y;
+                } else {
+                    const unsigned char* r = static_cast<const unsigned char*>(b.rec) + i * 64;
+                    const uint32_t* w = reinterpret_cast<const uint32_t*>(r);
+                    const uint64_t* qq = reinterpret_cast<const uint64_t*>(r + 48);
+                    src = w[0], dst = w[1], pkts = w[4], oct = w[5], start = qq[0], end = qq[1];
+                }
             }
+            it = FwdItem{0, oct, end - start};
+            const bool f = classify<kSmem>(ok, src, dst, pkts, oct, it.dur, p, gt, t, it.packed);
+            push<kHot>(f, it, q, qn, lane, mask, P, h);
         }
     }
+    // Drain the partial queue.
+    __syncwarp();
+    if (lane < qn) accumulate<kHot>(q[lane], mask, P, h);
     flush_tallies(t, P.sums + static_cast<size_t>(P.n_sites) * 4);
     if constexpr (kHot) {
         __syncthreads();
@@ -593,7 +713,7 @@ LaunchCfg k2_config(int device, uint64_t n, uint32_t table_words, bool hot, int*
     c.block = kK2Block;
     const size_t tbytes = table_smem_bytes(table_words);
     c.table_in_smem = tbytes <= kSmemTableMax;
-    c.smem = (c.table_in_smem ? tbytes : 0) + (hot ? kHotBytes : 0);
+    c.smem = (c.table_in_smem ? tbytes : 0) + (hot ? kHotBytes : 0) + kQueueBytes;
     int per_sm = occ_cache ? occ_cache[hot ? 1 : 0] : 0;
     if (per_sm > 0) {
     } else if (c.table_in_smem)
