@@ -279,7 +279,7 @@ void launch_k2_timed(gnm_ctx* c, const gnm::DevBatch& b, const gnm::DevParams& p
         ck(cudaEventRecord(pe.a, c->stream), "cudaEventRecord");
     }
     // K1: hot-site plan for this batch (skipped when no site can be hot).
-    const gnm::LaunchCfg cold = gnm::k2_config(c->device, b.n, c->table.n_words, false, c->occ);
+    const gnm::LaunchCfg cold = gnm::k2_config(c->device, b, c->table.n_words, false, c->occ);
     bool hot = false;
     if (c->hot_mode != GNM_HOT_OFF) {
         cudaError_t e;
@@ -287,7 +287,7 @@ void launch_k2_timed(gnm_ctx* c, const gnm::DevBatch& b, const gnm::DevParams& p
                             c->hot_mode == GNM_HOT_FORCE, c->stream, &c->kernel_launches, &e);
         ck(e, "hot-site plan");
     }
-    const gnm::LaunchCfg cfg = hot ? gnm::k2_config(c->device, b.n, c->table.n_words, true, c->occ) : cold;
+    const gnm::LaunchCfg cfg = hot ? gnm::k2_config(c->device, b, c->table.n_words, true, c->occ) : cold;
     gnm::DevHot h{c->d_scratch + 2 * static_cast<size_t>(c->P.n_sites), hot ? gnm::kHotSlots : 0u};
     if (c->timing) {
         ck(cudaEventRecord(pe.b, c->stream), "cudaEventRecord");
@@ -785,7 +785,10 @@ int gnm_classify(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* p
                 temps.push_back(t);
                 dout = static_cast<uint32_t*>(t);
             }
-            const gnm::LaunchCfg cfg = gnm::k2_config(c->device, b->n, c->table.n_words, false, c->occ);
+            gnm::DevBatch cb{};
+            cb.n = b->n;
+            cb.aos = true; // the classify kernel uses the plain launch shape
+            const gnm::LaunchCfg cfg = gnm::k2_config(c->device, cb, c->table.n_words, false, c->occ);
             ck(gnm::launch_classify(cfg, d, c->table, p, dout, c->stream), "classify launch");
             c->kernel_launches += 1;
             if (out_mem == GNM_MEM_HOST)

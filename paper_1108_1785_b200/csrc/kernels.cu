@@ -436,6 +436,190 @@ __global__ void __launch_bounds__(kK2Block, 2) k2(DevBatch b, const uint32_t* __
     }
 }
 
+// ---- K2, TMA-staged SoA variant ---------------------------------------------
+// One persistent CTA per SM (kTmaBlock threads). Each CTA walks tiles
+// blockIdx.x, +gridDim.x, ... of kTile records; a tile's six columns (32 KB)
+// land in a shared-memory stage through cp.async.bulk (TMA bulk copies,
+// evict-first in L2 so the stream does not push the L2-resident histogram and
+// accumulators out), completing on the stage's mbarrier. kStages tiles are in
+// flight at all times: the LAST warp to finish with a stage re-arms it with
+// the CTA's next-but-(kStages-1) tile, so loads never wait for compute.
+// Lane l of warp w reads record w*32+l of the tile from shared memory.
+constexpr int kTmaBlock = 1024;
+constexpr uint32_t kTile = 1024;
+constexpr uint32_t kStageBytes = kTile * 32;
+constexpr uint32_t kMaxStages = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+struct Stage {
+    uint32_t* src;
+    uint32_t* dst;
+    uint32_t* pkts;
+    uint32_t* oct;
+    uint64_t* start;
+    uint64_t* end;
+};
+
+__device__ __forceinline__ Stage stage_at(unsigned char* base, uint32_t s) {
+    unsigned char* b = base + static_cast<size_t>(s) * kStageBytes;
+    Stage st;
+    st.src = reinterpret_cast<uint32_t*>(b);
+    st.dst = st.src + kTile;
+    st.pkts = st.dst + kTile;
+    st.oct = st.pkts + kTile;
+    st.start = reinterpret_cast<uint64_t*>(st.oct + kTile);
+    st.end = st.start + kTile;
+    return st;
+}
+
+// Records [first, first + count) of the 4-aligned prefix into stage st.
+__device__ __forceinline__ void issue_tile(const Stage& st, const DevSoA& c, uint64_t first,
+                                           uint32_t count, uint64_t* bar, uint64_t pol) {
+    mbar_expect_tx(bar, count * 32u);
+    tma_load_1d(st.src, c.src + first, count * 4u, bar, pol);
+    tma_load_1d(st.dst, c.dst + first, count * 4u, bar, pol);
+    tma_load_1d(st.pkts, c.pkts + first, count * 4u, bar, pol);
+    tma_load_1d(st.oct, c.octets + first, count * 4u, bar, pol);
+    tma_load_1d(st.start, c.start + first, count * 8u, bar, pol);
+    tma_load_1d(st.end, c.end + first, count * 8u, bar, pol);
+}
+
+template <bool kSmem, bool kHot>
+__global__ void __launch_bounds__(kTmaBlock, 1) k2_tma(DevSoA c, const uint32_t* __restrict__ gt,
+                                                        uint32_t table_words, DevParams p,
+                                                        DevPartials P, DevHot hot,
+                                                        uint32_t n_stages) {
+    const uint32_t smem_words = kSmem ? table_words : 0u;
+    load_table<kSmem>(gt, table_words);
+    HotSmem h{};
+    if constexpr (kHot) {
+        h = hot_smem(smem_words);
+        hot_init(h);
+    }
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t nwarps = blockDim.x >> 5;
+    uint32_t* after_hot = g_smem + smem_words + (kHot ? kHotBytes / 4 : 0u);
+    FwdItem* q = reinterpret_cast<FwdItem*>(after_hot) + warp * kQueue;
+    unsigned char* stages = reinterpret_cast<unsigned char*>(after_hot) + nwarps * kQueue * sizeof(FwdItem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(stages + static_cast<size_t>(n_stages) * kStageBytes);
+    uint32_t* done = reinterpret_cast<uint32_t*>(full + kMaxStages);
+
+    const uint64_t n_vec = c.n & ~3ull; // TMA-covered prefix (16-byte multiples)
+    const uint64_t n_tiles = (n_vec + kTile - 1) / kTile;
+    const uint64_t pol = evict_first_policy();
+    auto tile_first = [&](uint64_t local) { return (blockIdx.x + local * gridDim.x) * kTile; };
+    auto tile_count = [&](uint64_t first) {
+        return static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), n_vec - first));
+    };
+    const uint64_t my_tiles =
+        blockIdx.x < n_tiles ? (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+
+    if (threadIdx.x == 0) {
+        for (uint32_t s = 0; s < n_stages; ++s) {
+            mbar_init(full + s, 1);
+            done[s] = 0;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (uint32_t s = 0; s < n_stages && s < my_tiles; ++s) {
+            const uint64_t f = tile_first(s);
+            issue_tile(stage_at(stages, s), c, f, tile_count(f), full + s, pol);
+        }
+    }
+
+    Tally t;
+    const uint32_t mask = p.site_mask;
+    FwdItem it;
+    uint32_t qn = 0;
+    for (uint64_t i = 0; i < my_tiles; ++i) {
+        const uint32_t s = static_cast<uint32_t>(i % n_stages);
+        const uint32_t parity = static_cast<uint32_t>((i / n_stages) & 1u);
+        const uint64_t first = tile_first(i);
+        const uint32_t count = tile_count(first);
+        const Stage st = stage_at(stages, s);
+        mbar_wait(full + s, parity);
+        const uint32_t k = warp * 32 + lane;
+        const bool ok = k < count;
+        uint32_t src = 0, dst = 0, pkts = 0;
+        it = FwdItem{0, 0, 0};
+        if (ok) {
+            src = st.src[k];
+            dst = st.dst[k];
+            pkts = st.pkts[k];
+            it.oct = st.oct[k];
+            it.dur = st.end[k] - st.start[k];
+        }
+        // Release the stage: the last warp out re-arms it with tile i + n_stages.
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();
+            if (atomicAdd(done + s, 1u) == nwarps - 1) {
+                done[s] = 0;
+                __threadfence_block();
+                if (i + n_stages < my_tiles) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    const uint64_t f = tile_first(i + n_stages);
+                    issue_tile(st, c, f, tile_count(f), full + s, pol);
+                }
+            }
+        }
+        const bool f = classify<kSmem>(ok, src, dst, pkts, it.oct, it.dur, p, gt, t, it.packed);
+        push<kHot>(f, it, q, qn, lane, mask, P, h);
+    }
+    // The n % 4 tail records: block 0, warp 0, direct loads.
+    if (blockIdx.x == 0 && warp == 0) {
+        const uint64_t r = n_vec + lane;
+        const bool ok = r < c.n;
+        it = FwdItem{0, ok ? c.octets[r] : 0u, ok ? c.end[r] - c.start[r] : 0ull};
+        const bool f = classify<kSmem>(ok, ok ? c.src[r] : 0u, ok ? c.dst[r] : 0u,
+                                       ok ? c.pkts[r] : 0u, it.oct, it.dur, p, gt, t, it.packed);
+        push<kHot>(f, it, q, qn, lane, mask, P, h);
+    }
+    __syncwarp();
+    if (lane < qn) accumulate<kHot>(q[lane], mask, P, h);
+    flush_tallies(t, P.sums + static_cast<size_t>(P.n_sites) * 4);
+    if constexpr (kHot) {
+        __syncthreads();
+        hot_flush(h, hot, P);
+    }
+}
+
 // ---- K1: hot-site plan ------------------------------------------------------
 // Each block classifies one contiguous chunk of the batch and counts Forward
 // flows per site.
@@ -704,14 +888,47 @@ cudaError_t init_kernel_attributes() {
     if ((e = allow_layout<1>())) return e;
     if ((e = allow_layout<2>())) return e;
     if ((e = allow_layout<3>())) return e;
+    if ((e = allow_smem(k2_tma<true, true>))) return e;
+    if ((e = allow_smem(k2_tma<true, false>))) return e;
+    if ((e = allow_smem(k2_tma<false, true>))) return e;
+    if ((e = allow_smem(k2_tma<false, false>))) return e;
     if ((e = allow_smem(k_sample<true>))) return e;
     return allow_smem(k_classify<true>);
 }
 
-LaunchCfg k2_config(int device, uint64_t n, uint32_t table_words, bool hot, int* occ_cache) {
+namespace {
+bool soa_aligned(const DevBatch& b) {
+    const DevSoA& c = b.soa;
+    return !b.aos &&
+           ((reinterpret_cast<uintptr_t>(c.src) | reinterpret_cast<uintptr_t>(c.dst) |
+             reinterpret_cast<uintptr_t>(c.pkts) | reinterpret_cast<uintptr_t>(c.octets) |
+             reinterpret_cast<uintptr_t>(c.start) | reinterpret_cast<uintptr_t>(c.end)) & 15u) == 0;
+}
+} // namespace
+
+LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool hot, int* occ_cache) {
     LaunchCfg c;
-    c.block = kK2Block;
     const size_t tbytes = table_smem_bytes(table_words);
+    const uint64_t n_tiles = ((b.n & ~3ull) + kTile - 1) / kTile;
+    c.stages = 0;
+    if (soa_aligned(b) && n_tiles > 0) {
+        // TMA-staged variant: one 1024-thread CTA per SM, >= 2 stages in flight.
+        const size_t fixed = (hot ? kHotBytes : 0) + (kTmaBlock / 32) * kQueue * sizeof(FwdItem) +
+                             kMaxStages * 16;
+        const bool tsm = tbytes + fixed + 2 * kStageBytes <= kSmemMax;
+        const size_t base = fixed + (tsm ? tbytes : 0);
+        const uint32_t stages =
+            base < kSmemMax ? static_cast<uint32_t>(std::min<size_t>(kMaxStages, (kSmemMax - base) / kStageBytes)) : 0;
+        if (stages >= 2) {
+            c.block = kTmaBlock;
+            c.table_in_smem = tsm;
+            c.smem = base + static_cast<size_t>(stages) * kStageBytes;
+            c.stages = stages;
+            c.grid = static_cast<int>(std::min<uint64_t>(sm_count(device), n_tiles));
+            return c;
+        }
+    }
+    c.block = kK2Block;
     c.table_in_smem = tbytes <= kSmemTableMax;
     c.smem = (c.table_in_smem ? tbytes : 0) + (hot ? kHotBytes : 0) + kQueueBytes;
     int per_sm = occ_cache ? occ_cache[hot ? 1 : 0] : 0;
@@ -726,7 +943,7 @@ LaunchCfg k2_config(int device, uint64_t n, uint32_t table_words, bool hot, int*
     const uint64_t resident = static_cast<uint64_t>(per_sm) * sm_count(device);
     // At least 16 records per thread so the per-CTA table load amortises.
     const uint64_t per_block = static_cast<uint64_t>(c.block) * 16;
-    const uint64_t want = (n + per_block - 1) / per_block;
+    const uint64_t want = (b.n + per_block - 1) / per_block;
     c.grid = static_cast<int>(std::max<uint64_t>(1, std::min(resident, want)));
     return c;
 }
@@ -778,6 +995,17 @@ bool plan_hot(int device, const DevBatch& b, const DevTable& t, const DevParams&
 cudaError_t launch_k2(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t,
                       const DevParams& p, const DevPartials& P, const DevHot& hot,
                       cudaStream_t s) {
+    if (cfg.stages) {
+        const bool hh = hot.n_slots > 0;
+        if (cfg.table_in_smem) {
+            if (hh) k2_tma<true, true><<<cfg.grid, cfg.block, cfg.smem, s>>>(b.soa, t.words, t.n_words, p, P, hot, cfg.stages);
+            else k2_tma<true, false><<<cfg.grid, cfg.block, cfg.smem, s>>>(b.soa, t.words, t.n_words, p, P, hot, cfg.stages);
+        } else {
+            if (hh) k2_tma<false, true><<<cfg.grid, cfg.block, cfg.smem, s>>>(b.soa, t.words, t.n_words, p, P, hot, cfg.stages);
+            else k2_tma<false, false><<<cfg.grid, cfg.block, cfg.smem, s>>>(b.soa, t.words, t.n_words, p, P, hot, cfg.stages);
+        }
+        return cudaGetLastError();
+    }
     if (b.aos) {
         const bool vec = (reinterpret_cast<uintptr_t>(b.rec) & 15u) == 0;
         if (vec) launch_k2_l<2>(cfg, b, t, p, P, hot, s);

@@ -67,6 +67,7 @@ struct LaunchCfg {
     int block;
     size_t smem;
     bool table_in_smem;
+    uint32_t stages; // > 0: TMA-staged SoA variant with this many stages
 };
 
 // Once per device: opt the shared-memory kernels into large dynamic smem.
@@ -74,7 +75,7 @@ cudaError_t init_kernel_attributes();
 
 // Occupancy-derived launch configuration for K2 over n records.
 // occ_cache[hot] memoises blocks/SM (0 = unknown) for this table size.
-LaunchCfg k2_config(int device, uint64_t n, uint32_t table_words, bool hot, int* occ_cache);
+LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool hot, int* occ_cache);
 
 // K1 (optional, skewed batches): sample the batch, pick the hot sites and
 // write their slots into the table words. Returns false when the batch is
