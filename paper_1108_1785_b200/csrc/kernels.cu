@@ -58,6 +58,20 @@ __device__ __forceinline__ ulonglong2 ld_stream_u64x2(const void* p) {
     return r;
 }
 
+// ---- fire-and-forget global reductions (RED, never a returning ATOM) -------
+__device__ __forceinline__ void red_add(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_add(unsigned int* p, unsigned int v) {
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_min(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_max(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 // ---- registry table (layout in registry.hpp, DeviceTable) -----------------
 template <bool kSmem>
 __device__ __forceinline__ uint32_t table_word(const uint32_t* __restrict__ gt, uint32_t i) {
@@ -216,7 +230,7 @@ __device__ __forceinline__ void accumulate(const FwdItem& it, uint32_t site_mask
     const uint32_t bucket = bucket_of(rate);
     uint64_t lo, hi;
     ubps_of(oct, it.dur, rate, lo, hi);
-    atomicAdd(P.hist + static_cast<size_t>(site) * kBuckets + bucket, 1u);
+    red_add(P.hist + static_cast<size_t>(site) * kBuckets + bucket, 1u);
     const unsigned long long rb = static_cast<unsigned long long>(__double_as_longlong(rate));
     if (hot) {
         // 32-bit shared atomics with exact carry propagation.
@@ -238,12 +252,12 @@ __device__ __forceinline__ void accumulate(const FwdItem& it, uint32_t site_mask
         if (rb > h.mx[slot]) atomicMax(h.mx + slot, rb);
     } else {
         unsigned long long* s = P.sums + static_cast<size_t>(site) * 4;
-        atomicAdd(s + 0, static_cast<unsigned long long>(oct));
-        atomicAdd(s + 1, lo & 0xFFFFFFFFull);
-        if (lo >> 32) atomicAdd(s + 2, lo >> 32);
-        if (hi) atomicAdd(s + 3, hi);
-        if (rb < cur_mn) atomicMin(P.mn + site, rb);
-        if (rb > cur_mx) atomicMax(P.mx + site, rb);
+        red_add(s + 0, static_cast<unsigned long long>(oct));
+        red_add(s + 1, lo & 0xFFFFFFFFull);
+        if (lo >> 32) red_add(s + 2, lo >> 32);
+        if (hi) red_add(s + 3, hi);
+        if (rb < cur_mn) red_min(P.mn + site, rb);
+        if (rb > cur_mx) red_max(P.mx + site, rb);
     }
 }
 
@@ -305,10 +319,10 @@ __device__ __forceinline__ void flush_tallies(const Tally& t, unsigned long long
     const uint32_t d = __reduce_add_sync(0xFFFFFFFFu, t.admin);
     const uint32_t u = __reduce_add_sync(0xFFFFFFFFu, t.unm);
     if ((threadIdx.x & 31u) == 0) {
-        if (f) atomicAdd(out + 0, static_cast<unsigned long long>(f));
-        if (a) atomicAdd(out + 1, static_cast<unsigned long long>(a));
-        if (d) atomicAdd(out + 2, static_cast<unsigned long long>(d));
-        if (u) atomicAdd(out + 3, static_cast<unsigned long long>(u));
+        if (f) red_add(out + 0, static_cast<unsigned long long>(f));
+        if (a) red_add(out + 1, static_cast<unsigned long long>(a));
+        if (d) red_add(out + 2, static_cast<unsigned long long>(d));
+        if (u) red_add(out + 3, static_cast<unsigned long long>(u));
     }
 }
 
@@ -318,12 +332,12 @@ __device__ __forceinline__ void hot_flush(const HotSmem& h, const DevHot& hot, c
         if (oct == 0) continue; // untouched: every Forward flow has >= 97 octets
         const uint32_t site = __ldg(hot.hot_site + slot);
         unsigned long long* s = P.sums + static_cast<size_t>(site) * 4;
-        atomicAdd(s + 0, oct);
-        atomicAdd(s + 1, static_cast<unsigned long long>(h.u0[slot]));
-        if (h.u1[slot]) atomicAdd(s + 2, static_cast<unsigned long long>(h.u1[slot]));
-        if (h.u2[slot]) atomicAdd(s + 3, static_cast<unsigned long long>(h.u2[slot]));
-        atomicMin(P.mn + site, h.mn[slot]);
-        atomicMax(P.mx + site, h.mx[slot]);
+        red_add(s + 0, oct);
+        red_add(s + 1, static_cast<unsigned long long>(h.u0[slot]));
+        if (h.u1[slot]) red_add(s + 2, static_cast<unsigned long long>(h.u1[slot]));
+        if (h.u2[slot]) red_add(s + 3, static_cast<unsigned long long>(h.u2[slot]));
+        red_min(P.mn + site, h.mn[slot]);
+        red_max(P.mx + site, h.mx[slot]);
     }
 }
 
