@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <new>
@@ -79,6 +80,7 @@ struct gnm_ctx {
     size_t table_cap_words = 0;
     gnm::DevTable table{};
     int hot_mode = GNM_HOT_AUTO;
+    uint32_t cold_red = 0; // GNM_COLD_MINMAX=red: unconditional cold-site min/max RED
 
     // partials
     gnm::DevPartials P{};
@@ -147,6 +149,7 @@ gnm::DevParams dev_params(const gnm_ctx* c, const gnm_filter_params* p) {
     q.min_packets = p->min_packets;
     q.min_duration_ms = p->min_duration_ms;
     q.site_mask = c->table.packed ? gnm::kPackedSiteMask : 0x7FFFFFFFu;
+    q.cold_red = c->cold_red;
     return q;
 }
 
@@ -595,6 +598,8 @@ int gnm_ctx_create(int device, gnm_ctx** out) {
             ck(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
             ck(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
             c->stream = c->own_stream;
+            const char* cm = std::getenv("GNM_COLD_MINMAX");
+            c->cold_red = cm && std::strcmp(cm, "red") == 0;
             for (int i = 0; i < 2; ++i) {
                 ck(cudaEventCreateWithFlags(&c->ev_h2d[i], cudaEventDisableTiming), "cudaEventCreate");
                 ck(cudaEventCreateWithFlags(&c->ev_k2[i], cudaEventDisableTiming), "cudaEventCreate");

@@ -98,6 +98,30 @@ __device__ __forceinline__ uint32_t lookup(const uint32_t* __restrict__ gt, uint
     return table_word<kSmem>(gt, node + ((ip >> 8) & 0xFFu));
 }
 
+// attribute (rate_engine.cpp:127-146) as one branch-free probe of both
+// endpoints: the two directory words, nodes and leaf words are loaded with
+// predicated selects (a uniform node reads word 0 as a dummy leaf), and the
+// src value wins when both hit. Avoids the divergent src-then-dst chain.
+template <bool kSmem>
+__device__ __forceinline__ uint32_t lookup2(const uint32_t* __restrict__ gt, uint32_t src,
+                                            uint32_t dst) {
+    const uint32_t ds = src >> 16, dd = dst >> 16;
+    const uint2 ws = table_pair<kSmem>(gt, ds >> 5);
+    const uint2 wd = table_pair<kSmem>(gt, dd >> 5);
+    const uint32_t bs = ds & 31u, bd = dd & 31u;
+    const bool hs = (ws.x >> bs) & 1u, hd = (wd.x >> bd) & 1u;
+    const uint32_t ns =
+        hs ? table_word<kSmem>(gt, 4096u + ws.y + __popc(ws.x & ((1u << bs) - 1u))) : 0x80000000u | kNone;
+    const uint32_t nd =
+        hd ? table_word<kSmem>(gt, 4096u + wd.y + __popc(wd.x & ((1u << bd) - 1u))) : 0x80000000u | kNone;
+    const bool us = ns & 0x80000000u, ud = nd & 0x80000000u;
+    const uint32_t ls = table_word<kSmem>(gt, us ? 0u : ns + ((src >> 8) & 0xFFu));
+    const uint32_t ld = table_word<kSmem>(gt, ud ? 0u : nd + ((dst >> 8) & 0xFFu));
+    const uint32_t vs = us ? (hs ? (ns & 0x7FFFFFFFu) : kNone) : ls;
+    const uint32_t vd = ud ? (hd ? (nd & 0x7FFFFFFFu) : kNone) : ld;
+    return vs != kNone ? vs : vd;
+}
+
 template <bool kSmem>
 __device__ __forceinline__ void load_table(const uint32_t* __restrict__ gt, uint32_t words) {
     if constexpr (kSmem) {
@@ -213,14 +237,15 @@ constexpr uint32_t kQueue = 64; // per-warp FwdItem capacity (< 32 left + 32 pus
 //   (a stale value is never below the current min / above the current max).
 // Called on warp-compacted items, so the arithmetic runs with full warps.
 template <bool kHot>
-__device__ __forceinline__ void accumulate(const FwdItem& it, uint32_t site_mask,
+__device__ __forceinline__ void accumulate(const FwdItem& it, const DevParams& p,
                                            const DevPartials& P, const HotSmem& h) {
-    const uint32_t site = it.packed & site_mask;
+    const uint32_t site = it.packed & p.site_mask;
     const uint32_t slot = kHot ? it.packed >> 20 : 0u;
     const bool hot = kHot && slot;
-    // Cold sites: fetch the current min/max first; the loads overlap the math.
-    unsigned long long cur_mn = 0, cur_mx = 0;
-    if (!hot) {
+    // Cold sites: fetch the current min/max first (the loads overlap the
+    // math), unless the context asked for unconditional min/max reductions.
+    unsigned long long cur_mn = 0, cur_mx = ~0ull;
+    if (!hot && !p.cold_red) {
         cur_mn = __ldcg(P.mn + site);
         cur_mx = __ldcg(P.mx + site);
     }
@@ -256,8 +281,8 @@ __device__ __forceinline__ void accumulate(const FwdItem& it, uint32_t site_mask
         red_add(s + 1, lo & 0xFFFFFFFFull);
         if (lo >> 32) red_add(s + 2, lo >> 32);
         if (hi) red_add(s + 3, hi);
-        if (rb < cur_mn) red_min(P.mn + site, rb);
-        if (rb > cur_mx) red_max(P.mx + site, rb);
+        if (p.cold_red || rb < cur_mn) red_min(P.mn + site, rb);
+        if (p.cold_red || rb > cur_mx) red_max(P.mx + site, rb);
     }
 }
 
@@ -282,8 +307,7 @@ __device__ __forceinline__ bool classify(bool valid, uint32_t src, uint32_t dst,
         ++t.admin;
         return false;
     }
-    uint32_t v = lookup<kSmem>(gt, src);
-    if (v == kNone) v = lookup<kSmem>(gt, dst);
+    const uint32_t v = lookup2<kSmem>(gt, src, dst);
     if (v == kNone) {
         ++t.unm;
         return false;
@@ -299,7 +323,7 @@ __device__ __forceinline__ bool classify(bool valid, uint32_t src, uint32_t dst,
 // ~40% lane occupancy the class mix would otherwise leave it.
 template <bool kHot>
 __device__ __forceinline__ void push(bool fwd, const FwdItem& it, FwdItem* q, uint32_t& qn,
-                                     uint32_t lane, uint32_t site_mask, const DevPartials& P,
+                                     uint32_t lane, const DevParams& p, const DevPartials& P,
                                      const HotSmem& h) {
     const unsigned m = __ballot_sync(0xFFFFFFFFu, fwd);
     if (fwd) q[qn + __popc(m & ((1u << lane) - 1u))] = it;
@@ -309,7 +333,7 @@ __device__ __forceinline__ void push(bool fwd, const FwdItem& it, FwdItem* q, ui
         const FwdItem x = q[qn - 32 + lane];
         qn -= 32;
         __syncwarp();
-        accumulate<kHot>(x, site_mask, P, h);
+        accumulate<kHot>(x, p, P, h);
     }
 }
 
@@ -367,7 +391,6 @@ __global__ void __launch_bounds__(kK2Block, 2) k2(DevBatch b, const uint32_t* __
     Tally t;
     const uint64_t warp_gid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-    const uint32_t mask = p.site_mask;
     FwdItem it;
     if constexpr (kLayout == 0) {
         const DevSoA& c = b.soa;
@@ -390,16 +413,16 @@ __global__ void __launch_bounds__(kK2Block, 2) k2(DevBatch b, const uint32_t* __
             bool f;
             it = FwdItem{0, o.x, e0.x - t0.x};
             f = classify<kSmem>(ok, s.x, d.x, k.x, o.x, it.dur, p, gt, t, it.packed);
-            push<kHot>(f, it, q, qn, lane, mask, P, h);
+            push<kHot>(f, it, q, qn, lane, p, P, h);
             it = FwdItem{0, o.y, e0.y - t0.y};
             f = classify<kSmem>(ok, s.y, d.y, k.y, o.y, it.dur, p, gt, t, it.packed);
-            push<kHot>(f, it, q, qn, lane, mask, P, h);
+            push<kHot>(f, it, q, qn, lane, p, P, h);
             it = FwdItem{0, o.z, e1.x - t1.x};
             f = classify<kSmem>(ok, s.z, d.z, k.z, o.z, it.dur, p, gt, t, it.packed);
-            push<kHot>(f, it, q, qn, lane, mask, P, h);
+            push<kHot>(f, it, q, qn, lane, p, P, h);
             it = FwdItem{0, o.w, e1.y - t1.y};
             f = classify<kSmem>(ok, s.w, d.w, k.w, o.w, it.dur, p, gt, t, it.packed);
-            push<kHot>(f, it, q, qn, lane, mask, P, h);
+            push<kHot>(f, it, q, qn, lane, p, P, h);
         }
         // The n % 4 tail records: the first warp of the grid.
         if (warp_gid == 0) {
@@ -408,7 +431,7 @@ __global__ void __launch_bounds__(kK2Block, 2) k2(DevBatch b, const uint32_t* __
             it = FwdItem{0, ok ? c.octets[i] : 0u, ok ? c.end[i] - c.start[i] : 0ull};
             const bool f = classify<kSmem>(ok, ok ? c.src[i] : 0u, ok ? c.dst[i] : 0u,
                                            ok ? c.pkts[i] : 0u, it.oct, it.dur, p, gt, t, it.packed);
-            push<kHot>(f, it, q, qn, lane, mask, P, h);
+            push<kHot>(f, it, q, qn, lane, p, P, h);
         }
     } else {
         const uint64_t n = b.n;
@@ -437,12 +460,12 @@ __global__ void __launch_bounds__(kK2Block, 2) k2(DevBatch b, const uint32_t* __
             }
             it = FwdItem{0, oct, end - start};
             const bool f = classify<kSmem>(ok, src, dst, pkts, oct, it.dur, p, gt, t, it.packed);
-            push<kHot>(f, it, q, qn, lane, mask, P, h);
+            push<kHot>(f, it, q, qn, lane, p, P, h);
         }
     }
     // Drain the partial queue.
     __syncwarp();
-    if (lane < qn) accumulate<kHot>(q[lane], mask, P, h);
+    if (lane < qn) accumulate<kHot>(q[lane], p, P, h);
     flush_tallies(t, P.sums + static_cast<size_t>(P.n_sites) * 4);
     if constexpr (kHot) {
         __syncthreads();
@@ -463,6 +486,7 @@ constexpr int kTmaBlock = 1024;
 constexpr uint32_t kTile = 1024;
 constexpr uint32_t kStageBytes = kTile * 32;
 constexpr uint32_t kMaxStages = 4;
+constexpr uint32_t kChunksPerTile = kTile / 32;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -550,7 +574,8 @@ __global__ void __launch_bounds__(kTmaBlock, 1) k2_tma(DevSoA c, const uint32_t*
     FwdItem* q = reinterpret_cast<FwdItem*>(after_hot) + warp * kQueue;
     unsigned char* stages = reinterpret_cast<unsigned char*>(after_hot) + nwarps * kQueue * sizeof(FwdItem);
     uint64_t* full = reinterpret_cast<uint64_t*>(stages + static_cast<size_t>(n_stages) * kStageBytes);
-    uint32_t* done = reinterpret_cast<uint32_t*>(full + kMaxStages);
+    uint32_t* released = reinterpret_cast<uint32_t*>(full + kMaxStages);
+    uint32_t* claim = released + kMaxStages;
 
     const uint64_t n_vec = c.n & ~3ull; // TMA-covered prefix (16-byte multiples)
     const uint64_t n_tiles = (n_vec + kTile - 1) / kTile;
@@ -561,12 +586,14 @@ __global__ void __launch_bounds__(kTmaBlock, 1) k2_tma(DevSoA c, const uint32_t*
     };
     const uint64_t my_tiles =
         blockIdx.x < n_tiles ? (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const uint64_t my_chunks = my_tiles * kChunksPerTile;
 
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < n_stages; ++s) {
             mbar_init(full + s, 1);
-            done[s] = 0;
+            released[s] = 0;
         }
+        *claim = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -577,18 +604,27 @@ __global__ void __launch_bounds__(kTmaBlock, 1) k2_tma(DevSoA c, const uint32_t*
         }
     }
 
+    // Warps claim 32-record chunks dynamically, so a warp held up in
+    // accumulate() never delays a stage refill: a stage is re-armed (tile
+    // i + n_stages) by whichever warp releases its 32nd chunk. With >= 2
+    // stages, at most one tile beyond the loaded window can be claimed, so
+    // the parity of every wait names the right phase.
     Tally t;
-    const uint32_t mask = p.site_mask;
     FwdItem it;
     uint32_t qn = 0;
-    for (uint64_t i = 0; i < my_tiles; ++i) {
+    for (;;) {
+        uint32_t cl = 0;
+        if (lane == 0) cl = atomicAdd(claim, 1u);
+        cl = __shfl_sync(0xFFFFFFFFu, cl, 0);
+        if (cl >= my_chunks) break;
+        const uint64_t i = cl / kChunksPerTile;
+        const uint32_t chunk = cl % kChunksPerTile;
         const uint32_t s = static_cast<uint32_t>(i % n_stages);
         const uint32_t parity = static_cast<uint32_t>((i / n_stages) & 1u);
-        const uint64_t first = tile_first(i);
-        const uint32_t count = tile_count(first);
+        const uint32_t count = tile_count(tile_first(i));
         const Stage st = stage_at(stages, s);
         mbar_wait(full + s, parity);
-        const uint32_t k = warp * 32 + lane;
+        const uint32_t k = chunk * 32 + lane;
         const bool ok = k < count;
         uint32_t src = 0, dst = 0, pkts = 0;
         it = FwdItem{0, 0, 0};
@@ -599,12 +635,11 @@ __global__ void __launch_bounds__(kTmaBlock, 1) k2_tma(DevSoA c, const uint32_t*
             it.oct = st.oct[k];
             it.dur = st.end[k] - st.start[k];
         }
-        // Release the stage: the last warp out re-arms it with tile i + n_stages.
         __syncwarp();
         if (lane == 0) {
             __threadfence_block();
-            if (atomicAdd(done + s, 1u) == nwarps - 1) {
-                done[s] = 0;
+            if (atomicAdd(released + s, 1u) == kChunksPerTile - 1) {
+                released[s] = 0;
                 __threadfence_block();
                 if (i + n_stages < my_tiles) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -614,7 +649,7 @@ __global__ void __launch_bounds__(kTmaBlock, 1) k2_tma(DevSoA c, const uint32_t*
             }
         }
         const bool f = classify<kSmem>(ok, src, dst, pkts, it.oct, it.dur, p, gt, t, it.packed);
-        push<kHot>(f, it, q, qn, lane, mask, P, h);
+        push<kHot>(f, it, q, qn, lane, p, P, h);
     }
     // The n % 4 tail records: block 0, warp 0, direct loads.
     if (blockIdx.x == 0 && warp == 0) {
@@ -623,10 +658,10 @@ __global__ void __launch_bounds__(kTmaBlock, 1) k2_tma(DevSoA c, const uint32_t*
         it = FwdItem{0, ok ? c.octets[r] : 0u, ok ? c.end[r] - c.start[r] : 0ull};
         const bool f = classify<kSmem>(ok, ok ? c.src[r] : 0u, ok ? c.dst[r] : 0u,
                                        ok ? c.pkts[r] : 0u, it.oct, it.dur, p, gt, t, it.packed);
-        push<kHot>(f, it, q, qn, lane, mask, P, h);
+        push<kHot>(f, it, q, qn, lane, p, P, h);
     }
     __syncwarp();
-    if (lane < qn) accumulate<kHot>(q[lane], mask, P, h);
+    if (lane < qn) accumulate<kHot>(q[lane], p, P, h);
     flush_tallies(t, P.sums + static_cast<size_t>(P.n_sites) * 4);
     if constexpr (kHot) {
         __syncthreads();

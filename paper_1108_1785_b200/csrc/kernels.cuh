@@ -19,6 +19,7 @@ struct DevParams {
     uint32_t min_packets;
     uint32_t min_duration_ms;
     uint32_t site_mask;       // kPackedSiteMask, or 0x7FFFFFFF for wide tables
+    uint32_t cold_red;        // 1: cold-site min/max as unconditional RED (no L2 read)
 };
 
 // Device partial accumulators of one context (layout in gnetmon.h, gnm_partials).
