@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(kK2Block, 2) k2(DevBatch b, const uint32_t* __
 constexpr int kTmaBlock = 1024;
 constexpr uint32_t kTile = 1024;
 constexpr uint32_t kStageBytes = kTile * 32;
-constexpr uint32_t kMaxStages = 4;
+constexpr uint32_t kStages = 3;
 constexpr uint32_t kChunksPerTile = kTile / 32;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -498,6 +498,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                  "r"(bytes)
                  : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
@@ -558,8 +561,7 @@ __device__ __forceinline__ void issue_tile(const Stage& st, const DevSoA& c, uin
 template <bool kSmem, bool kHot>
 __global__ void __launch_bounds__(kTmaBlock, 1) k2_tma(DevSoA c, const uint32_t* __restrict__ gt,
                                                         uint32_t table_words, DevParams p,
-                                                        DevPartials P, DevHot hot,
-                                                        uint32_t n_stages) {
+                                                        DevPartials P, DevHot hot) {
     const uint32_t smem_words = kSmem ? table_words : 0u;
     load_table<kSmem>(gt, table_words);
     HotSmem h{};
@@ -573,95 +575,94 @@ __global__ void __launch_bounds__(kTmaBlock, 1) k2_tma(DevSoA c, const uint32_t*
     uint32_t* after_hot = g_smem + smem_words + (kHot ? kHotBytes / 4 : 0u);
     FwdItem* q = reinterpret_cast<FwdItem*>(after_hot) + warp * kQueue;
     unsigned char* stages = reinterpret_cast<unsigned char*>(after_hot) + nwarps * kQueue * sizeof(FwdItem);
-    uint64_t* full = reinterpret_cast<uint64_t*>(stages + static_cast<size_t>(n_stages) * kStageBytes);
-    uint32_t* released = reinterpret_cast<uint32_t*>(full + kMaxStages);
-    uint32_t* claim = released + kMaxStages;
+    uint64_t* full = reinterpret_cast<uint64_t*>(stages + static_cast<size_t>(kStages) * kStageBytes);
+    uint64_t* empty = full + kStages;
+    uint32_t* claim = reinterpret_cast<uint32_t*>(empty + kStages);
 
     const uint64_t n_vec = c.n & ~3ull; // TMA-covered prefix (16-byte multiples)
     const uint64_t n_tiles = (n_vec + kTile - 1) / kTile;
-    const uint64_t pol = evict_first_policy();
-    auto tile_first = [&](uint64_t local) { return (blockIdx.x + local * gridDim.x) * kTile; };
+    auto tile_first = [&](uint32_t local) {
+        return (static_cast<uint64_t>(blockIdx.x) + static_cast<uint64_t>(local) * gridDim.x) * kTile;
+    };
     auto tile_count = [&](uint64_t first) {
         return static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), n_vec - first));
     };
-    const uint64_t my_tiles =
-        blockIdx.x < n_tiles ? (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    const uint64_t my_chunks = my_tiles * kChunksPerTile;
+    const uint32_t my_tiles = static_cast<uint32_t>(
+        blockIdx.x < n_tiles ? (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0);
+    const uint32_t my_chunks = my_tiles * kChunksPerTile;
 
     if (threadIdx.x == 0) {
-        for (uint32_t s = 0; s < n_stages; ++s) {
+        for (uint32_t s = 0; s < kStages; ++s) {
             mbar_init(full + s, 1);
-            released[s] = 0;
+            mbar_init(empty + s, kChunksPerTile);
         }
         *claim = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        for (uint32_t s = 0; s < n_stages && s < my_tiles; ++s) {
-            const uint64_t f = tile_first(s);
-            issue_tile(stage_at(stages, s), c, f, tile_count(f), full + s, pol);
-        }
-    }
 
-    // Warps claim 32-record chunks dynamically, so a warp held up in
-    // accumulate() never delays a stage refill: a stage is re-armed (tile
-    // i + n_stages) by whichever warp releases its 32nd chunk. With >= 2
-    // stages, at most one tile beyond the loaded window can be claimed, so
-    // the parity of every wait names the right phase.
     Tally t;
     FwdItem it;
     uint32_t qn = 0;
-    for (;;) {
-        uint32_t cl = 0;
-        if (lane == 0) cl = atomicAdd(claim, 1u);
-        cl = __shfl_sync(0xFFFFFFFFu, cl, 0);
-        if (cl >= my_chunks) break;
-        const uint64_t i = cl / kChunksPerTile;
-        const uint32_t chunk = cl % kChunksPerTile;
-        const uint32_t s = static_cast<uint32_t>(i % n_stages);
-        const uint32_t parity = static_cast<uint32_t>((i / n_stages) & 1u);
-        const uint32_t count = tile_count(tile_first(i));
-        const Stage st = stage_at(stages, s);
-        mbar_wait(full + s, parity);
-        const uint32_t k = chunk * 32 + lane;
-        const bool ok = k < count;
-        uint32_t src = 0, dst = 0, pkts = 0;
-        it = FwdItem{0, 0, 0};
-        if (ok) {
-            src = st.src[k];
-            dst = st.dst[k];
-            pkts = st.pkts[k];
-            it.oct = st.oct[k];
-            it.dur = st.end[k] - st.start[k];
-        }
-        __syncwarp();
+    if (warp == 0) {
+        // Producer: one lane keeps kStages tiles in flight. A stage is
+        // re-armed once all 32 chunks of its previous tile were read
+        // (empty[s] phase), so loads never wait for the accumulate() work.
         if (lane == 0) {
-            __threadfence_block();
-            if (atomicAdd(released + s, 1u) == kChunksPerTile - 1) {
-                released[s] = 0;
-                __threadfence_block();
-                if (i + n_stages < my_tiles) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    const uint64_t f = tile_first(i + n_stages);
-                    issue_tile(st, c, f, tile_count(f), full + s, pol);
-                }
+            const uint64_t pol = evict_first_policy();
+            for (uint32_t j = 0; j < my_tiles; ++j) {
+                const uint32_t s = j % kStages;
+                if (j >= kStages) mbar_wait(empty + s, ((j / kStages) - 1) & 1u);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                const uint64_t f = tile_first(j);
+                issue_tile(stage_at(stages, s), c, f, tile_count(f), full + s, pol);
             }
         }
-        const bool f = classify<kSmem>(ok, src, dst, pkts, it.oct, it.dur, p, gt, t, it.packed);
-        push<kHot>(f, it, q, qn, lane, p, P, h);
+        __syncwarp();
+    } else {
+        // Consumers claim 32-record chunks dynamically: a warp held up in
+        // accumulate() never delays a stage's release. Claims can run at most
+        // one tile past the loaded window (< 32 warps can be parked on an
+        // unloaded tile), so every parity below names the right phase.
+        for (;;) {
+            uint32_t cl = 0;
+            if (lane == 0) cl = atomicAdd(claim, 1u);
+            cl = __shfl_sync(0xFFFFFFFFu, cl, 0);
+            if (cl >= my_chunks) break;
+            const uint32_t i = cl / kChunksPerTile;
+            const uint32_t chunk = cl % kChunksPerTile;
+            const uint32_t s = i % kStages;
+            const uint32_t count = tile_count(tile_first(i));
+            const Stage st = stage_at(stages, s);
+            mbar_wait(full + s, (i / kStages) & 1u);
+            const uint32_t k = chunk * 32 + lane;
+            const bool ok = k < count;
+            uint32_t src = 0, dst = 0, pkts = 0;
+            it = FwdItem{0, 0, 0};
+            if (ok) {
+                src = st.src[k];
+                dst = st.dst[k];
+                pkts = st.pkts[k];
+                it.oct = st.oct[k];
+                it.dur = st.end[k] - st.start[k];
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + s);
+            const bool f = classify<kSmem>(ok, src, dst, pkts, it.oct, it.dur, p, gt, t, it.packed);
+            push<kHot>(f, it, q, qn, lane, p, P, h);
+        }
+        // The n % 4 tail records: block 0, warp 1, direct loads.
+        if (blockIdx.x == 0 && warp == 1) {
+            const uint64_t r = n_vec + lane;
+            const bool ok = r < c.n;
+            it = FwdItem{0, ok ? c.octets[r] : 0u, ok ? c.end[r] - c.start[r] : 0ull};
+            const bool f = classify<kSmem>(ok, ok ? c.src[r] : 0u, ok ? c.dst[r] : 0u,
+                                           ok ? c.pkts[r] : 0u, it.oct, it.dur, p, gt, t, it.packed);
+            push<kHot>(f, it, q, qn, lane, p, P, h);
+        }
+        __syncwarp();
+        if (lane < qn) accumulate<kHot>(q[lane], p, P, h);
     }
-    // The n % 4 tail records: block 0, warp 0, direct loads.
-    if (blockIdx.x == 0 && warp == 0) {
-        const uint64_t r = n_vec + lane;
-        const bool ok = r < c.n;
-        it = FwdItem{0, ok ? c.octets[r] : 0u, ok ? c.end[r] - c.start[r] : 0ull};
-        const bool f = classify<kSmem>(ok, ok ? c.src[r] : 0u, ok ? c.dst[r] : 0u,
-                                       ok ? c.pkts[r] : 0u, it.oct, it.dur, p, gt, t, it.packed);
-        push<kHot>(f, it, q, qn, lane, p, P, h);
-    }
-    __syncwarp();
-    if (lane < qn) accumulate<kHot>(q[lane], p, P, h);
     flush_tallies(t, P.sums + static_cast<size_t>(P.n_sites) * 4);
     if constexpr (kHot) {
         __syncthreads();
@@ -961,18 +962,14 @@ LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool ho
     const uint64_t n_tiles = ((b.n & ~3ull) + kTile - 1) / kTile;
     c.stages = 0;
     if (soa_aligned(b) && n_tiles > 0) {
-        // TMA-staged variant: one 1024-thread CTA per SM, >= 2 stages in flight.
+        // TMA-staged variant: one 1024-thread CTA per SM, kStages tiles in flight.
         const size_t fixed = (hot ? kHotBytes : 0) + (kTmaBlock / 32) * kQueue * sizeof(FwdItem) +
-                             kMaxStages * 16;
-        const bool tsm = tbytes + fixed + 2 * kStageBytes <= kSmemMax;
-        const size_t base = fixed + (tsm ? tbytes : 0);
-        const uint32_t stages =
-            base < kSmemMax ? static_cast<uint32_t>(std::min<size_t>(kMaxStages, (kSmemMax - base) / kStageBytes)) : 0;
-        if (stages >= 2) {
+                             kStages * kStageBytes + 2 * kStages * 8 + 16;
+        if (fixed <= kSmemMax) {
             c.block = kTmaBlock;
-            c.table_in_smem = tsm;
-            c.smem = base + static_cast<size_t>(stages) * kStageBytes;
-            c.stages = stages;
+            c.table_in_smem = tbytes + fixed <= kSmemMax;
+            c.smem = fixed + (c.table_in_smem ? tbytes : 0);
+            c.stages = kStages;
             c.grid = static_cast<int>(std::min<uint64_t>(sm_count(device), n_tiles));
             return c;
         }
@@ -1047,11 +1044,11 @@ cudaError_t launch_k2(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t
     if (cfg.stages) {
         const bool hh = hot.n_slots > 0;
         if (cfg.table_in_smem) {
-            if (hh) k2_tma<true, true><<<cfg.grid, cfg.block, cfg.smem, s>>>(b.soa, t.words, t.n_words, p, P, hot, cfg.stages);
-            else k2_tma<true, false><<<cfg.grid, cfg.block, cfg.smem, s>>>(b.soa, t.words, t.n_words, p, P, hot, cfg.stages);
+            if (hh) k2_tma<true, true><<<cfg.grid, cfg.block, cfg.smem, s>>>(b.soa, t.words, t.n_words, p, P, hot);
+            else k2_tma<true, false><<<cfg.grid, cfg.block, cfg.smem, s>>>(b.soa, t.words, t.n_words, p, P, hot);
         } else {
-            if (hh) k2_tma<false, true><<<cfg.grid, cfg.block, cfg.smem, s>>>(b.soa, t.words, t.n_words, p, P, hot, cfg.stages);
-            else k2_tma<false, false><<<cfg.grid, cfg.block, cfg.smem, s>>>(b.soa, t.words, t.n_words, p, P, hot, cfg.stages);
+            if (hh) k2_tma<false, true><<<cfg.grid, cfg.block, cfg.smem, s>>>(b.soa, t.words, t.n_words, p, P, hot);
+            else k2_tma<false, false><<<cfg.grid, cfg.block, cfg.smem, s>>>(b.soa, t.words, t.n_words, p, P, hot);
         }
         return cudaGetLastError();
     }
