@@ -53,6 +53,7 @@ def parse_args():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--cpu-sample", type=int, default=2_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--hot-mode", default="auto", choices=["auto", "off", "force"])
     return ap.parse_args()
 
 
@@ -262,6 +263,7 @@ def main():
 
     eng = Engine(local)
     eng.enable_timing(True)
+    eng.set_hot_mode(args.hot_mode)
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=f"cuda:{local}")
 
     def step(batch):

@@ -80,7 +80,16 @@ struct gnm_ctx {
     size_t table_cap_words = 0;
     gnm::DevTable table{};
     int hot_mode = GNM_HOT_AUTO;
-    uint32_t cold_red = 0; // GNM_COLD_MINMAX=red: unconditional cold-site min/max RED
+    // Tuning knobs (environment, read at context creation; results are
+    // identical for every setting):
+    //   GNM_COLD_MINMAX=check  cold-site min/max: L2 read then RED only if it
+    //                          can win (default: unconditional RED)
+    //   GNM_K2_VARIANT=tma     TMA-staged K2 (default: software-pipelined
+    //                          direct loads, measured faster; profiles/)
+    //   GNM_LOOKUP=chain       src-then-dst probes (default: dual probe)
+    uint32_t cold_red = 1;
+    bool allow_tma = false;
+    uint32_t lookup_mode = 0;
 
     // partials
     gnm::DevPartials P{};
@@ -150,6 +159,7 @@ gnm::DevParams dev_params(const gnm_ctx* c, const gnm_filter_params* p) {
     q.min_duration_ms = p->min_duration_ms;
     q.site_mask = c->table.packed ? gnm::kPackedSiteMask : 0x7FFFFFFFu;
     q.cold_red = c->cold_red;
+    q.lookup_mode = c->lookup_mode;
     return q;
 }
 
@@ -282,7 +292,7 @@ void launch_k2_timed(gnm_ctx* c, const gnm::DevBatch& b, const gnm::DevParams& p
         ck(cudaEventRecord(pe.a, c->stream), "cudaEventRecord");
     }
     // K1: hot-site plan for this batch (skipped when no site can be hot).
-    const gnm::LaunchCfg cold = gnm::k2_config(c->device, b, c->table.n_words, false, c->occ);
+    const gnm::LaunchCfg cold = gnm::k2_config(c->device, b, c->table.n_words, false, c->occ, c->allow_tma);
     bool hot = false;
     if (c->hot_mode != GNM_HOT_OFF) {
         cudaError_t e;
@@ -290,7 +300,7 @@ void launch_k2_timed(gnm_ctx* c, const gnm::DevBatch& b, const gnm::DevParams& p
                             c->hot_mode == GNM_HOT_FORCE, c->stream, &c->kernel_launches, &e);
         ck(e, "hot-site plan");
     }
-    const gnm::LaunchCfg cfg = hot ? gnm::k2_config(c->device, b, c->table.n_words, true, c->occ) : cold;
+    const gnm::LaunchCfg cfg = hot ? gnm::k2_config(c->device, b, c->table.n_words, true, c->occ, c->allow_tma) : cold;
     gnm::DevHot h{c->d_scratch + 2 * static_cast<size_t>(c->P.n_sites), hot ? gnm::kHotSlots : 0u};
     if (c->timing) {
         ck(cudaEventRecord(pe.b, c->stream), "cudaEventRecord");
@@ -599,7 +609,11 @@ int gnm_ctx_create(int device, gnm_ctx** out) {
             ck(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
             c->stream = c->own_stream;
             const char* cm = std::getenv("GNM_COLD_MINMAX");
-            c->cold_red = cm && std::strcmp(cm, "red") == 0;
+            c->cold_red = !(cm && std::strcmp(cm, "check") == 0);
+            const char* kv = std::getenv("GNM_K2_VARIANT");
+            c->allow_tma = kv && std::strcmp(kv, "tma") == 0;
+            const char* lk = std::getenv("GNM_LOOKUP");
+            c->lookup_mode = lk && std::strcmp(lk, "chain") == 0;
             for (int i = 0; i < 2; ++i) {
                 ck(cudaEventCreateWithFlags(&c->ev_h2d[i], cudaEventDisableTiming), "cudaEventCreate");
                 ck(cudaEventCreateWithFlags(&c->ev_k2[i], cudaEventDisableTiming), "cudaEventCreate");

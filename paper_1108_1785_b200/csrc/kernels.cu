@@ -50,6 +50,13 @@ __device__ __forceinline__ uint4 ld_stream_u4(const void* p) {
                  : "l"(p));
     return r;
 }
+__device__ __forceinline__ uint2 ld_stream_u2(const void* p) {
+    uint2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v2.u32 {%0,%1}, [%2];"
+                 : "=r"(r.x), "=r"(r.y)
+                 : "l"(p));
+    return r;
+}
 __device__ __forceinline__ ulonglong2 ld_stream_u64x2(const void* p) {
     ulonglong2 r;
     asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v2.u64 {%0,%1}, [%2];"
@@ -60,16 +67,16 @@ __device__ __forceinline__ ulonglong2 ld_stream_u64x2(const void* p) {
 
 // ---- fire-and-forget global reductions (RED, never a returning ATOM) -------
 __device__ __forceinline__ void red_add(unsigned long long* p, unsigned long long v) {
-    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v));
 }
 __device__ __forceinline__ void red_add(unsigned int* p, unsigned int v) {
-    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v));
 }
 __device__ __forceinline__ void red_min(unsigned long long* p, unsigned long long v) {
-    asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v));
 }
 __device__ __forceinline__ void red_max(unsigned long long* p, unsigned long long v) {
-    asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(p), "l"(v));
 }
 
 // ---- registry table (layout in registry.hpp, DeviceTable) -----------------
@@ -307,7 +314,13 @@ __device__ __forceinline__ bool classify(bool valid, uint32_t src, uint32_t dst,
         ++t.admin;
         return false;
     }
-    const uint32_t v = lookup2<kSmem>(gt, src, dst);
+    uint32_t v;
+    if (p.lookup_mode) {
+        v = lookup<kSmem>(gt, src);
+        if (v == kNone) v = lookup<kSmem>(gt, dst);
+    } else {
+        v = lookup2<kSmem>(gt, src, dst);
+    }
     if (v == kNone) {
         ++t.unm;
         return false;
@@ -393,23 +406,33 @@ __global__ void __launch_bounds__(kK2Block, 2) k2(DevBatch b, const uint32_t* __
     const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
     FwdItem it;
     if constexpr (kLayout == 0) {
+        // Two records per lane per 64-record warp tile, software-pipelined:
+        // the next tile's six loads are in flight while this one is
+        // classified, so the load latency is not exposed at first use.
         const DevSoA& c = b.soa;
-        const uint64_t n4 = c.n / 4;
-        for (uint64_t base = warp_gid * 32; base < n4; base += nwarps * 32) {
-            const uint64_t g = base + lane;
-            const bool ok = g < n4;
-            uint4 s{}, d{}, k{}, o{};
-            ulonglong2 t0{}, t1{}, e0{}, e1{};
-            if (ok) {
-                s = ld_stream_u4(c.src + 4 * g);
-                d = ld_stream_u4(c.dst + 4 * g);
-                k = ld_stream_u4(c.pkts + 4 * g);
-                o = ld_stream_u4(c.octets + 4 * g);
-                t0 = ld_stream_u64x2(c.start + 4 * g);
-                t1 = ld_stream_u64x2(c.start + 4 * g + 2);
-                e0 = ld_stream_u64x2(c.end + 4 * g);
-                e1 = ld_stream_u64x2(c.end + 4 * g + 2);
+        const uint64_t n2 = c.n / 2;
+        const uint64_t step = nwarps * 32;
+        uint64_t base = warp_gid * 32;
+        uint2 s{}, d{}, k{}, o{};
+        ulonglong2 t0{}, e0{};
+        auto fetch = [&](uint64_t bs, uint2& fs, uint2& fd, uint2& fk, uint2& fo, ulonglong2& ft,
+                         ulonglong2& fe) {
+            const uint64_t g = bs + lane;
+            if (bs < n2 && g < n2) {
+                fs = ld_stream_u2(c.src + 2 * g);
+                fd = ld_stream_u2(c.dst + 2 * g);
+                fk = ld_stream_u2(c.pkts + 2 * g);
+                fo = ld_stream_u2(c.octets + 2 * g);
+                ft = ld_stream_u64x2(c.start + 2 * g);
+                fe = ld_stream_u64x2(c.end + 2 * g);
             }
+        };
+        fetch(base, s, d, k, o, t0, e0);
+        for (; base < n2; base += step) {
+            const bool ok = base + lane < n2;
+            uint2 ns{}, nd{}, nk{}, no{};
+            ulonglong2 nt{}, ne{};
+            fetch(base + step, ns, nd, nk, no, nt, ne);
             bool f;
             it = FwdItem{0, o.x, e0.x - t0.x};
             f = classify<kSmem>(ok, s.x, d.x, k.x, o.x, it.dur, p, gt, t, it.packed);
@@ -417,16 +440,11 @@ __global__ void __launch_bounds__(kK2Block, 2) k2(DevBatch b, const uint32_t* __
             it = FwdItem{0, o.y, e0.y - t0.y};
             f = classify<kSmem>(ok, s.y, d.y, k.y, o.y, it.dur, p, gt, t, it.packed);
             push<kHot>(f, it, q, qn, lane, p, P, h);
-            it = FwdItem{0, o.z, e1.x - t1.x};
-            f = classify<kSmem>(ok, s.z, d.z, k.z, o.z, it.dur, p, gt, t, it.packed);
-            push<kHot>(f, it, q, qn, lane, p, P, h);
-            it = FwdItem{0, o.w, e1.y - t1.y};
-            f = classify<kSmem>(ok, s.w, d.w, k.w, o.w, it.dur, p, gt, t, it.packed);
-            push<kHot>(f, it, q, qn, lane, p, P, h);
+            s = ns, d = nd, k = nk, o = no, t0 = nt, e0 = ne;
         }
-        // The n % 4 tail records: the first warp of the grid.
+        // The odd tail record: the first warp of the grid.
         if (warp_gid == 0) {
-            const uint64_t i = n4 * 4 + lane;
+            const uint64_t i = n2 * 2 + lane;
             const bool ok = i < c.n;
             it = FwdItem{0, ok ? c.octets[i] : 0u, ok ? c.end[i] - c.start[i] : 0ull};
             const bool f = classify<kSmem>(ok, ok ? c.src[i] : 0u, ok ? c.dst[i] : 0u,
@@ -956,12 +974,13 @@ bool soa_aligned(const DevBatch& b) {
 }
 } // namespace
 
-LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool hot, int* occ_cache) {
+LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool hot, int* occ_cache,
+                    bool allow_tma) {
     LaunchCfg c;
     const size_t tbytes = table_smem_bytes(table_words);
     const uint64_t n_tiles = ((b.n & ~3ull) + kTile - 1) / kTile;
     c.stages = 0;
-    if (soa_aligned(b) && n_tiles > 0) {
+    if (allow_tma && soa_aligned(b) && n_tiles > 0) {
         // TMA-staged variant: one 1024-thread CTA per SM, kStages tiles in flight.
         const size_t fixed = (hot ? kHotBytes : 0) + (kTmaBlock / 32) * kQueue * sizeof(FwdItem) +
                              kStages * kStageBytes + 2 * kStages * 8 + 16;

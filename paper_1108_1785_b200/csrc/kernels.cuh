@@ -20,6 +20,7 @@ struct DevParams {
     uint32_t min_duration_ms;
     uint32_t site_mask;       // kPackedSiteMask, or 0x7FFFFFFF for wide tables
     uint32_t cold_red;        // 1: cold-site min/max as unconditional RED (no L2 read)
+    uint32_t lookup_mode;     // 0: branch-free dual probe, 1: src-then-dst probes
 };
 
 // Device partial accumulators of one context (layout in gnetmon.h, gnm_partials).
@@ -76,7 +77,8 @@ cudaError_t init_kernel_attributes();
 
 // Occupancy-derived launch configuration for K2 over n records.
 // occ_cache[hot] memoises blocks/SM (0 = unknown) for this table size.
-LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool hot, int* occ_cache);
+LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool hot, int* occ_cache,
+                    bool allow_tma = true);
 
 // K1 (optional, skewed batches): sample the batch, pick the hot sites and
 // write their slots into the table words. Returns false when the batch is
