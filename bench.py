@@ -242,6 +242,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_1108_1785_b200 import Engine, FlowBatch, SiteCatalog, synth
+    from paper_1108_1785_b200 import distributed as D
 
     world, rank, local = dist_env()
     if world > 1:
@@ -269,13 +270,12 @@ def main():
     def step(batch):
         if world == 1:
             return eng.aggregate(batch, cat)
+        # K2 on this rank's shard, one NCCL all-reduce of the per-site
+        # partials over NVLink (paper_1108_1785_b200.distributed), K3.
         eng.accumulate(batch, cat)
         t = eng.device_tensors(cat)
         with torch.cuda.stream(stream):
-            dist.all_reduce(t["sums"], op=dist.ReduceOp.SUM)
-            dist.all_reduce(t["min_bps"], op=dist.ReduceOp.MIN)
-            dist.all_reduce(t["max_bps"], op=dist.ReduceOp.MAX)
-            dist.all_reduce(t["hist"], op=dist.ReduceOp.SUM)
+            D.allreduce_partials(t)
         return eng.finalize(cat)
 
     def barrier():

@@ -1,0 +1,54 @@
+"""Loading helpers for the golden fixtures (tests/golden/, made by
+tests/golden/make_golden.py from the unmodified reference)."""
+import os
+
+import numpy as np
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+ANALYSIS_SETS = ["engine_stress", "edge", "tiny_duration", "d1_small", "d2_small", "d3_small"]
+
+
+def load(name):
+    return np.load(os.path.join(GOLDEN, f"{name}.npz"))
+
+
+def sites(z):
+    return [s.split("|") for s in z["sites"].tolist()]
+
+
+def cols(z):
+    return tuple(np.ascontiguousarray(z[k]) for k in ("src", "dst", "pkts", "octets", "start", "end"))
+
+
+def params(z):
+    return tuple(int(x) for x in z["params"])
+
+
+def dense_hist(z):
+    n = len(z["count"])
+    h = np.zeros((n, 10001), np.uint32)
+    h[z["hist_site"], z["hist_bucket"]] = z["hist_count"]
+    return h
+
+
+def expected(z):
+    """The reference's result in the oracle dict layout (Oracle.finalize)."""
+    st = z["stats"]
+    return {"count": z["count"], "octets": z["octet_sum"], "ubps_lo": z["ubps_lo"],
+            "ubps_hi": z["ubps_hi"], "min": st[:, 0], "max": st[:, 1], "avg": st[:, 2],
+            "median": st[:, 3], "hist": dense_hist(z), "tallies": z["tallies"]}
+
+
+def assert_acc_equal(got, want, check_hist=True):
+    """Bit-exact comparison of two result dicts (oracle layout)."""
+    pres = want["count"] > 0
+    np.testing.assert_array_equal(got["count"], want["count"])
+    np.testing.assert_array_equal(got["octets"], want["octets"])
+    np.testing.assert_array_equal(got["ubps_lo"], want["ubps_lo"])
+    np.testing.assert_array_equal(got["ubps_hi"], want["ubps_hi"])
+    for k in ("min", "max", "avg", "median"):
+        np.testing.assert_array_equal(np.asarray(got[k])[pres].view(np.uint64),
+                                      np.asarray(want[k])[pres].view(np.uint64), err_msg=k)
+    np.testing.assert_array_equal(np.asarray(got["tallies"], np.uint64), want["tallies"])
+    if check_hist:
+        np.testing.assert_array_equal(got["hist"], want["hist"])
