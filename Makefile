@@ -15,7 +15,7 @@ PKG := paper_1108_1785_b200
 SRCS := $(PKG)/csrc/capi.cu $(PKG)/csrc/kernels.cu $(PKG)/csrc/registry.cpp
 HDRS := include/gnetmon.h $(PKG)/csrc/kernels.cuh $(PKG)/csrc/registry.hpp
 
-.PHONY: all ref clean oracle
+.PHONY: all ref clean oracle ablation
 all: $(PKG)/lib/libgnetmon.so $(PKG)/lib/libgnm_synth.so oracle
 
 $(PKG)/lib/libgnetmon.so: $(SRCS) $(HDRS)
@@ -25,6 +25,13 @@ $(PKG)/lib/libgnetmon.so: $(SRCS) $(HDRS)
 $(PKG)/lib/libgnm_synth.so: $(PKG)/csrc/synth.c
 	@mkdir -p $(PKG)/lib
 	gcc -std=c11 -O2 -fPIC -shared -fopenmp -Wall -Wextra -o $@ $< -lm
+
+# Measurement build with the K2 ablation switches (tools/ablation.sh); never
+# loaded by the product or the tests.
+ablation: $(PKG)/lib/ablation/libgnetmon.so
+$(PKG)/lib/ablation/libgnetmon.so: $(SRCS) $(HDRS)
+	@mkdir -p $(PKG)/lib/ablation
+	$(NVCC) $(NVFLAGS) -DGNM_K2_ABLATION -shared -o $@ $(SRCS) 2> /dev/null
 
 oracle:
 	$(MAKE) -C oracle all

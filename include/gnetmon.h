@@ -211,7 +211,9 @@ int gnm_reset(gnm_ctx* ctx);
  *          limb1, limb2 (32-bit limbs); then tallies fwd, ack, admin, unmatched)
  *   min:   float64 [n_sites]       reduce MIN  (+inf when empty)
  *   max:   float64 [n_sites]       reduce MAX  (0 when empty)
- *   hist:  uint32 [n_sites*10001]  reduce SUM */
+ *   hist:  uint32 [n_sites*10008]  reduce SUM; sector-blocked bucket-major:
+ *          count(site, b) = hist[((b >> 3) * n_sites + site) * 8 + (b & 7)]
+ *          (gnm_finalize exports the dense [site][10001] order) */
 typedef struct gnm_partials {
     uint64_t* sums;
     double* min_bps;

@@ -13,7 +13,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(_HERE, "lib")
-LIB_PATH = os.path.join(LIB_DIR, "libgnetmon.so")
+# GNM_LIB: measurement builds only (tools/ablation.sh); the product and the
+# tests load the in-tree library.
+LIB_PATH = os.environ.get("GNM_LIB") or os.path.join(LIB_DIR, "libgnetmon.so")
 SYNTH_PATH = os.path.join(LIB_DIR, "libgnm_synth.so")
 
 BUCKET_COUNT = 10001

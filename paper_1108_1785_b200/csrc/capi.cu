@@ -80,16 +80,11 @@ struct gnm_ctx {
     size_t table_cap_words = 0;
     gnm::DevTable table{};
     int hot_mode = GNM_HOT_AUTO;
-    // Tuning knobs (environment, read at context creation; results are
-    // identical for every setting):
-    //   GNM_COLD_MINMAX=check  cold-site min/max: L2 read then RED only if it
-    //                          can win (default: unconditional RED)
-    //   GNM_K2_VARIANT=tma     TMA-staged K2 (default: software-pipelined
-    //                          direct loads, measured faster; profiles/)
-    //   GNM_LOOKUP=chain       src-then-dst probes (default: dual probe)
-    uint32_t cold_red = 1;
-    bool allow_tma = false;
-    uint32_t lookup_mode = 0;
+    // K2 variant for aligned SoA batches (environment GNM_K2_VARIANT, read at
+    // context creation; results are identical): "reg" double-buffers the
+    // next tile in registers, "l2" asks the TMA engine to prefetch tiles
+    // into L2 (cp.async.bulk.prefetch) and loads the current one directly.
+    int k2_variant = 0;
 
     // partials
     gnm::DevPartials P{};
@@ -158,8 +153,12 @@ gnm::DevParams dev_params(const gnm_ctx* c, const gnm_filter_params* p) {
     q.min_packets = p->min_packets;
     q.min_duration_ms = p->min_duration_ms;
     q.site_mask = c->table.packed ? gnm::kPackedSiteMask : 0x7FFFFFFFu;
-    q.cold_red = c->cold_red;
-    q.lookup_mode = c->lookup_mode;
+    q.min_packets1 = std::max<uint32_t>(p->min_packets, 1);
+    q.min_duration1 = std::max<uint32_t>(p->min_duration_ms, 1);
+    q.ablation = 0;
+#ifdef GNM_K2_ABLATION
+    if (const char* a = std::getenv("GNM_K2_ABLATION")) q.ablation = static_cast<uint32_t>(std::atoi(a));
+#endif
     return q;
 }
 
@@ -206,7 +205,7 @@ void ensure_partials(gnm_ctx* c, uint32_t n_sites) {
         ck(cudaMalloc(&c->P.sums, (static_cast<size_t>(cap) * 4 + 4) * 8), "cudaMalloc(sums)");
         ck(cudaMalloc(&c->P.mn, static_cast<size_t>(cap) * 8), "cudaMalloc(min)");
         ck(cudaMalloc(&c->P.mx, static_cast<size_t>(cap) * 8), "cudaMalloc(max)");
-        ck(cudaMalloc(&c->P.hist, static_cast<size_t>(cap) * gnm::kBuckets * 4), "cudaMalloc(hist)");
+        ck(cudaMalloc(&c->P.hist, static_cast<size_t>(cap) * gnm::kHistStride * 4), "cudaMalloc(hist)");
         const size_t scratch_words = 2 * static_cast<size_t>(cap) + gnm::kHotStride + 1;
         ck(cudaMalloc(&c->d_scratch, scratch_words * 4), "cudaMalloc(scratch)");
         ck(cudaMemsetAsync(c->d_scratch, 0, scratch_words * 4, c->stream), "cudaMemsetAsync");
@@ -292,7 +291,7 @@ void launch_k2_timed(gnm_ctx* c, const gnm::DevBatch& b, const gnm::DevParams& p
         ck(cudaEventRecord(pe.a, c->stream), "cudaEventRecord");
     }
     // K1: hot-site plan for this batch (skipped when no site can be hot).
-    const gnm::LaunchCfg cold = gnm::k2_config(c->device, b, c->table.n_words, false, c->occ, c->allow_tma);
+    const gnm::LaunchCfg cold = gnm::k2_config(c->device, b, c->table.n_words, false, c->occ, c->k2_variant);
     bool hot = false;
     if (c->hot_mode != GNM_HOT_OFF) {
         cudaError_t e;
@@ -300,7 +299,7 @@ void launch_k2_timed(gnm_ctx* c, const gnm::DevBatch& b, const gnm::DevParams& p
                             c->hot_mode == GNM_HOT_FORCE, c->stream, &c->kernel_launches, &e);
         ck(e, "hot-site plan");
     }
-    const gnm::LaunchCfg cfg = hot ? gnm::k2_config(c->device, b, c->table.n_words, true, c->occ, c->allow_tma) : cold;
+    const gnm::LaunchCfg cfg = hot ? gnm::k2_config(c->device, b, c->table.n_words, true, c->occ, c->k2_variant) : cold;
     gnm::DevHot h{c->d_scratch + 2 * static_cast<size_t>(c->P.n_sites), hot ? gnm::kHotSlots : 0u};
     if (c->timing) {
         ck(cudaEventRecord(pe.b, c->stream), "cudaEventRecord");
@@ -468,9 +467,15 @@ int finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* r) {
                        cudaMemcpyDeviceToHost, c->stream),
        "cudaMemcpyAsync(D2H)");
     if (export_hist) {
-        ck(cudaMemcpyAsync(r->histograms, c->P.hist, static_cast<size_t>(n_sites) * gnm::kBuckets * 4,
-                           cudaMemcpyDeviceToHost, c->stream),
+        const size_t bytes = static_cast<size_t>(n_sites) * gnm::kBuckets * 4;
+        uint32_t* dense = nullptr;
+        ck(cudaMallocAsync(reinterpret_cast<void**>(&dense), std::max<size_t>(bytes, 4), c->stream),
+           "cudaMallocAsync(hist export)");
+        ck(gnm::launch_hist_export(c->P, dense, c->stream), "hist export");
+        c->kernel_launches += 1;
+        ck(cudaMemcpyAsync(r->histograms, dense, bytes, cudaMemcpyDeviceToHost, c->stream),
            "cudaMemcpyAsync(D2H hist)");
+        ck(cudaFreeAsync(dense, c->stream), "cudaFreeAsync(hist export)");
         ck(gnm::launch_reset(c->device, c->P, c->stream), "reset launch");
         c->kernel_launches += 1;
     }
@@ -608,12 +613,12 @@ int gnm_ctx_create(int device, gnm_ctx** out) {
             ck(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
             ck(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
             c->stream = c->own_stream;
-            const char* cm = std::getenv("GNM_COLD_MINMAX");
-            c->cold_red = !(cm && std::strcmp(cm, "check") == 0);
             const char* kv = std::getenv("GNM_K2_VARIANT");
-            c->allow_tma = kv && std::strcmp(kv, "tma") == 0;
-            const char* lk = std::getenv("GNM_LOOKUP");
-            c->lookup_mode = lk && std::strcmp(lk, "chain") == 0;
+            c->k2_variant = !kv                             ? 0
+                            : std::strcmp(kv, "l2") == 0    ? 1
+                            : std::strcmp(kv, "tma") == 0   ? 2
+                            : std::strcmp(kv, "async") == 0 ? 3
+                                                            : 0;
             for (int i = 0; i < 2; ++i) {
                 ck(cudaEventCreateWithFlags(&c->ev_h2d[i], cudaEventDisableTiming), "cudaEventCreate");
                 ck(cudaEventCreateWithFlags(&c->ev_k2[i], cudaEventDisableTiming), "cudaEventCreate");
@@ -764,7 +769,7 @@ int gnm_get_partials(gnm_ctx* c, const gnm_registry* reg, gnm_partials* out) {
         out->hist = c->P.hist;
         out->n_sites = c->P.n_sites;
         out->sums_count = static_cast<uint64_t>(c->P.n_sites) * 4 + 4;
-        out->hist_count = static_cast<uint64_t>(c->P.n_sites) * gnm::kBuckets;
+        out->hist_count = static_cast<uint64_t>(c->P.n_sites) * gnm::kHistStride;
         return static_cast<int>(GNM_OK);
     });
 }

@@ -1,8 +1,8 @@
 // kernels.cu — sm_100a kernels of the flow-analysis hot path.
 //
-//   K1  k_sample, k_hot_assign, k_table_slots
+//   K1  k_sample, k_hot_select, k_table_slots
 //                         hot-site plan for skewed batches (see plan_hot)
-//   K2  k2                classify -> attribute -> rate -> per-site aggregate
+//   K2  k2_soa / k2_gen   classify -> attribute -> rate -> per-site aggregate
 //                         (reduce_slice, rate_engine.cpp:197-240 + add :9-23)
 //   K3  k3_finalize       per-site count / median / clamp / flag
 //                         (finalize + stats_from + median_bps,
@@ -12,18 +12,26 @@
 // Paths are relative to /root/reference/proj/core/src.
 //
 // The path is HBM-bound integer work: 32 algorithmic bytes per
-// record, no tensor cores. K2 streams the six SoA columns with 128-bit
-// non-allocating loads (4 records per thread per iteration), probes a
-// shared-memory-resident radix table (registry.hpp), and reduces into
-// order-independent integer/min/max accumulators, so the result is
-// bit-identical to the reference for any grid, partitioning or GPU count.
+// record, no tensor cores. K2 streams the six SoA columns with vector
+// non-allocating loads, probes a shared-memory-resident radix table
+// (registry.hpp), and reduces into order-independent integer/min/max
+// accumulators, so the result is bit-identical to the reference for any
+// grid, partitioning or GPU count.
+//
+// K2 is two stages per warp. Stage A (every lane, every record): the class
+// filter and the /16 directory bits of both endpoints. Candidates (~50% of
+// records at D3) are compacted into a per-warp shared-memory queue, and
+// stage B drains it 32 at a time with full warps: the /24 lookup tail, the
+// rate, the exact micro-bps, the bucket and the reductions.
 //
 // Contention: with Zipf-distributed sites the hottest site receives ~10% of
-// all Forward flows, and same-address L2 atomics serialise (~1 ns each). The
-// scalar sums of the hot sites (chosen per call by K1 from a 1/64 sample) are
-// therefore accumulated in block-private shared memory with native 32-bit
-// atomics and explicit carry propagation, and flushed once per CTA; cold
-// sites and every histogram bucket go straight to L2 with RED.
+// all Forward flows; same-address L2 atomics serialise (~1 ns each) and
+// returning shared-memory atomics expose their (contended) latency to the
+// warp. The scalar sums of the hot sites (the top 512 of a 1/64 sample, K1)
+// therefore accumulate in block-private shared memory through NON-returning
+// 32-bit adds of 16-bit limbs; a CTA processes < 2^16 records, so no limb
+// can overflow before the CTA's single flush. Cold sites and every histogram
+// bucket go straight to L2 with RED.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -34,38 +42,46 @@ namespace gnm {
 namespace {
 
 constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr uint32_t kDirWordsDev = 4096u; // registry.hpp kDirWords
 constexpr int kK2Block = 512;
+constexpr uint32_t kWarps = kK2Block / 32;
+// Records one K2 CTA may process: every 16-bit limb of a hot slot then
+// sums fewer than 2^16 values below 2^16 and cannot wrap its u32.
+constexpr uint64_t kCtaRecords = 65536 - 64;
+constexpr uint32_t kCtaTiles = static_cast<uint32_t>(kCtaRecords / 64) - 1; // + a < 64-record tail
+constexpr uint32_t kQueue = 96; // per-warp queue capacity: < 32 left + 2 x 32 pushed
 constexpr size_t kHotBytes = kHotStride * (5 * 4 + 2 * 8);
 constexpr size_t kSmemMax = 227 * 1024;
-constexpr size_t kQueueBytes = (kK2Block / 32) * 64 * 16; // per-warp FwdItem queues
+constexpr size_t kQueueBytes = kWarps * kQueue * 16;
 constexpr size_t kSmemTableMax = kSmemMax - kHotBytes - kQueueBytes - 1024;
 
 extern __shared__ __align__(16) uint32_t g_smem[];
 
 // ---- streaming loads (read once: do not pollute L1) ----------------------
-__device__ __forceinline__ uint4 ld_stream_u4(const void* p) {
-    uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
+// The input is read once: stream it through L2 with an evict-first policy so
+// it does not push out the histogram and accumulator lines the reductions
+// hit (profiles/round1: RED throughput collapses once they miss L2).
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
 }
 __device__ __forceinline__ uint2 ld_stream_u2(const void* p) {
     uint2 r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v2.u32 {%0,%1}, [%2];"
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::256B.v2.u32 {%0,%1}, [%2], %3;"
                  : "=r"(r.x), "=r"(r.y)
-                 : "l"(p));
+                 : "l"(p), "l"(evict_first_policy()));
     return r;
 }
 __device__ __forceinline__ ulonglong2 ld_stream_u64x2(const void* p) {
     ulonglong2 r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v2.u64 {%0,%1}, [%2];"
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::256B.v2.u64 {%0,%1}, [%2], %3;"
                  : "=l"(r.x), "=l"(r.y)
-                 : "l"(p));
+                 : "l"(p), "l"(evict_first_policy()));
     return r;
 }
 
-// ---- fire-and-forget global reductions (RED, never a returning ATOM) -------
+// ---- fire-and-forget reductions (RED, never a returning ATOM) --------------
 __device__ __forceinline__ void red_add(unsigned long long* p, unsigned long long v) {
     asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v));
 }
@@ -77,6 +93,11 @@ __device__ __forceinline__ void red_min(unsigned long long* p, unsigned long lon
 }
 __device__ __forceinline__ void red_max(unsigned long long* p, unsigned long long v) {
     asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(p), "l"(v));
+}
+__device__ __forceinline__ void red_add_shared(uint32_t* p, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))),
+                 "r"(v)
+                 : "memory");
 }
 
 // ---- registry table (layout in registry.hpp, DeviceTable) -----------------
@@ -100,33 +121,17 @@ __device__ __forceinline__ uint32_t lookup(const uint32_t* __restrict__ gt, uint
     const uint2 w = table_pair<kSmem>(gt, d >> 5);
     const uint32_t bit = d & 31u;
     if (!((w.x >> bit) & 1u)) return kNone;
-    const uint32_t node = table_word<kSmem>(gt, 4096u + w.y + __popc(w.x & ((1u << bit) - 1u)));
+    const uint32_t node = table_word<kSmem>(gt, kDirWordsDev + w.y + __popc(w.x & ((1u << bit) - 1u)));
     if (node & 0x80000000u) return node & 0x7FFFFFFFu;
     return table_word<kSmem>(gt, node + ((ip >> 8) & 0xFFu));
 }
 
-// attribute (rate_engine.cpp:127-146) as one branch-free probe of both
-// endpoints: the two directory words, nodes and leaf words are loaded with
-// predicated selects (a uniform node reads word 0 as a dummy leaf), and the
-// src value wins when both hit. Avoids the divergent src-then-dst chain.
+// attribute (rate_engine.cpp:127-146) with full src-then-dst probes.
 template <bool kSmem>
-__device__ __forceinline__ uint32_t lookup2(const uint32_t* __restrict__ gt, uint32_t src,
-                                            uint32_t dst) {
-    const uint32_t ds = src >> 16, dd = dst >> 16;
-    const uint2 ws = table_pair<kSmem>(gt, ds >> 5);
-    const uint2 wd = table_pair<kSmem>(gt, dd >> 5);
-    const uint32_t bs = ds & 31u, bd = dd & 31u;
-    const bool hs = (ws.x >> bs) & 1u, hd = (wd.x >> bd) & 1u;
-    const uint32_t ns =
-        hs ? table_word<kSmem>(gt, 4096u + ws.y + __popc(ws.x & ((1u << bs) - 1u))) : 0x80000000u | kNone;
-    const uint32_t nd =
-        hd ? table_word<kSmem>(gt, 4096u + wd.y + __popc(wd.x & ((1u << bd) - 1u))) : 0x80000000u | kNone;
-    const bool us = ns & 0x80000000u, ud = nd & 0x80000000u;
-    const uint32_t ls = table_word<kSmem>(gt, us ? 0u : ns + ((src >> 8) & 0xFFu));
-    const uint32_t ld = table_word<kSmem>(gt, ud ? 0u : nd + ((dst >> 8) & 0xFFu));
-    const uint32_t vs = us ? (hs ? (ns & 0x7FFFFFFFu) : kNone) : ls;
-    const uint32_t vd = ud ? (hd ? (nd & 0x7FFFFFFFu) : kNone) : ld;
-    return vs != kNone ? vs : vd;
+__device__ __forceinline__ uint32_t site_of_full(const uint32_t* __restrict__ gt, uint32_t src,
+                                                 uint32_t dst) {
+    const uint32_t v = lookup<kSmem>(gt, src);
+    return v != kNone ? v : lookup<kSmem>(gt, dst);
 }
 
 template <bool kSmem>
@@ -139,24 +144,19 @@ __device__ __forceinline__ void load_table(const uint32_t* __restrict__ gt, uint
 }
 
 // ---- block-private hot-site accumulators ---------------------------------
+// Per slot: octets as two 16-bit limbs, micro-bps (< 2^48) as three 16-bit
+// limbs, each summed into its own u32 by non-returning shared adds; min/max
+// as f64 bit patterns.
 struct HotSmem {
-    uint32_t* oct_lo;          // octets, 64-bit as two u32 with carry
-    uint32_t* oct_hi;
-    uint32_t* u0;              // micro-bps, 96-bit as three u32 with carries
-    uint32_t* u1;
-    uint32_t* u2;
-    unsigned long long* mn;    // f64 bits
+    uint32_t* limb; // [5][kHotStride]: oct lo16, oct hi16, ubps bits 0-15, 16-31, 32-47
+    unsigned long long* mn;
     unsigned long long* mx;
 };
 
 __device__ __forceinline__ HotSmem hot_smem(uint32_t table_words_in_smem) {
     uint32_t* base = g_smem + table_words_in_smem;
     HotSmem h;
-    h.oct_lo = base;
-    h.oct_hi = base + kHotStride;
-    h.u0 = base + 2 * kHotStride;
-    h.u1 = base + 3 * kHotStride;
-    h.u2 = base + 4 * kHotStride;
+    h.limb = base;
     h.mn = reinterpret_cast<unsigned long long*>(base + 5 * kHotStride);
     h.mx = h.mn + kHotStride;
     return h;
@@ -164,196 +164,267 @@ __device__ __forceinline__ HotSmem hot_smem(uint32_t table_words_in_smem) {
 
 __device__ __forceinline__ void hot_init(const HotSmem& h) {
     for (uint32_t i = threadIdx.x; i < kHotStride; i += blockDim.x) {
-        h.oct_lo[i] = 0;
-        h.oct_hi[i] = 0;
-        h.u0[i] = 0;
-        h.u1[i] = 0;
-        h.u2[i] = 0;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) h.limb[k * kHotStride + i] = 0;
         h.mn[i] = kMinInitBits;
         h.mx[i] = kMaxInitBits;
     }
 }
 
-// ---- per-record arithmetic -------------------------------------------------
-// bucket_index (rate_engine.cpp:119-125): IEEE division, truncation.
+// ---- per-flow arithmetic -----------------------------------------------------
+// Exact micro-bps of one flow, rate_ubps_of (rate_engine.cpp:100-107):
+// X = floor(octets * 8e9 / dur) as a 128-bit value (hi is non-zero only
+// when dur is a few ms and octets are huge).
+//
+// Fast path: the f64 rate (one IEEE division, needed for min/max anyway) is
+// within 2^-52 relative of 8000*oct/dur (2^-53 more when double(dur) rounds),
+// so y = rate * 1e6 is within 3*X*2^-53 of X; below rate 1e9 (X < 2^50)
+// that is < 0.375, and q = rint(y) satisfies |q - X| < 0.875. Hence
+// floor(X) is q or q - 1, decided by the sign of the exact residual
+// p - q*dur (|residual| < dur, so its 64-bit wrapped value is exact).
+// Everything else takes the exact integer division.
+__device__ __noinline__ uint4 ubps_slow(uint32_t oct, uint64_t dur) {
+    if (oct <= 2305843009u) {
+        const uint64_t q = static_cast<uint64_t>(oct) * 8000000000ull / dur;
+        return make_uint4(static_cast<uint32_t>(q), static_cast<uint32_t>(q >> 32), 0u, 0u);
+    }
+    const unsigned __int128 q = static_cast<unsigned __int128>(oct) * 8000000000ull / dur;
+    const uint64_t lo = static_cast<uint64_t>(q), hi = static_cast<uint64_t>(q >> 64);
+    return make_uint4(static_cast<uint32_t>(lo), static_cast<uint32_t>(lo >> 32),
+                      static_cast<uint32_t>(hi), static_cast<uint32_t>(hi >> 32));
+}
+
+__device__ __forceinline__ void ubps_of(uint32_t oct, uint64_t dur, double rate, uint64_t& lo,
+                                        uint64_t& hi) {
+    if (oct <= 2305843009u && rate < 1.0e9) {
+        const uint64_t pp = static_cast<uint64_t>(oct) * 8000000000ull;
+        const uint64_t q = __double2ull_rn(__dmul_rn(rate, 1.0e6));
+        const int64_t r = static_cast<int64_t>(pp - q * dur);
+        lo = r < 0 ? q - 1 : q;
+        hi = 0;
+        return;
+    }
+    const uint4 s = ubps_slow(oct, dur);
+    lo = static_cast<uint64_t>(s.y) << 32 | s.x;
+    hi = static_cast<uint64_t>(s.w) << 32 | s.z;
+}
+
+// bucket_index (rate_engine.cpp:119-125) from the exact quotient:
+// floor(RN(RN(8000*oct/dur)/1e4)) == floor(4*oct/(5*dur)) for every u32 oct
+// (the two roundings move the value by < v*2^-52, while a non-integer
+// 4*oct/(5*dur) is at least 1/(5*dur) away from the next integer, and
+// 4*oct < 2^52), and floor(4*oct/(5*dur)) == floor(ubps / 1e10).
+// Checked against the reference's double arithmetic on adversarial inputs
+// (tests/test_oracle_golden.py::test_integer_bucket_identity).
+__device__ __forceinline__ uint32_t bucket_of_ubps(uint64_t lo, uint64_t hi) {
+    const uint64_t b = lo / 10000000000ull;
+    return (hi || b >= 10000u) ? 10000u : static_cast<uint32_t>(b);
+}
+
+// bucket_index on a double (K3: the buckets of the min/max rates).
 __device__ __forceinline__ uint32_t bucket_of(double rate) {
     const double b = __ddiv_rn(rate, 10000.0);
     return b >= 10000.0 ? 10000u : static_cast<uint32_t>(b);
 }
 
-struct Tally {
-    uint32_t fwd = 0, ack = 0, admin = 0, unm = 0;
+// ---- per-record classification (stage A, every lane) -----------------------
+// Per-lane tallies (ClassTallies, rate_engine.hpp:101-110).
+struct Ctr {
+    uint32_t fwd = 0, ack = 0, adm = 0, unm = 0;
 };
 
-// Exact micro-bps of one flow, rate_ubps_of (rate_engine.cpp:100-107):
-// floor(octets * 8e9 / dur) as a 128-bit value (hi is non-zero only when
-// dur is a few ms and octets are huge). Fast path: the f64 rate already
-// approximates the quotient to ~2^-51 relative, so q0 = rz(rate * 1e6)
-// lands within a few units of it; the exact integer residual then fixes
-// it up. Preconditions of the fast path (product fits in u64, dur <= 2^40,
-// quotient < 2^62) bound the estimate error by < 2^12 units and therefore
-// the true residual by < 2^52 * 2^0 < 2^63, so the wrapped u64 residual is
-// the real one; any estimate the fix-up loop cannot settle falls back to
-// the exact division.
-__device__ __forceinline__ void ubps_of(uint32_t oct, uint64_t dur, double rate, uint64_t& lo,
-                                        uint64_t& hi) {
-    hi = 0;
-    if (oct <= 2305843009u) {
-        const uint64_t p = static_cast<uint64_t>(oct) * 8000000000ull;
-        if (dur <= (1ull << 40) && rate < 4.0e12) {
-            uint64_t q = static_cast<uint64_t>(__dmul_rz(rate, 1.0e6));
-            int64_t r = static_cast<int64_t>(p - q * dur);
-            const int64_t d = static_cast<int64_t>(dur);
-#pragma unroll 1
-            for (int i = 0; i < 4 && r < 0; ++i) {
-                --q;
-                r += d;
-            }
-#pragma unroll 1
-            for (int i = 0; i < 4 && r >= d; ++i) {
-                ++q;
-                r -= d;
-            }
-            if (r >= 0 && r < d) {
-                lo = q;
-                return;
-            }
-        }
-        lo = p / dur;
-        return;
+// A queued flow's site code: either RESOLVED | site value, or the node index
+// (< 2^16) of the /16 block that holds the winning endpoint << 8 | the
+// endpoint's third octet, resolved to a site in stage B.
+constexpr uint32_t kResolved = 0x80000000u;
+constexpr uint32_t kSkip = 0xFFFFFFFFu;
+
+// reduce_slice's per-record filter (rate_engine.cpp:199-215) and the first
+// half of attribute (:127-146), branch-free, in the reference's order:
+//   ack = octets < (ack_max+1) * pkts          (false when pkts == 0)
+//   rej = pkts < max(min_packets,1) || dur < max(min_duration,1)
+// (pkts == 0 and dur == 0 fold into rej), then both endpoints' /16
+// directory bits (one LDS.64 each). A candidate whose endpoints both miss
+// is Unmatched here; otherwise the src-first winner's node index is queued.
+// When both /16s hold sites (src may still miss at /24) the full lookup runs
+// now, on those lanes only.
+template <bool kSmem>
+__device__ __forceinline__ uint32_t stage_a(uint32_t src, uint32_t dst, uint32_t pkts, uint32_t oct,
+                                            uint64_t dur, const DevParams& p,
+                                            const uint32_t* __restrict__ gt, Ctr& c) {
+    const bool ack = static_cast<uint64_t>(oct) < p.ack_plus1 * pkts;
+    const bool rej = pkts < p.min_packets1 || dur < static_cast<uint64_t>(p.min_duration1);
+    const uint32_t ds = src >> 16, dd = dst >> 16;
+    const uint2 ws = table_pair<kSmem>(gt, ds >> 5);
+    const uint2 wd = table_pair<kSmem>(gt, dd >> 5);
+    const bool hs = (ws.x >> (ds & 31u)) & 1u;
+    const bool hd = (wd.x >> (dd & 31u)) & 1u;
+    if (ack) ++c.ack;
+    if (!ack && rej) ++c.adm;
+    const bool cand = !ack && !rej;
+    if (cand && !(hs | hd)) ++c.unm;
+    const uint32_t bits = hs ? ws.x : wd.x;
+    const uint32_t rank0 = hs ? ws.y : wd.y;
+    const uint32_t d = hs ? ds : dd;
+    const uint32_t ip = hs ? src : dst;
+    const uint32_t rank = rank0 + __popc(bits & ~(0xFFFFFFFFu << (d & 31u)));
+    uint32_t code = (cand && (hs | hd)) ? (rank << 8 | ((ip >> 8) & 0xFFu)) : kSkip;
+#ifdef GNM_K2_ABLATION
+    if (p.ablation == 1) {
+        if (cand) c.fwd += rank;
+        code = kSkip;
     }
-    const unsigned __int128 q = static_cast<unsigned __int128>(oct) * 8000000000ull / dur;
-    lo = static_cast<uint64_t>(q);
-    hi = static_cast<uint64_t>(q >> 64);
+#endif
+    if (cand && hs && hd) {
+        const uint32_t v = site_of_full<kSmem>(gt, src, dst);
+        if (v == kNone) ++c.unm;
+        code = v == kNone ? kSkip : (kResolved | v);
+    }
+    return code;
 }
 
-// A Forward flow waiting in a warp's queue: packed (slot << 20 | site), octets, duration.
-struct FwdItem {
-    uint32_t packed;
-    uint32_t oct;
-    uint64_t dur;
-};
-constexpr uint32_t kQueue = 64; // per-warp FwdItem capacity (< 32 left + 32 pushed)
+// Stage B: the site value of a queued code (kNone: Unmatched at /24).
+template <bool kSmem>
+__device__ __forceinline__ uint32_t resolve(const uint32_t* __restrict__ gt, uint32_t code) {
+    const bool res = code & kResolved;
+    const uint32_t node = table_word<kSmem>(gt, res ? 0u : kDirWordsDev + (code >> 8));
+    const bool uni = node >> 31;
+    const uint32_t leaf = table_word<kSmem>(gt, (res || uni) ? 0u : node + (code & 0xFFu));
+    return res ? (code & 0x7FFFFFFFu) : (uni ? (node & 0x7FFFFFFFu) : leaf);
+}
 
 // RateHistogram::add (rate_engine.cpp:9-23) for one Forward flow, as
 // order-independent reductions:
 //   hist[site][bucket] += 1                              (u32, as the reference)
 //   octets and micro-bps sums                            exact integers
 //   min/max of the f64 rate via u64 min/max on the bit pattern (rates > 0,
-//   SURVEY.md §8a' #8); a cached read skips the atomic when it cannot win
-//   (a stale value is never below the current min / above the current max).
-// Called on warp-compacted items, so the arithmetic runs with full warps.
-template <bool kHot>
-__device__ __forceinline__ void accumulate(const FwdItem& it, const DevParams& p,
-                                           const DevPartials& P, const HotSmem& h) {
-    const uint32_t site = it.packed & p.site_mask;
-    const uint32_t slot = kHot ? it.packed >> 20 : 0u;
-    const bool hot = kHot && slot;
-    // Cold sites: fetch the current min/max first (the loads overlap the
-    // math), unless the context asked for unconditional min/max reductions.
-    unsigned long long cur_mn = 0, cur_mx = ~0ull;
-    if (!hot && !p.cold_red) {
-        cur_mn = __ldcg(P.mn + site);
-        cur_mx = __ldcg(P.mx + site);
+//   SURVEY.md §8a' #8)
+// Hot sites: non-returning shared adds of 16-bit limbs (micro-bps >= 2^48 go
+// to L2 instead); min/max go to L2 only when the slot's cached bounds say
+// they can win. Cold sites: straight to L2 (RED).
+template <bool kSmem, bool kHot>
+__device__ __forceinline__ void accumulate(uint32_t code, uint32_t oct, uint64_t dur,
+                                           const uint32_t* __restrict__ gt, const DevParams& p,
+                                           const DevPartials& P, const HotSmem& h, Ctr& c) {
+    const uint32_t v = resolve<kSmem>(gt, code);
+    if (v == kNone) {
+        ++c.unm;
+        return;
     }
-    const uint32_t oct = it.oct;
+    ++c.fwd;
+#ifdef GNM_K2_ABLATION
+    if (p.ablation == 2) {
+        c.unm ^= v ^ oct ^ static_cast<uint32_t>(dur);
+        return;
+    }
+#endif
+    const uint32_t site = v & p.site_mask;
+    const uint32_t slot = kHot ? (v >> 20) & 0x7FFu : 0u;
+    unsigned long long cmn = 0, cmx = ~0ull;
+    if (kHot && slot) { // issued early: the latency hides behind the division
+        cmn = h.mn[slot];
+        cmx = h.mx[slot];
+    }
     // flow_rate (rate_engine.cpp:88-94): exact product, one IEEE division.
-    const double rate = __ddiv_rn(8000.0 * static_cast<double>(oct), __ull2double_rn(it.dur));
-    const uint32_t bucket = bucket_of(rate);
+    const double rate = __ddiv_rn(8000.0 * static_cast<double>(oct), __ull2double_rn(dur));
     uint64_t lo, hi;
-    ubps_of(oct, it.dur, rate, lo, hi);
-    red_add(P.hist + static_cast<size_t>(site) * kBuckets + bucket, 1u);
+    ubps_of(oct, dur, rate, lo, hi);
     const unsigned long long rb = static_cast<unsigned long long>(__double_as_longlong(rate));
-    if (hot) {
-        // 32-bit shared atomics with exact carry propagation.
-        const uint32_t o = atomicAdd(h.oct_lo + slot, oct);
-        if (o + oct < o) atomicAdd(h.oct_hi + slot, 1u);
-        const uint32_t vl = static_cast<uint32_t>(lo), vh = static_cast<uint32_t>(lo >> 32);
-        const uint32_t a = atomicAdd(h.u0 + slot, vl);
-        uint32_t c2 = 0;
-        if (vh) {
-            const uint32_t b = atomicAdd(h.u1 + slot, vh);
-            c2 = b + vh < b;
+#ifdef GNM_K2_ABLATION
+    // Measurement builds only (tools/ablation.sh): 3 = no reductions,
+    // 4 = the histogram RED only. Results are wrong in these modes.
+    if (p.ablation == 3 || p.ablation == 4) {
+        if (p.ablation == 4) red_add(P.hist + hist_index(site, bucket_of_ubps(lo, hi), P.n_sites), 1u);
+        c.unm ^= static_cast<uint32_t>(lo ^ hi ^ rb) ^ bucket_of_ubps(lo, hi) ^ static_cast<uint32_t>(cmn ^ cmx);
+        return;
+    }
+#endif
+    red_add(P.hist + hist_index(site, bucket_of_ubps(lo, hi), P.n_sites), 1u);
+    unsigned long long* s = P.sums + static_cast<size_t>(site) * 4;
+    if (kHot && slot) {
+        uint32_t* l = h.limb + slot;
+        red_add_shared(l, oct & 0xFFFFu);
+        red_add_shared(l + kHotStride, oct >> 16);
+        if (hi == 0 && lo < (1ull << 48)) {
+            red_add_shared(l + 2 * kHotStride, static_cast<uint32_t>(lo) & 0xFFFFu);
+            red_add_shared(l + 3 * kHotStride, static_cast<uint32_t>(lo) >> 16);
+            red_add_shared(l + 4 * kHotStride, static_cast<uint32_t>(lo >> 32));
+        } else {
+            red_add(s + 1, lo & 0xFFFFFFFFull);
+            red_add(s + 2, lo >> 32);
+            if (hi) red_add(s + 3, hi);
         }
-        if (a + vl < a) {
-            const uint32_t b = atomicAdd(h.u1 + slot, 1u);
-            c2 += b == 0xFFFFFFFFu;
+        // min/max: the slot's cached bounds filter the global reductions. The
+        // cache is written with plain stores AFTER the RED, so it only ever
+        // holds rates whose RED was issued; a lost race loosens the filter
+        // (an extra RED) but never hides a winning update.
+        if (rb < cmn) {
+            red_min(P.mn + site, rb);
+            h.mn[slot] = rb;
         }
-        if (c2 | hi) atomicAdd(h.u2 + slot, c2 + static_cast<uint32_t>(hi));
-        if (rb < h.mn[slot]) atomicMin(h.mn + slot, rb);
-        if (rb > h.mx[slot]) atomicMax(h.mx + slot, rb);
+        if (rb > cmx) {
+            red_max(P.mx + site, rb);
+            h.mx[slot] = rb;
+        }
     } else {
-        unsigned long long* s = P.sums + static_cast<size_t>(site) * 4;
         red_add(s + 0, static_cast<unsigned long long>(oct));
         red_add(s + 1, lo & 0xFFFFFFFFull);
         if (lo >> 32) red_add(s + 2, lo >> 32);
         if (hi) red_add(s + 3, hi);
-        if (p.cold_red || rb < cur_mn) red_min(P.mn + site, rb);
-        if (p.cold_red || rb > cur_mx) red_max(P.mx + site, rb);
+        red_min(P.mn + site, rb);
+        red_max(P.mx + site, rb);
     }
 }
 
-// reduce_slice's per-record filter + attribution (rate_engine.cpp:199-233),
-// fixed order: zero packets, pure ACK, administrative, src-first
-// attribution. Returns true (and the packed site value) for Forward flows.
-template <bool kSmem>
-__device__ __forceinline__ bool classify(bool valid, uint32_t src, uint32_t dst, uint32_t pkts,
-                                         uint32_t oct, uint64_t dur, const DevParams& p,
-                                         const uint32_t* __restrict__ gt, Tally& t,
-                                         uint32_t& packed) {
-    if (!valid) return false;
-    if (pkts == 0) {
-        ++t.admin;
-        return false;
-    }
-    if (static_cast<uint64_t>(oct) < p.ack_plus1 * pkts) {
-        ++t.ack;
-        return false;
-    }
-    if (pkts < p.min_packets || dur < p.min_duration_ms || dur == 0) {
-        ++t.admin;
-        return false;
-    }
-    uint32_t v;
-    if (p.lookup_mode) {
-        v = lookup<kSmem>(gt, src);
-        if (v == kNone) v = lookup<kSmem>(gt, dst);
-    } else {
-        v = lookup2<kSmem>(gt, src, dst);
-    }
-    if (v == kNone) {
-        ++t.unm;
-        return false;
-    }
-    ++t.fwd;
-    packed = v;
-    return true;
+// Warp-level stream compaction of candidates: lanes append {code, octets,
+// duration} to the warp's shared queue (ballot + popc, one STS.128), and
+// every time 32 are queued the whole warp drains one per lane (stage B), so
+// the lookup tail and the per-flow arithmetic never run with the ~50% lane
+// occupancy the class mix would otherwise leave them.
+struct WarpQueue {
+    uint4* q;
+    uint32_t n; // warp-uniform fill
+};
+
+__device__ __forceinline__ void push(uint32_t code, uint32_t oct, uint64_t dur, WarpQueue& wq,
+                                     uint32_t lane) {
+    const bool f = code != kSkip;
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, f);
+    if (f)
+        wq.q[wq.n + __popc(m & ((1u << lane) - 1u))] =
+            make_uint4(code, oct, static_cast<uint32_t>(dur), static_cast<uint32_t>(dur >> 32));
+    wq.n += __popc(m);
 }
 
-// Warp-level stream compaction of Forward flows: lanes append their item to
-// the warp's shared queue (ballot + popc), and every time 32 are queued the
-// whole warp drains one item per lane, so accumulate() never runs with the
-// ~40% lane occupancy the class mix would otherwise leave it.
-template <bool kHot>
-__device__ __forceinline__ void push(bool fwd, const FwdItem& it, FwdItem* q, uint32_t& qn,
-                                     uint32_t lane, const DevParams& p, const DevPartials& P,
-                                     const HotSmem& h) {
-    const unsigned m = __ballot_sync(0xFFFFFFFFu, fwd);
-    if (fwd) q[qn + __popc(m & ((1u << lane) - 1u))] = it;
-    qn += __popc(m);
-    if (qn >= 32) {
+template <bool kSmem, bool kHot>
+__device__ __forceinline__ void drain_full(WarpQueue& wq, uint32_t lane,
+                                           const uint32_t* __restrict__ gt, const DevParams& p,
+                                           const DevPartials& P, const HotSmem& h, Ctr& c) {
+    while (wq.n >= 32) {
         __syncwarp();
-        const FwdItem x = q[qn - 32 + lane];
-        qn -= 32;
+        const uint4 x = wq.q[wq.n - 32 + lane];
+        wq.n -= 32;
         __syncwarp();
-        accumulate<kHot>(x, p, P, h);
+        accumulate<kSmem, kHot>(x.x, x.y, static_cast<uint64_t>(x.w) << 32 | x.z, gt, p, P, h, c);
     }
 }
 
-__device__ __forceinline__ void flush_tallies(const Tally& t, unsigned long long* out) {
+template <bool kSmem, bool kHot>
+__device__ __forceinline__ void drain_rest(WarpQueue& wq, uint32_t lane,
+                                           const uint32_t* __restrict__ gt, const DevParams& p,
+                                           const DevPartials& P, const HotSmem& h, Ctr& c) {
+    __syncwarp();
+    if (lane < wq.n) {
+        const uint4 x = wq.q[lane];
+        accumulate<kSmem, kHot>(x.x, x.y, static_cast<uint64_t>(x.w) << 32 | x.z, gt, p, P, h, c);
+    }
+    wq.n = 0;
+}
+
+__device__ __forceinline__ void flush_tallies(const Ctr& t, unsigned long long* out) {
     const uint32_t f = __reduce_add_sync(0xFFFFFFFFu, t.fwd);
     const uint32_t a = __reduce_add_sync(0xFFFFFFFFu, t.ack);
-    const uint32_t d = __reduce_add_sync(0xFFFFFFFFu, t.admin);
+    const uint32_t d = __reduce_add_sync(0xFFFFFFFFu, t.adm);
     const uint32_t u = __reduce_add_sync(0xFFFFFFFFu, t.unm);
     if ((threadIdx.x & 31u) == 0) {
         if (f) red_add(out + 0, static_cast<unsigned long long>(f));
@@ -363,127 +434,98 @@ __device__ __forceinline__ void flush_tallies(const Tally& t, unsigned long long
     }
 }
 
+// One flush per CTA. The limb sums are exact (< 2^32 each, see kCtaRecords)
+// and land in the global limbs K3 reassembles: sums[1] takes the low 32 bits
+// of every flow's micro-bps (so it stays below count * 2^32), sums[2] the
+// bits above. (min/max went to L2 during the run.)
 __device__ __forceinline__ void hot_flush(const HotSmem& h, const DevHot& hot, const DevPartials& P) {
     for (uint32_t slot = 1 + threadIdx.x; slot <= hot.n_slots; slot += blockDim.x) {
-        const uint64_t oct = static_cast<uint64_t>(h.oct_hi[slot]) << 32 | h.oct_lo[slot];
-        if (oct == 0) continue; // untouched: every Forward flow has >= 97 octets
+        const uint32_t* l = h.limb + slot;
+        const uint64_t oct = static_cast<uint64_t>(l[0]) + (static_cast<uint64_t>(l[kHotStride]) << 16);
+        const uint64_t u01 = static_cast<uint64_t>(l[2 * kHotStride]) +
+                             (static_cast<uint64_t>(l[3 * kHotStride]) << 16);
+        const uint32_t u2 = l[4 * kHotStride];
         const uint32_t site = __ldg(hot.hot_site + slot);
         unsigned long long* s = P.sums + static_cast<size_t>(site) * 4;
-        red_add(s + 0, oct);
-        red_add(s + 1, static_cast<unsigned long long>(h.u0[slot]));
-        if (h.u1[slot]) red_add(s + 2, static_cast<unsigned long long>(h.u1[slot]));
-        if (h.u2[slot]) red_add(s + 3, static_cast<unsigned long long>(h.u2[slot]));
-        red_min(P.mn + site, h.mn[slot]);
-        red_max(P.mx + site, h.mx[slot]);
+        if (oct) red_add(s + 0, oct);
+        if (u01) red_add(s + 1, u01);
+        if (u2) red_add(s + 2, static_cast<unsigned long long>(u2));
+    }
+}
+
+// One record by index (scalar loads; tails and the non-vector layouts).
+// kLayout 1: SoA; 2/3: 64-byte flowmon::FlowRecord rows (netflow.hpp:59-67).
+template <int kLayout>
+__device__ __forceinline__ void load_record(const DevBatch& b, uint64_t i, uint32_t& src, uint32_t& dst,
+                                            uint32_t& pkts, uint32_t& oct, uint64_t& dur) {
+    if constexpr (kLayout == 1) {
+        const DevSoA& c = b.soa;
+        src = c.src[i], dst = c.dst[i], pkts = c.pkts[i], oct = c.octets[i];
+        dur = c.end[i] - c.start[i];
+    } else if constexpr (kLayout == 2) {
+        const unsigned char* r = static_cast<const unsigned char*>(b.rec) + i * 64;
+        const uint2 a = __ldg(reinterpret_cast<const uint2*>(r));                 // src dst
+        const uint2 cc = __ldg(reinterpret_cast<const uint2*>(r + 16));           // pkts octets
+        const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(r + 48));  // start end
+        src = a.x, dst = a.y, pkts = cc.x, oct = cc.y, dur = e.y - e.x;
+    } else {
+        const unsigned char* r = static_cast<const unsigned char*>(b.rec) + i * 64;
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(r);
+        const uint64_t* qq = reinterpret_cast<const uint64_t*>(r + 48);
+        src = w[0], dst = w[1], pkts = w[4], oct = w[5], dur = qq[1] - qq[0];
+    }
+}
+
+// Records [first, last) in warp-strided 32-record rounds, scalar loads.
+template <int kLayout, bool kSmem, bool kHot>
+__device__ __forceinline__ void run_scalar(const DevBatch& b, uint64_t first, uint64_t last,
+                                           uint64_t stride, uint32_t lane,
+                                           const uint32_t* __restrict__ gt, const DevParams& p,
+                                           const DevPartials& P, const HotSmem& h, Ctr& t,
+                                           WarpQueue& wq) {
+    for (uint64_t base = first; base < last; base += stride) {
+        const uint64_t i = base + lane;
+        uint32_t src = 0, dst = 0, pkts = 0, oct = 0;
+        uint64_t dur = 0;
+        const bool ok = i < last;
+        if (ok) load_record<kLayout>(b, i, src, dst, pkts, oct, dur);
+        Ctr one;
+        const uint32_t code = stage_a<kSmem>(src, dst, pkts, oct, dur, p, gt, one);
+        if (ok) {
+            t.ack += one.ack;
+            t.adm += one.adm;
+            t.unm += one.unm;
+        }
+        push(ok ? code : kSkip, oct, dur, wq, lane);
+        drain_full<kSmem, kHot>(wq, lane, gt, p, P, h, t);
     }
 }
 
 // ---- K2 ----------------------------------------------------------------------
-// kLayout 0: SoA, 128-bit vector loads (all columns 16-byte aligned)
-//         1: SoA, scalar loads
-//         2: AoS 64-byte rows, 128-bit loads
-//         3: AoS, scalar loads
-// Loops are warp-uniform (each warp walks whole 32- or 128-record tiles with
-// a per-lane validity flag) so the queue's warp collectives stay converged.
-template <int kLayout, bool kSmem, bool kHot>
-__global__ void __launch_bounds__(kK2Block, 2) k2(DevBatch b, const uint32_t* __restrict__ gt,
-                                                uint32_t table_words, DevParams p, DevPartials P,
-                                                DevHot hot) {
+// Block prologue: registry table and hot slots into shared memory, the
+// warp's queue after them.
+template <bool kSmem, bool kHot>
+__device__ __forceinline__ void k2_prologue(const uint32_t* __restrict__ gt, uint32_t table_words,
+                                            HotSmem& h, WarpQueue& wq) {
     load_table<kSmem>(gt, table_words);
-    HotSmem h{};
     const uint32_t smem_words = kSmem ? table_words : 0u;
     if constexpr (kHot) {
         h = hot_smem(smem_words);
         hot_init(h);
     }
-    const uint32_t lane = threadIdx.x & 31u;
-    FwdItem* q = reinterpret_cast<FwdItem*>(g_smem + smem_words + (kHot ? kHotBytes / 4 : 0u)) +
-                 (threadIdx.x >> 5) * kQueue;
-    uint32_t qn = 0;
+    wq.q = reinterpret_cast<uint4*>(g_smem + smem_words + (kHot ? kHotBytes / 4 : 0u)) +
+           (threadIdx.x >> 5) * kQueue;
+    wq.n = 0;
     __syncthreads();
-    Tally t;
-    const uint64_t warp_gid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-    FwdItem it;
-    if constexpr (kLayout == 0) {
-        // Two records per lane per 64-record warp tile, software-pipelined:
-        // the next tile's six loads are in flight while this one is
-        // classified, so the load latency is not exposed at first use.
-        const DevSoA& c = b.soa;
-        const uint64_t n2 = c.n / 2;
-        const uint64_t step = nwarps * 32;
-        uint64_t base = warp_gid * 32;
-        uint2 s{}, d{}, k{}, o{};
-        ulonglong2 t0{}, e0{};
-        auto fetch = [&](uint64_t bs, uint2& fs, uint2& fd, uint2& fk, uint2& fo, ulonglong2& ft,
-                         ulonglong2& fe) {
-            const uint64_t g = bs + lane;
-            if (bs < n2 && g < n2) {
-                fs = ld_stream_u2(c.src + 2 * g);
-                fd = ld_stream_u2(c.dst + 2 * g);
-                fk = ld_stream_u2(c.pkts + 2 * g);
-                fo = ld_stream_u2(c.octets + 2 * g);
-                ft = ld_stream_u64x2(c.start + 2 * g);
-                fe = ld_stream_u64x2(c.end + 2 * g);
-            }
-        };
-        fetch(base, s, d, k, o, t0, e0);
-        for (; base < n2; base += step) {
-            const bool ok = base + lane < n2;
-            uint2 ns{}, nd{}, nk{}, no{};
-            ulonglong2 nt{}, ne{};
-            fetch(base + step, ns, nd, nk, no, nt, ne);
-            bool f;
-            it = FwdItem{0, o.x, e0.x - t0.x};
-            f = classify<kSmem>(ok, s.x, d.x, k.x, o.x, it.dur, p, gt, t, it.packed);
-            push<kHot>(f, it, q, qn, lane, p, P, h);
-            it = FwdItem{0, o.y, e0.y - t0.y};
-            f = classify<kSmem>(ok, s.y, d.y, k.y, o.y, it.dur, p, gt, t, it.packed);
-            push<kHot>(f, it, q, qn, lane, p, P, h);
-            s = ns, d = nd, k = nk, o = no, t0 = nt, e0 = ne;
-        }
-        // The odd tail record: the first warp of the grid.
-        if (warp_gid == 0) {
-            const uint64_t i = n2 * 2 + lane;
-            const bool ok = i < c.n;
-            it = FwdItem{0, ok ? c.octets[i] : 0u, ok ? c.end[i] - c.start[i] : 0ull};
-            const bool f = classify<kSmem>(ok, ok ? c.src[i] : 0u, ok ? c.dst[i] : 0u,
-                                           ok ? c.pkts[i] : 0u, it.oct, it.dur, p, gt, t, it.packed);
-            push<kHot>(f, it, q, qn, lane, p, P, h);
-        }
-    } else {
-        const uint64_t n = b.n;
-        for (uint64_t base = warp_gid * 32; base < n; base += nwarps * 32) {
-            const uint64_t i = base + lane;
-            const bool ok = i < n;
-            uint32_t src = 0, dst = 0, pkts = 0, oct = 0;
-            uint64_t start = 0, end = 0;
-            if (ok) {
-                if constexpr (kLayout == 1) {
-                    const DevSoA& c = b.soa;
-                    src = c.src[i], dst = c.dst[i], pkts = c.pkts[i], oct = c.octets[i];
-                    start = c.start[i], end = c.end[i];
-                } else if constexpr (kLayout == 2) {
-                    const unsigned char* r = static_cast<const unsigned char*>(b.rec) + i * 64;
-                    const uint4 a = __ldg(reinterpret_cast<const uint4*>(r));        // src dst nexthop ifs
-                    const uint4 cc = __ldg(reinterpret_cast<const uint4*>(r + 16));  // pkts octets first last
-                    const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(r + 48)); // start end
-                    src = a.x, dst = a.y, pkts = cc.x, oct = cc.y, start = e.x, end = e.y;
-                } else {
-                    const unsigned char* r = static_cast<const unsigned char*>(b.rec) + i * 64;
-                    const uint32_t* w = reinterpret_cast<const uint32_t*>(r);
-                    const uint64_t* qq = reinterpret_cast<const uint64_t*>(r + 48);
-                    src = w[0], dst = w[1], pkts = w[4], oct = w[5], start = qq[0], end = qq[1];
-                }
-            }
-            it = FwdItem{0, oct, end - start};
-            const bool f = classify<kSmem>(ok, src, dst, pkts, oct, it.dur, p, gt, t, it.packed);
-            push<kHot>(f, it, q, qn, lane, p, P, h);
-        }
-    }
-    // Drain the partial queue.
-    __syncwarp();
-    if (lane < qn) accumulate<kHot>(q[lane], p, P, h);
+}
+
+template <bool kSmem, bool kHot>
+__device__ __forceinline__ void k2_epilogue(Ctr& t, WarpQueue& wq, uint32_t lane,
+                                            const uint32_t* __restrict__ gt, const DevParams& p,
+                                            const DevPartials& P, const HotSmem& h,
+                                            const DevHot& hot) {
+    drain_full<kSmem, kHot>(wq, lane, gt, p, P, h, t);
+    drain_rest<kSmem, kHot>(wq, lane, gt, p, P, h, t);
     flush_tallies(t, P.sums + static_cast<size_t>(P.n_sites) * 4);
     if constexpr (kHot) {
         __syncthreads();
@@ -491,34 +533,155 @@ __global__ void __launch_bounds__(kK2Block, 2) k2(DevBatch b, const uint32_t* __
     }
 }
 
-// ---- K2, TMA-staged SoA variant ---------------------------------------------
-// One persistent CTA per SM (kTmaBlock threads). Each CTA walks tiles
-// blockIdx.x, +gridDim.x, ... of kTile records; a tile's six columns (32 KB)
-// land in a shared-memory stage through cp.async.bulk (TMA bulk copies,
-// evict-first in L2 so the stream does not push the L2-resident histogram and
-// accumulators out), completing on the stage's mbarrier. kStages tiles are in
-// flight at all times: the LAST warp to finish with a stage re-arms it with
-// the CTA's next-but-(kStages-1) tile, so loads never wait for compute.
-// Lane l of warp w reads record w*32+l of the tile from shared memory.
-constexpr int kTmaBlock = 1024;
-constexpr uint32_t kTile = 1024;
-constexpr uint32_t kStageBytes = kTile * 32;
-constexpr uint32_t kStages = 3;
-constexpr uint32_t kChunksPerTile = kTile / 32;
+// Main variant: SoA columns, 16-byte aligned, n < 2^32. CTA b owns the
+// contiguous 64-record tiles [b*T/G, (b+1)*T/G) (at most kCtaTiles); its
+// warps walk them strided, two records per lane per tile (one LDG.64 per u32
+// column, one LDG.128 per u64 column, non-allocating), software-pipelined:
+// the next tile's six loads are in flight while this one is classified. The
+// last CTA also takes the < 64-record remainder through the scalar path.
+template <bool kSmem, bool kHot>
+__global__ void __launch_bounds__(kK2Block, 2) k2_soa(DevBatch b, const uint32_t* __restrict__ gt,
+                                                    uint32_t table_words, DevParams p,
+                                                    DevPartials P, DevHot hot) {
+    HotSmem h{};
+    WarpQueue wq;
+    k2_prologue<kSmem, kHot>(gt, table_words, h, wq);
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warp = threadIdx.x >> 5;
+    const DevSoA& c = b.soa;
+    const uint64_t tiles = c.n >> 6;
+    const uint32_t t_end = static_cast<uint32_t>(tiles * (blockIdx.x + 1) / gridDim.x);
+    const uint2* src2 = reinterpret_cast<const uint2*>(c.src) + lane;
+    const uint2* dst2 = reinterpret_cast<const uint2*>(c.dst) + lane;
+    const uint2* pkt2 = reinterpret_cast<const uint2*>(c.pkts) + lane;
+    const uint2* oct2 = reinterpret_cast<const uint2*>(c.octets) + lane;
+    const ulonglong2* st2 = reinterpret_cast<const ulonglong2*>(c.start) + lane;
+    const ulonglong2* en2 = reinterpret_cast<const ulonglong2*>(c.end) + lane;
+    Ctr t;
+    uint32_t tile = static_cast<uint32_t>(tiles * blockIdx.x / gridDim.x) + warp;
+    uint2 s, d, k, o;
+    ulonglong2 t0, e0;
+    if (tile < t_end) {
+        const uint32_t g = tile * 32u;
+        s = ld_stream_u2(src2 + g);
+        d = ld_stream_u2(dst2 + g);
+        k = ld_stream_u2(pkt2 + g);
+        o = ld_stream_u2(oct2 + g);
+        t0 = ld_stream_u64x2(st2 + g);
+        e0 = ld_stream_u64x2(en2 + g);
+    }
+    for (; tile < t_end; tile += kWarps) {
+        const uint32_t next = tile + kWarps;
+        uint2 ns, nd, nk, no;
+        ulonglong2 nt, ne;
+        if (next < t_end) {
+            const uint32_t g = next * 32u;
+            ns = ld_stream_u2(src2 + g);
+            nd = ld_stream_u2(dst2 + g);
+            nk = ld_stream_u2(pkt2 + g);
+            no = ld_stream_u2(oct2 + g);
+            nt = ld_stream_u64x2(st2 + g);
+            ne = ld_stream_u64x2(en2 + g);
+        }
+        const uint64_t dx = e0.x - t0.x, dy = e0.y - t0.y;
+        const uint32_t cx = stage_a<kSmem>(s.x, d.x, k.x, o.x, dx, p, gt, t);
+        const uint32_t cy = stage_a<kSmem>(s.y, d.y, k.y, o.y, dy, p, gt, t);
+        push(cx, o.x, dx, wq, lane);
+        push(cy, o.y, dy, wq, lane);
+        drain_full<kSmem, kHot>(wq, lane, gt, p, P, h, t);
+        s = ns, d = nd, k = nk, o = no, t0 = nt, e0 = ne;
+    }
+    if (blockIdx.x == gridDim.x - 1 && warp == 0)
+        run_scalar<1, kSmem, kHot>(b, tiles << 6, c.n, 32, lane, gt, p, P, h, t, wq);
+    k2_epilogue<kSmem, kHot>(t, wq, lane, gt, p, P, h, hot);
+}
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+// Variant: no register double-buffering. Each warp asks the TMA engine to
+// pull the tile it will read kAhead iterations later into L2
+// (cp.async.bulk.prefetch.L2, one bulk request per column segment, issued
+// by lanes 0-5), then loads the current tile with plain vector loads that
+// hit L2. Frees the 16 registers the in-register prefetch holds.
+constexpr uint32_t kAhead = 3;
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <bool kSmem, bool kHot>
+__global__ void __launch_bounds__(kK2Block, 2) k2_soa_pf(DevBatch b, const uint32_t* __restrict__ gt,
+                                                       uint32_t table_words, DevParams p,
+                                                       DevPartials P, DevHot hot) {
+    HotSmem h{};
+    WarpQueue wq;
+    k2_prologue<kSmem, kHot>(gt, table_words, h, wq);
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warp = threadIdx.x >> 5;
+    const DevSoA& c = b.soa;
+    const uint64_t tiles = c.n >> 6;
+    const uint32_t t_end = static_cast<uint32_t>(tiles * (blockIdx.x + 1) / gridDim.x);
+    uint32_t tile = static_cast<uint32_t>(tiles * blockIdx.x / gridDim.x) + warp;
+    // Lane l < 6 prefetches column l's 64-record segment (256 or 512 bytes).
+    const char* pf_col = reinterpret_cast<const char*>(
+        lane == 0 ? static_cast<const void*>(c.src)
+        : lane == 1 ? static_cast<const void*>(c.dst)
+        : lane == 2 ? static_cast<const void*>(c.pkts)
+        : lane == 3 ? static_cast<const void*>(c.octets)
+        : lane == 4 ? static_cast<const void*>(c.start)
+                    : static_cast<const void*>(c.end));
+    const uint32_t pf_bytes = lane < 4 ? 256u : 512u;
+    if (lane < 6)
+        for (uint32_t a = 0; a < kAhead; ++a) {
+            const uint32_t tl = tile + a * kWarps;
+            if (tl < t_end) bulk_prefetch_l2(pf_col + static_cast<size_t>(tl) * pf_bytes, pf_bytes);
+        }
+    const uint2* src2 = reinterpret_cast<const uint2*>(c.src) + lane;
+    const uint2* dst2 = reinterpret_cast<const uint2*>(c.dst) + lane;
+    const uint2* pkt2 = reinterpret_cast<const uint2*>(c.pkts) + lane;
+    const uint2* oct2 = reinterpret_cast<const uint2*>(c.octets) + lane;
+    const ulonglong2* st2 = reinterpret_cast<const ulonglong2*>(c.start) + lane;
+    const ulonglong2* en2 = reinterpret_cast<const ulonglong2*>(c.end) + lane;
+    Ctr t;
+    for (; tile < t_end; tile += kWarps) {
+        const uint32_t ahead = tile + kAhead * kWarps;
+        if (lane < 6 && ahead < t_end)
+            bulk_prefetch_l2(pf_col + static_cast<size_t>(ahead) * pf_bytes, pf_bytes);
+        const uint32_t g = tile * 32u;
+        const uint2 s = ld_stream_u2(src2 + g);
+        const uint2 d = ld_stream_u2(dst2 + g);
+        const uint2 k = ld_stream_u2(pkt2 + g);
+        const uint2 o = ld_stream_u2(oct2 + g);
+        const ulonglong2 t0 = ld_stream_u64x2(st2 + g);
+        const ulonglong2 e0 = ld_stream_u64x2(en2 + g);
+        const uint64_t dx = e0.x - t0.x, dy = e0.y - t0.y;
+        const uint32_t cx = stage_a<kSmem>(s.x, d.x, k.x, o.x, dx, p, gt, t);
+        const uint32_t cy = stage_a<kSmem>(s.y, d.y, k.y, o.y, dy, p, gt, t);
+        push(cx, o.x, dx, wq, lane);
+        push(cy, o.y, dy, wq, lane);
+        drain_full<kSmem, kHot>(wq, lane, gt, p, P, h, t);
+    }
+    if (blockIdx.x == gridDim.x - 1 && warp == 0)
+        run_scalar<1, kSmem, kHot>(b, tiles << 6, c.n, 32, lane, gt, p, P, h, t, wq);
+    k2_epilogue<kSmem, kHot>(t, wq, lane, gt, p, P, h, hot);
+}
+
+// ---- K2, TMA-staged variant ----------------------------------------------------
+// Each warp owns a kRing-deep ring of 64-record tiles in shared memory, fed
+// by its own lane 0 with cp.async.bulk (one bulk copy per column segment,
+// completing on the stage's mbarrier): the next tile streams in while this
+// one is classified, without holding it in registers and without any
+// global address arithmetic in the loop. Stage layout (2 KB): src[64],
+// dst[64], pkts[64], octets[64] (u32), start[64], end[64] (u64); lane l
+// reads records 2l and 2l+1 with immediate-offset LDS.64 / LDS.128.
+constexpr int kTmaWarps = 24;
+constexpr int kTmaBlock = kTmaWarps * 32;
+constexpr uint32_t kRing = 2;
+constexpr uint32_t kTileBytes = 64 * 32;
+constexpr size_t kTmaFixed = kTmaWarps * kQueue * 16 + kTmaWarps * kRing * (kTileBytes + 8);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
@@ -529,163 +692,139 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ uint64_t evict_first_policy() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
-                                            uint64_t* bar, uint64_t pol) {
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
-
-struct Stage {
-    uint32_t* src;
-    uint32_t* dst;
-    uint32_t* pkts;
-    uint32_t* oct;
-    uint64_t* start;
-    uint64_t* end;
-};
-
-__device__ __forceinline__ Stage stage_at(unsigned char* base, uint32_t s) {
-    unsigned char* b = base + static_cast<size_t>(s) * kStageBytes;
-    Stage st;
-    st.src = reinterpret_cast<uint32_t*>(b);
-    st.dst = st.src + kTile;
-    st.pkts = st.dst + kTile;
-    st.oct = st.pkts + kTile;
-    st.start = reinterpret_cast<uint64_t*>(st.oct + kTile);
-    st.end = st.start + kTile;
-    return st;
+// Lane 0: tile `tile` of the batch into stage buffer `st`.
+__device__ __forceinline__ void issue_tile(unsigned char* st, uint64_t* bar, const DevSoA& c, uint32_t tile) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(kTileBytes)
+                 : "memory");
+    const size_t r = static_cast<size_t>(tile) * 64;
+    bulk_g2s(st, c.src + r, 256, bar);
+    bulk_g2s(st + 256, c.dst + r, 256, bar);
+    bulk_g2s(st + 512, c.pkts + r, 256, bar);
+    bulk_g2s(st + 768, c.octets + r, 256, bar);
+    bulk_g2s(st + 1024, c.start + r, 512, bar);
+    bulk_g2s(st + 1536, c.end + r, 512, bar);
 }
 
-// Records [first, first + count) of the 4-aligned prefix into stage st.
-__device__ __forceinline__ void issue_tile(const Stage& st, const DevSoA& c, uint64_t first,
-                                           uint32_t count, uint64_t* bar, uint64_t pol) {
-    mbar_expect_tx(bar, count * 32u);
-    tma_load_1d(st.src, c.src + first, count * 4u, bar, pol);
-    tma_load_1d(st.dst, c.dst + first, count * 4u, bar, pol);
-    tma_load_1d(st.pkts, c.pkts + first, count * 4u, bar, pol);
-    tma_load_1d(st.oct, c.octets + first, count * 4u, bar, pol);
-    tma_load_1d(st.start, c.start + first, count * 8u, bar, pol);
-    tma_load_1d(st.end, c.end + first, count * 8u, bar, pol);
+// The same ring fed by per-lane async copies (cp.async.cg, 16 B each, no
+// registers): lane l moves bytes [64l, 64l+64) of the 2 KB stage, i.e.
+// lanes 0-15 the four u32 column segments and 16-31 the two u64 ones; each
+// tile is one commit group, waited with wait_group + __syncwarp.
+__device__ __forceinline__ void async_tile(unsigned char* st, const char* col, uint32_t seg_bytes,
+                                           uint32_t lane_off, uint32_t tile) {
+    const char* g = col + static_cast<size_t>(tile) * seg_bytes + lane_off;
+    const uint32_t sa = smem_u32(st) + 64 * (threadIdx.x & 31u);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + 16 * k), "l"(g + 16 * k)
+                     : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-template <bool kSmem, bool kHot>
-__global__ void __launch_bounds__(kTmaBlock, 1) k2_tma(DevSoA c, const uint32_t* __restrict__ gt,
-                                                        uint32_t table_words, DevParams p,
-                                                        DevPartials P, DevHot hot) {
-    const uint32_t smem_words = kSmem ? table_words : 0u;
-    load_table<kSmem>(gt, table_words);
+template <bool kSmem, bool kHot, bool kBulk>
+__global__ void __launch_bounds__(kTmaBlock, 1) k2_tma(DevBatch b, const uint32_t* __restrict__ gt,
+                                                     uint32_t table_words, DevParams p,
+                                                     DevPartials P, DevHot hot) {
     HotSmem h{};
-    if constexpr (kHot) {
-        h = hot_smem(smem_words);
-        hot_init(h);
-    }
+    WarpQueue wq;
+    k2_prologue<kSmem, kHot>(gt, table_words, h, wq);
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warp = threadIdx.x >> 5;
-    const uint32_t nwarps = blockDim.x >> 5;
-    uint32_t* after_hot = g_smem + smem_words + (kHot ? kHotBytes / 4 : 0u);
-    FwdItem* q = reinterpret_cast<FwdItem*>(after_hot) + warp * kQueue;
-    unsigned char* stages = reinterpret_cast<unsigned char*>(after_hot) + nwarps * kQueue * sizeof(FwdItem);
-    uint64_t* full = reinterpret_cast<uint64_t*>(stages + static_cast<size_t>(kStages) * kStageBytes);
-    uint64_t* empty = full + kStages;
-    uint32_t* claim = reinterpret_cast<uint32_t*>(empty + kStages);
-
-    const uint64_t n_vec = c.n & ~3ull; // TMA-covered prefix (16-byte multiples)
-    const uint64_t n_tiles = (n_vec + kTile - 1) / kTile;
-    auto tile_first = [&](uint32_t local) {
-        return (static_cast<uint64_t>(blockIdx.x) + static_cast<uint64_t>(local) * gridDim.x) * kTile;
-    };
-    auto tile_count = [&](uint64_t first) {
-        return static_cast<uint32_t>(min(static_cast<uint64_t>(kTile), n_vec - first));
-    };
-    const uint32_t my_tiles = static_cast<uint32_t>(
-        blockIdx.x < n_tiles ? (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0);
-    const uint32_t my_chunks = my_tiles * kChunksPerTile;
-
-    if (threadIdx.x == 0) {
-        for (uint32_t s = 0; s < kStages; ++s) {
-            mbar_init(full + s, 1);
-            mbar_init(empty + s, kChunksPerTile);
-        }
-        *claim = 0;
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-
-    Tally t;
-    FwdItem it;
-    uint32_t qn = 0;
-    if (warp == 0) {
-        // Producer: one lane keeps kStages tiles in flight. A stage is
-        // re-armed once all 32 chunks of its previous tile were read
-        // (empty[s] phase), so loads never wait for the accumulate() work.
+    const uint32_t smem_words = kSmem ? table_words : 0u;
+    unsigned char* rings = reinterpret_cast<unsigned char*>(g_smem + smem_words + (kHot ? kHotBytes / 4 : 0u)) +
+                           kTmaWarps * kQueue * 16;
+    unsigned char* ring = rings + static_cast<size_t>(warp) * kRing * kTileBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(rings + static_cast<size_t>(kTmaWarps) * kRing * kTileBytes) +
+                     warp * kRing;
+    const DevSoA& c = b.soa;
+    const uint64_t tiles = c.n >> 6;
+    const uint32_t t0 = static_cast<uint32_t>(tiles * blockIdx.x / gridDim.x);
+    const uint32_t t1 = static_cast<uint32_t>(tiles * (blockIdx.x + 1) / gridDim.x);
+    const uint32_t mine = t1 - t0 > warp ? (t1 - t0 - warp + kTmaWarps - 1) / kTmaWarps : 0u;
+    // cp.async feed: this lane's column and byte offset within the segment.
+    const uint32_t cidx = lane < 16 ? lane >> 2 : 4 + ((lane - 16) >> 3);
+    const char* col = reinterpret_cast<const char*>(
+        cidx == 0 ? static_cast<const void*>(c.src)
+        : cidx == 1 ? static_cast<const void*>(c.dst)
+        : cidx == 2 ? static_cast<const void*>(c.pkts)
+        : cidx == 3 ? static_cast<const void*>(c.octets)
+        : cidx == 4 ? static_cast<const void*>(c.start)
+                    : static_cast<const void*>(c.end));
+    const uint32_t seg_bytes = lane < 16 ? 256u : 512u;
+    const uint32_t lane_off = lane < 16 ? (lane & 3u) * 64 : ((lane - 16) & 7u) * 64;
+    if constexpr (kBulk) {
         if (lane == 0) {
-            const uint64_t pol = evict_first_policy();
-            for (uint32_t j = 0; j < my_tiles; ++j) {
-                const uint32_t s = j % kStages;
-                if (j >= kStages) mbar_wait(empty + s, ((j / kStages) - 1) & 1u);
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                const uint64_t f = tile_first(j);
-                issue_tile(stage_at(stages, s), c, f, tile_count(f), full + s, pol);
-            }
+            for (uint32_t st = 0; st < kRing; ++st) mbar_init(bars + st, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            for (uint32_t i = 0; i < kRing && i < mine; ++i)
+                issue_tile(ring + i * kTileBytes, bars + i, c, t0 + warp + i * kTmaWarps);
         }
-        __syncwarp();
     } else {
-        // Consumers claim 32-record chunks dynamically: a warp held up in
-        // accumulate() never delays a stage's release. Claims can run at most
-        // one tile past the loaded window (< 32 warps can be parked on an
-        // unloaded tile), so every parity below names the right phase.
-        for (;;) {
-            uint32_t cl = 0;
-            if (lane == 0) cl = atomicAdd(claim, 1u);
-            cl = __shfl_sync(0xFFFFFFFFu, cl, 0);
-            if (cl >= my_chunks) break;
-            const uint32_t i = cl / kChunksPerTile;
-            const uint32_t chunk = cl % kChunksPerTile;
-            const uint32_t s = i % kStages;
-            const uint32_t count = tile_count(tile_first(i));
-            const Stage st = stage_at(stages, s);
-            mbar_wait(full + s, (i / kStages) & 1u);
-            const uint32_t k = chunk * 32 + lane;
-            const bool ok = k < count;
-            uint32_t src = 0, dst = 0, pkts = 0;
-            it = FwdItem{0, 0, 0};
-            if (ok) {
-                src = st.src[k];
-                dst = st.dst[k];
-                pkts = st.pkts[k];
-                it.oct = st.oct[k];
-                it.dur = st.end[k] - st.start[k];
-            }
+        for (uint32_t i = 0; i < kRing; ++i) {
+            if (i < mine) async_tile(ring + i * kTileBytes, col, seg_bytes, lane_off, t0 + warp + i * kTmaWarps);
+            else asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+    }
+    __syncwarp();
+    Ctr t;
+    for (uint32_t i = 0; i < mine; ++i) {
+        const uint32_t st = i % kRing;
+        unsigned char* sb = ring + st * kTileBytes;
+        if constexpr (kBulk) {
+            mbar_wait(bars + st, (i / kRing) & 1u);
+        } else {
+            asm volatile("cp.async.wait_group %0;" ::"n"(kRing - 1) : "memory");
             __syncwarp();
-            if (lane == 0) mbar_arrive(empty + s);
-            const bool f = classify<kSmem>(ok, src, dst, pkts, it.oct, it.dur, p, gt, t, it.packed);
-            push<kHot>(f, it, q, qn, lane, p, P, h);
         }
-        // The n % 4 tail records: block 0, warp 1, direct loads.
-        if (blockIdx.x == 0 && warp == 1) {
-            const uint64_t r = n_vec + lane;
-            const bool ok = r < c.n;
-            it = FwdItem{0, ok ? c.octets[r] : 0u, ok ? c.end[r] - c.start[r] : 0ull};
-            const bool f = classify<kSmem>(ok, ok ? c.src[r] : 0u, ok ? c.dst[r] : 0u,
-                                           ok ? c.pkts[r] : 0u, it.oct, it.dur, p, gt, t, it.packed);
-            push<kHot>(f, it, q, qn, lane, p, P, h);
-        }
+        const uint2 s = *reinterpret_cast<const uint2*>(sb + 8 * lane);
+        const uint2 d = *reinterpret_cast<const uint2*>(sb + 256 + 8 * lane);
+        const uint2 k = *reinterpret_cast<const uint2*>(sb + 512 + 8 * lane);
+        const uint2 o = *reinterpret_cast<const uint2*>(sb + 768 + 8 * lane);
+        const ulonglong2 ts = *reinterpret_cast<const ulonglong2*>(sb + 1024 + 16 * lane);
+        const ulonglong2 te = *reinterpret_cast<const ulonglong2*>(sb + 1536 + 16 * lane);
         __syncwarp();
-        if (lane < qn) accumulate<kHot>(q[lane], p, P, h);
+        if constexpr (kBulk) {
+            if (lane == 0 && i + kRing < mine) issue_tile(sb, bars + st, c, t0 + warp + (i + kRing) * kTmaWarps);
+        } else {
+            if (i + kRing < mine) async_tile(sb, col, seg_bytes, lane_off, t0 + warp + (i + kRing) * kTmaWarps);
+            else asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        const uint64_t dx = te.x - ts.x, dy = te.y - ts.y;
+        const uint32_t cx = stage_a<kSmem>(s.x, d.x, k.x, o.x, dx, p, gt, t);
+        const uint32_t cy = stage_a<kSmem>(s.y, d.y, k.y, o.y, dy, p, gt, t);
+        push(cx, o.x, dx, wq, lane);
+        push(cy, o.y, dy, wq, lane);
+        drain_full<kSmem, kHot>(wq, lane, gt, p, P, h, t);
     }
-    flush_tallies(t, P.sums + static_cast<size_t>(P.n_sites) * 4);
-    if constexpr (kHot) {
-        __syncthreads();
-        hot_flush(h, hot, P);
-    }
+    if (blockIdx.x == gridDim.x - 1 && warp == 0)
+        run_scalar<1, kSmem, kHot>(b, tiles << 6, c.n, 32, lane, gt, p, P, h, t, wq);
+    k2_epilogue<kSmem, kHot>(t, wq, lane, gt, p, P, h, hot);
+}
+
+// Other layouts: unaligned SoA (1), AoS 64-byte rows with vector (2) or
+// scalar (3) loads. CTA b owns records [b*n/G, (b+1)*n/G) (at most
+// kCtaRecords), one record per lane per round.
+template <int kLayout, bool kSmem, bool kHot>
+__global__ void __launch_bounds__(kK2Block, 2) k2_gen(DevBatch b, const uint32_t* __restrict__ gt,
+                                                    uint32_t table_words, DevParams p,
+                                                    DevPartials P, DevHot hot) {
+    HotSmem h{};
+    WarpQueue wq;
+    k2_prologue<kSmem, kHot>(gt, table_words, h, wq);
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t r0 = b.n * blockIdx.x / gridDim.x, r1 = b.n * (blockIdx.x + 1) / gridDim.x;
+    Ctr t;
+    run_scalar<kLayout, kSmem, kHot>(b, r0 + (threadIdx.x >> 5) * 32, r1, kK2Block, lane, gt, p, P, h,
+                                     t, wq);
+    k2_epilogue<kSmem, kHot>(t, wq, lane, gt, p, P, h, hot);
 }
 
 // ---- K1: hot-site plan ------------------------------------------------------
@@ -702,54 +841,79 @@ __global__ void __launch_bounds__(kK2Block) k_sample(DevBatch b, const uint32_t*
     for (uint32_t j = threadIdx.x; j < chunk_len; j += blockDim.x) {
         const uint64_t i = base + j;
         uint32_t src, dst, pkts, oct;
-        uint64_t start, end;
-        if (b.aos) {
-            const unsigned char* r = static_cast<const unsigned char*>(b.rec) + i * 64;
-            const uint32_t* w = reinterpret_cast<const uint32_t*>(r);
-            const uint64_t* q = reinterpret_cast<const uint64_t*>(r + 48);
-            src = w[0], dst = w[1], pkts = w[4], oct = w[5], start = q[0], end = q[1];
-        } else {
-            src = b.soa.src[i], dst = b.soa.dst[i], pkts = b.soa.pkts[i], oct = b.soa.octets[i];
-            start = b.soa.start[i], end = b.soa.end[i];
-        }
-        const uint64_t dur = end - start;
-        if (pkts == 0 || static_cast<uint64_t>(oct) < p.ack_plus1 * pkts || pkts < p.min_packets ||
-            dur < p.min_duration_ms || dur == 0)
+        uint64_t dur;
+        if (b.aos) load_record<3>(b, i, src, dst, pkts, oct, dur);
+        else load_record<1>(b, i, src, dst, pkts, oct, dur);
+        if (static_cast<uint64_t>(oct) < p.ack_plus1 * pkts || pkts < p.min_packets1 ||
+            dur < static_cast<uint64_t>(p.min_duration1))
             continue;
-        uint32_t v = lookup<kSmem>(gt, src);
-        if (v == kNone) v = lookup<kSmem>(gt, dst);
+        const uint32_t v = site_of_full<kSmem>(gt, src, dst);
         if (v != kNone) atomicAdd(cnt + (v & p.site_mask), 1u);
     }
 }
 
-// Sites with at least `thr` sampled Forward flows get a slot (first come,
-// first served up to kHotSlots; the numbering does not affect results).
-// Resets the counts for the next call.
-__global__ void k_hot_assign(uint32_t* __restrict__ cnt, uint32_t n_sites, uint32_t thr,
-                             uint32_t* __restrict__ site_slot, uint32_t* __restrict__ hot_site,
-                             uint32_t* __restrict__ next) {
-    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n_sites; s += gridDim.x * blockDim.x) {
+// One block: the sites with the most sampled Forward flows (at least `thr`)
+// get slots 1..kHotSlots. A 4096-bin histogram of the counts gives the
+// smallest count threshold whose sites fit the slots; the numbering itself
+// does not affect results. Resets the counts for the next call.
+constexpr int kSelectBlock = 1024;
+constexpr uint32_t kCountBins = 4096;
+__global__ void __launch_bounds__(kSelectBlock) k_hot_select(uint32_t* __restrict__ cnt, uint32_t n_sites,
+                                                             uint32_t thr, uint32_t* __restrict__ site_slot,
+                                                             uint32_t* __restrict__ hot_site) {
+    __shared__ uint32_t bins[kCountBins];
+    __shared__ uint32_t part[kSelectBlock];
+    __shared__ uint32_t cut, next;
+    for (uint32_t i = threadIdx.x; i < kCountBins; i += blockDim.x) bins[i] = 0;
+    if (threadIdx.x == 0) next = 0;
+    __syncthreads();
+    for (uint32_t s = threadIdx.x; s < n_sites; s += blockDim.x) {
+        const uint32_t c = cnt[s];
+        if (c >= thr) atomicAdd(&bins[min(c, kCountBins - 1)], 1u);
+    }
+    __syncthreads();
+    // Suffix sums over the bins: thread i owns bins [4i, 4i+4).
+    const uint32_t i0 = threadIdx.x * (kCountBins / kSelectBlock);
+    uint32_t own = 0;
+    for (uint32_t k = 0; k < kCountBins / kSelectBlock; ++k) own += bins[i0 + k];
+    part[threadIdx.x] = own;
+    __syncthreads();
+    for (uint32_t off = 1; off < kSelectBlock; off <<= 1) { // inclusive suffix scan
+        const uint32_t x = threadIdx.x + off < kSelectBlock ? part[threadIdx.x + off] : 0u;
+        __syncthreads();
+        part[threadIdx.x] += x;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) cut = 0xFFFFFFFFu;
+    __syncthreads();
+    {
+        // The cut is the lowest bin b with suffix(b) <= kHotSlots.
+        uint32_t suffix = threadIdx.x + 1 < kSelectBlock ? part[threadIdx.x + 1] : 0u;
+        for (int k = kCountBins / kSelectBlock - 1; k >= 0; --k) {
+            suffix += bins[i0 + k];
+            if (suffix <= kHotSlots) atomicMin(&cut, i0 + k);
+        }
+    }
+    __syncthreads();
+    const uint32_t t = max(cut, thr);
+    for (uint32_t s = threadIdx.x; s < n_sites; s += blockDim.x) {
         const uint32_t c = cnt[s];
         cnt[s] = 0;
         uint32_t slot = 0;
-        if (c >= thr) {
-            const uint32_t k = atomicAdd(next, 1u);
-            if (k < kHotSlots) {
-                slot = k + 1;
-                hot_site[slot] = s;
-            }
+        if (c >= t && c > 0) {
+            slot = atomicAdd(&next, 1u) + 1;
+            hot_site[slot] = s;
         }
         site_slot[s] = slot;
     }
 }
 
 // Rewrites the slot bits of every site value in the table (nodes flagged
-// uniform and leaf entries) and resets the slot counter.
+// uniform and leaf entries).
 __global__ void k_table_slots(uint32_t* __restrict__ words, uint32_t node_begin,
                               uint32_t leaf_begin, uint32_t end,
-                              const uint32_t* __restrict__ site_slot, uint32_t* __restrict__ next) {
+                              const uint32_t* __restrict__ site_slot) {
     const uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i0 == 0) *next = 0;
     for (uint32_t i = node_begin + i0; i < end; i += gridDim.x * blockDim.x) {
         const uint32_t w = words[i];
         if (i < leaf_begin) {
@@ -830,10 +994,11 @@ __global__ void __launch_bounds__(256) k3_finalize(DevPartials P, double thresho
         const double mn = __longlong_as_double(static_cast<long long>(mnb));
         const double mx = __longlong_as_double(static_cast<long long>(mxb));
         const uint32_t b0 = bucket_of(mn), b1 = bucket_of(mx);
-        unsigned int* row = P.hist + static_cast<size_t>(site) * kBuckets;
+        unsigned int* hist = P.hist;
+        const uint32_t n = P.n_sites;
         if (write_out) {
             uint64_t c = 0;
-            for (uint32_t b = b0 + lane; b <= b1; b += 32) c += row[b];
+            for (uint32_t b = b0 + lane; b <= b1; b += 32) c += hist[hist_index(site, b, n)];
             c = warp_sum_u64(c);
             // median_bps (rate_engine.cpp:42-58): first k with cumulative >= ceil(c/2).
             const uint64_t target = (c + 1) / 2;
@@ -841,7 +1006,7 @@ __global__ void __launch_bounds__(256) k3_finalize(DevPartials P, double thresho
             uint32_t k = kBuckets - 1;
             for (uint32_t base = b0; base <= b1; base += 32) {
                 const uint32_t b = base + lane;
-                uint64_t x = b <= b1 ? row[b] : 0u;
+                uint64_t x = b <= b1 ? hist[hist_index(site, b, n)] : 0u;
 #pragma unroll
                 for (int off = 1; off < 32; off <<= 1) {
                     const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, x, off);
@@ -879,13 +1044,25 @@ __global__ void __launch_bounds__(256) k3_finalize(DevPartials P, double thresho
         }
         if (reset) {
             __syncwarp();
-            for (uint32_t b = b0 + lane; b <= b1; b += 32) row[b] = 0;
+            for (uint32_t b = b0 + lane; b <= b1; b += 32) hist[hist_index(site, b, n)] = 0;
             if (lane < 4) P.sums[static_cast<size_t>(site) * 4 + lane] = 0;
             if (lane == 0) {
                 P.mn[site] = kMinInitBits;
                 P.mx[site] = kMaxInitBits;
             }
         }
+    }
+}
+
+// Blocked -> dense [site][bucket]; one thread per output word (coalesced
+// writes; reads hit 8-word runs).
+__global__ void k_hist_export(const unsigned int* __restrict__ hist, uint32_t n_sites,
+                              unsigned int* __restrict__ dense) {
+    const size_t total = static_cast<size_t>(n_sites) * kBuckets;
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const uint32_t site = static_cast<uint32_t>(i / kBuckets), b = static_cast<uint32_t>(i % kBuckets);
+        dense[i] = hist[hist_index(site, b, n_sites)];
     }
 }
 
@@ -918,19 +1095,28 @@ cudaError_t allow_smem(K kernel) {
                                 static_cast<int>(kSmemMax));
 }
 
+template <int L, bool kS, bool kH>
+constexpr auto k2_kernel() {
+    if constexpr (L == 0) return k2_soa<kS, kH>;
+    else if constexpr (L == 4) return k2_soa_pf<kS, kH>;
+    else if constexpr (L == 5) return k2_tma<kS, kH, true>;
+    else if constexpr (L == 6) return k2_tma<kS, kH, false>;
+    else return k2_gen<L, kS, kH>;
+}
+
 template <int L>
 cudaError_t allow_layout() {
     cudaError_t e;
-    if ((e = allow_smem(k2<L, true, true>))) return e;
-    if ((e = allow_smem(k2<L, true, false>))) return e;
-    if ((e = allow_smem(k2<L, false, true>))) return e;
-    return allow_smem(k2<L, false, false>);
+    if ((e = allow_smem(k2_kernel<L, true, true>()))) return e;
+    if ((e = allow_smem(k2_kernel<L, true, false>()))) return e;
+    if ((e = allow_smem(k2_kernel<L, false, true>()))) return e;
+    return allow_smem(k2_kernel<L, false, false>());
 }
 
 template <int L, bool kS, bool kH>
 void launch_k2_t(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t, const DevParams& p,
                  const DevPartials& P, const DevHot& hot, cudaStream_t s) {
-    k2<L, kS, kH><<<cfg.grid, cfg.block, cfg.smem, s>>>(b, t.words, t.n_words, p, P, hot);
+    k2_kernel<L, kS, kH>()<<<cfg.grid, cfg.block, cfg.smem, s>>>(b, t.words, t.n_words, p, P, hot);
 }
 
 template <int L>
@@ -948,6 +1134,16 @@ void launch_k2_l(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t, con
 
 size_t table_smem_bytes(uint32_t table_words) { return static_cast<size_t>(table_words) * 4; }
 
+int k2_layout(const DevBatch& b) {
+    if (b.aos) return (reinterpret_cast<uintptr_t>(b.rec) & 15u) == 0 ? 2 : 3;
+    const DevSoA& c = b.soa;
+    const bool vec = ((reinterpret_cast<uintptr_t>(c.src) | reinterpret_cast<uintptr_t>(c.dst) |
+                       reinterpret_cast<uintptr_t>(c.pkts) | reinterpret_cast<uintptr_t>(c.octets) |
+                       reinterpret_cast<uintptr_t>(c.start) | reinterpret_cast<uintptr_t>(c.end)) &
+                      15u) == 0;
+    return vec ? 0 : 1;
+}
+
 } // namespace
 
 cudaError_t init_kernel_attributes() {
@@ -956,60 +1152,61 @@ cudaError_t init_kernel_attributes() {
     if ((e = allow_layout<1>())) return e;
     if ((e = allow_layout<2>())) return e;
     if ((e = allow_layout<3>())) return e;
-    if ((e = allow_smem(k2_tma<true, true>))) return e;
-    if ((e = allow_smem(k2_tma<true, false>))) return e;
-    if ((e = allow_smem(k2_tma<false, true>))) return e;
-    if ((e = allow_smem(k2_tma<false, false>))) return e;
+    if ((e = allow_layout<4>())) return e;
+    if ((e = allow_layout<5>())) return e;
+    if ((e = allow_layout<6>())) return e;
     if ((e = allow_smem(k_sample<true>))) return e;
     return allow_smem(k_classify<true>);
 }
 
-namespace {
-bool soa_aligned(const DevBatch& b) {
-    const DevSoA& c = b.soa;
-    return !b.aos &&
-           ((reinterpret_cast<uintptr_t>(c.src) | reinterpret_cast<uintptr_t>(c.dst) |
-             reinterpret_cast<uintptr_t>(c.pkts) | reinterpret_cast<uintptr_t>(c.octets) |
-             reinterpret_cast<uintptr_t>(c.start) | reinterpret_cast<uintptr_t>(c.end)) & 15u) == 0;
-}
-} // namespace
-
 LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool hot, int* occ_cache,
-                    bool allow_tma) {
+                    int variant) {
     LaunchCfg c;
+    c.variant = variant;
     const size_t tbytes = table_smem_bytes(table_words);
-    const uint64_t n_tiles = ((b.n & ~3ull) + kTile - 1) / kTile;
-    c.stages = 0;
-    if (allow_tma && soa_aligned(b) && n_tiles > 0) {
-        // TMA-staged variant: one 1024-thread CTA per SM, kStages tiles in flight.
-        const size_t fixed = (hot ? kHotBytes : 0) + (kTmaBlock / 32) * kQueue * sizeof(FwdItem) +
-                             kStages * kStageBytes + 2 * kStages * 8 + 16;
-        if (fixed <= kSmemMax) {
+    if ((variant == 2 || variant == 3) && k2_layout(b) == 0) {
+        // TMA-staged: one 768-thread CTA per SM, < 2^16 records per CTA.
+        const size_t fixed = (hot ? kHotBytes : 0) + kTmaFixed;
+        if (fixed + 1024 <= kSmemMax) {
             c.block = kTmaBlock;
-            c.table_in_smem = tbytes + fixed <= kSmemMax;
+            c.table_in_smem = tbytes + fixed + 1024 <= kSmemMax;
             c.smem = fixed + (c.table_in_smem ? tbytes : 0);
-            c.stages = kStages;
-            c.grid = static_cast<int>(std::min<uint64_t>(sm_count(device), n_tiles));
+            const uint64_t resident = static_cast<uint64_t>(sm_count(device));
+            const uint64_t cap = static_cast<uint64_t>(kCtaTiles) * 64;
+            uint64_t grid = (b.n + cap - 1) / cap;
+            grid = grid <= resident ? std::min<uint64_t>(resident, std::max<uint64_t>(grid, (b.n + 16383) / 16384))
+                                    : (grid + resident - 1) / resident * resident;
+            c.grid = static_cast<int>(std::max<uint64_t>(1, grid));
             return c;
         }
+        c.variant = 0;
     }
     c.block = kK2Block;
     c.table_in_smem = tbytes <= kSmemTableMax;
     c.smem = (c.table_in_smem ? tbytes : 0) + (hot ? kHotBytes : 0) + kQueueBytes;
     int per_sm = occ_cache ? occ_cache[hot ? 1 : 0] : 0;
-    if (per_sm > 0) {
-    } else if (c.table_in_smem)
-        per_sm = hot ? occupancy(k2<0, true, true>, c.block, c.smem)
-                     : occupancy(k2<0, true, false>, c.block, c.smem);
-    else
-        per_sm = hot ? occupancy(k2<0, false, true>, c.block, c.smem)
-                     : occupancy(k2<0, false, false>, c.block, c.smem);
-    if (occ_cache) occ_cache[hot ? 1 : 0] = per_sm;
+    if (per_sm <= 0) {
+        if (c.table_in_smem)
+            per_sm = hot ? occupancy(k2_soa<true, true>, c.block, c.smem)
+                         : occupancy(k2_soa<true, false>, c.block, c.smem);
+        else
+            per_sm = hot ? occupancy(k2_soa<false, true>, c.block, c.smem)
+                         : occupancy(k2_soa<false, false>, c.block, c.smem);
+        if (occ_cache) occ_cache[hot ? 1 : 0] = per_sm;
+    }
     const uint64_t resident = static_cast<uint64_t>(per_sm) * sm_count(device);
-    // At least 16 records per thread so the per-CTA table load amortises.
-    const uint64_t per_block = static_cast<uint64_t>(c.block) * 16;
-    const uint64_t want = (b.n + per_block - 1) / per_block;
-    c.grid = static_cast<int>(std::max<uint64_t>(1, std::min(resident, want)));
+    // A CTA takes at most kCtaRecords records (the hot limbs' bound). Beyond
+    // one resident wave the grid is a whole number of waves; below it, at
+    // least 16 records per thread so the per-CTA table load amortises.
+    const uint64_t cap = k2_layout(b) == 0 ? static_cast<uint64_t>(kCtaTiles) * 64 : kCtaRecords;
+    uint64_t grid = (b.n + cap - 1) / cap;
+    if (grid <= resident) {
+        const uint64_t per_block = static_cast<uint64_t>(c.block) * 16;
+        grid = std::max(grid, std::min(resident, (b.n + per_block - 1) / per_block));
+    } else {
+        grid = (grid + resident - 1) / resident * resident;
+    }
+    c.grid = static_cast<int>(std::max<uint64_t>(1, grid));
     return c;
 }
 
@@ -1029,17 +1226,16 @@ bool plan_hot(int device, const DevBatch& b, const DevTable& t, const DevParams&
         thr = 1;
     } else {
         if (chunk_len < 256) return false;
-        // A site is hot when it is expected to see >= 32 Forward flows per
-        // K2 CTA, so its block-private accumulator amortises the flush.
+        // Eligible: expected to see >= 2 Forward flows per K2 CTA (a slot's
+        // one flush then costs no more L2 reductions than the flows would).
         const double thr_d =
-            32.0 * k2_grid * static_cast<double>(chunk_len) * chunks / static_cast<double>(b.n);
+            2.0 * k2_grid * static_cast<double>(chunk_len) * chunks / static_cast<double>(b.n);
         thr = static_cast<uint32_t>(std::max(2.0, thr_d));
         if (thr > chunk_len * chunks) return false;
     }
     uint32_t* cnt = scratch;
     uint32_t* site_slot = scratch + n_sites;
     uint32_t* hot_site = site_slot + n_sites;
-    uint32_t* next = hot_site + kHotStride;
     const uint64_t stride = std::max<uint64_t>(b.n / chunks, chunk_len);
     const uint32_t nchunks = static_cast<uint32_t>(std::min<uint64_t>(chunks, b.n / chunk_len));
     const size_t tbytes = table_smem_bytes(t.n_words);
@@ -1047,11 +1243,10 @@ bool plan_hot(int device, const DevBatch& b, const DevTable& t, const DevParams&
         k_sample<true><<<nchunks, kK2Block, tbytes, s>>>(b, t.words, t.n_words, p, stride, chunk_len, cnt);
     else
         k_sample<false><<<nchunks, kK2Block, 0, s>>>(b, t.words, t.n_words, p, stride, chunk_len, cnt);
-    const uint32_t ag = std::min<uint32_t>((n_sites + 255) / 256, 1024);
-    k_hot_assign<<<ag, 256, 0, s>>>(cnt, n_sites, thr, site_slot, hot_site, next);
+    k_hot_select<<<1, kSelectBlock, 0, s>>>(cnt, n_sites, thr, site_slot, hot_site);
     const uint32_t span = t.n_words - t.node_begin;
     const uint32_t rg = std::max<uint32_t>(1, std::min<uint32_t>((span + 255) / 256, 1024));
-    k_table_slots<<<rg, 256, 0, s>>>(t.words, t.node_begin, t.leaf_begin, t.n_words, site_slot, next);
+    k_table_slots<<<rg, 256, 0, s>>>(t.words, t.node_begin, t.leaf_begin, t.n_words, site_slot);
     *launches += 3;
     *err = cudaGetLastError();
     return *err == cudaSuccess;
@@ -1060,29 +1255,16 @@ bool plan_hot(int device, const DevBatch& b, const DevTable& t, const DevParams&
 cudaError_t launch_k2(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t,
                       const DevParams& p, const DevPartials& P, const DevHot& hot,
                       cudaStream_t s) {
-    if (cfg.stages) {
-        const bool hh = hot.n_slots > 0;
-        if (cfg.table_in_smem) {
-            if (hh) k2_tma<true, true><<<cfg.grid, cfg.block, cfg.smem, s>>>(b.soa, t.words, t.n_words, p, P, hot);
-            else k2_tma<true, false><<<cfg.grid, cfg.block, cfg.smem, s>>>(b.soa, t.words, t.n_words, p, P, hot);
-        } else {
-            if (hh) k2_tma<false, true><<<cfg.grid, cfg.block, cfg.smem, s>>>(b.soa, t.words, t.n_words, p, P, hot);
-            else k2_tma<false, false><<<cfg.grid, cfg.block, cfg.smem, s>>>(b.soa, t.words, t.n_words, p, P, hot);
-        }
-        return cudaGetLastError();
-    }
-    if (b.aos) {
-        const bool vec = (reinterpret_cast<uintptr_t>(b.rec) & 15u) == 0;
-        if (vec) launch_k2_l<2>(cfg, b, t, p, P, hot, s);
-        else launch_k2_l<3>(cfg, b, t, p, P, hot, s);
-    } else {
-        const DevSoA& c = b.soa;
-        const bool vec = ((reinterpret_cast<uintptr_t>(c.src) | reinterpret_cast<uintptr_t>(c.dst) |
-                           reinterpret_cast<uintptr_t>(c.pkts) | reinterpret_cast<uintptr_t>(c.octets) |
-                           reinterpret_cast<uintptr_t>(c.start) | reinterpret_cast<uintptr_t>(c.end)) &
-                          15u) == 0;
-        if (vec) launch_k2_l<0>(cfg, b, t, p, P, hot, s);
-        else launch_k2_l<1>(cfg, b, t, p, P, hot, s);
+    switch (k2_layout(b)) {
+    case 0:
+        if (cfg.variant == 1) launch_k2_l<4>(cfg, b, t, p, P, hot, s);
+        else if (cfg.variant == 2) launch_k2_l<5>(cfg, b, t, p, P, hot, s);
+        else if (cfg.variant == 3) launch_k2_l<6>(cfg, b, t, p, P, hot, s);
+        else launch_k2_l<0>(cfg, b, t, p, P, hot, s);
+        break;
+    case 1: launch_k2_l<1>(cfg, b, t, p, P, hot, s); break;
+    case 2: launch_k2_l<2>(cfg, b, t, p, P, hot, s); break;
+    default: launch_k2_l<3>(cfg, b, t, p, P, hot, s); break;
     }
     return cudaGetLastError();
 }
@@ -1111,10 +1293,16 @@ cudaError_t launch_init_partials(const DevPartials& P, cudaStream_t s) {
     cudaError_t e;
     if ((e = cudaMemsetAsync(P.sums, 0, (static_cast<size_t>(P.n_sites) * 4 + 4) * 8, s))) return e;
     if ((e = cudaMemsetAsync(P.mx, 0, static_cast<size_t>(P.n_sites) * 8, s))) return e;
-    if ((e = cudaMemsetAsync(P.hist, 0, static_cast<size_t>(P.n_sites) * kBuckets * 4, s))) return e;
+    if ((e = cudaMemsetAsync(P.hist, 0, static_cast<size_t>(P.n_sites) * kHistStride * 4, s))) return e;
     if (P.n_sites)
         k_fill_u64<<<std::min<uint32_t>((P.n_sites + 255) / 256, 1024), 256, 0, s>>>(P.mn, P.n_sites,
                                                                                      kMinInitBits);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hist_export(const DevPartials& P, uint32_t* dense, cudaStream_t s) {
+    if (P.n_sites == 0) return cudaSuccess;
+    k_hist_export<<<1184, 256, 0, s>>>(P.hist, P.n_sites, dense);
     return cudaGetLastError();
 }
 

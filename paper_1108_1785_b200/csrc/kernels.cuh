@@ -9,6 +9,17 @@
 namespace gnm {
 
 constexpr uint32_t kBuckets = 10001;
+// Per-site histograms, sector-blocked and bucket-major: the 8 buckets of
+// one 32-byte sector belong to one site (the sector footprint of a site's
+// touched buckets is the same as a site-major row), while consecutive
+// 8-bucket groups of a site lie n_sites * 32 B apart. A hot site's buckets
+// therefore spread over every L2 slice instead of the few slices a 40 KB
+// row would map to (same-slice RED contention, profiles/round1).
+constexpr uint32_t kBucketGroups = (kBuckets + 7) / 8; // 1251
+constexpr uint32_t kHistStride = kBucketGroups * 8;   // words per site
+__host__ __device__ inline size_t hist_index(uint32_t site, uint32_t bucket, uint32_t n_sites) {
+    return (static_cast<size_t>(bucket >> 3) * n_sites + site) * 8 + (bucket & 7u);
+}
 constexpr uint64_t kMinInitBits = 0x7FF0000000000000ull; // +inf: empty min
 constexpr uint64_t kMaxInitBits = 0;                     // +0.0: empty max (rates are > 0)
 constexpr uint32_t kHotSlots = 512;   // block-private accumulators for hot sites
@@ -18,9 +29,10 @@ struct DevParams {
     uint64_t ack_plus1;       // ack_avg_size_max + 1, u64 (rate_engine.cpp:78)
     uint32_t min_packets;
     uint32_t min_duration_ms;
+    uint32_t min_packets1;    // max(min_packets, 1): folds d_pkts == 0 (:75) into one compare
+    uint32_t min_duration1;   // max(min_duration_ms, 1): folds duration == 0 (:81)
     uint32_t site_mask;       // kPackedSiteMask, or 0x7FFFFFFF for wide tables
-    uint32_t cold_red;        // 1: cold-site min/max as unconditional RED (no L2 read)
-    uint32_t lookup_mode;     // 0: branch-free dual probe, 1: src-then-dst probes
+    uint32_t ablation;        // GNM_K2_ABLATION builds only (tools/ablation.sh); 0 otherwise
 };
 
 // Device partial accumulators of one context (layout in gnetmon.h, gnm_partials).
@@ -69,7 +81,8 @@ struct LaunchCfg {
     int block;
     size_t smem;
     bool table_in_smem;
-    uint32_t stages; // > 0: TMA-staged SoA variant with this many stages
+    int variant; // aligned SoA: 0 register double-buffered loads, 1 TMA L2 prefetch,
+                 // 2 TMA bulk copies into per-warp shared-memory rings
 };
 
 // Once per device: opt the shared-memory kernels into large dynamic smem.
@@ -78,13 +91,13 @@ cudaError_t init_kernel_attributes();
 // Occupancy-derived launch configuration for K2 over n records.
 // occ_cache[hot] memoises blocks/SM (0 = unknown) for this table size.
 LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool hot, int* occ_cache,
-                    bool allow_tma = true);
+                    int variant = 0);
 
 // K1 (optional, skewed batches): sample the batch, pick the hot sites and
 // write their slots into the table words. Returns false when the batch is
 // too small for block-private accumulation to pay; `scratch` holds
-// n_sites u32 counts (zero at rest), n_sites u32 site->slot, kHotStride u32
-// slot->site and one u32 counter.
+// n_sites u32 counts (zero at rest), n_sites u32 site->slot and kHotStride
+// u32 slot->site.
 bool plan_hot(int device, const DevBatch& b, const DevTable& t, const DevParams& p,
               uint32_t n_sites, uint32_t* scratch, int k2_grid, bool force, cudaStream_t s,
               uint64_t* launches, cudaError_t* err);
@@ -97,6 +110,9 @@ cudaError_t launch_k3(int device, const DevPartials& P, double threshold, gnm_si
                       int reset, cudaStream_t s);
 cudaError_t launch_reset(int device, const DevPartials& P, cudaStream_t s);
 cudaError_t launch_init_partials(const DevPartials& P, cudaStream_t s);
+// Dense [n_sites][10001] copy of the blocked histograms (the reference's
+// RateHistogram::buckets_ order) into `dense` (device memory).
+cudaError_t launch_hist_export(const DevPartials& P, uint32_t* dense, cudaStream_t s);
 cudaError_t launch_classify(const LaunchCfg& cfg, const DevSoA& b, const DevTable& t,
                             const DevParams& p, uint32_t* out, cudaStream_t s);
 

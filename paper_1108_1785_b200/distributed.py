@@ -12,7 +12,7 @@ Partials layout (gnetmon.h, gnm_partials):
   sums     int64 [n_sites*4 + 4]   SUM  (octets, ubps limb0/1/2 per site; tallies)
   min_bps  float64 [n_sites]       MIN  (+inf when empty)
   max_bps  float64 [n_sites]       MAX  (0 when empty)
-  hist     int32 [n_sites*10001]   SUM
+  hist     int32 [n_sites*10008]   SUM  (sector-blocked bucket-major, see gnetmon.h)
 """
 from __future__ import annotations
 

@@ -123,3 +123,38 @@ def test_oracle_matches_live_reference_random(orc, ref):
         np.testing.assert_array_equal(got["ubps_lo"], lo)
         np.testing.assert_array_equal(got["ubps_hi"], hi)
         np.testing.assert_array_equal(got["octets"], octs)
+
+
+def test_integer_bucket_identity():
+    """K2 computes bucket_index (rate_engine.cpp:119-125) as
+    min(10000, floor(ubps / 1e10)) from the exact micro-bps instead of
+    dividing the f64 rate by 1e4 (kernels.cu, bucket_of_ubps). Check the
+    identity against the reference's double arithmetic (numpy float64 is the
+    same IEEE round-to-nearest division) on random and adversarial inputs:
+    octets/durations placed within +-2 of every bucket boundary
+    4*oct == 5*dur*k, where double rounding would bite if it could."""
+    rng = np.random.default_rng(7)
+    n = 400_000
+    oct_ = rng.integers(0, 2**32, n, dtype=np.uint64)
+    dur = np.concatenate([rng.integers(1, 20_000, n // 4), rng.integers(1, 10**8, n // 4),
+                          rng.integers(1, 2**63, n // 4, dtype=np.int64),
+                          (rng.integers(1, 2**62, n // 4, dtype=np.int64) >> rng.integers(0, 62, n // 4))
+                          + 1]).astype(np.uint64)
+    # adversarial: oct = floor(5*dur*k/4) + d, d in [-2, 2]
+    m = 200_000
+    ad = rng.integers(1, 10**7, m).astype(np.uint64)
+    k = rng.integers(0, 10002, m).astype(np.uint64)
+    ao = (5 * ad * k) // 4 + rng.integers(-2, 3, m).astype(np.int64).astype(np.uint64)
+    keep = ao < 2**32
+    oct_ = np.concatenate([oct_, ao[keep]])
+    dur = np.concatenate([dur, ad[keep]])
+    rate = 8000.0 * oct_.astype(np.float64) / dur.astype(np.float64)
+    b = rate / 10000.0
+    ref = np.where(b >= 10000.0, 10000, b.astype(np.uint64))
+    # floor(oct * 8e9 / dur) / 1e10 == floor(4 * oct / (5 * dur)) (nested
+    # floors); 4*oct < 2^34 and 5*dur may be up to 2^66, so use Python ints.
+    num = (4 * oct_.astype(object))
+    den = (5 * dur.astype(object))
+    got = np.minimum(np.array(num // den, dtype=object), 10000).astype(np.uint64)
+    bad = np.nonzero(got != ref)[0]
+    assert bad.size == 0, (oct_[bad[:5]], dur[bad[:5]], ref[bad[:5]], got[bad[:5]])
