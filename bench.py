@@ -270,12 +270,12 @@ def main():
     def step(batch):
         if world == 1:
             return eng.aggregate(batch, cat)
-        # K2 on this rank's shard, one NCCL all-reduce of the per-site
-        # partials over NVLink (paper_1108_1785_b200.distributed), K3.
+        # K2 on this rank's shard, then the two-round exact-median combine
+        # over NCCL (paper_1108_1785_b200.distributed): all-reduce of sums /
+        # min / max / coarse counts, K3a+K2b on this rank's log, all-reduce
+        # of the median super-buckets' fine counts, K3b.
         eng.accumulate(batch, cat)
-        t = eng.device_tensors(cat)
-        with torch.cuda.stream(stream):
-            D.allreduce_partials(t)
+        D.combine(eng, cat, stream=stream)
         return eng.finalize(cat)
 
     def barrier():

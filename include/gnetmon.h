@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define GNM_ABI_VERSION 1
+#define GNM_ABI_VERSION 2
 
 /* rate_engine.hpp:18-20 */
 #define GNM_BUCKET_COUNT 10001
@@ -207,23 +207,34 @@ int gnm_reset(gnm_ctx* ctx);
 
 /* Device partials of the current accumulation, for a cross-GPU all-reduce
  * (SURVEY.md §8e). All are device pointers on the context's device.
- *   sums:  uint64 [n_sites*4 + 4]  reduce SUM  (per site: octets, ubps limb0,
- *          limb1, limb2 (32-bit limbs); then tallies fwd, ack, admin, unmatched)
- *   min:   float64 [n_sites]       reduce MIN  (+inf when empty)
- *   max:   float64 [n_sites]       reduce MAX  (0 when empty)
- *   hist:  uint32 [n_sites*10008]  reduce SUM; sector-blocked bucket-major:
- *          count(site, b) = hist[((b >> 3) * n_sites + site) * 8 + (b & 7)]
- *          (gnm_finalize exports the dense [site][10001] order) */
+ *   sums:   uint64 [n_sites*4 + 4]   reduce SUM  (per site: octets, ubps limb0,
+ *           limb1, limb2 (32-bit limbs); then tallies fwd, ack, admin, unmatched)
+ *   min:    float64 [n_sites]        reduce MIN  (+inf when empty)
+ *   max:    float64 [n_sites]        reduce MAX  (0 when empty)
+ *   coarse: uint32 [157*n_sites]     reduce SUM  flows per (super-bucket, site),
+ *           super-bucket = bucket >> 6, index sb*n_sites + site
+ *   fine:   uint32 [n_sites*64]      reduce SUM  the median super-bucket's
+ *           64 bucket counts; valid after gnm_prepare_median
+ * The exact median is a two-round selection. Multi-GPU protocol, per rank:
+ *   gnm_accumulate (own shard) -> all-reduce sums/min/max/coarse ->
+ *   gnm_prepare_median (finds the global median super-bucket, counts this
+ *   rank's flows inside it) -> all-reduce fine -> gnm_finalize.
+ * A single context just calls gnm_finalize, which prepares itself. */
 typedef struct gnm_partials {
     uint64_t* sums;
     double* min_bps;
     double* max_bps;
-    uint32_t* hist;
+    uint32_t* coarse;
+    uint32_t* fine;
     uint64_t n_sites;
     uint64_t sums_count;
-    uint64_t hist_count;
+    uint64_t coarse_count;
+    uint64_t fine_count;
 } gnm_partials;
 int gnm_get_partials(gnm_ctx* ctx, const gnm_registry* reg, gnm_partials* out);
+/* Round 2 of the median on this context's log (see gnm_partials); no further
+ * gnm_accumulate until gnm_finalize or gnm_reset. */
+int gnm_prepare_median(gnm_ctx* ctx, const gnm_registry* reg);
 
 /* Per-record classification (classify/attribute, rate_engine.cpp:71-86,
  * 127-146): out[i] = class << 30 | (site & 0x3FFFFFFF), site = 0x3FFFFFFF

@@ -75,8 +75,9 @@ class gnm_result(C.Structure):
 
 class gnm_partials(C.Structure):
     _fields_ = [("sums", C.c_void_p), ("min_bps", C.c_void_p), ("max_bps", C.c_void_p),
-                ("hist", C.c_void_p), ("n_sites", C.c_uint64), ("sums_count", C.c_uint64),
-                ("hist_count", C.c_uint64)]
+                ("coarse", C.c_void_p), ("fine", C.c_void_p), ("n_sites", C.c_uint64),
+                ("sums_count", C.c_uint64), ("coarse_count", C.c_uint64),
+                ("fine_count", C.c_uint64)]
 
 
 class gnm_timing(C.Structure):
@@ -145,6 +146,7 @@ _SIGS = [
     ("gnm_finalize", C.c_int, [_P, _P, C.POINTER(gnm_result)]),
     ("gnm_reset", C.c_int, [_P]),
     ("gnm_get_partials", C.c_int, [_P, _P, C.POINTER(gnm_partials)]),
+    ("gnm_prepare_median", C.c_int, [_P, _P]),
     ("gnm_classify", C.c_int,
      [_P, _P, C.POINTER(gnm_filter_params), C.POINTER(gnm_batch_soa), _P, C.c_int32]),
     ("gnm_ctx_timing", C.c_int, [_P, C.POINTER(gnm_timing)]),

@@ -88,6 +88,20 @@ struct gnm_ctx {
 
     // partials
     gnm::DevPartials P{};
+    // per-flow log of the current accumulation (round 2 of the median):
+    // entries (and, for wide registries, buckets) in per-launch slices
+    struct LogSlice {
+        size_t entry_off, count_off;
+        uint32_t warp_cap, regions;
+    };
+    unsigned int* d_log = nullptr;
+    unsigned int* d_logb = nullptr;
+    size_t log_cap = 0, log_used = 0;
+    bool log_wide = false;
+    unsigned int* d_counts = nullptr;
+    size_t counts_cap = 0, counts_used = 0;
+    std::vector<LogSlice> slices;
+    bool prepared = false; // K3a + K2b ran (gnm_prepare_median) for this accumulation
     uint32_t* d_scratch = nullptr; // hot-site plan: counts, site->slot, slot->site, counter
     uint32_t partial_cap = 0;
     bool accumulating = false;
@@ -155,6 +169,7 @@ gnm::DevParams dev_params(const gnm_ctx* c, const gnm_filter_params* p) {
     q.site_mask = c->table.packed ? gnm::kPackedSiteMask : 0x7FFFFFFFu;
     q.min_packets1 = std::max<uint32_t>(p->min_packets, 1);
     q.min_duration1 = std::max<uint32_t>(p->min_duration_ms, 1);
+    q.wide_log = c->P.n_sites >= gnm::kLogPackedSites;
     q.ablation = 0;
 #ifdef GNM_K2_ABLATION
     if (const char* a = std::getenv("GNM_K2_ABLATION")) q.ablation = static_cast<uint32_t>(std::atoi(a));
@@ -196,7 +211,12 @@ void ensure_partials(gnm_ctx* c, uint32_t n_sites) {
             cudaFree(c->P.sums);
             cudaFree(c->P.mn);
             cudaFree(c->P.mx);
-            cudaFree(c->P.hist);
+            cudaFree(c->P.coarse);
+            cudaFree(c->P.fine);
+            cudaFree(c->P.msb);
+            cudaFree(c->P.mrank);
+            cudaFree(c->P.cnt);
+            cudaFree(c->P.heavy_next);
             cudaFree(c->d_scratch);
             c->d_scratch = nullptr;
         }
@@ -205,7 +225,12 @@ void ensure_partials(gnm_ctx* c, uint32_t n_sites) {
         ck(cudaMalloc(&c->P.sums, (static_cast<size_t>(cap) * 4 + 4) * 8), "cudaMalloc(sums)");
         ck(cudaMalloc(&c->P.mn, static_cast<size_t>(cap) * 8), "cudaMalloc(min)");
         ck(cudaMalloc(&c->P.mx, static_cast<size_t>(cap) * 8), "cudaMalloc(max)");
-        ck(cudaMalloc(&c->P.hist, static_cast<size_t>(cap) * gnm::kHistStride * 4), "cudaMalloc(hist)");
+        ck(cudaMalloc(&c->P.coarse, static_cast<size_t>(cap) * gnm::kCoarse * 4), "cudaMalloc(coarse)");
+        ck(cudaMalloc(&c->P.fine, static_cast<size_t>(cap) * gnm::kFineW * 4), "cudaMalloc(fine)");
+        ck(cudaMalloc(&c->P.msb, static_cast<size_t>(cap) * 4), "cudaMalloc(msb)");
+        ck(cudaMalloc(&c->P.mrank, static_cast<size_t>(cap) * 4), "cudaMalloc(mrank)");
+        ck(cudaMalloc(&c->P.cnt, static_cast<size_t>(cap) * 8), "cudaMalloc(cnt)");
+        ck(cudaMalloc(&c->P.heavy_next, 4), "cudaMalloc(heavy)");
         const size_t scratch_words = 2 * static_cast<size_t>(cap) + gnm::kHotStride + 1;
         ck(cudaMalloc(&c->d_scratch, scratch_words * 4), "cudaMalloc(scratch)");
         ck(cudaMemsetAsync(c->d_scratch, 0, scratch_words * 4, c->stream), "cudaMemsetAsync");
@@ -283,6 +308,54 @@ int begin_accumulate(gnm_ctx* c, const gnm_registry* reg) {
     return GNM_OK;
 }
 
+gnm::DevLog slice_view(const gnm_ctx* c, const gnm_ctx::LogSlice& sl) {
+    gnm::DevLog lg;
+    lg.entries = c->d_log + sl.entry_off;
+    lg.buckets = c->log_wide ? c->d_logb + sl.entry_off : nullptr;
+    lg.counts = c->d_counts + sl.count_off;
+    lg.warp_cap = sl.warp_cap;
+    lg.regions = sl.regions;
+    return lg;
+}
+
+// Grow a device buffer of u32 preserving its first `used` words (stream-ordered).
+void grow_u32(gnm_ctx* c, unsigned int** buf, size_t* cap, size_t used, size_t need, const char* what) {
+    if (need <= *cap) return;
+    const size_t ncap = std::max(need, *cap + *cap / 2);
+    unsigned int* nb = nullptr;
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&nb), ncap * 4, c->stream), what);
+    if (*buf) {
+        if (used) ck(cudaMemcpyAsync(nb, *buf, used * 4, cudaMemcpyDeviceToDevice, c->stream), what);
+        ck(cudaFreeAsync(*buf, c->stream), what);
+    }
+    *buf = nb;
+    *cap = ncap;
+}
+
+// This launch's slice of the per-flow log: one region of warp_cap entries per
+// warp of the grid, the per-warp counts after the previous slices'.
+gnm::DevLog reserve_log(gnm_ctx* c, const gnm::LaunchCfg& cfg, const gnm::DevBatch& b) {
+    gnm_ctx::LogSlice sl;
+    sl.warp_cap = gnm::k2_warp_cap(cfg, b);
+    sl.regions = gnm::k2_regions(cfg);
+    sl.entry_off = c->log_used;
+    sl.count_off = c->counts_used;
+    const size_t need = static_cast<size_t>(sl.warp_cap) * sl.regions;
+    const bool wide = c->P.n_sites >= gnm::kLogPackedSites;
+    if (c->slices.empty()) c->log_wide = wide;
+    size_t bcap = c->log_cap;
+    grow_u32(c, &c->d_log, &c->log_cap, c->log_used, c->log_used + need, "log");
+    if (wide) {
+        if (!c->d_logb) bcap = 0;
+        grow_u32(c, &c->d_logb, &bcap, c->log_used, c->log_cap, "log buckets");
+    }
+    grow_u32(c, &c->d_counts, &c->counts_cap, c->counts_used, c->counts_used + sl.regions, "log counts");
+    c->log_used += need;
+    c->counts_used += sl.regions;
+    c->slices.push_back(sl);
+    return slice_view(c, sl);
+}
+
 void launch_k2_timed(gnm_ctx* c, const gnm::DevBatch& b, const gnm::DevParams& p) {
     if (b.n == 0) return;
     EventPair pe, ev;
@@ -307,7 +380,8 @@ void launch_k2_timed(gnm_ctx* c, const gnm::DevBatch& b, const gnm::DevParams& p
         ev = take_pair(c);
         ck(cudaEventRecord(ev.a, c->stream), "cudaEventRecord");
     }
-    ck(gnm::launch_k2(cfg, b, c->table, p, c->P, h, c->stream), "K2 launch");
+    const gnm::DevLog lg = reserve_log(c, cfg, b);
+    ck(gnm::launch_k2(cfg, b, c->table, p, c->P, h, lg, c->stream), "K2 launch");
     if (c->timing) {
         ck(cudaEventRecord(ev.b, c->stream), "cudaEventRecord");
         c->k2_pairs.push_back(ev);
@@ -411,6 +485,7 @@ int check_soa(const gnm_batch_soa* b) {
 int accumulate_soa(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* params,
                    const gnm_batch_soa* b) {
     if (int e = check_soa(b)) return e;
+    if (c->prepared) return fail(GNM_ERR_INVALID_ARGUMENT, "gnm_prepare_median already ran; finalize first");
     if (int e = begin_accumulate(c, reg)) return e;
     const gnm::DevParams p = dev_params(c, params);
     if (b->n == 0) return GNM_OK;
@@ -429,6 +504,7 @@ int accumulate_aos(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params*
                    const gnm_batch_aos* b) {
     if (!b) return fail(GNM_ERR_INVALID_ARGUMENT, "null batch");
     if (b->n && !b->records) return fail(GNM_ERR_INVALID_ARGUMENT, "null records");
+    if (c->prepared) return fail(GNM_ERR_INVALID_ARGUMENT, "gnm_prepare_median already ran; finalize first");
     if (int e = begin_accumulate(c, reg)) return e;
     const gnm::DevParams p = dev_params(c, params);
     if (b->n == 0) return GNM_OK;
@@ -440,6 +516,27 @@ int accumulate_aos(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params*
         load_and_run(c, true, cols, widths, 1, b->n, p);
     }
     return GNM_OK;
+}
+
+// Round 1 -> round 2 of the median: K3a finds every site's median
+// super-bucket from the (possibly all-reduced) coarse counts, K2b rebuilds
+// that super-bucket's fine counts from this context's log.
+void prepare_median(gnm_ctx* c) {
+    if (c->prepared) return;
+    ck(gnm::launch_k3a(c->device, c->P, c->stream), "K3a launch");
+    c->kernel_launches += 1;
+    for (const auto& sl : c->slices) {
+        ck(gnm::launch_k2b(c->device, c->P, slice_view(c, sl), c->stream), "K2b launch");
+        c->kernel_launches += 1;
+    }
+    c->prepared = true;
+}
+
+void clear_log(gnm_ctx* c) {
+    c->log_used = 0;
+    c->counts_used = 0;
+    c->slices.clear();
+    c->prepared = false;
 }
 
 int finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* r) {
@@ -457,7 +554,8 @@ int finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* r) {
     }
     const double thr = r->threshold_bps;
     const bool export_hist = r->histograms != nullptr;
-    ck(gnm::launch_k3(c->device, c->P, thr, c->d_out, export_hist ? 0 : 1, c->stream), "K3 launch");
+    prepare_median(c);
+    ck(gnm::launch_k3b(c->device, c->P, thr, c->d_out, 1, c->stream), "K3b launch");
     c->kernel_launches += 1;
     if (c->timing) {
         ck(cudaEventRecord(ev.b, c->stream), "cudaEventRecord");
@@ -467,27 +565,34 @@ int finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* r) {
                        cudaMemcpyDeviceToHost, c->stream),
        "cudaMemcpyAsync(D2H)");
     if (export_hist) {
+        // RateHistogram::buckets_ per site, rebuilt exactly from the log.
         const size_t bytes = static_cast<size_t>(n_sites) * gnm::kBuckets * 4;
         uint32_t* dense = nullptr;
         ck(cudaMallocAsync(reinterpret_cast<void**>(&dense), std::max<size_t>(bytes, 4), c->stream),
            "cudaMallocAsync(hist export)");
-        ck(gnm::launch_hist_export(c->P, dense, c->stream), "hist export");
-        c->kernel_launches += 1;
+        ck(cudaMemsetAsync(dense, 0, bytes, c->stream), "cudaMemsetAsync(hist export)");
+        for (const auto& sl : c->slices) {
+            ck(gnm::launch_hist_from_log(c->device, slice_view(c, sl), n_sites, dense, c->stream), "hist export");
+            c->kernel_launches += 1;
+        }
         ck(cudaMemcpyAsync(r->histograms, dense, bytes, cudaMemcpyDeviceToHost, c->stream),
            "cudaMemcpyAsync(D2H hist)");
         ck(cudaFreeAsync(dense, c->stream), "cudaFreeAsync(hist export)");
-        ck(gnm::launch_reset(c->device, c->P, c->stream), "reset launch");
-        c->kernel_launches += 1;
     }
+    clear_log(c);
     ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
     for (uint32_t s = 0; s < n_sites; ++s) {
         gnm_site_stats o = c->h_out[s];
         // stats_from (rate_engine.cpp:250): avg = (double(u128)/1e6)/count,
         // converted on the host exactly as the reference (libgcc RNE).
         if (o.flow_count) {
-            const unsigned __int128 u =
-                static_cast<unsigned __int128>(o.rate_ubps_hi) << 64 | o.rate_ubps_lo;
-            o.avg_bps = (static_cast<double>(u) / 1e6) / static_cast<double>(o.flow_count);
+            // Both conversions round to nearest-even, so the hardware u64 path
+            // equals libgcc's __floatuntidf whenever the sum fits 64 bits.
+            const double sum = o.rate_ubps_hi == 0
+                                   ? static_cast<double>(o.rate_ubps_lo)
+                                   : static_cast<double>(static_cast<unsigned __int128>(o.rate_ubps_hi) << 64 |
+                                                         o.rate_ubps_lo);
+            o.avg_bps = (sum / 1e6) / static_cast<double>(o.flow_count);
         }
         r->sites[s] = o;
     }
@@ -641,7 +746,15 @@ void gnm_ctx_destroy(gnm_ctx* c) {
     cudaFree(c->P.sums);
     cudaFree(c->P.mn);
     cudaFree(c->P.mx);
-    cudaFree(c->P.hist);
+    cudaFree(c->P.coarse);
+    cudaFree(c->P.fine);
+    cudaFree(c->P.msb);
+    cudaFree(c->P.mrank);
+    cudaFree(c->P.cnt);
+    cudaFree(c->P.heavy_next);
+    cudaFree(c->d_log);
+    cudaFree(c->d_logb);
+    cudaFree(c->d_counts);
     cudaFree(c->d_scratch);
     cudaFree(c->d_out);
     if (c->h_out) cudaFreeHost(c->h_out);
@@ -721,6 +834,24 @@ int gnm_finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* result) {
     return guarded([&] { return finalize(c, reg, result); });
 }
 
+int gnm_prepare_median(gnm_ctx* c, const gnm_registry* reg) {
+    if (!c || !reg) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx/registry");
+    return guarded([&] {
+        if (int e = begin_accumulate(c, reg)) return e;
+        EventPair ev;
+        if (c->timing) {
+            ev = take_pair(c);
+            ck(cudaEventRecord(ev.a, c->stream), "cudaEventRecord");
+        }
+        prepare_median(c);
+        if (c->timing) {
+            ck(cudaEventRecord(ev.b, c->stream), "cudaEventRecord");
+            c->k3_pairs.push_back(ev);
+        }
+        return static_cast<int>(GNM_OK);
+    });
+}
+
 int gnm_reset(gnm_ctx* c) {
     if (!c) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx");
     return guarded([&] {
@@ -730,6 +861,7 @@ int gnm_reset(gnm_ctx* c) {
             c->kernel_launches += 1;
             ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
         }
+        clear_log(c);
         drain_pairs(c, c->k2_pairs);
         drain_pairs(c, c->plan_pairs);
         drain_pairs(c, c->k3_pairs);
@@ -766,10 +898,12 @@ int gnm_get_partials(gnm_ctx* c, const gnm_registry* reg, gnm_partials* out) {
         out->sums = reinterpret_cast<uint64_t*>(c->P.sums);
         out->min_bps = reinterpret_cast<double*>(c->P.mn);
         out->max_bps = reinterpret_cast<double*>(c->P.mx);
-        out->hist = c->P.hist;
+        out->coarse = c->P.coarse;
+        out->fine = c->P.fine;
         out->n_sites = c->P.n_sites;
         out->sums_count = static_cast<uint64_t>(c->P.n_sites) * 4 + 4;
-        out->hist_count = static_cast<uint64_t>(c->P.n_sites) * gnm::kHistStride;
+        out->coarse_count = static_cast<uint64_t>(c->P.n_sites) * gnm::kCoarse;
+        out->fine_count = static_cast<uint64_t>(c->P.n_sites) * gnm::kFineW;
         return static_cast<int>(GNM_OK);
     });
 }

@@ -50,7 +50,16 @@ constexpr uint32_t kWarps = kK2Block / 32;
 constexpr uint64_t kCtaRecords = 65536 - 64;
 constexpr uint32_t kCtaTiles = static_cast<uint32_t>(kCtaRecords / 64) - 1; // + a < 64-record tail
 constexpr uint32_t kQueue = 96; // per-warp queue capacity: < 32 left + 2 x 32 pushed
-constexpr size_t kHotBytes = kHotStride * (5 * 4 + 2 * 8);
+// The top kCoarseSlots hot slots also keep their coarse counts in shared
+// memory, two u16 super-buckets per u32 (a CTA's < 2^16 records cannot
+// carry one half into the other).
+constexpr uint32_t kCoarseSlots = 32;
+// K2b's shared-memory fine rows for the heaviest sites.
+constexpr uint32_t kHeavy = 64;
+constexpr uint32_t kHeavyNone = 0xFFFFFFu;
+constexpr uint64_t kHeavyMin = 1u << 16;
+constexpr uint32_t kCoarseWords = (kCoarse + 1) / 2;
+constexpr size_t kHotBytes = kHotStride * (5 * 4 + 2 * 8) + kCoarseSlots * kCoarseWords * 4;
 constexpr size_t kSmemMax = 227 * 1024;
 constexpr size_t kQueueBytes = kWarps * kQueue * 16;
 constexpr size_t kSmemTableMax = kSmemMax - kHotBytes - kQueueBytes - 1024;
@@ -151,6 +160,7 @@ struct HotSmem {
     uint32_t* limb; // [5][kHotStride]: oct lo16, oct hi16, ubps bits 0-15, 16-31, 32-47
     unsigned long long* mn;
     unsigned long long* mx;
+    uint32_t* coarse; // [kCoarseSlots][kCoarseWords], slot 1 first
 };
 
 __device__ __forceinline__ HotSmem hot_smem(uint32_t table_words_in_smem) {
@@ -159,6 +169,7 @@ __device__ __forceinline__ HotSmem hot_smem(uint32_t table_words_in_smem) {
     h.limb = base;
     h.mn = reinterpret_cast<unsigned long long*>(base + 5 * kHotStride);
     h.mx = h.mn + kHotStride;
+    h.coarse = reinterpret_cast<uint32_t*>(h.mx + kHotStride);
     return h;
 }
 
@@ -169,6 +180,7 @@ __device__ __forceinline__ void hot_init(const HotSmem& h) {
         h.mn[i] = kMinInitBits;
         h.mx[i] = kMaxInitBits;
     }
+    for (uint32_t i = threadIdx.x; i < kCoarseSlots * kCoarseWords; i += blockDim.x) h.coarse[i] = 0;
 }
 
 // ---- per-flow arithmetic -----------------------------------------------------
@@ -295,30 +307,34 @@ __device__ __forceinline__ uint32_t resolve(const uint32_t* __restrict__ gt, uin
 
 // RateHistogram::add (rate_engine.cpp:9-23) for one Forward flow, as
 // order-independent reductions:
-//   hist[site][bucket] += 1                              (u32, as the reference)
-//   octets and micro-bps sums                            exact integers
+//   coarse[site][bucket >> 6] += 1   (+ a log entry: the exact bucket for round 2)
+//   octets and micro-bps sums        exact integers
 //   min/max of the f64 rate via u64 min/max on the bit pattern (rates > 0,
 //   SURVEY.md §8a' #8)
 // Hot sites: non-returning shared adds of 16-bit limbs (micro-bps >= 2^48 go
-// to L2 instead); min/max go to L2 only when the slot's cached bounds say
-// they can win. Cold sites: straight to L2 (RED).
+// to L2 instead), coarse counts of the top kCoarseSlots slots in shared
+// memory too; min/max go to L2 only when the slot's cached bounds say they
+// can win. Cold sites: straight to L2 (RED).
+// Returns the site (kNone: Unmatched at /24) and the bucket.
 template <bool kSmem, bool kHot>
-__device__ __forceinline__ void accumulate(uint32_t code, uint32_t oct, uint64_t dur,
-                                           const uint32_t* __restrict__ gt, const DevParams& p,
-                                           const DevPartials& P, const HotSmem& h, Ctr& c) {
+__device__ __forceinline__ uint32_t accumulate(uint32_t code, uint32_t oct, uint64_t dur,
+                                               const uint32_t* __restrict__ gt, const DevParams& p,
+                                               const DevPartials& P, const HotSmem& h, Ctr& c,
+                                               uint32_t& bucket) {
+    bucket = 0;
     const uint32_t v = resolve<kSmem>(gt, code);
     if (v == kNone) {
         ++c.unm;
-        return;
+        return kNone;
     }
     ++c.fwd;
+    const uint32_t site = v & p.site_mask;
 #ifdef GNM_K2_ABLATION
     if (p.ablation == 2) {
         c.unm ^= v ^ oct ^ static_cast<uint32_t>(dur);
-        return;
+        return site;
     }
 #endif
-    const uint32_t site = v & p.site_mask;
     const uint32_t slot = kHot ? (v >> 20) & 0x7FFu : 0u;
     unsigned long long cmn = 0, cmx = ~0ull;
     if (kHot && slot) { // issued early: the latency hides behind the division
@@ -330,16 +346,21 @@ __device__ __forceinline__ void accumulate(uint32_t code, uint32_t oct, uint64_t
     uint64_t lo, hi;
     ubps_of(oct, dur, rate, lo, hi);
     const unsigned long long rb = static_cast<unsigned long long>(__double_as_longlong(rate));
+    bucket = bucket_of_ubps(lo, hi);
+    const uint32_t sb = bucket >> 6;
 #ifdef GNM_K2_ABLATION
-    // Measurement builds only (tools/ablation.sh): 3 = no reductions,
-    // 4 = the histogram RED only. Results are wrong in these modes.
+    // Measurement builds only (tools/ablation.sh): 3 = no reductions at all,
+    // 4 = coarse counts (and the log) only. Results are wrong in these modes.
     if (p.ablation == 3 || p.ablation == 4) {
-        if (p.ablation == 4) red_add(P.hist + hist_index(site, bucket_of_ubps(lo, hi), P.n_sites), 1u);
-        c.unm ^= static_cast<uint32_t>(lo ^ hi ^ rb) ^ bucket_of_ubps(lo, hi) ^ static_cast<uint32_t>(cmn ^ cmx);
-        return;
+        if (p.ablation == 4) {
+            if (kHot && slot && slot <= kCoarseSlots)
+                red_add_shared(h.coarse + (slot - 1) * kCoarseWords + (sb >> 1), (sb & 1u) ? 0x10000u : 1u);
+            else red_add(P.coarse + static_cast<size_t>(sb) * P.n_sites + site, 1u);
+        }
+        c.unm ^= static_cast<uint32_t>(lo ^ hi ^ rb) ^ static_cast<uint32_t>(cmn ^ cmx);
+        return p.ablation == 3 ? kNone : site;
     }
 #endif
-    red_add(P.hist + hist_index(site, bucket_of_ubps(lo, hi), P.n_sites), 1u);
     unsigned long long* s = P.sums + static_cast<size_t>(site) * 4;
     if (kHot && slot) {
         uint32_t* l = h.limb + slot;
@@ -354,6 +375,10 @@ __device__ __forceinline__ void accumulate(uint32_t code, uint32_t oct, uint64_t
             red_add(s + 2, lo >> 32);
             if (hi) red_add(s + 3, hi);
         }
+        if (slot <= kCoarseSlots)
+            red_add_shared(h.coarse + (slot - 1) * kCoarseWords + (sb >> 1), (sb & 1u) ? 0x10000u : 1u);
+        else
+            red_add(P.coarse + static_cast<size_t>(sb) * P.n_sites + site, 1u);
         // min/max: the slot's cached bounds filter the global reductions. The
         // cache is written with plain stores AFTER the RED, so it only ever
         // holds rates whose RED was issued; a lost race loosens the filter
@@ -367,6 +392,7 @@ __device__ __forceinline__ void accumulate(uint32_t code, uint32_t oct, uint64_t
             h.mx[slot] = rb;
         }
     } else {
+        red_add(P.coarse + static_cast<size_t>(sb) * P.n_sites + site, 1u);
         red_add(s + 0, static_cast<unsigned long long>(oct));
         red_add(s + 1, lo & 0xFFFFFFFFull);
         if (lo >> 32) red_add(s + 2, lo >> 32);
@@ -374,16 +400,22 @@ __device__ __forceinline__ void accumulate(uint32_t code, uint32_t oct, uint64_t
         red_min(P.mn + site, rb);
         red_max(P.mx + site, rb);
     }
+    return site;
 }
 
 // Warp-level stream compaction of candidates: lanes append {code, octets,
 // duration} to the warp's shared queue (ballot + popc, one STS.128), and
 // every time 32 are queued the whole warp drains one per lane (stage B), so
 // the lookup tail and the per-flow arithmetic never run with the ~50% lane
-// occupancy the class mix would otherwise leave them.
+// occupancy the class mix would otherwise leave them. Each drained item
+// leaves one log entry (a 128-byte coalesced streaming store per drain) in
+// the warp's region of the launch's log.
 struct WarpQueue {
     uint4* q;
-    uint32_t n; // warp-uniform fill
+    uint32_t n;         // warp-uniform fill
+    uint32_t pos;       // warp-uniform log entries written
+    unsigned int* log;  // this warp's log region
+    unsigned int* logb; // wide registries: bucket column of the region
 };
 
 __device__ __forceinline__ void push(uint32_t code, uint32_t oct, uint64_t dur, WarpQueue& wq,
@@ -396,6 +428,15 @@ __device__ __forceinline__ void push(uint32_t code, uint32_t oct, uint64_t dur, 
     wq.n += __popc(m);
 }
 
+__device__ __forceinline__ void log_entry(WarpQueue& wq, uint32_t lane, uint32_t site, uint32_t bucket) {
+    if (wq.logb) {
+        __stcs(wq.log + wq.pos + lane, site == kNone ? kLogSkip : site);
+        __stcs(wq.logb + wq.pos + lane, bucket);
+    } else {
+        __stcs(wq.log + wq.pos + lane, site == kNone ? kLogSkip : site << kLogSiteShift | bucket);
+    }
+}
+
 template <bool kSmem, bool kHot>
 __device__ __forceinline__ void drain_full(WarpQueue& wq, uint32_t lane,
                                            const uint32_t* __restrict__ gt, const DevParams& p,
@@ -405,7 +446,11 @@ __device__ __forceinline__ void drain_full(WarpQueue& wq, uint32_t lane,
         const uint4 x = wq.q[wq.n - 32 + lane];
         wq.n -= 32;
         __syncwarp();
-        accumulate<kSmem, kHot>(x.x, x.y, static_cast<uint64_t>(x.w) << 32 | x.z, gt, p, P, h, c);
+        uint32_t bucket;
+        const uint32_t site =
+            accumulate<kSmem, kHot>(x.x, x.y, static_cast<uint64_t>(x.w) << 32 | x.z, gt, p, P, h, c, bucket);
+        log_entry(wq, lane, site, bucket);
+        wq.pos += 32;
     }
 }
 
@@ -416,8 +461,12 @@ __device__ __forceinline__ void drain_rest(WarpQueue& wq, uint32_t lane,
     __syncwarp();
     if (lane < wq.n) {
         const uint4 x = wq.q[lane];
-        accumulate<kSmem, kHot>(x.x, x.y, static_cast<uint64_t>(x.w) << 32 | x.z, gt, p, P, h, c);
+        uint32_t bucket;
+        const uint32_t site =
+            accumulate<kSmem, kHot>(x.x, x.y, static_cast<uint64_t>(x.w) << 32 | x.z, gt, p, P, h, c, bucket);
+        log_entry(wq, lane, site, bucket);
     }
+    wq.pos += wq.n;
     wq.n = 0;
 }
 
@@ -435,9 +484,10 @@ __device__ __forceinline__ void flush_tallies(const Ctr& t, unsigned long long* 
 }
 
 // One flush per CTA. The limb sums are exact (< 2^32 each, see kCtaRecords)
-// and land in the global limbs K3 reassembles: sums[1] takes the low 32 bits
-// of every flow's micro-bps (so it stays below count * 2^32), sums[2] the
-// bits above. (min/max went to L2 during the run.)
+// and land in the global limbs K3b reassembles: sums[1] takes the low 32
+// bits of every flow's micro-bps (so it stays below count * 2^32), sums[2]
+// the bits above. Coarse counts of the top slots: each u16 half to its
+// super-bucket. (min/max went to L2 during the run.)
 __device__ __forceinline__ void hot_flush(const HotSmem& h, const DevHot& hot, const DevPartials& P) {
     for (uint32_t slot = 1 + threadIdx.x; slot <= hot.n_slots; slot += blockDim.x) {
         const uint32_t* l = h.limb + slot;
@@ -445,11 +495,21 @@ __device__ __forceinline__ void hot_flush(const HotSmem& h, const DevHot& hot, c
         const uint64_t u01 = static_cast<uint64_t>(l[2 * kHotStride]) +
                              (static_cast<uint64_t>(l[3 * kHotStride]) << 16);
         const uint32_t u2 = l[4 * kHotStride];
+        if (oct == 0) continue; // untouched: every Forward flow has >= 1 octet
         const uint32_t site = __ldg(hot.hot_site + slot);
         unsigned long long* s = P.sums + static_cast<size_t>(site) * 4;
-        if (oct) red_add(s + 0, oct);
+        red_add(s + 0, oct);
         if (u01) red_add(s + 1, u01);
         if (u2) red_add(s + 2, static_cast<unsigned long long>(u2));
+    }
+    const uint32_t words = min(hot.n_slots, kCoarseSlots) * kCoarseWords;
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) {
+        const uint32_t w = h.coarse[i];
+        if (!w) continue;
+        const uint32_t site = __ldg(hot.hot_site + 1 + i / kCoarseWords);
+        const uint32_t sb = 2 * (i % kCoarseWords);
+        if (w & 0xFFFFu) red_add(P.coarse + static_cast<size_t>(sb) * P.n_sites + site, w & 0xFFFFu);
+        if (w >> 16) red_add(P.coarse + static_cast<size_t>(sb + 1) * P.n_sites + site, w >> 16);
     }
 }
 
@@ -503,19 +563,23 @@ __device__ __forceinline__ void run_scalar(const DevBatch& b, uint64_t first, ui
 
 // ---- K2 ----------------------------------------------------------------------
 // Block prologue: registry table and hot slots into shared memory, the
-// warp's queue after them.
+// warp's queue after them, the warp's log region.
 template <bool kSmem, bool kHot>
 __device__ __forceinline__ void k2_prologue(const uint32_t* __restrict__ gt, uint32_t table_words,
-                                            HotSmem& h, WarpQueue& wq) {
+                                            const DevLog& L, HotSmem& h, WarpQueue& wq) {
     load_table<kSmem>(gt, table_words);
     const uint32_t smem_words = kSmem ? table_words : 0u;
     if constexpr (kHot) {
         h = hot_smem(smem_words);
         hot_init(h);
     }
-    wq.q = reinterpret_cast<uint4*>(g_smem + smem_words + (kHot ? kHotBytes / 4 : 0u)) +
-           (threadIdx.x >> 5) * kQueue;
+    const uint32_t warp = threadIdx.x >> 5;
+    wq.q = reinterpret_cast<uint4*>(g_smem + smem_words + (kHot ? kHotBytes / 4 : 0u)) + warp * kQueue;
     wq.n = 0;
+    wq.pos = 0;
+    const size_t region = static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp;
+    wq.log = L.entries + region * L.warp_cap;
+    wq.logb = L.buckets ? L.buckets + region * L.warp_cap : nullptr;
     __syncthreads();
 }
 
@@ -523,9 +587,10 @@ template <bool kSmem, bool kHot>
 __device__ __forceinline__ void k2_epilogue(Ctr& t, WarpQueue& wq, uint32_t lane,
                                             const uint32_t* __restrict__ gt, const DevParams& p,
                                             const DevPartials& P, const HotSmem& h,
-                                            const DevHot& hot) {
+                                            const DevHot& hot, const DevLog& L) {
     drain_full<kSmem, kHot>(wq, lane, gt, p, P, h, t);
     drain_rest<kSmem, kHot>(wq, lane, gt, p, P, h, t);
+    if (lane == 0) L.counts[static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)] = wq.pos;
     flush_tallies(t, P.sums + static_cast<size_t>(P.n_sites) * 4);
     if constexpr (kHot) {
         __syncthreads();
@@ -542,10 +607,10 @@ __device__ __forceinline__ void k2_epilogue(Ctr& t, WarpQueue& wq, uint32_t lane
 template <bool kSmem, bool kHot>
 __global__ void __launch_bounds__(kK2Block, 2) k2_soa(DevBatch b, const uint32_t* __restrict__ gt,
                                                     uint32_t table_words, DevParams p,
-                                                    DevPartials P, DevHot hot) {
+                                                    DevPartials P, DevHot hot, DevLog L) {
     HotSmem h{};
     WarpQueue wq;
-    k2_prologue<kSmem, kHot>(gt, table_words, h, wq);
+    k2_prologue<kSmem, kHot>(gt, table_words, L, h, wq);
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warp = threadIdx.x >> 5;
     const DevSoA& c = b.soa;
@@ -593,7 +658,7 @@ __global__ void __launch_bounds__(kK2Block, 2) k2_soa(DevBatch b, const uint32_t
     }
     if (blockIdx.x == gridDim.x - 1 && warp == 0)
         run_scalar<1, kSmem, kHot>(b, tiles << 6, c.n, 32, lane, gt, p, P, h, t, wq);
-    k2_epilogue<kSmem, kHot>(t, wq, lane, gt, p, P, h, hot);
+    k2_epilogue<kSmem, kHot>(t, wq, lane, gt, p, P, h, hot, L);
 }
 
 // Variant: no register double-buffering. Each warp asks the TMA engine to
@@ -609,10 +674,10 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) 
 template <bool kSmem, bool kHot>
 __global__ void __launch_bounds__(kK2Block, 2) k2_soa_pf(DevBatch b, const uint32_t* __restrict__ gt,
                                                        uint32_t table_words, DevParams p,
-                                                       DevPartials P, DevHot hot) {
+                                                       DevPartials P, DevHot hot, DevLog L) {
     HotSmem h{};
     WarpQueue wq;
-    k2_prologue<kSmem, kHot>(gt, table_words, h, wq);
+    k2_prologue<kSmem, kHot>(gt, table_words, L, h, wq);
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warp = threadIdx.x >> 5;
     const DevSoA& c = b.soa;
@@ -660,7 +725,7 @@ __global__ void __launch_bounds__(kK2Block, 2) k2_soa_pf(DevBatch b, const uint3
     }
     if (blockIdx.x == gridDim.x - 1 && warp == 0)
         run_scalar<1, kSmem, kHot>(b, tiles << 6, c.n, 32, lane, gt, p, P, h, t, wq);
-    k2_epilogue<kSmem, kHot>(t, wq, lane, gt, p, P, h, hot);
+    k2_epilogue<kSmem, kHot>(t, wq, lane, gt, p, P, h, hot, L);
 }
 
 // ---- K2, TMA-staged variant ----------------------------------------------------
@@ -732,10 +797,10 @@ __device__ __forceinline__ void async_tile(unsigned char* st, const char* col, u
 template <bool kSmem, bool kHot, bool kBulk>
 __global__ void __launch_bounds__(kTmaBlock, 1) k2_tma(DevBatch b, const uint32_t* __restrict__ gt,
                                                      uint32_t table_words, DevParams p,
-                                                     DevPartials P, DevHot hot) {
+                                                     DevPartials P, DevHot hot, DevLog L) {
     HotSmem h{};
     WarpQueue wq;
-    k2_prologue<kSmem, kHot>(gt, table_words, h, wq);
+    k2_prologue<kSmem, kHot>(gt, table_words, L, h, wq);
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t smem_words = kSmem ? table_words : 0u;
@@ -806,7 +871,7 @@ __global__ void __launch_bounds__(kTmaBlock, 1) k2_tma(DevBatch b, const uint32_
     }
     if (blockIdx.x == gridDim.x - 1 && warp == 0)
         run_scalar<1, kSmem, kHot>(b, tiles << 6, c.n, 32, lane, gt, p, P, h, t, wq);
-    k2_epilogue<kSmem, kHot>(t, wq, lane, gt, p, P, h, hot);
+    k2_epilogue<kSmem, kHot>(t, wq, lane, gt, p, P, h, hot, L);
 }
 
 // Other layouts: unaligned SoA (1), AoS 64-byte rows with vector (2) or
@@ -815,16 +880,16 @@ __global__ void __launch_bounds__(kTmaBlock, 1) k2_tma(DevBatch b, const uint32_
 template <int kLayout, bool kSmem, bool kHot>
 __global__ void __launch_bounds__(kK2Block, 2) k2_gen(DevBatch b, const uint32_t* __restrict__ gt,
                                                     uint32_t table_words, DevParams p,
-                                                    DevPartials P, DevHot hot) {
+                                                    DevPartials P, DevHot hot, DevLog L) {
     HotSmem h{};
     WarpQueue wq;
-    k2_prologue<kSmem, kHot>(gt, table_words, h, wq);
+    k2_prologue<kSmem, kHot>(gt, table_words, L, h, wq);
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t r0 = b.n * blockIdx.x / gridDim.x, r1 = b.n * (blockIdx.x + 1) / gridDim.x;
     Ctr t;
     run_scalar<kLayout, kSmem, kHot>(b, r0 + (threadIdx.x >> 5) * 32, r1, kK2Block, lane, gt, p, P, h,
                                      t, wq);
-    k2_epilogue<kSmem, kHot>(t, wq, lane, gt, p, P, h, hot);
+    k2_epilogue<kSmem, kHot>(t, wq, lane, gt, p, P, h, hot, L);
 }
 
 // ---- K1: hot-site plan ------------------------------------------------------
@@ -863,7 +928,7 @@ __global__ void __launch_bounds__(kSelectBlock) k_hot_select(uint32_t* __restric
                                                              uint32_t* __restrict__ hot_site) {
     __shared__ uint32_t bins[kCountBins];
     __shared__ uint32_t part[kSelectBlock];
-    __shared__ uint32_t cut, next;
+    __shared__ uint32_t cut, cut_a, next, next_a;
     for (uint32_t i = threadIdx.x; i < kCountBins; i += blockDim.x) bins[i] = 0;
     if (threadIdx.x == 0) next = 0;
     __syncthreads();
@@ -884,26 +949,43 @@ __global__ void __launch_bounds__(kSelectBlock) k_hot_select(uint32_t* __restric
         part[threadIdx.x] += x;
         __syncthreads();
     }
-    if (threadIdx.x == 0) cut = 0xFFFFFFFFu;
+    if (threadIdx.x == 0) {
+        cut = 0xFFFFFFFFu;
+        cut_a = 0xFFFFFFFFu;
+        next_a = 0;
+    }
     __syncthreads();
     {
-        // The cut is the lowest bin b with suffix(b) <= kHotSlots.
+        // cut: the lowest bin b with suffix(b) <= kHotSlots; cut_a the same
+        // for the kCoarseSlots slots that also keep coarse counts in smem.
         uint32_t suffix = threadIdx.x + 1 < kSelectBlock ? part[threadIdx.x + 1] : 0u;
         for (int k = kCountBins / kSelectBlock - 1; k >= 0; --k) {
             suffix += bins[i0 + k];
             if (suffix <= kHotSlots) atomicMin(&cut, i0 + k);
+            if (suffix <= kCoarseSlots) atomicMin(&cut_a, i0 + k);
         }
     }
     __syncthreads();
-    const uint32_t t = max(cut, thr);
+    const uint32_t t = max(max(cut, thr), 1u);
+    const uint32_t ta = max(cut_a, t);
+    // Slots 1..n_a: the top sites (count >= ta); the rest follow them.
+    uint32_t n_a = 0;
+    for (uint32_t b = threadIdx.x; b < kCountBins; b += blockDim.x)
+        if (b >= ta) n_a += bins[b];
+    n_a = __reduce_add_sync(0xFFFFFFFFu, n_a);
+    if ((threadIdx.x & 31u) == 0 && n_a) atomicAdd(&next_a, n_a);
+    __syncthreads();
+    const uint32_t base_b = next_a;
+    __syncthreads();
+    if (threadIdx.x == 0) next_a = 0;
+    __syncthreads();
     for (uint32_t s = threadIdx.x; s < n_sites; s += blockDim.x) {
         const uint32_t c = cnt[s];
         cnt[s] = 0;
         uint32_t slot = 0;
-        if (c >= t && c > 0) {
-            slot = atomicAdd(&next, 1u) + 1;
-            hot_site[slot] = s;
-        }
+        if (c >= ta) slot = atomicAdd(&next_a, 1u) + 1;
+        else if (c >= t) slot = base_b + atomicAdd(&next, 1u) + 1;
+        if (slot) hot_site[slot] = s;
         site_slot[s] = slot;
     }
 }
@@ -957,79 +1039,167 @@ __global__ void __launch_bounds__(kK2Block) k_classify(DevSoA b, const uint32_t*
     }
 }
 
-// ---- K3: per-site synthesis --------------------------------------------------
-__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+// ---- K3: per-site synthesis (two-round exact median) ---------------------------
+// K3a, thread per site (coalesced over the sb-major coarse array): the flow
+// count and the super-bucket holding the lower median, i.e. the first
+// super-bucket whose cumulative count reaches ceil(count/2)
+// (RateHistogram::median_bps, rate_engine.cpp:42-58), and the median's rank
+// inside it. The 157 counts are loaded in unrolled batches (independent
+// loads in flight) and kept in registers between the two passes.
+__global__ void __launch_bounds__(128) k3a_median_sb(DevPartials P) {
+    const uint32_t n = P.n_sites;
+    for (uint32_t site = blockIdx.x * blockDim.x + threadIdx.x; site < n; site += gridDim.x * blockDim.x) {
+        const unsigned int* col = P.coarse + site;
+        uint64_t cnt = 0;
+#pragma unroll 16
+        for (uint32_t sb = 0; sb < kCoarse; ++sb) cnt += __ldcg(col + static_cast<size_t>(sb) * n);
+        uint32_t msb = kLogSkip, rank = 0;
+        if (cnt) {
+            const uint64_t target = (cnt + 1) / 2;
+            uint64_t cum = 0;
+            for (uint32_t sb0 = 0; sb0 < kCoarse; sb0 += 8) {
+                uint32_t c[8];
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, off);
-    return v;
+                for (uint32_t u = 0; u < 8; ++u)
+                    c[u] = sb0 + u < kCoarse ? __ldcg(col + static_cast<size_t>(sb0 + u) * n) : 0u;
+                uint64_t part = 0;
+#pragma unroll
+                for (uint32_t u = 0; u < 8; ++u) part += c[u];
+                if (cum + part < target) {
+                    cum += part;
+                    continue;
+                }
+#pragma unroll
+                for (uint32_t u = 0; u < 8; ++u) {
+                    if (cum + c[u] >= target) {
+                        msb = sb0 + u;
+                        rank = static_cast<uint32_t>(target - cum);
+                        break;
+                    }
+                    cum += c[u];
+                }
+                break;
+            }
+        }
+        // Heavy sites (>= kHeavyMin flows) get one of kHeavy shared-memory
+        // fine rows in K2b: their median super-bucket draws thousands of
+        // same-address reductions otherwise.
+        uint32_t hidx = kHeavyNone;
+        if (cnt >= kHeavyMin) {
+            const uint32_t k = atomicAdd(P.heavy_next, 1u);
+            if (k < kHeavy) hidx = k;
+        }
+        P.msb[site] = msb | hidx << 8;
+        P.mrank[site] = rank;
+        P.cnt[site] = cnt;
+    }
 }
 
-// One warp per site. The site's rates all lie in [min, max], so its histogram
-// is non-zero only on [bucket(min), bucket(max)] (bucket_index is monotone):
-// K3 scans (and, with reset, clears) just that range.
-__global__ void __launch_bounds__(256) k3_finalize(DevPartials P, double threshold,
-                                                   gnm_site_stats* __restrict__ out,
-                                                   unsigned long long* __restrict__ tallies_out,
-                                                   int write_out, int reset) {
+// K2b: one launch's log, warp per region, 8 entries per lane in flight: the
+// entries that fall into their site's median super-bucket count into its 64
+// fine buckets -- in shared memory for the heavy sites (flushed once per
+// CTA, persistent grid), with L2 reductions for the rest.
+__global__ void __launch_bounds__(512, 2) k2b_fine(DevPartials P, DevLog L) {
+    __shared__ uint32_t hf[kHeavy * kFineW];
+    __shared__ uint32_t hsite[kHeavy];
+    for (uint32_t i = threadIdx.x; i < kHeavy * kFineW; i += blockDim.x) hf[i] = 0;
+    __syncthreads();
     const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    constexpr uint32_t kU = 16;
+    for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < L.regions; r += nwarps) {
+        const uint32_t cnt = L.counts[r];
+        const unsigned int* e = L.entries + static_cast<size_t>(r) * L.warp_cap;
+        const unsigned int* eb = L.buckets ? L.buckets + static_cast<size_t>(r) * L.warp_cap : nullptr;
+        for (uint32_t base = 0; base < cnt; base += 32 * kU) {
+            uint32_t x[kU], b[kU];
+#pragma unroll
+            for (uint32_t u = 0; u < kU; ++u) {
+                const uint32_t i = base + u * 32 + lane;
+                x[u] = i < cnt ? __ldcs(e + i) : kLogSkip;
+            }
+            if (eb) {
+#pragma unroll
+                for (uint32_t u = 0; u < kU; ++u) {
+                    const uint32_t i = base + u * 32 + lane;
+                    b[u] = i < cnt ? __ldcs(eb + i) : 0u;
+                }
+            }
+            uint32_t site[kU], m[kU];
+#pragma unroll
+            for (uint32_t u = 0; u < kU; ++u) {
+                site[u] = eb ? x[u] : x[u] >> kLogSiteShift;
+                if (!eb) b[u] = x[u] & ((1u << kLogSiteShift) - 1u);
+                m[u] = x[u] == kLogSkip ? kLogSkip : __ldg(P.msb + site[u]);
+            }
+#pragma unroll
+            for (uint32_t u = 0; u < kU; ++u) {
+                if (x[u] == kLogSkip || (b[u] >> 6) != (m[u] & 0xFFu)) continue;
+                const uint32_t h = m[u] >> 8;
+                if (h != kHeavyNone) {
+                    red_add_shared(hf + h * kFineW + (b[u] & 63u), 1u);
+                    hsite[h] = site[u]; // every writer stores the same value
+                } else {
+                    red_add(P.fine + static_cast<size_t>(site[u]) * kFineW + (b[u] & 63u), 1u);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < kHeavy * kFineW; i += blockDim.x)
+        if (hf[i]) red_add(P.fine + static_cast<size_t>(hsite[i / kFineW]) * kFineW + (i % kFineW), hf[i]);
+}
+
+// K3b, thread per site: count (coarse), the exact median bucket from the
+// fine counts, stats_from (rate_engine.cpp:242-253: median clamped into
+// [min, max]) and the flag (monitor.cpp:22); optionally resets the sums and
+// min/max (the launcher clears coarse and fine).
+__global__ void __launch_bounds__(128) k3b_finalize(DevPartials P, double threshold,
+                                                    gnm_site_stats* __restrict__ out,
+                                                    unsigned long long* __restrict__ tallies_out,
+                                                    int write_out, int reset) {
+    const uint32_t n = P.n_sites;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        unsigned long long* t = P.sums + static_cast<size_t>(P.n_sites) * 4;
+        unsigned long long* t = P.sums + static_cast<size_t>(n) * 4;
         if (write_out)
             for (int i = 0; i < 4; ++i) tallies_out[i] = t[i];
         if (reset)
             for (int i = 0; i < 4; ++i) t[i] = 0;
     }
-    for (uint32_t site = warp; site < P.n_sites; site += nwarps) {
-        const unsigned long long mxb = P.mx[site];
-        const unsigned long long mnb = P.mn[site];
-        if (mxb == 0) { // no Forward flow: absent from result.sites
-            if (write_out && lane == 0) {
-                gnm_site_stats z = {};
-                out[site] = z;
-            }
-            continue;
-        }
-        const double mn = __longlong_as_double(static_cast<long long>(mnb));
-        const double mx = __longlong_as_double(static_cast<long long>(mxb));
-        const uint32_t b0 = bucket_of(mn), b1 = bucket_of(mx);
-        unsigned int* hist = P.hist;
-        const uint32_t n = P.n_sites;
+    for (uint32_t site = blockIdx.x * blockDim.x + threadIdx.x; site < n; site += gridDim.x * blockDim.x) {
+        const uint64_t cnt = P.cnt[site];
+        uint4* fine = reinterpret_cast<uint4*>(P.fine + static_cast<size_t>(site) * kFineW);
+        unsigned long long* s = P.sums + static_cast<size_t>(site) * 4;
         if (write_out) {
-            uint64_t c = 0;
-            for (uint32_t b = b0 + lane; b <= b1; b += 32) c += hist[hist_index(site, b, n)];
-            c = warp_sum_u64(c);
-            // median_bps (rate_engine.cpp:42-58): first k with cumulative >= ceil(c/2).
-            const uint64_t target = (c + 1) / 2;
-            uint64_t cum = 0;
-            uint32_t k = kBuckets - 1;
-            for (uint32_t base = b0; base <= b1; base += 32) {
-                const uint32_t b = base + lane;
-                uint64_t x = b <= b1 ? hist[hist_index(site, b, n)] : 0u;
+            gnm_site_stats o = {};
+            if (cnt) {
+                const uint32_t msb = P.msb[site] & 0xFFu, rank = P.mrank[site];
+                uint4 f[kFineW / 4];
 #pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, x, off);
-                    if (lane >= static_cast<uint32_t>(off)) x += y;
+                for (uint32_t j = 0; j < kFineW / 4; ++j) f[j] = __ldcg(fine + j);
+                uint32_t cum = 0, k = kBuckets - 1;
+                bool found = false;
+#pragma unroll
+                for (uint32_t j = 0; j < kFineW / 4; ++j) {
+                    const uint32_t v[4] = {f[j].x, f[j].y, f[j].z, f[j].w};
+#pragma unroll
+                    for (uint32_t q = 0; q < 4; ++q) {
+                        cum += v[q];
+                        const bool hit = !found && cum >= rank;
+                        if (hit) k = msb * kFineW + 4 * j + q;
+                        found |= hit;
+                    }
                 }
-                const unsigned hit = __ballot_sync(0xFFFFFFFFu, cum + x >= target);
-                if (hit) {
-                    k = base + static_cast<uint32_t>(__ffs(hit)) - 1u;
-                    break;
-                }
-                cum += __shfl_sync(0xFFFFFFFFu, x, 31);
-            }
-            if (lane == 0) {
-                double med = k == kBuckets - 1
-                                 ? 100000000.0
-                                 : __dadd_rn(__dmul_rn(static_cast<double>(k), 10000.0), 5000.0);
-                med = med < mn ? mn : (mx < med ? mx : med); // std::clamp (stats_from :251)
-                const unsigned long long* s = P.sums + static_cast<size_t>(site) * 4;
+                const double mn = __longlong_as_double(static_cast<long long>(P.mn[site]));
+                const double mx = __longlong_as_double(static_cast<long long>(P.mx[site]));
+                // median_bps (rate_engine.cpp:42-58), clamped (stats_from :251).
+                double med = k == kBuckets - 1 ? 100000000.0
+                                               : __dadd_rn(__dmul_rn(static_cast<double>(k), 10000.0), 5000.0);
+                med = med < mn ? mn : (mx < med ? mx : med);
                 const unsigned __int128 u = static_cast<unsigned __int128>(s[1]) +
                                             (static_cast<unsigned __int128>(s[2]) << 32) +
                                             (static_cast<unsigned __int128>(s[3]) << 64);
-                gnm_site_stats o;
-                o.flow_count = c;
+                o.flow_count = cnt;
                 o.octets = s[0];
                 o.rate_ubps_lo = static_cast<uint64_t>(u);
                 o.rate_ubps_hi = static_cast<uint64_t>(u >> 64);
@@ -1038,31 +1208,32 @@ __global__ void __launch_bounds__(256) k3_finalize(DevPartials P, double thresho
                 o.avg_bps = 0; // host: double(u128)/1e6/count, libgcc rounding
                 o.median_bps = med;
                 o.below_threshold = med < threshold ? 1u : 0u; // monitor.cpp:22
-                o.reserved = 0;
-                out[site] = o;
             }
+            out[site] = o;
         }
-        if (reset) {
-            __syncwarp();
-            for (uint32_t b = b0 + lane; b <= b1; b += 32) hist[hist_index(site, b, n)] = 0;
-            if (lane < 4) P.sums[static_cast<size_t>(site) * 4 + lane] = 0;
-            if (lane == 0) {
-                P.mn[site] = kMinInitBits;
-                P.mx[site] = kMaxInitBits;
-            }
+        if (reset) { // coarse and fine: bulk memsets after this kernel
+            s[0] = s[1] = s[2] = s[3] = 0;
+            P.mn[site] = kMinInitBits;
+            P.mx[site] = kMaxInitBits;
         }
     }
 }
 
-// Blocked -> dense [site][bucket]; one thread per output word (coalesced
-// writes; reads hit 8-word runs).
-__global__ void k_hist_export(const unsigned int* __restrict__ hist, uint32_t n_sites,
-                              unsigned int* __restrict__ dense) {
-    const size_t total = static_cast<size_t>(n_sites) * kBuckets;
-    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
-         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const uint32_t site = static_cast<uint32_t>(i / kBuckets), b = static_cast<uint32_t>(i % kBuckets);
-        dense[i] = hist[hist_index(site, b, n_sites)];
+// Dense [site][10001] histograms (RateHistogram::buckets_) from one launch's log.
+__global__ void __launch_bounds__(256) k_hist_from_log(DevLog L, uint32_t* __restrict__ dense) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < L.regions; r += nwarps) {
+        const uint32_t cnt = L.counts[r];
+        const unsigned int* e = L.entries + static_cast<size_t>(r) * L.warp_cap;
+        const unsigned int* eb = L.buckets ? L.buckets + static_cast<size_t>(r) * L.warp_cap : nullptr;
+        for (uint32_t i = lane; i < cnt; i += 32) {
+            const uint32_t x = e[i];
+            if (x == kLogSkip) continue;
+            const uint32_t site = eb ? x : x >> kLogSiteShift;
+            const uint32_t b = eb ? eb[i] : x & ((1u << kLogSiteShift) - 1u);
+            red_add(dense + static_cast<size_t>(site) * kBuckets + b, 1u);
+        }
     }
 }
 
@@ -1115,20 +1286,20 @@ cudaError_t allow_layout() {
 
 template <int L, bool kS, bool kH>
 void launch_k2_t(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t, const DevParams& p,
-                 const DevPartials& P, const DevHot& hot, cudaStream_t s) {
-    k2_kernel<L, kS, kH>()<<<cfg.grid, cfg.block, cfg.smem, s>>>(b, t.words, t.n_words, p, P, hot);
+                 const DevPartials& P, const DevHot& hot, const DevLog& log, cudaStream_t s) {
+    k2_kernel<L, kS, kH>()<<<cfg.grid, cfg.block, cfg.smem, s>>>(b, t.words, t.n_words, p, P, hot, log);
 }
 
 template <int L>
 void launch_k2_l(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t, const DevParams& p,
-                 const DevPartials& P, const DevHot& hot, cudaStream_t s) {
+                 const DevPartials& P, const DevHot& hot, const DevLog& log, cudaStream_t s) {
     const bool hh = hot.n_slots > 0;
     if (cfg.table_in_smem) {
-        if (hh) launch_k2_t<L, true, true>(cfg, b, t, p, P, hot, s);
-        else launch_k2_t<L, true, false>(cfg, b, t, p, P, hot, s);
+        if (hh) launch_k2_t<L, true, true>(cfg, b, t, p, P, hot, log, s);
+        else launch_k2_t<L, true, false>(cfg, b, t, p, P, hot, log, s);
     } else {
-        if (hh) launch_k2_t<L, false, true>(cfg, b, t, p, P, hot, s);
-        else launch_k2_t<L, false, false>(cfg, b, t, p, P, hot, s);
+        if (hh) launch_k2_t<L, false, true>(cfg, b, t, p, P, hot, log, s);
+        else launch_k2_t<L, false, false>(cfg, b, t, p, P, hot, log, s);
     }
 }
 
@@ -1254,55 +1425,89 @@ bool plan_hot(int device, const DevBatch& b, const DevTable& t, const DevParams&
 
 cudaError_t launch_k2(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t,
                       const DevParams& p, const DevPartials& P, const DevHot& hot,
-                      cudaStream_t s) {
+                      const DevLog& log, cudaStream_t s) {
     switch (k2_layout(b)) {
     case 0:
-        if (cfg.variant == 1) launch_k2_l<4>(cfg, b, t, p, P, hot, s);
-        else if (cfg.variant == 2) launch_k2_l<5>(cfg, b, t, p, P, hot, s);
-        else if (cfg.variant == 3) launch_k2_l<6>(cfg, b, t, p, P, hot, s);
-        else launch_k2_l<0>(cfg, b, t, p, P, hot, s);
+        if (cfg.variant == 1) launch_k2_l<4>(cfg, b, t, p, P, hot, log, s);
+        else if (cfg.variant == 2) launch_k2_l<5>(cfg, b, t, p, P, hot, log, s);
+        else if (cfg.variant == 3) launch_k2_l<6>(cfg, b, t, p, P, hot, log, s);
+        else launch_k2_l<0>(cfg, b, t, p, P, hot, log, s);
         break;
-    case 1: launch_k2_l<1>(cfg, b, t, p, P, hot, s); break;
-    case 2: launch_k2_l<2>(cfg, b, t, p, P, hot, s); break;
-    default: launch_k2_l<3>(cfg, b, t, p, P, hot, s); break;
+    case 1: launch_k2_l<1>(cfg, b, t, p, P, hot, log, s); break;
+    case 2: launch_k2_l<2>(cfg, b, t, p, P, hot, log, s); break;
+    default: launch_k2_l<3>(cfg, b, t, p, P, hot, log, s); break;
     }
     return cudaGetLastError();
 }
 
-cudaError_t launch_k3(int device, const DevPartials& P, double threshold, gnm_site_stats* out,
-                      int reset, cudaStream_t s) {
-    const int block = 256;
-    const uint64_t warps_needed = std::max<uint32_t>(P.n_sites, 1);
-    const uint64_t grid = std::min<uint64_t>((warps_needed * 32 + block - 1) / block,
-                                             static_cast<uint64_t>(sm_count(device)) * 8);
-    auto* tallies_out = reinterpret_cast<unsigned long long*>(out + P.n_sites);
-    k3_finalize<<<static_cast<unsigned>(grid), block, 0, s>>>(P, threshold, out, tallies_out, 1, reset);
+uint32_t k2_regions(const LaunchCfg& cfg) { return static_cast<uint32_t>(cfg.grid) * (cfg.block / 32); }
+
+uint32_t k2_warp_cap(const LaunchCfg& cfg, const DevBatch& b) {
+    // A warp sees at most ceil(ceil(n/G) / (64 * warps)) 64-record tiles (or
+    // 32-record rounds), plus the last CTA's < 64-record remainder; every
+    // candidate leaves exactly one entry.
+    const uint64_t warps = static_cast<uint64_t>(cfg.block / 32);
+    const uint64_t per_cta = (b.n + cfg.grid - 1) / cfg.grid;
+    return static_cast<uint32_t>((per_cta + 64 * warps - 1) / (64 * warps) * 64 + 128);
+}
+
+namespace {
+uint32_t small_grid(int device, uint64_t items, uint32_t block) {
+    const uint64_t g = (items + block - 1) / block;
+    return static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(g, static_cast<uint64_t>(sm_count(device)) * 8)));
+}
+} // namespace
+
+cudaError_t launch_k3a(int device, const DevPartials& P, cudaStream_t s) {
+    if (P.n_sites == 0) return cudaSuccess;
+    if (cudaError_t e = cudaMemsetAsync(P.heavy_next, 0, 4, s)) return e;
+    k3a_median_sb<<<small_grid(device, P.n_sites, 128), 128, 0, s>>>(P);
     return cudaGetLastError();
 }
 
-cudaError_t launch_reset(int device, const DevPartials& P, cudaStream_t s) {
-    const int block = 256;
-    const uint64_t warps_needed = std::max<uint32_t>(P.n_sites, 1);
-    const uint64_t grid = std::min<uint64_t>((warps_needed * 32 + block - 1) / block,
-                                             static_cast<uint64_t>(sm_count(device)) * 8);
-    k3_finalize<<<static_cast<unsigned>(grid), block, 0, s>>>(P, 0.0, nullptr, nullptr, 0, 1);
+cudaError_t launch_k2b(int device, const DevPartials& P, const DevLog& log, cudaStream_t s) {
+    if (log.regions == 0) return cudaSuccess;
+    // Persistent: a few CTAs per SM, so the heavy rows flush rarely.
+    const uint32_t grid = std::min<uint32_t>(small_grid(device, static_cast<uint64_t>(log.regions) * 32, 512),
+                                             static_cast<uint32_t>(sm_count(device)) * 2);
+    k2b_fine<<<grid, 512, 0, s>>>(P, log);
     return cudaGetLastError();
+}
+
+cudaError_t launch_k3b(int device, const DevPartials& P, double threshold, gnm_site_stats* out,
+                       int reset, cudaStream_t s) {
+    auto* tallies_out = reinterpret_cast<unsigned long long*>(out + P.n_sites);
+    k3b_finalize<<<small_grid(device, std::max<uint32_t>(P.n_sites, 1), 128), 128, 0, s>>>(
+        P, threshold, out, tallies_out, 1, reset);
+    cudaError_t e = cudaGetLastError();
+    if (e || !reset) return e;
+    if ((e = cudaMemsetAsync(P.coarse, 0, static_cast<size_t>(P.n_sites) * kCoarse * 4, s))) return e;
+    return cudaMemsetAsync(P.fine, 0, static_cast<size_t>(P.n_sites) * kFineW * 4, s);
+}
+
+cudaError_t launch_reset(int device, const DevPartials& P, cudaStream_t s) {
+    (void)device;
+    return launch_init_partials(P, s);
 }
 
 cudaError_t launch_init_partials(const DevPartials& P, cudaStream_t s) {
     cudaError_t e;
-    if ((e = cudaMemsetAsync(P.sums, 0, (static_cast<size_t>(P.n_sites) * 4 + 4) * 8, s))) return e;
-    if ((e = cudaMemsetAsync(P.mx, 0, static_cast<size_t>(P.n_sites) * 8, s))) return e;
-    if ((e = cudaMemsetAsync(P.hist, 0, static_cast<size_t>(P.n_sites) * kHistStride * 4, s))) return e;
-    if (P.n_sites)
+    const size_t n = P.n_sites;
+    if ((e = cudaMemsetAsync(P.sums, 0, (n * 4 + 4) * 8, s))) return e;
+    if ((e = cudaMemsetAsync(P.mx, 0, n * 8, s))) return e;
+    if ((e = cudaMemsetAsync(P.coarse, 0, n * kCoarse * 4, s))) return e;
+    if ((e = cudaMemsetAsync(P.fine, 0, n * kFineW * 4, s))) return e;
+    if (n)
         k_fill_u64<<<std::min<uint32_t>((P.n_sites + 255) / 256, 1024), 256, 0, s>>>(P.mn, P.n_sites,
                                                                                      kMinInitBits);
     return cudaGetLastError();
 }
 
-cudaError_t launch_hist_export(const DevPartials& P, uint32_t* dense, cudaStream_t s) {
-    if (P.n_sites == 0) return cudaSuccess;
-    k_hist_export<<<1184, 256, 0, s>>>(P.hist, P.n_sites, dense);
+cudaError_t launch_hist_from_log(int device, const DevLog& log, uint32_t n_sites, uint32_t* dense,
+                                 cudaStream_t s) {
+    (void)n_sites;
+    if (log.regions == 0) return cudaSuccess;
+    k_hist_from_log<<<small_grid(device, static_cast<uint64_t>(log.regions) * 32, 256), 256, 0, s>>>(log, dense);
     return cudaGetLastError();
 }
 

@@ -9,17 +9,23 @@
 namespace gnm {
 
 constexpr uint32_t kBuckets = 10001;
-// Per-site histograms, sector-blocked and bucket-major: the 8 buckets of
-// one 32-byte sector belong to one site (the sector footprint of a site's
-// touched buckets is the same as a site-major row), while consecutive
-// 8-bucket groups of a site lie n_sites * 32 B apart. A hot site's buckets
-// therefore spread over every L2 slice instead of the few slices a 40 KB
-// row would map to (same-slice RED contention, profiles/round1).
-constexpr uint32_t kBucketGroups = (kBuckets + 7) / 8; // 1251
-constexpr uint32_t kHistStride = kBucketGroups * 8;   // words per site
-__host__ __device__ inline size_t hist_index(uint32_t site, uint32_t bucket, uint32_t n_sites) {
-    return (static_cast<size_t>(bucket >> 3) * n_sites + site) * 8 + (bucket & 7u);
-}
+// Exact lower median by two-round selection instead of dense 10001-bucket
+// histograms:
+//   round 1  coarse counts per (site, super-bucket), super-bucket = bucket >> 6
+//            (157 of them; bucket 10000 -> 156), kept by K2 in a 6 MB
+//            L2-resident array (sb-major: coarse[sb * n_sites + site]);
+//   round 2  each site's median super-bucket is found from the coarse
+//            counts (K3a); the fine counts of just that super-bucket (64
+//            buckets) are rebuilt from K2's per-flow log (K2b); K3b walks
+//            them to the exact bucket.
+// The log holds one entry per candidate flow: site << 14 | bucket (or a
+// skip marker), plus a second u32 array of buckets for registries of >=
+// 2^18 sites. Dense histograms, when asked for, are rebuilt from the log.
+constexpr uint32_t kCoarse = 157;
+constexpr uint32_t kFineW = 64;
+constexpr uint32_t kLogSkip = 0xFFFFFFFFu;
+constexpr uint32_t kLogSiteShift = 14;
+constexpr uint32_t kLogPackedSites = 1u << 18;
 constexpr uint64_t kMinInitBits = 0x7FF0000000000000ull; // +inf: empty min
 constexpr uint64_t kMaxInitBits = 0;                     // +0.0: empty max (rates are > 0)
 constexpr uint32_t kHotSlots = 512;   // block-private accumulators for hot sites
@@ -32,6 +38,7 @@ struct DevParams {
     uint32_t min_packets1;    // max(min_packets, 1): folds d_pkts == 0 (:75) into one compare
     uint32_t min_duration1;   // max(min_duration_ms, 1): folds duration == 0 (:81)
     uint32_t site_mask;       // kPackedSiteMask, or 0x7FFFFFFF for wide tables
+    uint32_t wide_log;        // registry >= kLogPackedSites sites: log buckets in their own array
     uint32_t ablation;        // GNM_K2_ABLATION builds only (tools/ablation.sh); 0 otherwise
 };
 
@@ -40,8 +47,24 @@ struct DevPartials {
     unsigned long long* sums; // [n_sites*4 + 4]
     unsigned long long* mn;   // f64 bits
     unsigned long long* mx;   // f64 bits
-    unsigned int* hist;       // [n_sites * 10001]
+    unsigned int* coarse;     // [kCoarse * n_sites], sb-major
+    unsigned int* fine;       // [n_sites * kFineW]: the median super-bucket's buckets
+    unsigned int* msb;        // [n_sites]: median super-bucket (K3a, low 8 bits; 0xFF if
+                              // empty) | K2b heavy-row index << 8 (0xFFFFFF: none)
+    unsigned int* mrank;      // [n_sites]: rank of the lower median within it (1-based)
+    unsigned long long* cnt;  // [n_sites]: flow count (K3a)
+    unsigned int* heavy_next; // K3a's heavy-row counter
     uint32_t n_sites;
+};
+
+// One K2 launch's slice of the log: per-warp regions of warp_cap entries
+// (region = blockIdx * warps + warp), each warp's entry count in counts[].
+struct DevLog {
+    unsigned int* entries;
+    unsigned int* buckets; // wide registries only (>= kLogPackedSites sites), else null
+    unsigned int* counts;
+    uint32_t warp_cap;
+    uint32_t regions;
 };
 
 // Per-call hot-site plan: slot -> site (slots 1..n_slots), 0 slots = off.
@@ -102,17 +125,27 @@ bool plan_hot(int device, const DevBatch& b, const DevTable& t, const DevParams&
               uint32_t n_sites, uint32_t* scratch, int k2_grid, bool force, cudaStream_t s,
               uint64_t* launches, cudaError_t* err);
 
+// Entries one warp region must hold for a launch of `cfg` over b (>= the
+// warp's records, rounded up to the 32-entry drain granularity).
+uint32_t k2_warp_cap(const LaunchCfg& cfg, const DevBatch& b);
+uint32_t k2_regions(const LaunchCfg& cfg);
 cudaError_t launch_k2(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t,
                       const DevParams& p, const DevPartials& P, const DevHot& hot,
-                      cudaStream_t s);
-// K3: per-site count/median/flag; reset != 0 also clears the partials.
-cudaError_t launch_k3(int device, const DevPartials& P, double threshold, gnm_site_stats* out,
-                      int reset, cudaStream_t s);
+                      const DevLog& log, cudaStream_t s);
+// K3a: per-site flow count -> median super-bucket and rank (round 1).
+cudaError_t launch_k3a(int device, const DevPartials& P, cudaStream_t s);
+// K2b: fine counts of every site's median super-bucket from one launch's log (round 2).
+cudaError_t launch_k2b(int device, const DevPartials& P, const DevLog& log, cudaStream_t s);
+// K3b: exact median, clamp, flag and the site table; reset != 0 clears the
+// partials (sums, min/max, coarse, fine).
+cudaError_t launch_k3b(int device, const DevPartials& P, double threshold, gnm_site_stats* out,
+                       int reset, cudaStream_t s);
 cudaError_t launch_reset(int device, const DevPartials& P, cudaStream_t s);
 cudaError_t launch_init_partials(const DevPartials& P, cudaStream_t s);
-// Dense [n_sites][10001] copy of the blocked histograms (the reference's
-// RateHistogram::buckets_ order) into `dense` (device memory).
-cudaError_t launch_hist_export(const DevPartials& P, uint32_t* dense, cudaStream_t s);
+// Dense [n_sites][10001] histograms (RateHistogram::buckets_ order) from one
+// launch's log, added into `dense` (device memory, zeroed by the caller).
+cudaError_t launch_hist_from_log(int device, const DevLog& log, uint32_t n_sites, uint32_t* dense,
+                                 cudaStream_t s);
 cudaError_t launch_classify(const LaunchCfg& cfg, const DevSoA& b, const DevTable& t,
                             const DevParams& p, uint32_t* out, cudaStream_t s);
 

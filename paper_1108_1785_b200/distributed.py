@@ -2,17 +2,30 @@
 
 Records shard by contiguous index ranges, exactly the reference's worker
 slicing (rate_engine.cpp:341-344: boundaries ``n*i/workers``); each rank
-accumulates its shard into its own device partials (K2), the partials are
-combined with one grouped all-reduce over NCCL (NVLink), and every rank then
-runs K3 on the combined partials. The combine is exact by construction: the
+accumulates its shard into its own device partials (K2). The combine is two
+small all-reduces over NCCL (NVLink), the two rounds of the exact median:
+
+  round 1  sums / min / max / coarse  -> every rank holds the global
+           per-site sums and the global super-bucket counts;
+  (each rank: ``Engine.prepare_median`` finds every site's median
+           super-bucket from the global coarse counts and counts its OWN
+           flows inside it, from its own per-flow log)
+  round 2  fine                       -> the global counts of those 64
+           buckets; every rank can then finalize (K3b).
+
+Payload at 10k sites: ~0.4 MB of sums + 6.3 MB coarse + 2.6 MB fine, instead
+of 400 MB of dense histograms. The combine is exact by construction: the
 per-site state is a commutative monoid (integer sums as 32-bit limbs in
-64-bit lanes, f64 min/max, u32 bucket counts).
+64-bit lanes, f64 min/max, u32 counts), and the median
+super-bucket every rank derives from the same reduced coarse counts is the
+same.
 
 Partials layout (gnetmon.h, gnm_partials):
   sums     int64 [n_sites*4 + 4]   SUM  (octets, ubps limb0/1/2 per site; tallies)
   min_bps  float64 [n_sites]       MIN  (+inf when empty)
   max_bps  float64 [n_sites]       MAX  (0 when empty)
-  hist     int32 [n_sites*10008]   SUM  (sector-blocked bucket-major, see gnetmon.h)
+  coarse   int32 [157*n_sites]     SUM  (flows per (super-bucket, site), sb-major)
+  fine     int32 [n_sites*64]      SUM  (after prepare_median)
 """
 from __future__ import annotations
 
@@ -26,12 +39,39 @@ def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
 
 
 def allreduce_partials(t: dict, group=None) -> None:
-    """In-place all-reduce of one rank's partials (torch tensors, any device
-    the process group's backend supports: CUDA for NCCL, CPU for gloo)."""
+    """Round 1: in-place all-reduce of one rank's sums, min/max and coarse
+    counts (torch tensors on any device the group's backend supports: CUDA
+    for NCCL, CPU for gloo)."""
     dist.all_reduce(t["sums"], op=dist.ReduceOp.SUM, group=group)
-    dist.all_reduce(t["hist"], op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(t["coarse"], op=dist.ReduceOp.SUM, group=group)
     dist.all_reduce(t["min_bps"], op=dist.ReduceOp.MIN, group=group)
     dist.all_reduce(t["max_bps"], op=dist.ReduceOp.MAX, group=group)
+
+
+def allreduce_fine(t: dict, group=None) -> None:
+    """Round 2: all-reduce of the median super-buckets' fine counts."""
+    dist.all_reduce(t["fine"], op=dist.ReduceOp.SUM, group=group)
+
+
+def combine(engine, catalog, group=None, stream=None) -> None:
+    """The whole combine for one rank's engine: round 1, prepare, round 2.
+    ``stream``: the torch stream wrapping the engine's stream (collectives
+    are ordered after K2 on it)."""
+    t = engine.device_tensors(catalog)
+    ctx = torch.cuda.stream(stream) if stream is not None else _nullctx()
+    with ctx:
+        allreduce_partials(t, group)
+    engine.prepare_median(catalog)
+    with ctx:
+        allreduce_fine(t, group)
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
 
 
 def limbs_to_int(sums: torch.Tensor, n_sites: int) -> list[tuple[int, int]]:

@@ -543,8 +543,15 @@ class Engine:
         p = gnm_partials()
         _check(lib.gnm_get_partials(self._h, catalog.handle, C.byref(p)))
         return {"sums": (p.sums, p.sums_count), "min_bps": (p.min_bps, p.n_sites),
-                "max_bps": (p.max_bps, p.n_sites), "hist": (p.hist, p.hist_count),
-                "n_sites": p.n_sites}
+                "max_bps": (p.max_bps, p.n_sites), "coarse": (p.coarse, p.coarse_count),
+                "fine": (p.fine, p.fine_count), "n_sites": p.n_sites}
+
+    def prepare_median(self, catalog: SiteCatalog) -> None:
+        """Round 2 of the exact median (gnm_prepare_median): after the
+        sums/min/max/coarse all-reduce, find every site's median
+        super-bucket and count this context's flows inside it into ``fine``
+        (then all-reduce ``fine`` and finalize)."""
+        _check(lib.gnm_prepare_median(self._h, catalog.handle))
 
     def device_tensors(self, catalog: SiteCatalog) -> dict:
         """torch views of the device partials (zero-copy, __cuda_array_interface__)."""
@@ -561,7 +568,8 @@ class Engine:
             "sums": torch.as_tensor(_View(p["sums"][0], p["sums"][1], "<i8"), device=dev),
             "min_bps": torch.as_tensor(_View(p["min_bps"][0], p["min_bps"][1], "<f8"), device=dev),
             "max_bps": torch.as_tensor(_View(p["max_bps"][0], p["max_bps"][1], "<f8"), device=dev),
-            "hist": torch.as_tensor(_View(p["hist"][0], p["hist"][1], "<i4"), device=dev),
+            "coarse": torch.as_tensor(_View(p["coarse"][0], p["coarse"][1], "<i4"), device=dev),
+            "fine": torch.as_tensor(_View(p["fine"][0], p["fine"][1], "<i4"), device=dev),
         }
 
     def classify(self, batch: FlowBatch, catalog: SiteCatalog,

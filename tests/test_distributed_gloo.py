@@ -1,8 +1,11 @@
 """The N>1 path on CPU: two gloo ranks shard the records by index
 (rate_engine.cpp:341-344 boundaries), build per-rank partials in the device
-layout (gnetmon.h gnm_partials), all-reduce them with the same function
-bench.py uses on NCCL, and the combined result equals the single-process
-oracle bit-exactly (SPEC.md:310 partition independence)."""
+layout (gnetmon.h gnm_partials), and run the two-round exact-median combine
+with the same functions bench.py uses on NCCL: all-reduce of sums / min /
+max / coarse counts, each rank's median super-bucket and its own fine counts
+inside it (here from the rank's oracle histograms; on the GPU K3a + K2b from
+the rank's log), all-reduce of the fine counts. The combined result equals
+the single-process oracle bit-exactly (SPEC.md:310 partition independence)."""
 import os
 import socket
 
@@ -23,8 +26,12 @@ def _free_port():
     return port
 
 
+COARSE, FINE = 157, 64
+
+
 def partials_from_oracle(acc, n_sites):
-    """Oracle accumulators -> the device partial layout (limbs in int64 lanes)."""
+    """Oracle accumulators -> the device partial layout (limbs in int64 lanes,
+    coarse counts sb-major)."""
     sums = np.zeros(n_sites * 4 + 4, np.int64)
     lo = acc["ubps_lo"].astype(np.uint64)
     sums[0:4 * n_sites:4] = acc["octets"].astype(np.int64)
@@ -32,9 +39,26 @@ def partials_from_oracle(acc, n_sites):
     sums[2:4 * n_sites:4] = (lo >> np.uint64(32)).astype(np.int64)
     sums[3:4 * n_sites:4] = acc["ubps_hi"].astype(np.int64)
     sums[4 * n_sites:] = acc["tallies"].astype(np.int64)
+    hist = acc["hist"].astype(np.int64)
+    padded = np.zeros((n_sites, COARSE * FINE), np.int64)
+    padded[:, :hist.shape[1]] = hist
+    coarse = padded.reshape(n_sites, COARSE, FINE).sum(axis=2).T.reshape(-1)
     return {"sums": torch.from_numpy(sums), "min_bps": torch.from_numpy(acc["min"].copy()),
             "max_bps": torch.from_numpy(acc["max"].copy()),
-            "hist": torch.from_numpy(acc["hist"].reshape(-1).astype(np.int32))}
+            "coarse": torch.from_numpy(coarse.astype(np.int32)),
+            "fine": torch.zeros(n_sites * FINE, dtype=torch.int32)}, padded
+
+
+def median_superbucket(coarse, n_sites):
+    """K3a's rule: the first super-bucket whose cumulative count reaches
+    ceil(count/2), and the median's rank inside it."""
+    c = coarse.reshape(COARSE, n_sites).T.astype(np.int64)
+    cnt = c.sum(axis=1)
+    target = (cnt + 1) // 2
+    cum = np.cumsum(c, axis=1)
+    msb = np.argmax(cum >= target[:, None], axis=1)
+    before = np.where(msb > 0, cum[np.arange(n_sites), msb - 1], 0)
+    return cnt, msb, target - before
 
 
 def _worker(rank, world, port, q):
@@ -53,25 +77,32 @@ def _worker(rank, world, port, q):
     oc = orc.catalog(p, s)
     b, e = D.shard_range(len(cols[0]), rank, world)
     acc = orc.aggregate(tuple(c[b:e] for c in cols), oc, len(sites))
-    t = partials_from_oracle(acc, len(sites))
-    D.allreduce_partials(t)
+    n = len(sites)
+    t, dense = partials_from_oracle(acc, n)
+    D.allreduce_partials(t)                       # round 1
+    cnt, msb, rank_in = median_superbucket(t["coarse"].numpy(), n)
+    own = dense.reshape(n, COARSE, FINE)[np.arange(n), msb]  # this rank's flows in it
+    t["fine"].copy_(torch.from_numpy(own.reshape(-1).astype(np.int32)))
+    D.allreduce_fine(t)                           # round 2
     if rank == 0:
-        n = len(sites)
-        hist = t["hist"].numpy().astype(np.uint32).reshape(n, 10001)
+        fine = t["fine"].numpy().astype(np.int64).reshape(n, FINE)
+        j = np.argmax(np.cumsum(fine, axis=1) >= rank_in[:, None], axis=1)
+        k = msb * FINE + j
+        mn, mx = t["min_bps"].numpy(), t["max_bps"].numpy()
+        med = np.where(k == 10000, 1e8, k * 10000.0 + 5000.0)
+        med = np.minimum(np.maximum(med, mn), mx)
         per = D.limbs_to_int(t["sums"], n)
-        comb = {"count": hist.sum(axis=1).astype(np.uint64), "octets": np.array([x[0] for x in per], np.uint64),
-                "ubps_lo": np.array([x[1] & (2**64 - 1) for x in per], np.uint64),
-                "ubps_hi": np.array([x[1] >> 64 for x in per], np.uint64),
-                "min": t["min_bps"].numpy(), "max": t["max_bps"].numpy(), "hist": hist,
-                "tallies": t["sums"].numpy()[4 * n:].astype(np.uint64)}
-        got = orc.finalize(comb)
         want = orc.finalize(orc.aggregate(cols, oc, n))
-        ok = all(np.array_equal(np.asarray(got[k]).view(np.uint64) if np.asarray(got[k]).dtype == np.float64
-                                else got[k], np.asarray(want[k]).view(np.uint64)
-                                if np.asarray(want[k]).dtype == np.float64 else want[k])
-                 for k in ("count", "octets", "ubps_lo", "ubps_hi", "min", "max", "avg", "median",
-                           "tallies"))
-        q.put(ok and np.array_equal(got["hist"], want["hist"]))
+        present = cnt > 0
+        ok = (np.array_equal(cnt.astype(np.uint64), np.asarray(want["count"]))
+              and np.array_equal(np.array([x[0] for x in per], np.uint64), want["octets"])
+              and np.array_equal(np.array([x[1] & (2**64 - 1) for x in per], np.uint64), want["ubps_lo"])
+              and np.array_equal(np.array([x[1] >> 64 for x in per], np.uint64), want["ubps_hi"])
+              and np.array_equal(mn[present].view(np.uint64), np.asarray(want["min"])[present].view(np.uint64))
+              and np.array_equal(mx[present].view(np.uint64), np.asarray(want["max"])[present].view(np.uint64))
+              and np.array_equal(med[present].view(np.uint64), np.asarray(want["median"])[present].view(np.uint64))
+              and np.array_equal(t["sums"].numpy()[4 * n:].astype(np.uint64), want["tallies"]))
+        q.put(bool(ok))
     dist.barrier()
     dist.destroy_process_group()
 

@@ -95,11 +95,17 @@ def test_device_partials_zero_copy_views(engine):
     engine.accumulate(FlowBatch(*cols).to_device(), cat)
     t = engine.device_tensors(cat)
     torch.cuda.synchronize()  # K2 ran on the engine's stream
-    t["sums"].mul_(2)
-    t["hist"].mul_(2)
+    t["sums"].mul_(2)          # round 1 of two equal ranks
+    t["coarse"].mul_(2)
+    torch.cuda.synchronize()
+    engine.prepare_median(cat)
+    torch.cuda.synchronize()
+    t["fine"].mul_(2)          # round 2
     torch.cuda.synchronize()
     doubled = engine.finalize(cat)
     np.testing.assert_array_equal(doubled.table["flow_count"], 2 * single.table["flow_count"])
     np.testing.assert_array_equal(doubled.table["octets"], 2 * single.table["octets"])
     np.testing.assert_array_equal(doubled.table["min_bps"], single.table["min_bps"])
     assert doubled.tallies.forward == 2 * single.tallies.forward
+    # the lower median of a doubled multiset is the same element
+    np.testing.assert_array_equal(doubled.table["median_bps"], single.table["median_bps"])
