@@ -31,7 +31,7 @@ $(PKG)/lib/libgnm_synth.so: $(PKG)/csrc/synth.c
 ablation: $(PKG)/lib/ablation/libgnetmon.so
 $(PKG)/lib/ablation/libgnetmon.so: $(SRCS) $(HDRS)
 	@mkdir -p $(PKG)/lib/ablation
-	$(NVCC) $(NVFLAGS) -DGNM_K2_ABLATION -shared -o $@ $(SRCS) 2> /dev/null
+	$(NVCC) $(NVFLAGS) -DGNM_K2_ABLATION $(ABLATION_FLAGS) -shared -o $@ $(SRCS) 2> /dev/null
 
 oracle:
 	$(MAKE) -C oracle all

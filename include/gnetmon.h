@@ -252,9 +252,17 @@ typedef struct gnm_timing {
     uint64_t kernel_launches; /* every kernel this library launched since ctx creation */
     uint64_t records;         /* records accumulated since the last finalize */
     double plan_ms;           /* K1 hot-site planning (sample, assign, table slots) */
+    /* Running totals since timing was last enabled, over every finalize:
+     * K1, K2 and finalize device time, and the number of finalizes. */
+    double total_plan_ms;
+    double total_accumulate_ms;
+    double total_finalize_ms;
+    uint64_t total_finalizes;
+    uint64_t total_k2_launches;
 } gnm_timing;
 int gnm_ctx_timing(gnm_ctx* ctx, gnm_timing* out);
-/* 1 = record CUDA events around every kernel (default 0). */
+/* 1 = record CUDA events around every kernel (default 0); enabling resets
+ * the running totals. */
 int gnm_ctx_enable_timing(gnm_ctx* ctx, int enable);
 
 /* ---- Warning rule: evaluate_warnings (monitor.cpp:13-34) ----------------- */

@@ -84,7 +84,9 @@ class gnm_timing(C.Structure):
     _fields_ = [("accumulate_ms", C.c_double), ("finalize_ms", C.c_double),
                 ("h2d_ms", C.c_double), ("k2_launches", C.c_uint64),
                 ("kernel_launches", C.c_uint64), ("records", C.c_uint64),
-                ("plan_ms", C.c_double)]
+                ("plan_ms", C.c_double), ("total_plan_ms", C.c_double),
+                ("total_accumulate_ms", C.c_double), ("total_finalize_ms", C.c_double),
+                ("total_finalizes", C.c_uint64), ("total_k2_launches", C.c_uint64)]
 
 
 class gnm_warning(C.Structure):

@@ -80,11 +80,6 @@ struct gnm_ctx {
     size_t table_cap_words = 0;
     gnm::DevTable table{};
     int hot_mode = GNM_HOT_AUTO;
-    // K2 variant for aligned SoA batches (environment GNM_K2_VARIANT, read at
-    // context creation; results are identical): "reg" double-buffers the
-    // next tile in registers, "l2" asks the TMA engine to prefetch tiles
-    // into L2 (cp.async.bulk.prefetch) and loads the current one directly.
-    int k2_variant = 0;
 
     // partials
     gnm::DevPartials P{};
@@ -127,6 +122,8 @@ struct gnm_ctx {
     std::vector<EventPair> pool;
     std::vector<EventPair> k2_pairs, k3_pairs, h2d_pairs, plan_pairs;
     double acc_ms = 0, fin_ms = 0, h2d_ms = 0, plan_ms = 0;
+    double tot_plan_ms = 0, tot_acc_ms = 0, tot_fin_ms = 0;
+    uint64_t tot_finalizes = 0, tot_k2 = 0, k2_since_fin = 0;
     int occ[2] = {0, 0}; // K2 blocks/SM (cold, hot) for the current table size
     uint64_t k2_launches = 0, kernel_launches = 0, records = 0;
 };
@@ -364,7 +361,7 @@ void launch_k2_timed(gnm_ctx* c, const gnm::DevBatch& b, const gnm::DevParams& p
         ck(cudaEventRecord(pe.a, c->stream), "cudaEventRecord");
     }
     // K1: hot-site plan for this batch (skipped when no site can be hot).
-    const gnm::LaunchCfg cold = gnm::k2_config(c->device, b, c->table.n_words, false, c->occ, c->k2_variant);
+    const gnm::LaunchCfg cold = gnm::k2_config(c->device, b, c->table.n_words, false, c->occ);
     bool hot = false;
     if (c->hot_mode != GNM_HOT_OFF) {
         cudaError_t e;
@@ -372,7 +369,7 @@ void launch_k2_timed(gnm_ctx* c, const gnm::DevBatch& b, const gnm::DevParams& p
                             c->hot_mode == GNM_HOT_FORCE, c->stream, &c->kernel_launches, &e);
         ck(e, "hot-site plan");
     }
-    const gnm::LaunchCfg cfg = hot ? gnm::k2_config(c->device, b, c->table.n_words, true, c->occ, c->k2_variant) : cold;
+    const gnm::LaunchCfg cfg = hot ? gnm::k2_config(c->device, b, c->table.n_words, true, c->occ) : cold;
     gnm::DevHot h{c->d_scratch + 2 * static_cast<size_t>(c->P.n_sites), hot ? gnm::kHotSlots : 0u};
     if (c->timing) {
         ck(cudaEventRecord(pe.b, c->stream), "cudaEventRecord");
@@ -603,10 +600,15 @@ int finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* r) {
     r->tallies.unmatched = t[3];
     r->n_sites = n_sites;
     if (c->timing) {
+        c->tot_k2 += c->k2_pairs.size();
         c->acc_ms = drain_pairs(c, c->k2_pairs);
         c->plan_ms = drain_pairs(c, c->plan_pairs);
         c->fin_ms = drain_pairs(c, c->k3_pairs);
         c->h2d_ms = drain_pairs(c, c->h2d_pairs);
+        c->tot_acc_ms += c->acc_ms;
+        c->tot_plan_ms += c->plan_ms;
+        c->tot_fin_ms += c->fin_ms;
+        c->tot_finalizes += 1;
     }
     c->accumulating = false;
     return GNM_OK;
@@ -718,12 +720,6 @@ int gnm_ctx_create(int device, gnm_ctx** out) {
             ck(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
             ck(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
             c->stream = c->own_stream;
-            const char* kv = std::getenv("GNM_K2_VARIANT");
-            c->k2_variant = !kv                             ? 0
-                            : std::strcmp(kv, "l2") == 0    ? 1
-                            : std::strcmp(kv, "tma") == 0   ? 2
-                            : std::strcmp(kv, "async") == 0 ? 3
-                                                            : 0;
             for (int i = 0; i < 2; ++i) {
                 ck(cudaEventCreateWithFlags(&c->ev_h2d[i], cudaEventDisableTiming), "cudaEventCreate");
                 ck(cudaEventCreateWithFlags(&c->ev_k2[i], cudaEventDisableTiming), "cudaEventCreate");
@@ -801,6 +797,10 @@ int gnm_ctx_set_hot_mode(gnm_ctx* c, int mode) {
 int gnm_ctx_enable_timing(gnm_ctx* c, int enable) {
     if (!c) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx");
     c->timing = enable != 0;
+    if (c->timing) {
+        c->tot_plan_ms = c->tot_acc_ms = c->tot_fin_ms = 0;
+        c->tot_finalizes = c->tot_k2 = 0;
+    }
     return GNM_OK;
 }
 
@@ -813,6 +813,11 @@ int gnm_ctx_timing(gnm_ctx* c, gnm_timing* out) {
     out->k2_launches = c->k2_launches;
     out->kernel_launches = c->kernel_launches;
     out->records = c->records;
+    out->total_plan_ms = c->tot_plan_ms;
+    out->total_accumulate_ms = c->tot_acc_ms;
+    out->total_finalize_ms = c->tot_fin_ms;
+    out->total_finalizes = c->tot_finalizes;
+    out->total_k2_launches = c->tot_k2;
     return GNM_OK;
 }
 

@@ -43,23 +43,32 @@ namespace {
 
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kDirWordsDev = 4096u; // registry.hpp kDirWords
-constexpr int kK2Block = 512;
+#ifndef GNM_K2_BLOCK
+#define GNM_K2_BLOCK 768
+#endif
+constexpr int kK2Block = GNM_K2_BLOCK; // 24 warps: up to 80 registers per thread
 constexpr uint32_t kWarps = kK2Block / 32;
-// Records one K2 CTA may process: every 16-bit limb of a hot slot then
-// sums fewer than 2^16 values below 2^16 and cannot wrap its u32.
+// Records one non-persistent K2 CTA (k2_gen) may process: every 16-bit limb
+// of a hot slot then sums fewer than 2^16 values below 2^16 and cannot wrap
+// its u32. The persistent k2_soa bounds them per epoch instead.
 constexpr uint64_t kCtaRecords = 65536 - 64;
-constexpr uint32_t kCtaTiles = static_cast<uint32_t>(kCtaRecords / 64) - 1; // + a < 64-record tail
+// k2_soa epochs: kEpochRounds rounds of kWarps 64-record tiles, plus the
+// queue residue (< 32 per warp) and the < 64-record tail, stay below 2^16
+// adds per limb; between epochs any limb that could wrap in the next one
+// (>= kLimbFlush) is flushed to L2.
+#ifndef GNM_EPOCH_ROUNDS
+#define GNM_EPOCH_ROUNDS 29
+#endif
+constexpr uint32_t kEpochRounds = GNM_EPOCH_ROUNDS; // measurement builds may override (unsafe above 29)
+constexpr uint32_t kLimbFlush = 1u << 28;
 constexpr uint32_t kQueue = 96; // per-warp queue capacity: < 32 left + 2 x 32 pushed
-// The top kCoarseSlots hot slots also keep their coarse counts in shared
-// memory, two u16 super-buckets per u32 (a CTA's < 2^16 records cannot
-// carry one half into the other).
+// The top kCoarseSlots hot slots also keep their coarse counts in shared memory.
 constexpr uint32_t kCoarseSlots = 32;
 // K2b's shared-memory fine rows for the heaviest sites.
 constexpr uint32_t kHeavy = 64;
 constexpr uint32_t kHeavyNone = 0xFFFFFFu;
 constexpr uint64_t kHeavyMin = 1u << 16;
-constexpr uint32_t kCoarseWords = (kCoarse + 1) / 2;
-constexpr size_t kHotBytes = kHotStride * (5 * 4 + 2 * 8) + kCoarseSlots * kCoarseWords * 4;
+constexpr size_t kHotBytes = kHotStride * (5 * 4 + 2 * 8) + kCoarseSlots * kCoarse * 4;
 constexpr size_t kSmemMax = 227 * 1024;
 constexpr size_t kQueueBytes = kWarps * kQueue * 16;
 constexpr size_t kSmemTableMax = kSmemMax - kHotBytes - kQueueBytes - 1024;
@@ -75,18 +84,18 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
-__device__ __forceinline__ uint2 ld_stream_u2(const void* p) {
+__device__ __forceinline__ uint2 ld_stream_u2(const void* p, uint64_t pol) {
     uint2 r;
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::256B.v2.u32 {%0,%1}, [%2], %3;"
                  : "=r"(r.x), "=r"(r.y)
-                 : "l"(p), "l"(evict_first_policy()));
+                 : "l"(p), "l"(pol));
     return r;
 }
-__device__ __forceinline__ ulonglong2 ld_stream_u64x2(const void* p) {
+__device__ __forceinline__ ulonglong2 ld_stream_u64x2(const void* p, uint64_t pol) {
     ulonglong2 r;
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::256B.v2.u64 {%0,%1}, [%2], %3;"
                  : "=l"(r.x), "=l"(r.y)
-                 : "l"(p), "l"(evict_first_policy()));
+                 : "l"(p), "l"(pol));
     return r;
 }
 
@@ -160,7 +169,7 @@ struct HotSmem {
     uint32_t* limb; // [5][kHotStride]: oct lo16, oct hi16, ubps bits 0-15, 16-31, 32-47
     unsigned long long* mn;
     unsigned long long* mx;
-    uint32_t* coarse; // [kCoarseSlots][kCoarseWords], slot 1 first
+    uint32_t* coarse; // [kCoarseSlots][kCoarse], slot 1 first
 };
 
 __device__ __forceinline__ HotSmem hot_smem(uint32_t table_words_in_smem) {
@@ -180,7 +189,7 @@ __device__ __forceinline__ void hot_init(const HotSmem& h) {
         h.mn[i] = kMinInitBits;
         h.mx[i] = kMaxInitBits;
     }
-    for (uint32_t i = threadIdx.x; i < kCoarseSlots * kCoarseWords; i += blockDim.x) h.coarse[i] = 0;
+    for (uint32_t i = threadIdx.x; i < kCoarseSlots * kCoarse; i += blockDim.x) h.coarse[i] = 0;
 }
 
 // ---- per-flow arithmetic -----------------------------------------------------
@@ -354,7 +363,7 @@ __device__ __forceinline__ uint32_t accumulate(uint32_t code, uint32_t oct, uint
     if (p.ablation == 3 || p.ablation == 4) {
         if (p.ablation == 4) {
             if (kHot && slot && slot <= kCoarseSlots)
-                red_add_shared(h.coarse + (slot - 1) * kCoarseWords + (sb >> 1), (sb & 1u) ? 0x10000u : 1u);
+                red_add_shared(h.coarse + (slot - 1) * kCoarse + sb, 1u);
             else red_add(P.coarse + static_cast<size_t>(sb) * P.n_sites + site, 1u);
         }
         c.unm ^= static_cast<uint32_t>(lo ^ hi ^ rb) ^ static_cast<uint32_t>(cmn ^ cmx);
@@ -376,7 +385,7 @@ __device__ __forceinline__ uint32_t accumulate(uint32_t code, uint32_t oct, uint
             if (hi) red_add(s + 3, hi);
         }
         if (slot <= kCoarseSlots)
-            red_add_shared(h.coarse + (slot - 1) * kCoarseWords + (sb >> 1), (sb & 1u) ? 0x10000u : 1u);
+            red_add_shared(h.coarse + (slot - 1) * kCoarse + sb, 1u);
         else
             red_add(P.coarse + static_cast<size_t>(sb) * P.n_sites + site, 1u);
         // min/max: the slot's cached bounds filter the global reductions. The
@@ -502,14 +511,37 @@ __device__ __forceinline__ void hot_flush(const HotSmem& h, const DevHot& hot, c
         if (u01) red_add(s + 1, u01);
         if (u2) red_add(s + 2, static_cast<unsigned long long>(u2));
     }
-    const uint32_t words = min(hot.n_slots, kCoarseSlots) * kCoarseWords;
+    const uint32_t words = min(hot.n_slots, kCoarseSlots) * kCoarse;
     for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) {
         const uint32_t w = h.coarse[i];
         if (!w) continue;
-        const uint32_t site = __ldg(hot.hot_site + 1 + i / kCoarseWords);
-        const uint32_t sb = 2 * (i % kCoarseWords);
-        if (w & 0xFFFFu) red_add(P.coarse + static_cast<size_t>(sb) * P.n_sites + site, w & 0xFFFFu);
-        if (w >> 16) red_add(P.coarse + static_cast<size_t>(sb + 1) * P.n_sites + site, w >> 16);
+        const uint32_t site = __ldg(hot.hot_site + 1 + i / kCoarse);
+        red_add(P.coarse + static_cast<size_t>(i % kCoarse) * P.n_sites + site, w);
+    }
+}
+
+// Between k2_soa epochs (CTA-wide, after a barrier): flush and clear every
+// limb that might wrap during the next epoch; everything else stays.
+__device__ __forceinline__ void hot_normalize(const HotSmem& h, const DevHot& hot, const DevPartials& P) {
+    for (uint32_t slot = 1 + threadIdx.x; slot <= hot.n_slots; slot += blockDim.x) {
+        uint32_t* l = h.limb + slot;
+        const uint32_t m = max(max(max(l[0], l[kHotStride]), max(l[2 * kHotStride], l[3 * kHotStride])),
+                               l[4 * kHotStride]);
+        if (m < kLimbFlush) continue;
+        const uint32_t site = __ldg(hot.hot_site + slot);
+        unsigned long long* s = P.sums + static_cast<size_t>(site) * 4;
+        red_add(s + 0, static_cast<uint64_t>(l[0]) + (static_cast<uint64_t>(l[kHotStride]) << 16));
+        red_add(s + 1, static_cast<uint64_t>(l[2 * kHotStride]) + (static_cast<uint64_t>(l[3 * kHotStride]) << 16));
+        red_add(s + 2, static_cast<unsigned long long>(l[4 * kHotStride]));
+#pragma unroll
+        for (int k = 0; k < 5; ++k) l[k * kHotStride] = 0;
+    }
+    const uint32_t words = min(hot.n_slots, kCoarseSlots) * kCoarse;
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) {
+        const uint32_t w = h.coarse[i];
+        if (w < kLimbFlush) continue;
+        red_add(P.coarse + static_cast<size_t>(i % kCoarse) * P.n_sites + __ldg(hot.hot_site + 1 + i / kCoarse), w);
+        h.coarse[i] = 0;
     }
 }
 
@@ -598,14 +630,17 @@ __device__ __forceinline__ void k2_epilogue(Ctr& t, WarpQueue& wq, uint32_t lane
     }
 }
 
-// Main variant: SoA columns, 16-byte aligned, n < 2^32. CTA b owns the
-// contiguous 64-record tiles [b*T/G, (b+1)*T/G) (at most kCtaTiles); its
-// warps walk them strided, two records per lane per tile (one LDG.64 per u32
-// column, one LDG.128 per u64 column, non-allocating), software-pipelined:
-// the next tile's six loads are in flight while this one is classified. The
-// last CTA also takes the < 64-record remainder through the scalar path.
+// Main variant: SoA columns, 16-byte aligned, n < 2^32. Persistent: one
+// 1024-thread CTA per SM owns the contiguous 64-record tiles
+// [b*T/G, (b+1)*T/G) and walks them in rounds of kWarps tiles (warp w takes
+// tile t0 + r*kWarps + w), two records per lane per tile (one LDG.64 per u32
+// column, one LDG.128 per u64 column, non-allocating, evict-first),
+// software-pipelined: the next round's six loads are in flight while this
+// one is classified. Every kEpochRounds rounds the CTA meets at a barrier
+// and normalizes the hot limbs (hot_normalize). The last CTA also takes the
+// < 64-record remainder through the scalar path.
 template <bool kSmem, bool kHot>
-__global__ void __launch_bounds__(kK2Block, 2) k2_soa(DevBatch b, const uint32_t* __restrict__ gt,
+__global__ void __launch_bounds__(kK2Block, 1) k2_soa(DevBatch b, const uint32_t* __restrict__ gt,
                                                     uint32_t table_words, DevParams p,
                                                     DevPartials P, DevHot hot, DevLog L) {
     HotSmem h{};
@@ -615,7 +650,9 @@ __global__ void __launch_bounds__(kK2Block, 2) k2_soa(DevBatch b, const uint32_t
     const uint32_t warp = threadIdx.x >> 5;
     const DevSoA& c = b.soa;
     const uint64_t tiles = c.n >> 6;
+    const uint32_t t0 = static_cast<uint32_t>(tiles * blockIdx.x / gridDim.x);
     const uint32_t t_end = static_cast<uint32_t>(tiles * (blockIdx.x + 1) / gridDim.x);
+    const uint32_t rounds = (t_end - t0 + kWarps - 1) / kWarps; // CTA-uniform
     const uint2* src2 = reinterpret_cast<const uint2*>(c.src) + lane;
     const uint2* dst2 = reinterpret_cast<const uint2*>(c.dst) + lane;
     const uint2* pkt2 = reinterpret_cast<const uint2*>(c.pkts) + lane;
@@ -623,251 +660,49 @@ __global__ void __launch_bounds__(kK2Block, 2) k2_soa(DevBatch b, const uint32_t
     const ulonglong2* st2 = reinterpret_cast<const ulonglong2*>(c.start) + lane;
     const ulonglong2* en2 = reinterpret_cast<const ulonglong2*>(c.end) + lane;
     Ctr t;
-    uint32_t tile = static_cast<uint32_t>(tiles * blockIdx.x / gridDim.x) + warp;
+    const uint64_t pol = evict_first_policy();
+    uint32_t tile = t0 + warp;
     uint2 s, d, k, o;
-    ulonglong2 t0, e0;
+    ulonglong2 ts, te;
     if (tile < t_end) {
         const uint32_t g = tile * 32u;
-        s = ld_stream_u2(src2 + g);
-        d = ld_stream_u2(dst2 + g);
-        k = ld_stream_u2(pkt2 + g);
-        o = ld_stream_u2(oct2 + g);
-        t0 = ld_stream_u64x2(st2 + g);
-        e0 = ld_stream_u64x2(en2 + g);
+        s = ld_stream_u2(src2 + g, pol);
+        d = ld_stream_u2(dst2 + g, pol);
+        k = ld_stream_u2(pkt2 + g, pol);
+        o = ld_stream_u2(oct2 + g, pol);
+        ts = ld_stream_u64x2(st2 + g, pol);
+        te = ld_stream_u64x2(en2 + g, pol);
     }
-    for (; tile < t_end; tile += kWarps) {
+    for (uint32_t r = 0; r < rounds; ++r) {
         const uint32_t next = tile + kWarps;
         uint2 ns, nd, nk, no;
         ulonglong2 nt, ne;
         if (next < t_end) {
             const uint32_t g = next * 32u;
-            ns = ld_stream_u2(src2 + g);
-            nd = ld_stream_u2(dst2 + g);
-            nk = ld_stream_u2(pkt2 + g);
-            no = ld_stream_u2(oct2 + g);
-            nt = ld_stream_u64x2(st2 + g);
-            ne = ld_stream_u64x2(en2 + g);
+            ns = ld_stream_u2(src2 + g, pol);
+            nd = ld_stream_u2(dst2 + g, pol);
+            nk = ld_stream_u2(pkt2 + g, pol);
+            no = ld_stream_u2(oct2 + g, pol);
+            nt = ld_stream_u64x2(st2 + g, pol);
+            ne = ld_stream_u64x2(en2 + g, pol);
         }
-        const uint64_t dx = e0.x - t0.x, dy = e0.y - t0.y;
-        const uint32_t cx = stage_a<kSmem>(s.x, d.x, k.x, o.x, dx, p, gt, t);
-        const uint32_t cy = stage_a<kSmem>(s.y, d.y, k.y, o.y, dy, p, gt, t);
-        push(cx, o.x, dx, wq, lane);
-        push(cy, o.y, dy, wq, lane);
-        drain_full<kSmem, kHot>(wq, lane, gt, p, P, h, t);
-        s = ns, d = nd, k = nk, o = no, t0 = nt, e0 = ne;
-    }
-    if (blockIdx.x == gridDim.x - 1 && warp == 0)
-        run_scalar<1, kSmem, kHot>(b, tiles << 6, c.n, 32, lane, gt, p, P, h, t, wq);
-    k2_epilogue<kSmem, kHot>(t, wq, lane, gt, p, P, h, hot, L);
-}
-
-// Variant: no register double-buffering. Each warp asks the TMA engine to
-// pull the tile it will read kAhead iterations later into L2
-// (cp.async.bulk.prefetch.L2, one bulk request per column segment, issued
-// by lanes 0-5), then loads the current tile with plain vector loads that
-// hit L2. Frees the 16 registers the in-register prefetch holds.
-constexpr uint32_t kAhead = 3;
-__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
-template <bool kSmem, bool kHot>
-__global__ void __launch_bounds__(kK2Block, 2) k2_soa_pf(DevBatch b, const uint32_t* __restrict__ gt,
-                                                       uint32_t table_words, DevParams p,
-                                                       DevPartials P, DevHot hot, DevLog L) {
-    HotSmem h{};
-    WarpQueue wq;
-    k2_prologue<kSmem, kHot>(gt, table_words, L, h, wq);
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t warp = threadIdx.x >> 5;
-    const DevSoA& c = b.soa;
-    const uint64_t tiles = c.n >> 6;
-    const uint32_t t_end = static_cast<uint32_t>(tiles * (blockIdx.x + 1) / gridDim.x);
-    uint32_t tile = static_cast<uint32_t>(tiles * blockIdx.x / gridDim.x) + warp;
-    // Lane l < 6 prefetches column l's 64-record segment (256 or 512 bytes).
-    const char* pf_col = reinterpret_cast<const char*>(
-        lane == 0 ? static_cast<const void*>(c.src)
-        : lane == 1 ? static_cast<const void*>(c.dst)
-        : lane == 2 ? static_cast<const void*>(c.pkts)
-        : lane == 3 ? static_cast<const void*>(c.octets)
-        : lane == 4 ? static_cast<const void*>(c.start)
-                    : static_cast<const void*>(c.end));
-    const uint32_t pf_bytes = lane < 4 ? 256u : 512u;
-    if (lane < 6)
-        for (uint32_t a = 0; a < kAhead; ++a) {
-            const uint32_t tl = tile + a * kWarps;
-            if (tl < t_end) bulk_prefetch_l2(pf_col + static_cast<size_t>(tl) * pf_bytes, pf_bytes);
+        if (tile < t_end) {
+            const uint64_t dx = te.x - ts.x, dy = te.y - ts.y;
+            const uint32_t cx = stage_a<kSmem>(s.x, d.x, k.x, o.x, dx, p, gt, t);
+            const uint32_t cy = stage_a<kSmem>(s.y, d.y, k.y, o.y, dy, p, gt, t);
+            push(cx, o.x, dx, wq, lane);
+            push(cy, o.y, dy, wq, lane);
+            drain_full<kSmem, kHot>(wq, lane, gt, p, P, h, t);
         }
-    const uint2* src2 = reinterpret_cast<const uint2*>(c.src) + lane;
-    const uint2* dst2 = reinterpret_cast<const uint2*>(c.dst) + lane;
-    const uint2* pkt2 = reinterpret_cast<const uint2*>(c.pkts) + lane;
-    const uint2* oct2 = reinterpret_cast<const uint2*>(c.octets) + lane;
-    const ulonglong2* st2 = reinterpret_cast<const ulonglong2*>(c.start) + lane;
-    const ulonglong2* en2 = reinterpret_cast<const ulonglong2*>(c.end) + lane;
-    Ctr t;
-    for (; tile < t_end; tile += kWarps) {
-        const uint32_t ahead = tile + kAhead * kWarps;
-        if (lane < 6 && ahead < t_end)
-            bulk_prefetch_l2(pf_col + static_cast<size_t>(ahead) * pf_bytes, pf_bytes);
-        const uint32_t g = tile * 32u;
-        const uint2 s = ld_stream_u2(src2 + g);
-        const uint2 d = ld_stream_u2(dst2 + g);
-        const uint2 k = ld_stream_u2(pkt2 + g);
-        const uint2 o = ld_stream_u2(oct2 + g);
-        const ulonglong2 t0 = ld_stream_u64x2(st2 + g);
-        const ulonglong2 e0 = ld_stream_u64x2(en2 + g);
-        const uint64_t dx = e0.x - t0.x, dy = e0.y - t0.y;
-        const uint32_t cx = stage_a<kSmem>(s.x, d.x, k.x, o.x, dx, p, gt, t);
-        const uint32_t cy = stage_a<kSmem>(s.y, d.y, k.y, o.y, dy, p, gt, t);
-        push(cx, o.x, dx, wq, lane);
-        push(cy, o.y, dy, wq, lane);
-        drain_full<kSmem, kHot>(wq, lane, gt, p, P, h, t);
-    }
-    if (blockIdx.x == gridDim.x - 1 && warp == 0)
-        run_scalar<1, kSmem, kHot>(b, tiles << 6, c.n, 32, lane, gt, p, P, h, t, wq);
-    k2_epilogue<kSmem, kHot>(t, wq, lane, gt, p, P, h, hot, L);
-}
-
-// ---- K2, TMA-staged variant ----------------------------------------------------
-// Each warp owns a kRing-deep ring of 64-record tiles in shared memory, fed
-// by its own lane 0 with cp.async.bulk (one bulk copy per column segment,
-// completing on the stage's mbarrier): the next tile streams in while this
-// one is classified, without holding it in registers and without any
-// global address arithmetic in the loop. Stage layout (2 KB): src[64],
-// dst[64], pkts[64], octets[64] (u32), start[64], end[64] (u64); lane l
-// reads records 2l and 2l+1 with immediate-offset LDS.64 / LDS.128.
-constexpr int kTmaWarps = 24;
-constexpr int kTmaBlock = kTmaWarps * 32;
-constexpr uint32_t kRing = 2;
-constexpr uint32_t kTileBytes = 64 * 32;
-constexpr size_t kTmaFixed = kTmaWarps * kQueue * 16 + kTmaWarps * kRing * (kTileBytes + 8);
-
-__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-// Lane 0: tile `tile` of the batch into stage buffer `st`.
-__device__ __forceinline__ void issue_tile(unsigned char* st, uint64_t* bar, const DevSoA& c, uint32_t tile) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(kTileBytes)
-                 : "memory");
-    const size_t r = static_cast<size_t>(tile) * 64;
-    bulk_g2s(st, c.src + r, 256, bar);
-    bulk_g2s(st + 256, c.dst + r, 256, bar);
-    bulk_g2s(st + 512, c.pkts + r, 256, bar);
-    bulk_g2s(st + 768, c.octets + r, 256, bar);
-    bulk_g2s(st + 1024, c.start + r, 512, bar);
-    bulk_g2s(st + 1536, c.end + r, 512, bar);
-}
-
-// The same ring fed by per-lane async copies (cp.async.cg, 16 B each, no
-// registers): lane l moves bytes [64l, 64l+64) of the 2 KB stage, i.e.
-// lanes 0-15 the four u32 column segments and 16-31 the two u64 ones; each
-// tile is one commit group, waited with wait_group + __syncwarp.
-__device__ __forceinline__ void async_tile(unsigned char* st, const char* col, uint32_t seg_bytes,
-                                           uint32_t lane_off, uint32_t tile) {
-    const char* g = col + static_cast<size_t>(tile) * seg_bytes + lane_off;
-    const uint32_t sa = smem_u32(st) + 64 * (threadIdx.x & 31u);
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + 16 * k), "l"(g + 16 * k)
-                     : "memory");
-    asm volatile("cp.async.commit_group;" ::: "memory");
-}
-
-template <bool kSmem, bool kHot, bool kBulk>
-__global__ void __launch_bounds__(kTmaBlock, 1) k2_tma(DevBatch b, const uint32_t* __restrict__ gt,
-                                                     uint32_t table_words, DevParams p,
-                                                     DevPartials P, DevHot hot, DevLog L) {
-    HotSmem h{};
-    WarpQueue wq;
-    k2_prologue<kSmem, kHot>(gt, table_words, L, h, wq);
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t warp = threadIdx.x >> 5;
-    const uint32_t smem_words = kSmem ? table_words : 0u;
-    unsigned char* rings = reinterpret_cast<unsigned char*>(g_smem + smem_words + (kHot ? kHotBytes / 4 : 0u)) +
-                           kTmaWarps * kQueue * 16;
-    unsigned char* ring = rings + static_cast<size_t>(warp) * kRing * kTileBytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(rings + static_cast<size_t>(kTmaWarps) * kRing * kTileBytes) +
-                     warp * kRing;
-    const DevSoA& c = b.soa;
-    const uint64_t tiles = c.n >> 6;
-    const uint32_t t0 = static_cast<uint32_t>(tiles * blockIdx.x / gridDim.x);
-    const uint32_t t1 = static_cast<uint32_t>(tiles * (blockIdx.x + 1) / gridDim.x);
-    const uint32_t mine = t1 - t0 > warp ? (t1 - t0 - warp + kTmaWarps - 1) / kTmaWarps : 0u;
-    // cp.async feed: this lane's column and byte offset within the segment.
-    const uint32_t cidx = lane < 16 ? lane >> 2 : 4 + ((lane - 16) >> 3);
-    const char* col = reinterpret_cast<const char*>(
-        cidx == 0 ? static_cast<const void*>(c.src)
-        : cidx == 1 ? static_cast<const void*>(c.dst)
-        : cidx == 2 ? static_cast<const void*>(c.pkts)
-        : cidx == 3 ? static_cast<const void*>(c.octets)
-        : cidx == 4 ? static_cast<const void*>(c.start)
-                    : static_cast<const void*>(c.end));
-    const uint32_t seg_bytes = lane < 16 ? 256u : 512u;
-    const uint32_t lane_off = lane < 16 ? (lane & 3u) * 64 : ((lane - 16) & 7u) * 64;
-    if constexpr (kBulk) {
-        if (lane == 0) {
-            for (uint32_t st = 0; st < kRing; ++st) mbar_init(bars + st, 1);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-            for (uint32_t i = 0; i < kRing && i < mine; ++i)
-                issue_tile(ring + i * kTileBytes, bars + i, c, t0 + warp + i * kTmaWarps);
+        s = ns, d = nd, k = nk, o = no, ts = nt, te = ne;
+        tile = next;
+        if constexpr (kHot) {
+            if ((r + 1) % kEpochRounds == 0 && r + 1 < rounds) {
+                __syncthreads();
+                hot_normalize(h, hot, P);
+                __syncthreads();
+            }
         }
-    } else {
-        for (uint32_t i = 0; i < kRing; ++i) {
-            if (i < mine) async_tile(ring + i * kTileBytes, col, seg_bytes, lane_off, t0 + warp + i * kTmaWarps);
-            else asm volatile("cp.async.commit_group;" ::: "memory");
-        }
-    }
-    __syncwarp();
-    Ctr t;
-    for (uint32_t i = 0; i < mine; ++i) {
-        const uint32_t st = i % kRing;
-        unsigned char* sb = ring + st * kTileBytes;
-        if constexpr (kBulk) {
-            mbar_wait(bars + st, (i / kRing) & 1u);
-        } else {
-            asm volatile("cp.async.wait_group %0;" ::"n"(kRing - 1) : "memory");
-            __syncwarp();
-        }
-        const uint2 s = *reinterpret_cast<const uint2*>(sb + 8 * lane);
-        const uint2 d = *reinterpret_cast<const uint2*>(sb + 256 + 8 * lane);
-        const uint2 k = *reinterpret_cast<const uint2*>(sb + 512 + 8 * lane);
-        const uint2 o = *reinterpret_cast<const uint2*>(sb + 768 + 8 * lane);
-        const ulonglong2 ts = *reinterpret_cast<const ulonglong2*>(sb + 1024 + 16 * lane);
-        const ulonglong2 te = *reinterpret_cast<const ulonglong2*>(sb + 1536 + 16 * lane);
-        __syncwarp();
-        if constexpr (kBulk) {
-            if (lane == 0 && i + kRing < mine) issue_tile(sb, bars + st, c, t0 + warp + (i + kRing) * kTmaWarps);
-        } else {
-            if (i + kRing < mine) async_tile(sb, col, seg_bytes, lane_off, t0 + warp + (i + kRing) * kTmaWarps);
-            else asm volatile("cp.async.commit_group;" ::: "memory");
-        }
-        const uint64_t dx = te.x - ts.x, dy = te.y - ts.y;
-        const uint32_t cx = stage_a<kSmem>(s.x, d.x, k.x, o.x, dx, p, gt, t);
-        const uint32_t cy = stage_a<kSmem>(s.y, d.y, k.y, o.y, dy, p, gt, t);
-        push(cx, o.x, dx, wq, lane);
-        push(cy, o.y, dy, wq, lane);
-        drain_full<kSmem, kHot>(wq, lane, gt, p, P, h, t);
     }
     if (blockIdx.x == gridDim.x - 1 && warp == 0)
         run_scalar<1, kSmem, kHot>(b, tiles << 6, c.n, 32, lane, gt, p, P, h, t, wq);
@@ -878,7 +713,7 @@ __global__ void __launch_bounds__(kTmaBlock, 1) k2_tma(DevBatch b, const uint32_
 // scalar (3) loads. CTA b owns records [b*n/G, (b+1)*n/G) (at most
 // kCtaRecords), one record per lane per round.
 template <int kLayout, bool kSmem, bool kHot>
-__global__ void __launch_bounds__(kK2Block, 2) k2_gen(DevBatch b, const uint32_t* __restrict__ gt,
+__global__ void __launch_bounds__(kK2Block, 1) k2_gen(DevBatch b, const uint32_t* __restrict__ gt,
                                                     uint32_t table_words, DevParams p,
                                                     DevPartials P, DevHot hot, DevLog L) {
     HotSmem h{};
@@ -1269,9 +1104,6 @@ cudaError_t allow_smem(K kernel) {
 template <int L, bool kS, bool kH>
 constexpr auto k2_kernel() {
     if constexpr (L == 0) return k2_soa<kS, kH>;
-    else if constexpr (L == 4) return k2_soa_pf<kS, kH>;
-    else if constexpr (L == 5) return k2_tma<kS, kH, true>;
-    else if constexpr (L == 6) return k2_tma<kS, kH, false>;
     else return k2_gen<L, kS, kH>;
 }
 
@@ -1323,59 +1155,29 @@ cudaError_t init_kernel_attributes() {
     if ((e = allow_layout<1>())) return e;
     if ((e = allow_layout<2>())) return e;
     if ((e = allow_layout<3>())) return e;
-    if ((e = allow_layout<4>())) return e;
-    if ((e = allow_layout<5>())) return e;
-    if ((e = allow_layout<6>())) return e;
     if ((e = allow_smem(k_sample<true>))) return e;
     return allow_smem(k_classify<true>);
 }
 
-LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool hot, int* occ_cache,
-                    int variant) {
+LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool hot, int* occ_cache) {
+    (void)occ_cache;
     LaunchCfg c;
-    c.variant = variant;
     const size_t tbytes = table_smem_bytes(table_words);
-    if ((variant == 2 || variant == 3) && k2_layout(b) == 0) {
-        // TMA-staged: one 768-thread CTA per SM, < 2^16 records per CTA.
-        const size_t fixed = (hot ? kHotBytes : 0) + kTmaFixed;
-        if (fixed + 1024 <= kSmemMax) {
-            c.block = kTmaBlock;
-            c.table_in_smem = tbytes + fixed + 1024 <= kSmemMax;
-            c.smem = fixed + (c.table_in_smem ? tbytes : 0);
-            const uint64_t resident = static_cast<uint64_t>(sm_count(device));
-            const uint64_t cap = static_cast<uint64_t>(kCtaTiles) * 64;
-            uint64_t grid = (b.n + cap - 1) / cap;
-            grid = grid <= resident ? std::min<uint64_t>(resident, std::max<uint64_t>(grid, (b.n + 16383) / 16384))
-                                    : (grid + resident - 1) / resident * resident;
-            c.grid = static_cast<int>(std::max<uint64_t>(1, grid));
-            return c;
-        }
-        c.variant = 0;
-    }
     c.block = kK2Block;
     c.table_in_smem = tbytes <= kSmemTableMax;
     c.smem = (c.table_in_smem ? tbytes : 0) + (hot ? kHotBytes : 0) + kQueueBytes;
-    int per_sm = occ_cache ? occ_cache[hot ? 1 : 0] : 0;
-    if (per_sm <= 0) {
-        if (c.table_in_smem)
-            per_sm = hot ? occupancy(k2_soa<true, true>, c.block, c.smem)
-                         : occupancy(k2_soa<true, false>, c.block, c.smem);
-        else
-            per_sm = hot ? occupancy(k2_soa<false, true>, c.block, c.smem)
-                         : occupancy(k2_soa<false, false>, c.block, c.smem);
-        if (occ_cache) occ_cache[hot ? 1 : 0] = per_sm;
-    }
-    const uint64_t resident = static_cast<uint64_t>(per_sm) * sm_count(device);
-    // A CTA takes at most kCtaRecords records (the hot limbs' bound). Beyond
-    // one resident wave the grid is a whole number of waves; below it, at
-    // least 16 records per thread so the per-CTA table load amortises.
-    const uint64_t cap = k2_layout(b) == 0 ? static_cast<uint64_t>(kCtaTiles) * 64 : kCtaRecords;
-    uint64_t grid = (b.n + cap - 1) / cap;
-    if (grid <= resident) {
-        const uint64_t per_block = static_cast<uint64_t>(c.block) * 16;
-        grid = std::max(grid, std::min(resident, (b.n + per_block - 1) / per_block));
+    const uint64_t sms = static_cast<uint64_t>(sm_count(device));
+    // At least 16 records per thread so the per-CTA table load amortises.
+    const uint64_t per_block = static_cast<uint64_t>(c.block) * 16;
+    const uint64_t want = (b.n + per_block - 1) / per_block;
+    uint64_t grid;
+    if (k2_layout(b) == 0) {
+        grid = std::min(sms, want); // persistent, one CTA per SM
     } else {
-        grid = (grid + resident - 1) / resident * resident;
+        // k2_gen: < 2^16 records per CTA (the hot limbs' bound); beyond one
+        // wave, a whole number of waves.
+        grid = (b.n + kCtaRecords - 1) / kCtaRecords;
+        grid = grid <= sms ? std::max(grid, std::min(sms, want)) : (grid + sms - 1) / sms * sms;
     }
     c.grid = static_cast<int>(std::max<uint64_t>(1, grid));
     return c;
@@ -1428,10 +1230,7 @@ cudaError_t launch_k2(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t
                       const DevLog& log, cudaStream_t s) {
     switch (k2_layout(b)) {
     case 0:
-        if (cfg.variant == 1) launch_k2_l<4>(cfg, b, t, p, P, hot, log, s);
-        else if (cfg.variant == 2) launch_k2_l<5>(cfg, b, t, p, P, hot, log, s);
-        else if (cfg.variant == 3) launch_k2_l<6>(cfg, b, t, p, P, hot, log, s);
-        else launch_k2_l<0>(cfg, b, t, p, P, hot, log, s);
+        launch_k2_l<0>(cfg, b, t, p, P, hot, log, s);
         break;
     case 1: launch_k2_l<1>(cfg, b, t, p, P, hot, log, s); break;
     case 2: launch_k2_l<2>(cfg, b, t, p, P, hot, log, s); break;

@@ -28,8 +28,8 @@ constexpr uint32_t kLogSiteShift = 14;
 constexpr uint32_t kLogPackedSites = 1u << 18;
 constexpr uint64_t kMinInitBits = 0x7FF0000000000000ull; // +inf: empty min
 constexpr uint64_t kMaxInitBits = 0;                     // +0.0: empty max (rates are > 0)
-constexpr uint32_t kHotSlots = 512;   // block-private accumulators for hot sites
-constexpr uint32_t kHotStride = 520;  // kHotSlots + 1 (slot 0 = cold), padded
+constexpr uint32_t kHotSlots = 2047;  // block-private accumulators for hot sites (11 slot bits)
+constexpr uint32_t kHotStride = 2048; // kHotSlots + 1 (slot 0 = cold)
 
 struct DevParams {
     uint64_t ack_plus1;       // ack_avg_size_max + 1, u64 (rate_engine.cpp:78)
@@ -104,8 +104,6 @@ struct LaunchCfg {
     int block;
     size_t smem;
     bool table_in_smem;
-    int variant; // aligned SoA: 0 register double-buffered loads, 1 TMA L2 prefetch,
-                 // 2 TMA bulk copies into per-warp shared-memory rings
 };
 
 // Once per device: opt the shared-memory kernels into large dynamic smem.
@@ -113,8 +111,7 @@ cudaError_t init_kernel_attributes();
 
 // Occupancy-derived launch configuration for K2 over n records.
 // occ_cache[hot] memoises blocks/SM (0 = unknown) for this table size.
-LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool hot, int* occ_cache,
-                    int variant = 0);
+LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool hot, int* occ_cache);
 
 // K1 (optional, skewed batches): sample the batch, pick the hot sites and
 // write their slots into the table words. Returns false when the batch is

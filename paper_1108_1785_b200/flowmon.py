@@ -493,7 +493,10 @@ class Engine:
         return {"accumulate_ms": t.accumulate_ms, "finalize_ms": t.finalize_ms,
                 "h2d_ms": t.h2d_ms, "k2_launches": t.k2_launches,
                 "kernel_launches": t.kernel_launches, "records": t.records,
-                "plan_ms": t.plan_ms}
+                "plan_ms": t.plan_ms, "total_plan_ms": t.total_plan_ms,
+                "total_accumulate_ms": t.total_accumulate_ms,
+                "total_finalize_ms": t.total_finalize_ms, "total_finalizes": t.total_finalizes,
+                "total_k2_launches": t.total_k2_launches}
 
     @staticmethod
     def _params(params: Optional[FilterParams]) -> gnm_filter_params:

@@ -193,25 +193,20 @@ def test_state_resets_between_calls(engine, orc):
     np.testing.assert_array_equal(r3.table, r.table)
 
 
-@pytest.mark.parametrize("variant", ["reg", "l2", "tma", "async"])
-def test_k2_variants_bit_exact(orc, variant, monkeypatch):
-    """Every K2 load-pipeline variant (GNM_K2_VARIANT, read at context
-    creation) gives the oracle's result: register double-buffering, TMA L2
-    prefetch, TMA bulk-copy rings and cp.async rings. Sizes cover several
-    CTAs, ring wrap-around and the < 64-record remainder."""
-    from paper_1108_1785_b200 import Engine
-    monkeypatch.setenv("GNM_K2_VARIANT", variant)
-    with Engine(0) as eng:
-        sites, cols = parity.engine_stress_set(300_007, seed=23)
-        cat = catalog_of(sites)
-        res = eng.aggregate(FlowBatch(*cols).to_device(), cat, histograms=True)
-        parity.assert_matches_oracle(res, parity.oracle_reference(orc, cat, cols))
-        w = synth.workload("D3")
-        cols = synth.generate(w, 3_000_001)
-        cat = layout_catalog(w.sites)
-        res = eng.aggregate(FlowBatch(*cols).to_device(), cat)
-        parity.assert_matches_oracle(res, parity.oracle_reference(orc, cat, cols))
-        tsites, tcols = parity.tiny_duration_set()
-        tcat = catalog_of(tsites)
-        res = eng.aggregate(FlowBatch(*tcols).to_device(), tcat, FilterParams(min_duration_ms=0, min_packets=1))
-        parity.assert_matches_oracle(res, parity.oracle_reference(orc, tcat, tcols, (96, 1, 0)))
+@pytest.mark.parametrize("n", [300_007, 12_000_001])
+def test_multi_cta_remainders_and_epochs(engine, orc, n):
+    """Sizes that span several persistent CTAs, the < 64-record remainder
+    and (12M: > 29 rounds of 32 tiles per CTA) K2 epochs with limb
+    normalization, on the engine stress set (full-range octets push the
+    16-bit limbs of the few hot sites past the flush bound) and the D3
+    shape."""
+    sites, cols = parity.engine_stress_set(n, seed=23)
+    cat = catalog_of(sites)
+    res = engine.aggregate(FlowBatch(*cols).to_device(), cat, histograms=(n < 1_000_000))
+    parity.assert_matches_oracle(res, parity.oracle_reference(orc, cat, cols),
+                                 check_hist=(n < 1_000_000))
+    w = synth.workload("D3")
+    cols = synth.generate(w, n)
+    cat = layout_catalog(w.sites)
+    res = engine.aggregate(FlowBatch(*cols).to_device(), cat)
+    parity.assert_matches_oracle(res, parity.oracle_reference(orc, cat, cols))

@@ -36,7 +36,7 @@ if has launches; then
   echo "ncu launches exit $?" | tee -a gpurun_out/status.txt
 fi
 if has full; then
-  timeout 1200 $NCU --set full --clock-control none --import-source on -k regex:k2 -s 3 -c 1 \
+  timeout 1200 $NCU --set full --clock-control none --import-source on -k regex:k2_soa -s 3 -c 1 \
       -f -o gpurun_out/prof_k2 \
       python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/prof_k2.log 2>&1
   echo "ncu full exit $?" | tee -a gpurun_out/status.txt
