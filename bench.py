@@ -203,9 +203,12 @@ def run_reference_arm(args):
     nproc = os.cpu_count() or 1
     R, cat, rec = reference_sample(w, args.cpu_sample)
     workers = reference_workers(args.cpu_sample, nproc)
-    # Pick the fastest worker count on one probe run each (the reference gets
-    # slower with more workers on shuffled data).
-    probe = {wk: R.time_range(rec, cat, 0, args.cpu_sample, wk) for wk in workers}
+    # Pick the fastest worker count (the reference gets slower with more
+    # workers on shuffled data): one warm-up run first (page
+    # faults, allocator), then the median of two runs per worker count.
+    R.time_range(rec, cat, 0, args.cpu_sample, 1)
+    probe = {wk: statistics.median(R.time_range(rec, cat, 0, args.cpu_sample, wk) for _ in range(2))
+             for wk in workers}
     best = min(probe, key=probe.get)
     for _ in range(args.warmup):
         R.time_range(rec, cat, 0, args.cpu_sample, best)

@@ -29,7 +29,7 @@ def launches(path):
         if len(r) > vi:
             name = r[ki].split("(")[0].replace("void ", "").split("::")[-1]
             t = float(r[vi].replace(",", ""))
-            if name.startswith("k2") and t > 1e6:
+            if name.startswith("k2") and t > 3e5:
                 name += " [full batch]"
             elif name.startswith("k2"):
                 name += " [e2e chunk]"
