@@ -578,21 +578,8 @@ int finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* r) {
     }
     clear_log(c);
     ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
-    for (uint32_t s = 0; s < n_sites; ++s) {
-        gnm_site_stats o = c->h_out[s];
-        // stats_from (rate_engine.cpp:250): avg = (double(u128)/1e6)/count,
-        // converted on the host exactly as the reference (libgcc RNE).
-        if (o.flow_count) {
-            // Both conversions round to nearest-even, so the hardware u64 path
-            // equals libgcc's __floatuntidf whenever the sum fits 64 bits.
-            const double sum = o.rate_ubps_hi == 0
-                                   ? static_cast<double>(o.rate_ubps_lo)
-                                   : static_cast<double>(static_cast<unsigned __int128>(o.rate_ubps_hi) << 64 |
-                                                         o.rate_ubps_lo);
-            o.avg_bps = (sum / 1e6) / static_cast<double>(o.flow_count);
-        }
-        r->sites[s] = o;
-    }
+    // K3b computed every field, avg included (rounded like the host's libgcc).
+    if (n_sites) std::memcpy(r->sites, c->h_out, static_cast<size_t>(n_sites) * sizeof(gnm_site_stats));
     const auto* t = reinterpret_cast<const uint64_t*>(c->h_out + n_sites);
     r->tallies.forward = t[0];
     r->tallies.pure_ack = t[1];

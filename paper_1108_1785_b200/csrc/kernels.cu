@@ -68,6 +68,7 @@ constexpr uint32_t kCoarseSlots = 32;
 constexpr uint32_t kHeavy = 64;
 constexpr uint32_t kHeavyNone = 0xFFFFFFu;
 constexpr uint64_t kHeavyMin = 1u << 16;
+constexpr uint32_t kLogChunk = 2048; // K2b work-item size
 constexpr size_t kHotBytes = kHotStride * (5 * 4 + 2 * 8) + kCoarseSlots * kCoarse * 4;
 constexpr size_t kSmemMax = 227 * 1024;
 constexpr size_t kQueueBytes = kWarps * kQueue * 16;
@@ -242,11 +243,6 @@ __device__ __forceinline__ uint32_t bucket_of_ubps(uint64_t lo, uint64_t hi) {
     return (hi || b >= 10000u) ? 10000u : static_cast<uint32_t>(b);
 }
 
-// bucket_index on a double (K3: the buckets of the min/max rates).
-__device__ __forceinline__ uint32_t bucket_of(double rate) {
-    const double b = __ddiv_rn(rate, 10000.0);
-    return b >= 10000.0 ? 10000u : static_cast<uint32_t>(b);
-}
 
 // ---- per-record classification (stage A, every lane) -----------------------
 // Per-lane tallies (ClassTallies, rate_engine.hpp:101-110).
@@ -437,13 +433,21 @@ __device__ __forceinline__ void push(uint32_t code, uint32_t oct, uint64_t dur, 
     wq.n += __popc(m);
 }
 
+// The drained Forward flows' entries, compacted (Unmatched lanes write none);
+// every lane of the warp calls this.
 __device__ __forceinline__ void log_entry(WarpQueue& wq, uint32_t lane, uint32_t site, uint32_t bucket) {
-    if (wq.logb) {
-        __stcs(wq.log + wq.pos + lane, site == kNone ? kLogSkip : site);
-        __stcs(wq.logb + wq.pos + lane, bucket);
-    } else {
-        __stcs(wq.log + wq.pos + lane, site == kNone ? kLogSkip : site << kLogSiteShift | bucket);
+    const bool v = site != kNone;
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, v);
+    if (v) {
+        const uint32_t i = wq.pos + __popc(m & ((1u << lane) - 1u));
+        if (wq.logb) {
+            __stcs(wq.log + i, site);
+            __stcs(wq.logb + i, bucket);
+        } else {
+            __stcs(wq.log + i, site << kLogSiteShift | bucket);
+        }
     }
+    wq.pos += __popc(m);
 }
 
 template <bool kSmem, bool kHot>
@@ -459,7 +463,6 @@ __device__ __forceinline__ void drain_full(WarpQueue& wq, uint32_t lane,
         const uint32_t site =
             accumulate<kSmem, kHot>(x.x, x.y, static_cast<uint64_t>(x.w) << 32 | x.z, gt, p, P, h, c, bucket);
         log_entry(wq, lane, site, bucket);
-        wq.pos += 32;
     }
 }
 
@@ -468,14 +471,12 @@ __device__ __forceinline__ void drain_rest(WarpQueue& wq, uint32_t lane,
                                            const uint32_t* __restrict__ gt, const DevParams& p,
                                            const DevPartials& P, const HotSmem& h, Ctr& c) {
     __syncwarp();
+    uint32_t site = kNone, bucket = 0;
     if (lane < wq.n) {
         const uint4 x = wq.q[lane];
-        uint32_t bucket;
-        const uint32_t site =
-            accumulate<kSmem, kHot>(x.x, x.y, static_cast<uint64_t>(x.w) << 32 | x.z, gt, p, P, h, c, bucket);
-        log_entry(wq, lane, site, bucket);
+        site = accumulate<kSmem, kHot>(x.x, x.y, static_cast<uint64_t>(x.w) << 32 | x.z, gt, p, P, h, c, bucket);
     }
-    wq.pos += wq.n;
+    log_entry(wq, lane, site, bucket);
     wq.n = 0;
 }
 
@@ -930,52 +931,78 @@ __global__ void __launch_bounds__(128) k3a_median_sb(DevPartials P) {
     }
 }
 
-// K2b: one launch's log, warp per region, 8 entries per lane in flight: the
-// entries that fall into their site's median super-bucket count into its 64
-// fine buckets -- in shared memory for the heavy sites (flushed once per
-// CTA, persistent grid), with L2 reductions for the rest.
+// K2b: one launch's log, the entries that fall into their site's median
+// super-bucket count into its 64 fine buckets -- in shared memory for the
+// heavy sites (flushed once per CTA, persistent grid), with L2 reductions
+// for the rest. Work item = (region, chunk of kLogChunk entries), many
+// warps per region; each lane reads 4 entries per LDG.128 (region bases are
+// multiples of 4 entries), 4 of those in flight. kMap: each site's
+// (median super-bucket | heavy row << 8) in shared memory (small
+// registries), else read from L2/L1.
+constexpr uint32_t kMapSites = 12288; // 24 KB of static shared memory
+template <bool kMap, bool kWide>
 __global__ void __launch_bounds__(512, 2) k2b_fine(DevPartials P, DevLog L) {
     __shared__ uint32_t hf[kHeavy * kFineW];
     __shared__ uint32_t hsite[kHeavy];
+    __shared__ uint16_t map[kMap ? kMapSites : 1];
     for (uint32_t i = threadIdx.x; i < kHeavy * kFineW; i += blockDim.x) hf[i] = 0;
+    if constexpr (kMap)
+        for (uint32_t i = threadIdx.x; i < P.n_sites; i += blockDim.x) {
+            const uint32_t m = __ldg(P.msb + i);
+            const uint32_t hh = m >> 8;
+            map[i] = static_cast<uint16_t>((m & 0xFFu) | (hh == kHeavyNone ? 0xFF00u : hh << 8));
+        }
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    constexpr uint32_t kU = 16;
-    for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < L.regions; r += nwarps) {
-        const uint32_t cnt = L.counts[r];
+    const uint32_t chunks = (L.warp_cap + kLogChunk - 1) / kLogChunk;
+    const uint32_t items = L.regions * chunks;
+    constexpr uint32_t kV = kWide ? 4 : 8; // LDG.128 per lane in flight
+    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < items; w += nwarps) {
+        const uint32_t r = w / chunks;
+        const uint32_t c0 = (w % chunks) * kLogChunk;
+        const uint32_t cnt = min(L.counts[r], c0 + kLogChunk);
         const unsigned int* e = L.entries + static_cast<size_t>(r) * L.warp_cap;
-        const unsigned int* eb = L.buckets ? L.buckets + static_cast<size_t>(r) * L.warp_cap : nullptr;
-        for (uint32_t base = 0; base < cnt; base += 32 * kU) {
-            uint32_t x[kU], b[kU];
+        const unsigned int* eb = kWide ? L.buckets + static_cast<size_t>(r) * L.warp_cap : nullptr;
+        for (uint32_t base = c0; base < cnt; base += 32 * 4 * kV) {
+            uint4 x[kV], bb[kWide ? kV : 1];
 #pragma unroll
-            for (uint32_t u = 0; u < kU; ++u) {
-                const uint32_t i = base + u * 32 + lane;
-                x[u] = i < cnt ? __ldcs(e + i) : kLogSkip;
+            for (uint32_t u = 0; u < kV; ++u) {
+                const uint32_t i = base + (u * 32 + lane) * 4;
+                x[u] = i < cnt ? __ldcs(reinterpret_cast<const uint4*>(e + i)) : make_uint4(0, 0, 0, 0);
+                if constexpr (kWide)
+                    bb[u] = i < cnt ? __ldcs(reinterpret_cast<const uint4*>(eb + i)) : make_uint4(0, 0, 0, 0);
             }
-            if (eb) {
 #pragma unroll
-                for (uint32_t u = 0; u < kU; ++u) {
-                    const uint32_t i = base + u * 32 + lane;
-                    b[u] = i < cnt ? __ldcs(eb + i) : 0u;
+            for (uint32_t u = 0; u < kV; ++u) {
+                const uint32_t i = base + (u * 32 + lane) * 4;
+                const uint32_t xs[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+                uint32_t bs[4] = {0, 0, 0, 0};
+                if constexpr (kWide) {
+                    bs[0] = bb[u].x, bs[1] = bb[u].y, bs[2] = bb[u].z, bs[3] = bb[u].w;
                 }
-            }
-            uint32_t site[kU], m[kU];
 #pragma unroll
-            for (uint32_t u = 0; u < kU; ++u) {
-                site[u] = eb ? x[u] : x[u] >> kLogSiteShift;
-                if (!eb) b[u] = x[u] & ((1u << kLogSiteShift) - 1u);
-                m[u] = x[u] == kLogSkip ? kLogSkip : __ldg(P.msb + site[u]);
-            }
-#pragma unroll
-            for (uint32_t u = 0; u < kU; ++u) {
-                if (x[u] == kLogSkip || (b[u] >> 6) != (m[u] & 0xFFu)) continue;
-                const uint32_t h = m[u] >> 8;
-                if (h != kHeavyNone) {
-                    red_add_shared(hf + h * kFineW + (b[u] & 63u), 1u);
-                    hsite[h] = site[u]; // every writer stores the same value
-                } else {
-                    red_add(P.fine + static_cast<size_t>(site[u]) * kFineW + (b[u] & 63u), 1u);
+                for (uint32_t q = 0; q < 4; ++q) {
+                    if (i + q >= cnt) continue;
+                    const uint32_t site = kWide ? xs[q] : xs[q] >> kLogSiteShift;
+                    const uint32_t bk = kWide ? bs[q] : xs[q] & ((1u << kLogSiteShift) - 1u);
+                    uint32_t msb, hh;
+                    if constexpr (kMap) {
+                        const uint32_t m = map[site];
+                        msb = m & 0xFFu;
+                        hh = m >> 8;
+                    } else {
+                        const uint32_t m = __ldg(P.msb + site);
+                        msb = m & 0xFFu;
+                        hh = (m >> 8) == kHeavyNone ? 0xFFu : m >> 8;
+                    }
+                    if ((bk >> 6) != msb) continue;
+                    if (hh != 0xFFu) {
+                        red_add_shared(hf + hh * kFineW + (bk & 63u), 1u);
+                        hsite[hh] = site; // every writer stores the same value
+                    } else {
+                        red_add(P.fine + static_cast<size_t>(site) * kFineW + (bk & 63u), 1u);
+                    }
                 }
             }
         }
@@ -983,6 +1010,25 @@ __global__ void __launch_bounds__(512, 2) k2b_fine(DevPartials P, DevLog L) {
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < kHeavy * kFineW; i += blockDim.x)
         if (hf[i]) red_add(P.fine + static_cast<size_t>(hsite[i / kFineW]) * kFineW + (i % kFineW), hf[i]);
+}
+
+// stats_from's avg (rate_engine.cpp:250; sum_bps rate_engine.hpp:62):
+// (double(u128 sum) / 1e6) / double(count), each step rounded to nearest
+// even like the host (libgcc __floatuntidf): a sum of >= 2^64 keeps its top
+// 64 bits with the shifted-out bits folded into a sticky LSB, which rounds
+// to 53 bits exactly as the 128-bit value would, then scales by 2^shift.
+__device__ __forceinline__ double avg_of(uint64_t lo, uint64_t hi, uint64_t count) {
+    double sum;
+    if (hi == 0) {
+        sum = __ull2double_rn(lo);
+    } else {
+        const int lz = __clzll(static_cast<long long>(hi));
+        const int sh = 64 - lz;
+        const uint64_t top = (hi << lz) | (lo >> sh);
+        const uint64_t sticky = (lo << lz) != 0 ? 1u : 0u;
+        sum = ldexp(__ull2double_rn(top | sticky), sh);
+    }
+    return __ddiv_rn(__ddiv_rn(sum, 1e6), __ull2double_rn(count));
 }
 
 // K3b, thread per site: count (coarse), the exact median bucket from the
@@ -1040,7 +1086,7 @@ __global__ void __launch_bounds__(128) k3b_finalize(DevPartials P, double thresh
                 o.rate_ubps_hi = static_cast<uint64_t>(u >> 64);
                 o.min_bps = mn;
                 o.max_bps = mx;
-                o.avg_bps = 0; // host: double(u128)/1e6/count, libgcc rounding
+                o.avg_bps = avg_of(static_cast<uint64_t>(u), static_cast<uint64_t>(u >> 64), cnt);
                 o.median_bps = med;
                 o.below_threshold = med < threshold ? 1u : 0u; // monitor.cpp:22
             }
@@ -1189,9 +1235,10 @@ bool plan_hot(int device, const DevBatch& b, const DevTable& t, const DevParams&
     (void)device;
     *err = cudaSuccess;
     if (!t.packed || n_sites == 0 || b.n == 0) return false;
-    // Sample 1/64 of the batch (at most 256k records) in 64 contiguous chunks.
-    const uint32_t chunks = 64;
+    // Sample 1/64 of the batch (at most 256k records) in 16..256 contiguous
+    // chunks of about 1024 records (one CTA each).
     uint64_t sample = std::min<uint64_t>(262144, b.n / 64);
+    const uint32_t chunks = static_cast<uint32_t>(std::min<uint64_t>(256, std::max<uint64_t>(16, sample / 1024)));
     uint32_t chunk_len = static_cast<uint32_t>(sample / chunks);
     uint32_t thr;
     if (force) {
@@ -1211,11 +1258,9 @@ bool plan_hot(int device, const DevBatch& b, const DevTable& t, const DevParams&
     uint32_t* hot_site = site_slot + n_sites;
     const uint64_t stride = std::max<uint64_t>(b.n / chunks, chunk_len);
     const uint32_t nchunks = static_cast<uint32_t>(std::min<uint64_t>(chunks, b.n / chunk_len));
-    const size_t tbytes = table_smem_bytes(t.n_words);
-    if (tbytes <= kSmemTableMax)
-        k_sample<true><<<nchunks, kK2Block, tbytes, s>>>(b, t.words, t.n_words, p, stride, chunk_len, cnt);
-    else
-        k_sample<false><<<nchunks, kK2Block, 0, s>>>(b, t.words, t.n_words, p, stride, chunk_len, cnt);
+    // The sample is small: probe the table through L1 rather than copying
+    // it into every CTA's shared memory.
+    k_sample<false><<<nchunks, kK2Block, 0, s>>>(b, t.words, t.n_words, p, stride, chunk_len, cnt);
     k_hot_select<<<1, kSelectBlock, 0, s>>>(cnt, n_sites, thr, site_slot, hot_site);
     const uint32_t span = t.n_words - t.node_begin;
     const uint32_t rg = std::max<uint32_t>(1, std::min<uint32_t>((span + 255) / 256, 1024));
@@ -1266,10 +1311,16 @@ cudaError_t launch_k3a(int device, const DevPartials& P, cudaStream_t s) {
 
 cudaError_t launch_k2b(int device, const DevPartials& P, const DevLog& log, cudaStream_t s) {
     if (log.regions == 0) return cudaSuccess;
-    // Persistent: a few CTAs per SM, so the heavy rows flush rarely.
-    const uint32_t grid = std::min<uint32_t>(small_grid(device, static_cast<uint64_t>(log.regions) * 32, 512),
-                                             static_cast<uint32_t>(sm_count(device)) * 2);
-    k2b_fine<<<grid, 512, 0, s>>>(P, log);
+    // Persistent: two CTAs per SM, so the heavy rows flush rarely.
+    const uint32_t grid = static_cast<uint32_t>(sm_count(device)) * 2;
+    const bool wide = log.buckets != nullptr;
+    if (P.n_sites <= kMapSites) {
+        if (wide) k2b_fine<true, true><<<grid, 512, 0, s>>>(P, log);
+        else k2b_fine<true, false><<<grid, 512, 0, s>>>(P, log);
+    } else {
+        if (wide) k2b_fine<false, true><<<grid, 512, 0, s>>>(P, log);
+        else k2b_fine<false, false><<<grid, 512, 0, s>>>(P, log);
+    }
     return cudaGetLastError();
 }
 

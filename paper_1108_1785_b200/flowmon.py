@@ -511,11 +511,11 @@ class Engine:
             b = batch._c()
             _check(lib.gnm_accumulate(self._h, catalog.handle, C.byref(p), C.byref(b)))
 
-    def finalize(self, catalog: SiteCatalog, window_start_ms: int = 0, window_end_ms: int = 0,
-                 threshold_bps: float = kDefaultWarnThresholdBps,
-                 histograms: bool = False) -> AnalysisResult:
+    def _result(self, catalog: SiteCatalog, window_start_ms: int, window_end_ms: int,
+                threshold_bps: float, histograms: bool):
         n = catalog.site_count()
-        table = np.zeros(max(n, 1), SITE_STATS_DTYPE)
+        # gnm_finalize writes every row: no zero-fill on the step's critical path.
+        table = np.empty(max(n, 1), SITE_STATS_DTYPE)
         hist = np.zeros((max(n, 1), BUCKET_COUNT), np.uint32) if histograms else None
         r = gnm_result()
         r.window_start_ms = window_start_ms
@@ -524,6 +524,13 @@ class Engine:
         r.sites_capacity = len(table)
         r.sites = table.ctypes.data
         r.histograms = hist.ctypes.data if hist is not None else None
+        return r, table, hist, n
+
+    def finalize(self, catalog: SiteCatalog, window_start_ms: int = 0, window_end_ms: int = 0,
+                 threshold_bps: float = kDefaultWarnThresholdBps,
+                 histograms: bool = False) -> AnalysisResult:
+        r, table, hist, n = self._result(catalog, window_start_ms, window_end_ms, threshold_bps,
+                                         histograms)
         _check(lib.gnm_finalize(self._h, catalog.handle, C.byref(r)))
         return _build_result(r, table[:n], None if hist is None else hist[:n])
 
@@ -536,9 +543,16 @@ class Engine:
                   histograms: bool = False) -> AnalysisResult:
         """rate_engine.hpp:143-146. ``workers``/``mode`` are accepted and ignored:
         results are identical for any worker count and lookup mode by contract
-        (SPEC.md:310, engine_test.cpp:344-360)."""
-        self.accumulate(view, catalog, params)
-        return self.finalize(catalog, window_start_ms, window_end_ms, threshold_bps, histograms)
+        (engine_test.cpp:344-360). One gnm_analyze call."""
+        p = self._params(params)
+        b = view._c()
+        r, table, hist, n = self._result(catalog, window_start_ms, window_end_ms, threshold_bps,
+                                         histograms)
+        if isinstance(view, FlowRecords):
+            _check(lib.gnm_analyze_aos(self._h, catalog.handle, C.byref(p), C.byref(b), C.byref(r)))
+        else:
+            _check(lib.gnm_analyze(self._h, catalog.handle, C.byref(p), C.byref(b), C.byref(r)))
+        return _build_result(r, table[:n], None if hist is None else hist[:n])
 
     def partials(self, catalog: SiteCatalog) -> dict:
         """Device pointers of the accumulation (gnm_get_partials) for a
