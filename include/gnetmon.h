@@ -199,6 +199,20 @@ int gnm_analyze_aos(gnm_ctx* ctx, const gnm_registry* reg, const gnm_filter_para
  * (K3 + result D2H + partial reset; synchronous). */
 int gnm_accumulate(gnm_ctx* ctx, const gnm_registry* reg, const gnm_filter_params* params,
                    const gnm_batch_soa* batch);
+/* FlowStore::snapshot(window_start_ms, window_end_ms) fused into the
+ * accumulation (flow_store.cpp:62-80): only records with end_ms in
+ * [window_start_ms, window_end_ms) are classified or counted, as if the
+ * reference's aggregate ran on the snapshot's copy. */
+int gnm_accumulate_window(gnm_ctx* ctx, const gnm_registry* reg, const gnm_filter_params* params,
+                          const gnm_batch_soa* batch, uint64_t window_start_ms,
+                          uint64_t window_end_ms);
+int gnm_accumulate_window_aos(gnm_ctx* ctx, const gnm_registry* reg, const gnm_filter_params* params,
+                              const gnm_batch_aos* batch, uint64_t window_start_ms,
+                              uint64_t window_end_ms);
+/* snapshot(result->window_start_ms, result->window_end_ms) + aggregate + finalize in one call:
+ * monitor.cpp:109-120 (run_cycle) on the GPU. */
+int gnm_analyze_window(gnm_ctx* ctx, const gnm_registry* reg, const gnm_filter_params* params,
+                       const gnm_batch_soa* batch, gnm_result* result);
 int gnm_accumulate_aos(gnm_ctx* ctx, const gnm_registry* reg, const gnm_filter_params* params,
                        const gnm_batch_aos* batch);
 int gnm_finalize(gnm_ctx* ctx, const gnm_registry* reg, gnm_result* result);

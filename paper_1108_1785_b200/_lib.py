@@ -143,6 +143,12 @@ _SIGS = [
     ("gnm_analyze_aos", C.c_int,
      [_P, _P, C.POINTER(gnm_filter_params), C.POINTER(gnm_batch_aos), C.POINTER(gnm_result)]),
     ("gnm_accumulate", C.c_int, [_P, _P, C.POINTER(gnm_filter_params), C.POINTER(gnm_batch_soa)]),
+    ("gnm_accumulate_window", C.c_int,
+     [_P, _P, C.POINTER(gnm_filter_params), C.POINTER(gnm_batch_soa), C.c_uint64, C.c_uint64]),
+    ("gnm_accumulate_window_aos", C.c_int,
+     [_P, _P, C.POINTER(gnm_filter_params), C.POINTER(gnm_batch_aos), C.c_uint64, C.c_uint64]),
+    ("gnm_analyze_window", C.c_int,
+     [_P, _P, C.POINTER(gnm_filter_params), C.POINTER(gnm_batch_soa), C.POINTER(gnm_result)]),
     ("gnm_accumulate_aos", C.c_int,
      [_P, _P, C.POINTER(gnm_filter_params), C.POINTER(gnm_batch_aos)]),
     ("gnm_finalize", C.c_int, [_P, _P, C.POINTER(gnm_result)]),

@@ -167,6 +167,8 @@ gnm::DevParams dev_params(const gnm_ctx* c, const gnm_filter_params* p) {
     q.min_packets1 = std::max<uint32_t>(p->min_packets, 1);
     q.min_duration1 = std::max<uint32_t>(p->min_duration_ms, 1);
     q.wide_log = c->P.n_sites >= gnm::kLogPackedSites;
+    q.windowed = 0;
+    q.win_lo = q.win_hi = 0;
     q.ablation = 0;
 #ifdef GNM_K2_ABLATION
     if (const char* a = std::getenv("GNM_K2_ABLATION")) q.ablation = static_cast<uint32_t>(std::atoi(a));
@@ -479,12 +481,24 @@ int check_soa(const gnm_batch_soa* b) {
     return GNM_OK;
 }
 
+struct Window {
+    uint64_t lo, hi;
+};
+
+void apply_window(gnm::DevParams& p, const Window* w) {
+    if (!w) return;
+    p.windowed = 1;
+    p.win_lo = w->lo;
+    p.win_hi = w->hi;
+}
+
 int accumulate_soa(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* params,
-                   const gnm_batch_soa* b) {
+                   const gnm_batch_soa* b, const Window* win = nullptr) {
     if (int e = check_soa(b)) return e;
     if (c->prepared) return fail(GNM_ERR_INVALID_ARGUMENT, "gnm_prepare_median already ran; finalize first");
     if (int e = begin_accumulate(c, reg)) return e;
-    const gnm::DevParams p = dev_params(c, params);
+    gnm::DevParams p = dev_params(c, params);
+    apply_window(p, win);
     if (b->n == 0) return GNM_OK;
     if (b->mem == GNM_MEM_DEVICE) {
         const void* cols[6] = {b->src_addr, b->dst_addr, b->d_pkts, b->d_octets, b->start_ms, b->end_ms};
@@ -498,12 +512,13 @@ int accumulate_soa(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params*
 }
 
 int accumulate_aos(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* params,
-                   const gnm_batch_aos* b) {
+                   const gnm_batch_aos* b, const Window* win = nullptr) {
     if (!b) return fail(GNM_ERR_INVALID_ARGUMENT, "null batch");
     if (b->n && !b->records) return fail(GNM_ERR_INVALID_ARGUMENT, "null records");
     if (c->prepared) return fail(GNM_ERR_INVALID_ARGUMENT, "gnm_prepare_median already ran; finalize first");
     if (int e = begin_accumulate(c, reg)) return e;
-    const gnm::DevParams p = dev_params(c, params);
+    gnm::DevParams p = dev_params(c, params);
+    apply_window(p, win);
     if (b->n == 0) return GNM_OK;
     if (b->mem == GNM_MEM_DEVICE) {
         launch_k2_timed(c, aos_batch(b->records, b->n), p);
@@ -860,6 +875,32 @@ int gnm_reset(gnm_ctx* c) {
         drain_pairs(c, c->h2d_pairs);
         c->accumulating = false;
         return static_cast<int>(GNM_OK);
+    });
+}
+
+int gnm_accumulate_window(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* params,
+                          const gnm_batch_soa* batch, uint64_t window_start_ms, uint64_t window_end_ms) {
+    if (!c || !reg) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx/registry");
+    const Window w{window_start_ms, window_end_ms};
+    return guarded([&] { return accumulate_soa(c, reg, params, batch, &w); });
+}
+
+int gnm_accumulate_window_aos(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* params,
+                              const gnm_batch_aos* batch, uint64_t window_start_ms,
+                              uint64_t window_end_ms) {
+    if (!c || !reg) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx/registry");
+    const Window w{window_start_ms, window_end_ms};
+    return guarded([&] { return accumulate_aos(c, reg, params, batch, &w); });
+}
+
+int gnm_analyze_window(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* params,
+                       const gnm_batch_soa* batch, gnm_result* result) {
+    if (!c || !reg || !result) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx/registry/result");
+    if (c->accumulating) return fail(GNM_ERR_INVALID_ARGUMENT, "an accumulation is in progress");
+    const Window w{result->window_start_ms, result->window_end_ms};
+    return guarded([&] {
+        if (int e = accumulate_soa(c, reg, params, batch, &w)) return e;
+        return finalize(c, reg, result);
     });
 }
 

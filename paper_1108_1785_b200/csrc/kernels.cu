@@ -245,6 +245,15 @@ __device__ __forceinline__ uint32_t bucket_of_ubps(uint64_t lo, uint64_t hi) {
 
 
 // ---- per-record classification (stage A, every lane) -----------------------
+// FlowStore::snapshot's predicate (flow_store.cpp:75): end_ms in [lo, hi).
+// The window-fused K2 applies it before classification, exactly as the
+// reference analyzes only the snapshot's copy of the window.
+template <bool kWin>
+__device__ __forceinline__ bool window_in(uint64_t end, const DevParams& p) {
+    if constexpr (kWin) return end >= p.win_lo && end < p.win_hi;
+    else return true;
+}
+
 // Per-lane tallies (ClassTallies, rate_engine.hpp:101-110).
 struct Ctr {
     uint32_t fwd = 0, ack = 0, adm = 0, unm = 0;
@@ -256,6 +265,8 @@ struct Ctr {
 constexpr uint32_t kResolved = 0x80000000u;
 constexpr uint32_t kSkip = 0xFFFFFFFFu;
 
+// `in`: the record lies in the analysis window (window-fused variant, see
+// window_in); records outside it are not counted at all.
 // reduce_slice's per-record filter (rate_engine.cpp:199-215) and the first
 // half of attribute (:127-146), branch-free, in the reference's order:
 //   ack = octets < (ack_max+1) * pkts          (false when pkts == 0)
@@ -268,7 +279,7 @@ constexpr uint32_t kSkip = 0xFFFFFFFFu;
 template <bool kSmem>
 __device__ __forceinline__ uint32_t stage_a(uint32_t src, uint32_t dst, uint32_t pkts, uint32_t oct,
                                             uint64_t dur, const DevParams& p,
-                                            const uint32_t* __restrict__ gt, Ctr& c) {
+                                            const uint32_t* __restrict__ gt, Ctr& c, bool in = true) {
     const bool ack = static_cast<uint64_t>(oct) < p.ack_plus1 * pkts;
     const bool rej = pkts < p.min_packets1 || dur < static_cast<uint64_t>(p.min_duration1);
     const uint32_t ds = src >> 16, dd = dst >> 16;
@@ -276,9 +287,9 @@ __device__ __forceinline__ uint32_t stage_a(uint32_t src, uint32_t dst, uint32_t
     const uint2 wd = table_pair<kSmem>(gt, dd >> 5);
     const bool hs = (ws.x >> (ds & 31u)) & 1u;
     const bool hd = (wd.x >> (dd & 31u)) & 1u;
-    if (ack) ++c.ack;
-    if (!ack && rej) ++c.adm;
-    const bool cand = !ack && !rej;
+    if (in && ack) ++c.ack;
+    if (in && !ack && rej) ++c.adm;
+    const bool cand = in && !ack && !rej;
     if (cand && !(hs | hd)) ++c.unm;
     const uint32_t bits = hs ? ws.x : wd.x;
     const uint32_t rank0 = hs ? ws.y : wd.y;
@@ -550,27 +561,28 @@ __device__ __forceinline__ void hot_normalize(const HotSmem& h, const DevHot& ho
 // kLayout 1: SoA; 2/3: 64-byte flowmon::FlowRecord rows (netflow.hpp:59-67).
 template <int kLayout>
 __device__ __forceinline__ void load_record(const DevBatch& b, uint64_t i, uint32_t& src, uint32_t& dst,
-                                            uint32_t& pkts, uint32_t& oct, uint64_t& dur) {
+                                            uint32_t& pkts, uint32_t& oct, uint64_t& dur, uint64_t& end) {
     if constexpr (kLayout == 1) {
         const DevSoA& c = b.soa;
         src = c.src[i], dst = c.dst[i], pkts = c.pkts[i], oct = c.octets[i];
-        dur = c.end[i] - c.start[i];
+        end = c.end[i];
+        dur = end - c.start[i];
     } else if constexpr (kLayout == 2) {
         const unsigned char* r = static_cast<const unsigned char*>(b.rec) + i * 64;
         const uint2 a = __ldg(reinterpret_cast<const uint2*>(r));                 // src dst
         const uint2 cc = __ldg(reinterpret_cast<const uint2*>(r + 16));           // pkts octets
         const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(r + 48));  // start end
-        src = a.x, dst = a.y, pkts = cc.x, oct = cc.y, dur = e.y - e.x;
+        src = a.x, dst = a.y, pkts = cc.x, oct = cc.y, dur = e.y - e.x, end = e.y;
     } else {
         const unsigned char* r = static_cast<const unsigned char*>(b.rec) + i * 64;
         const uint32_t* w = reinterpret_cast<const uint32_t*>(r);
         const uint64_t* qq = reinterpret_cast<const uint64_t*>(r + 48);
-        src = w[0], dst = w[1], pkts = w[4], oct = w[5], dur = qq[1] - qq[0];
+        src = w[0], dst = w[1], pkts = w[4], oct = w[5], dur = qq[1] - qq[0], end = qq[1];
     }
 }
 
 // Records [first, last) in warp-strided 32-record rounds, scalar loads.
-template <int kLayout, bool kSmem, bool kHot>
+template <int kLayout, bool kSmem, bool kHot, bool kWin>
 __device__ __forceinline__ void run_scalar(const DevBatch& b, uint64_t first, uint64_t last,
                                            uint64_t stride, uint32_t lane,
                                            const uint32_t* __restrict__ gt, const DevParams& p,
@@ -579,11 +591,11 @@ __device__ __forceinline__ void run_scalar(const DevBatch& b, uint64_t first, ui
     for (uint64_t base = first; base < last; base += stride) {
         const uint64_t i = base + lane;
         uint32_t src = 0, dst = 0, pkts = 0, oct = 0;
-        uint64_t dur = 0;
+        uint64_t dur = 0, end = 0;
         const bool ok = i < last;
-        if (ok) load_record<kLayout>(b, i, src, dst, pkts, oct, dur);
+        if (ok) load_record<kLayout>(b, i, src, dst, pkts, oct, dur, end);
         Ctr one;
-        const uint32_t code = stage_a<kSmem>(src, dst, pkts, oct, dur, p, gt, one);
+        const uint32_t code = stage_a<kSmem>(src, dst, pkts, oct, dur, p, gt, one, window_in<kWin>(end, p));
         if (ok) {
             t.ack += one.ack;
             t.adm += one.adm;
@@ -640,7 +652,7 @@ __device__ __forceinline__ void k2_epilogue(Ctr& t, WarpQueue& wq, uint32_t lane
 // one is classified. Every kEpochRounds rounds the CTA meets at a barrier
 // and normalizes the hot limbs (hot_normalize). The last CTA also takes the
 // < 64-record remainder through the scalar path.
-template <bool kSmem, bool kHot>
+template <bool kSmem, bool kHot, bool kWin>
 __global__ void __launch_bounds__(kK2Block, 1) k2_soa(DevBatch b, const uint32_t* __restrict__ gt,
                                                     uint32_t table_words, DevParams p,
                                                     DevPartials P, DevHot hot, DevLog L) {
@@ -689,8 +701,8 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_soa(DevBatch b, const uint32_t
         }
         if (tile < t_end) {
             const uint64_t dx = te.x - ts.x, dy = te.y - ts.y;
-            const uint32_t cx = stage_a<kSmem>(s.x, d.x, k.x, o.x, dx, p, gt, t);
-            const uint32_t cy = stage_a<kSmem>(s.y, d.y, k.y, o.y, dy, p, gt, t);
+            const uint32_t cx = stage_a<kSmem>(s.x, d.x, k.x, o.x, dx, p, gt, t, window_in<kWin>(te.x, p));
+            const uint32_t cy = stage_a<kSmem>(s.y, d.y, k.y, o.y, dy, p, gt, t, window_in<kWin>(te.y, p));
             push(cx, o.x, dx, wq, lane);
             push(cy, o.y, dy, wq, lane);
             drain_full<kSmem, kHot>(wq, lane, gt, p, P, h, t);
@@ -706,14 +718,14 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_soa(DevBatch b, const uint32_t
         }
     }
     if (blockIdx.x == gridDim.x - 1 && warp == 0)
-        run_scalar<1, kSmem, kHot>(b, tiles << 6, c.n, 32, lane, gt, p, P, h, t, wq);
+        run_scalar<1, kSmem, kHot, kWin>(b, tiles << 6, c.n, 32, lane, gt, p, P, h, t, wq);
     k2_epilogue<kSmem, kHot>(t, wq, lane, gt, p, P, h, hot, L);
 }
 
 // Other layouts: unaligned SoA (1), AoS 64-byte rows with vector (2) or
 // scalar (3) loads. CTA b owns records [b*n/G, (b+1)*n/G) (at most
 // kCtaRecords), one record per lane per round.
-template <int kLayout, bool kSmem, bool kHot>
+template <int kLayout, bool kSmem, bool kHot, bool kWin>
 __global__ void __launch_bounds__(kK2Block, 1) k2_gen(DevBatch b, const uint32_t* __restrict__ gt,
                                                     uint32_t table_words, DevParams p,
                                                     DevPartials P, DevHot hot, DevLog L) {
@@ -723,8 +735,8 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_gen(DevBatch b, const uint32_t
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t r0 = b.n * blockIdx.x / gridDim.x, r1 = b.n * (blockIdx.x + 1) / gridDim.x;
     Ctr t;
-    run_scalar<kLayout, kSmem, kHot>(b, r0 + (threadIdx.x >> 5) * 32, r1, kK2Block, lane, gt, p, P, h,
-                                     t, wq);
+    run_scalar<kLayout, kSmem, kHot, kWin>(b, r0 + (threadIdx.x >> 5) * 32, r1, kK2Block, lane, gt, p, P,
+                                           h, t, wq);
     k2_epilogue<kSmem, kHot>(t, wq, lane, gt, p, P, h, hot, L);
 }
 
@@ -742,11 +754,11 @@ __global__ void __launch_bounds__(kK2Block) k_sample(DevBatch b, const uint32_t*
     for (uint32_t j = threadIdx.x; j < chunk_len; j += blockDim.x) {
         const uint64_t i = base + j;
         uint32_t src, dst, pkts, oct;
-        uint64_t dur;
-        if (b.aos) load_record<3>(b, i, src, dst, pkts, oct, dur);
-        else load_record<1>(b, i, src, dst, pkts, oct, dur);
+        uint64_t dur, end;
+        if (b.aos) load_record<3>(b, i, src, dst, pkts, oct, dur, end);
+        else load_record<1>(b, i, src, dst, pkts, oct, dur, end);
         if (static_cast<uint64_t>(oct) < p.ack_plus1 * pkts || pkts < p.min_packets1 ||
-            dur < static_cast<uint64_t>(p.min_duration1))
+            dur < static_cast<uint64_t>(p.min_duration1) || (p.windowed && !(end >= p.win_lo && end < p.win_hi)))
             continue;
         const uint32_t v = site_of_full<kSmem>(gt, src, dst);
         if (v != kNone) atomicAdd(cnt + (v & p.site_mask), 1u);
@@ -1147,38 +1159,52 @@ cudaError_t allow_smem(K kernel) {
                                 static_cast<int>(kSmemMax));
 }
 
-template <int L, bool kS, bool kH>
+template <int L, bool kS, bool kH, bool kW>
 constexpr auto k2_kernel() {
-    if constexpr (L == 0) return k2_soa<kS, kH>;
-    else return k2_gen<L, kS, kH>;
+    if constexpr (L == 0) return k2_soa<kS, kH, kW>;
+    else return k2_gen<L, kS, kH, kW>;
+}
+
+template <int L, bool kW>
+cudaError_t allow_layout_w() {
+    cudaError_t e;
+    if ((e = allow_smem(k2_kernel<L, true, true, kW>()))) return e;
+    if ((e = allow_smem(k2_kernel<L, true, false, kW>()))) return e;
+    if ((e = allow_smem(k2_kernel<L, false, true, kW>()))) return e;
+    return allow_smem(k2_kernel<L, false, false, kW>());
 }
 
 template <int L>
 cudaError_t allow_layout() {
     cudaError_t e;
-    if ((e = allow_smem(k2_kernel<L, true, true>()))) return e;
-    if ((e = allow_smem(k2_kernel<L, true, false>()))) return e;
-    if ((e = allow_smem(k2_kernel<L, false, true>()))) return e;
-    return allow_smem(k2_kernel<L, false, false>());
+    if ((e = allow_layout_w<L, false>())) return e;
+    return allow_layout_w<L, true>();
 }
 
-template <int L, bool kS, bool kH>
+template <int L, bool kS, bool kH, bool kW>
 void launch_k2_t(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t, const DevParams& p,
                  const DevPartials& P, const DevHot& hot, const DevLog& log, cudaStream_t s) {
-    k2_kernel<L, kS, kH>()<<<cfg.grid, cfg.block, cfg.smem, s>>>(b, t.words, t.n_words, p, P, hot, log);
+    k2_kernel<L, kS, kH, kW>()<<<cfg.grid, cfg.block, cfg.smem, s>>>(b, t.words, t.n_words, p, P, hot, log);
+}
+
+template <int L, bool kW>
+void launch_k2_w(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t, const DevParams& p,
+                 const DevPartials& P, const DevHot& hot, const DevLog& log, cudaStream_t s) {
+    const bool hh = hot.n_slots > 0;
+    if (cfg.table_in_smem) {
+        if (hh) launch_k2_t<L, true, true, kW>(cfg, b, t, p, P, hot, log, s);
+        else launch_k2_t<L, true, false, kW>(cfg, b, t, p, P, hot, log, s);
+    } else {
+        if (hh) launch_k2_t<L, false, true, kW>(cfg, b, t, p, P, hot, log, s);
+        else launch_k2_t<L, false, false, kW>(cfg, b, t, p, P, hot, log, s);
+    }
 }
 
 template <int L>
 void launch_k2_l(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t, const DevParams& p,
                  const DevPartials& P, const DevHot& hot, const DevLog& log, cudaStream_t s) {
-    const bool hh = hot.n_slots > 0;
-    if (cfg.table_in_smem) {
-        if (hh) launch_k2_t<L, true, true>(cfg, b, t, p, P, hot, log, s);
-        else launch_k2_t<L, true, false>(cfg, b, t, p, P, hot, log, s);
-    } else {
-        if (hh) launch_k2_t<L, false, true>(cfg, b, t, p, P, hot, log, s);
-        else launch_k2_t<L, false, false>(cfg, b, t, p, P, hot, log, s);
-    }
+    if (p.windowed) launch_k2_w<L, true>(cfg, b, t, p, P, hot, log, s);
+    else launch_k2_w<L, false>(cfg, b, t, p, P, hot, log, s);
 }
 
 size_t table_smem_bytes(uint32_t table_words) { return static_cast<size_t>(table_words) * 4; }

@@ -39,6 +39,9 @@ struct DevParams {
     uint32_t min_duration1;   // max(min_duration_ms, 1): folds duration == 0 (:81)
     uint32_t site_mask;       // kPackedSiteMask, or 0x7FFFFFFF for wide tables
     uint32_t wide_log;        // registry >= kLogPackedSites sites: log buckets in their own array
+    uint32_t windowed;        // 1: analyze only records with end_ms in [win_lo, win_hi)
+    uint64_t win_lo;          //    (FlowStore::snapshot, flow_store.cpp:75), fused into K1/K2
+    uint64_t win_hi;
     uint32_t ablation;        // GNM_K2_ABLATION builds only (tools/ablation.sh); 0 otherwise
 };
 

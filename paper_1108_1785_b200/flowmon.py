@@ -502,13 +502,21 @@ class Engine:
     def _params(params: Optional[FilterParams]) -> gnm_filter_params:
         return (params or FilterParams())._c()
 
-    def accumulate(self, batch, catalog: SiteCatalog, params: Optional[FilterParams] = None) -> None:
+    def accumulate(self, batch, catalog: SiteCatalog, params: Optional[FilterParams] = None,
+                   window: Optional[tuple] = None) -> None:
+        """Add a batch to the accumulation. ``window=(start_ms, end_ms)``
+        fuses FlowStore::snapshot (flow_store.cpp:62-80): only records with
+        end_ms in [start_ms, end_ms) are analyzed."""
         p = self._params(params)
-        if isinstance(batch, FlowRecords):
-            b = batch._c()
+        b = batch._c()
+        aos = isinstance(batch, FlowRecords)
+        if window is not None:
+            ws, we = int(window[0]), int(window[1])
+            fn = lib.gnm_accumulate_window_aos if aos else lib.gnm_accumulate_window
+            _check(fn(self._h, catalog.handle, C.byref(p), C.byref(b), ws, we))
+        elif aos:
             _check(lib.gnm_accumulate_aos(self._h, catalog.handle, C.byref(p), C.byref(b)))
         else:
-            b = batch._c()
             _check(lib.gnm_accumulate(self._h, catalog.handle, C.byref(p), C.byref(b)))
 
     def _result(self, catalog: SiteCatalog, window_start_ms: int, window_end_ms: int,
@@ -552,6 +560,23 @@ class Engine:
             _check(lib.gnm_analyze_aos(self._h, catalog.handle, C.byref(p), C.byref(b), C.byref(r)))
         else:
             _check(lib.gnm_analyze(self._h, catalog.handle, C.byref(p), C.byref(b), C.byref(r)))
+        return _build_result(r, table[:n], None if hist is None else hist[:n])
+
+    def aggregate_window(self, view, catalog: SiteCatalog, window_start_ms: int, window_end_ms: int,
+                         params: Optional[FilterParams] = None,
+                         threshold_bps: float = kDefaultWarnThresholdBps,
+                         histograms: bool = False) -> AnalysisResult:
+        """FlowStore::snapshot(start, end) + aggregate(..., start, end) fused
+        (monitor.cpp:109-120, run_cycle): records outside [start, end) by
+        end_ms are neither analyzed nor tallied."""
+        if isinstance(view, FlowRecords):
+            self.accumulate(view, catalog, params, window=(window_start_ms, window_end_ms))
+            return self.finalize(catalog, window_start_ms, window_end_ms, threshold_bps, histograms)
+        p = self._params(params)
+        b = view._c()
+        r, table, hist, n = self._result(catalog, window_start_ms, window_end_ms, threshold_bps,
+                                         histograms)
+        _check(lib.gnm_analyze_window(self._h, catalog.handle, C.byref(p), C.byref(b), C.byref(r)))
         return _build_result(r, table[:n], None if hist is None else hist[:n])
 
     def partials(self, catalog: SiteCatalog) -> dict:

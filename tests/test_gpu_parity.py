@@ -210,3 +210,54 @@ def test_multi_cta_remainders_and_epochs(engine, orc, n):
     cat = layout_catalog(w.sites)
     res = engine.aggregate(FlowBatch(*cols).to_device(), cat)
     parity.assert_matches_oracle(res, parity.oracle_reference(orc, cat, cols))
+
+
+def _window_mask(cols, lo, hi):
+    end = cols[5]
+    return (end >= np.uint64(lo)) & (end < np.uint64(hi))
+
+
+@pytest.mark.parametrize("on_device", [False, True])
+def test_window_fused_snapshot_bit_exact(engine, orc, on_device):
+    """gnm_analyze_window / gnm_accumulate_window = FlowStore::snapshot
+    (flow_store.cpp:62-80: end_ms in [start, end)) fused into K1/K2: equal to
+    the oracle on the host-filtered records, tallies included, for a
+    partial, an empty, a full and a one-millisecond window."""
+    w = synth.workload("D2")
+    cols = synth.generate(w, 400_000)
+    cat = layout_catalog(w.sites)
+    end = cols[5]
+    lo_all, hi_all = int(end.min()), int(end.max()) + 1
+    mid = (lo_all + hi_all) // 2
+    windows = [(lo_all + (hi_all - lo_all) // 4, mid), (hi_all + 10, hi_all + 20), (0, 2**64 - 1),
+               (int(end[12345]), int(end[12345]) + 1)]
+    batch = FlowBatch(*cols)
+    if on_device:
+        batch = batch.to_device()
+    for lo, hi in windows:
+        m = _window_mask(cols, lo, hi)
+        sub = tuple(np.ascontiguousarray(c[m]) for c in cols)
+        want = parity.oracle_reference(orc, cat, sub)
+        got = engine.aggregate_window(batch, cat, lo, hi, histograms=True)
+        parity.assert_matches_oracle(got, want)
+        assert got.tallies.total() == int(m.sum())
+        assert (got.window_start_ms, got.window_end_ms) == (lo, hi)
+    # split accumulation: two batches, one window
+    lo, hi = windows[0]
+    engine.accumulate(FlowBatch(*[c[:150_000] for c in cols]), cat, window=(lo, hi))
+    engine.accumulate(FlowBatch(*[c[150_000:] for c in cols]), cat, window=(lo, hi))
+    got = engine.finalize(cat, lo, hi)
+    m = _window_mask(cols, lo, hi)
+    parity.assert_matches_oracle(got, parity.oracle_reference(orc, cat, tuple(np.ascontiguousarray(c[m]) for c in cols)))
+
+
+def test_window_fused_aos(engine, orc):
+    sites, cols = parity.engine_stress_set(50_000, seed=31)
+    cat = catalog_of(sites)
+    end = cols[5]
+    lo = int(np.percentile(end, 30))
+    hi = int(np.percentile(end, 80))
+    from paper_1108_1785_b200 import FlowRecords
+    got = engine.aggregate_window(FlowRecords(synth.to_aos(cols)), cat, lo, hi)
+    m = _window_mask(cols, lo, hi)
+    parity.assert_matches_oracle(got, parity.oracle_reference(orc, cat, tuple(np.ascontiguousarray(c[m]) for c in cols)))
