@@ -279,6 +279,29 @@ int gnm_ctx_timing(gnm_ctx* ctx, gnm_timing* out);
  * the running totals. */
 int gnm_ctx_enable_timing(gnm_ctx* ctx, int enable);
 
+/* ---- NetFlow v5 ingest: Collector::ingest_datagram, batched ---------------
+ * (collector.cpp:101-129; decode_packet netflow.cpp:78-113, resolve_times
+ * :150-161; paths relative to /root/reference/proj/core/src). Decodes n
+ * datagrams on the GPU: datagram i is bytes [offsets[i], offsets[i+1]) of
+ * `datagrams` (both in memory `in_mem`). A datagram the reference would
+ * reject with CodecError is dropped (status 1 bad version, 2 truncated,
+ * 3 bad count; 0 ok); records with d_pkts == 0 or d_octets < d_pkts are
+ * rejected as the collector does; the rest are written as 64-byte
+ * flowmon::FlowRecord rows (netflow.hpp:59-67) to `out_records` (memory
+ * `out_mem`, `capacity` rows) in datagram order, then record order -- the
+ * order the collector appends them to the FlowStore. `status` (optional)
+ * is a host array of n bytes. GNM_ERR_CAPACITY when the accepted records
+ * do not fit. */
+typedef struct gnm_netflow_stats {
+    uint64_t datagrams;
+    uint64_t decode_errors;    /* CollectorMetrics::decode_errors */
+    uint64_t records_rejected; /* CollectorMetrics::records_rejected */
+    uint64_t records_accepted; /* records written */
+} gnm_netflow_stats;
+int gnm_decode_netflow(gnm_ctx* ctx, const uint8_t* datagrams, uint64_t bytes, const uint64_t* offsets,
+                       uint64_t n, int32_t in_mem, void* out_records, uint64_t capacity, int32_t out_mem,
+                       uint8_t* status, gnm_netflow_stats* stats);
+
 /* ---- Warning rule: evaluate_warnings (monitor.cpp:13-34) ----------------- */
 typedef struct gnm_warning_state gnm_warning_state;
 typedef struct gnm_warning {

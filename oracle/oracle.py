@@ -222,6 +222,9 @@ class Reference:
             "ref_wstate_destroy": (None, [V]),
             "ref_wstate_streak": (U32, [V, U32]),
             "ref_evaluate_warnings": (C.c_size_t, [V, V, V, D, V, V, V, C.c_size_t]),
+            "ref_ingest_datagram": (C.c_int, [V, C.c_size_t, V, V, V]),
+            "ref_encode_packet": (C.c_size_t, [V, V, C.c_size_t, V]),
+            "ref_raw_record_size": (C.c_size_t, []),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -231,6 +234,26 @@ class Reference:
 
     def err(self) -> str:
         return self.L.ref_last_error().decode()
+
+    # -- NetFlow v5 (netflow.cpp, collector.cpp:101-129) -------------------------
+    def ingest_datagram(self, datagram: bytes):
+        """(status 0 | 1+CodecError::Kind, FlowRecord rows as bytes, rejected)."""
+        buf = np.frombuffer(datagram, np.uint8) if len(datagram) else np.zeros(1, np.uint8)
+        out = np.zeros(30 * 64, np.uint8)
+        n = C.c_size_t()
+        rej = C.c_uint32()
+        st = self.L.ref_ingest_datagram(buf.ctypes.data, len(datagram), out.ctypes.data, C.byref(n),
+                                        C.byref(rej))
+        return st, out[: n.value * 64].tobytes(), rej.value
+
+    def encode_packet(self, header: Sequence[int], raw: np.ndarray) -> bytes:
+        """encode_packet(ExportHeader{header...}, raw RawFlowRecord rows)."""
+        h = np.asarray(header, np.uint32)
+        r = np.ascontiguousarray(raw)
+        out = np.zeros(24 + 48 * 30, np.uint8)
+        n = self.L.ref_encode_packet(h.ctypes.data, r.ctypes.data, len(r) // 48 if r.dtype == np.uint8 else len(r),
+                                     out.ctypes.data)
+        return out[:n].tobytes()
 
     # -- catalog ---------------------------------------------------------------
     def catalog(self, sites: Sequence[Sequence[str]] = ()) -> "RefHandle":

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "flowmon/monitor.hpp"
+#include "flowmon/netflow.hpp"
 #include "flowmon/rate_engine.hpp"
 #include "flowmon/site_catalog.hpp"
 #include "flowmon/toolkit.hpp"
@@ -397,4 +398,57 @@ size_t ref_evaluate_warnings(const void* r, const void* c, void* w, double thres
     return warns.size();
 }
 
+
+// ---- NetFlow v5 ingest (collector.cpp:101-129, netflow.cpp:78-161) ------------
+// Collector::ingest_datagram without the store and the sequence tracker:
+// decode_packet, the collector's reject rule (d_pkts == 0 || d_octets <
+// d_pkts), resolve_times. Returns 0, or 1 + CodecError::Kind (BadVersion,
+// Truncated, BadCount) when the datagram is dropped; `out` receives up to 30
+// FlowRecords (64 bytes each) in order.
+int ref_ingest_datagram(const uint8_t* d, size_t len, void* out, size_t* n_out, uint32_t* rejected) {
+    *n_out = 0;
+    *rejected = 0;
+    DecodedPacket packet;
+    try {
+        packet = decode_packet(std::span<const std::uint8_t>(d, len));
+    } catch (const CodecError& e) {
+        return 1 + static_cast<int>(e.kind());
+    }
+    auto* o = static_cast<FlowRecord*>(out);
+    for (const RawFlowRecord& raw : packet.records) {
+        if (raw.d_pkts == 0 || raw.d_octets < raw.d_pkts) {
+            ++*rejected;
+            continue;
+        }
+        o[(*n_out)++] = resolve_times(packet.header, raw);
+    }
+    return 0;
+}
+
+// encode_packet (netflow.cpp:115-143): h = {version, count, sys_uptime,
+// unix_secs, unix_nsecs, flow_sequence, engine_type, engine_id,
+// sampling_interval}; `raw` holds `n` RawFlowRecords (48-byte struct).
+// Returns the datagram length written to `out`, or 0 on CodecError.
+size_t ref_encode_packet(const uint32_t* h, const void* raw, size_t n, uint8_t* out) {
+    ExportHeader header;
+    header.version = static_cast<std::uint16_t>(h[0]);
+    header.count = static_cast<std::uint16_t>(h[1]);
+    header.sys_uptime = h[2];
+    header.unix_secs = h[3];
+    header.unix_nsecs = h[4];
+    header.flow_sequence = h[5];
+    header.engine_type = static_cast<std::uint8_t>(h[6]);
+    header.engine_id = static_cast<std::uint8_t>(h[7]);
+    header.sampling_interval = static_cast<std::uint16_t>(h[8]);
+    try {
+        const auto buf = encode_packet(
+            header, std::span<const RawFlowRecord>(static_cast<const RawFlowRecord*>(raw), n));
+        std::memcpy(out, buf.data(), buf.size());
+        return buf.size();
+    } catch (const CodecError& e) {
+        set_err(e);
+        return 0;
+    }
+}
+size_t ref_raw_record_size() { return sizeof(RawFlowRecord); }
 } // extern "C"

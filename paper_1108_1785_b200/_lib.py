@@ -80,6 +80,11 @@ class gnm_partials(C.Structure):
                 ("fine_count", C.c_uint64)]
 
 
+class gnm_netflow_stats(C.Structure):
+    _fields_ = [("datagrams", C.c_uint64), ("decode_errors", C.c_uint64),
+                ("records_rejected", C.c_uint64), ("records_accepted", C.c_uint64)]
+
+
 class gnm_timing(C.Structure):
     _fields_ = [("accumulate_ms", C.c_double), ("finalize_ms", C.c_double),
                 ("h2d_ms", C.c_double), ("k2_launches", C.c_uint64),
@@ -155,6 +160,9 @@ _SIGS = [
     ("gnm_reset", C.c_int, [_P]),
     ("gnm_get_partials", C.c_int, [_P, _P, C.POINTER(gnm_partials)]),
     ("gnm_prepare_median", C.c_int, [_P, _P]),
+    ("gnm_decode_netflow", C.c_int,
+     [_P, _P, C.c_uint64, _P, C.c_uint64, C.c_int32, _P, C.c_uint64, C.c_int32, _P,
+      C.POINTER(gnm_netflow_stats)]),
     ("gnm_classify", C.c_int,
      [_P, _P, C.POINTER(gnm_filter_params), C.POINTER(gnm_batch_soa), _P, C.c_int32]),
     ("gnm_ctx_timing", C.c_int, [_P, C.POINTER(gnm_timing)]),

@@ -18,6 +18,7 @@
 
 #include "gnetmon.h"
 #include "kernels.cuh"
+#include "netflow.cuh"
 #include "registry.hpp"
 
 namespace {
@@ -875,6 +876,81 @@ int gnm_reset(gnm_ctx* c) {
         drain_pairs(c, c->h2d_pairs);
         c->accumulating = false;
         return static_cast<int>(GNM_OK);
+    });
+}
+
+int gnm_decode_netflow(gnm_ctx* c, const uint8_t* datagrams, uint64_t bytes, const uint64_t* offsets,
+                       uint64_t n, int32_t in_mem, void* out_records, uint64_t capacity, int32_t out_mem,
+                       uint8_t* status, gnm_netflow_stats* stats) {
+    if (!c || (n && (!datagrams || !offsets)) || (capacity && !out_records))
+        return fail(GNM_ERR_INVALID_ARGUMENT, "null argument");
+    if ((in_mem != GNM_MEM_HOST && in_mem != GNM_MEM_DEVICE) || (out_mem != GNM_MEM_HOST && out_mem != GNM_MEM_DEVICE))
+        return fail(GNM_ERR_INVALID_ARGUMENT, "mem must be GNM_MEM_HOST or GNM_MEM_DEVICE");
+    return guarded([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        cudaStream_t s = c->stream;
+        if (in_mem == GNM_MEM_HOST && n) {
+            if (offsets[n] > bytes) return fail(GNM_ERR_INVALID_ARGUMENT, "offsets[n] exceeds bytes");
+            for (uint64_t i = 0; i < n; ++i)
+                if (offsets[i + 1] < offsets[i]) return fail(GNM_ERR_INVALID_ARGUMENT, "offsets must be non-decreasing");
+        }
+        // Device scratch: datagrams + offsets (host input), per-datagram counts,
+        // offsets, status, stats, and the output rows when they cannot go
+        // straight to device memory of sufficient capacity.
+        const uint64_t max_rows = n * 30;
+        const bool direct = out_mem == GNM_MEM_DEVICE && capacity >= max_rows;
+        const size_t in_bytes = in_mem == GNM_MEM_HOST ? bytes : 0;
+        const size_t off_bytes = in_mem == GNM_MEM_HOST ? (n + 1) * 8 : 0;
+        auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+        const size_t total = up(in_bytes) + up(off_bytes) + up(n * 4) + up(n * 8) + up(n) + up(5 * 8) +
+                             (direct ? 0 : up(max_rows * 64));
+        unsigned char* scratch = nullptr;
+        ck(cudaMallocAsync(reinterpret_cast<void**>(&scratch), std::max<size_t>(total, 256), s), "cudaMallocAsync(netflow)");
+        unsigned char* q = scratch;
+        const uint8_t* d = datagrams;
+        const uint64_t* off = offsets;
+        if (in_mem == GNM_MEM_HOST) {
+            ck(cudaMemcpyAsync(q, datagrams, bytes, cudaMemcpyHostToDevice, s), "H2D datagrams");
+            d = q;
+            q += up(in_bytes);
+            ck(cudaMemcpyAsync(q, offsets, (n + 1) * 8, cudaMemcpyHostToDevice, s), "H2D offsets");
+            off = reinterpret_cast<const uint64_t*>(q);
+            q += up(off_bytes);
+        }
+        auto* acc = reinterpret_cast<uint32_t*>(q);
+        q += up(n * 4);
+        auto* base = reinterpret_cast<uint64_t*>(q);
+        q += up(n * 8);
+        auto* st = reinterpret_cast<uint8_t*>(q);
+        q += up(n);
+        auto* dstats = reinterpret_cast<unsigned long long*>(q);
+        q += up(5 * 8);
+        uint8_t* out = direct ? static_cast<uint8_t*>(out_records) : q;
+        ck(cudaMemsetAsync(dstats, 0, 5 * 8, s), "cudaMemsetAsync");
+        ck(gnm::launch_netflow_decode(d, off, n, acc, base, st, dstats, out, s), "netflow decode");
+        c->kernel_launches += n ? 3 : 0;
+        unsigned long long hs[5] = {0, 0, 0, 0, 0};
+        ck(cudaMemcpyAsync(hs, dstats, sizeof hs, cudaMemcpyDeviceToHost, s), "D2H stats");
+        if (status && n) ck(cudaMemcpyAsync(status, st, n, cudaMemcpyDeviceToHost, s), "D2H status");
+        ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        int rc = GNM_OK;
+        if (hs[3] > capacity) {
+            rc = fail(GNM_ERR_CAPACITY, std::to_string(hs[3]) + " accepted records exceed capacity " +
+                                            std::to_string(capacity));
+        } else if (!direct && hs[3]) {
+            ck(cudaMemcpyAsync(out_records, out, hs[3] * 64,
+                               out_mem == GNM_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s),
+               "copy records");
+        }
+        ck(cudaFreeAsync(scratch, s), "cudaFreeAsync(netflow)");
+        ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        if (stats) {
+            stats->datagrams = n;
+            stats->decode_errors = hs[1];
+            stats->records_rejected = hs[2];
+            stats->records_accepted = hs[3];
+        }
+        return rc;
     });
 }
 

@@ -1,0 +1,19 @@
+// netflow.cuh — launch interface of the batched NetFlow v5 ingest (netflow.cu).
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gnm {
+
+// d: concatenated datagrams; off[n+1]: datagram i is bytes [off[i], off[i+1]).
+// accepted[n], base[n]: scratch. status[n] (optional): 0 ok, 1 bad version,
+// 2 truncated, 3 bad count. stats[5] (zeroed by the caller): datagrams
+// (unused here), decode errors, records rejected, records accepted, total
+// written. out: accepted FlowRecords (64 B each), datagram order.
+cudaError_t launch_netflow_decode(const uint8_t* d, const uint64_t* off, uint64_t n, uint32_t* accepted,
+                                  uint64_t* base, uint8_t* status, unsigned long long* stats,
+                                  uint8_t* out, cudaStream_t s);
+
+} // namespace gnm

@@ -38,7 +38,7 @@ import numpy as np
 from . import _lib
 from ._lib import (BUCKET_COUNT, FLOW_RECORD_DTYPE, SITE_STATS_DTYPE, gnm_batch_aos,
                    gnm_batch_soa, gnm_cidr, gnm_filter_params, gnm_partials, gnm_result,
-                   gnm_timing, gnm_warning, lib)
+                   gnm_netflow_stats, gnm_timing, gnm_warning, lib)
 
 kBucketCount = BUCKET_COUNT
 kBucketWidthBps = 10_000.0
@@ -578,6 +578,44 @@ class Engine:
                                          histograms)
         _check(lib.gnm_analyze_window(self._h, catalog.handle, C.byref(p), C.byref(b), C.byref(r)))
         return _build_result(r, table[:n], None if hist is None else hist[:n])
+
+    def decode_netflow(self, datagrams, offsets, out_device: bool = False):
+        """Batched Collector::ingest_datagram without the store
+        (collector.cpp:101-129): NetFlow v5 datagrams -> FlowRecord rows on
+        the GPU (gnm_decode_netflow). ``datagrams``: one byte buffer (numpy
+        uint8 or a CUDA uint8 tensor), ``offsets``: n+1 u64 boundaries.
+        Returns (records, status, stats): records as a FLOW_RECORD_DTYPE
+        array (or a CUDA uint8 tensor of rows when ``out_device``), status
+        per datagram (0 ok, 1 bad version, 2 truncated, 3 bad count) and the
+        collector's counters."""
+        n = len(offsets) - 1
+        if _is_torch(datagrams):
+            import torch
+            offs = offsets if _is_torch(offsets) else torch.as_tensor(np.asarray(offsets, np.uint64).view(np.int64),
+                                                                       device=datagrams.device)
+            d_ptr, nbytes, off_ptr, mem = datagrams.data_ptr(), datagrams.numel(), offs.data_ptr(), _lib.MEM_DEVICE
+        else:
+            buf = np.ascontiguousarray(datagrams, np.uint8)
+            offs = np.ascontiguousarray(offsets, np.uint64)
+            d_ptr = buf.ctypes.data if buf.size else None
+            nbytes, off_ptr, mem = buf.size, offs.ctypes.data, _lib.MEM_HOST
+        cap = 30 * n
+        status = np.zeros(max(n, 1), np.uint8)
+        st = gnm_netflow_stats()
+        if out_device:
+            import torch
+            out = torch.empty(max(cap, 1) * 64, dtype=torch.uint8, device=f"cuda:{self.device}")
+            out_ptr, out_mem = out.data_ptr(), _lib.MEM_DEVICE
+        else:
+            out = np.zeros(max(cap, 1), FLOW_RECORD_DTYPE)
+            out_ptr, out_mem = out.ctypes.data, _lib.MEM_HOST
+        _check(lib.gnm_decode_netflow(self._h, d_ptr, nbytes, off_ptr, n, mem, out_ptr, cap, out_mem,
+                                      status.ctypes.data, C.byref(st)))
+        k = st.records_accepted
+        recs = out[:k * 64] if out_device else out[:k]
+        stats = {"datagrams": st.datagrams, "decode_errors": st.decode_errors,
+                 "records_rejected": st.records_rejected, "records_accepted": k}
+        return recs, status[:n], stats
 
     def partials(self, catalog: SiteCatalog) -> dict:
         """Device pointers of the accumulation (gnm_get_partials) for a

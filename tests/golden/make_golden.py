@@ -188,7 +188,29 @@ def warning_fixture():
     np.savez_compressed(os.path.join(HERE, "warnings.npz"), base=K_BASE, hour=K_HOUR, **out)
 
 
+def netflow_fixture():
+    """NetFlow v5 datagrams (valid and every CodecError kind) and the rows
+    the unmodified reference's ingest path (decode_packet, the collector's
+    reject rule, resolve_times) produces from them."""
+    import netflow_gen as NG
+    rng = np.random.default_rng(19)
+    ds = NG.make_stream(rng, 400)
+    buf, offs = NG.pack(ds)
+    rows, status = [], []
+    for d in ds:
+        st, r, _ = R.ingest_datagram(d)
+        rows.append(r)
+        status.append(st)
+    np.savez_compressed(os.path.join(HERE, "netflow.npz"), datagrams=buf, offsets=offs,
+                        status=np.array(status, np.uint8),
+                        records=np.frombuffer(b"".join(rows), np.uint8))
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:  # regenerate only the named fixtures
+        for name in sys.argv[1:]:
+            globals()[f"{name}_fixture"]()
+        sys.exit(0)
     sites, cols = parity.engine_stress_set(50_000, seed=37)
     analysis_fixture("engine_stress", sites, cols)
     sites, cols = parity.edge_set()
@@ -202,3 +224,4 @@ if __name__ == "__main__":
     catalog_fixture()
     scalar_fixture()
     warning_fixture()
+    netflow_fixture()
