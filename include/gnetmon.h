@@ -44,7 +44,10 @@ typedef enum gnm_status {
     GNM_ERR_ZERO_DURATION = 6,  /* RateError::Kind::ZeroDuration    rate_engine.hpp:37 */
     GNM_ERR_EMPTY_HISTOGRAM = 7,/* RateError::Kind::EmptyHistogram  rate_engine.hpp:37 */
     GNM_ERR_NO_DEVICE = 8,      /* no CUDA device: there is no CPU fallback */
-    GNM_ERR_CAPACITY = 9        /* caller buffer too small */
+    GNM_ERR_CAPACITY = 9,       /* caller buffer too small */
+    GNM_ERR_BAD_MAGIC = 10,     /* ArchiveError::Kind::BadMagic          flow_store.hpp:24 */
+    GNM_ERR_BAD_VERSION = 11,   /* ArchiveError::Kind::BadVersion */
+    GNM_ERR_TRUNCATED = 12      /* ArchiveError::Kind::TruncatedArchive (incl. trailing bytes) */
 } gnm_status;
 
 /* FlowClass (rate_engine.hpp:31), same ordinal values. */
@@ -301,6 +304,23 @@ typedef struct gnm_netflow_stats {
 int gnm_decode_netflow(gnm_ctx* ctx, const uint8_t* datagrams, uint64_t bytes, const uint64_t* offsets,
                        uint64_t n, int32_t in_mem, void* out_records, uint64_t capacity, int32_t out_mem,
                        uint8_t* status, gnm_netflow_stats* stats);
+
+/* ---- FLOWARC1 archives (flow_store.cpp:144-207) ---------------------------
+ * An archive in memory (host or device, device buffers 4-byte aligned):
+ * "FLOWARC1", be32 version 1, be64 count, then count 64-byte big-endian
+ * entries (be64 start_ms, be64 end_ms, 48-byte raw record). The header and
+ * length checks are FlowStore::load's, as status codes.
+ * gnm_decode_archive: FlowStore::load -> FlowRecord rows (64 B) in
+ *   `out_records` (memory `out_mem`, `capacity` rows); *n_out = count.
+ * gnm_accumulate_archive / gnm_analyze_archive: aggregate over the
+ *   archive's records with K2 reading the entries in place (no decode pass;
+ *   host archives stream through the chunked H2D loader). */
+int gnm_decode_archive(gnm_ctx* ctx, const uint8_t* bytes, uint64_t len, int32_t in_mem, void* out_records,
+                       uint64_t capacity, int32_t out_mem, uint64_t* n_out);
+int gnm_accumulate_archive(gnm_ctx* ctx, const gnm_registry* reg, const gnm_filter_params* params,
+                           const uint8_t* bytes, uint64_t len, int32_t mem);
+int gnm_analyze_archive(gnm_ctx* ctx, const gnm_registry* reg, const gnm_filter_params* params,
+                        const uint8_t* bytes, uint64_t len, int32_t mem, gnm_result* result);
 
 /* ---- Warning rule: evaluate_warnings (monitor.cpp:13-34) ----------------- */
 typedef struct gnm_warning_state gnm_warning_state;

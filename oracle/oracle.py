@@ -225,6 +225,8 @@ class Reference:
             "ref_ingest_datagram": (C.c_int, [V, C.c_size_t, V, V, V]),
             "ref_encode_packet": (C.c_size_t, [V, V, C.c_size_t, V]),
             "ref_raw_record_size": (C.c_size_t, []),
+            "ref_archive_write": (C.c_int, [V, C.c_char_p]),
+            "ref_archive_load": (V, [C.c_char_p, V]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -245,6 +247,38 @@ class Reference:
         st = self.L.ref_ingest_datagram(buf.ctypes.data, len(datagram), out.ctypes.data, C.byref(n),
                                         C.byref(rej))
         return st, out[: n.value * 64].tobytes(), rej.value
+
+    def write_archive(self, rows: np.ndarray, path: str) -> None:
+        """FlowStore::write_archive of FlowRecord rows (64-byte structured or
+        uint8 array)."""
+        b = np.ascontiguousarray(rows).view(np.uint8).reshape(-1, 64)
+        import ctypes as _C
+        n = len(b)
+        cols = [np.ascontiguousarray(b[:, o:o + w]).view(t).ravel() for o, w, t in
+                ((0, 4, np.uint32), (4, 4, np.uint32), (16, 4, np.uint32), (20, 4, np.uint32),
+                 (48, 8, np.uint64), (56, 8, np.uint64))]
+        h = self.L.ref_records_create(*[c.ctypes.data for c in cols], n)
+        # ref_records_create fills only the hot fields: overwrite with the full rows
+        if n:
+            _C.memmove(self.L.ref_records_data(h), b.ctypes.data, n * 64)
+        try:
+            if self.L.ref_archive_write(h, path.encode()) != 0:
+                raise RuntimeError(self.err())
+        finally:
+            self.L.ref_records_destroy(h)
+
+    def load_archive(self, path: str):
+        """FlowStore::load -> (FlowRecord rows as uint8 bytes, error kind or -1)."""
+        kind = C.c_int()
+        h = self.L.ref_archive_load(path.encode(), C.byref(kind))
+        if not h:
+            return None, kind.value
+        try:
+            n = self.L.ref_records_size(h)
+            buf = (C.c_uint8 * (n * 64)).from_address(self.L.ref_records_data(h)) if n else b""
+            return bytes(buf), -1
+        finally:
+            self.L.ref_records_destroy(h)
 
     def encode_packet(self, header: Sequence[int], raw: np.ndarray) -> bytes:
         """encode_packet(ExportHeader{header...}, raw RawFlowRecord rows)."""

@@ -15,6 +15,7 @@
 #include <string>
 #include <vector>
 
+#include "flowmon/flow_store.hpp"
 #include "flowmon/monitor.hpp"
 #include "flowmon/netflow.hpp"
 #include "flowmon/rate_engine.hpp"
@@ -451,4 +452,29 @@ size_t ref_encode_packet(const uint32_t* h, const void* raw, size_t n, uint8_t* 
     }
 }
 size_t ref_raw_record_size() { return sizeof(RawFlowRecord); }
+
+// ---- FLOWARC1 archives (flow_store.cpp:144-207) ------------------------------
+// FlowStore::write_archive of a records handle (ref_records_create /
+// ref_generate); 0 or -1 (ref_last_error).
+int ref_archive_write(const void* records, const char* path) {
+    try {
+        const auto* v = static_cast<const std::vector<FlowRecord>*>(records);
+        FlowStore::write_archive(path, *v);
+        return 0;
+    } catch (const std::exception& e) {
+        set_err(e);
+        return -1;
+    }
+}
+// FlowStore::load -> a records handle, or null with *kind = ArchiveError::Kind.
+void* ref_archive_load(const char* path, int* kind) {
+    *kind = -1;
+    try {
+        return new std::vector<FlowRecord>(FlowStore::load(path));
+    } catch (const ArchiveError& e) {
+        set_err(e);
+        *kind = static_cast<int>(e.kind());
+        return nullptr;
+    }
+}
 } // extern "C"

@@ -33,6 +33,9 @@ ERR_ZERO_DURATION = 6
 ERR_EMPTY_HISTOGRAM = 7
 ERR_NO_DEVICE = 8
 ERR_CAPACITY = 9
+ERR_BAD_MAGIC = 10
+ERR_BAD_VERSION = 11
+ERR_TRUNCATED = 12
 
 HOT_OFF = 0
 HOT_AUTO = 1
@@ -160,6 +163,11 @@ _SIGS = [
     ("gnm_reset", C.c_int, [_P]),
     ("gnm_get_partials", C.c_int, [_P, _P, C.POINTER(gnm_partials)]),
     ("gnm_prepare_median", C.c_int, [_P, _P]),
+    ("gnm_decode_archive", C.c_int, [_P, _P, C.c_uint64, C.c_int32, _P, C.c_uint64, C.c_int32, _P]),
+    ("gnm_accumulate_archive", C.c_int,
+     [_P, _P, C.POINTER(gnm_filter_params), _P, C.c_uint64, C.c_int32]),
+    ("gnm_analyze_archive", C.c_int,
+     [_P, _P, C.POINTER(gnm_filter_params), _P, C.c_uint64, C.c_int32, C.POINTER(gnm_result)]),
     ("gnm_decode_netflow", C.c_int,
      [_P, _P, C.c_uint64, _P, C.c_uint64, C.c_int32, _P, C.c_uint64, C.c_int32, _P,
       C.POINTER(gnm_netflow_stats)]),

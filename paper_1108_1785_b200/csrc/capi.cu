@@ -414,7 +414,7 @@ gnm::DevBatch aos_batch(const void* rec, uint64_t n) {
 // Columns already in pinned memory DMA straight from the caller's buffers;
 // pageable columns go through the context's pinned staging slots.
 void load_and_run(gnm_ctx* c, bool aos, const void* const* cols, const size_t* widths, int ncols,
-                  uint64_t n, const gnm::DevParams& p) {
+                  uint64_t n, const gnm::DevParams& p, bool archive = false) {
     size_t rec_bytes = 0;
     bool pinned = true;
     for (int i = 0; i < ncols; ++i) {
@@ -466,7 +466,9 @@ void load_and_run(gnm_ctx* c, bool aos, const void* const* cols, const size_t* w
         }
         ck(cudaEventRecord(c->ev_h2d[slot], c->copy_stream), "cudaEventRecord");
         ck(cudaStreamWaitEvent(c->stream, c->ev_h2d[slot], 0), "cudaStreamWaitEvent");
-        launch_k2_timed(c, aos ? aos_batch(dcols[0], m) : soa_batch(dcols, m), p);
+        gnm::DevBatch db = aos ? aos_batch(dcols[0], m) : soa_batch(dcols, m);
+        db.archive = archive;
+        launch_k2_timed(c, db, p);
         ck(cudaEventRecord(c->ev_k2[slot], c->stream), "cudaEventRecord");
     }
     // The caller's host buffers may be reused once their copies are done.
@@ -951,6 +953,110 @@ int gnm_decode_netflow(gnm_ctx* c, const uint8_t* datagrams, uint64_t bytes, con
             stats->records_accepted = hs[3];
         }
         return rc;
+    });
+}
+
+// FlowStore::load's checks (flow_store.cpp:167-207) on an in-memory archive:
+// returns the record count or fails with the ArchiveError kind's status.
+int archive_header(gnm_ctx* c, const uint8_t* bytes, uint64_t len, int32_t mem, uint64_t* count) {
+    if (mem != GNM_MEM_HOST && mem != GNM_MEM_DEVICE)
+        return fail(GNM_ERR_INVALID_ARGUMENT, "mem must be GNM_MEM_HOST or GNM_MEM_DEVICE");
+    if (len < 20) return fail(GNM_ERR_TRUNCATED, "archive header truncated");
+    if (!bytes) return fail(GNM_ERR_INVALID_ARGUMENT, "null archive");
+    uint8_t h[20];
+    if (mem == GNM_MEM_DEVICE) {
+        ck(cudaMemcpyAsync(h, bytes, 20, cudaMemcpyDeviceToHost, c->stream), "D2H archive header");
+        ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    } else {
+        std::memcpy(h, bytes, 20);
+    }
+    if (std::memcmp(h, "FLOWARC1", 8) != 0) return fail(GNM_ERR_BAD_MAGIC, "bad archive magic");
+    const uint32_t version = uint32_t(h[8]) << 24 | uint32_t(h[9]) << 16 | uint32_t(h[10]) << 8 | h[11];
+    if (version != 1) return fail(GNM_ERR_BAD_VERSION, "unsupported archive version " + std::to_string(version));
+    uint64_t n = 0;
+    for (int i = 0; i < 8; ++i) n = n << 8 | h[12 + i];
+    if ((len - 20) / 64 < n) return fail(GNM_ERR_TRUNCATED, "archive body truncated");
+    if (len - 20 != n * 64) return fail(GNM_ERR_TRUNCATED, "trailing bytes after " + std::to_string(n) + " records");
+    if (mem == GNM_MEM_DEVICE && (reinterpret_cast<uintptr_t>(bytes) & 3u))
+        return fail(GNM_ERR_INVALID_ARGUMENT, "device archive must be 4-byte aligned");
+    *count = n;
+    return GNM_OK;
+}
+
+int accumulate_archive(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* params,
+                       const uint8_t* bytes, uint64_t len, int32_t mem, const Window* win) {
+    uint64_t n = 0;
+    if (int e = archive_header(c, bytes, len, mem, &n)) return e;
+    if (c->prepared) return fail(GNM_ERR_INVALID_ARGUMENT, "gnm_prepare_median already ran; finalize first");
+    if (int e = begin_accumulate(c, reg)) return e;
+    gnm::DevParams p = dev_params(c, params);
+    apply_window(p, win);
+    if (n == 0) return GNM_OK;
+    if (mem == GNM_MEM_DEVICE) {
+        gnm::DevBatch b = aos_batch(bytes + 20, n);
+        b.archive = true;
+        launch_k2_timed(c, b, p);
+    } else {
+        const void* cols[1] = {bytes + 20};
+        const size_t widths[1] = {64};
+        load_and_run(c, true, cols, widths, 1, n, p, true);
+    }
+    return GNM_OK;
+}
+
+int gnm_decode_archive(gnm_ctx* c, const uint8_t* bytes, uint64_t len, int32_t in_mem, void* out_records,
+                       uint64_t capacity, int32_t out_mem, uint64_t* n_out) {
+    if (!c || !n_out) return fail(GNM_ERR_INVALID_ARGUMENT, "null argument");
+    if (out_mem != GNM_MEM_HOST && out_mem != GNM_MEM_DEVICE)
+        return fail(GNM_ERR_INVALID_ARGUMENT, "out_mem must be GNM_MEM_HOST or GNM_MEM_DEVICE");
+    return guarded([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        uint64_t n = 0;
+        if (int e = archive_header(c, bytes, len, in_mem, &n)) return e;
+        *n_out = n;
+        if (n > capacity) return fail(GNM_ERR_CAPACITY, std::to_string(n) + " records exceed capacity");
+        if (n == 0) return static_cast<int>(GNM_OK);
+        cudaStream_t s = c->stream;
+        const uint8_t* d = bytes + 20;
+        uint8_t* din = nullptr;
+        uint8_t* dout = static_cast<uint8_t*>(out_records);
+        const bool dev_out = out_mem == GNM_MEM_DEVICE && (reinterpret_cast<uintptr_t>(out_records) & 15u) == 0;
+        if (in_mem == GNM_MEM_HOST) {
+            ck(cudaMallocAsync(reinterpret_cast<void**>(&din), n * 64, s), "cudaMallocAsync(archive)");
+            ck(cudaMemcpyAsync(din, bytes + 20, n * 64, cudaMemcpyHostToDevice, s), "H2D archive");
+            d = din;
+        }
+        uint8_t* staged = nullptr;
+        if (!dev_out) {
+            ck(cudaMallocAsync(reinterpret_cast<void**>(&staged), n * 64, s), "cudaMallocAsync(archive out)");
+            dout = staged;
+        }
+        ck(gnm::launch_archive_decode(d, n, dout, s), "archive decode");
+        c->kernel_launches += 1;
+        if (!dev_out)
+            ck(cudaMemcpyAsync(out_records, staged, n * 64,
+                               out_mem == GNM_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s),
+               "copy records");
+        if (din) ck(cudaFreeAsync(din, s), "cudaFreeAsync");
+        if (staged) ck(cudaFreeAsync(staged, s), "cudaFreeAsync");
+        ck(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        return static_cast<int>(GNM_OK);
+    });
+}
+
+int gnm_accumulate_archive(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* params,
+                           const uint8_t* bytes, uint64_t len, int32_t mem) {
+    if (!c || !reg) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx/registry");
+    return guarded([&] { return accumulate_archive(c, reg, params, bytes, len, mem, nullptr); });
+}
+
+int gnm_analyze_archive(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* params,
+                        const uint8_t* bytes, uint64_t len, int32_t mem, gnm_result* result) {
+    if (!c || !reg) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx/registry");
+    if (c->accumulating) return fail(GNM_ERR_INVALID_ARGUMENT, "an accumulation is in progress");
+    return guarded([&] {
+        if (int e = accumulate_archive(c, reg, params, bytes, len, mem, nullptr)) return e;
+        return finalize(c, reg, result);
     });
 }
 

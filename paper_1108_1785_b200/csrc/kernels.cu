@@ -573,11 +573,24 @@ __device__ __forceinline__ void load_record(const DevBatch& b, uint64_t i, uint3
         const uint2 cc = __ldg(reinterpret_cast<const uint2*>(r + 16));           // pkts octets
         const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(r + 48));  // start end
         src = a.x, dst = a.y, pkts = cc.x, oct = cc.y, dur = e.y - e.x, end = e.y;
-    } else {
+    } else if constexpr (kLayout == 3) {
         const unsigned char* r = static_cast<const unsigned char*>(b.rec) + i * 64;
         const uint32_t* w = reinterpret_cast<const uint32_t*>(r);
         const uint64_t* qq = reinterpret_cast<const uint64_t*>(r + 48);
         src = w[0], dst = w[1], pkts = w[4], oct = w[5], dur = qq[1] - qq[0], end = qq[1];
+    } else {
+        // FLOWARC1 entry in place (flow_store.cpp:158-162): be64 start, be64
+        // end, then the 48-byte big-endian raw record (netflow.cpp:52-75).
+        // Entries sit at 20 + 64*i: 4-byte aligned words, byte-swapped.
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(static_cast<const unsigned char*>(b.rec) + i * 64);
+        const uint64_t start = static_cast<uint64_t>(__byte_perm(__ldg(w + 0), 0, 0x0123)) << 32 |
+                               __byte_perm(__ldg(w + 1), 0, 0x0123);
+        end = static_cast<uint64_t>(__byte_perm(__ldg(w + 2), 0, 0x0123)) << 32 | __byte_perm(__ldg(w + 3), 0, 0x0123);
+        src = __byte_perm(__ldg(w + 4), 0, 0x0123);
+        dst = __byte_perm(__ldg(w + 5), 0, 0x0123);
+        pkts = __byte_perm(__ldg(w + 8), 0, 0x0123);
+        oct = __byte_perm(__ldg(w + 9), 0, 0x0123);
+        dur = end - start;
     }
 }
 
@@ -723,7 +736,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_soa(DevBatch b, const uint32_t
 }
 
 // Other layouts: unaligned SoA (1), AoS 64-byte rows with vector (2) or
-// scalar (3) loads. CTA b owns records [b*n/G, (b+1)*n/G) (at most
+// scalar (3) loads, FLOWARC1 archive entries read in place (4). CTA b owns records [b*n/G, (b+1)*n/G) (at most
 // kCtaRecords), one record per lane per round.
 template <int kLayout, bool kSmem, bool kHot, bool kWin>
 __global__ void __launch_bounds__(kK2Block, 1) k2_gen(DevBatch b, const uint32_t* __restrict__ gt,
@@ -755,7 +768,8 @@ __global__ void __launch_bounds__(kK2Block) k_sample(DevBatch b, const uint32_t*
         const uint64_t i = base + j;
         uint32_t src, dst, pkts, oct;
         uint64_t dur, end;
-        if (b.aos) load_record<3>(b, i, src, dst, pkts, oct, dur, end);
+        if (b.archive) load_record<4>(b, i, src, dst, pkts, oct, dur, end);
+        else if (b.aos) load_record<3>(b, i, src, dst, pkts, oct, dur, end);
         else load_record<1>(b, i, src, dst, pkts, oct, dur, end);
         if (static_cast<uint64_t>(oct) < p.ack_plus1 * pkts || pkts < p.min_packets1 ||
             dur < static_cast<uint64_t>(p.min_duration1) || (p.windowed && !(end >= p.win_lo && end < p.win_hi)))
@@ -1210,6 +1224,7 @@ void launch_k2_l(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t, con
 size_t table_smem_bytes(uint32_t table_words) { return static_cast<size_t>(table_words) * 4; }
 
 int k2_layout(const DevBatch& b) {
+    if (b.archive) return 4;
     if (b.aos) return (reinterpret_cast<uintptr_t>(b.rec) & 15u) == 0 ? 2 : 3;
     const DevSoA& c = b.soa;
     const bool vec = ((reinterpret_cast<uintptr_t>(c.src) | reinterpret_cast<uintptr_t>(c.dst) |
@@ -1227,6 +1242,7 @@ cudaError_t init_kernel_attributes() {
     if ((e = allow_layout<1>())) return e;
     if ((e = allow_layout<2>())) return e;
     if ((e = allow_layout<3>())) return e;
+    if ((e = allow_layout<4>())) return e;
     if ((e = allow_smem(k_sample<true>))) return e;
     return allow_smem(k_classify<true>);
 }
@@ -1305,7 +1321,8 @@ cudaError_t launch_k2(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t
         break;
     case 1: launch_k2_l<1>(cfg, b, t, p, P, hot, log, s); break;
     case 2: launch_k2_l<2>(cfg, b, t, p, P, hot, log, s); break;
-    default: launch_k2_l<3>(cfg, b, t, p, P, hot, log, s); break;
+    case 3: launch_k2_l<3>(cfg, b, t, p, P, hot, log, s); break;
+    default: launch_k2_l<4>(cfg, b, t, p, P, hot, log, s); break;
     }
     return cudaGetLastError();
 }

@@ -89,6 +89,7 @@ struct DevSoA {
 // A batch is SoA columns or 64-byte flowmon::FlowRecord AoS rows.
 struct DevBatch {
     bool aos;
+    bool archive; // aos rows are FLOWARC1 entries (big-endian, flow_store.cpp:144-165)
     DevSoA soa;
     const void* rec;
     uint64_t n;

@@ -167,7 +167,36 @@ __global__ void __launch_bounds__(256) n3_decode(const uint8_t* __restrict__ d,
     }
 }
 
+// FlowStore::load's entry decode (flow_store.cpp:194-200), thread per entry:
+// be64 start/end and decode_raw_record of the big-endian raw record, written
+// as the 64-byte little-endian FlowRecord (raw fields, start_ms, end_ms).
+__global__ void __launch_bounds__(256) a1_decode(const uint32_t* __restrict__ e, uint64_t n,
+                                                 uint4* __restrict__ out) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t* w = e + i * 16;
+        uint32_t x[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) x[k] = __ldg(w + k);
+        auto sw = [](uint32_t v) { return __byte_perm(v, 0, 0x0123); };  // be32
+        auto sw16 = [](uint32_t v) { return __byte_perm(v, 0, 0x2301); }; // two be16
+        uint4* o = out + i * 4;
+        // raw record = entry words 4..15
+        o[0] = make_uint4(sw(x[4]), sw(x[5]), sw(x[6]), sw16(x[7]));
+        o[1] = make_uint4(sw(x[8]), sw(x[9]), sw(x[10]), sw(x[11]));
+        o[2] = make_uint4(sw16(x[12]), x[13], sw16(x[14]), __byte_perm(x[15], 0, 0x2310));
+        o[3] = make_uint4(sw(x[1]), sw(x[0]), sw(x[3]), sw(x[2])); // start_ms, end_ms (LE u64)
+    }
+}
+
 } // namespace
+
+cudaError_t launch_archive_decode(const uint8_t* entries, uint64_t n, uint8_t* out, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const uint32_t g = static_cast<uint32_t>(std::min<uint64_t>((n + 255) / 256, 148 * 16));
+    a1_decode<<<g, 256, 0, s>>>(reinterpret_cast<const uint32_t*>(entries), n, reinterpret_cast<uint4*>(out));
+    return cudaGetLastError();
+}
 
 cudaError_t launch_netflow_decode(const uint8_t* d, const uint64_t* off, uint64_t n, uint32_t* accepted,
                                   uint64_t* base, uint8_t* status, unsigned long long* stats,

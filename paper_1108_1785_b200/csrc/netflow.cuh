@@ -16,4 +16,7 @@ cudaError_t launch_netflow_decode(const uint8_t* d, const uint64_t* off, uint64_
                                   uint64_t* base, uint8_t* status, unsigned long long* stats,
                                   uint8_t* out, cudaStream_t s);
 
+// FLOWARC1 entries (64 B, big-endian, 4-byte aligned) -> FlowRecord rows.
+cudaError_t launch_archive_decode(const uint8_t* entries, uint64_t n, uint8_t* out, cudaStream_t s);
+
 } // namespace gnm

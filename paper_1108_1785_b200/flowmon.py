@@ -64,6 +64,15 @@ class CatalogError(ValueError):
         self.kind = kind
 
 
+class ArchiveError(RuntimeError):
+    """flow_store.hpp:22-33; ``kind`` is "BadMagic", "BadVersion" or
+    "TruncatedArchive" (IoFailure has no in-memory counterpart)."""
+
+    def __init__(self, kind: str, message: str):
+        super().__init__(message)
+        self.kind = kind
+
+
 class RateError(ArithmeticError):
     """rate_engine.hpp:35-45; ``kind`` is "ZeroDuration" or "EmptyHistogram"."""
 
@@ -80,6 +89,9 @@ def _check(status: int) -> None:
         raise CatalogError("Overlap", msg)
     if status == _lib.ERR_INVALID_CIDR:
         raise CatalogError("InvalidCidr", msg)
+    if status in (_lib.ERR_BAD_MAGIC, _lib.ERR_BAD_VERSION, _lib.ERR_TRUNCATED):
+        raise ArchiveError({_lib.ERR_BAD_MAGIC: "BadMagic", _lib.ERR_BAD_VERSION: "BadVersion",
+                            _lib.ERR_TRUNCATED: "TruncatedArchive"}[status], msg)
     raise GnmError(status, msg)
 
 
@@ -616,6 +628,38 @@ class Engine:
         stats = {"datagrams": st.datagrams, "decode_errors": st.decode_errors,
                  "records_rejected": st.records_rejected, "records_accepted": k}
         return recs, status[:n], stats
+
+    @staticmethod
+    def _archive_arg(archive):
+        if _is_torch(archive):
+            return archive.data_ptr(), archive.numel(), (_lib.MEM_DEVICE if archive.is_cuda else _lib.MEM_HOST), archive
+        a = np.frombuffer(archive, np.uint8) if isinstance(archive, (bytes, bytearray)) else \
+            np.ascontiguousarray(archive, np.uint8)
+        return (a.ctypes.data if a.size else None), a.size, _lib.MEM_HOST, a
+
+    def decode_archive(self, archive) -> np.ndarray:
+        """FlowStore::load (flow_store.cpp:167-207) of an in-memory FLOWARC1
+        archive (bytes, numpy uint8 or a uint8 tensor) on the GPU:
+        FLOW_RECORD_DTYPE rows. Raises ArchiveError as the reference does."""
+        ptr, n, mem, keep = self._archive_arg(archive)
+        cap = max((n - 20) // 64, 0) if n >= 20 else 0
+        out = np.zeros(max(cap, 1), FLOW_RECORD_DTYPE)
+        k = C.c_uint64()
+        _check(lib.gnm_decode_archive(self._h, ptr, n, mem, out.ctypes.data, cap, _lib.MEM_HOST, C.byref(k)))
+        return out[:k.value]
+
+    def aggregate_archive(self, archive, catalog: SiteCatalog, params: Optional[FilterParams] = None,
+                          window_start_ms: int = 0, window_end_ms: int = 0,
+                          threshold_bps: float = kDefaultWarnThresholdBps,
+                          histograms: bool = False) -> AnalysisResult:
+        """aggregate(FlowStore::load(archive), ...) (flowmon.cpp analyze):
+        K2 reads the archive's big-endian entries in place."""
+        ptr, n, mem, keep = self._archive_arg(archive)
+        p = self._params(params)
+        r, table, hist, ns = self._result(catalog, window_start_ms, window_end_ms, threshold_bps,
+                                          histograms)
+        _check(lib.gnm_analyze_archive(self._h, catalog.handle, C.byref(p), ptr, n, mem, C.byref(r)))
+        return _build_result(r, table[:ns], None if hist is None else hist[:ns])
 
     def partials(self, catalog: SiteCatalog) -> dict:
         """Device pointers of the accumulation (gnm_get_partials) for a
