@@ -12,8 +12,8 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
            -Xptxas -v -cudart static -Iinclude
 PKG := paper_1108_1785_b200
-SRCS := $(PKG)/csrc/capi.cu $(PKG)/csrc/kernels.cu $(PKG)/csrc/netflow.cu $(PKG)/csrc/registry.cpp
-HDRS := include/gnetmon.h $(PKG)/csrc/kernels.cuh $(PKG)/csrc/netflow.cuh $(PKG)/csrc/registry.hpp
+SRCS := $(PKG)/csrc/capi.cu $(PKG)/csrc/kernels.cu $(PKG)/csrc/netflow.cu $(PKG)/csrc/hosts.cu $(PKG)/csrc/registry.cpp
+HDRS := include/gnetmon.h $(PKG)/csrc/kernels.cuh $(PKG)/csrc/netflow.cuh $(PKG)/csrc/hosts.cuh $(PKG)/csrc/registry.hpp
 
 .PHONY: all ref clean oracle ablation
 all: $(PKG)/lib/libgnetmon.so $(PKG)/lib/libgnm_synth.so oracle

@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define GNM_ABI_VERSION 2
+#define GNM_ABI_VERSION 3
 
 /* rate_engine.hpp:18-20 */
 #define GNM_BUCKET_COUNT 10001
@@ -167,6 +167,22 @@ typedef struct gnm_result {
     gnm_tallies tallies;
 } gnm_result;
 
+/* Per-host statistics: one row per (site, host) of SiteResult::hosts
+ * (rate_engine.hpp:84-99; finalize, rate_engine.cpp:272-289). The host is
+ * the flow's matched endpoint: src_addr when the src lookup hits, else
+ * dst_addr (reduce_slice, rate_engine.cpp:216-232). */
+typedef struct gnm_host_stats {
+    uint32_t site;
+    uint32_t host;          /* IPv4, host order */
+    uint64_t flow_count;    /* RateStats of the host's histogram (stats_from) */
+    uint64_t rate_ubps_lo;  /* exact u128 sum of per-flow micro-bps */
+    uint64_t rate_ubps_hi;
+    double min_bps;
+    double max_bps;
+    double avg_bps;
+    double median_bps;      /* lower median, clamped into [min,max] */
+} gnm_host_stats;
+
 /* ---- Device context -------------------------------------------------------- */
 typedef struct gnm_ctx gnm_ctx;
 
@@ -187,6 +203,19 @@ int gnm_ctx_set_chunk_records(gnm_ctx* ctx, uint64_t records);
 #define GNM_HOT_AUTO 1
 #define GNM_HOT_FORCE 2
 int gnm_ctx_set_hot_mode(gnm_ctx* ctx, int mode);
+/* Per-host mode (off by default): K2 also logs each Forward flow's host,
+ * rate and micro-bps, and every finalize then builds the per-host rows,
+ * sorted by (site, host) like the reference's std::map iteration. Only
+ * between accumulations. The rows reflect this context's own accumulation
+ * (per-host results are not part of the cross-GPU partials). */
+int gnm_ctx_set_hosts(gnm_ctx* ctx, int enable);
+/* Rows of the last finalize in per-host mode (0 otherwise). */
+uint64_t gnm_host_count(gnm_ctx* ctx);
+/* Copy the last finalize's rows into out[capacity] (GNM_ERR_CAPACITY when
+ * short) and, when `histograms` is non-NULL, each row's RateHistogram
+ * buckets (HostResult::histogram) into histograms[capacity * 10001]. Valid
+ * until the next finalize or reset. */
+int gnm_host_results(gnm_ctx* ctx, gnm_host_stats* out, uint64_t capacity, uint32_t* histograms);
 
 /* aggregate() (rate_engine.cpp:335-347) + the K3 site synthesis
  * (finalize/stats_from, rate_engine.cpp:242-292) in one synchronous call.

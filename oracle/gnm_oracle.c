@@ -210,6 +210,36 @@ void orc_aggregate(const uint32_t* src, const uint32_t* dst, const uint32_t* pkt
     }
 }
 
+/* Per-flow keys for the per-host restatement (reduce_slice,
+ * rate_engine.cpp:197-239): class, and for Forward flows the site, the host
+ * (src when the src lookup hits, else dst: :216-231), the bucket (:10), the
+ * f64 rate (:236) and the exact micro-bps (flow_rate_ubps, :111-117). The
+ * grouping by (site << 32 | host) and stats_from per group (:272-289) are in
+ * oracle.py (Oracle.host_stats). */
+void orc_flow_keys(const uint32_t* src, const uint32_t* dst, const uint32_t* pkts,
+                   const uint32_t* octets, const uint64_t* start, const uint64_t* end, size_t n,
+                   const orc_params* p, const orc_catalog* c, uint8_t* cls, uint32_t* site,
+                   uint32_t* host, uint32_t* bucket, double* rate, uint64_t* ubps_lo,
+                   uint64_t* ubps_hi) {
+    for (size_t i = 0; i < n; ++i) {
+        uint32_t s = 0, h = 0;
+        const int k = orc_classify_one(src[i], dst[i], pkts[i], octets[i], start[i], end[i], p, c, 0, &s, &h);
+        cls[i] = (uint8_t)k;
+        site[i] = k == 0 ? s : ORC_NO_SITE;
+        host[i] = k == 0 ? h : 0;
+        bucket[i] = 0;
+        rate[i] = 0;
+        ubps_lo[i] = ubps_hi[i] = 0;
+        if (k != 0) continue;
+        const uint64_t dur = end[i] - start[i];
+        rate[i] = orc_flow_rate(octets[i], dur);
+        bucket[i] = orc_bucket_index(rate[i]);
+        const u128 u = orc_rate_ubps(octets[i], dur);
+        ubps_lo[i] = (uint64_t)u;
+        ubps_hi[i] = (uint64_t)(u >> 64);
+    }
+}
+
 /* RateHistogram::median_bps, rate_engine.cpp:42-58 (count > 0). */
 double orc_median_bps(const uint32_t* row, uint64_t count) {
     const uint64_t target = (count + 1) / 2;

@@ -67,6 +67,7 @@ class Oracle:
                                      V, V, V]
         L.orc_evaluate_warnings.restype = C.c_size_t
         L.orc_evaluate_warnings.argtypes = [C.c_uint32, V, V, V, C.c_double, V]
+        L.orc_flow_keys.argtypes = [V] * 6 + [C.c_size_t, C.POINTER(_Params), V] + [V] * 7
         L.orc_u128_to_double.restype = C.c_double
         L.orc_u128_to_double.argtypes = [C.c_uint64, C.c_uint64]
         self.L = L
@@ -144,6 +145,60 @@ class Oracle:
 
     def analyze(self, cols, cat: "OrcCatalog", n_sites: int, params=DEFAULT_PARAMS) -> dict:
         return self.finalize(self.aggregate(cols, cat, n_sites, params))
+
+    def flow_keys(self, cols, cat: "OrcCatalog", params=DEFAULT_PARAMS) -> dict:
+        c = _cols(cols)
+        n = len(c[0])
+        out = {"cls": np.zeros(n, np.uint8), "site": np.zeros(n, np.uint32), "host": np.zeros(n, np.uint32),
+               "bucket": np.zeros(n, np.uint32), "rate": np.zeros(n), "ubps_lo": np.zeros(n, np.uint64),
+               "ubps_hi": np.zeros(n, np.uint64)}
+        p = _Params(*params, 1)
+        self.L.orc_flow_keys(*[_p(x) for x in c], n, C.byref(p), cat.h,
+                             *[out[k].ctypes.data for k in ("cls", "site", "host", "bucket", "rate",
+                                                           "ubps_lo", "ubps_hi")])
+        return out
+
+    def host_stats(self, cols, cat: "OrcCatalog", params=DEFAULT_PARAMS, hist: bool = False) -> dict:
+        """SiteResult::hosts of finalize (rate_engine.cpp:272-289): one row per
+        (site, host) in (site, host) order -- the std::map iteration order --
+        with stats_from (:242-253) of the host's flows. ``hist``: sparse
+        histograms (row, bucket, count)."""
+        k = self.flow_keys(cols, cat, params)
+        fwd = k["cls"] == 0
+        key = (k["site"][fwd].astype(np.uint64) << np.uint64(32)) | k["host"][fwd].astype(np.uint64)
+        bucket = k["bucket"][fwd]
+        order = np.lexsort((bucket, key))
+        key, bucket = key[order], bucket[order]
+        rate, lo, hi = k["rate"][fwd][order], k["ubps_lo"][fwd][order], k["ubps_hi"][fwd][order]
+        uk, start, cnt = np.unique(key, return_index=True, return_counts=True)
+        n = len(uk)
+        out = {"site": (uk >> np.uint64(32)).astype(np.uint32), "host": (uk & np.uint64(0xFFFFFFFF)).astype(np.uint32),
+               "count": cnt.astype(np.uint64), "ubps_lo": np.zeros(n, np.uint64), "ubps_hi": np.zeros(n, np.uint64),
+               "min": np.zeros(n), "max": np.zeros(n), "avg": np.zeros(n), "median": np.zeros(n)}
+        if n == 0:
+            return out
+        m32 = np.uint64(0xFFFFFFFF)
+        l0 = np.add.reduceat(lo & m32, start)
+        l1 = np.add.reduceat(lo >> np.uint64(32), start)
+        l2 = np.add.reduceat(hi, start)
+        out["min"] = np.minimum.reduceat(rate, start)
+        out["max"] = np.maximum.reduceat(rate, start)
+        kmed = bucket[start + (cnt + 1) // 2 - 1]
+        med = np.where(kmed == BUCKETS - 1, 100000000.0, kmed.astype(np.float64) * 10000.0 + 5000.0)
+        out["median"] = np.minimum(np.maximum(med, out["min"]), out["max"])  # std::clamp
+        for i in range(n):
+            u = int(l0[i]) + (int(l1[i]) << 32) + (int(l2[i]) << 64)
+            out["ubps_lo"][i] = u & (2**64 - 1)
+            out["ubps_hi"][i] = u >> 64
+            out["avg"][i] = (self.u128_to_double(u) / 1e6) / float(cnt[i])
+        if hist:
+            row = np.repeat(np.arange(n), cnt)
+            pair = row.astype(np.uint64) << np.uint64(14) | bucket.astype(np.uint64)
+            up, pc = np.unique(pair, return_counts=True)
+            out["hist_row"] = (up >> np.uint64(14)).astype(np.uint32)
+            out["hist_bucket"] = (up & np.uint64(0x3FFF)).astype(np.uint32)
+            out["hist_count"] = pc.astype(np.uint32)
+        return out
 
     def evaluate_warnings(self, count, median, streak: np.ndarray, threshold: float = 1e6):
         cnt = np.ascontiguousarray(count, np.uint64)

@@ -110,6 +110,14 @@ SITE_STATS_DTYPE = np.dtype([
 ])
 assert SITE_STATS_DTYPE.itemsize == 72
 
+# gnm_host_stats (64 bytes, C layout).
+HOST_STATS_DTYPE = np.dtype([
+    ("site", "<u4"), ("host", "<u4"), ("flow_count", "<u8"), ("rate_ubps_lo", "<u8"),
+    ("rate_ubps_hi", "<u8"), ("min_bps", "<f8"), ("max_bps", "<f8"), ("avg_bps", "<f8"),
+    ("median_bps", "<f8"),
+])
+assert HOST_STATS_DTYPE.itemsize == 64
+
 # The 64-byte flowmon::FlowRecord (netflow.hpp:32-67).
 FLOW_RECORD_DTYPE = np.dtype({
     "names": ["src_addr", "dst_addr", "next_hop", "input_if", "output_if", "d_pkts", "d_octets",
@@ -146,6 +154,9 @@ _SIGS = [
     ("gnm_ctx_stream", _P, [_P]),
     ("gnm_ctx_set_chunk_records", C.c_int, [_P, C.c_uint64]),
     ("gnm_ctx_set_hot_mode", C.c_int, [_P, C.c_int]),
+    ("gnm_ctx_set_hosts", C.c_int, [_P, C.c_int]),
+    ("gnm_host_count", C.c_uint64, [_P]),
+    ("gnm_host_results", C.c_int, [_P, _P, C.c_uint64, _P]),
     ("gnm_analyze", C.c_int,
      [_P, _P, C.POINTER(gnm_filter_params), C.POINTER(gnm_batch_soa), C.POINTER(gnm_result)]),
     ("gnm_analyze_aos", C.c_int,

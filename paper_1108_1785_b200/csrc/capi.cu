@@ -18,6 +18,7 @@
 
 #include "gnetmon.h"
 #include "kernels.cuh"
+#include "hosts.cuh"
 #include "netflow.cuh"
 #include "registry.hpp"
 
@@ -97,6 +98,14 @@ struct gnm_ctx {
     unsigned int* d_counts = nullptr;
     size_t counts_cap = 0, counts_used = 0;
     std::vector<LogSlice> slices;
+    // hosts mode (gnm_ctx_set_hosts): per-entry host, rate bits, micro-bps
+    bool hosts = false;
+    unsigned int* d_lhost = nullptr;
+    unsigned long long* d_lrate = nullptr;
+    unsigned long long* d_llo = nullptr;
+    unsigned int* d_lhi = nullptr;
+    size_t lhost_cap = 0;
+    gnm::HostRows hrows;
     bool prepared = false; // K3a + K2b ran (gnm_prepare_median) for this accumulation
     uint32_t* d_scratch = nullptr; // hot-site plan: counts, site->slot, slot->site, counter
     uint32_t partial_cap = 0;
@@ -315,21 +324,30 @@ gnm::DevLog slice_view(const gnm_ctx* c, const gnm_ctx::LogSlice& sl) {
     lg.counts = c->d_counts + sl.count_off;
     lg.warp_cap = sl.warp_cap;
     lg.regions = sl.regions;
+    lg.hosts = c->hosts ? c->d_lhost + sl.entry_off : nullptr;
+    lg.rates = c->hosts ? c->d_lrate + sl.entry_off : nullptr;
+    lg.ulo = c->hosts ? c->d_llo + sl.entry_off : nullptr;
+    lg.uhi = c->hosts ? c->d_lhi + sl.entry_off : nullptr;
     return lg;
 }
 
-// Grow a device buffer of u32 preserving its first `used` words (stream-ordered).
-void grow_u32(gnm_ctx* c, unsigned int** buf, size_t* cap, size_t used, size_t need, const char* what) {
+// Grow a device buffer preserving its first `used` elements (stream-ordered).
+template <typename T>
+void grow_buf(gnm_ctx* c, T** buf, size_t* cap, size_t used, size_t need, const char* what) {
     if (need <= *cap) return;
     const size_t ncap = std::max(need, *cap + *cap / 2);
-    unsigned int* nb = nullptr;
-    ck(cudaMallocAsync(reinterpret_cast<void**>(&nb), ncap * 4, c->stream), what);
+    T* nb = nullptr;
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&nb), ncap * sizeof(T), c->stream), what);
     if (*buf) {
-        if (used) ck(cudaMemcpyAsync(nb, *buf, used * 4, cudaMemcpyDeviceToDevice, c->stream), what);
+        if (used) ck(cudaMemcpyAsync(nb, *buf, used * sizeof(T), cudaMemcpyDeviceToDevice, c->stream), what);
         ck(cudaFreeAsync(*buf, c->stream), what);
     }
     *buf = nb;
     *cap = ncap;
+}
+
+void grow_u32(gnm_ctx* c, unsigned int** buf, size_t* cap, size_t used, size_t need, const char* what) {
+    grow_buf(c, buf, cap, used, need, what);
 }
 
 // This launch's slice of the per-flow log: one region of warp_cap entries per
@@ -350,6 +368,18 @@ gnm::DevLog reserve_log(gnm_ctx* c, const gnm::LaunchCfg& cfg, const gnm::DevBat
         grow_u32(c, &c->d_logb, &bcap, c->log_used, c->log_cap, "log buckets");
     }
     grow_u32(c, &c->d_counts, &c->counts_cap, c->counts_used, c->counts_used + sl.regions, "log counts");
+    if (c->hosts && c->lhost_cap < c->log_cap) {
+        const size_t used = c->log_used, want = c->log_cap;
+        size_t k = c->lhost_cap;
+        grow_buf(c, &c->d_lhost, &k, used, want, "log hosts");
+        k = c->lhost_cap;
+        grow_buf(c, &c->d_lrate, &k, used, want, "log rates");
+        k = c->lhost_cap;
+        grow_buf(c, &c->d_llo, &k, used, want, "log micro-bps");
+        k = c->lhost_cap;
+        grow_buf(c, &c->d_lhi, &k, used, want, "log micro-bps");
+        c->lhost_cap = k;
+    }
     c->log_used += need;
     c->counts_used += sl.regions;
     c->slices.push_back(sl);
@@ -364,7 +394,7 @@ void launch_k2_timed(gnm_ctx* c, const gnm::DevBatch& b, const gnm::DevParams& p
         ck(cudaEventRecord(pe.a, c->stream), "cudaEventRecord");
     }
     // K1: hot-site plan for this batch (skipped when no site can be hot).
-    const gnm::LaunchCfg cold = gnm::k2_config(c->device, b, c->table.n_words, false, c->occ);
+    const gnm::LaunchCfg cold = gnm::k2_config(c->device, b, c->table.n_words, false, c->occ, c->hosts);
     bool hot = false;
     if (c->hot_mode != GNM_HOT_OFF) {
         cudaError_t e;
@@ -372,7 +402,8 @@ void launch_k2_timed(gnm_ctx* c, const gnm::DevBatch& b, const gnm::DevParams& p
                             c->hot_mode == GNM_HOT_FORCE, c->stream, &c->kernel_launches, &e);
         ck(e, "hot-site plan");
     }
-    const gnm::LaunchCfg cfg = hot ? gnm::k2_config(c->device, b, c->table.n_words, true, c->occ) : cold;
+    const gnm::LaunchCfg cfg =
+        hot ? gnm::k2_config(c->device, b, c->table.n_words, true, c->occ, c->hosts) : cold;
     gnm::DevHot h{c->d_scratch + 2 * static_cast<size_t>(c->P.n_sites), hot ? gnm::kHotSlots : 0u};
     if (c->timing) {
         ck(cudaEventRecord(pe.b, c->stream), "cudaEventRecord");
@@ -569,6 +600,9 @@ int finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* r) {
     }
     const double thr = r->threshold_bps;
     const bool export_hist = r->histograms != nullptr;
+    gnm::free_hosts(c->hrows, c->stream);
+    if (c->hosts && c->log_used >= (1ull << 32))
+        return fail(GNM_ERR_CAPACITY, "per-host mode holds < 2^32 log entries per finalize");
     prepare_median(c);
     ck(gnm::launch_k3b(c->device, c->P, thr, c->d_out, 1, c->stream), "K3b launch");
     c->kernel_launches += 1;
@@ -593,6 +627,20 @@ int finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* r) {
         ck(cudaMemcpyAsync(r->histograms, dense, bytes, cudaMemcpyDeviceToHost, c->stream),
            "cudaMemcpyAsync(D2H hist)");
         ck(cudaFreeAsync(dense, c->stream), "cudaFreeAsync(hist export)");
+    }
+    if (c->hosts) {
+        // SiteResult::hosts: the per-host post-pass over the same log.
+        gnm::DevLog whole{};
+        whole.hosts = c->d_lhost;
+        whole.rates = c->d_lrate;
+        whole.ulo = c->d_llo;
+        whole.uhi = c->d_lhi;
+        std::vector<gnm::HostSlice> hs;
+        for (const auto& sl : c->slices) hs.push_back({slice_view(c, sl), sl.entry_off, sl.count_off});
+        ck(gnm::build_hosts(c->device, whole, hs.data(), static_cast<int>(hs.size()), c->d_counts,
+                            c->counts_used, c->hrows, c->stream),
+           "per-host post-pass");
+        c->kernel_launches += 7 + hs.size(); // own kernels; cub scan/sorts not counted
     }
     clear_log(c);
     ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
@@ -756,6 +804,12 @@ void gnm_ctx_destroy(gnm_ctx* c) {
     cudaFree(c->d_log);
     cudaFree(c->d_logb);
     cudaFree(c->d_counts);
+    cudaFree(c->d_lhost);
+    cudaFree(c->d_lrate);
+    cudaFree(c->d_llo);
+    cudaFree(c->d_lhi);
+    gnm::free_hosts(c->hrows, c->stream);
+    if (c->stream) cudaStreamSynchronize(c->stream);
     cudaFree(c->d_scratch);
     cudaFree(c->d_out);
     if (c->h_out) cudaFreeHost(c->h_out);
@@ -797,6 +851,40 @@ int gnm_ctx_set_hot_mode(gnm_ctx* c, int mode) {
     if (!c || mode < GNM_HOT_OFF || mode > GNM_HOT_FORCE) return fail(GNM_ERR_INVALID_ARGUMENT, "bad hot mode");
     c->hot_mode = mode;
     return GNM_OK;
+}
+
+int gnm_ctx_set_hosts(gnm_ctx* c, int enable) {
+    if (!c) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx");
+    if (c->accumulating) return fail(GNM_ERR_INVALID_ARGUMENT, "per-host mode changes only between accumulations");
+    c->hosts = enable != 0;
+    return GNM_OK;
+}
+
+uint64_t gnm_host_count(gnm_ctx* c) { return c ? c->hrows.n_rows : 0; }
+
+int gnm_host_results(gnm_ctx* c, gnm_host_stats* out, uint64_t capacity, uint32_t* histograms) {
+    if (!c) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx");
+    const uint64_t n = c->hrows.n_rows;
+    if (capacity < n || (n && !out))
+        return fail(GNM_ERR_CAPACITY, "host rows: capacity " + std::to_string(capacity) + " < " + std::to_string(n));
+    return guarded([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        if (n) ck(cudaMemcpyAsync(out, c->hrows.rows, n * sizeof(gnm_host_stats), cudaMemcpyDeviceToHost, c->stream),
+                  "cudaMemcpyAsync(D2H host rows)");
+        if (n && histograms) {
+            const size_t bytes = n * gnm::kBuckets * 4;
+            uint32_t* dense = nullptr;
+            ck(cudaMallocAsync(reinterpret_cast<void**>(&dense), bytes, c->stream), "cudaMallocAsync(host hist)");
+            ck(cudaMemsetAsync(dense, 0, bytes, c->stream), "cudaMemsetAsync(host hist)");
+            ck(gnm::hosts_histograms(c->device, c->hrows, dense, c->stream), "host histograms");
+            c->kernel_launches += 1;
+            ck(cudaMemcpyAsync(histograms, dense, bytes, cudaMemcpyDeviceToHost, c->stream),
+               "cudaMemcpyAsync(D2H host hist)");
+            ck(cudaFreeAsync(dense, c->stream), "cudaFreeAsync(host hist)");
+        }
+        ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+        return static_cast<int>(GNM_OK);
+    });
 }
 
 int gnm_ctx_enable_timing(gnm_ctx* c, int enable) {
@@ -872,6 +960,7 @@ int gnm_reset(gnm_ctx* c) {
             ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
         }
         clear_log(c);
+        gnm::free_hosts(c->hrows, c->stream);
         drain_pairs(c, c->k2_pairs);
         drain_pairs(c, c->plan_pairs);
         drain_pairs(c, c->k3_pairs);

@@ -1,0 +1,41 @@
+// hosts.cuh — per-host statistics post-pass (hosts.cu), SURVEY.md §8f next #1.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+
+namespace gnm {
+
+// One K2 launch's slice of the hosts-mode log (the DevLog K2 wrote) and where
+// it sits in the context's concatenated log and per-warp counts.
+struct HostSlice {
+    DevLog log;
+    size_t entry_off; // first entry of the slice in the whole log
+    size_t count_off; // first per-warp count of the slice
+};
+
+// Device results of one post-pass; owned by the caller's context, released
+// with free_hosts. `sorted` keeps every flow's (host row, bucket) key in
+// (row, bucket) order for the optional histogram export.
+struct HostRows {
+    gnm_host_stats* rows = nullptr;
+    uint64_t n_rows = 0;
+    void* sorted = nullptr; // u32 (row << 14 | bucket) or u64, per key64
+    bool key64 = false;
+    uint64_t n_flows = 0;
+};
+
+// Builds the per-host rows from the log: whole-log base pointers of the host
+// columns (L.hosts/rates/ulo/uhi relative to entry 0), the slices, and all
+// per-warp counts. Synchronises `s` twice (to size the tables).
+cudaError_t build_hosts(int device, const DevLog& whole, const HostSlice* slices, int n_slices,
+                        const unsigned int* counts, size_t n_counts, HostRows& out, cudaStream_t s);
+
+// Dense [n_rows][kBuckets] histograms of the rows (device buffer, zeroed by the caller).
+cudaError_t hosts_histograms(int device, const HostRows& h, uint32_t* dense, cudaStream_t s);
+
+void free_hosts(HostRows& h, cudaStream_t s);
+
+} // namespace gnm

@@ -279,7 +279,8 @@ constexpr uint32_t kSkip = 0xFFFFFFFFu;
 template <bool kSmem>
 __device__ __forceinline__ uint32_t stage_a(uint32_t src, uint32_t dst, uint32_t pkts, uint32_t oct,
                                             uint64_t dur, const DevParams& p,
-                                            const uint32_t* __restrict__ gt, Ctr& c, bool in = true) {
+                                            const uint32_t* __restrict__ gt, Ctr& c, uint32_t& host,
+                                            bool in = true) {
     const bool ack = static_cast<uint64_t>(oct) < p.ack_plus1 * pkts;
     const bool rej = pkts < p.min_packets1 || dur < static_cast<uint64_t>(p.min_duration1);
     const uint32_t ds = src >> 16, dd = dst >> 16;
@@ -297,6 +298,7 @@ __device__ __forceinline__ uint32_t stage_a(uint32_t src, uint32_t dst, uint32_t
     const uint32_t ip = hs ? src : dst;
     const uint32_t rank = rank0 + __popc(bits & ~(0xFFFFFFFFu << (d & 31u)));
     uint32_t code = (cand && (hs | hd)) ? (rank << 8 | ((ip >> 8) & 0xFFu)) : kSkip;
+    host = ip; // the matched endpoint (rate_engine.cpp:218-223): src unless only dst's /16 holds sites
 #ifdef GNM_K2_ABLATION
     if (p.ablation == 1) {
         if (cand) c.fwd += rank;
@@ -304,7 +306,9 @@ __device__ __forceinline__ uint32_t stage_a(uint32_t src, uint32_t dst, uint32_t
     }
 #endif
     if (cand && hs && hd) {
-        const uint32_t v = site_of_full<kSmem>(gt, src, dst);
+        const uint32_t vs = lookup<kSmem>(gt, src);
+        const uint32_t v = vs != kNone ? vs : lookup<kSmem>(gt, dst);
+        host = vs != kNone ? src : dst;
         if (v == kNone) ++c.unm;
         code = v == kNone ? kSkip : (kResolved | v);
     }
@@ -332,11 +336,22 @@ __device__ __forceinline__ uint32_t resolve(const uint32_t* __restrict__ gt, uin
 // memory too; min/max go to L2 only when the slot's cached bounds say they
 // can win. Cold sites: straight to L2 (RED).
 // Returns the site (kNone: Unmatched at /24) and the bucket.
+// K2 compile-time modes (kMode bits).
+constexpr int kModeWindow = 1; // FlowStore::snapshot window fused (DevParams::windowed)
+constexpr int kModeHosts = 2;  // hosts mode: log host, rate, micro-bps per Forward flow
+
+struct FlowOut {
+    uint32_t bucket = 0;
+    unsigned long long rate_bits = 0;
+    uint64_t lo = 0, hi = 0;
+};
+
 template <bool kSmem, bool kHot>
 __device__ __forceinline__ uint32_t accumulate(uint32_t code, uint32_t oct, uint64_t dur,
                                                const uint32_t* __restrict__ gt, const DevParams& p,
                                                const DevPartials& P, const HotSmem& h, Ctr& c,
-                                               uint32_t& bucket) {
+                                               FlowOut& fo) {
+    uint32_t& bucket = fo.bucket;
     bucket = 0;
     const uint32_t v = resolve<kSmem>(gt, code);
     if (v == kNone) {
@@ -363,6 +378,9 @@ __device__ __forceinline__ uint32_t accumulate(uint32_t code, uint32_t oct, uint
     ubps_of(oct, dur, rate, lo, hi);
     const unsigned long long rb = static_cast<unsigned long long>(__double_as_longlong(rate));
     bucket = bucket_of_ubps(lo, hi);
+    fo.rate_bits = rb;
+    fo.lo = lo;
+    fo.hi = hi;
     const uint32_t sb = bucket >> 6;
 #ifdef GNM_K2_ABLATION
     // Measurement builds only (tools/ablation.sh): 3 = no reductions at all,
@@ -428,66 +446,87 @@ __device__ __forceinline__ uint32_t accumulate(uint32_t code, uint32_t oct, uint
 // the warp's region of the launch's log.
 struct WarpQueue {
     uint4* q;
+    uint32_t* qh;       // hosts mode: the matched host IP per queued item
     uint32_t n;         // warp-uniform fill
     uint32_t pos;       // warp-uniform log entries written
     unsigned int* log;  // this warp's log region
     unsigned int* logb; // wide registries: bucket column of the region
+    size_t region_off;  // hosts mode: the region's offset into the host columns
 };
 
+template <bool kHosts>
 __device__ __forceinline__ void push(uint32_t code, uint32_t oct, uint64_t dur, WarpQueue& wq,
-                                     uint32_t lane) {
+                                     uint32_t lane, uint32_t host) {
     const bool f = code != kSkip;
     const unsigned m = __ballot_sync(0xFFFFFFFFu, f);
-    if (f)
-        wq.q[wq.n + __popc(m & ((1u << lane) - 1u))] =
-            make_uint4(code, oct, static_cast<uint32_t>(dur), static_cast<uint32_t>(dur >> 32));
+    if (f) {
+        const uint32_t i = wq.n + __popc(m & ((1u << lane) - 1u));
+        wq.q[i] = make_uint4(code, oct, static_cast<uint32_t>(dur), static_cast<uint32_t>(dur >> 32));
+        if constexpr (kHosts) wq.qh[i] = host;
+    }
     wq.n += __popc(m);
 }
 
 // The drained Forward flows' entries, compacted (Unmatched lanes write none);
 // every lane of the warp calls this.
-__device__ __forceinline__ void log_entry(WarpQueue& wq, uint32_t lane, uint32_t site, uint32_t bucket) {
+template <bool kHosts>
+__device__ __forceinline__ void log_entry(WarpQueue& wq, uint32_t lane, uint32_t site, const FlowOut& fo,
+                                          uint32_t host, const DevLog& L) {
     const bool v = site != kNone;
     const unsigned m = __ballot_sync(0xFFFFFFFFu, v);
     if (v) {
         const uint32_t i = wq.pos + __popc(m & ((1u << lane) - 1u));
         if (wq.logb) {
             __stcs(wq.log + i, site);
-            __stcs(wq.logb + i, bucket);
+            __stcs(wq.logb + i, fo.bucket);
         } else {
-            __stcs(wq.log + i, site << kLogSiteShift | bucket);
+            __stcs(wq.log + i, site << kLogSiteShift | fo.bucket);
+        }
+        if constexpr (kHosts) { // the flow's host, rate and exact micro-bps
+            const size_t j = wq.region_off + i;
+            __stcs(L.hosts + j, host);
+            __stcs(L.rates + j, fo.rate_bits);
+            __stcs(L.ulo + j, static_cast<unsigned long long>(fo.lo));
+            __stcs(L.uhi + j, static_cast<unsigned int>(fo.hi));
         }
     }
     wq.pos += __popc(m);
 }
 
-template <bool kSmem, bool kHot>
+template <bool kSmem, bool kHot, bool kHosts>
 __device__ __forceinline__ void drain_full(WarpQueue& wq, uint32_t lane,
                                            const uint32_t* __restrict__ gt, const DevParams& p,
-                                           const DevPartials& P, const HotSmem& h, Ctr& c) {
+                                           const DevPartials& P, const HotSmem& h, Ctr& c,
+                                           const DevLog& L) {
     while (wq.n >= 32) {
         __syncwarp();
-        const uint4 x = wq.q[wq.n - 32 + lane];
+        const uint32_t k = wq.n - 32 + lane;
+        const uint4 x = wq.q[k];
+        uint32_t host = 0;
+        if constexpr (kHosts) host = wq.qh[k];
         wq.n -= 32;
         __syncwarp();
-        uint32_t bucket;
+        FlowOut fo;
         const uint32_t site =
-            accumulate<kSmem, kHot>(x.x, x.y, static_cast<uint64_t>(x.w) << 32 | x.z, gt, p, P, h, c, bucket);
-        log_entry(wq, lane, site, bucket);
+            accumulate<kSmem, kHot>(x.x, x.y, static_cast<uint64_t>(x.w) << 32 | x.z, gt, p, P, h, c, fo);
+        log_entry<kHosts>(wq, lane, site, fo, host, L);
     }
 }
 
-template <bool kSmem, bool kHot>
+template <bool kSmem, bool kHot, bool kHosts>
 __device__ __forceinline__ void drain_rest(WarpQueue& wq, uint32_t lane,
                                            const uint32_t* __restrict__ gt, const DevParams& p,
-                                           const DevPartials& P, const HotSmem& h, Ctr& c) {
+                                           const DevPartials& P, const HotSmem& h, Ctr& c,
+                                           const DevLog& L) {
     __syncwarp();
-    uint32_t site = kNone, bucket = 0;
+    uint32_t site = kNone, host = 0;
+    FlowOut fo;
     if (lane < wq.n) {
         const uint4 x = wq.q[lane];
-        site = accumulate<kSmem, kHot>(x.x, x.y, static_cast<uint64_t>(x.w) << 32 | x.z, gt, p, P, h, c, bucket);
+        if constexpr (kHosts) host = wq.qh[lane];
+        site = accumulate<kSmem, kHot>(x.x, x.y, static_cast<uint64_t>(x.w) << 32 | x.z, gt, p, P, h, c, fo);
     }
-    log_entry(wq, lane, site, bucket);
+    log_entry<kHosts>(wq, lane, site, fo, host, L);
     wq.n = 0;
 }
 
@@ -595,12 +634,13 @@ __device__ __forceinline__ void load_record(const DevBatch& b, uint64_t i, uint3
 }
 
 // Records [first, last) in warp-strided 32-record rounds, scalar loads.
-template <int kLayout, bool kSmem, bool kHot, bool kWin>
+template <int kLayout, bool kSmem, bool kHot, int kMode>
 __device__ __forceinline__ void run_scalar(const DevBatch& b, uint64_t first, uint64_t last,
                                            uint64_t stride, uint32_t lane,
                                            const uint32_t* __restrict__ gt, const DevParams& p,
                                            const DevPartials& P, const HotSmem& h, Ctr& t,
-                                           WarpQueue& wq) {
+                                           WarpQueue& wq, const DevLog& L) {
+    constexpr bool kWin = kMode & kModeWindow, kHosts = kMode & kModeHosts;
     for (uint64_t base = first; base < last; base += stride) {
         const uint64_t i = base + lane;
         uint32_t src = 0, dst = 0, pkts = 0, oct = 0;
@@ -608,21 +648,22 @@ __device__ __forceinline__ void run_scalar(const DevBatch& b, uint64_t first, ui
         const bool ok = i < last;
         if (ok) load_record<kLayout>(b, i, src, dst, pkts, oct, dur, end);
         Ctr one;
-        const uint32_t code = stage_a<kSmem>(src, dst, pkts, oct, dur, p, gt, one, window_in<kWin>(end, p));
+        uint32_t host;
+        const uint32_t code = stage_a<kSmem>(src, dst, pkts, oct, dur, p, gt, one, host, window_in<kWin>(end, p));
         if (ok) {
             t.ack += one.ack;
             t.adm += one.adm;
             t.unm += one.unm;
         }
-        push(ok ? code : kSkip, oct, dur, wq, lane);
-        drain_full<kSmem, kHot>(wq, lane, gt, p, P, h, t);
+        push<kHosts>(ok ? code : kSkip, oct, dur, wq, lane, host);
+        drain_full<kSmem, kHot, kHosts>(wq, lane, gt, p, P, h, t, L);
     }
 }
 
 // ---- K2 ----------------------------------------------------------------------
 // Block prologue: registry table and hot slots into shared memory, the
 // warp's queue after them, the warp's log region.
-template <bool kSmem, bool kHot>
+template <bool kSmem, bool kHot, bool kHosts>
 __device__ __forceinline__ void k2_prologue(const uint32_t* __restrict__ gt, uint32_t table_words,
                                             const DevLog& L, HotSmem& h, WarpQueue& wq) {
     load_table<kSmem>(gt, table_words);
@@ -632,22 +673,25 @@ __device__ __forceinline__ void k2_prologue(const uint32_t* __restrict__ gt, uin
         hot_init(h);
     }
     const uint32_t warp = threadIdx.x >> 5;
-    wq.q = reinterpret_cast<uint4*>(g_smem + smem_words + (kHot ? kHotBytes / 4 : 0u)) + warp * kQueue;
+    uint4* queues = reinterpret_cast<uint4*>(g_smem + smem_words + (kHot ? kHotBytes / 4 : 0u));
+    wq.q = queues + warp * kQueue;
+    wq.qh = kHosts ? reinterpret_cast<uint32_t*>(queues + (blockDim.x >> 5) * kQueue) + warp * kQueue : nullptr;
     wq.n = 0;
     wq.pos = 0;
     const size_t region = static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp;
     wq.log = L.entries + region * L.warp_cap;
     wq.logb = L.buckets ? L.buckets + region * L.warp_cap : nullptr;
+    wq.region_off = region * L.warp_cap;
     __syncthreads();
 }
 
-template <bool kSmem, bool kHot>
+template <bool kSmem, bool kHot, bool kHosts>
 __device__ __forceinline__ void k2_epilogue(Ctr& t, WarpQueue& wq, uint32_t lane,
                                             const uint32_t* __restrict__ gt, const DevParams& p,
                                             const DevPartials& P, const HotSmem& h,
                                             const DevHot& hot, const DevLog& L) {
-    drain_full<kSmem, kHot>(wq, lane, gt, p, P, h, t);
-    drain_rest<kSmem, kHot>(wq, lane, gt, p, P, h, t);
+    drain_full<kSmem, kHot, kHosts>(wq, lane, gt, p, P, h, t, L);
+    drain_rest<kSmem, kHot, kHosts>(wq, lane, gt, p, P, h, t, L);
     if (lane == 0) L.counts[static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)] = wq.pos;
     flush_tallies(t, P.sums + static_cast<size_t>(P.n_sites) * 4);
     if constexpr (kHot) {
@@ -665,13 +709,14 @@ __device__ __forceinline__ void k2_epilogue(Ctr& t, WarpQueue& wq, uint32_t lane
 // one is classified. Every kEpochRounds rounds the CTA meets at a barrier
 // and normalizes the hot limbs (hot_normalize). The last CTA also takes the
 // < 64-record remainder through the scalar path.
-template <bool kSmem, bool kHot, bool kWin>
+template <bool kSmem, bool kHot, int kMode>
 __global__ void __launch_bounds__(kK2Block, 1) k2_soa(DevBatch b, const uint32_t* __restrict__ gt,
                                                     uint32_t table_words, DevParams p,
                                                     DevPartials P, DevHot hot, DevLog L) {
+    constexpr bool kWin = kMode & kModeWindow, kHosts = kMode & kModeHosts;
     HotSmem h{};
     WarpQueue wq;
-    k2_prologue<kSmem, kHot>(gt, table_words, L, h, wq);
+    k2_prologue<kSmem, kHot, kHosts>(gt, table_words, L, h, wq);
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warp = threadIdx.x >> 5;
     const DevSoA& c = b.soa;
@@ -714,11 +759,12 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_soa(DevBatch b, const uint32_t
         }
         if (tile < t_end) {
             const uint64_t dx = te.x - ts.x, dy = te.y - ts.y;
-            const uint32_t cx = stage_a<kSmem>(s.x, d.x, k.x, o.x, dx, p, gt, t, window_in<kWin>(te.x, p));
-            const uint32_t cy = stage_a<kSmem>(s.y, d.y, k.y, o.y, dy, p, gt, t, window_in<kWin>(te.y, p));
-            push(cx, o.x, dx, wq, lane);
-            push(cy, o.y, dy, wq, lane);
-            drain_full<kSmem, kHot>(wq, lane, gt, p, P, h, t);
+            uint32_t hx, hy;
+            const uint32_t cx = stage_a<kSmem>(s.x, d.x, k.x, o.x, dx, p, gt, t, hx, window_in<kWin>(te.x, p));
+            const uint32_t cy = stage_a<kSmem>(s.y, d.y, k.y, o.y, dy, p, gt, t, hy, window_in<kWin>(te.y, p));
+            push<kHosts>(cx, o.x, dx, wq, lane, hx);
+            push<kHosts>(cy, o.y, dy, wq, lane, hy);
+            drain_full<kSmem, kHot, kHosts>(wq, lane, gt, p, P, h, t, L);
         }
         s = ns, d = nd, k = nk, o = no, ts = nt, te = ne;
         tile = next;
@@ -731,26 +777,27 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_soa(DevBatch b, const uint32_t
         }
     }
     if (blockIdx.x == gridDim.x - 1 && warp == 0)
-        run_scalar<1, kSmem, kHot, kWin>(b, tiles << 6, c.n, 32, lane, gt, p, P, h, t, wq);
-    k2_epilogue<kSmem, kHot>(t, wq, lane, gt, p, P, h, hot, L);
+        run_scalar<1, kSmem, kHot, kMode>(b, tiles << 6, c.n, 32, lane, gt, p, P, h, t, wq, L);
+    k2_epilogue<kSmem, kHot, kHosts>(t, wq, lane, gt, p, P, h, hot, L);
 }
 
 // Other layouts: unaligned SoA (1), AoS 64-byte rows with vector (2) or
 // scalar (3) loads, FLOWARC1 archive entries read in place (4). CTA b owns records [b*n/G, (b+1)*n/G) (at most
 // kCtaRecords), one record per lane per round.
-template <int kLayout, bool kSmem, bool kHot, bool kWin>
+template <int kLayout, bool kSmem, bool kHot, int kMode>
 __global__ void __launch_bounds__(kK2Block, 1) k2_gen(DevBatch b, const uint32_t* __restrict__ gt,
                                                     uint32_t table_words, DevParams p,
                                                     DevPartials P, DevHot hot, DevLog L) {
+    constexpr bool kHosts = kMode & kModeHosts;
     HotSmem h{};
     WarpQueue wq;
-    k2_prologue<kSmem, kHot>(gt, table_words, L, h, wq);
+    k2_prologue<kSmem, kHot, kHosts>(gt, table_words, L, h, wq);
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t r0 = b.n * blockIdx.x / gridDim.x, r1 = b.n * (blockIdx.x + 1) / gridDim.x;
     Ctr t;
-    run_scalar<kLayout, kSmem, kHot, kWin>(b, r0 + (threadIdx.x >> 5) * 32, r1, kK2Block, lane, gt, p, P,
-                                           h, t, wq);
-    k2_epilogue<kSmem, kHot>(t, wq, lane, gt, p, P, h, hot, L);
+    run_scalar<kLayout, kSmem, kHot, kMode>(b, r0 + (threadIdx.x >> 5) * 32, r1, kK2Block, lane, gt, p, P,
+                                            h, t, wq, L);
+    k2_epilogue<kSmem, kHot, kHosts>(t, wq, lane, gt, p, P, h, hot, L);
 }
 
 // ---- K1: hot-site plan ------------------------------------------------------
@@ -1038,25 +1085,6 @@ __global__ void __launch_bounds__(512, 2) k2b_fine(DevPartials P, DevLog L) {
         if (hf[i]) red_add(P.fine + static_cast<size_t>(hsite[i / kFineW]) * kFineW + (i % kFineW), hf[i]);
 }
 
-// stats_from's avg (rate_engine.cpp:250; sum_bps rate_engine.hpp:62):
-// (double(u128 sum) / 1e6) / double(count), each step rounded to nearest
-// even like the host (libgcc __floatuntidf): a sum of >= 2^64 keeps its top
-// 64 bits with the shifted-out bits folded into a sticky LSB, which rounds
-// to 53 bits exactly as the 128-bit value would, then scales by 2^shift.
-__device__ __forceinline__ double avg_of(uint64_t lo, uint64_t hi, uint64_t count) {
-    double sum;
-    if (hi == 0) {
-        sum = __ull2double_rn(lo);
-    } else {
-        const int lz = __clzll(static_cast<long long>(hi));
-        const int sh = 64 - lz;
-        const uint64_t top = (hi << lz) | (lo >> sh);
-        const uint64_t sticky = (lo << lz) != 0 ? 1u : 0u;
-        sum = ldexp(__ull2double_rn(top | sticky), sh);
-    }
-    return __ddiv_rn(__ddiv_rn(sum, 1e6), __ull2double_rn(count));
-}
-
 // K3b, thread per site: count (coarse), the exact median bucket from the
 // fine counts, stats_from (rate_engine.cpp:242-253: median clamped into
 // [min, max]) and the flag (monitor.cpp:22); optionally resets the sums and
@@ -1100,8 +1128,7 @@ __global__ void __launch_bounds__(128) k3b_finalize(DevPartials P, double thresh
                 const double mn = __longlong_as_double(static_cast<long long>(P.mn[site]));
                 const double mx = __longlong_as_double(static_cast<long long>(P.mx[site]));
                 // median_bps (rate_engine.cpp:42-58), clamped (stats_from :251).
-                double med = k == kBuckets - 1 ? 100000000.0
-                                               : __dadd_rn(__dmul_rn(static_cast<double>(k), 10000.0), 5000.0);
+                double med = median_of_bucket(k);
                 med = med < mn ? mn : (mx < med ? mx : med);
                 const unsigned __int128 u = static_cast<unsigned __int128>(s[1]) +
                                             (static_cast<unsigned __int128>(s[2]) << 32) +
@@ -1173,13 +1200,13 @@ cudaError_t allow_smem(K kernel) {
                                 static_cast<int>(kSmemMax));
 }
 
-template <int L, bool kS, bool kH, bool kW>
+template <int L, bool kS, bool kH, int kW>
 constexpr auto k2_kernel() {
     if constexpr (L == 0) return k2_soa<kS, kH, kW>;
     else return k2_gen<L, kS, kH, kW>;
 }
 
-template <int L, bool kW>
+template <int L, int kW>
 cudaError_t allow_layout_w() {
     cudaError_t e;
     if ((e = allow_smem(k2_kernel<L, true, true, kW>()))) return e;
@@ -1191,17 +1218,19 @@ cudaError_t allow_layout_w() {
 template <int L>
 cudaError_t allow_layout() {
     cudaError_t e;
-    if ((e = allow_layout_w<L, false>())) return e;
-    return allow_layout_w<L, true>();
+    if ((e = allow_layout_w<L, 0>())) return e;
+    if ((e = allow_layout_w<L, kModeWindow>())) return e;
+    if ((e = allow_layout_w<L, kModeHosts>())) return e;
+    return allow_layout_w<L, kModeWindow | kModeHosts>();
 }
 
-template <int L, bool kS, bool kH, bool kW>
+template <int L, bool kS, bool kH, int kW>
 void launch_k2_t(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t, const DevParams& p,
                  const DevPartials& P, const DevHot& hot, const DevLog& log, cudaStream_t s) {
     k2_kernel<L, kS, kH, kW>()<<<cfg.grid, cfg.block, cfg.smem, s>>>(b, t.words, t.n_words, p, P, hot, log);
 }
 
-template <int L, bool kW>
+template <int L, int kW>
 void launch_k2_w(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t, const DevParams& p,
                  const DevPartials& P, const DevHot& hot, const DevLog& log, cudaStream_t s) {
     const bool hh = hot.n_slots > 0;
@@ -1217,8 +1246,13 @@ void launch_k2_w(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t, con
 template <int L>
 void launch_k2_l(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t, const DevParams& p,
                  const DevPartials& P, const DevHot& hot, const DevLog& log, cudaStream_t s) {
-    if (p.windowed) launch_k2_w<L, true>(cfg, b, t, p, P, hot, log, s);
-    else launch_k2_w<L, false>(cfg, b, t, p, P, hot, log, s);
+    // Fused snapshot window and hosts-mode logging are compile-time modes.
+    switch ((p.windowed ? kModeWindow : 0) | (log.hosts ? kModeHosts : 0)) {
+    case 0: launch_k2_w<L, 0>(cfg, b, t, p, P, hot, log, s); break;
+    case kModeWindow: launch_k2_w<L, kModeWindow>(cfg, b, t, p, P, hot, log, s); break;
+    case kModeHosts: launch_k2_w<L, kModeHosts>(cfg, b, t, p, P, hot, log, s); break;
+    default: launch_k2_w<L, kModeWindow | kModeHosts>(cfg, b, t, p, P, hot, log, s); break;
+    }
 }
 
 size_t table_smem_bytes(uint32_t table_words) { return static_cast<size_t>(table_words) * 4; }
@@ -1247,13 +1281,15 @@ cudaError_t init_kernel_attributes() {
     return allow_smem(k_classify<true>);
 }
 
-LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool hot, int* occ_cache) {
+LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool hot, int* occ_cache,
+                    bool hosts) {
     (void)occ_cache;
     LaunchCfg c;
     const size_t tbytes = table_smem_bytes(table_words);
+    const size_t qbytes = kQueueBytes + (hosts ? kWarps * kQueue * 4 : 0);
     c.block = kK2Block;
-    c.table_in_smem = tbytes <= kSmemTableMax;
-    c.smem = (c.table_in_smem ? tbytes : 0) + (hot ? kHotBytes : 0) + kQueueBytes;
+    c.table_in_smem = tbytes + qbytes <= kSmemTableMax + kQueueBytes;
+    c.smem = (c.table_in_smem ? tbytes : 0) + (hot ? kHotBytes : 0) + qbytes;
     const uint64_t sms = static_cast<uint64_t>(sm_count(device));
     // At least 16 records per thread so the per-CTA table load amortises.
     const uint64_t per_block = static_cast<uint64_t>(c.block) * 16;

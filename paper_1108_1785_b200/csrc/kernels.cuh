@@ -31,6 +31,33 @@ constexpr uint64_t kMaxInitBits = 0;                     // +0.0: empty max (rat
 constexpr uint32_t kHotSlots = 2047;  // block-private accumulators for hot sites (11 slot bits)
 constexpr uint32_t kHotStride = 2048; // kHotSlots + 1 (slot 0 = cold)
 
+#ifdef __CUDACC__
+// stats_from's avg (rate_engine.cpp:250; sum_bps rate_engine.hpp:62):
+// (double(u128 sum) / 1e6) / double(count), each step rounded to nearest
+// even like the host (libgcc __floatuntidf): a sum of >= 2^64 keeps its top
+// 64 bits with the shifted-out bits folded into a sticky LSB, which rounds
+// to 53 bits exactly as the 128-bit value would, then scales by 2^shift.
+__device__ __forceinline__ double avg_of(uint64_t lo, uint64_t hi, uint64_t count) {
+    double sum;
+    if (hi == 0) {
+        sum = __ull2double_rn(lo);
+    } else {
+        const int lz = __clzll(static_cast<long long>(hi));
+        const int sh = 64 - lz;
+        const uint64_t top = (hi << lz) | (lo >> sh);
+        const uint64_t sticky = (lo << lz) != 0 ? 1u : 0u;
+        sum = ldexp(__ull2double_rn(top | sticky), sh);
+    }
+    return __ddiv_rn(__ddiv_rn(sum, 1e6), __ull2double_rn(count));
+}
+
+// median_bps (rate_engine.cpp:42-58) of lower-median bucket k, before the
+// clamp into [min, max] (stats_from :251).
+__device__ __forceinline__ double median_of_bucket(uint32_t k) {
+    return k == kBuckets - 1 ? 100000000.0 : __dadd_rn(__dmul_rn(static_cast<double>(k), 10000.0), 5000.0);
+}
+#endif
+
 struct DevParams {
     uint64_t ack_plus1;       // ack_avg_size_max + 1, u64 (rate_engine.cpp:78)
     uint32_t min_packets;
@@ -68,6 +95,13 @@ struct DevLog {
     unsigned int* counts;
     uint32_t warp_cap;
     uint32_t regions;
+    // Hosts mode (gnm_ctx_set_hosts), else null: per entry the matched host
+    // IP, the f64 rate bits and the exact micro-bps (lo, hi); indexed like
+    // `entries` from this slice's base.
+    unsigned int* hosts;
+    unsigned long long* rates;
+    unsigned long long* ulo;
+    unsigned int* uhi;
 };
 
 // Per-call hot-site plan: slot -> site (slots 1..n_slots), 0 slots = off.
@@ -115,7 +149,8 @@ cudaError_t init_kernel_attributes();
 
 // Occupancy-derived launch configuration for K2 over n records.
 // occ_cache[hot] memoises blocks/SM (0 = unknown) for this table size.
-LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool hot, int* occ_cache);
+LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool hot, int* occ_cache,
+                    bool hosts = false);
 
 // K1 (optional, skewed batches): sample the batch, pick the hot sites and
 // write their slots into the table words. Returns false when the batch is

@@ -366,12 +366,21 @@ class RateStats:
 
 
 @dataclass
+class HostResult:
+    """rate_engine.hpp:84-91: one host's RateStats (and histogram when requested)."""
+    stats: RateStats
+    rate_ubps_sum: int = 0
+    histogram: Optional[np.ndarray] = None
+
+
+@dataclass
 class SiteResult:
     stats: RateStats
     octets: int = 0                 # north-star byte sum (oracle extension)
     rate_ubps_sum: int = 0          # exact u128 sum of per-flow micro-bps
     below_threshold: bool = False   # K3 flag: median < threshold
     histogram: Optional[np.ndarray] = None  # 10001 u32 when requested
+    hosts: dict = field(default_factory=dict)  # host IP -> HostResult (Engine.set_hosts)
 
 
 @dataclass
@@ -401,6 +410,8 @@ class AnalysisResult:
         self.histograms = histograms
         self.threshold_bps = threshold_bps
         self._sites = sites
+        self.host_table = None       # HOST_STATS_DTYPE rows in (site, host) order (hosts mode)
+        self.host_histograms = None  # [rows, 10001] u32 when requested
 
     @property
     def sites(self) -> dict:
@@ -416,6 +427,14 @@ class AnalysisResult:
                                         flow_count=cnt),
                         octets=octs, rate_ubps_sum=hi << 64 | lo, below_threshold=bool(below),
                         histogram=None if self.histograms is None else self.histograms[s])
+            if self.host_table is not None:
+                for i, row in enumerate(self.host_table.tolist()):
+                    (site, host, cnt, lo, hi, mn, mx, avg, med) = row
+                    self._sites[site].hosts[host] = HostResult(
+                        stats=RateStats(max_bps=mx, min_bps=mn, avg_bps=avg, median_bps=med,
+                                        flow_count=cnt),
+                        rate_ubps_sum=hi << 64 | lo,
+                        histogram=None if self.host_histograms is None else self.host_histograms[i])
         return self._sites
 
     @staticmethod
@@ -460,6 +479,7 @@ class Engine:
         _check(lib.gnm_ctx_create(device, C.byref(h)))
         self._h = h
         self.device = device
+        self._hosts = False
 
     def close(self):
         if getattr(self, "_h", None):
@@ -495,6 +515,25 @@ class Engine:
         """"auto" (default), "off" or "force" block-private hot-site accumulation."""
         m = {"off": _lib.HOT_OFF, "auto": _lib.HOT_AUTO, "force": _lib.HOT_FORCE}[mode]
         _check(lib.gnm_ctx_set_hot_mode(self._h, m))
+
+    def set_hosts(self, on: bool = True) -> None:
+        """Per-host mode (SiteResult::hosts, rate_engine.cpp:272-289): every
+        later result carries ``host_table`` and ``sites[s].hosts``. Only
+        between accumulations."""
+        _check(lib.gnm_ctx_set_hosts(self._h, 1 if on else 0))
+        self._hosts = bool(on)
+
+    def _attach_hosts(self, res: AnalysisResult, histograms: bool) -> AnalysisResult:
+        if not getattr(self, "_hosts", False):
+            return res
+        n = lib.gnm_host_count(self._h)
+        rows = np.empty(max(n, 1), _lib.HOST_STATS_DTYPE)
+        hist = np.empty((max(n, 1), BUCKET_COUNT), np.uint32) if histograms else None
+        _check(lib.gnm_host_results(self._h, rows.ctypes.data, len(rows),
+                                    hist.ctypes.data if hist is not None else None))
+        res.host_table = rows[:n]
+        res.host_histograms = None if hist is None else hist[:n]
+        return res
 
     def enable_timing(self, on: bool = True) -> None:
         _check(lib.gnm_ctx_enable_timing(self._h, 1 if on else 0))
@@ -552,7 +591,7 @@ class Engine:
         r, table, hist, n = self._result(catalog, window_start_ms, window_end_ms, threshold_bps,
                                          histograms)
         _check(lib.gnm_finalize(self._h, catalog.handle, C.byref(r)))
-        return _build_result(r, table[:n], None if hist is None else hist[:n])
+        return self._attach_hosts(_build_result(r, table[:n], None if hist is None else hist[:n]), histograms)
 
     def reset(self) -> None:
         _check(lib.gnm_reset(self._h))
@@ -572,7 +611,7 @@ class Engine:
             _check(lib.gnm_analyze_aos(self._h, catalog.handle, C.byref(p), C.byref(b), C.byref(r)))
         else:
             _check(lib.gnm_analyze(self._h, catalog.handle, C.byref(p), C.byref(b), C.byref(r)))
-        return _build_result(r, table[:n], None if hist is None else hist[:n])
+        return self._attach_hosts(_build_result(r, table[:n], None if hist is None else hist[:n]), histograms)
 
     def aggregate_window(self, view, catalog: SiteCatalog, window_start_ms: int, window_end_ms: int,
                          params: Optional[FilterParams] = None,
@@ -589,7 +628,7 @@ class Engine:
         r, table, hist, n = self._result(catalog, window_start_ms, window_end_ms, threshold_bps,
                                          histograms)
         _check(lib.gnm_analyze_window(self._h, catalog.handle, C.byref(p), C.byref(b), C.byref(r)))
-        return _build_result(r, table[:n], None if hist is None else hist[:n])
+        return self._attach_hosts(_build_result(r, table[:n], None if hist is None else hist[:n]), histograms)
 
     def decode_netflow(self, datagrams, offsets, out_device: bool = False):
         """Batched Collector::ingest_datagram without the store
@@ -659,7 +698,7 @@ class Engine:
         r, table, hist, ns = self._result(catalog, window_start_ms, window_end_ms, threshold_bps,
                                           histograms)
         _check(lib.gnm_analyze_archive(self._h, catalog.handle, C.byref(p), ptr, n, mem, C.byref(r)))
-        return _build_result(r, table[:ns], None if hist is None else hist[:ns])
+        return self._attach_hosts(_build_result(r, table[:ns], None if hist is None else hist[:ns]), histograms)
 
     def partials(self, catalog: SiteCatalog) -> dict:
         """Device pointers of the accumulation (gnm_get_partials) for a

@@ -206,6 +206,41 @@ def netflow_fixture():
                         records=np.frombuffer(b"".join(rows), np.uint8))
 
 
+def hosts_fixture():
+    """SiteResult::hosts of the unmodified reference (rate_engine.cpp:272-289)
+    on the inputs of every analysis fixture: per (site, host) row, in the
+    std::map's (site, host) order, count, min, max, avg, median, sum_bps and
+    the host's histogram (sparse: row, bucket, count)."""
+    import golden_io as G
+    out = {}
+    for name in G.ANALYSIS_SETS:
+        z = G.load(name)
+        params = G.params(z)
+        cat = R.catalog(G.sites(z))
+        res = R.aggregate(R.records(G.cols(z)), cat, params)
+        d = R.result(res, hist=True, hosts=True)
+        rows, stats, hr, hb, hc = [], [], [], [], []
+        for s in sorted(d["sites"]):
+            for ip in sorted(d["sites"][s]["hosts"]):
+                h = d["sites"][s]["hosts"][ip]
+                nz = np.nonzero(h["hist"])[0]
+                hr += [len(rows)] * len(nz)
+                hb += nz.tolist()
+                hc += h["hist"][nz].tolist()
+                rows.append((s, ip, h["count"]))
+                stats.append((h["min"], h["max"], h["avg"], h["median"], h["sum_bps"]))
+        r = np.array(rows, np.uint64).reshape(-1, 3)
+        out[f"{name}_site"] = r[:, 0].astype(np.uint32)
+        out[f"{name}_host"] = r[:, 1].astype(np.uint32)
+        out[f"{name}_count"] = r[:, 2]
+        out[f"{name}_stats"] = np.array(stats).reshape(-1, 5)
+        out[f"{name}_hist_row"] = np.array(hr, np.uint32)
+        out[f"{name}_hist_bucket"] = np.array(hb, np.uint32)
+        out[f"{name}_hist_count"] = np.array(hc, np.uint32)
+        print(f"hosts {name}: {len(rows)} (site, host) rows")
+    np.savez_compressed(os.path.join(HERE, "hosts.npz"), **out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:  # regenerate only the named fixtures
         for name in sys.argv[1:]:
@@ -225,3 +260,4 @@ if __name__ == "__main__":
     scalar_fixture()
     warning_fixture()
     netflow_fixture()
+    hosts_fixture()

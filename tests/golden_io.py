@@ -52,3 +52,38 @@ def assert_acc_equal(got, want, check_hist=True):
     np.testing.assert_array_equal(np.asarray(got["tallies"], np.uint64), want["tallies"])
     if check_hist:
         np.testing.assert_array_equal(got["hist"], want["hist"])
+
+
+def hosts_expected(name):
+    """The reference's SiteResult::hosts rows for an analysis fixture
+    (hosts.npz, make_golden.py hosts_fixture), in (site, host) order."""
+    z = np.load(os.path.join(GOLDEN, "hosts.npz"))
+    st = z[f"{name}_stats"]
+    n = len(st)
+    rows, bks, cnts = z[f"{name}_hist_row"], z[f"{name}_hist_bucket"], z[f"{name}_hist_count"]
+    return {"site": z[f"{name}_site"], "host": z[f"{name}_host"], "count": z[f"{name}_count"],
+            "min": st[:, 0], "max": st[:, 1], "avg": st[:, 2], "median": st[:, 3], "sum_bps": st[:, 4],
+            "hist_row": rows, "hist_bucket": bks, "hist_count": cnts, "n": n}
+
+
+def dense_host_hist(h):
+    d = np.zeros((len(h["count"]), 10001), np.uint32)
+    d[h["hist_row"], h["hist_bucket"]] = h["hist_count"]
+    return d
+
+
+def assert_hosts_equal(got, want, check_hist=True):
+    """Bit-exact comparison of per-host rows (dict layout of Oracle.host_stats)."""
+    for k in ("site", "host", "count"):
+        np.testing.assert_array_equal(np.asarray(got[k]).astype(np.uint64),
+                                      np.asarray(want[k]).astype(np.uint64), err_msg=k)
+    for k in ("min", "max", "avg", "median"):
+        np.testing.assert_array_equal(np.asarray(got[k], np.float64).view(np.uint64),
+                                      np.asarray(want[k], np.float64).view(np.uint64), err_msg=k)
+    if "sum_bps" in want and "ubps_lo" in got:
+        sb = [float(int(h) << 64 | int(lo)) / 1e6 for lo, h in zip(got["ubps_lo"], got["ubps_hi"])]
+        np.testing.assert_array_equal(np.array(sb).view(np.uint64),
+                                      np.asarray(want["sum_bps"]).view(np.uint64), err_msg="sum_bps")
+    if check_hist:
+        np.testing.assert_array_equal(got["hist"] if "hist" in got else dense_host_hist(got),
+                                      dense_host_hist(want))

@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version_and_defaults():
-    assert _lib.lib.gnm_abi_version() == 2
+    assert _lib.lib.gnm_abi_version() == 3
     p = _lib.gnm_filter_params()
     _lib.lib.gnm_filter_params_default(C.byref(p))
     assert (p.ack_avg_size_max, p.min_packets, p.min_duration_ms, p.workers) == (96, 20, 100, 1)
