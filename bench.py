@@ -54,6 +54,8 @@ def parse_args():
     ap.add_argument("--cpu-sample", type=int, default=2_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--hot-mode", default="auto", choices=["auto", "off", "force"])
+    ap.add_argument("--hosts", action="store_true",
+                    help="per-host mode: every step also builds SiteResult::hosts (N=1 only)")
     return ap.parse_args()
 
 
@@ -348,6 +350,10 @@ def main():
 
     eng = Engine(local)
     eng.set_hot_mode(args.hot_mode)
+    if args.hosts:
+        if world > 1:
+            raise SystemExit("--hosts: per-host rows are per context (N=1 only)")
+        eng.set_hosts(True)
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=f"cuda:{local}")
 
     def step(batch):
@@ -411,6 +417,9 @@ def main():
     traffic = load_traffic(args.workload)
     n_sites = cat.site_count()
     d2h = (n_sites + 1) * 72
+    if args.hosts:
+        d2h += len(res.host_table) * 64
+        assert np.array_equal(res.host_table, res_e2e.host_table), "device and host runs differ (hosts)"
 
     # Correctness guard on the measured runs: every record was classified.
     assert res.tallies.total() == total and res_e2e.tallies.total() == total, "tally mismatch"
@@ -423,7 +432,9 @@ def main():
         "dtype": "u32/u64 int + f64", "data": "synthetic",
         "config": {"workload": f"{w.name}: {n} records/GPU, {n_sites} /24 sites, Zipf s={w.zipf_s}, "
                                f"8 hosts/site, 40% forward",
-                   "records_per_gpu": n, "sites": n_sites, "parallelism": f"index shards x{world}",
+                   "records_per_gpu": n, "sites": n_sites,
+                   "hosts": (f"per-host rows built every step ({len(res.host_table)} rows)" if args.hosts
+                             else "site level only (gnm_ctx_set_hosts off)"), "parallelism": f"index shards x{world}",
                    "l2": "inputs 3.2 GB/GPU > 126 MB L2; no flush needed" if n >= 10_000_000
                          else "inputs may fit L2"},
         "e2e": {"value": e2e_value, "unit": "records/s",

@@ -630,17 +630,13 @@ int finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* r) {
     }
     if (c->hosts) {
         // SiteResult::hosts: the per-host post-pass over the same log.
-        gnm::DevLog whole{};
-        whole.hosts = c->d_lhost;
-        whole.rates = c->d_lrate;
-        whole.ulo = c->d_llo;
-        whole.uhi = c->d_lhi;
         std::vector<gnm::HostSlice> hs;
         for (const auto& sl : c->slices) hs.push_back({slice_view(c, sl), sl.entry_off, sl.count_off});
-        ck(gnm::build_hosts(c->device, whole, hs.data(), static_cast<int>(hs.size()), c->d_counts,
-                            c->counts_used, c->hrows, c->stream),
+        const uint64_t max_keys = 256ull * reg->r.entries().size(); // hosts lie in registered /24s
+        ck(gnm::build_hosts(c->device, hs.data(), static_cast<int>(hs.size()), c->d_counts,
+                            c->counts_used, max_keys, c->hrows, c->stream),
            "per-host post-pass");
-        c->kernel_launches += 7 + hs.size(); // own kernels; cub scan/sorts not counted
+        c->kernel_launches += 6 + hs.size(); // own kernels; cub scan/sorts not counted
     }
     clear_log(c);
     ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
@@ -770,6 +766,13 @@ int gnm_ctx_create(int device, gnm_ctx** out) {
             c->device = device;
             ck(cudaSetDevice(device), "cudaSetDevice");
             ck(gnm::init_kernel_attributes(), "kernel attributes");
+            // Keep stream-ordered allocations (log growth, the per-host
+            // post-pass scratch) in the device pool between calls instead of
+            // returning them to the driver at every synchronisation.
+            cudaMemPool_t pool;
+            ck(cudaDeviceGetDefaultMemPool(&pool, device), "cudaDeviceGetDefaultMemPool");
+            uint64_t keep = UINT64_MAX;
+            ck(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep), "cudaMemPoolSetAttribute");
             ck(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
             ck(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
             c->stream = c->own_stream;

@@ -10,14 +10,16 @@
 // bits and exact micro-bps; at finalize this post-pass turns the log into the
 // reference's rows without any per-host histogram storage:
 //   H0  flat offsets: exclusive scan of the per-warp log counts;
-//   H1  insert every (site, host) key into an open-addressing table and
-//       flatten the log (slot, bucket, log position per flow);
+//   H1  insert every (site, host) key into an open-addressing table (at most
+//       256 keys per registry /24 entry, so the table is sized by
+//       min(flows, 256 * entries)); accumulate the u128 micro-bps sum, min and
+//       max per slot (warp-aggregated over lanes that share a slot, one
+//       atomic per slot per warp); flatten (slot, bucket) per flow;
 //   H2  collect the distinct keys, radix-sort them: row = rank in (site,
 //       host) order, i.e. the std::map's iteration order;
-//   H3  per flow key = row << 14 | bucket, radix-sorted with the log position
-//       as payload, so every row's flows form one run in bucket order;
-//   H4  one pass over the sorted runs: count, u128 micro-bps sum, min, max
-//       (segmented warp scans, one atomic per run per warp) and run starts;
+//   H3  per flow key = row << 14 | bucket, radix-sorted (keys only), so
+//       every row's flows form one run in bucket order;
+//   H4  run starts; count = run length;
 //   H5  per row: the lower median is the run's element (count + 1) / 2 - 1
 //       (RateHistogram::median_bps, rate_engine.cpp:42-58), clamped, avg as
 //       the host rounds it (stats_from, :242-253).
@@ -63,29 +65,161 @@ __device__ __forceinline__ uint32_t insert_key(unsigned long long* keys, uint32_
     }
 }
 
-// H1, warp per log region of one slice.
-__global__ void __launch_bounds__(256) h_insert(DevLog L, const unsigned int* __restrict__ counts,
-                                                const uint32_t* __restrict__ off, uint32_t entry_off,
-                                                unsigned long long* keys, uint32_t mask, int shift,
-                                                uint32_t* __restrict__ slot_of,
-                                                uint32_t* __restrict__ bk,
-                                                uint32_t* __restrict__ logpos) {
+// Sum of v over the lanes of `m` (the lanes sharing this lane's slot), a
+// tree over the group's ranks with full-warp shuffles; valid in the group's
+// lowest lane.
+template <typename T, typename Op>
+__device__ __forceinline__ T group_reduce(unsigned m, uint32_t lane, T v, Op op) {
+    const uint32_t rank = __popc(m & ((1u << lane) - 1u));
+#pragma unroll
+    for (uint32_t d = 1; d < 32; d <<= 1) {
+        const uint32_t partner = __fns(m, lane, static_cast<int>(d) + 1);
+        const T o = __shfl_sync(0xFFFFFFFFu, v, partner == 0xFFFFFFFFu ? lane : partner);
+        if (partner != 0xFFFFFFFFu && (rank & (2 * d - 1)) == 0) v = op(v, o);
+    }
+    return v;
+}
+
+// H1, warp per log region of one slice. acc[slot] = {limb0, limb1, limb2,
+// ~min bits, max bits} (zero-initialised: the min is kept complemented).
+// Heavy hosts would serialise on their slot's L2 atomics, so each warp first
+// folds its flows into a private shared-memory table of kAggSlots entries
+// (an entry belongs to the first slot hashed to it; a flow whose entry is
+// taken goes to L2 directly) and flushes it once at the end. Within a warp
+// one leader lane per slot updates the entry, so the updates need no atomics.
+constexpr uint32_t kInsBlock = 256;
+constexpr uint32_t kInsWarps = kInsBlock / 32;
+constexpr uint32_t kAggSlots = 128;
+constexpr size_t kInsSmem = kInsWarps * kAggSlots * (4 + 5 * 8); // 44 KB
+
+__device__ __forceinline__ void red_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_max_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// One slot's partial into the L2 accumulators: fire-and-forget reductions
+// (no read round trip on the issuing warp's critical path).
+__device__ __forceinline__ void acc_flush(unsigned long long* a, unsigned long long l0, unsigned long long l1,
+                                          unsigned long long l2, unsigned long long nmn, unsigned long long mx) {
+    red_u64(a + 0, l0);
+    red_u64(a + 1, l1);
+    if (l2) red_u64(a + 2, l2);
+    red_max_u64(a + 3, nmn);
+    red_max_u64(a + 4, mx);
+}
+
+// One flow's contribution, folded into the warp's private table (leader
+// lanes only: one per distinct slot among the warp's 32 flows) or L2.
+__device__ __forceinline__ void fold(uint32_t slot, bool in, unsigned long long lo, unsigned long long hi,
+                                     unsigned long long rate, uint32_t lane, uint32_t* skey,
+                                     unsigned long long* sacc, unsigned long long* acc) {
+    const unsigned m = __match_any_sync(0xFFFFFFFFu, slot);
+    unsigned long long l0 = lo & 0xFFFFFFFFull, l1 = lo >> 32, l2 = hi, mn = rate, mx = rate;
+    if (__any_sync(0xFFFFFFFFu, in && (m & ~(1u << lane)) != 0)) { // some slot repeats in this warp
+        l0 = group_reduce(m, lane, l0, [](auto a, auto b) { return a + b; });
+        l1 = group_reduce(m, lane, l1, [](auto a, auto b) { return a + b; });
+        l2 = group_reduce(m, lane, l2, [](auto a, auto b) { return a + b; });
+        mn = group_reduce(m, lane, mn, [](auto a, auto b) { return a < b ? a : b; });
+        mx = group_reduce(m, lane, mx, [](auto a, auto b) { return a < b ? b : a; });
+    }
+    if (in && lane == static_cast<uint32_t>(__ffs(m) - 1)) {
+        const uint32_t h = (slot * 2654435761u) >> (32 - 7);
+        uint32_t cur = skey[h];
+        if (cur == 0xFFFFFFFFu) cur = atomicCAS(skey + h, 0xFFFFFFFFu, slot); // leaders of other slots race
+        if (cur == 0xFFFFFFFFu || cur == slot) {
+            unsigned long long* e = sacc + h * 5;
+            e[0] += l0;
+            e[1] += l1;
+            e[2] += l2;
+            e[3] = e[3] > ~mn ? e[3] : ~mn;
+            e[4] = e[4] > mx ? e[4] : mx;
+        } else {
+            acc_flush(acc + static_cast<size_t>(slot) * 5, l0, l1, l2, ~mn, mx);
+        }
+    }
+    __syncwarp();
+}
+
+// Work item = (region, chunk of kLogChunk entries); each lane takes 4
+// consecutive entries per step (LDG.128 on the u32 columns), and the four
+// table probes are issued before any is resolved.
+constexpr uint32_t kInsChunk = 2048;
+
+__global__ void __launch_bounds__(kInsBlock, 3) h_insert(DevLog L, const unsigned int* __restrict__ counts,
+                                                         const uint32_t* __restrict__ off,
+                                                         unsigned long long* keys, uint32_t mask, int shift,
+                                                         unsigned long long* __restrict__ acc,
+                                                         uint32_t* __restrict__ slot_of,
+                                                         uint32_t* __restrict__ bk) {
+    extern __shared__ __align__(16) unsigned char h_smem[];
     const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warp = threadIdx.x >> 5;
+    unsigned long long* sacc = reinterpret_cast<unsigned long long*>(h_smem) + warp * kAggSlots * 5;
+    uint32_t* skey = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned long long*>(h_smem) +
+                                                 kInsWarps * kAggSlots * 5) + warp * kAggSlots;
+    for (uint32_t i = lane; i < kAggSlots; i += 32) {
+        skey[i] = 0xFFFFFFFFu;
+#pragma unroll
+        for (int f = 0; f < 5; ++f) sacc[i * 5 + f] = 0;
+    }
+    __syncwarp();
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < L.regions; r += nwarps) {
-        const uint32_t n = counts[r];
+    const uint32_t chunks = (L.warp_cap + kInsChunk - 1) / kInsChunk;
+    const uint32_t items = L.regions * chunks;
+    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < items; w += nwarps) {
+        const uint32_t r = w / chunks;
+        const uint32_t c0 = (w % chunks) * kInsChunk;
+        const uint32_t n = min(counts[r], c0 + kInsChunk);
         const uint32_t base = off[r];
         const size_t rb = static_cast<size_t>(r) * L.warp_cap;
-        for (uint32_t i = lane; i < n; i += 32) {
+        for (uint32_t i0 = c0; i0 < n; i0 += 128) { // warp-uniform trip count
+            const uint32_t i = i0 + lane * 4;
             const size_t pos = rb + i;
-            const uint32_t x = L.entries[pos];
-            const uint32_t site = L.buckets ? x : x >> kLogSiteShift;
-            const uint32_t b = L.buckets ? L.buckets[pos] : x & kBucketMask;
-            const unsigned long long key = static_cast<unsigned long long>(site) << 32 | L.hosts[pos];
-            slot_of[base + i] = insert_key(keys, mask, shift, key);
-            bk[base + i] = b;
-            logpos[base + i] = entry_off + static_cast<uint32_t>(pos);
+            uint4 x = make_uint4(0, 0, 0, 0), hst = x, bb = x, uh = x;
+            ulonglong2 lo01{}, lo23{}, rt01{}, rt23{};
+            if (i < n) {
+                x = __ldcs(reinterpret_cast<const uint4*>(L.entries + pos));
+                hst = __ldcs(reinterpret_cast<const uint4*>(L.hosts + pos));
+                if (L.buckets) bb = __ldcs(reinterpret_cast<const uint4*>(L.buckets + pos));
+                uh = __ldcs(reinterpret_cast<const uint4*>(L.uhi + pos));
+                lo01 = __ldcs(reinterpret_cast<const ulonglong2*>(L.ulo + pos));
+                lo23 = __ldcs(reinterpret_cast<const ulonglong2*>(L.ulo + pos + 2));
+                rt01 = __ldcs(reinterpret_cast<const ulonglong2*>(L.rates + pos));
+                rt23 = __ldcs(reinterpret_cast<const ulonglong2*>(L.rates + pos + 2));
+            }
+            const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, hs[4] = {hst.x, hst.y, hst.z, hst.w};
+            const uint32_t bs[4] = {bb.x, bb.y, bb.z, bb.w}, us[4] = {uh.x, uh.y, uh.z, uh.w};
+            const unsigned long long los[4] = {lo01.x, lo01.y, lo23.x, lo23.y};
+            const unsigned long long rts[4] = {rt01.x, rt01.y, rt23.x, rt23.y};
+            unsigned long long key[4], first[4];
+            uint32_t h0[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) { // issue the four first probes
+                const uint32_t site = L.buckets ? xs[q] : xs[q] >> kLogSiteShift;
+                key[q] = static_cast<unsigned long long>(site) << 32 | hs[q];
+                h0[q] = static_cast<uint32_t>((key[q] * 0x9E3779B97F4A7C15ull) >> shift) & mask;
+                first[q] = i + q < n ? keys[h0[q]] : 0ull;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const bool in = i + q < n;
+                uint32_t slot = 0xFFFFFFFFu;
+                if (in) {
+                    slot = first[q] == key[q] ? h0[q] : insert_key(keys, mask, shift, key[q]);
+                    slot_of[base + i + q] = slot;
+                    bk[base + i + q] = L.buckets ? bs[q] : xs[q] & kBucketMask;
+                }
+                fold(slot, in, los[q], us[q], rts[q], lane, skey, sacc, acc);
+            }
         }
+    }
+    for (uint32_t i = lane; i < kAggSlots; i += 32) {
+        const uint32_t slot = skey[i];
+        if (slot == 0xFFFFFFFFu) continue;
+        const unsigned long long* e = sacc + i * 5;
+        acc_flush(acc + static_cast<size_t>(slot) * 5, e[0], e[1], e[2], e[3], e[4]);
     }
 }
 
@@ -124,85 +258,32 @@ __global__ void h_keys(const uint32_t* __restrict__ slot_of, const uint32_t* __r
         sk[j] = static_cast<K>(rank[slot_of[j]]) << kBucketBits | bk[j];
 }
 
-// H4: acc[row] = {count, limb0, limb1, limb2, min bits, max bits}.
+// H4: start[row] = first position of the row's run; start[n_rows] = n.
 template <typename K>
-__global__ void __launch_bounds__(256) h_reduce(const K* __restrict__ sk, const uint32_t* __restrict__ pos,
-                                                uint32_t n, DevLog whole,
-                                                unsigned long long* __restrict__ acc,
-                                                uint32_t* __restrict__ start) {
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += stride) {
-        const uint32_t i = base + threadIdx.x;
-        const bool in = i < n;
-        uint64_t row = ~0ull;
-        unsigned long long c = 0, l0 = 0, l1 = 0, l2 = 0, mn = kMinInitBits, mx = kMaxInitBits;
-        if (in) {
-            row = static_cast<uint64_t>(sk[i] >> kBucketBits);
-            const uint32_t p = pos[i];
-            const unsigned long long lo = whole.ulo[p];
-            c = 1;
-            l0 = lo & 0xFFFFFFFFull;
-            l1 = lo >> 32;
-            l2 = whole.uhi[p];
-            mn = mx = whole.rates[p];
-            if (i == 0 || static_cast<uint64_t>(sk[i - 1] >> kBucketBits) != row) start[row] = i;
-        }
-        // Segmented inclusive scan: runs are contiguous because rows are sorted.
-#pragma unroll
-        for (uint32_t d = 1; d < 32; d <<= 1) {
-            const uint64_t r2 = __shfl_up_sync(0xFFFFFFFFu, row, d);
-            const unsigned long long c2 = __shfl_up_sync(0xFFFFFFFFu, c, d);
-            const unsigned long long a0 = __shfl_up_sync(0xFFFFFFFFu, l0, d);
-            const unsigned long long a1 = __shfl_up_sync(0xFFFFFFFFu, l1, d);
-            const unsigned long long a2 = __shfl_up_sync(0xFFFFFFFFu, l2, d);
-            const unsigned long long m2 = __shfl_up_sync(0xFFFFFFFFu, mn, d);
-            const unsigned long long x2 = __shfl_up_sync(0xFFFFFFFFu, mx, d);
-            if (lane >= d && r2 == row) {
-                c += c2;
-                l0 += a0;
-                l1 += a1;
-                l2 += a2;
-                mn = min(mn, m2);
-                mx = max(mx, x2);
-            }
-        }
-        const uint64_t next = __shfl_down_sync(0xFFFFFFFFu, row, 1);
-        if (in && (lane == 31 || next != row)) { // run tail within this warp
-            unsigned long long* a = acc + row * 6;
-            atomicAdd(a + 0, c);
-            atomicAdd(a + 1, l0);
-            atomicAdd(a + 2, l1);
-            atomicAdd(a + 3, l2);
-            atomicMin(a + 4, mn);
-            atomicMax(a + 5, mx);
-        }
+__global__ void h_starts(const K* __restrict__ sk, uint32_t n, uint32_t n_rows, uint32_t* __restrict__ start) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const K row = sk[i] >> kBucketBits;
+        if (i == 0 || (sk[i - 1] >> kBucketBits) != row) start[row] = i;
     }
-}
-
-__global__ void h_init(unsigned long long* acc, uint32_t n_rows) {
-    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += gridDim.x * blockDim.x) {
-        unsigned long long* a = acc + static_cast<size_t>(r) * 6;
-        a[0] = a[1] = a[2] = a[3] = 0;
-        a[4] = kMinInitBits;
-        a[5] = kMaxInitBits;
-    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) start[n_rows] = n;
 }
 
 // H5, thread per row.
 template <typename K>
 __global__ void h_final(const unsigned long long* __restrict__ acc, const uint32_t* __restrict__ start,
                         const K* __restrict__ sk, const unsigned long long* __restrict__ hk_sorted,
-                        uint32_t n_rows, gnm_host_stats* __restrict__ rows) {
+                        const uint32_t* __restrict__ hs_sorted, uint32_t n_rows,
+                        gnm_host_stats* __restrict__ rows) {
     for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += gridDim.x * blockDim.x) {
-        const unsigned long long* a = acc + static_cast<size_t>(r) * 6;
-        const uint64_t cnt = a[0];
-        const unsigned __int128 u = static_cast<unsigned __int128>(a[1]) +
-                                    (static_cast<unsigned __int128>(a[2]) << 32) +
-                                    (static_cast<unsigned __int128>(a[3]) << 64);
-        const uint32_t k = static_cast<uint32_t>(sk[start[r] + (cnt + 1) / 2 - 1] & kBucketMask);
-        const double mn = __longlong_as_double(static_cast<long long>(a[4]));
-        const double mx = __longlong_as_double(static_cast<long long>(a[5]));
+        const unsigned long long* a = acc + static_cast<size_t>(hs_sorted[r]) * 5;
+        const uint32_t s0 = start[r];
+        const uint64_t cnt = start[r + 1] - s0;
+        const unsigned __int128 u = static_cast<unsigned __int128>(a[0]) +
+                                    (static_cast<unsigned __int128>(a[1]) << 32) +
+                                    (static_cast<unsigned __int128>(a[2]) << 64);
+        const uint32_t k = static_cast<uint32_t>(sk[s0 + (cnt + 1) / 2 - 1] & kBucketMask);
+        const double mn = __longlong_as_double(static_cast<long long>(~a[3]));
+        const double mx = __longlong_as_double(static_cast<long long>(a[4]));
         double med = median_of_bucket(k);
         med = med < mn ? mn : (mx < med ? mx : med);
         gnm_host_stats o;
@@ -248,38 +329,32 @@ cudaError_t dalloc(T** p, size_t n, cudaStream_t s) {
 
 // H3..H5 for one key width.
 template <typename K>
-cudaError_t sort_and_reduce(int device, uint32_t n, uint32_t n_rows, const uint32_t* slot_of, const uint32_t* bk,
-                            uint32_t* logpos, const unsigned long long* rank_tab,
-                            const unsigned long long* hk_sorted, const DevLog& whole, HostRows& out,
+cudaError_t sort_and_finish(int device, uint32_t n, uint32_t n_rows, const uint32_t* slot_of, const uint32_t* bk,
+                            const unsigned long long* rank_tab, const unsigned long long* acc,
+                            const unsigned long long* hk_sorted, const uint32_t* hs_sorted, HostRows& out,
                             cudaStream_t s) {
     K *sk = nullptr, *sk2 = nullptr;
-    uint32_t* pos2 = nullptr;
     HCK(dalloc(&sk, n, s));
     HCK(dalloc(&sk2, n, s));
-    HCK(dalloc(&pos2, n, s));
     h_keys<K><<<grid_for(device, n, 256), 256, 0, s>>>(slot_of, bk, n, rank_tab, sk);
     HCK(cudaGetLastError());
     const int end_bit = static_cast<int>(kBucketBits) + std::max(1, bits_for(n_rows));
     size_t tb = 0;
-    HCK(cub::DeviceRadixSort::SortPairs(nullptr, tb, sk, sk2, logpos, pos2, n, 0, end_bit, s));
+    HCK(cub::DeviceRadixSort::SortKeys(nullptr, tb, sk, sk2, n, 0, end_bit, s));
     void* tmp = nullptr;
     HCK(cudaMallocAsync(&tmp, std::max<size_t>(tb, 1), s));
-    HCK(cub::DeviceRadixSort::SortPairs(tmp, tb, sk, sk2, logpos, pos2, n, 0, end_bit, s));
+    HCK(cub::DeviceRadixSort::SortKeys(tmp, tb, sk, sk2, n, 0, end_bit, s));
     HCK(cudaFreeAsync(tmp, s));
     HCK(cudaFreeAsync(sk, s));
-    unsigned long long* acc = nullptr;
     uint32_t* start = nullptr;
-    HCK(dalloc(&acc, static_cast<size_t>(n_rows) * 6, s));
-    HCK(dalloc(&start, n_rows, s));
-    h_init<<<grid_for(device, n_rows, 256), 256, 0, s>>>(acc, n_rows);
-    h_reduce<K><<<grid_for(device, n, 256), 256, 0, s>>>(sk2, pos2, n, whole, acc, start);
+    HCK(dalloc(&start, static_cast<size_t>(n_rows) + 1, s));
+    h_starts<K><<<grid_for(device, n, 256), 256, 0, s>>>(sk2, n, n_rows, start);
     HCK(cudaGetLastError());
     HCK(dalloc(&out.rows, n_rows, s));
-    h_final<K><<<grid_for(device, n_rows, 128), 128, 0, s>>>(acc, start, sk2, hk_sorted, n_rows, out.rows);
+    h_final<K><<<grid_for(device, n_rows, 128), 128, 0, s>>>(acc, start, sk2, hk_sorted, hs_sorted, n_rows,
+                                                             out.rows);
     HCK(cudaGetLastError());
-    HCK(cudaFreeAsync(acc, s));
     HCK(cudaFreeAsync(start, s));
-    HCK(cudaFreeAsync(pos2, s));
     out.sorted = sk2;
     out.key64 = sizeof(K) == 8;
     out.n_rows = n_rows;
@@ -289,8 +364,9 @@ cudaError_t sort_and_reduce(int device, uint32_t n, uint32_t n_rows, const uint3
 
 } // namespace
 
-cudaError_t build_hosts(int device, const DevLog& whole, const HostSlice* slices, int n_slices,
-                        const unsigned int* counts, size_t n_counts, HostRows& out, cudaStream_t s) {
+cudaError_t build_hosts(int device, const HostSlice* slices, int n_slices,
+                        const unsigned int* counts, size_t n_counts, uint64_t max_keys, HostRows& out,
+                        cudaStream_t s) {
     free_hosts(out, s);
     if (n_counts == 0) return cudaSuccess;
     // H0: flat offsets of every warp region's entries.
@@ -315,28 +391,39 @@ cudaError_t build_hosts(int device, const DevLog& whole, const HostSlice* slices
         HCK(cudaFreeAsync(scal, s));
         return cudaSuccess;
     }
-    // H1: key table of at least 2 slots per flow.
-    const int tbits = std::max(10, bits_for(2 * n));
+    static bool attr = false;
+    if (!attr) {
+        HCK(cudaFuncSetAttribute(h_insert, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kInsSmem)));
+        attr = true;
+    }
+    int sms = 0;
+    HCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    // H1: at least two slots per possible key.
+    const int tbits = std::max(10, bits_for(2 * std::max<uint64_t>(1, std::min(n, max_keys))));
     const uint32_t cap = 1u << tbits;
-    unsigned long long* keys = nullptr;
-    uint32_t *slot_of = nullptr, *bk = nullptr, *logpos = nullptr;
+    unsigned long long *keys = nullptr, *acc = nullptr;
+    uint32_t *slot_of = nullptr, *bk = nullptr;
     HCK(dalloc(&keys, cap, s));
+    HCK(dalloc(&acc, static_cast<size_t>(cap) * 5, s));
     HCK(dalloc(&slot_of, n, s));
     HCK(dalloc(&bk, n, s));
-    HCK(dalloc(&logpos, n, s));
     HCK(cudaMemsetAsync(keys, 0xFF, static_cast<size_t>(cap) * 8, s));
+    HCK(cudaMemsetAsync(acc, 0, static_cast<size_t>(cap) * 40, s));
     for (int i = 0; i < n_slices; ++i) {
         const HostSlice& sl = slices[i];
-        h_insert<<<grid_for(device, static_cast<uint64_t>(sl.log.regions) * 32, 256), 256, 0, s>>>(
-            sl.log, counts + sl.count_off, off + sl.count_off, static_cast<uint32_t>(sl.entry_off), keys,
-            cap - 1, 64 - tbits, slot_of, bk, logpos);
+        // Three CTAs per SM (80 registers), fewer for small logs.
+        const uint64_t items = static_cast<uint64_t>(sl.log.regions) * ((sl.log.warp_cap + kInsChunk - 1) / kInsChunk);
+        const uint32_t g = std::min<uint32_t>(grid_for(device, items * 32, kInsBlock), 3 * sms);
+        h_insert<<<g, kInsBlock, kInsSmem, s>>>(sl.log, counts + sl.count_off, off + sl.count_off, keys, cap - 1,
+                                                64 - tbits, acc, slot_of, bk);
         HCK(cudaGetLastError());
     }
     // H2: distinct keys in (site, host) order -> rows.
     unsigned long long *hk = nullptr, *hk_sorted = nullptr;
     uint32_t *hs = nullptr, *hs_sorted = nullptr;
-    HCK(dalloc(&hk, n, s));
-    HCK(dalloc(&hs, n, s));
+    const uint64_t kcap = std::min<uint64_t>(n, cap);
+    HCK(dalloc(&hk, kcap, s));
+    HCK(dalloc(&hs, kcap, s));
     h_collect<<<grid_for(device, cap, 256), 256, 0, s>>>(keys, cap, hk, hs,
                                                         reinterpret_cast<unsigned int*>(scal + 1));
     HCK(cudaGetLastError());
@@ -355,12 +442,12 @@ cudaError_t build_hosts(int device, const DevLog& whole, const HostSlice* slices
     // H3..H5.
     const uint32_t n32 = static_cast<uint32_t>(n);
     if (kBucketBits + bits_for(n_rows) <= 32)
-        HCK(sort_and_reduce<uint32_t>(device, n32, n_rows, slot_of, bk, logpos, keys, hk_sorted, whole, out, s));
+        HCK(sort_and_finish<uint32_t>(device, n32, n_rows, slot_of, bk, keys, acc, hk_sorted, hs_sorted, out, s));
     else
-        HCK(sort_and_reduce<unsigned long long>(device, n32, n_rows, slot_of, bk, logpos, keys, hk_sorted, whole,
+        HCK(sort_and_finish<unsigned long long>(device, n32, n_rows, slot_of, bk, keys, acc, hk_sorted, hs_sorted,
                                                 out, s));
     for (void* p : {static_cast<void*>(off), static_cast<void*>(scal), static_cast<void*>(keys),
-                    static_cast<void*>(slot_of), static_cast<void*>(bk), static_cast<void*>(logpos),
+                    static_cast<void*>(acc), static_cast<void*>(slot_of), static_cast<void*>(bk),
                     static_cast<void*>(hk), static_cast<void*>(hs), static_cast<void*>(hk_sorted),
                     static_cast<void*>(hs_sorted)})
         HCK(cudaFreeAsync(p, s));

@@ -27,11 +27,12 @@ struct HostRows {
     uint64_t n_flows = 0;
 };
 
-// Builds the per-host rows from the log: whole-log base pointers of the host
-// columns (L.hosts/rates/ulo/uhi relative to entry 0), the slices, and all
-// per-warp counts. Synchronises `s` twice (to size the tables).
-cudaError_t build_hosts(int device, const DevLog& whole, const HostSlice* slices, int n_slices,
-                        const unsigned int* counts, size_t n_counts, HostRows& out, cudaStream_t s);
+// Builds the per-host rows from the log slices and all per-warp counts.
+// max_keys bounds the distinct (site, host) keys (256 per registry /24
+// entry). Synchronises `s` twice (to size the tables).
+cudaError_t build_hosts(int device, const HostSlice* slices, int n_slices,
+                        const unsigned int* counts, size_t n_counts, uint64_t max_keys, HostRows& out,
+                        cudaStream_t s);
 
 // Dense [n_rows][kBuckets] histograms of the rows (device buffer, zeroed by the caller).
 cudaError_t hosts_histograms(int device, const HostRows& h, uint32_t* dense, cudaStream_t s);
