@@ -271,6 +271,7 @@ class Reference:
             "ref_result_site_ids": (C.c_size_t, [V, V, C.c_size_t]),
             "ref_result_site": (C.c_int, [V, U32, V, V, V, V, V]),
             "ref_result_hosts": (C.c_size_t, [V, U32, V, C.c_size_t]),
+            "ref_ingest_batch": (C.c_size_t, [V, V, C.c_size_t, V, V]),
             "ref_result_host": (C.c_int, [V, U32, U32, V, V, V, V]),
             "ref_site_sums": (None, [V, V, U32, U32, U32, U32, V, V, V]),
             "ref_wstate_create": (V, []),
@@ -334,6 +335,15 @@ class Reference:
             return bytes(buf), -1
         finally:
             self.L.ref_records_destroy(h)
+
+    def ingest_batch(self, buf: np.ndarray, offsets: np.ndarray, out: np.ndarray):
+        """The collector's decode loop over n datagrams, timed in C:
+        (accepted records written to `out` (64-byte rows), elapsed ms)."""
+        b = np.ascontiguousarray(buf, np.uint8)
+        o = np.ascontiguousarray(offsets, np.uint64)
+        ms = C.c_double()
+        k = self.L.ref_ingest_batch(_p(b), _p(o), len(o) - 1, out.ctypes.data, C.byref(ms))
+        return k, ms.value
 
     def encode_packet(self, header: Sequence[int], raw: np.ndarray) -> bytes:
         """encode_packet(ExportHeader{header...}, raw RawFlowRecord rows)."""

@@ -426,6 +426,30 @@ int ref_ingest_datagram(const uint8_t* d, size_t len, void* out, size_t* n_out, 
     return 0;
 }
 
+// The collector's decode loop over a batch of datagrams (Collector::
+// ingest_datagram minus the socket and the store, collector.cpp:101-129),
+// timed in C: datagram i is bytes [off[i], off[i+1]). Returns the accepted
+// record count; *ms = wall time of the loop.
+size_t ref_ingest_batch(const uint8_t* buf, const uint64_t* off, size_t n, void* out, double* ms) {
+    auto* o = static_cast<FlowRecord*>(out);
+    size_t k = 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (size_t i = 0; i < n; ++i) {
+        DecodedPacket packet;
+        try {
+            packet = decode_packet(std::span<const std::uint8_t>(buf + off[i], off[i + 1] - off[i]));
+        } catch (const CodecError&) {
+            continue;
+        }
+        for (const RawFlowRecord& raw : packet.records) {
+            if (raw.d_pkts == 0 || raw.d_octets < raw.d_pkts) continue;
+            o[k++] = resolve_times(packet.header, raw);
+        }
+    }
+    *ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return k;
+}
+
 // encode_packet (netflow.cpp:115-143): h = {version, count, sys_uptime,
 // unix_secs, unix_nsecs, flow_sequence, engine_type, engine_id,
 // sampling_interval}; `raw` holds `n` RawFlowRecords (48-byte struct).

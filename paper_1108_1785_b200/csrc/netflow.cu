@@ -13,13 +13,16 @@
 // order, then record order -- exactly the order the collector appends to the
 // FlowStore. Paths are relative to /root/reference/proj/core/src.
 //
-// Three kernels: N1 validates every datagram and counts its accepted
-// records (thread per datagram), N2 turns the counts into output offsets (one
-// CTA, exclusive scan), N3 decodes (warp per datagram, lane = record) and
-// compacts the accepted records with a ballot.
+// N1 validates every datagram and counts its accepted records (thread per
+// datagram), N2 turns the counts into output offsets (cub's decoupled
+// look-back exclusive scan), N3 decodes (warp per datagram, lane = record)
+// and compacts the accepted records with a ballot.
 #include <cuda_runtime.h>
 
 #include <cstdint>
+
+#include <cub/device/device_scan.cuh>
+#include <cuda/std/functional>
 
 #include "netflow.cuh"
 
@@ -55,71 +58,85 @@ __device__ __forceinline__ uint32_t check_header(const uint8_t* p, uint64_t len,
     return 0;
 }
 
+__device__ __forceinline__ uint32_t ld_be32(const uint8_t* q, bool words) {
+    return words ? __byte_perm(__ldg(reinterpret_cast<const uint32_t*>(q)), 0, 0x0123) : be32(q);
+}
+
+// N1, warp per datagram: header checks (lane 0's view is every lane's), then
+// lane r tests record r's reject rule; the ballot's popcount is the
+// datagram's accepted count.
 __global__ void __launch_bounds__(256) n1_validate(const uint8_t* __restrict__ d,
                                                    const uint64_t* __restrict__ off, uint64_t n,
                                                    uint32_t* __restrict__ accepted,
                                                    uint8_t* __restrict__ status,
                                                    unsigned long long* __restrict__ stats) {
-    uint32_t err = 0, rej = 0, acc = 0;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    uint32_t err = 0, rej = 0, acc = 0; // lane 0's running totals
+    for (uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < n; i += nwarps) {
         const uint8_t* p = d + off[i];
         uint32_t count;
-        const uint32_t st = check_header(p, off[i + 1] - off[i], count);
-        uint32_t a = 0;
-        if (st == 0) {
-            for (uint32_t r = 0; r < count; ++r) {
-                const uint8_t* q = p + kHdr + kRec * r;
-                const uint32_t pkts = be32(q + 16), oct = be32(q + 20);
-                a += (pkts != 0 && oct >= pkts);
-            }
-            rej += count - a;
-        } else {
-            ++err;
+        const uint32_t st = check_header(p, off[i + 1] - off[i], count); // warp-uniform
+        bool ok = false;
+        if (st == 0 && lane < count) {
+            const uint8_t* q = p + kHdr + kRec * lane;
+            const bool words = (reinterpret_cast<uintptr_t>(p) & 3u) == 0;
+            const uint32_t pkts = ld_be32(q + 16, words), oct = ld_be32(q + 20, words);
+            ok = pkts != 0 && oct >= pkts;
         }
-        acc += a;
-        accepted[i] = a;
-        if (status) status[i] = static_cast<uint8_t>(st);
+        const uint32_t a = __popc(__ballot_sync(0xFFFFFFFFu, ok));
+        if (lane == 0) {
+            if (st == 0) rej += count - a;
+            else ++err;
+            acc += a;
+            accepted[i] = a;
+            if (status) status[i] = static_cast<uint8_t>(st);
+        }
     }
-    err = __reduce_add_sync(0xFFFFFFFFu, err);
-    rej = __reduce_add_sync(0xFFFFFFFFu, rej);
-    acc = __reduce_add_sync(0xFFFFFFFFu, acc);
-    if ((threadIdx.x & 31u) == 0) {
+    if (lane == 0) {
         if (err) atomicAdd(stats + 1, static_cast<unsigned long long>(err));
         if (rej) atomicAdd(stats + 2, static_cast<unsigned long long>(rej));
         if (acc) atomicAdd(stats + 3, static_cast<unsigned long long>(acc));
     }
 }
 
-// Exclusive scan of n u32 counts into u64 offsets, one 1024-thread CTA:
-// thread t owns the contiguous slice [t*chunk, (t+1)*chunk).
-__global__ void __launch_bounds__(1024) n2_scan(const uint32_t* __restrict__ in, uint64_t n,
-                                                uint64_t* __restrict__ out,
-                                                unsigned long long* __restrict__ total) {
-    __shared__ unsigned long long part[1024];
-    const uint64_t chunk = (n + blockDim.x - 1) / blockDim.x;
-    const uint64_t b = threadIdx.x * chunk, e = min(n, b + chunk);
-    unsigned long long s = 0;
-    for (uint64_t i = b; i < e; ++i) s += in[i];
-    part[threadIdx.x] = s;
-    __syncthreads();
-    for (uint32_t o = 1; o < blockDim.x; o <<= 1) { // inclusive scan
-        const unsigned long long x = threadIdx.x >= o ? part[threadIdx.x - o] : 0ull;
-        __syncthreads();
-        part[threadIdx.x] += x;
-        __syncthreads();
-    }
-    unsigned long long run = threadIdx.x ? part[threadIdx.x - 1] : 0ull;
-    for (uint64_t i = b; i < e; ++i) {
-        out[i] = run;
-        run += in[i];
-    }
-    if (threadIdx.x == blockDim.x - 1) *total = part[threadIdx.x];
+__global__ void n2_total(const uint32_t* __restrict__ in, const uint64_t* __restrict__ base, uint64_t n,
+                         unsigned long long* __restrict__ total) {
+    *total = base[n - 1] + in[n - 1];
 }
 
-// Warp per datagram; lane r decodes record r (decode_raw_record,
-// netflow.cpp:27-50) and resolve_times; accepted lanes are compacted in
-// record order.
+// Record fields of one 48-byte big-endian record (decode_raw_record,
+// netflow.cpp:27-50) as the RawFlowRecord words in memory order
+// (netflow.hpp:32-57): u32 src, dst, next_hop; u16 input_if, output_if; u32
+// d_pkts, d_octets, first, last; u16 src_port, dst_port; u8 pad1,
+// tcp_flags, protocol, tos; u16 src_as, dst_as; u8 src_mask, dst_mask; u16
+// pad2. kWords: the record is 4-byte aligned, so 12 word loads and byte
+// permutes replace 48 byte loads.
+template <bool kWords>
+__device__ __forceinline__ void load_raw(const uint8_t* q, uint4& w0, uint4& w1, uint4& w2) {
+    if constexpr (kWords) {
+        const uint32_t* u = reinterpret_cast<const uint32_t*>(q);
+        uint32_t x[12];
+#pragma unroll
+        for (int k = 0; k < 12; ++k) x[k] = __ldg(u + k);
+        auto sw = [](uint32_t v) { return __byte_perm(v, 0, 0x0123); };   // be32
+        auto sw16 = [](uint32_t v) { return __byte_perm(v, 0, 0x2301); }; // two be16
+        w0 = make_uint4(sw(x[0]), sw(x[1]), sw(x[2]), sw16(x[3]));
+        w1 = make_uint4(sw(x[4]), sw(x[5]), sw(x[6]), sw(x[7]));
+        w2 = make_uint4(sw16(x[8]), x[9], sw16(x[10]), __byte_perm(x[11], 0, 0x2310));
+    } else {
+        w0 = make_uint4(be32(q), be32(q + 4), be32(q + 8), be16(q + 12) | be16(q + 14) << 16);
+        w1 = make_uint4(be32(q + 16), be32(q + 20), be32(q + 24), be32(q + 28));
+        w2 = make_uint4(be16(q + 32) | be16(q + 34) << 16,
+                        static_cast<uint32_t>(q[36]) | static_cast<uint32_t>(q[37]) << 8 |
+                            static_cast<uint32_t>(q[38]) << 16 | static_cast<uint32_t>(q[39]) << 24,
+                        be16(q + 40) | be16(q + 42) << 16,
+                        static_cast<uint32_t>(q[44]) | static_cast<uint32_t>(q[45]) << 8 | be16(q + 46) << 16);
+    }
+}
+
+// Warp per datagram; lane r decodes record r and resolve_times; accepted
+// lanes are compacted in record order.
 __global__ void __launch_bounds__(256) n3_decode(const uint8_t* __restrict__ d,
                                                  const uint64_t* __restrict__ off, uint64_t n,
                                                  const uint64_t* __restrict__ base,
@@ -137,20 +154,10 @@ __global__ void __launch_bounds__(256) n3_decode(const uint8_t* __restrict__ d,
         uint64_t start = 0, end = 0;
         if (lane < count) {
             const uint8_t* q = p + kHdr + kRec * lane;
-            const uint32_t pkts = be32(q + 16), oct = be32(q + 20);
+            if ((reinterpret_cast<uintptr_t>(p) & 3u) == 0) load_raw<true>(q, w0, w1, w2); // warp-uniform
+            else load_raw<false>(q, w0, w1, w2);
+            const uint32_t pkts = w1.x, oct = w1.y, first = w1.z, last = w1.w;
             ok = pkts != 0 && oct >= pkts;
-            const uint32_t first = be32(q + 24), last = be32(q + 28);
-            // RawFlowRecord in memory order (netflow.hpp:32-57): u32 src, dst,
-            // next_hop; u16 input_if, output_if; u32 d_pkts, d_octets, first,
-            // last; u16 src_port, dst_port; u8 pad1, tcp_flags, protocol, tos;
-            // u16 src_as, dst_as; u8 src_mask, dst_mask; u16 pad2.
-            w0 = make_uint4(be32(q), be32(q + 4), be32(q + 8), be16(q + 12) | be16(q + 14) << 16);
-            w1 = make_uint4(pkts, oct, first, last);
-            w2 = make_uint4(be16(q + 32) | be16(q + 34) << 16,
-                            static_cast<uint32_t>(q[36]) | static_cast<uint32_t>(q[37]) << 8 |
-                                static_cast<uint32_t>(q[38]) << 16 | static_cast<uint32_t>(q[39]) << 24,
-                            be16(q + 40) | be16(q + 42) << 16,
-                            static_cast<uint32_t>(q[44]) | static_cast<uint32_t>(q[45]) << 8 | be16(q + 46) << 16);
             start = wall - wrap_diff(uptime, first);
             end = wall - wrap_diff(uptime, last);
             if (end < start) end = start; // degenerate record (netflow.cpp:157-159)
@@ -167,25 +174,51 @@ __global__ void __launch_bounds__(256) n3_decode(const uint8_t* __restrict__ d,
     }
 }
 
-// FlowStore::load's entry decode (flow_store.cpp:194-200), thread per entry:
-// be64 start/end and decode_raw_record of the big-endian raw record, written
-// as the 64-byte little-endian FlowRecord (raw fields, start_ms, end_ms).
-__global__ void __launch_bounds__(256) a1_decode(const uint32_t* __restrict__ e, uint64_t n,
-                                                 uint4* __restrict__ out) {
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint32_t* w = e + i * 16;
-        uint32_t x[16];
+// FlowStore::load's entry decode (flow_store.cpp:194-200): be64 start/end
+// and decode_raw_record of the big-endian raw record, written as the 64-byte
+// little-endian FlowRecord (raw fields, start_ms, end_ms). Entries sit at
+// 20 + 64*i (4-byte aligned only), so a warp moves 32 entries at a time
+// through shared memory: coalesced word loads in, a per-lane decode from a
+// padded tile (stride 17 words: conflict-free), coalesced 16-byte stores out.
+constexpr uint32_t kA1Block = 256;
+__global__ void __launch_bounds__(kA1Block) a1_decode(const uint32_t* __restrict__ e, uint64_t n,
+                                                      uint4* __restrict__ out) {
+    __shared__ uint32_t tile[kA1Block / 32][32 * 17];
+    __shared__ uint4 rows[kA1Block / 32][32 * 4];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    uint32_t* t = tile[warp];
+    uint4* o = rows[warp];
+    const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t b = ((static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 32; b < n;
+         b += nwarps * 32) {
+        const uint32_t cnt = n - b < 32 ? static_cast<uint32_t>(n - b) : 32u;
+        const uint32_t* src = e + b * 16;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) x[k] = __ldg(w + k);
-        auto sw = [](uint32_t v) { return __byte_perm(v, 0, 0x0123); };  // be32
-        auto sw16 = [](uint32_t v) { return __byte_perm(v, 0, 0x2301); }; // two be16
-        uint4* o = out + i * 4;
-        // raw record = entry words 4..15
-        o[0] = make_uint4(sw(x[4]), sw(x[5]), sw(x[6]), sw16(x[7]));
-        o[1] = make_uint4(sw(x[8]), sw(x[9]), sw(x[10]), sw(x[11]));
-        o[2] = make_uint4(sw16(x[12]), x[13], sw16(x[14]), __byte_perm(x[15], 0, 0x2310));
-        o[3] = make_uint4(sw(x[1]), sw(x[0]), sw(x[3]), sw(x[2])); // start_ms, end_ms (LE u64)
+        for (uint32_t k = 0; k < 16; ++k) {
+            const uint32_t idx = k * 32 + lane;
+            if (idx < cnt * 16) t[(idx >> 4) * 17 + (idx & 15u)] = __ldcs(src + idx);
+        }
+        __syncwarp();
+        if (lane < cnt) {
+            uint32_t x[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) x[k] = t[lane * 17 + k];
+            auto sw = [](uint32_t v) { return __byte_perm(v, 0, 0x0123); };  // be32
+            auto sw16 = [](uint32_t v) { return __byte_perm(v, 0, 0x2301); }; // two be16
+            // raw record = entry words 4..15
+            o[lane * 4 + 0] = make_uint4(sw(x[4]), sw(x[5]), sw(x[6]), sw16(x[7]));
+            o[lane * 4 + 1] = make_uint4(sw(x[8]), sw(x[9]), sw(x[10]), sw(x[11]));
+            o[lane * 4 + 2] = make_uint4(sw16(x[12]), x[13], sw16(x[14]), __byte_perm(x[15], 0, 0x2310));
+            o[lane * 4 + 3] = make_uint4(sw(x[1]), sw(x[0]), sw(x[3]), sw(x[2])); // start_ms, end_ms (LE u64)
+        }
+        __syncwarp();
+        uint4* dst = out + b * 4;
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k) {
+            const uint32_t idx = k * 32 + lane;
+            if (idx < cnt * 4) __stcs(dst + idx, o[idx]);
+        }
+        __syncwarp();
     }
 }
 
@@ -193,8 +226,8 @@ __global__ void __launch_bounds__(256) a1_decode(const uint32_t* __restrict__ e,
 
 cudaError_t launch_archive_decode(const uint8_t* entries, uint64_t n, uint8_t* out, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    const uint32_t g = static_cast<uint32_t>(std::min<uint64_t>((n + 255) / 256, 148 * 16));
-    a1_decode<<<g, 256, 0, s>>>(reinterpret_cast<const uint32_t*>(entries), n, reinterpret_cast<uint4*>(out));
+    const uint32_t g = static_cast<uint32_t>(std::min<uint64_t>((n + kA1Block - 1) / kA1Block, 148 * 8));
+    a1_decode<<<g, kA1Block, 0, s>>>(reinterpret_cast<const uint32_t*>(entries), n, reinterpret_cast<uint4*>(out));
     return cudaGetLastError();
 }
 
@@ -202,9 +235,20 @@ cudaError_t launch_netflow_decode(const uint8_t* d, const uint64_t* off, uint64_
                                   uint64_t* base, uint8_t* status, unsigned long long* stats,
                                   uint8_t* out, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    const uint32_t g1 = static_cast<uint32_t>(std::min<uint64_t>((n + 255) / 256, 4096));
+    const uint32_t g1 = static_cast<uint32_t>(std::min<uint64_t>((n * 32 + 255) / 256, 148 * 16));
     n1_validate<<<g1, 256, 0, s>>>(d, off, n, accepted, status, stats);
-    n2_scan<<<1, 1024, 0, s>>>(accepted, n, base, stats + 4);
+    // N2: exclusive scan (decoupled look-back) of the accepted counts into u64 offsets.
+    size_t tb = 0;
+    cudaError_t e = cub::DeviceScan::ExclusiveScan(nullptr, tb, accepted, base, ::cuda::std::plus<uint64_t>(),
+                                                   static_cast<uint64_t>(0), n, s);
+    if (e != cudaSuccess) return e;
+    void* tmp = nullptr;
+    if ((e = cudaMallocAsync(&tmp, std::max<size_t>(tb, 1), s)) != cudaSuccess) return e;
+    e = cub::DeviceScan::ExclusiveScan(tmp, tb, accepted, base, ::cuda::std::plus<uint64_t>(),
+                                       static_cast<uint64_t>(0), n, s);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaFreeAsync(tmp, s)) != cudaSuccess) return e;
+    n2_total<<<1, 1, 0, s>>>(accepted, base, n, stats + 4);
     const uint32_t g3 = static_cast<uint32_t>(std::min<uint64_t>((n * 32 + 255) / 256, 65535));
     n3_decode<<<g3, 256, 0, s>>>(d, off, n, base, out);
     return cudaGetLastError();
