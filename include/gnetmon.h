@@ -216,6 +216,12 @@ uint64_t gnm_host_count(gnm_ctx* ctx);
  * buckets (HostResult::histogram) into histograms[capacity * 10001]. Valid
  * until the next finalize or reset. */
 int gnm_host_results(gnm_ctx* ctx, gnm_host_stats* out, uint64_t capacity, uint32_t* histograms);
+/* The same histograms in sparse form: the non-zero (row, bucket) counts in
+ * (row, bucket) order; row indexes the gnm_host_results rows. With rows ==
+ * NULL only *n_entries is set (a query); otherwise GNM_ERR_CAPACITY when
+ * capacity < *n_entries. Host arrays. */
+int gnm_host_histogram_entries(gnm_ctx* ctx, uint32_t* rows, uint32_t* buckets, uint32_t* counts,
+                               uint64_t capacity, uint64_t* n_entries);
 
 /* aggregate() (rate_engine.cpp:335-347) + the K3 site synthesis
  * (finalize/stats_from, rate_engine.cpp:242-292) in one synchronous call.

@@ -157,6 +157,7 @@ _SIGS = [
     ("gnm_ctx_set_hosts", C.c_int, [_P, C.c_int]),
     ("gnm_host_count", C.c_uint64, [_P]),
     ("gnm_host_results", C.c_int, [_P, _P, C.c_uint64, _P]),
+    ("gnm_host_histogram_entries", C.c_int, [_P, _P, _P, _P, C.c_uint64, C.POINTER(C.c_uint64)]),
     ("gnm_analyze", C.c_int,
      [_P, _P, C.POINTER(gnm_filter_params), C.POINTER(gnm_batch_soa), C.POINTER(gnm_result)]),
     ("gnm_analyze_aos", C.c_int,

@@ -890,6 +890,31 @@ int gnm_host_results(gnm_ctx* c, gnm_host_stats* out, uint64_t capacity, uint32_
     });
 }
 
+int gnm_host_histogram_entries(gnm_ctx* c, uint32_t* rows, uint32_t* buckets, uint32_t* counts,
+                               uint64_t capacity, uint64_t* n_entries) {
+    if (!c || !n_entries) return fail(GNM_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        uint64_t n = 0;
+        ck(gnm::hosts_sparse(c->device, c->hrows, &n, c->stream), "host histogram entries");
+        *n_entries = n;
+        if (!rows || n == 0) return static_cast<int>(GNM_OK);
+        if (capacity < n || !buckets || !counts)
+            return fail(GNM_ERR_CAPACITY, "host histogram entries: capacity " + std::to_string(capacity) + " < " +
+                                              std::to_string(n));
+        uint32_t* d = nullptr;
+        ck(cudaMallocAsync(reinterpret_cast<void**>(&d), n * 12, c->stream), "cudaMallocAsync(host entries)");
+        ck(gnm::hosts_sparse_export(c->device, c->hrows, d, d + n, d + 2 * n, c->stream), "host entries export");
+        c->kernel_launches += 1;
+        ck(cudaMemcpyAsync(rows, d, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H rows");
+        ck(cudaMemcpyAsync(buckets, d + n, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H buckets");
+        ck(cudaMemcpyAsync(counts, d + 2 * n, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H counts");
+        ck(cudaFreeAsync(d, c->stream), "cudaFreeAsync(host entries)");
+        ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+        return static_cast<int>(GNM_OK);
+    });
+}
+
 int gnm_ctx_enable_timing(gnm_ctx* c, int enable) {
     if (!c) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx");
     c->timing = enable != 0;

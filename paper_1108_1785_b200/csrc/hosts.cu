@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_run_length_encode.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
@@ -465,9 +466,71 @@ cudaError_t hosts_histograms(int device, const HostRows& h, uint32_t* dense, cud
     return cudaGetLastError();
 }
 
+namespace {
+template <typename K>
+cudaError_t rle(HostRows& h, cudaStream_t s) {
+    const K* in = static_cast<const K*>(h.sorted);
+    K* keys = nullptr;
+    uint64_t* d_n = nullptr;
+    HCK(dalloc(&keys, h.n_flows, s));
+    HCK(dalloc(&h.sp_counts, h.n_flows, s));
+    HCK(dalloc(&d_n, 1, s));
+    size_t tb = 0;
+    HCK(cub::DeviceRunLengthEncode::Encode(nullptr, tb, in, keys, h.sp_counts, d_n, h.n_flows, s));
+    void* tmp = nullptr;
+    HCK(cudaMallocAsync(&tmp, std::max<size_t>(tb, 1), s));
+    HCK(cub::DeviceRunLengthEncode::Encode(tmp, tb, in, keys, h.sp_counts, d_n, h.n_flows, s));
+    HCK(cudaFreeAsync(tmp, s));
+    uint64_t n = 0;
+    HCK(cudaMemcpyAsync(&n, d_n, 8, cudaMemcpyDeviceToHost, s));
+    HCK(cudaFreeAsync(d_n, s));
+    HCK(cudaStreamSynchronize(s));
+    h.sp_keys = keys;
+    h.n_sparse = n;
+    return cudaSuccess;
+}
+
+template <typename K>
+__global__ void h_split(const K* __restrict__ keys, uint64_t n, uint32_t* __restrict__ rows,
+                        uint32_t* __restrict__ buckets) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        rows[i] = static_cast<uint32_t>(keys[i] >> kBucketBits);
+        buckets[i] = static_cast<uint32_t>(keys[i] & kBucketMask);
+    }
+}
+} // namespace
+
+cudaError_t hosts_sparse(int device, HostRows& h, uint64_t* n, cudaStream_t s) {
+    (void)device;
+    if (h.n_sparse == ~0ull) {
+        if (h.n_flows == 0) {
+            h.n_sparse = 0;
+        } else {
+            HCK(h.key64 ? rle<unsigned long long>(h, s) : rle<uint32_t>(h, s));
+        }
+    }
+    *n = h.n_sparse;
+    return cudaSuccess;
+}
+
+cudaError_t hosts_sparse_export(int device, const HostRows& h, uint32_t* rows, uint32_t* buckets, uint32_t* counts,
+                                cudaStream_t s) {
+    if (h.n_sparse == 0 || h.n_sparse == ~0ull) return cudaSuccess;
+    const uint32_t g = grid_for(device, h.n_sparse, 256);
+    if (h.key64)
+        h_split<<<g, 256, 0, s>>>(static_cast<const unsigned long long*>(h.sp_keys), h.n_sparse, rows, buckets);
+    else
+        h_split<<<g, 256, 0, s>>>(static_cast<const uint32_t*>(h.sp_keys), h.n_sparse, rows, buckets);
+    HCK(cudaGetLastError());
+    return cudaMemcpyAsync(counts, h.sp_counts, h.n_sparse * 4, cudaMemcpyDeviceToDevice, s);
+}
+
 void free_hosts(HostRows& h, cudaStream_t s) {
     if (h.rows) cudaFreeAsync(h.rows, s);
     if (h.sorted) cudaFreeAsync(h.sorted, s);
+    if (h.sp_keys) cudaFreeAsync(h.sp_keys, s);
+    if (h.sp_counts) cudaFreeAsync(h.sp_counts, s);
     h = HostRows{};
 }
 

@@ -25,6 +25,10 @@ struct HostRows {
     void* sorted = nullptr; // u32 (row << 14 | bucket) or u64, per key64
     bool key64 = false;
     uint64_t n_flows = 0;
+    // Sparse histograms (run-length encoding of `sorted`), built on demand.
+    void* sp_keys = nullptr; // unique (row << 14 | bucket), same width as `sorted`
+    uint32_t* sp_counts = nullptr;
+    uint64_t n_sparse = ~0ull; // ~0: not built yet
 };
 
 // Builds the per-host rows from the log slices and all per-warp counts.
@@ -36,6 +40,13 @@ cudaError_t build_hosts(int device, const HostSlice* slices, int n_slices,
 
 // Dense [n_rows][kBuckets] histograms of the rows (device buffer, zeroed by the caller).
 cudaError_t hosts_histograms(int device, const HostRows& h, uint32_t* dense, cudaStream_t s);
+
+// Sparse histograms: the non-zero (row, bucket) counts in (row, bucket)
+// order. hosts_sparse builds them (once per result) and returns their count
+// (synchronises `s`); hosts_sparse_export writes them to device arrays.
+cudaError_t hosts_sparse(int device, HostRows& h, uint64_t* n, cudaStream_t s);
+cudaError_t hosts_sparse_export(int device, const HostRows& h, uint32_t* rows, uint32_t* buckets, uint32_t* counts,
+                                cudaStream_t s);
 
 void free_hosts(HostRows& h, cudaStream_t s);
 

@@ -535,6 +535,18 @@ class Engine:
         res.host_histograms = None if hist is None else hist[:n]
         return res
 
+    def host_histogram_entries(self):
+        """The last hosts-mode result's per-host histograms, sparse: (row,
+        bucket, count) arrays in (row, bucket) order, row indexing
+        ``host_table`` (HostResult::histogram without the 40 KB per host)."""
+        n = C.c_uint64()
+        _check(lib.gnm_host_histogram_entries(self._h, None, None, None, 0, C.byref(n)))
+        rows, bks, cnt = (np.empty(max(n.value, 1), np.uint32) for _ in range(3))
+        _check(lib.gnm_host_histogram_entries(self._h, rows.ctypes.data, bks.ctypes.data, cnt.ctypes.data,
+                                              len(rows), C.byref(n)))
+        k = n.value
+        return rows[:k], bks[:k], cnt[:k]
+
     def enable_timing(self, on: bool = True) -> None:
         _check(lib.gnm_ctx_enable_timing(self._h, 1 if on else 0))
 

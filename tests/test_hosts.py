@@ -98,6 +98,10 @@ def test_gpu_hosts_reproduce_reference_fixture(hosts_engine, name, path):
     res = hosts_engine.aggregate(batch, cat, FilterParams(*G.params(z)), histograms=True)
     want = G.hosts_expected(name)
     G.assert_hosts_equal(host_dict(res), want)
+    rows, bks, cnt = hosts_engine.host_histogram_entries()  # sparse form of the same histograms
+    np.testing.assert_array_equal(rows, want["hist_row"])
+    np.testing.assert_array_equal(bks, want["hist_bucket"])
+    np.testing.assert_array_equal(cnt, want["hist_count"])
     # SiteResult.hosts view: every present site holds exactly its rows.
     n_rows = sum(len(sr.hosts) for sr in res.sites.values())
     assert n_rows == want["n"]
@@ -240,3 +244,8 @@ def test_gpu_hosts_large_properties(hosts_engine):
     want = [int(b) << 64 | int(a) for a, b in zip(st["rate_ubps_lo"], st["rate_ubps_hi"])]
     assert lo == want
     assert np.all((t["median_bps"] >= t["min_bps"]) & (t["median_bps"] <= t["max_bps"]))
+    rows, bks, c = hosts_engine.host_histogram_entries()  # 64-bit keys: sparse histograms sum to the counts
+    per_row = np.zeros(len(t), np.uint64)
+    np.add.at(per_row, rows, c)
+    np.testing.assert_array_equal(per_row, t["flow_count"])
+    assert np.all(bks <= 10000)
