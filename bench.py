@@ -45,8 +45,8 @@ METRIC = "flow records/sec analysed"
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="gnetmon", choices=["gnetmon", "reference"])
     ap.add_argument("--workload", default="D3")
     ap.add_argument("--records", type=int, default=None, help="records per GPU (default: workload)")
@@ -277,7 +277,8 @@ def run_stream(args):
     lat = []
     analysed = 0
     clocks = ClockSampler(local)
-    clocks.start()
+    if not os.environ.get("GNM_BENCH_NO_CLOCKS"):  # diagnosis only: the line then has no clocks
+        clocks.start()
     t_all = time.perf_counter()
     for i in range(steps):
         b, lo, _ = ring[i % 16]
@@ -402,7 +403,8 @@ def main():
         return ms, t["kernel_launches"] - launches0, res, per
 
     clocks = ClockSampler(local)
-    clocks.start()
+    if not os.environ.get("GNM_BENCH_NO_CLOCKS"):  # diagnosis only: the line then has no clocks
+        clocks.start()
     ms, launches, res, per = timed(dev_batch, args.steps)
     clk = clocks.stop()
     e2e_steps = args.e2e_steps or max(3, args.steps // 2)

@@ -239,7 +239,7 @@ void ensure_partials(gnm_ctx* c, uint32_t n_sites) {
         ck(cudaMalloc(&c->P.msb, static_cast<size_t>(cap) * 4), "cudaMalloc(msb)");
         ck(cudaMalloc(&c->P.mrank, static_cast<size_t>(cap) * 4), "cudaMalloc(mrank)");
         ck(cudaMalloc(&c->P.cnt, static_cast<size_t>(cap) * 8), "cudaMalloc(cnt)");
-        ck(cudaMalloc(&c->P.heavy_next, 4), "cudaMalloc(heavy)");
+        ck(cudaMalloc(&c->P.heavy_next, 4 * (1 + 64)), "cudaMalloc(heavy)"); // counter, row -> site
         const size_t scratch_words = 2 * static_cast<size_t>(cap) + gnm::kHotStride + 1;
         ck(cudaMalloc(&c->d_scratch, scratch_words * 4), "cudaMalloc(scratch)");
         ck(cudaMemsetAsync(c->d_scratch, 0, scratch_words * 4, c->stream), "cudaMemsetAsync");

@@ -996,7 +996,10 @@ __global__ void __launch_bounds__(128) k3a_median_sb(DevPartials P) {
         uint32_t hidx = kHeavyNone;
         if (cnt >= kHeavyMin) {
             const uint32_t k = atomicAdd(P.heavy_next, 1u);
-            if (k < kHeavy) hidx = k;
+            if (k < kHeavy) {
+                hidx = k;
+                P.heavy_next[1 + k] = site; // heavy row -> site, for K2b's flush
+            }
         }
         P.msb[site] = msb | hidx << 8;
         P.mrank[site] = rank;
@@ -1016,7 +1019,6 @@ constexpr uint32_t kMapSites = 12288; // 24 KB of static shared memory
 template <bool kMap, bool kWide>
 __global__ void __launch_bounds__(512, 2) k2b_fine(DevPartials P, DevLog L) {
     __shared__ uint32_t hf[kHeavy * kFineW];
-    __shared__ uint32_t hsite[kHeavy];
     __shared__ uint16_t map[kMap ? kMapSites : 1];
     for (uint32_t i = threadIdx.x; i < kHeavy * kFineW; i += blockDim.x) hf[i] = 0;
     if constexpr (kMap)
@@ -1026,11 +1028,31 @@ __global__ void __launch_bounds__(512, 2) k2b_fine(DevPartials P, DevLog L) {
             map[i] = static_cast<uint16_t>((m & 0xFFu) | (hh == kHeavyNone ? 0xFF00u : hh << 8));
         }
     __syncthreads();
+    const uint32_t hf_base = static_cast<uint32_t>(__cvta_generic_to_shared(hf));
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     const uint32_t chunks = (L.warp_cap + kLogChunk - 1) / kLogChunk;
     const uint32_t items = L.regions * chunks;
     constexpr uint32_t kV = kWide ? 4 : 8; // LDG.128 per lane in flight
+    // One log entry: skip unless in its site's median super-bucket; heavy
+    // sites count in shared memory, the rest in L2.
+    auto one = [&](uint32_t site, uint32_t bk) {
+        uint32_t msb, hh;
+        if constexpr (kMap) {
+            const uint32_t m = map[site];
+            msb = m & 0xFFu;
+            hh = m >> 8;
+        } else {
+            const uint32_t m = __ldg(P.msb + site);
+            msb = m & 0xFFu;
+            hh = (m >> 8) == kHeavyNone ? 0xFFu : m >> 8;
+        }
+        if ((bk >> 6) != msb) return;
+        if (hh != 0xFFu)
+            asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hf_base + (hh * kFineW + (bk & 63u)) * 4) : "memory");
+        else
+            red_add(P.fine + static_cast<size_t>(site) * kFineW + (bk & 63u), 1u);
+    };
     for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < items; w += nwarps) {
         const uint32_t r = w / chunks;
         const uint32_t c0 = (w % chunks) * kLogChunk;
@@ -1054,35 +1076,25 @@ __global__ void __launch_bounds__(512, 2) k2b_fine(DevPartials P, DevLog L) {
                 if constexpr (kWide) {
                     bs[0] = bb[u].x, bs[1] = bb[u].y, bs[2] = bb[u].z, bs[3] = bb[u].w;
                 }
+                if (i + 4 <= cnt) { // whole vector valid: no per-entry bounds checks
 #pragma unroll
-                for (uint32_t q = 0; q < 4; ++q) {
-                    if (i + q >= cnt) continue;
-                    const uint32_t site = kWide ? xs[q] : xs[q] >> kLogSiteShift;
-                    const uint32_t bk = kWide ? bs[q] : xs[q] & ((1u << kLogSiteShift) - 1u);
-                    uint32_t msb, hh;
-                    if constexpr (kMap) {
-                        const uint32_t m = map[site];
-                        msb = m & 0xFFu;
-                        hh = m >> 8;
-                    } else {
-                        const uint32_t m = __ldg(P.msb + site);
-                        msb = m & 0xFFu;
-                        hh = (m >> 8) == kHeavyNone ? 0xFFu : m >> 8;
-                    }
-                    if ((bk >> 6) != msb) continue;
-                    if (hh != 0xFFu) {
-                        red_add_shared(hf + hh * kFineW + (bk & 63u), 1u);
-                        hsite[hh] = site; // every writer stores the same value
-                    } else {
-                        red_add(P.fine + static_cast<size_t>(site) * kFineW + (bk & 63u), 1u);
-                    }
+                    for (uint32_t q = 0; q < 4; ++q)
+                        one(kWide ? xs[q] : xs[q] >> kLogSiteShift,
+                            kWide ? bs[q] : xs[q] & ((1u << kLogSiteShift) - 1u));
+                } else {
+#pragma unroll
+                    for (uint32_t q = 0; q < 4; ++q)
+                        if (i + q < cnt)
+                            one(kWide ? xs[q] : xs[q] >> kLogSiteShift,
+                                kWide ? bs[q] : xs[q] & ((1u << kLogSiteShift) - 1u));
                 }
             }
         }
     }
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < kHeavy * kFineW; i += blockDim.x)
-        if (hf[i]) red_add(P.fine + static_cast<size_t>(hsite[i / kFineW]) * kFineW + (i % kFineW), hf[i]);
+    const uint32_t n_heavy = min(*P.heavy_next, kHeavy);
+    for (uint32_t i = threadIdx.x; i < n_heavy * kFineW; i += blockDim.x)
+        if (hf[i]) red_add(P.fine + static_cast<size_t>(P.heavy_next[1 + i / kFineW]) * kFineW + (i % kFineW), hf[i]);
 }
 
 // K3b, thread per site: count (coarse), the exact median bucket from the

@@ -83,7 +83,7 @@ struct DevPartials {
                               // empty) | K2b heavy-row index << 8 (0xFFFFFF: none)
     unsigned int* mrank;      // [n_sites]: rank of the lower median within it (1-based)
     unsigned long long* cnt;  // [n_sites]: flow count (K3a)
-    unsigned int* heavy_next; // K3a's heavy-row counter
+    unsigned int* heavy_next; // K3a's heavy-row counter, then the site of each heavy row
     uint32_t n_sites;
 };
 
