@@ -103,3 +103,32 @@ def test_analyze_archive_in_place(engine, ref, orc, on_device):
     parity.assert_matches_oracle(got, parity.oracle_reference(orc, cat, cols))
     same = engine.aggregate(FlowRecords(rows.reshape(-1)), cat, histograms=True)
     np.testing.assert_array_equal(got.table, same.table)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("on_device", [False, True])
+def test_analyze_archive_hosts_mode(engine, ref, orc, on_device):
+    """Per-host rows from the in-place archive path (K2 layout 4, hosts mode)
+    equal the oracle's SiteResult::hosts restatement on the same records."""
+    w, cols, rows = _rows(200_003, seed=5)
+    data = _archive(ref, rows)
+    cat = SiteCatalog()
+    w.sites.register(cat)
+    arg = data
+    if on_device:
+        import torch
+        arg = torch.from_numpy(np.frombuffer(data, np.uint8).copy()).cuda()
+    engine.set_hosts(True)
+    try:
+        got = engine.aggregate_archive(arg, cat)
+    finally:
+        engine.reset()
+        engine.set_hosts(False)
+    p, s = cat.entries_arrays()
+    want = orc.host_stats(cols, orc.catalog(p, s))
+    t = got.host_table
+    for k_got, k_want in (("site", "site"), ("host", "host"), ("flow_count", "count"),
+                          ("rate_ubps_lo", "ubps_lo"), ("rate_ubps_hi", "ubps_hi")):
+        np.testing.assert_array_equal(t[k_got].astype(np.uint64), want[k_want].astype(np.uint64), err_msg=k_got)
+    for k_got, k_want in (("min_bps", "min"), ("max_bps", "max"), ("avg_bps", "avg"), ("median_bps", "median")):
+        np.testing.assert_array_equal(t[k_got].view(np.uint64), want[k_want].view(np.uint64), err_msg=k_got)
