@@ -66,32 +66,23 @@ __device__ __forceinline__ uint32_t insert_key(unsigned long long* keys, uint32_
     }
 }
 
-// Sum of v over the lanes of `m` (the lanes sharing this lane's slot), a
-// tree over the group's ranks with full-warp shuffles; valid in the group's
-// lowest lane.
-template <typename T, typename Op>
-__device__ __forceinline__ T group_reduce(unsigned m, uint32_t lane, T v, Op op) {
-    const uint32_t rank = __popc(m & ((1u << lane) - 1u));
-#pragma unroll
-    for (uint32_t d = 1; d < 32; d <<= 1) {
-        const uint32_t partner = __fns(m, lane, static_cast<int>(d) + 1);
-        const T o = __shfl_sync(0xFFFFFFFFu, v, partner == 0xFFFFFFFFu ? lane : partner);
-        if (partner != 0xFFFFFFFFu && (rank & (2 * d - 1)) == 0) v = op(v, o);
-    }
-    return v;
-}
-
-// H1, warp per log region of one slice. acc[slot] = {limb0, limb1, limb2,
-// ~min bits, max bits} (zero-initialised: the min is kept complemented).
-// Heavy hosts would serialise on their slot's L2 atomics, so each warp first
-// folds its flows into a private shared-memory table of kAggSlots entries
-// (an entry belongs to the first slot hashed to it; a flow whose entry is
-// taken goes to L2 directly) and flushes it once at the end. Within a warp
-// one leader lane per slot updates the entry, so the updates need no atomics.
+// H1, warp per work item (region, chunk of kInsChunk entries); each lane
+// takes 4 consecutive entries per step (LDG.128 on the u32 columns) and the
+// four table probes are issued before any is resolved.
+// acc[slot] = {limb0, limb1, limb2, ~min bits, max bits} in L2 (zero at
+// start: the min is kept complemented). Heavy hosts would serialise on their
+// slot's L2 atomics, so each CTA folds flows into a shared table of kAgg
+// entries first (an entry belongs to the first slot hashed to it; a flow
+// whose entry is taken goes to L2 directly). An entry keeps the micro-bps
+// as four 16-bit limbs in u32 counters (native shared atomics); the thread
+// whose add reaches kFlushAt moves the limbs to L2 with atomic exchanges, so
+// no counter can wrap. Cached per-entry min/max filter the L2 min/max
+// reductions (a stale cache only costs an extra reduction).
 constexpr uint32_t kInsBlock = 256;
-constexpr uint32_t kInsWarps = kInsBlock / 32;
-constexpr uint32_t kAggSlots = 128;
-constexpr size_t kInsSmem = kInsWarps * kAggSlots * (4 + 5 * 8); // 44 KB
+constexpr uint32_t kAgg = 1024;
+constexpr uint32_t kFlushAt = 1u << 15;
+constexpr size_t kInsSmem = kAgg * (4 + 4 + 4 * 4 + 8 + 8); // 40 KB
+constexpr uint32_t kInsChunk = 2048;
 
 __device__ __forceinline__ void red_u64(unsigned long long* p, unsigned long long v) {
     asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -100,72 +91,77 @@ __device__ __forceinline__ void red_max_u64(unsigned long long* p, unsigned long
     asm volatile("red.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// One slot's partial into the L2 accumulators: fire-and-forget reductions
-// (no read round trip on the issuing warp's critical path).
-__device__ __forceinline__ void acc_flush(unsigned long long* a, unsigned long long l0, unsigned long long l1,
-                                          unsigned long long l2, unsigned long long nmn, unsigned long long mx) {
-    red_u64(a + 0, l0);
-    red_u64(a + 1, l1);
-    if (l2) red_u64(a + 2, l2);
-    red_max_u64(a + 3, nmn);
-    red_max_u64(a + 4, mx);
+struct AggSmem {
+    unsigned long long* mn; // cached min rate bits (~0: none)
+    unsigned long long* mx; // cached max rate bits
+    uint32_t* key;
+    uint32_t* cnt;
+    uint32_t* limb; // [4][kAgg]
+};
+
+__device__ __forceinline__ void agg_flush(const AggSmem& t, uint32_t e, unsigned long long* a) {
+    const uint32_t x0 = atomicExch(t.limb + e, 0u), x1 = atomicExch(t.limb + kAgg + e, 0u);
+    const uint32_t x2 = atomicExch(t.limb + 2 * kAgg + e, 0u), x3 = atomicExch(t.limb + 3 * kAgg + e, 0u);
+    red_u64(a + 0, static_cast<unsigned long long>(x0) + (static_cast<unsigned long long>(x1) << 16));
+    red_u64(a + 1, static_cast<unsigned long long>(x2) + (static_cast<unsigned long long>(x3) << 16));
 }
 
-// One flow's contribution, folded into the warp's private table (leader
-// lanes only: one per distinct slot among the warp's 32 flows) or L2.
-__device__ __forceinline__ void fold(uint32_t slot, bool in, unsigned long long lo, unsigned long long hi,
-                                     unsigned long long rate, uint32_t lane, uint32_t* skey,
-                                     unsigned long long* sacc, unsigned long long* acc) {
-    const unsigned m = __match_any_sync(0xFFFFFFFFu, slot);
-    unsigned long long l0 = lo & 0xFFFFFFFFull, l1 = lo >> 32, l2 = hi, mn = rate, mx = rate;
-    if (__any_sync(0xFFFFFFFFu, in && (m & ~(1u << lane)) != 0)) { // some slot repeats in this warp
-        l0 = group_reduce(m, lane, l0, [](auto a, auto b) { return a + b; });
-        l1 = group_reduce(m, lane, l1, [](auto a, auto b) { return a + b; });
-        l2 = group_reduce(m, lane, l2, [](auto a, auto b) { return a + b; });
-        mn = group_reduce(m, lane, mn, [](auto a, auto b) { return a < b ? a : b; });
-        mx = group_reduce(m, lane, mx, [](auto a, auto b) { return a < b ? b : a; });
-    }
-    if (in && lane == static_cast<uint32_t>(__ffs(m) - 1)) {
-        const uint32_t h = (slot * 2654435761u) >> (32 - 7);
-        uint32_t cur = skey[h];
-        if (cur == 0xFFFFFFFFu) cur = atomicCAS(skey + h, 0xFFFFFFFFu, slot); // leaders of other slots race
-        if (cur == 0xFFFFFFFFu || cur == slot) {
-            unsigned long long* e = sacc + h * 5;
-            e[0] += l0;
-            e[1] += l1;
-            e[2] += l2;
-            e[3] = e[3] > ~mn ? e[3] : ~mn;
-            e[4] = e[4] > mx ? e[4] : mx;
-        } else {
-            acc_flush(acc + static_cast<size_t>(slot) * 5, l0, l1, l2, ~mn, mx);
+// One flow's contribution (any lane, no warp-level grouping).
+__device__ __forceinline__ void fold(uint32_t slot, unsigned long long lo, uint32_t hi, unsigned long long rate,
+                                     const AggSmem& t, unsigned long long* acc) {
+    unsigned long long* a = acc + static_cast<size_t>(slot) * 5;
+    if (hi) red_u64(a + 2, hi); // micro-bps >= 2^64: rare
+    const uint32_t e = (slot * 2654435761u) >> (32 - 10);
+    uint32_t cur = t.key[e];
+    if (cur == 0xFFFFFFFFu) cur = atomicCAS(t.key + e, 0xFFFFFFFFu, slot);
+    if (cur == 0xFFFFFFFFu || cur == slot) {
+        atomicAdd(t.limb + e, static_cast<uint32_t>(lo) & 0xFFFFu);
+        atomicAdd(t.limb + kAgg + e, static_cast<uint32_t>(lo) >> 16);
+        atomicAdd(t.limb + 2 * kAgg + e, static_cast<uint32_t>(lo >> 32) & 0xFFFFu);
+        atomicAdd(t.limb + 3 * kAgg + e, static_cast<uint32_t>(lo >> 48));
+        if (rate < t.mn[e]) {
+            red_max_u64(a + 3, ~rate);
+            t.mn[e] = rate;
         }
+        if (rate > t.mx[e]) {
+            red_max_u64(a + 4, rate);
+            t.mx[e] = rate;
+        }
+        if (atomicAdd(t.cnt + e, 1u) + 1u == kFlushAt) {
+            agg_flush(t, e, a);
+            atomicSub(t.cnt + e, kFlushAt);
+        }
+    } else {
+        red_u64(a + 0, lo & 0xFFFFFFFFull);
+        red_u64(a + 1, lo >> 32);
+        red_max_u64(a + 3, ~rate);
+        red_max_u64(a + 4, rate);
     }
-    __syncwarp();
 }
 
-// Work item = (region, chunk of kLogChunk entries); each lane takes 4
-// consecutive entries per step (LDG.128 on the u32 columns), and the four
-// table probes are issued before any is resolved.
-constexpr uint32_t kInsChunk = 2048;
-
-__global__ void __launch_bounds__(kInsBlock, 3) h_insert(DevLog L, const unsigned int* __restrict__ counts,
+__global__ void __launch_bounds__(kInsBlock, 4) h_insert(DevLog L, const unsigned int* __restrict__ counts,
                                                          const uint32_t* __restrict__ off,
                                                          unsigned long long* keys, uint32_t mask, int shift,
                                                          unsigned long long* __restrict__ acc,
                                                          uint32_t* __restrict__ slot_of,
                                                          uint32_t* __restrict__ bk) {
     extern __shared__ __align__(16) unsigned char h_smem[];
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t warp = threadIdx.x >> 5;
-    unsigned long long* sacc = reinterpret_cast<unsigned long long*>(h_smem) + warp * kAggSlots * 5;
-    uint32_t* skey = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned long long*>(h_smem) +
-                                                 kInsWarps * kAggSlots * 5) + warp * kAggSlots;
-    for (uint32_t i = lane; i < kAggSlots; i += 32) {
-        skey[i] = 0xFFFFFFFFu;
+    AggSmem t;
+    t.mn = reinterpret_cast<unsigned long long*>(h_smem);
+    t.mx = t.mn + kAgg;
+    t.key = reinterpret_cast<uint32_t*>(t.mx + kAgg);
+    t.cnt = t.key + kAgg;
+    t.limb = t.cnt + kAgg;
+    for (uint32_t i = threadIdx.x; i < kAgg; i += blockDim.x) {
+        t.mn[i] = ~0ull;
+        t.mx[i] = 0;
+        t.key[i] = 0xFFFFFFFFu;
+        t.cnt[i] = 0;
 #pragma unroll
-        for (int f = 0; f < 5; ++f) sacc[i * 5 + f] = 0;
+        for (int f = 0; f < 4; ++f) t.limb[f * kAgg + i] = 0;
     }
-    __syncwarp();
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31u;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     const uint32_t chunks = (L.warp_cap + kInsChunk - 1) / kInsChunk;
     const uint32_t items = L.regions * chunks;
@@ -175,21 +171,16 @@ __global__ void __launch_bounds__(kInsBlock, 3) h_insert(DevLog L, const unsigne
         const uint32_t n = min(counts[r], c0 + kInsChunk);
         const uint32_t base = off[r];
         const size_t rb = static_cast<size_t>(r) * L.warp_cap;
-        for (uint32_t i0 = c0; i0 < n; i0 += 128) { // warp-uniform trip count
-            const uint32_t i = i0 + lane * 4;
+        for (uint32_t i = c0 + lane * 4; i < n; i += 128) {
             const size_t pos = rb + i;
-            uint4 x = make_uint4(0, 0, 0, 0), hst = x, bb = x, uh = x;
-            ulonglong2 lo01{}, lo23{}, rt01{}, rt23{};
-            if (i < n) {
-                x = __ldcs(reinterpret_cast<const uint4*>(L.entries + pos));
-                hst = __ldcs(reinterpret_cast<const uint4*>(L.hosts + pos));
-                if (L.buckets) bb = __ldcs(reinterpret_cast<const uint4*>(L.buckets + pos));
-                uh = __ldcs(reinterpret_cast<const uint4*>(L.uhi + pos));
-                lo01 = __ldcs(reinterpret_cast<const ulonglong2*>(L.ulo + pos));
-                lo23 = __ldcs(reinterpret_cast<const ulonglong2*>(L.ulo + pos + 2));
-                rt01 = __ldcs(reinterpret_cast<const ulonglong2*>(L.rates + pos));
-                rt23 = __ldcs(reinterpret_cast<const ulonglong2*>(L.rates + pos + 2));
-            }
+            const uint4 x = __ldcs(reinterpret_cast<const uint4*>(L.entries + pos));
+            const uint4 hst = __ldcs(reinterpret_cast<const uint4*>(L.hosts + pos));
+            const uint4 bb = L.buckets ? __ldcs(reinterpret_cast<const uint4*>(L.buckets + pos)) : make_uint4(0, 0, 0, 0);
+            const uint4 uh = __ldcs(reinterpret_cast<const uint4*>(L.uhi + pos));
+            const ulonglong2 lo01 = __ldcs(reinterpret_cast<const ulonglong2*>(L.ulo + pos));
+            const ulonglong2 lo23 = __ldcs(reinterpret_cast<const ulonglong2*>(L.ulo + pos + 2));
+            const ulonglong2 rt01 = __ldcs(reinterpret_cast<const ulonglong2*>(L.rates + pos));
+            const ulonglong2 rt23 = __ldcs(reinterpret_cast<const ulonglong2*>(L.rates + pos + 2));
             const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, hs[4] = {hst.x, hst.y, hst.z, hst.w};
             const uint32_t bs[4] = {bb.x, bb.y, bb.z, bb.w}, us[4] = {uh.x, uh.y, uh.z, uh.w};
             const unsigned long long los[4] = {lo01.x, lo01.y, lo23.x, lo23.y};
@@ -205,22 +196,21 @@ __global__ void __launch_bounds__(kInsBlock, 3) h_insert(DevLog L, const unsigne
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const bool in = i + q < n;
-                uint32_t slot = 0xFFFFFFFFu;
-                if (in) {
-                    slot = first[q] == key[q] ? h0[q] : insert_key(keys, mask, shift, key[q]);
-                    slot_of[base + i + q] = slot;
-                    bk[base + i + q] = L.buckets ? bs[q] : xs[q] & kBucketMask;
-                }
-                fold(slot, in, los[q], us[q], rts[q], lane, skey, sacc, acc);
+                if (i + q >= n) break;
+                const uint32_t slot = first[q] == key[q] ? h0[q] : insert_key(keys, mask, shift, key[q]);
+                slot_of[base + i + q] = slot;
+                bk[base + i + q] = L.buckets ? bs[q] : xs[q] & kBucketMask;
+                fold(slot, los[q], us[q], rts[q], t, acc);
             }
         }
     }
-    for (uint32_t i = lane; i < kAggSlots; i += 32) {
-        const uint32_t slot = skey[i];
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < kAgg; e += blockDim.x) {
+        const uint32_t slot = t.key[e];
         if (slot == 0xFFFFFFFFu) continue;
-        const unsigned long long* e = sacc + i * 5;
-        acc_flush(acc + static_cast<size_t>(slot) * 5, e[0], e[1], e[2], e[3], e[4]);
+        unsigned long long* a = acc + static_cast<size_t>(slot) * 5;
+        agg_flush(t, e, a);
+        // the cached bounds were reduced into L2 when they were set
     }
 }
 
@@ -412,9 +402,9 @@ cudaError_t build_hosts(int device, const HostSlice* slices, int n_slices,
     HCK(cudaMemsetAsync(acc, 0, static_cast<size_t>(cap) * 40, s));
     for (int i = 0; i < n_slices; ++i) {
         const HostSlice& sl = slices[i];
-        // Three CTAs per SM (80 registers), fewer for small logs.
+        // Four CTAs per SM, fewer for small logs.
         const uint64_t items = static_cast<uint64_t>(sl.log.regions) * ((sl.log.warp_cap + kInsChunk - 1) / kInsChunk);
-        const uint32_t g = std::min<uint32_t>(grid_for(device, items * 32, kInsBlock), 3 * sms);
+        const uint32_t g = std::min<uint32_t>(grid_for(device, items * 32, kInsBlock), 4 * sms);
         h_insert<<<g, kInsBlock, kInsSmem, s>>>(sl.log, counts + sl.count_off, off + sl.count_off, keys, cap - 1,
                                                 64 - tbits, acc, slot_of, bk);
         HCK(cudaGetLastError());
