@@ -73,15 +73,15 @@ __device__ __forceinline__ uint32_t insert_key(unsigned long long* keys, uint32_
 // start: the min is kept complemented). Heavy hosts would serialise on their
 // slot's L2 atomics, so each CTA folds flows into a shared table of kAgg
 // entries first (an entry belongs to the first slot hashed to it; a flow
-// whose entry is taken goes to L2 directly). An entry keeps the micro-bps
-// as four 16-bit limbs in u32 counters (native shared atomics); the thread
-// whose add reaches kFlushAt moves the limbs to L2 with atomic exchanges, so
-// no counter can wrap. Cached per-entry min/max filter the L2 min/max
-// reductions (a stale cache only costs an extra reduction).
+// whose entry is taken goes to L2 directly). An entry keeps micro-bps below
+// 2^48 as three 16-bit limbs in u32 counters (native shared atomics); the
+// thread whose add reaches kFlushAt moves the limbs to L2 with atomic
+// exchanges, so no counter can wrap. Per-entry f32 bounds (rounded outward)
+// filter the L2 min/max reductions: a stale bound only costs an extra one.
 constexpr uint32_t kInsBlock = 256;
-constexpr uint32_t kAgg = 1024;
+constexpr uint32_t kAgg = 2048;
 constexpr uint32_t kFlushAt = 1u << 15;
-constexpr size_t kInsSmem = kAgg * (4 + 4 + 4 * 4 + 8 + 8); // 40 KB
+constexpr size_t kInsSmem = kAgg * (4 + 4 + 3 * 4 + 4 + 4); // 48 KB
 constexpr uint32_t kInsChunk = 2048;
 
 __device__ __forceinline__ void red_u64(unsigned long long* p, unsigned long long v) {
@@ -92,40 +92,39 @@ __device__ __forceinline__ void red_max_u64(unsigned long long* p, unsigned long
 }
 
 struct AggSmem {
-    unsigned long long* mn; // cached min rate bits (~0: none)
-    unsigned long long* mx; // cached max rate bits
+    float* mn; // >= the smallest rate this CTA reduced into L2 for the entry (+inf: none)
+    float* mx; // <= the largest
     uint32_t* key;
     uint32_t* cnt;
-    uint32_t* limb; // [4][kAgg]
+    uint32_t* limb; // [3][kAgg]
 };
 
 __device__ __forceinline__ void agg_flush(const AggSmem& t, uint32_t e, unsigned long long* a) {
     const uint32_t x0 = atomicExch(t.limb + e, 0u), x1 = atomicExch(t.limb + kAgg + e, 0u);
-    const uint32_t x2 = atomicExch(t.limb + 2 * kAgg + e, 0u), x3 = atomicExch(t.limb + 3 * kAgg + e, 0u);
+    const uint32_t x2 = atomicExch(t.limb + 2 * kAgg + e, 0u);
     red_u64(a + 0, static_cast<unsigned long long>(x0) + (static_cast<unsigned long long>(x1) << 16));
-    red_u64(a + 1, static_cast<unsigned long long>(x2) + (static_cast<unsigned long long>(x3) << 16));
+    if (x2) red_u64(a + 1, x2);
 }
 
 // One flow's contribution (any lane, no warp-level grouping).
 __device__ __forceinline__ void fold(uint32_t slot, unsigned long long lo, uint32_t hi, unsigned long long rate,
                                      const AggSmem& t, unsigned long long* acc) {
     unsigned long long* a = acc + static_cast<size_t>(slot) * 5;
-    if (hi) red_u64(a + 2, hi); // micro-bps >= 2^64: rare
-    const uint32_t e = (slot * 2654435761u) >> (32 - 10);
+    const uint32_t e = (slot * 2654435761u) >> (32 - 11);
     uint32_t cur = t.key[e];
     if (cur == 0xFFFFFFFFu) cur = atomicCAS(t.key + e, 0xFFFFFFFFu, slot);
-    if (cur == 0xFFFFFFFFu || cur == slot) {
+    if ((cur == 0xFFFFFFFFu || cur == slot) && hi == 0 && lo < (1ull << 48)) {
         atomicAdd(t.limb + e, static_cast<uint32_t>(lo) & 0xFFFFu);
         atomicAdd(t.limb + kAgg + e, static_cast<uint32_t>(lo) >> 16);
-        atomicAdd(t.limb + 2 * kAgg + e, static_cast<uint32_t>(lo >> 32) & 0xFFFFu);
-        atomicAdd(t.limb + 3 * kAgg + e, static_cast<uint32_t>(lo >> 48));
-        if (rate < t.mn[e]) {
+        atomicAdd(t.limb + 2 * kAgg + e, static_cast<uint32_t>(lo >> 32));
+        const double r = __longlong_as_double(static_cast<long long>(rate));
+        if (r < static_cast<double>(t.mn[e])) {
             red_max_u64(a + 3, ~rate);
-            t.mn[e] = rate;
+            t.mn[e] = __double2float_ru(r);
         }
-        if (rate > t.mx[e]) {
+        if (r > static_cast<double>(t.mx[e])) {
             red_max_u64(a + 4, rate);
-            t.mx[e] = rate;
+            t.mx[e] = __double2float_rd(r);
         }
         if (atomicAdd(t.cnt + e, 1u) + 1u == kFlushAt) {
             agg_flush(t, e, a);
@@ -134,6 +133,7 @@ __device__ __forceinline__ void fold(uint32_t slot, unsigned long long lo, uint3
     } else {
         red_u64(a + 0, lo & 0xFFFFFFFFull);
         red_u64(a + 1, lo >> 32);
+        if (hi) red_u64(a + 2, hi); // micro-bps >= 2^64: rare
         red_max_u64(a + 3, ~rate);
         red_max_u64(a + 4, rate);
     }
@@ -147,18 +147,18 @@ __global__ void __launch_bounds__(kInsBlock, 4) h_insert(DevLog L, const unsigne
                                                          uint32_t* __restrict__ bk) {
     extern __shared__ __align__(16) unsigned char h_smem[];
     AggSmem t;
-    t.mn = reinterpret_cast<unsigned long long*>(h_smem);
+    t.mn = reinterpret_cast<float*>(h_smem);
     t.mx = t.mn + kAgg;
     t.key = reinterpret_cast<uint32_t*>(t.mx + kAgg);
     t.cnt = t.key + kAgg;
     t.limb = t.cnt + kAgg;
     for (uint32_t i = threadIdx.x; i < kAgg; i += blockDim.x) {
-        t.mn[i] = ~0ull;
-        t.mx[i] = 0;
+        t.mn[i] = __int_as_float(0x7F800000); // +inf
+        t.mx[i] = 0.0f;
         t.key[i] = 0xFFFFFFFFu;
         t.cnt[i] = 0;
 #pragma unroll
-        for (int f = 0; f < 4; ++f) t.limb[f * kAgg + i] = 0;
+        for (int f = 0; f < 3; ++f) t.limb[f * kAgg + i] = 0;
     }
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31u;
