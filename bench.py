@@ -54,6 +54,9 @@ def parse_args():
     ap.add_argument("--cpu-sample", type=int, default=2_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--hot-mode", default="auto", choices=["auto", "off", "force"])
+    ap.add_argument("--input", default="soa", choices=["soa", "aos"],
+                    help="record layout handed to the API: SoA columns (default, the north star's "
+                         "loader layout) or the reference's 64-byte FlowRecord rows (gnm_analyze_aos)")
     ap.add_argument("--hosts", action="store_true",
                     help="per-host mode: every step also builds SiteResult::hosts (N=1 only)")
     return ap.parse_args()
@@ -328,7 +331,7 @@ def main():
 
     import torch
     import torch.distributed as dist
-    from paper_1108_1785_b200 import Engine, FlowBatch, SiteCatalog, synth
+    from paper_1108_1785_b200 import Engine, FlowBatch, FlowRecords, SiteCatalog, synth
     from paper_1108_1785_b200 import distributed as D
 
     world, rank, local = dist_env()
@@ -348,6 +351,16 @@ def main():
     torch.cuda.synchronize()
     dev_batch = FlowBatch(*dev_t)
     host_batch = FlowBatch(*host)
+    if args.input == "aos":
+        # The reference's own span<const FlowRecord> layout: 64 B rows, pinned.
+        rows_t = torch.empty(n * 64, dtype=torch.uint8).pin_memory()
+        rows = rows_t.numpy()
+        synth._lib().gnm_synth_to_aos(n, *[c.ctypes.data for c in host], rows.ctypes.data)
+        del dev_t, dev_batch
+        dev_rows = rows_t.to(f"cuda:{local}")
+        torch.cuda.synchronize()
+        dev_batch = FlowRecords(dev_rows)
+        host_batch = FlowRecords(rows)
 
     eng = Engine(local)
     eng.set_hot_mode(args.hot_mode)
@@ -416,7 +429,7 @@ def main():
     k2_avg, plan_avg, k3_avg = per["k2"], per["k1_plan"], per["k3_finalize"]
     peak, peak_kind = load_peaks()
     achieved = n * ALG_BYTES_PER_RECORD / (k2_avg / 1e3) / 1e9
-    traffic = load_traffic(args.workload)
+    traffic = load_traffic(args.workload) if args.input == "soa" else None
     n_sites = cat.site_count()
     d2h = (n_sites + 1) * 72
     if args.hosts:
@@ -434,19 +447,21 @@ def main():
         "dtype": "u32/u64 int + f64", "data": "synthetic",
         "config": {"workload": f"{w.name}: {n} records/GPU, {n_sites} /24 sites, Zipf s={w.zipf_s}, "
                                f"8 hosts/site, 40% forward",
-                   "records_per_gpu": n, "sites": n_sites,
+                   "records_per_gpu": n, "sites": n_sites, "input": args.input,
                    "hosts": (f"per-host rows built every step ({len(res.host_table)} rows)" if args.hosts
                              else "site level only (gnm_ctx_set_hosts off)"), "parallelism": f"index shards x{world}",
                    "l2": "inputs 3.2 GB/GPU > 126 MB L2; no flush needed" if n >= 10_000_000
                          else "inputs may fit L2"},
         "e2e": {"value": e2e_value, "unit": "records/s",
-                "h2d_bytes_per_step": n * ALG_BYTES_PER_RECORD, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e2e_ms / e2e_steps, "source": "pinned host SoA, chunked double-buffered H2D"},
+                "h2d_bytes_per_step": n * (ALG_BYTES_PER_RECORD if args.input == "soa" else 64),
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / e2e_steps,
+                "source": f"pinned host {args.input.upper()}, chunked double-buffered H2D"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_kind": peak_kind,
                      "traffic": traffic["bytes_per_launch"] if traffic else None,
                      "kernel": "k2_soa (classify+attribute+rate+aggregate)",
-                     "kernel_ms": k2_avg, "alg_bytes_per_record": ALG_BYTES_PER_RECORD},
+                     "kernel_ms": k2_avg, "alg_bytes_per_record": ALG_BYTES_PER_RECORD,
+                     "physical_bytes_per_record": ALG_BYTES_PER_RECORD if args.input == "soa" else 64},
         "gpu_launches": launches,
         "clocks": clk,
         "kernel_share": k2_avg / (ms / args.steps),

@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <vector>
 
 #include "hosts.cuh"
 
@@ -318,35 +319,51 @@ cudaError_t dalloc(T** p, size_t n, cudaStream_t s) {
     return cudaMallocAsync(reinterpret_cast<void**>(p), std::max<size_t>(n, 1) * sizeof(T), s);
 }
 
+// Stream-ordered temporaries released when the scope ends, on every path.
+struct Scratch {
+    cudaStream_t s;
+    std::vector<void*> held;
+    explicit Scratch(cudaStream_t st) : s(st) {}
+    Scratch(const Scratch&) = delete;
+    Scratch& operator=(const Scratch&) = delete;
+    ~Scratch() {
+        for (void* q : held) cudaFreeAsync(q, s);
+    }
+    template <typename T>
+    cudaError_t get(T** p, size_t n) {
+        const cudaError_t e = dalloc(p, n, s);
+        if (e == cudaSuccess) held.push_back(*p);
+        return e;
+    }
+};
+
 // H3..H5 for one key width.
 template <typename K>
 cudaError_t sort_and_finish(int device, uint32_t n, uint32_t n_rows, const uint32_t* slot_of, const uint32_t* bk,
                             const unsigned long long* rank_tab, const unsigned long long* acc,
                             const unsigned long long* hk_sorted, const uint32_t* hs_sorted, HostRows& out,
                             cudaStream_t s) {
+    Scratch tmp_(s);
     K *sk = nullptr, *sk2 = nullptr;
-    HCK(dalloc(&sk, n, s));
+    HCK(tmp_.get(&sk, n));
     HCK(dalloc(&sk2, n, s));
+    out.sorted = sk2; // owned by `out` from here (free_hosts)
     h_keys<K><<<grid_for(device, n, 256), 256, 0, s>>>(slot_of, bk, n, rank_tab, sk);
     HCK(cudaGetLastError());
     const int end_bit = static_cast<int>(kBucketBits) + std::max(1, bits_for(n_rows));
     size_t tb = 0;
     HCK(cub::DeviceRadixSort::SortKeys(nullptr, tb, sk, sk2, n, 0, end_bit, s));
-    void* tmp = nullptr;
-    HCK(cudaMallocAsync(&tmp, std::max<size_t>(tb, 1), s));
+    unsigned char* tmp = nullptr;
+    HCK(tmp_.get(&tmp, tb));
     HCK(cub::DeviceRadixSort::SortKeys(tmp, tb, sk, sk2, n, 0, end_bit, s));
-    HCK(cudaFreeAsync(tmp, s));
-    HCK(cudaFreeAsync(sk, s));
     uint32_t* start = nullptr;
-    HCK(dalloc(&start, static_cast<size_t>(n_rows) + 1, s));
+    HCK(tmp_.get(&start, static_cast<size_t>(n_rows) + 1));
     h_starts<K><<<grid_for(device, n, 256), 256, 0, s>>>(sk2, n, n_rows, start);
     HCK(cudaGetLastError());
     HCK(dalloc(&out.rows, n_rows, s));
     h_final<K><<<grid_for(device, n_rows, 128), 128, 0, s>>>(acc, start, sk2, hk_sorted, hs_sorted, n_rows,
                                                              out.rows);
     HCK(cudaGetLastError());
-    HCK(cudaFreeAsync(start, s));
-    out.sorted = sk2;
     out.key64 = sizeof(K) == 8;
     out.n_rows = n_rows;
     out.n_flows = n;
@@ -360,33 +377,25 @@ cudaError_t build_hosts(int device, const HostSlice* slices, int n_slices,
                         cudaStream_t s) {
     free_hosts(out, s);
     if (n_counts == 0) return cudaSuccess;
+    Scratch tmp_(s);
     // H0: flat offsets of every warp region's entries.
     uint32_t* off = nullptr;
     unsigned long long* scal = nullptr; // [0] total flows, [1] distinct keys
-    HCK(dalloc(&off, n_counts, s));
-    HCK(dalloc(&scal, 2, s));
+    HCK(tmp_.get(&off, n_counts));
+    HCK(tmp_.get(&scal, 2));
     size_t tb = 0;
     HCK(cub::DeviceScan::ExclusiveSum(nullptr, tb, counts, off, n_counts, s));
-    void* tmp = nullptr;
-    HCK(cudaMallocAsync(&tmp, std::max<size_t>(tb, 1), s));
+    unsigned char* tmp = nullptr;
+    HCK(tmp_.get(&tmp, tb));
     HCK(cub::DeviceScan::ExclusiveSum(tmp, tb, counts, off, n_counts, s));
-    HCK(cudaFreeAsync(tmp, s));
     HCK(cudaMemsetAsync(scal, 0, 16, s));
     h_total<<<1, 1, 0, s>>>(counts, off, n_counts, scal);
     unsigned long long h_scal[2] = {0, 0};
     HCK(cudaMemcpyAsync(h_scal, scal, 8, cudaMemcpyDeviceToHost, s));
     HCK(cudaStreamSynchronize(s));
     const uint64_t n = h_scal[0];
-    if (n == 0) {
-        HCK(cudaFreeAsync(off, s));
-        HCK(cudaFreeAsync(scal, s));
-        return cudaSuccess;
-    }
-    static bool attr = false;
-    if (!attr) {
-        HCK(cudaFuncSetAttribute(h_insert, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kInsSmem)));
-        attr = true;
-    }
+    if (n == 0) return cudaSuccess;
+    HCK(cudaFuncSetAttribute(h_insert, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kInsSmem)));
     int sms = 0;
     HCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     // H1: at least two slots per possible key.
@@ -394,10 +403,10 @@ cudaError_t build_hosts(int device, const HostSlice* slices, int n_slices,
     const uint32_t cap = 1u << tbits;
     unsigned long long *keys = nullptr, *acc = nullptr;
     uint32_t *slot_of = nullptr, *bk = nullptr;
-    HCK(dalloc(&keys, cap, s));
-    HCK(dalloc(&acc, static_cast<size_t>(cap) * 5, s));
-    HCK(dalloc(&slot_of, n, s));
-    HCK(dalloc(&bk, n, s));
+    HCK(tmp_.get(&keys, cap));
+    HCK(tmp_.get(&acc, static_cast<size_t>(cap) * 5));
+    HCK(tmp_.get(&slot_of, n));
+    HCK(tmp_.get(&bk, n));
     HCK(cudaMemsetAsync(keys, 0xFF, static_cast<size_t>(cap) * 8, s));
     HCK(cudaMemsetAsync(acc, 0, static_cast<size_t>(cap) * 40, s));
     for (int i = 0; i < n_slices; ++i) {
@@ -413,36 +422,29 @@ cudaError_t build_hosts(int device, const HostSlice* slices, int n_slices,
     unsigned long long *hk = nullptr, *hk_sorted = nullptr;
     uint32_t *hs = nullptr, *hs_sorted = nullptr;
     const uint64_t kcap = std::min<uint64_t>(n, cap);
-    HCK(dalloc(&hk, kcap, s));
-    HCK(dalloc(&hs, kcap, s));
+    HCK(tmp_.get(&hk, kcap));
+    HCK(tmp_.get(&hs, kcap));
     h_collect<<<grid_for(device, cap, 256), 256, 0, s>>>(keys, cap, hk, hs,
                                                         reinterpret_cast<unsigned int*>(scal + 1));
     HCK(cudaGetLastError());
     HCK(cudaMemcpyAsync(h_scal + 1, scal + 1, 8, cudaMemcpyDeviceToHost, s));
     HCK(cudaStreamSynchronize(s));
     const uint32_t n_rows = static_cast<uint32_t>(h_scal[1]);
-    HCK(dalloc(&hk_sorted, n_rows, s));
-    HCK(dalloc(&hs_sorted, n_rows, s));
+    HCK(tmp_.get(&hk_sorted, n_rows));
+    HCK(tmp_.get(&hs_sorted, n_rows));
     tb = 0;
     HCK(cub::DeviceRadixSort::SortPairs(nullptr, tb, hk, hk_sorted, hs, hs_sorted, n_rows, 0, 64, s));
-    HCK(cudaMallocAsync(&tmp, std::max<size_t>(tb, 1), s));
-    HCK(cub::DeviceRadixSort::SortPairs(tmp, tb, hk, hk_sorted, hs, hs_sorted, n_rows, 0, 64, s));
-    HCK(cudaFreeAsync(tmp, s));
+    unsigned char* tmp2 = nullptr;
+    HCK(tmp_.get(&tmp2, tb));
+    HCK(cub::DeviceRadixSort::SortPairs(tmp2, tb, hk, hk_sorted, hs, hs_sorted, n_rows, 0, 64, s));
     h_rank<<<grid_for(device, n_rows, 256), 256, 0, s>>>(hs_sorted, n_rows, keys);
     HCK(cudaGetLastError());
     // H3..H5.
     const uint32_t n32 = static_cast<uint32_t>(n);
     if (kBucketBits + bits_for(n_rows) <= 32)
-        HCK(sort_and_finish<uint32_t>(device, n32, n_rows, slot_of, bk, keys, acc, hk_sorted, hs_sorted, out, s));
-    else
-        HCK(sort_and_finish<unsigned long long>(device, n32, n_rows, slot_of, bk, keys, acc, hk_sorted, hs_sorted,
-                                                out, s));
-    for (void* p : {static_cast<void*>(off), static_cast<void*>(scal), static_cast<void*>(keys),
-                    static_cast<void*>(acc), static_cast<void*>(slot_of), static_cast<void*>(bk),
-                    static_cast<void*>(hk), static_cast<void*>(hs), static_cast<void*>(hk_sorted),
-                    static_cast<void*>(hs_sorted)})
-        HCK(cudaFreeAsync(p, s));
-    return cudaSuccess;
+        return sort_and_finish<uint32_t>(device, n32, n_rows, slot_of, bk, keys, acc, hk_sorted, hs_sorted, out, s);
+    return sort_and_finish<unsigned long long>(device, n32, n_rows, slot_of, bk, keys, acc, hk_sorted, hs_sorted,
+                                               out, s);
 }
 
 cudaError_t hosts_histograms(int device, const HostRows& h, uint32_t* dense, cudaStream_t s) {
@@ -460,22 +462,21 @@ namespace {
 template <typename K>
 cudaError_t rle(HostRows& h, cudaStream_t s) {
     const K* in = static_cast<const K*>(h.sorted);
+    Scratch tmp_(s);
     K* keys = nullptr;
     uint64_t* d_n = nullptr;
     HCK(dalloc(&keys, h.n_flows, s));
+    h.sp_keys = keys; // owned by `h` from here (free_hosts)
     HCK(dalloc(&h.sp_counts, h.n_flows, s));
-    HCK(dalloc(&d_n, 1, s));
+    HCK(tmp_.get(&d_n, 1));
     size_t tb = 0;
     HCK(cub::DeviceRunLengthEncode::Encode(nullptr, tb, in, keys, h.sp_counts, d_n, h.n_flows, s));
-    void* tmp = nullptr;
-    HCK(cudaMallocAsync(&tmp, std::max<size_t>(tb, 1), s));
+    unsigned char* tmp = nullptr;
+    HCK(tmp_.get(&tmp, tb));
     HCK(cub::DeviceRunLengthEncode::Encode(tmp, tb, in, keys, h.sp_counts, d_n, h.n_flows, s));
-    HCK(cudaFreeAsync(tmp, s));
     uint64_t n = 0;
     HCK(cudaMemcpyAsync(&n, d_n, 8, cudaMemcpyDeviceToHost, s));
-    HCK(cudaFreeAsync(d_n, s));
     HCK(cudaStreamSynchronize(s));
-    h.sp_keys = keys;
     h.n_sparse = n;
     return cudaSuccess;
 }
