@@ -45,7 +45,8 @@ METRIC = "flow records/sec analysed"
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default 100; D5: 600 batches; reference arm: 20 samples)")
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="gnetmon", choices=["gnetmon", "reference"])
     ap.add_argument("--workload", default="D3")
@@ -200,6 +201,8 @@ def time_reference(w, n_sample: int, reps: int):
 # ---- the reference arm -------------------------------------------------------
 
 def run_reference_arm(args):
+    if args.steps is None:
+        args.steps = 20  # each step is a 2M-record CPU sample (~0.6 s)
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
@@ -273,7 +276,7 @@ def run_stream(args):
         ring.append((FlowBatch(*views), t0 + j * 60_000, [t.to(f"cuda:{local}") for t in ts]))
     torch.cuda.synchronize()
     eng = Engine(local)
-    steps = args.steps if args.steps != 10 else 600
+    steps = args.steps or 600
     for j in range(max(args.warmup, 3)):
         b, lo, _ = ring[j % 16]
         eng.aggregate_window(b, cat, lo, lo + 60_000)
@@ -324,6 +327,8 @@ def run_stream(args):
 
 def main():
     args = parse_args()
+    if args.steps is None and args.impl != "reference" and args.workload != "D5":
+        args.steps = 100
     if args.impl == "reference":
         return run_reference_arm(args)
     if args.workload == "D5":

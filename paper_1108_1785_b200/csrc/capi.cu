@@ -1021,7 +1021,8 @@ int gnm_decode_netflow(gnm_ctx* c, const uint8_t* datagrams, uint64_t bytes, con
         const size_t in_bytes = in_mem == GNM_MEM_HOST ? bytes : 0;
         const size_t off_bytes = in_mem == GNM_MEM_HOST ? (n + 1) * 8 : 0;
         auto up = [](size_t x) { return (x + 255) / 256 * 256; };
-        const size_t total = up(in_bytes) + up(off_bytes) + up(n * 4) + up(n * 8) + up(n) + up(5 * 8) +
+        const size_t scratch_bytes = gnm::netflow_scratch_words(n) * 8;
+        const size_t total = up(in_bytes) + up(off_bytes) + up(scratch_bytes) + up(n) + up(5 * 8) +
                              (direct ? 0 : up(max_rows * 64));
         unsigned char* scratch = nullptr;
         ck(cudaMallocAsync(reinterpret_cast<void**>(&scratch), std::max<size_t>(total, 256), s), "cudaMallocAsync(netflow)");
@@ -1036,18 +1037,16 @@ int gnm_decode_netflow(gnm_ctx* c, const uint8_t* datagrams, uint64_t bytes, con
             off = reinterpret_cast<const uint64_t*>(q);
             q += up(off_bytes);
         }
-        auto* acc = reinterpret_cast<uint32_t*>(q);
-        q += up(n * 4);
-        auto* base = reinterpret_cast<uint64_t*>(q);
-        q += up(n * 8);
+        auto* tiles = reinterpret_cast<unsigned long long*>(q);
+        q += up(scratch_bytes);
         auto* st = reinterpret_cast<uint8_t*>(q);
         q += up(n);
         auto* dstats = reinterpret_cast<unsigned long long*>(q);
         q += up(5 * 8);
         uint8_t* out = direct ? static_cast<uint8_t*>(out_records) : q;
         ck(cudaMemsetAsync(dstats, 0, 5 * 8, s), "cudaMemsetAsync");
-        ck(gnm::launch_netflow_decode(d, off, n, acc, base, st, dstats, out, s), "netflow decode");
-        c->kernel_launches += n ? 3 : 0;
+        ck(gnm::launch_netflow_decode(d, off, n, tiles, st, dstats, out, c->device, s), "netflow decode");
+        c->kernel_launches += n ? 1 : 0;
         unsigned long long hs[5] = {0, 0, 0, 0, 0};
         ck(cudaMemcpyAsync(hs, dstats, sizeof hs, cudaMemcpyDeviceToHost, s), "D2H stats");
         if (status && n) ck(cudaMemcpyAsync(status, st, n, cudaMemcpyDeviceToHost, s), "D2H status");

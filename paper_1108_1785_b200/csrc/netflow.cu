@@ -13,16 +13,11 @@
 // order, then record order -- exactly the order the collector appends to the
 // FlowStore. Paths are relative to /root/reference/proj/core/src.
 //
-// N1 validates every datagram and counts its accepted records (thread per
-// datagram), N2 turns the counts into output offsets (cub's decoupled
-// look-back exclusive scan), N3 decodes (warp per datagram, lane = record)
-// and compacts the accepted records with a ballot.
+// One kernel (nf_decode): validate and count, a chained scan across tiles
+// of datagrams for the output offsets, then decode and compact.
 #include <cuda_runtime.h>
 
 #include <cstdint>
-
-#include <cub/device/device_scan.cuh>
-#include <cuda/std/functional>
 
 #include "netflow.cuh"
 
@@ -58,52 +53,6 @@ __device__ __forceinline__ uint32_t check_header(const uint8_t* p, uint64_t len,
     return 0;
 }
 
-__device__ __forceinline__ uint32_t ld_be32(const uint8_t* q, bool words) {
-    return words ? __byte_perm(__ldg(reinterpret_cast<const uint32_t*>(q)), 0, 0x0123) : be32(q);
-}
-
-// N1, warp per datagram: header checks (lane 0's view is every lane's), then
-// lane r tests record r's reject rule; the ballot's popcount is the
-// datagram's accepted count.
-__global__ void __launch_bounds__(256) n1_validate(const uint8_t* __restrict__ d,
-                                                   const uint64_t* __restrict__ off, uint64_t n,
-                                                   uint32_t* __restrict__ accepted,
-                                                   uint8_t* __restrict__ status,
-                                                   unsigned long long* __restrict__ stats) {
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-    uint32_t err = 0, rej = 0, acc = 0; // lane 0's running totals
-    for (uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < n; i += nwarps) {
-        const uint8_t* p = d + off[i];
-        uint32_t count;
-        const uint32_t st = check_header(p, off[i + 1] - off[i], count); // warp-uniform
-        bool ok = false;
-        if (st == 0 && lane < count) {
-            const uint8_t* q = p + kHdr + kRec * lane;
-            const bool words = (reinterpret_cast<uintptr_t>(p) & 3u) == 0;
-            const uint32_t pkts = ld_be32(q + 16, words), oct = ld_be32(q + 20, words);
-            ok = pkts != 0 && oct >= pkts;
-        }
-        const uint32_t a = __popc(__ballot_sync(0xFFFFFFFFu, ok));
-        if (lane == 0) {
-            if (st == 0) rej += count - a;
-            else ++err;
-            acc += a;
-            accepted[i] = a;
-            if (status) status[i] = static_cast<uint8_t>(st);
-        }
-    }
-    if (lane == 0) {
-        if (err) atomicAdd(stats + 1, static_cast<unsigned long long>(err));
-        if (rej) atomicAdd(stats + 2, static_cast<unsigned long long>(rej));
-        if (acc) atomicAdd(stats + 3, static_cast<unsigned long long>(acc));
-    }
-}
-
-__global__ void n2_total(const uint32_t* __restrict__ in, const uint64_t* __restrict__ base, uint64_t n,
-                         unsigned long long* __restrict__ total) {
-    *total = base[n - 1] + in[n - 1];
-}
 
 // Record fields of one 48-byte big-endian record (decode_raw_record,
 // netflow.cpp:27-50) as the RawFlowRecord words in memory order
@@ -135,42 +84,165 @@ __device__ __forceinline__ void load_raw(const uint8_t* q, uint4& w0, uint4& w1,
     }
 }
 
-// Warp per datagram; lane r decodes record r and resolve_times; accepted
-// lanes are compacted in record order.
-__global__ void __launch_bounds__(256) n3_decode(const uint8_t* __restrict__ d,
-                                                 const uint64_t* __restrict__ off, uint64_t n,
-                                                 const uint64_t* __restrict__ base,
-                                                 uint8_t* __restrict__ out) {
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-    for (uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < n; i += nwarps) {
-        const uint8_t* p = d + off[i];
-        uint32_t count;
-        if (check_header(p, off[i + 1] - off[i], count) != 0) continue; // warp-uniform
-        const uint32_t uptime = be32(p + 4), secs = be32(p + 8), nsecs = be32(p + 12);
-        const uint64_t wall = static_cast<uint64_t>(secs) * 1000u + nsecs / 1000000u;
-        bool ok = false;
-        uint4 w0{}, w1{}, w2{};
-        uint64_t start = 0, end = 0;
-        if (lane < count) {
-            const uint8_t* q = p + kHdr + kRec * lane;
-            if ((reinterpret_cast<uintptr_t>(p) & 3u) == 0) load_raw<true>(q, w0, w1, w2); // warp-uniform
-            else load_raw<false>(q, w0, w1, w2);
-            const uint32_t pkts = w1.x, oct = w1.y, first = w1.z, last = w1.w;
-            ok = pkts != 0 && oct >= pkts;
-            start = wall - wrap_diff(uptime, first);
-            end = wall - wrap_diff(uptime, last);
-            if (end < start) end = start; // degenerate record (netflow.cpp:157-159)
+// Single-pass decode with a chained scan (decoupled look-back). CTAs claim
+// tiles of kNfTile consecutive datagrams in order from a counter. Phase 1:
+// warp per datagram, the header checks of decode_packet and the collector's
+// reject rule per record (lane = record), ballot counts. The tile's count
+// total is published as an aggregate, the predecessors' are summed back to
+// the first inclusive prefix, and the tile's inclusive prefix is published.
+// Phase 2: warp per datagram again; a 4-byte-aligned datagram's record area
+// (an L2 hit: phase 1 just read it) moves into shared memory with coalesced
+// word loads (13-word record stride: conflict-free), others use byte loads;
+// decode (byte permutes), resolve_times, accepted rows staged in shared
+// memory and written with coalesced 16-byte stores at their final offsets.
+constexpr uint32_t kNfWarps = 8, kNfPerWarp = 4, kNfTile = kNfWarps * kNfPerWarp; // 32 datagrams (<= 32)
+constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagPrefix = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(kNfWarps * 32) nf_decode(const uint8_t* __restrict__ d,
+                                                           const uint64_t* __restrict__ off, uint64_t n,
+                                                           unsigned long long* __restrict__ tiles,
+                                                           uint8_t* __restrict__ status,
+                                                           unsigned long long* __restrict__ stats,
+                                                           uint8_t* __restrict__ out) {
+    __shared__ uint32_t s_cnt[kNfTile];
+    __shared__ unsigned long long s_base[kNfTile];
+    __shared__ unsigned long long s_tile;
+    __shared__ uint32_t s_rec[kNfWarps][kMaxRec * 13]; // a datagram's records, 13-word stride
+    __shared__ uint4 s_out[kNfWarps][kMaxRec * 4];     // its accepted rows
+    unsigned long long* counter = tiles; // tiles[0]: next tile; tiles[1 + t]: tile t's state
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint64_t n_tiles = (n + kNfTile - 1) / kNfTile;
+    uint32_t err = 0, rej = 0, acc = 0; // lane 0's running totals
+    while (true) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1ull);
+        __syncthreads();
+        const uint64_t tile = s_tile;
+        if (tile >= n_tiles) break; // CTA-uniform
+        for (uint32_t k = 0; k < kNfPerWarp; ++k) {
+            const uint32_t li = warp * kNfPerWarp + k;
+            const uint64_t i = tile * kNfTile + li;
+            uint32_t a = 0;
+            if (i < n) { // warp-uniform
+                const uint8_t* p = d + off[i];
+                uint32_t count;
+                const uint32_t st = check_header(p, off[i + 1] - off[i], count);
+                const bool words = (reinterpret_cast<uintptr_t>(p) & 3u) == 0;
+                bool ok = false;
+                if (st == 0 && lane < count) {
+                    const uint8_t* q = p + kHdr + kRec * lane;
+                    uint32_t pkts, oct;
+                    if (words) {
+                        pkts = __byte_perm(__ldg(reinterpret_cast<const uint32_t*>(q + 16)), 0, 0x0123);
+                        oct = __byte_perm(__ldg(reinterpret_cast<const uint32_t*>(q + 20)), 0, 0x0123);
+                    } else {
+                        pkts = be32(q + 16);
+                        oct = be32(q + 20);
+                    }
+                    ok = pkts != 0 && oct >= pkts;
+                }
+                a = __popc(__ballot_sync(0xFFFFFFFFu, ok));
+                if (lane == 0) {
+                    if (st == 0) rej += count - a;
+                    else ++err;
+                    acc += a;
+                    if (status) status[i] = static_cast<uint8_t>(st);
+                }
+            }
+            if (lane == 0) s_cnt[li] = a;
         }
-        const unsigned m = __ballot_sync(0xFFFFFFFFu, ok);
-        if (ok) {
-            uint4* o = reinterpret_cast<uint4*>(out + (base[i] + __popc(m & ((1u << lane) - 1u))) * 64);
-            o[0] = w0;
-            o[1] = w1;
-            o[2] = w2;
-            o[3] = make_uint4(static_cast<uint32_t>(start), static_cast<uint32_t>(start >> 32),
-                              static_cast<uint32_t>(end), static_cast<uint32_t>(end >> 32));
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t v = lane < kNfTile ? s_cnt[lane] : 0u;
+            uint32_t incl = v;
+#pragma unroll
+            for (uint32_t o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31); // lanes >= kNfTile add 0
+            unsigned long long prefix = 0;
+            if (lane == 0) {
+                if (tile == 0) {
+                    atomicExch(tiles + 1, kFlagPrefix | total);
+                } else {
+                    atomicExch(tiles + 1 + tile, kFlagAgg | total);
+                    for (uint64_t j = tile; j-- > 0;) { // predecessors were claimed earlier: they finish
+                        unsigned long long stj;
+                        do {
+                            stj = *reinterpret_cast<volatile unsigned long long*>(tiles + 1 + j);
+                        } while (stj == 0);
+                        prefix += stj & kValMask;
+                        if ((stj & ~kValMask) == kFlagPrefix) break;
+                    }
+                    atomicExch(tiles + 1 + tile, kFlagPrefix | (prefix + total));
+                }
+            }
+            prefix = __shfl_sync(0xFFFFFFFFu, prefix, 0);
+            if (lane < kNfTile) s_base[lane] = prefix + incl - v;
         }
+        __syncthreads();
+        for (uint32_t k = 0; k < kNfPerWarp; ++k) {
+            const uint32_t li = warp * kNfPerWarp + k;
+            const uint64_t i = tile * kNfTile + li;
+            if (i >= n) break;
+            const uint8_t* p = d + off[i];
+            uint32_t count;
+            if (check_header(p, off[i + 1] - off[i], count) != 0) continue; // warp-uniform
+            const uint32_t uptime = be32(p + 4), secs = be32(p + 8), nsecs = be32(p + 12);
+            const uint64_t wall = static_cast<uint64_t>(secs) * 1000u + nsecs / 1000000u;
+            const bool words = (reinterpret_cast<uintptr_t>(p) & 3u) == 0; // warp-uniform
+            uint32_t* recw = s_rec[warp];
+            if (words) { // coalesced word loads of the record area (an L2 hit) into a padded tile
+                const uint32_t* src = reinterpret_cast<const uint32_t*>(p + kHdr);
+                for (uint32_t idx = lane; idx < count * 12; idx += 32) {
+                    const uint32_t r = idx / 12;
+                    recw[r * 13 + (idx - r * 12)] = __ldg(src + idx);
+                }
+                __syncwarp();
+            }
+            bool ok = false;
+            uint4 w0{}, w1{}, w2{};
+            uint64_t start = 0, end = 0;
+            if (lane < count) {
+                if (words) {
+                    const uint32_t* x = recw + lane * 13;
+                    auto sw = [](uint32_t v) { return __byte_perm(v, 0, 0x0123); };   // be32
+                    auto sw16 = [](uint32_t v) { return __byte_perm(v, 0, 0x2301); }; // two be16
+                    w0 = make_uint4(sw(x[0]), sw(x[1]), sw(x[2]), sw16(x[3]));
+                    w1 = make_uint4(sw(x[4]), sw(x[5]), sw(x[6]), sw(x[7]));
+                    w2 = make_uint4(sw16(x[8]), x[9], sw16(x[10]), __byte_perm(x[11], 0, 0x2310));
+                } else {
+                    load_raw<false>(p + kHdr + kRec * lane, w0, w1, w2);
+                }
+                const uint32_t pkts = w1.x, oct = w1.y, first = w1.z, last = w1.w;
+                ok = pkts != 0 && oct >= pkts;
+                start = wall - wrap_diff(uptime, first);
+                end = wall - wrap_diff(uptime, last);
+                if (end < start) end = start; // degenerate record (netflow.cpp:157-159)
+            }
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, ok);
+            // Rows through shared memory, then coalesced 16-byte stores.
+            uint4* rows = s_out[warp];
+            __syncwarp();
+            if (ok) {
+                const uint32_t j = __popc(m & ((1u << lane) - 1u));
+                rows[j * 4 + 0] = w0;
+                rows[j * 4 + 1] = w1;
+                rows[j * 4 + 2] = w2;
+                rows[j * 4 + 3] = make_uint4(static_cast<uint32_t>(start), static_cast<uint32_t>(start >> 32),
+                                             static_cast<uint32_t>(end), static_cast<uint32_t>(end >> 32));
+            }
+            __syncwarp();
+            uint4* dst = reinterpret_cast<uint4*>(out + s_base[li] * 64);
+            for (uint32_t idx = lane; idx < __popc(m) * 4; idx += 32) __stcs(dst + idx, rows[idx]);
+            __syncwarp();
+        }
+        __syncthreads(); // s_tile, s_cnt and s_base are reused
+    }
+    if (lane == 0) {
+        if (err) atomicAdd(stats + 1, static_cast<unsigned long long>(err));
+        if (rej) atomicAdd(stats + 2, static_cast<unsigned long long>(rej));
+        if (acc) atomicAdd(stats + 3, static_cast<unsigned long long>(acc));
     }
 }
 
@@ -231,26 +303,21 @@ cudaError_t launch_archive_decode(const uint8_t* entries, uint64_t n, uint8_t* o
     return cudaGetLastError();
 }
 
-cudaError_t launch_netflow_decode(const uint8_t* d, const uint64_t* off, uint64_t n, uint32_t* accepted,
-                                  uint64_t* base, uint8_t* status, unsigned long long* stats,
-                                  uint8_t* out, cudaStream_t s) {
+uint64_t netflow_scratch_words(uint64_t n) { return 1 + (n + kNfTile - 1) / kNfTile; }
+
+cudaError_t launch_netflow_decode(const uint8_t* d, const uint64_t* off, uint64_t n, unsigned long long* scratch,
+                                  uint8_t* status, unsigned long long* stats, uint8_t* out, int device,
+                                  cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    const uint32_t g1 = static_cast<uint32_t>(std::min<uint64_t>((n * 32 + 255) / 256, 148 * 16));
-    n1_validate<<<g1, 256, 0, s>>>(d, off, n, accepted, status, stats);
-    // N2: exclusive scan (decoupled look-back) of the accepted counts into u64 offsets.
-    size_t tb = 0;
-    cudaError_t e = cub::DeviceScan::ExclusiveScan(nullptr, tb, accepted, base, ::cuda::std::plus<uint64_t>(),
-                                                   static_cast<uint64_t>(0), n, s);
+    cudaError_t e = cudaMemsetAsync(scratch, 0, netflow_scratch_words(n) * 8, s);
     if (e != cudaSuccess) return e;
-    void* tmp = nullptr;
-    if ((e = cudaMallocAsync(&tmp, std::max<size_t>(tb, 1), s)) != cudaSuccess) return e;
-    e = cub::DeviceScan::ExclusiveScan(tmp, tb, accepted, base, ::cuda::std::plus<uint64_t>(),
-                                       static_cast<uint64_t>(0), n, s);
-    if (e != cudaSuccess) return e;
-    if ((e = cudaFreeAsync(tmp, s)) != cudaSuccess) return e;
-    n2_total<<<1, 1, 0, s>>>(accepted, base, n, stats + 4);
-    const uint32_t g3 = static_cast<uint32_t>(std::min<uint64_t>((n * 32 + 255) / 256, 65535));
-    n3_decode<<<g3, 256, 0, s>>>(d, off, n, base, out);
+    int sms = 0, per_sm = 0;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nf_decode, kNfWarps * 32, 0)) != cudaSuccess)
+        return e;
+    const uint64_t n_tiles = (n + kNfTile - 1) / kNfTile;
+    const uint32_t g = static_cast<uint32_t>(std::min<uint64_t>(n_tiles, static_cast<uint64_t>(sms) * std::max(per_sm, 1)));
+    nf_decode<<<g, kNfWarps * 32, 0, s>>>(d, off, n, scratch, status, stats, out);
     return cudaGetLastError();
 }
 
