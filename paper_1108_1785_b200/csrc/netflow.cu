@@ -55,33 +55,19 @@ __device__ __forceinline__ uint32_t check_header(const uint8_t* p, uint64_t len,
 
 
 // Record fields of one 48-byte big-endian record (decode_raw_record,
-// netflow.cpp:27-50) as the RawFlowRecord words in memory order
-// (netflow.hpp:32-57): u32 src, dst, next_hop; u16 input_if, output_if; u32
-// d_pkts, d_octets, first, last; u16 src_port, dst_port; u8 pad1,
-// tcp_flags, protocol, tos; u16 src_as, dst_as; u8 src_mask, dst_mask; u16
-// pad2. kWords: the record is 4-byte aligned, so 12 word loads and byte
-// permutes replace 48 byte loads.
-template <bool kWords>
-__device__ __forceinline__ void load_raw(const uint8_t* q, uint4& w0, uint4& w1, uint4& w2) {
-    if constexpr (kWords) {
-        const uint32_t* u = reinterpret_cast<const uint32_t*>(q);
-        uint32_t x[12];
-#pragma unroll
-        for (int k = 0; k < 12; ++k) x[k] = __ldg(u + k);
-        auto sw = [](uint32_t v) { return __byte_perm(v, 0, 0x0123); };   // be32
-        auto sw16 = [](uint32_t v) { return __byte_perm(v, 0, 0x2301); }; // two be16
-        w0 = make_uint4(sw(x[0]), sw(x[1]), sw(x[2]), sw16(x[3]));
-        w1 = make_uint4(sw(x[4]), sw(x[5]), sw(x[6]), sw(x[7]));
-        w2 = make_uint4(sw16(x[8]), x[9], sw16(x[10]), __byte_perm(x[11], 0, 0x2310));
-    } else {
-        w0 = make_uint4(be32(q), be32(q + 4), be32(q + 8), be16(q + 12) | be16(q + 14) << 16);
-        w1 = make_uint4(be32(q + 16), be32(q + 20), be32(q + 24), be32(q + 28));
-        w2 = make_uint4(be16(q + 32) | be16(q + 34) << 16,
-                        static_cast<uint32_t>(q[36]) | static_cast<uint32_t>(q[37]) << 8 |
-                            static_cast<uint32_t>(q[38]) << 16 | static_cast<uint32_t>(q[39]) << 24,
-                        be16(q + 40) | be16(q + 42) << 16,
-                        static_cast<uint32_t>(q[44]) | static_cast<uint32_t>(q[45]) << 8 | be16(q + 46) << 16);
-    }
+// netflow.cpp:27-50), byte loads (datagrams that are not 4-byte aligned), as
+// the RawFlowRecord words in memory order (netflow.hpp:32-57): u32 src, dst,
+// next_hop; u16 input_if, output_if; u32 d_pkts, d_octets, first, last; u16
+// src_port, dst_port; u8 pad1, tcp_flags, protocol, tos; u16 src_as, dst_as;
+// u8 src_mask, dst_mask; u16 pad2.
+__device__ __forceinline__ void load_raw_bytes(const uint8_t* q, uint4& w0, uint4& w1, uint4& w2) {
+    w0 = make_uint4(be32(q), be32(q + 4), be32(q + 8), be16(q + 12) | be16(q + 14) << 16);
+    w1 = make_uint4(be32(q + 16), be32(q + 20), be32(q + 24), be32(q + 28));
+    w2 = make_uint4(be16(q + 32) | be16(q + 34) << 16,
+                    static_cast<uint32_t>(q[36]) | static_cast<uint32_t>(q[37]) << 8 |
+                        static_cast<uint32_t>(q[38]) << 16 | static_cast<uint32_t>(q[39]) << 24,
+                    be16(q + 40) | be16(q + 42) << 16,
+                    static_cast<uint32_t>(q[44]) | static_cast<uint32_t>(q[45]) << 8 | be16(q + 46) << 16);
 }
 
 // Single-pass decode with a chained scan (decoupled look-back). CTAs claim
@@ -212,7 +198,7 @@ __global__ void __launch_bounds__(kNfWarps * 32) nf_decode(const uint8_t* __rest
                     w1 = make_uint4(sw(x[4]), sw(x[5]), sw(x[6]), sw(x[7]));
                     w2 = make_uint4(sw16(x[8]), x[9], sw16(x[10]), __byte_perm(x[11], 0, 0x2310));
                 } else {
-                    load_raw<false>(p + kHdr + kRec * lane, w0, w1, w2);
+                    load_raw_bytes(p + kHdr + kRec * lane, w0, w1, w2);
                 }
                 const uint32_t pkts = w1.x, oct = w1.y, first = w1.z, last = w1.w;
                 ok = pkts != 0 && oct >= pkts;
