@@ -67,6 +67,8 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("GNM_BENCH_ONE_DEVICE"):  # test hook: every rank on cuda:0 (gloo; see tests)
+        local = 0
     return world, rank, local
 
 
@@ -341,7 +343,13 @@ def main():
 
     world, rank, local = dist_env()
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL over NVLink; GNM_BENCH_BACKEND=gloo is a test hook for several
+        # ranks on the one GPU a test box has (NCCL refuses shared devices).
+        backend = os.environ.get("GNM_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     w = synth.workload(args.workload)
     n = args.records or w.n
