@@ -13,16 +13,22 @@
 //   H1  insert every (site, host) key into an open-addressing table (at most
 //       256 keys per registry /24 entry, so the table is sized by
 //       min(flows, 256 * entries)); accumulate the u128 micro-bps sum, min and
-//       max per slot (warp-aggregated over lanes that share a slot, one
-//       atomic per slot per warp); flatten (slot, bucket) per flow;
+//       max per slot (through a per-CTA shared table for the hot slots);
+//       flatten (slot, bucket) per flow;
 //   H2  collect the distinct keys, radix-sort them: row = rank in (site,
-//       host) order, i.e. the std::map's iteration order;
-//   H3  per flow key = row << 14 | bucket, radix-sorted (keys only), so
-//       every row's flows form one run in bucket order;
-//   H4  run starts; count = run length;
-//   H5  per row: the lower median is the run's element (count + 1) / 2 - 1
-//       (RateHistogram::median_bps, rate_engine.cpp:42-58), clamped, avg as
-//       the host rounds it (stats_from, :242-253).
+//       host) order, i.e. the std::map's iteration order; every flow's slot
+//       becomes its row;
+//   H3  the exact lower median per row (RateHistogram::median_bps,
+//       rate_engine.cpp:42-58): with rows * 628 B <= 64 MB, the sites'
+//       two-round scheme (coarse counts per (super-bucket, row), each row's
+//       median super-bucket, that super-bucket's 64 fine counts; all
+//       L2-resident, warp-aggregated); otherwise a radix sort of the
+//       row << 14 | bucket keys, where the median is the run's element
+//       (count + 1) / 2 - 1;
+//   H5  per row: count, clamp into [min, max], avg as the host rounds it
+//       (stats_from, :242-253).
+// Histograms (dense or sparse) are built from the per-flow (row, bucket)
+// arrays only when asked for.
 #include <cuda_runtime.h>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -243,14 +249,140 @@ __global__ void h_rank(const uint32_t* __restrict__ hs_sorted, uint32_t n, unsig
         keys[hs_sorted[i]] = i;
 }
 
-template <typename K>
-__global__ void h_keys(const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ bk, uint32_t n,
-                       const unsigned long long* __restrict__ rank, K* __restrict__ sk) {
+// Flat per-flow row ids in place of the slots.
+__global__ void h_to_rows(uint32_t* __restrict__ slot_row, uint32_t n, const unsigned long long* __restrict__ rank) {
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
-        sk[j] = static_cast<K>(rank[slot_of[j]]) << kBucketBits | bk[j];
+        slot_row[j] = static_cast<uint32_t>(rank[slot_row[j]]);
 }
 
-// H4: start[row] = first position of the row's run; start[n_rows] = n.
+// ---- per-row exact lower median, two rounds (rows * 628 B L2-resident) -------
+// The sites' scheme (kernels.cuh): coarse counts per (super-bucket, row),
+// super-bucket-major; each row's median super-bucket and the median's rank
+// in it; the fine counts of that super-bucket only. Lanes of a warp that
+// carry the same (row, super-bucket) or (row, bucket) add once, together.
+constexpr uint32_t kCoarseH = 157, kFineH = 64;
+constexpr size_t kTwoRoundBytes = 64ull << 20;
+
+// Hot (row, super-bucket) pairs would serialise on one L2 counter, so each
+// CTA counts into a shared table first (first come, first served; a pair
+// whose entry is taken goes to L2 directly) and flushes it once.
+constexpr uint32_t kCoarseAgg = 4096;
+// Also turns every flow's slot into its row (in place).
+__global__ void __launch_bounds__(512) h_coarse(uint32_t* __restrict__ row, const uint32_t* __restrict__ bk,
+                                                uint32_t n, uint32_t n_rows, const unsigned long long* __restrict__ rank,
+                                                uint32_t* __restrict__ coarse) {
+    __shared__ uint32_t tkey[kCoarseAgg], tcnt[kCoarseAgg];
+    for (uint32_t i = threadIdx.x; i < kCoarseAgg; i += blockDim.x) {
+        tkey[i] = 0xFFFFFFFFu;
+        tcnt[i] = 0;
+    }
+    __syncthreads();
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const uint32_t r = static_cast<uint32_t>(rank[row[j]]), sb = bk[j] >> 6;
+        row[j] = r;
+        const uint32_t key = r << 8 | sb; // rows < 2^24 on this path (rows * 628 B <= 64 MB)
+        const uint32_t e = (key * 2654435761u) >> (32 - 12);
+        uint32_t cur = tkey[e];
+        if (cur == 0xFFFFFFFFu) cur = atomicCAS(tkey + e, 0xFFFFFFFFu, key);
+        if (cur == 0xFFFFFFFFu || cur == key)
+            atomicAdd(tcnt + e, 1u);
+        else
+            atomicAdd(coarse + static_cast<size_t>(sb) * n_rows + r, 1u);
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < kCoarseAgg; i += blockDim.x)
+        if (tcnt[i]) atomicAdd(coarse + static_cast<size_t>(tkey[i] & 0xFFu) * n_rows + (tkey[i] >> 8), tcnt[i]);
+}
+
+__global__ void h_msb(const uint32_t* __restrict__ coarse, uint32_t n_rows, uint32_t* __restrict__ msb,
+                      uint32_t* __restrict__ mrank, uint32_t* __restrict__ cnt) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += gridDim.x * blockDim.x) {
+        uint32_t total = 0;
+        for (uint32_t sb = 0; sb < kCoarseH; ++sb) total += coarse[static_cast<size_t>(sb) * n_rows + r];
+        const uint32_t target = (total + 1) / 2; // RateHistogram::median_bps (rate_engine.cpp:47)
+        uint32_t cum = 0, m = 0, k = 0;
+        for (uint32_t sb = 0; sb < kCoarseH; ++sb) {
+            const uint32_t c = coarse[static_cast<size_t>(sb) * n_rows + r];
+            if (cum + c >= target) {
+                m = sb;
+                k = target - cum;
+                break;
+            }
+            cum += c;
+        }
+        msb[r] = m;
+        mrank[r] = k;
+        cnt[r] = total;
+    }
+}
+
+__global__ void __launch_bounds__(256) h_fine(const uint32_t* __restrict__ row, const uint32_t* __restrict__ bk,
+                                              uint32_t n, const uint32_t* __restrict__ msb,
+                                              uint32_t* __restrict__ fine) {
+    const uint32_t lane = threadIdx.x & 31u;
+    for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+        const uint32_t j = base + threadIdx.x;
+        bool hit = false;
+        uint32_t r = 0, b = 0;
+        if (j < n) {
+            r = row[j];
+            b = bk[j];
+            hit = (b >> 6) == __ldg(msb + r);
+        }
+        const unsigned long long key = hit ? (static_cast<unsigned long long>(r) << 8 | (b & 63u)) : ~0ull;
+        const unsigned m = __match_any_sync(0xFFFFFFFFu, key);
+        if (hit && lane == static_cast<uint32_t>(__ffs(m) - 1))
+            atomicAdd(fine + static_cast<size_t>(r) * kFineH + (b & 63u), __popc(m));
+    }
+}
+
+// H5 (two-round), thread per row: the exact bucket from the fine counts.
+__global__ void h_final2(const unsigned long long* __restrict__ acc, const uint32_t* __restrict__ cnt,
+                         const uint32_t* __restrict__ msb, const uint32_t* __restrict__ mrank,
+                         const uint32_t* __restrict__ fine, const unsigned long long* __restrict__ hk_sorted,
+                         const uint32_t* __restrict__ hs_sorted, uint32_t n_rows, gnm_host_stats* __restrict__ rows) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += gridDim.x * blockDim.x) {
+        const uint32_t* f = fine + static_cast<size_t>(r) * kFineH;
+        uint32_t cum = 0, k = msb[r] * kFineH + kFineH - 1;
+        const uint32_t want = mrank[r];
+        for (uint32_t q = 0; q < kFineH; ++q) {
+            cum += f[q];
+            if (cum >= want) {
+                k = msb[r] * kFineH + q;
+                break;
+            }
+        }
+        const unsigned long long* a = acc + static_cast<size_t>(hs_sorted[r]) * 5;
+        const unsigned __int128 u = static_cast<unsigned __int128>(a[0]) +
+                                    (static_cast<unsigned __int128>(a[1]) << 32) +
+                                    (static_cast<unsigned __int128>(a[2]) << 64);
+        const double mn = __longlong_as_double(static_cast<long long>(~a[3]));
+        const double mx = __longlong_as_double(static_cast<long long>(a[4]));
+        double med = median_of_bucket(k);
+        med = med < mn ? mn : (mx < med ? mx : med);
+        gnm_host_stats o;
+        o.site = static_cast<uint32_t>(hk_sorted[r] >> 32);
+        o.host = static_cast<uint32_t>(hk_sorted[r]);
+        o.flow_count = cnt[r];
+        o.rate_ubps_lo = static_cast<uint64_t>(u);
+        o.rate_ubps_hi = static_cast<uint64_t>(u >> 64);
+        o.min_bps = mn;
+        o.max_bps = mx;
+        o.avg_bps = avg_of(o.rate_ubps_lo, o.rate_ubps_hi, o.flow_count);
+        o.median_bps = med;
+        rows[r] = o;
+    }
+}
+
+// ---- per-row median from sorted (row, bucket) keys (many rows) -------------------
+template <typename K>
+__global__ void h_keys(const uint32_t* __restrict__ row, const uint32_t* __restrict__ bk, uint32_t n,
+                       K* __restrict__ sk) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+        sk[j] = static_cast<K>(row[j]) << kBucketBits | bk[j];
+}
+
+// start[row] = first position of the row's run; start[n_rows] = n.
 template <typename K>
 __global__ void h_starts(const K* __restrict__ sk, uint32_t n, uint32_t n_rows, uint32_t* __restrict__ start) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -260,7 +392,8 @@ __global__ void h_starts(const K* __restrict__ sk, uint32_t n, uint32_t n_rows, 
     if (blockIdx.x == 0 && threadIdx.x == 0) start[n_rows] = n;
 }
 
-// H5, thread per row.
+// H5 (sorted), thread per row: the lower median is the run's element
+// (count + 1) / 2 - 1.
 template <typename K>
 __global__ void h_final(const unsigned long long* __restrict__ acc, const uint32_t* __restrict__ start,
                         const K* __restrict__ sk, const unsigned long long* __restrict__ hk_sorted,
@@ -292,13 +425,11 @@ __global__ void h_final(const unsigned long long* __restrict__ acc, const uint32
     }
 }
 
-template <typename K>
-__global__ void h_hist(const K* __restrict__ sk, uint64_t n, uint32_t* __restrict__ dense) {
+__global__ void h_hist(const uint32_t* __restrict__ row, const uint32_t* __restrict__ bk, uint64_t n,
+                       uint32_t* __restrict__ dense) {
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const K k = sk[i];
-        atomicAdd(dense + static_cast<size_t>(k >> kBucketBits) * kBuckets + (k & kBucketMask), 1u);
-    }
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        atomicAdd(dense + static_cast<size_t>(row[i]) * kBuckets + bk[i], 1u);
 }
 
 uint32_t grid_for(int device, uint64_t n, uint32_t block) {
@@ -337,37 +468,63 @@ struct Scratch {
     }
 };
 
-// H3..H5 for one key width.
+// h.sorted: every flow's (row, bucket) key in (row, bucket) order.
 template <typename K>
-cudaError_t sort_and_finish(int device, uint32_t n, uint32_t n_rows, const uint32_t* slot_of, const uint32_t* bk,
-                            const unsigned long long* rank_tab, const unsigned long long* acc,
-                            const unsigned long long* hk_sorted, const uint32_t* hs_sorted, HostRows& out,
-                            cudaStream_t s) {
+cudaError_t sort_keys(int device, HostRows& h, cudaStream_t s) {
     Scratch tmp_(s);
+    const uint32_t n = static_cast<uint32_t>(h.n_flows);
     K *sk = nullptr, *sk2 = nullptr;
     HCK(tmp_.get(&sk, n));
     HCK(dalloc(&sk2, n, s));
-    out.sorted = sk2; // owned by `out` from here (free_hosts)
-    h_keys<K><<<grid_for(device, n, 256), 256, 0, s>>>(slot_of, bk, n, rank_tab, sk);
+    h.sorted = sk2; // owned by `h` from here (free_hosts)
+    h_keys<K><<<grid_for(device, n, 256), 256, 0, s>>>(h.row_of, h.bkt, n, sk);
     HCK(cudaGetLastError());
-    const int end_bit = static_cast<int>(kBucketBits) + std::max(1, bits_for(n_rows));
+    const int end_bit = static_cast<int>(kBucketBits) + std::max(1, bits_for(h.n_rows));
     size_t tb = 0;
     HCK(cub::DeviceRadixSort::SortKeys(nullptr, tb, sk, sk2, n, 0, end_bit, s));
     unsigned char* tmp = nullptr;
     HCK(tmp_.get(&tmp, tb));
-    HCK(cub::DeviceRadixSort::SortKeys(tmp, tb, sk, sk2, n, 0, end_bit, s));
+    return cub::DeviceRadixSort::SortKeys(tmp, tb, sk, sk2, n, 0, end_bit, s);
+}
+
+cudaError_t ensure_sorted(int device, HostRows& h, cudaStream_t s) {
+    if (h.sorted || h.n_flows == 0) return cudaSuccess;
+    return h.key64 ? sort_keys<unsigned long long>(device, h, s) : sort_keys<uint32_t>(device, h, s);
+}
+
+template <typename K>
+cudaError_t finish_sorted(int device, HostRows& h, const unsigned long long* acc, const unsigned long long* hk_sorted,
+                          const uint32_t* hs_sorted, cudaStream_t s) {
+    Scratch tmp_(s);
+    HCK(ensure_sorted(device, h, s));
+    const uint32_t n = static_cast<uint32_t>(h.n_flows);
     uint32_t* start = nullptr;
-    HCK(tmp_.get(&start, static_cast<size_t>(n_rows) + 1));
-    h_starts<K><<<grid_for(device, n, 256), 256, 0, s>>>(sk2, n, n_rows, start);
+    HCK(tmp_.get(&start, static_cast<size_t>(h.n_rows) + 1));
+    const K* sk = static_cast<const K*>(h.sorted);
+    h_starts<K><<<grid_for(device, n, 256), 256, 0, s>>>(sk, n, static_cast<uint32_t>(h.n_rows), start);
     HCK(cudaGetLastError());
-    HCK(dalloc(&out.rows, n_rows, s));
-    h_final<K><<<grid_for(device, n_rows, 128), 128, 0, s>>>(acc, start, sk2, hk_sorted, hs_sorted, n_rows,
-                                                             out.rows);
-    HCK(cudaGetLastError());
-    out.key64 = sizeof(K) == 8;
-    out.n_rows = n_rows;
-    out.n_flows = n;
-    return cudaSuccess;
+    h_final<K><<<grid_for(device, h.n_rows, 128), 128, 0, s>>>(acc, start, sk, hk_sorted, hs_sorted,
+                                                               static_cast<uint32_t>(h.n_rows), h.rows);
+    return cudaGetLastError();
+}
+
+cudaError_t finish_two_round(int device, HostRows& h, const unsigned long long* rank, const unsigned long long* acc,
+                             const unsigned long long* hk_sorted, const uint32_t* hs_sorted, cudaStream_t s) {
+    Scratch tmp_(s);
+    const uint32_t n = static_cast<uint32_t>(h.n_flows), nr = static_cast<uint32_t>(h.n_rows);
+    uint32_t *coarse = nullptr, *msb = nullptr, *mrank = nullptr, *cnt = nullptr, *fine = nullptr;
+    HCK(tmp_.get(&coarse, static_cast<size_t>(nr) * kCoarseH));
+    HCK(tmp_.get(&msb, nr));
+    HCK(tmp_.get(&mrank, nr));
+    HCK(tmp_.get(&cnt, nr));
+    HCK(tmp_.get(&fine, static_cast<size_t>(nr) * kFineH));
+    HCK(cudaMemsetAsync(coarse, 0, static_cast<size_t>(nr) * kCoarseH * 4, s));
+    HCK(cudaMemsetAsync(fine, 0, static_cast<size_t>(nr) * kFineH * 4, s));
+    h_coarse<<<grid_for(device, n, 512), 512, 0, s>>>(h.row_of, h.bkt, n, nr, rank, coarse);
+    h_msb<<<grid_for(device, nr, 128), 128, 0, s>>>(coarse, nr, msb, mrank, cnt);
+    h_fine<<<grid_for(device, n, 256), 256, 0, s>>>(h.row_of, h.bkt, n, msb, fine);
+    h_final2<<<grid_for(device, nr, 128), 128, 0, s>>>(acc, cnt, msb, mrank, fine, hk_sorted, hs_sorted, nr, h.rows);
+    return cudaGetLastError();
 }
 
 } // namespace
@@ -402,11 +559,11 @@ cudaError_t build_hosts(int device, const HostSlice* slices, int n_slices,
     const int tbits = std::max(10, bits_for(2 * std::max<uint64_t>(1, std::min(n, max_keys))));
     const uint32_t cap = 1u << tbits;
     unsigned long long *keys = nullptr, *acc = nullptr;
-    uint32_t *slot_of = nullptr, *bk = nullptr;
     HCK(tmp_.get(&keys, cap));
     HCK(tmp_.get(&acc, static_cast<size_t>(cap) * 5));
-    HCK(tmp_.get(&slot_of, n));
-    HCK(tmp_.get(&bk, n));
+    HCK(dalloc(&out.row_of, n, s)); // slots first, rows after H2; owned by `out`
+    HCK(dalloc(&out.bkt, n, s));
+    out.n_flows = n;
     HCK(cudaMemsetAsync(keys, 0xFF, static_cast<size_t>(cap) * 8, s));
     HCK(cudaMemsetAsync(acc, 0, static_cast<size_t>(cap) * 40, s));
     for (int i = 0; i < n_slices; ++i) {
@@ -415,7 +572,7 @@ cudaError_t build_hosts(int device, const HostSlice* slices, int n_slices,
         const uint64_t items = static_cast<uint64_t>(sl.log.regions) * ((sl.log.warp_cap + kInsChunk - 1) / kInsChunk);
         const uint32_t g = std::min<uint32_t>(grid_for(device, items * 32, kInsBlock), 4 * sms);
         h_insert<<<g, kInsBlock, kInsSmem, s>>>(sl.log, counts + sl.count_off, off + sl.count_off, keys, cap - 1,
-                                                64 - tbits, acc, slot_of, bk);
+                                                64 - tbits, acc, out.row_of, out.bkt);
         HCK(cudaGetLastError());
     }
     // H2: distinct keys in (site, host) order -> rows.
@@ -439,22 +596,21 @@ cudaError_t build_hosts(int device, const HostSlice* slices, int n_slices,
     HCK(cub::DeviceRadixSort::SortPairs(tmp2, tb, hk, hk_sorted, hs, hs_sorted, n_rows, 0, 64, s));
     h_rank<<<grid_for(device, n_rows, 256), 256, 0, s>>>(hs_sorted, n_rows, keys);
     HCK(cudaGetLastError());
-    // H3..H5.
-    const uint32_t n32 = static_cast<uint32_t>(n);
-    if (kBucketBits + bits_for(n_rows) <= 32)
-        return sort_and_finish<uint32_t>(device, n32, n_rows, slot_of, bk, keys, acc, hk_sorted, hs_sorted, out, s);
-    return sort_and_finish<unsigned long long>(device, n32, n_rows, slot_of, bk, keys, acc, hk_sorted, hs_sorted,
-                                               out, s);
+    out.n_rows = n_rows;
+    out.key64 = kBucketBits + bits_for(n_rows) > 32;
+    HCK(dalloc(&out.rows, n_rows, s));
+    // H3..H5: the exact lower median per row (slots become rows on the way).
+    if (static_cast<size_t>(n_rows) * kCoarseH * 4 <= kTwoRoundBytes)
+        return finish_two_round(device, out, keys, acc, hk_sorted, hs_sorted, s);
+    h_to_rows<<<grid_for(device, n, 256), 256, 0, s>>>(out.row_of, static_cast<uint32_t>(n), keys);
+    HCK(cudaGetLastError());
+    return out.key64 ? finish_sorted<unsigned long long>(device, out, acc, hk_sorted, hs_sorted, s)
+                     : finish_sorted<uint32_t>(device, out, acc, hk_sorted, hs_sorted, s);
 }
 
 cudaError_t hosts_histograms(int device, const HostRows& h, uint32_t* dense, cudaStream_t s) {
     if (h.n_flows == 0) return cudaSuccess;
-    const uint32_t g = grid_for(device, h.n_flows, 256);
-    if (h.key64)
-        h_hist<unsigned long long><<<g, 256, 0, s>>>(static_cast<const unsigned long long*>(h.sorted), h.n_flows,
-                                                     dense);
-    else
-        h_hist<uint32_t><<<g, 256, 0, s>>>(static_cast<const uint32_t*>(h.sorted), h.n_flows, dense);
+    h_hist<<<grid_for(device, h.n_flows, 256), 256, 0, s>>>(h.row_of, h.bkt, h.n_flows, dense);
     return cudaGetLastError();
 }
 
@@ -493,11 +649,11 @@ __global__ void h_split(const K* __restrict__ keys, uint64_t n, uint32_t* __rest
 } // namespace
 
 cudaError_t hosts_sparse(int device, HostRows& h, uint64_t* n, cudaStream_t s) {
-    (void)device;
     if (h.n_sparse == ~0ull) {
         if (h.n_flows == 0) {
             h.n_sparse = 0;
         } else {
+            HCK(ensure_sorted(device, h, s)); // the two-round median needs no sort; histograms do
             HCK(h.key64 ? rle<unsigned long long>(h, s) : rle<uint32_t>(h, s));
         }
     }
@@ -518,10 +674,9 @@ cudaError_t hosts_sparse_export(int device, const HostRows& h, uint32_t* rows, u
 }
 
 void free_hosts(HostRows& h, cudaStream_t s) {
-    if (h.rows) cudaFreeAsync(h.rows, s);
-    if (h.sorted) cudaFreeAsync(h.sorted, s);
-    if (h.sp_keys) cudaFreeAsync(h.sp_keys, s);
-    if (h.sp_counts) cudaFreeAsync(h.sp_counts, s);
+    for (void* p : {static_cast<void*>(h.rows), h.sorted, h.sp_keys, static_cast<void*>(h.sp_counts),
+                    static_cast<void*>(h.row_of), static_cast<void*>(h.bkt)})
+        if (p) cudaFreeAsync(p, s);
     h = HostRows{};
 }
 

@@ -17,14 +17,16 @@ struct HostSlice {
 };
 
 // Device results of one post-pass; owned by the caller's context, released
-// with free_hosts. `sorted` keeps every flow's (host row, bucket) key in
-// (row, bucket) order for the optional histogram export.
+// with free_hosts. row_of/bkt keep every flow's (row, bucket) for the
+// optional histogram exports.
 struct HostRows {
     gnm_host_stats* rows = nullptr;
     uint64_t n_rows = 0;
-    void* sorted = nullptr; // u32 (row << 14 | bucket) or u64, per key64
-    bool key64 = false;
+    uint32_t* row_of = nullptr; // per flow: its row
+    uint32_t* bkt = nullptr;    // per flow: its bucket
     uint64_t n_flows = 0;
+    void* sorted = nullptr;     // (row << 14 | bucket) keys in order, u32 or u64 per key64; on demand
+    bool key64 = false;
     // Sparse histograms (run-length encoding of `sorted`), built on demand.
     void* sp_keys = nullptr; // unique (row << 14 | bucket), same width as `sorted`
     uint32_t* sp_counts = nullptr;
