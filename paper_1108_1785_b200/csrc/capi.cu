@@ -265,6 +265,8 @@ void ensure_out(gnm_ctx* c, uint32_t n_sites) {
     c->d_out = nullptr;
     c->h_out = nullptr;
     ck(cudaMalloc(&c->d_out, rows * sizeof(gnm_site_stats)), "cudaMalloc(out)");
+    // The last row holds only the 32 bytes of tallies; the rest stays zero.
+    ck(cudaMemset(c->d_out, 0, rows * sizeof(gnm_site_stats)), "cudaMemset(out)");
     ck(cudaMallocHost(&c->h_out, rows * sizeof(gnm_site_stats)), "cudaMallocHost(out)");
     c->out_cap_rows = rows;
 }

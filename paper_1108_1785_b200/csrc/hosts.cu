@@ -124,14 +124,16 @@ __device__ __forceinline__ void fold(uint32_t slot, unsigned long long lo, uint3
         atomicAdd(t.limb + e, static_cast<uint32_t>(lo) & 0xFFFFu);
         atomicAdd(t.limb + kAgg + e, static_cast<uint32_t>(lo) >> 16);
         atomicAdd(t.limb + 2 * kAgg + e, static_cast<uint32_t>(lo >> 32));
+        // Bounds move by shared atomics on the f32 bits (positive floats
+        // order as integers), only after their reduction was issued.
         const double r = __longlong_as_double(static_cast<long long>(rate));
         if (r < static_cast<double>(t.mn[e])) {
             red_max_u64(a + 3, ~rate);
-            t.mn[e] = __double2float_ru(r);
+            atomicMin(reinterpret_cast<int*>(t.mn + e), __float_as_int(__double2float_ru(r)));
         }
         if (r > static_cast<double>(t.mx[e])) {
             red_max_u64(a + 4, rate);
-            t.mx[e] = __double2float_rd(r);
+            atomicMax(reinterpret_cast<int*>(t.mx + e), __float_as_int(__double2float_rd(r)));
         }
         if (atomicAdd(t.cnt + e, 1u) + 1u == kFlushAt) {
             agg_flush(t, e, a);

@@ -414,16 +414,16 @@ __device__ __forceinline__ uint32_t accumulate(uint32_t code, uint32_t oct, uint
         else
             red_add(P.coarse + static_cast<size_t>(sb) * P.n_sites + site, 1u);
         // min/max: the slot's cached bounds filter the global reductions. The
-        // cache is written with plain stores AFTER the RED, so it only ever
-        // holds rates whose RED was issued; a lost race loosens the filter
-        // (an extra RED) but never hides a winning update.
+        // cache moves (shared atomics; rare after the first flows) only AFTER
+        // the RED, so it only ever holds rates whose RED was issued: a stale
+        // read costs an extra RED but never hides a winning update.
         if (rb < cmn) {
             red_min(P.mn + site, rb);
-            h.mn[slot] = rb;
+            atomicMin(h.mn + slot, rb);
         }
         if (rb > cmx) {
             red_max(P.mx + site, rb);
-            h.mx[slot] = rb;
+            atomicMax(h.mx + slot, rb);
         }
     } else {
         red_add(P.coarse + static_cast<size_t>(sb) * P.n_sites + site, 1u);
@@ -693,6 +693,20 @@ __device__ __forceinline__ void k2_epilogue(Ctr& t, WarpQueue& wq, uint32_t lane
     drain_full<kSmem, kHot, kHosts>(wq, lane, gt, p, P, h, t, L);
     drain_rest<kSmem, kHot, kHosts>(wq, lane, gt, p, P, h, t, L);
     if (lane == 0) L.counts[static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)] = wq.pos;
+    // Zero the region's entries up to the next multiple of 4: the log
+    // readers load whole 16-byte vectors (and ignore entries past the count).
+    const uint32_t i = wq.pos + lane;
+    if (lane < ((4u - (wq.pos & 3u)) & 3u)) {
+        wq.log[i] = 0;
+        if (wq.logb) wq.logb[i] = 0;
+        if constexpr (kHosts) {
+            const size_t j = wq.region_off + i;
+            L.hosts[j] = 0;
+            L.rates[j] = 0;
+            L.ulo[j] = 0;
+            L.uhi[j] = 0;
+        }
+    }
     flush_tallies(t, P.sums + static_cast<size_t>(P.n_sites) * 4);
     if constexpr (kHot) {
         __syncthreads();
