@@ -4,9 +4,12 @@
 //                         hot-site plan for skewed batches (see plan_hot)
 //   K2  k2_soa / k2_gen   classify -> attribute -> rate -> per-site aggregate
 //                         (reduce_slice, rate_engine.cpp:197-240 + add :9-23)
-//   K3  k3_finalize       per-site count / median / clamp / flag
+//   K3a k3a_median_sb     per-site count and median super-bucket (round 1)
+//   K2b k2b_fine          the median super-bucket's fine counts from the log
+//   K3b k3b_finalize      per-site median / clamp / avg / flag
 //                         (finalize + stats_from + median_bps,
 //                          rate_engine.cpp:42-58, 242-292; monitor.cpp:22)
+//       k_hist_from_log   dense histograms on request
 //       k_classify        per-record class/site (classify/attribute :71-86, 127-146)
 //
 // Paths are relative to /root/reference/proj/core/src.
@@ -19,19 +22,22 @@
 // grid, partitioning or GPU count.
 //
 // K2 is two stages per warp. Stage A (every lane, every record): the class
-// filter and the /16 directory bits of both endpoints. Candidates (~50% of
+// filter and the /16 directory bits of both endpoints. Candidates (~40% of
 // records at D3) are compacted into a per-warp shared-memory queue, and
 // stage B drains it 32 at a time with full warps: the /24 lookup tail, the
-// rate, the exact micro-bps, the bucket and the reductions.
+// rate, the exact micro-bps, the bucket and the reductions, plus one log
+// entry per flow (site, bucket) for the second round of the median.
 //
 // Contention: with Zipf-distributed sites the hottest site receives ~10% of
-// all Forward flows; same-address L2 atomics serialise (~1 ns each) and
-// returning shared-memory atomics expose their (contended) latency to the
-// warp. The scalar sums of the hot sites (the top 512 of a 1/64 sample, K1)
-// therefore accumulate in block-private shared memory through NON-returning
-// 32-bit adds of 16-bit limbs; a CTA processes < 2^16 records, so no limb
-// can overflow before the CTA's single flush. Cold sites and every histogram
-// bucket go straight to L2 with RED.
+// all Forward flows; same-address L2 atomics serialise and returning
+// shared-memory atomics expose their latency to the warp. The sums of the hot
+// sites (up to 2047, chosen by K1 from a 1/64 sample) therefore accumulate in
+// block-private shared memory through NON-returning 32-bit adds of 16-bit
+// limbs; a persistent CTA normalises the limbs at a barrier every
+// kEpochRounds rounds (fewer than 2^16 adds per limb in between), and the
+// top 32 hot sites also keep their coarse counts in shared memory. Cold sites
+// go straight to L2 with RED; the median needs only 157 coarse counts per
+// site (round 1) and, at finalize, the fine counts of one super-bucket.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -715,7 +721,7 @@ __device__ __forceinline__ void k2_epilogue(Ctr& t, WarpQueue& wq, uint32_t lane
 }
 
 // Main variant: SoA columns, 16-byte aligned, n < 2^32. Persistent: one
-// 1024-thread CTA per SM owns the contiguous 64-record tiles
+// 768-thread CTA per SM owns the contiguous 64-record tiles
 // [b*T/G, (b+1)*T/G) and walks them in rounds of kWarps tiles (warp w takes
 // tile t0 + r*kWarps + w), two records per lane per tile (one LDG.64 per u32
 // column, one LDG.128 per u64 column, non-allocating, evict-first),
