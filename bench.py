@@ -39,6 +39,18 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 ALG_BYTES_PER_RECORD = 32  # src, dst, d_pkts, d_octets (u32) + start_ms, end_ms (u64)
+NOMINAL_HBM_GBS = 8000.0   # the north star's "~8 TB/s" (SURVEY.md §8d asks for both fractions)
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 METRIC = "flow records/sec analysed"
 
 
@@ -237,7 +249,7 @@ def run_reference_arm(args):
                          "sample": f"first {args.cpu_sample} records of {args.workload}; "
                                    f"flowmon::aggregate(FilterParams{{}}, workers={best}, Hash); "
                                    f"probe ms by workers {json.dumps({str(k): round(v, 1) for k, v in probe.items()})}; "
-                                   f"nproc={nproc}"},
+                                   f"nproc={nproc}, cpu={cpu_model()}"},
         "e2e": {"value": value, "unit": "records/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -474,7 +486,8 @@ def main():
                      "traffic": traffic["bytes_per_launch"] if traffic else None,
                      "kernel": "k2_soa (classify+attribute+rate+aggregate)",
                      "kernel_ms": k2_avg, "alg_bytes_per_record": ALG_BYTES_PER_RECORD,
-                     "physical_bytes_per_record": ALG_BYTES_PER_RECORD if args.input == "soa" else 64},
+                     "physical_bytes_per_record": ALG_BYTES_PER_RECORD if args.input == "soa" else 64,
+                     "frac_of_nominal_8tbs": achieved / NOMINAL_HBM_GBS},
         "gpu_launches": launches,
         "clocks": clk,
         "kernel_share": k2_avg / (ms / args.steps),
@@ -491,7 +504,8 @@ def main():
                 "kind": "reference",
                 "sample": f"first {args.cpu_sample} records of {w.name}, unmodified flowmon::aggregate "
                           f"(oracle/_ref, -O3), median of {reps}; ms by workers "
-                          f"{json.dumps({str(k): round(v, 1) for k, v in t.items()})}"}
+                          f"{json.dumps({str(k): round(v, 1) for k, v in t.items()})}; "
+                          f"nproc={os.cpu_count()}, cpu={cpu_model()}"}
         except ImportError as e:
             line["cpu_baseline"] = {"value": None, "unit": "records/s", "cores": 0,
                                     "kind": "reference", "sample": f"unavailable: {e}"}
