@@ -249,3 +249,32 @@ def test_gpu_hosts_large_properties(hosts_engine):
     np.add.at(per_row, rows, c)
     np.testing.assert_array_equal(per_row, t["flow_count"])
     assert np.all(bks <= 10000)
+
+
+@pytest.mark.gpu
+def test_gpu_host_results_c_abi_errors(hosts_engine):
+    """The C-ABI's capacity rules (gnetmon.h): rows and sparse entries report
+    GNM_ERR_CAPACITY when the caller's arrays are short, the NULL query form
+    only sets the count, and rows outlive later accumulate calls until the
+    next finalize."""
+    import ctypes as C
+    from paper_1108_1785_b200 import _lib
+    cat = catalog_of([["10.1.1.0/24"], ["10.1.2.0/24"]])
+    ip = lambda a, b, c, d: (a << 24) | (b << 16) | (c << 8) | d
+    src = np.array([ip(10, 1, 1, 5), ip(10, 1, 1, 6), ip(10, 1, 2, 7)], np.uint32)
+    cols = parity.make_cols(src, np.full(3, 1, np.uint32), np.full(3, 50), np.full(3, 500_000), np.full(3, 1000))
+    hosts_engine.aggregate(FlowBatch(*cols), cat)
+    h = hosts_engine.handle
+    assert _lib.lib.gnm_host_count(h) == 3
+    rows = np.zeros(2, _lib.HOST_STATS_DTYPE)
+    assert _lib.lib.gnm_host_results(h, rows.ctypes.data, 2, None) == _lib.ERR_CAPACITY
+    n = C.c_uint64()
+    assert _lib.lib.gnm_host_histogram_entries(h, None, None, None, 0, C.byref(n)) == _lib.OK
+    assert n.value == 3
+    a = np.zeros(2, np.uint32)
+    assert _lib.lib.gnm_host_histogram_entries(h, a.ctypes.data, a.ctypes.data, a.ctypes.data, 2,
+                                               C.byref(n)) == _lib.ERR_CAPACITY
+    hosts_engine.accumulate(FlowBatch(*cols), cat)  # rows stay valid until the next finalize
+    assert _lib.lib.gnm_host_count(h) == 3
+    hosts_engine.reset()
+    assert _lib.lib.gnm_host_count(h) == 0
