@@ -226,6 +226,7 @@ void ensure_partials(gnm_ctx* c, uint32_t n_sites) {
             cudaFree(c->P.mrank);
             cudaFree(c->P.cnt);
             cudaFree(c->P.heavy_next);
+            cudaFree(c->P.map16);
             cudaFree(c->d_scratch);
             c->d_scratch = nullptr;
         }
@@ -240,6 +241,9 @@ void ensure_partials(gnm_ctx* c, uint32_t n_sites) {
         ck(cudaMalloc(&c->P.mrank, static_cast<size_t>(cap) * 4), "cudaMalloc(mrank)");
         ck(cudaMalloc(&c->P.cnt, static_cast<size_t>(cap) * 8), "cudaMalloc(cnt)");
         ck(cudaMalloc(&c->P.heavy_next, 4 * (1 + 64)), "cudaMalloc(heavy)"); // counter, row -> site
+        const size_t map_bytes = (static_cast<size_t>(cap) + 8) * 2; // whole 16-byte vectors
+        ck(cudaMalloc(&c->P.map16, map_bytes), "cudaMalloc(map16)");
+        ck(cudaMemsetAsync(c->P.map16, 0, map_bytes, c->stream), "cudaMemsetAsync(map16)");
         const size_t scratch_words = 2 * static_cast<size_t>(cap) + gnm::kHotStride + 1;
         ck(cudaMalloc(&c->d_scratch, scratch_words * 4), "cudaMalloc(scratch)");
         ck(cudaMemsetAsync(c->d_scratch, 0, scratch_words * 4, c->stream), "cudaMemsetAsync");
@@ -806,6 +810,7 @@ void gnm_ctx_destroy(gnm_ctx* c) {
     cudaFree(c->P.mrank);
     cudaFree(c->P.cnt);
     cudaFree(c->P.heavy_next);
+    cudaFree(c->P.map16);
     cudaFree(c->d_log);
     cudaFree(c->d_logb);
     cudaFree(c->d_counts);

@@ -1022,6 +1022,7 @@ __global__ void __launch_bounds__(128) k3a_median_sb(DevPartials P) {
             }
         }
         P.msb[site] = msb | hidx << 8;
+        P.map16[site] = static_cast<unsigned short>((msb & 0xFFu) | (hidx == kHeavyNone ? 0xFF00u : hidx << 8));
         P.mrank[site] = rank;
         P.cnt[site] = cnt;
     }
@@ -1039,14 +1040,12 @@ constexpr uint32_t kMapSites = 12288; // 24 KB of static shared memory
 template <bool kMap, bool kWide>
 __global__ void __launch_bounds__(512, 2) k2b_fine(DevPartials P, DevLog L) {
     __shared__ uint32_t hf[kHeavy * kFineW];
-    __shared__ uint16_t map[kMap ? kMapSites : 1];
+    __shared__ uint4 map4[kMap ? kMapSites / 8 : 1];
+    const uint16_t* map = reinterpret_cast<const uint16_t*>(map4);
     for (uint32_t i = threadIdx.x; i < kHeavy * kFineW; i += blockDim.x) hf[i] = 0;
-    if constexpr (kMap)
-        for (uint32_t i = threadIdx.x; i < P.n_sites; i += blockDim.x) {
-            const uint32_t m = __ldg(P.msb + i);
-            const uint32_t hh = m >> 8;
-            map[i] = static_cast<uint16_t>((m & 0xFFu) | (hh == kHeavyNone ? 0xFF00u : hh << 8));
-        }
+    if constexpr (kMap) // K3a's packed per-site map, 8 sites per 16-byte load
+        for (uint32_t i = threadIdx.x; i < (P.n_sites + 7) / 8; i += blockDim.x)
+            map4[i] = __ldg(reinterpret_cast<const uint4*>(P.map16) + i);
     __syncthreads();
     const uint32_t hf_base = static_cast<uint32_t>(__cvta_generic_to_shared(hf));
     const uint32_t lane = threadIdx.x & 31u;

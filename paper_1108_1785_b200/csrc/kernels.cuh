@@ -84,6 +84,7 @@ struct DevPartials {
     unsigned int* mrank;      // [n_sites]: rank of the lower median within it (1-based)
     unsigned long long* cnt;  // [n_sites]: flow count (K3a)
     unsigned int* heavy_next; // K3a's heavy-row counter, then the site of each heavy row
+    unsigned short* map16;    // [n_sites + 8]: K3a's (median super-bucket | heavy row << 8) for K2b
     uint32_t n_sites;
 };
 
