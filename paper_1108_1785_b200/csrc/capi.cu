@@ -244,7 +244,7 @@ void ensure_partials(gnm_ctx* c, uint32_t n_sites) {
         const size_t map_bytes = (static_cast<size_t>(cap) + 8) * 2; // whole 16-byte vectors
         ck(cudaMalloc(&c->P.map16, map_bytes), "cudaMalloc(map16)");
         ck(cudaMemsetAsync(c->P.map16, 0, map_bytes, c->stream), "cudaMemsetAsync(map16)");
-        const size_t scratch_words = 2 * static_cast<size_t>(cap) + gnm::kHotStride + 1;
+        const size_t scratch_words = gnm::plan_scratch_words(cap);
         ck(cudaMalloc(&c->d_scratch, scratch_words * 4), "cudaMalloc(scratch)");
         ck(cudaMemsetAsync(c->d_scratch, 0, scratch_words * 4, c->stream), "cudaMemsetAsync");
         c->P.n_sites = cap;
@@ -257,6 +257,9 @@ void ensure_partials(gnm_ctx* c, uint32_t n_sites) {
         c->P.n_sites = n_sites;
         ck(cudaMemsetAsync(c->P.sums + static_cast<size_t>(n_sites) * 4, 0, 32, c->stream),
            "cudaMemsetAsync");
+        // The hot-plan layout depends on n_sites: start from zero counts.
+        ck(cudaMemsetAsync(c->d_scratch, 0, gnm::plan_scratch_words(c->partial_cap) * 4, c->stream),
+           "cudaMemsetAsync(scratch)");
     }
 }
 
@@ -410,7 +413,7 @@ void launch_k2_timed(gnm_ctx* c, const gnm::DevBatch& b, const gnm::DevParams& p
     }
     const gnm::LaunchCfg cfg =
         hot ? gnm::k2_config(c->device, b, c->table.n_words, true, c->occ, c->hosts) : cold;
-    gnm::DevHot h{c->d_scratch + 2 * static_cast<size_t>(c->P.n_sites), hot ? gnm::kHotSlots : 0u};
+    gnm::DevHot h{c->d_scratch + gnm::plan_hot_site_offset(c->P.n_sites), hot ? gnm::kHotSlots : 0u};
     if (c->timing) {
         ck(cudaEventRecord(pe.b, c->stream), "cudaEventRecord");
         c->plan_pairs.push_back(pe);

@@ -830,8 +830,11 @@ __global__ void __launch_bounds__(kK2Block) k_sample(DevBatch b, const uint32_t*
                                                       uint32_t* __restrict__ cnt) {
     load_table<kSmem>(gt, table_words);
     if constexpr (kSmem) __syncthreads();
-    const uint64_t base = static_cast<uint64_t>(blockIdx.x) * chunk_stride;
-    for (uint32_t j = threadIdx.x; j < chunk_len; j += blockDim.x) {
+    // blockIdx.y picks the chunk; blockIdx.x * blockDim.x the first record
+    // within it: one record per thread, so the whole sample is one wave of
+    // independent lookup chains.
+    const uint64_t base = static_cast<uint64_t>(blockIdx.y) * chunk_stride;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < chunk_len; j += gridDim.x * blockDim.x) {
         const uint64_t i = base + j;
         uint32_t src, dst, pkts, oct;
         uint64_t dur, end;
@@ -861,23 +864,41 @@ __global__ void __launch_bounds__(kSelectBlock) k_hot_select(uint32_t* __restric
     for (uint32_t i = threadIdx.x; i < kCountBins; i += blockDim.x) bins[i] = 0;
     if (threadIdx.x == 0) next = 0;
     __syncthreads();
-    for (uint32_t s = threadIdx.x; s < n_sites; s += blockDim.x) {
-        const uint32_t c = cnt[s];
-        if (c >= thr) atomicAdd(&bins[min(c, kCountBins - 1)], 1u);
+    for (uint32_t s4 = threadIdx.x * 4; s4 < n_sites; s4 += blockDim.x * 4) { // 16-byte loads
+        const uint4 c4 = *reinterpret_cast<const uint4*>(cnt + s4);
+        const uint32_t cs[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q)
+            if (s4 + q < n_sites && cs[q] >= thr) atomicAdd(&bins[min(cs[q], kCountBins - 1)], 1u);
     }
     __syncthreads();
     // Suffix sums over the bins: thread i owns bins [4i, 4i+4).
     const uint32_t i0 = threadIdx.x * (kCountBins / kSelectBlock);
     uint32_t own = 0;
     for (uint32_t k = 0; k < kCountBins / kSelectBlock; ++k) own += bins[i0 + k];
-    part[threadIdx.x] = own;
-    __syncthreads();
-    for (uint32_t off = 1; off < kSelectBlock; off <<= 1) { // inclusive suffix scan
-        const uint32_t x = threadIdx.x + off < kSelectBlock ? part[threadIdx.x + off] : 0u;
-        __syncthreads();
-        part[threadIdx.x] += x;
-        __syncthreads();
+    // Inclusive suffix scan of `own` over the threads: within each warp by
+    // shuffles, then over the 32 warp totals by warp 0.
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    uint32_t suf = own;
+#pragma unroll
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_down_sync(0xFFFFFFFFu, suf, o);
+        if (lane + o < 32) suf += y;
     }
+    __shared__ uint32_t wsum[kSelectBlock / 32];
+    if (lane == 0) wsum[warp] = suf;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t v = wsum[lane], t = v;
+#pragma unroll
+        for (uint32_t o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_down_sync(0xFFFFFFFFu, t, o);
+            if (lane + o < 32) t += y;
+        }
+        wsum[lane] = t - v; // the warps after this one
+    }
+    __syncthreads();
+    part[threadIdx.x] = suf + wsum[warp];
     if (threadIdx.x == 0) {
         cut = 0xFFFFFFFFu;
         cut_a = 0xFFFFFFFFu;
@@ -908,14 +929,20 @@ __global__ void __launch_bounds__(kSelectBlock) k_hot_select(uint32_t* __restric
     __syncthreads();
     if (threadIdx.x == 0) next_a = 0;
     __syncthreads();
-    for (uint32_t s = threadIdx.x; s < n_sites; s += blockDim.x) {
-        const uint32_t c = cnt[s];
-        cnt[s] = 0;
-        uint32_t slot = 0;
-        if (c >= ta) slot = atomicAdd(&next_a, 1u) + 1;
-        else if (c >= t) slot = base_b + atomicAdd(&next, 1u) + 1;
-        if (slot) hot_site[slot] = s;
-        site_slot[s] = slot;
+    for (uint32_t s4 = threadIdx.x * 4; s4 < n_sites; s4 += blockDim.x * 4) {
+        const uint4 c4 = *reinterpret_cast<const uint4*>(cnt + s4);
+        const uint32_t cs[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q) {
+            const uint32_t s = s4 + q;
+            if (s >= n_sites) break;
+            cnt[s] = 0;
+            uint32_t slot = 0;
+            if (cs[q] >= ta) slot = atomicAdd(&next_a, 1u) + 1;
+            else if (cs[q] >= t) slot = base_b + atomicAdd(&next, 1u) + 1;
+            if (slot) hot_site[slot] = s;
+            site_slot[s] = slot;
+        }
     }
 }
 
@@ -1363,13 +1390,14 @@ bool plan_hot(int device, const DevBatch& b, const DevTable& t, const DevParams&
         if (thr > chunk_len * chunks) return false;
     }
     uint32_t* cnt = scratch;
-    uint32_t* site_slot = scratch + n_sites;
-    uint32_t* hot_site = site_slot + n_sites;
+    uint32_t* site_slot = scratch + plan_slot_offset(n_sites);
+    uint32_t* hot_site = scratch + plan_hot_site_offset(n_sites);
     const uint64_t stride = std::max<uint64_t>(b.n / chunks, chunk_len);
     const uint32_t nchunks = static_cast<uint32_t>(std::min<uint64_t>(chunks, b.n / chunk_len));
     // The sample is small: probe the table through L1 rather than copying
     // it into every CTA's shared memory.
-    k_sample<false><<<nchunks, kK2Block, 0, s>>>(b, t.words, t.n_words, p, stride, chunk_len, cnt);
+    const dim3 sg((chunk_len + 255) / 256, nchunks);
+    k_sample<false><<<sg, 256, 0, s>>>(b, t.words, t.n_words, p, stride, chunk_len, cnt);
     k_hot_select<<<1, kSelectBlock, 0, s>>>(cnt, n_sites, thr, site_slot, hot_site);
     const uint32_t span = t.n_words - t.node_begin;
     const uint32_t rg = std::max<uint32_t>(1, std::min<uint32_t>((span + 255) / 256, 1024));

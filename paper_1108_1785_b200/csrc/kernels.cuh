@@ -58,6 +58,12 @@ __device__ __forceinline__ double median_of_bucket(uint32_t k) {
 }
 #endif
 
+// Hot-site plan scratch (u32 words): per-site sample counts (padded to a
+// multiple of 4: read as 16-byte vectors), site -> slot, slot -> site.
+inline size_t plan_slot_offset(uint32_t n_sites) { return (static_cast<size_t>(n_sites) + 3) / 4 * 4; }
+inline size_t plan_hot_site_offset(uint32_t n_sites) { return plan_slot_offset(n_sites) + n_sites; }
+inline size_t plan_scratch_words(uint32_t n_sites) { return plan_hot_site_offset(n_sites) + kHotStride + 1; }
+
 struct DevParams {
     uint64_t ack_plus1;       // ack_avg_size_max + 1, u64 (rate_engine.cpp:78)
     uint32_t min_packets;
