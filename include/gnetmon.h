@@ -9,8 +9,11 @@
  * thread-local last-error string (gnm_last_error).
  *
  * Hot path:  classify -> attribute -> rate -> per-site
- * aggregate (K2, sm_100a) -> per-site median/avg/flag (K3, sm_100a) ->
- * streak rule (host).
+ * aggregate (K1 plan + K2, sm_100a) -> per-site median/avg/flag (K3a, K2b,
+ * K3b: the two-round exact median, sm_100a) -> streak rule (host).
+ * Around it (§8f): per-host rows (gnm_ctx_set_hosts), the snapshot window
+ * fused into K2 (gnm_*_window), NetFlow v5 decode (gnm_decode_netflow) and
+ * FLOWARC1 archives (gnm_decode_archive, gnm_*_archive).
  */
 #ifndef GNETMON_H
 #define GNETMON_H
@@ -298,7 +301,7 @@ int gnm_classify(gnm_ctx* ctx, const gnm_registry* reg, const gnm_filter_params*
  * the context stream. */
 typedef struct gnm_timing {
     double accumulate_ms; /* K2 (sum over launches since the last finalize) */
-    double finalize_ms;   /* K3 */
+    double finalize_ms;   /* K3a + K2b + K3b */
     double h2d_ms;        /* loader copies (host batches) */
     uint64_t k2_launches;
     uint64_t kernel_launches; /* every kernel this library launched since ctx creation */
