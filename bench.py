@@ -71,7 +71,7 @@ def parse_args():
                     help="record layout handed to the API: SoA columns (default, the north star's "
                          "loader layout) or the reference's 64-byte FlowRecord rows (gnm_analyze_aos)")
     ap.add_argument("--hosts", action="store_true",
-                    help="per-host mode: every step also builds SiteResult::hosts (N=1 only)")
+                    help="per-host mode: every step also builds SiteResult::hosts")
     return ap.parse_args()
 
 
@@ -390,9 +390,7 @@ def main():
     eng = Engine(local)
     eng.set_hot_mode(args.hot_mode)
     if args.hosts:
-        if world > 1:
-            raise SystemExit("--hosts: per-host rows are per context (N=1 only)")
-        eng.set_hosts(True)
+        eng.set_hosts(True)  # N > 1: distributed.combine also merges the host rows
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=f"cuda:{local}")
 
     def step(batch):

@@ -226,6 +226,35 @@ int gnm_host_results(gnm_ctx* ctx, gnm_host_stats* out, uint64_t capacity, uint3
 int gnm_host_histogram_entries(gnm_ctx* ctx, uint32_t* rows, uint32_t* buckets, uint32_t* counts,
                                uint64_t capacity, uint64_t* n_entries);
 
+/* Per-host rows across GPUs (hosts mode): the two-round protocol of
+ * gnm_partials applied to (site, host) rows. Per rank, after gnm_accumulate:
+ *   gnm_hosts_local_keys      this context's distinct keys (site << 32 | host),
+ *                             sorted, as a device array of *n u64;
+ *   [caller: the sorted union of every rank's keys, on this device]
+ *   gnm_hosts_set_keys        partials of the union: sums u64[3n] (micro-bps
+ *                             in 32-bit limbs) SUM, min f64[n] MIN (+inf
+ *                             where this rank has no flow of the row), max
+ *                             f64[n] MAX, coarse u32[157n] (super-bucket-
+ *                             major) SUM;
+ *   [caller: all-reduce them]
+ *   gnm_hosts_prepare_median  each row's median super-bucket; fine u32[64n]
+ *                             counts this rank's flows inside it;
+ *   [caller: all-reduce fine]
+ *   gnm_finalize              rows of the union (gnm_host_results; no
+ *                             histograms for combined rows).
+ * The union may hold up to 2^24 - 1 rows. */
+typedef struct gnm_host_partials {
+    uint64_t* sums;
+    double* min;
+    double* max;
+    uint32_t* coarse;
+    uint32_t* fine;
+    uint64_t n;
+} gnm_host_partials;
+int gnm_hosts_local_keys(gnm_ctx* ctx, const gnm_registry* reg, const uint64_t** keys, uint64_t* n);
+int gnm_hosts_set_keys(gnm_ctx* ctx, const uint64_t* keys, uint64_t n, gnm_host_partials* out);
+int gnm_hosts_prepare_median(gnm_ctx* ctx);
+
 /* aggregate() (rate_engine.cpp:335-347) + the K3 site synthesis
  * (finalize/stats_from, rate_engine.cpp:242-292) in one synchronous call.
  * Results are identical for any batch split (commutative monoid). */

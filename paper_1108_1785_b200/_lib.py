@@ -83,6 +83,11 @@ class gnm_partials(C.Structure):
                 ("fine_count", C.c_uint64)]
 
 
+class gnm_host_partials(C.Structure):
+    _fields_ = [("sums", C.c_void_p), ("min", C.c_void_p), ("max", C.c_void_p), ("coarse", C.c_void_p),
+                ("fine", C.c_void_p), ("n", C.c_uint64)]
+
+
 class gnm_netflow_stats(C.Structure):
     _fields_ = [("datagrams", C.c_uint64), ("decode_errors", C.c_uint64),
                 ("records_rejected", C.c_uint64), ("records_accepted", C.c_uint64)]
@@ -158,6 +163,9 @@ _SIGS = [
     ("gnm_host_count", C.c_uint64, [_P]),
     ("gnm_host_results", C.c_int, [_P, _P, C.c_uint64, _P]),
     ("gnm_host_histogram_entries", C.c_int, [_P, _P, _P, _P, C.c_uint64, C.POINTER(C.c_uint64)]),
+    ("gnm_hosts_local_keys", C.c_int, [_P, _P, C.POINTER(_P), C.POINTER(C.c_uint64)]),
+    ("gnm_hosts_set_keys", C.c_int, [_P, _P, C.c_uint64, C.POINTER(gnm_host_partials)]),
+    ("gnm_hosts_prepare_median", C.c_int, [_P]),
     ("gnm_analyze", C.c_int,
      [_P, _P, C.POINTER(gnm_filter_params), C.POINTER(gnm_batch_soa), C.POINTER(gnm_result)]),
     ("gnm_analyze_aos", C.c_int,

@@ -106,6 +106,8 @@ struct gnm_ctx {
     unsigned int* d_lhi = nullptr;
     size_t lhost_cap = 0;
     gnm::HostRows hrows;
+    gnm::HostLocal hlocal;   // hosts local phase done (gnm_hosts_local_keys)
+    gnm::HostGlobal hglobal; // cross-context rows (gnm_hosts_set_keys)
     bool prepared = false; // K3a + K2b ran (gnm_prepare_median) for this accumulation
     uint32_t* d_scratch = nullptr; // hot-site plan: counts, site->slot, slot->site, counter
     uint32_t partial_cap = 0;
@@ -573,6 +575,16 @@ int accumulate_aos(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params*
     return GNM_OK;
 }
 
+// Hosts local phase (H0..H2) on this context's log.
+cudaError_t build_hosts_local(gnm_ctx* c, const gnm_registry* reg) {
+    std::vector<gnm::HostSlice> hs;
+    for (const auto& sl : c->slices) hs.push_back({slice_view(c, sl), sl.entry_off, sl.count_off});
+    const uint64_t max_keys = 256ull * reg->r.entries().size(); // hosts lie in registered /24s
+    c->kernel_launches += 3 + hs.size(); // own kernels; cub scan/sorts not counted
+    return gnm::build_hosts_local(c->device, hs.data(), static_cast<int>(hs.size()), c->d_counts, c->counts_used,
+                                  max_keys, c->hrows, c->hlocal, c->stream);
+}
+
 // Round 1 -> round 2 of the median: K3a finds every site's median
 // super-bucket from the (possibly all-reduced) coarse counts, K2b rebuilds
 // that super-bucket's fine counts from this context's log.
@@ -609,7 +621,7 @@ int finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* r) {
     }
     const double thr = r->threshold_bps;
     const bool export_hist = r->histograms != nullptr;
-    gnm::free_hosts(c->hrows, c->stream);
+    if (!c->hlocal.ready) gnm::free_hosts(c->hrows, c->stream); // else: gnm_hosts_local_keys built them
     if (c->hosts && c->log_used >= (1ull << 32))
         return fail(GNM_ERR_CAPACITY, "per-host mode holds < 2^32 log entries per finalize");
     prepare_median(c);
@@ -639,13 +651,16 @@ int finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* r) {
     }
     if (c->hosts) {
         // SiteResult::hosts: the per-host post-pass over the same log.
-        std::vector<gnm::HostSlice> hs;
-        for (const auto& sl : c->slices) hs.push_back({slice_view(c, sl), sl.entry_off, sl.count_off});
-        const uint64_t max_keys = 256ull * reg->r.entries().size(); // hosts lie in registered /24s
-        ck(gnm::build_hosts(c->device, hs.data(), static_cast<int>(hs.size()), c->d_counts,
-                            c->counts_used, max_keys, c->hrows, c->stream),
-           "per-host post-pass");
-        c->kernel_launches += 6 + hs.size(); // own kernels; cub scan/sorts not counted
+        if (c->hglobal.prepared) { // rows of the cross-context union
+            ck(gnm::hosts_global_finish(c->device, c->hrows, c->hglobal, c->stream), "per-host rows (union)");
+            c->kernel_launches += 1;
+        } else {
+            if (!c->hlocal.ready) ck(build_hosts_local(c, reg), "per-host post-pass");
+            ck(gnm::finish_hosts(c->device, c->hrows, c->hlocal, c->stream), "per-host post-pass");
+            c->kernel_launches += 4;
+        }
+        gnm::free_local(c->hlocal, c->stream);
+        gnm::free_global(c->hglobal, c->stream);
     }
     clear_log(c);
     ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
@@ -822,6 +837,8 @@ void gnm_ctx_destroy(gnm_ctx* c) {
     cudaFree(c->d_llo);
     cudaFree(c->d_lhi);
     gnm::free_hosts(c->hrows, c->stream);
+    gnm::free_local(c->hlocal, c->stream);
+    gnm::free_global(c->hglobal, c->stream);
     if (c->stream) cudaStreamSynchronize(c->stream);
     cudaFree(c->d_scratch);
     cudaFree(c->d_out);
@@ -885,6 +902,7 @@ int gnm_host_results(gnm_ctx* c, gnm_host_stats* out, uint64_t capacity, uint32_
         if (n) ck(cudaMemcpyAsync(out, c->hrows.rows, n * sizeof(gnm_host_stats), cudaMemcpyDeviceToHost, c->stream),
                   "cudaMemcpyAsync(D2H host rows)");
         if (n && histograms) {
+            if (c->hrows.global) return fail(GNM_ERR_INVALID_ARGUMENT, "no histograms for cross-context rows");
             const size_t bytes = n * gnm::kBuckets * 4;
             uint32_t* dense = nullptr;
             ck(cudaMallocAsync(reinterpret_cast<void**>(&dense), bytes, c->stream), "cudaMallocAsync(host hist)");
@@ -905,6 +923,7 @@ int gnm_host_histogram_entries(gnm_ctx* c, uint32_t* rows, uint32_t* buckets, ui
     if (!c || !n_entries) return fail(GNM_ERR_INVALID_ARGUMENT, "null argument");
     return guarded([&] {
         ck(cudaSetDevice(c->device), "cudaSetDevice");
+        if (c->hrows.global) return fail(GNM_ERR_INVALID_ARGUMENT, "no histograms for cross-context rows");
         uint64_t n = 0;
         ck(gnm::hosts_sparse(c->device, c->hrows, &n, c->stream), "host histogram entries");
         *n_entries = n;
@@ -920,6 +939,54 @@ int gnm_host_histogram_entries(gnm_ctx* c, uint32_t* rows, uint32_t* buckets, ui
         ck(cudaMemcpyAsync(buckets, d + n, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H buckets");
         ck(cudaMemcpyAsync(counts, d + 2 * n, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H counts");
         ck(cudaFreeAsync(d, c->stream), "cudaFreeAsync(host entries)");
+        ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+        return static_cast<int>(GNM_OK);
+    });
+}
+
+int gnm_hosts_local_keys(gnm_ctx* c, const gnm_registry* reg, const uint64_t** keys, uint64_t* n) {
+    if (!c || !reg || !keys || !n) return fail(GNM_ERR_INVALID_ARGUMENT, "null argument");
+    if (!c->hosts) return fail(GNM_ERR_INVALID_ARGUMENT, "per-host mode is off (gnm_ctx_set_hosts)");
+    return guarded([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        if (int e = begin_accumulate(c, reg)) return e;
+        if (c->log_used >= (1ull << 32))
+            return fail(GNM_ERR_CAPACITY, "per-host mode holds < 2^32 log entries per finalize");
+        if (!c->hlocal.ready) ck(build_hosts_local(c, reg), "per-host local phase");
+        *keys = reinterpret_cast<const uint64_t*>(c->hlocal.hk_sorted);
+        *n = c->hrows.n_rows;
+        return static_cast<int>(GNM_OK);
+    });
+}
+
+int gnm_hosts_set_keys(gnm_ctx* c, const uint64_t* keys, uint64_t n, gnm_host_partials* out) {
+    if (!c || !out || (n && !keys)) return fail(GNM_ERR_INVALID_ARGUMENT, "null argument");
+    if (!c->hlocal.ready) return fail(GNM_ERR_INVALID_ARGUMENT, "gnm_hosts_local_keys first");
+    if (n >= (1ull << 24)) return fail(GNM_ERR_CAPACITY, "the key union holds at most 2^24 - 1 rows");
+    return guarded([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        ck(gnm::hosts_global_begin(c->device, c->hrows, c->hlocal, reinterpret_cast<const unsigned long long*>(keys),
+                                   n, c->hglobal, c->stream),
+           "per-host union partials");
+        c->kernel_launches += 4;
+        out->sums = reinterpret_cast<uint64_t*>(c->hglobal.sums);
+        out->min = reinterpret_cast<double*>(c->hglobal.min);
+        out->max = reinterpret_cast<double*>(c->hglobal.max);
+        out->coarse = c->hglobal.coarse;
+        out->fine = c->hglobal.fine;
+        out->n = n;
+        ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize"); // the caller's collectives read them
+        return static_cast<int>(GNM_OK);
+    });
+}
+
+int gnm_hosts_prepare_median(gnm_ctx* c) {
+    if (!c) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx");
+    if (!c->hglobal.keys) return fail(GNM_ERR_INVALID_ARGUMENT, "gnm_hosts_set_keys first");
+    return guarded([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        ck(gnm::hosts_global_prepare(c->device, c->hrows, c->hglobal, c->stream), "per-host round 2");
+        c->kernel_launches += 2;
         ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
         return static_cast<int>(GNM_OK);
     });
@@ -999,6 +1066,8 @@ int gnm_reset(gnm_ctx* c) {
         }
         clear_log(c);
         gnm::free_hosts(c->hrows, c->stream);
+        gnm::free_local(c->hlocal, c->stream);
+        gnm::free_global(c->hglobal, c->stream);
         drain_pairs(c, c->k2_pairs);
         drain_pairs(c, c->plan_pairs);
         drain_pairs(c, c->k3_pairs);

@@ -269,7 +269,7 @@ constexpr size_t kTwoRoundBytes = 64ull << 20;
 // CTA counts into a shared table first (first come, first served; a pair
 // whose entry is taken goes to L2 directly) and flushes it once.
 constexpr uint32_t kCoarseAgg = 4096;
-// Also turns every flow's slot into its row (in place).
+// With `rank`, also turns every flow's slot into its row (in place).
 __global__ void __launch_bounds__(512) h_coarse(uint32_t* __restrict__ row, const uint32_t* __restrict__ bk,
                                                 uint32_t n, uint32_t n_rows, const unsigned long long* __restrict__ rank,
                                                 uint32_t* __restrict__ coarse) {
@@ -280,8 +280,8 @@ __global__ void __launch_bounds__(512) h_coarse(uint32_t* __restrict__ row, cons
     }
     __syncthreads();
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-        const uint32_t r = static_cast<uint32_t>(rank[row[j]]), sb = bk[j] >> 6;
-        row[j] = r;
+        const uint32_t r = rank ? static_cast<uint32_t>(rank[row[j]]) : row[j], sb = bk[j] >> 6;
+        if (rank) row[j] = r;
         const uint32_t key = r << 8 | sb; // rows < 2^24 on this path (rows * 628 B <= 64 MB)
         const uint32_t e = (key * 2654435761u) >> (32 - 12);
         uint32_t cur = tkey[e];
@@ -531,10 +531,11 @@ cudaError_t finish_two_round(int device, HostRows& h, const unsigned long long* 
 
 } // namespace
 
-cudaError_t build_hosts(int device, const HostSlice* slices, int n_slices,
-                        const unsigned int* counts, size_t n_counts, uint64_t max_keys, HostRows& out,
-                        cudaStream_t s) {
+cudaError_t build_hosts_local(int device, const HostSlice* slices, int n_slices, const unsigned int* counts,
+                              size_t n_counts, uint64_t max_keys, HostRows& out, HostLocal& loc, cudaStream_t s) {
     free_hosts(out, s);
+    free_local(loc, s);
+    loc.ready = true;
     if (n_counts == 0) return cudaSuccess;
     Scratch tmp_(s);
     // H0: flat offsets of every warp region's entries.
@@ -560,54 +561,236 @@ cudaError_t build_hosts(int device, const HostSlice* slices, int n_slices,
     // H1: at least two slots per possible key.
     const int tbits = std::max(10, bits_for(2 * std::max<uint64_t>(1, std::min(n, max_keys))));
     const uint32_t cap = 1u << tbits;
-    unsigned long long *keys = nullptr, *acc = nullptr;
-    HCK(tmp_.get(&keys, cap));
-    HCK(tmp_.get(&acc, static_cast<size_t>(cap) * 5));
-    HCK(dalloc(&out.row_of, n, s)); // slots first, rows after H2; owned by `out`
+    HCK(dalloc(&loc.table, cap, s)); // owned by `loc` (free_local)
+    HCK(dalloc(&loc.acc, static_cast<size_t>(cap) * 5, s));
+    loc.cap = cap;
+    HCK(dalloc(&out.row_of, n, s)); // slots first, rows later; owned by `out`
     HCK(dalloc(&out.bkt, n, s));
     out.n_flows = n;
-    HCK(cudaMemsetAsync(keys, 0xFF, static_cast<size_t>(cap) * 8, s));
-    HCK(cudaMemsetAsync(acc, 0, static_cast<size_t>(cap) * 40, s));
+    HCK(cudaMemsetAsync(loc.table, 0xFF, static_cast<size_t>(cap) * 8, s));
+    HCK(cudaMemsetAsync(loc.acc, 0, static_cast<size_t>(cap) * 40, s));
     for (int i = 0; i < n_slices; ++i) {
         const HostSlice& sl = slices[i];
         // Four CTAs per SM, fewer for small logs.
         const uint64_t items = static_cast<uint64_t>(sl.log.regions) * ((sl.log.warp_cap + kInsChunk - 1) / kInsChunk);
         const uint32_t g = std::min<uint32_t>(grid_for(device, items * 32, kInsBlock), 4 * sms);
-        h_insert<<<g, kInsBlock, kInsSmem, s>>>(sl.log, counts + sl.count_off, off + sl.count_off, keys, cap - 1,
-                                                64 - tbits, acc, out.row_of, out.bkt);
+        h_insert<<<g, kInsBlock, kInsSmem, s>>>(sl.log, counts + sl.count_off, off + sl.count_off, loc.table,
+                                                cap - 1, 64 - tbits, loc.acc, out.row_of, out.bkt);
         HCK(cudaGetLastError());
     }
     // H2: distinct keys in (site, host) order -> rows.
-    unsigned long long *hk = nullptr, *hk_sorted = nullptr;
-    uint32_t *hs = nullptr, *hs_sorted = nullptr;
+    unsigned long long* hk = nullptr;
+    uint32_t* hs = nullptr;
     const uint64_t kcap = std::min<uint64_t>(n, cap);
     HCK(tmp_.get(&hk, kcap));
     HCK(tmp_.get(&hs, kcap));
-    h_collect<<<grid_for(device, cap, 256), 256, 0, s>>>(keys, cap, hk, hs,
+    h_collect<<<grid_for(device, cap, 256), 256, 0, s>>>(loc.table, cap, hk, hs,
                                                         reinterpret_cast<unsigned int*>(scal + 1));
     HCK(cudaGetLastError());
     HCK(cudaMemcpyAsync(h_scal + 1, scal + 1, 8, cudaMemcpyDeviceToHost, s));
     HCK(cudaStreamSynchronize(s));
     const uint32_t n_rows = static_cast<uint32_t>(h_scal[1]);
-    HCK(tmp_.get(&hk_sorted, n_rows));
-    HCK(tmp_.get(&hs_sorted, n_rows));
+    HCK(dalloc(&loc.hk_sorted, n_rows, s));
+    HCK(dalloc(&loc.hs_sorted, n_rows, s));
     tb = 0;
-    HCK(cub::DeviceRadixSort::SortPairs(nullptr, tb, hk, hk_sorted, hs, hs_sorted, n_rows, 0, 64, s));
+    HCK(cub::DeviceRadixSort::SortPairs(nullptr, tb, hk, loc.hk_sorted, hs, loc.hs_sorted, n_rows, 0, 64, s));
     unsigned char* tmp2 = nullptr;
     HCK(tmp_.get(&tmp2, tb));
-    HCK(cub::DeviceRadixSort::SortPairs(tmp2, tb, hk, hk_sorted, hs, hs_sorted, n_rows, 0, 64, s));
-    h_rank<<<grid_for(device, n_rows, 256), 256, 0, s>>>(hs_sorted, n_rows, keys);
+    HCK(cub::DeviceRadixSort::SortPairs(tmp2, tb, hk, loc.hk_sorted, hs, loc.hs_sorted, n_rows, 0, 64, s));
+    h_rank<<<grid_for(device, n_rows, 256), 256, 0, s>>>(loc.hs_sorted, n_rows, loc.table);
     HCK(cudaGetLastError());
     out.n_rows = n_rows;
     out.key64 = kBucketBits + bits_for(n_rows) > 32;
-    HCK(dalloc(&out.rows, n_rows, s));
-    // H3..H5: the exact lower median per row (slots become rows on the way).
-    if (static_cast<size_t>(n_rows) * kCoarseH * 4 <= kTwoRoundBytes)
-        return finish_two_round(device, out, keys, acc, hk_sorted, hs_sorted, s);
-    h_to_rows<<<grid_for(device, n, 256), 256, 0, s>>>(out.row_of, static_cast<uint32_t>(n), keys);
-    HCK(cudaGetLastError());
-    return out.key64 ? finish_sorted<unsigned long long>(device, out, acc, hk_sorted, hs_sorted, s)
-                     : finish_sorted<uint32_t>(device, out, acc, hk_sorted, hs_sorted, s);
+    return cudaSuccess;
+}
+
+cudaError_t finish_hosts(int device, HostRows& out, HostLocal& loc, cudaStream_t s) {
+    cudaError_t e = cudaSuccess;
+    if (out.n_flows) {
+        const uint32_t n_rows = static_cast<uint32_t>(out.n_rows);
+        e = dalloc(&out.rows, n_rows, s);
+        // H3..H5: the exact lower median per row (slots become rows on the way).
+        if (e == cudaSuccess) {
+            if (static_cast<size_t>(n_rows) * kCoarseH * 4 <= kTwoRoundBytes) {
+                e = finish_two_round(device, out, loc.table, loc.acc, loc.hk_sorted, loc.hs_sorted, s);
+            } else {
+                h_to_rows<<<grid_for(device, out.n_flows, 256), 256, 0, s>>>(
+                    out.row_of, static_cast<uint32_t>(out.n_flows), loc.table);
+                e = cudaGetLastError();
+                if (e == cudaSuccess)
+                    e = out.key64 ? finish_sorted<unsigned long long>(device, out, loc.acc, loc.hk_sorted,
+                                                                      loc.hs_sorted, s)
+                                  : finish_sorted<uint32_t>(device, out, loc.acc, loc.hk_sorted, loc.hs_sorted, s);
+            }
+        }
+    }
+    free_local(loc, s);
+    return e;
+}
+
+cudaError_t build_hosts(int device, const HostSlice* slices, int n_slices, const unsigned int* counts,
+                        size_t n_counts, uint64_t max_keys, HostRows& out, cudaStream_t s) {
+    HostLocal loc;
+    const cudaError_t e = build_hosts_local(device, slices, n_slices, counts, n_counts, max_keys, out, loc, s);
+    if (e != cudaSuccess) {
+        free_local(loc, s);
+        return e;
+    }
+    return finish_hosts(device, out, loc, s);
+}
+
+// ---- cross-context combine ---------------------------------------------------------
+namespace {
+// Local row -> its index in the sorted union (every local key is in it).
+__global__ void g_map(const unsigned long long* __restrict__ local, uint32_t n_local,
+                      const unsigned long long* __restrict__ global, uint32_t n_global, uint32_t* __restrict__ map) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_local; r += gridDim.x * blockDim.x) {
+        const unsigned long long k = local[r];
+        uint32_t lo = 0, hi = n_global;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (global[mid] < k) lo = mid + 1;
+            else hi = mid;
+        }
+        map[r] = lo;
+    }
+}
+
+__global__ void g_init_min(unsigned long long* __restrict__ mn, uint32_t n) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) mn[r] = kMinInitBits;
+}
+
+__global__ void g_fill(const uint32_t* __restrict__ map, const uint32_t* __restrict__ hs_sorted, uint32_t n_local,
+                       const unsigned long long* __restrict__ acc, unsigned long long* __restrict__ sums,
+                       unsigned long long* __restrict__ mn, unsigned long long* __restrict__ mx) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_local; r += gridDim.x * blockDim.x) {
+        const unsigned long long* a = acc + static_cast<size_t>(hs_sorted[r]) * 5;
+        const uint32_t g = map[r];
+        sums[static_cast<size_t>(g) * 3 + 0] = a[0];
+        sums[static_cast<size_t>(g) * 3 + 1] = a[1];
+        sums[static_cast<size_t>(g) * 3 + 2] = a[2];
+        mn[g] = ~a[3]; // the slot keeps its min complemented
+        mx[g] = a[4];
+    }
+}
+
+// Every flow's slot -> its global row.
+__global__ void g_rows(uint32_t* __restrict__ row, uint32_t n, const unsigned long long* __restrict__ table,
+                       const uint32_t* __restrict__ map) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+        row[j] = map[static_cast<uint32_t>(table[row[j]])];
+}
+
+__global__ void g_final(const unsigned long long* __restrict__ keys, const unsigned long long* __restrict__ sums,
+                        const unsigned long long* __restrict__ mn, const unsigned long long* __restrict__ mx,
+                        const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ msb,
+                        const uint32_t* __restrict__ mrank, const uint32_t* __restrict__ fine, uint32_t n,
+                        gnm_host_stats* __restrict__ rows) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        const uint32_t* f = fine + static_cast<size_t>(r) * kFineH;
+        uint32_t cum = 0, k = msb[r] * kFineH + kFineH - 1;
+        for (uint32_t q = 0; q < kFineH; ++q) {
+            cum += f[q];
+            if (cum >= mrank[r]) {
+                k = msb[r] * kFineH + q;
+                break;
+            }
+        }
+        const unsigned long long* a = sums + static_cast<size_t>(r) * 3;
+        const unsigned __int128 u = static_cast<unsigned __int128>(a[0]) +
+                                    (static_cast<unsigned __int128>(a[1]) << 32) +
+                                    (static_cast<unsigned __int128>(a[2]) << 64);
+        const double lo_b = __longlong_as_double(static_cast<long long>(mn[r]));
+        const double hi_b = __longlong_as_double(static_cast<long long>(mx[r]));
+        double med = median_of_bucket(k);
+        med = med < lo_b ? lo_b : (hi_b < med ? hi_b : med);
+        gnm_host_stats o;
+        o.site = static_cast<uint32_t>(keys[r] >> 32);
+        o.host = static_cast<uint32_t>(keys[r]);
+        o.flow_count = cnt[r];
+        o.rate_ubps_lo = static_cast<uint64_t>(u);
+        o.rate_ubps_hi = static_cast<uint64_t>(u >> 64);
+        o.min_bps = lo_b;
+        o.max_bps = hi_b;
+        o.avg_bps = avg_of(o.rate_ubps_lo, o.rate_ubps_hi, o.flow_count);
+        o.median_bps = med;
+        rows[r] = o;
+    }
+}
+} // namespace
+
+cudaError_t hosts_global_begin(int device, HostRows& out, const HostLocal& loc, const unsigned long long* keys,
+                               uint64_t n, HostGlobal& g, cudaStream_t s) {
+    free_global(g, s);
+    if (n >= (1ull << 24)) return cudaErrorInvalidValue; // the coarse pass keys rows in 24 bits
+    g.n = n;
+    const size_t ng = std::max<uint64_t>(n, 1);
+    HCK(dalloc(&g.keys, ng, s));
+    HCK(dalloc(&g.local_to_global, std::max<uint64_t>(out.n_rows, 1), s));
+    HCK(dalloc(&g.sums, ng * 3, s));
+    HCK(dalloc(&g.min, ng, s));
+    HCK(dalloc(&g.max, ng, s));
+    HCK(dalloc(&g.coarse, ng * kCoarseH, s));
+    HCK(dalloc(&g.fine, ng * kFineH, s));
+    HCK(dalloc(&g.msb, ng, s));
+    HCK(dalloc(&g.mrank, ng, s));
+    HCK(dalloc(&g.cnt, ng, s));
+    if (n) HCK(cudaMemcpyAsync(g.keys, keys, n * 8, cudaMemcpyDeviceToDevice, s));
+    HCK(cudaMemsetAsync(g.sums, 0, ng * 24, s));
+    g_init_min<<<grid_for(device, ng, 256), 256, 0, s>>>(g.min, static_cast<uint32_t>(ng));
+    HCK(cudaMemsetAsync(g.max, 0, ng * 8, s));
+    HCK(cudaMemsetAsync(g.coarse, 0, ng * kCoarseH * 4, s));
+    HCK(cudaMemsetAsync(g.fine, 0, ng * kFineH * 4, s));
+    const uint32_t nl = static_cast<uint32_t>(out.n_rows);
+    if (nl) {
+        g_map<<<grid_for(device, nl, 256), 256, 0, s>>>(loc.hk_sorted, nl, g.keys, static_cast<uint32_t>(n),
+                                                        g.local_to_global);
+        g_fill<<<grid_for(device, nl, 256), 256, 0, s>>>(g.local_to_global, loc.hs_sorted, nl, loc.acc, g.sums,
+                                                         g.min, g.max);
+        const uint32_t nf = static_cast<uint32_t>(out.n_flows);
+        g_rows<<<grid_for(device, nf, 256), 256, 0, s>>>(out.row_of, nf, loc.table, g.local_to_global);
+        h_coarse<<<grid_for(device, nf, 512), 512, 0, s>>>(out.row_of, out.bkt, nf, static_cast<uint32_t>(n),
+                                                           nullptr, g.coarse);
+        HCK(cudaGetLastError());
+    }
+    out.global = true;
+    return cudaSuccess;
+}
+
+cudaError_t hosts_global_prepare(int device, const HostRows& out, HostGlobal& g, cudaStream_t s) {
+    const uint32_t n = static_cast<uint32_t>(g.n), nf = static_cast<uint32_t>(out.n_flows);
+    if (n) h_msb<<<grid_for(device, n, 128), 128, 0, s>>>(g.coarse, n, g.msb, g.mrank, g.cnt);
+    if (nf) h_fine<<<grid_for(device, nf, 256), 256, 0, s>>>(out.row_of, out.bkt, nf, g.msb, g.fine);
+    g.prepared = true;
+    return cudaGetLastError();
+}
+
+cudaError_t hosts_global_finish(int device, HostRows& out, HostGlobal& g, cudaStream_t s) {
+    if (out.rows) cudaFreeAsync(out.rows, s);
+    out.rows = nullptr;
+    const uint32_t n = static_cast<uint32_t>(g.n);
+    HCK(dalloc(&out.rows, std::max<uint32_t>(n, 1), s));
+    if (n)
+        g_final<<<grid_for(device, n, 128), 128, 0, s>>>(g.keys, g.sums, g.min, g.max, g.cnt, g.msb, g.mrank,
+                                                         g.fine, n, out.rows);
+    out.n_rows = n;
+    return cudaGetLastError();
+}
+
+void free_local(HostLocal& loc, cudaStream_t s) {
+    for (void* p : {static_cast<void*>(loc.table), static_cast<void*>(loc.acc), static_cast<void*>(loc.hk_sorted),
+                    static_cast<void*>(loc.hs_sorted)})
+        if (p) cudaFreeAsync(p, s);
+    loc = HostLocal{};
+}
+
+void free_global(HostGlobal& g, cudaStream_t s) {
+    for (void* p : {static_cast<void*>(g.keys), static_cast<void*>(g.local_to_global), static_cast<void*>(g.sums),
+                    static_cast<void*>(g.min), static_cast<void*>(g.max), static_cast<void*>(g.coarse),
+                    static_cast<void*>(g.fine), static_cast<void*>(g.msb), static_cast<void*>(g.mrank),
+                    static_cast<void*>(g.cnt)})
+        if (p) cudaFreeAsync(p, s);
+    g = HostGlobal{};
 }
 
 cudaError_t hosts_histograms(int device, const HostRows& h, uint32_t* dense, cudaStream_t s) {

@@ -27,11 +27,58 @@ struct HostRows {
     uint64_t n_flows = 0;
     void* sorted = nullptr;     // (row << 14 | bucket) keys in order, u32 or u64 per key64; on demand
     bool key64 = false;
+    bool global = false;        // rows are a cross-context union: histograms would be local only
     // Sparse histograms (run-length encoding of `sorted`), built on demand.
     void* sp_keys = nullptr; // unique (row << 14 | bucket), same width as `sorted`
     uint32_t* sp_counts = nullptr;
     uint64_t n_sparse = ~0ull; // ~0: not built yet
 };
+
+// The local phase's state, kept for the cross-GPU combine (H0..H2 done).
+struct HostLocal {
+    unsigned long long* table = nullptr;     // slot -> local row (after H2)
+    unsigned long long* acc = nullptr;       // per slot {limb0, limb1, limb2, ~min, max}
+    unsigned long long* hk_sorted = nullptr; // local distinct keys (site << 32 | host), sorted
+    uint32_t* hs_sorted = nullptr;           // local row -> slot
+    uint32_t cap = 0;
+    bool ready = false;
+};
+
+// Global rows of a multi-context combine (gnm_hosts_*): every rank's
+// partials indexed by the union of all ranks' keys, reduced by the caller
+// (sums / coarse / fine: SUM; min: MIN; max: MAX -- f64 bits, +inf / 0
+// where a rank saw no flow of the row).
+struct HostGlobal {
+    unsigned long long* keys = nullptr; // [n] sorted union of keys
+    uint32_t* local_to_global = nullptr;
+    unsigned long long* sums = nullptr; // [n * 3] micro-bps limbs
+    unsigned long long* min = nullptr;  // [n] min rate bits
+    unsigned long long* max = nullptr;  // [n]
+    uint32_t* coarse = nullptr;         // [157 * n] super-bucket-major
+    uint32_t* fine = nullptr;           // [n * 64]
+    uint32_t* msb = nullptr;
+    uint32_t* mrank = nullptr;
+    uint32_t* cnt = nullptr;
+    uint64_t n = 0;
+    bool prepared = false;
+};
+
+// Local phase (H0..H2): flat per-flow (slot, bucket), per-slot sums, the
+// sorted local keys; `out.n_rows` = local rows. Then either finish_hosts
+// (this context's rows) or the global combine below.
+cudaError_t build_hosts_local(int device, const HostSlice* slices, int n_slices, const unsigned int* counts,
+                              size_t n_counts, uint64_t max_keys, HostRows& out, HostLocal& loc, cudaStream_t s);
+cudaError_t finish_hosts(int device, HostRows& out, HostLocal& loc, cudaStream_t s);
+// Global combine: begin (map local rows into the union, fill sums/min/max
+// and coarse counts), [caller all-reduces], prepare (each row's median
+// super-bucket, this context's fine counts), [caller all-reduces fine],
+// finish (rows of the union in out.rows).
+cudaError_t hosts_global_begin(int device, HostRows& out, const HostLocal& loc, const unsigned long long* keys,
+                               uint64_t n, HostGlobal& g, cudaStream_t s);
+cudaError_t hosts_global_prepare(int device, const HostRows& out, HostGlobal& g, cudaStream_t s);
+cudaError_t hosts_global_finish(int device, HostRows& out, HostGlobal& g, cudaStream_t s);
+void free_local(HostLocal& loc, cudaStream_t s);
+void free_global(HostGlobal& g, cudaStream_t s);
 
 // Builds the per-host rows from the log slices and all per-warp counts.
 // max_keys bounds the distinct (site, host) keys (256 per registry /24

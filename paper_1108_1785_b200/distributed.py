@@ -54,7 +54,8 @@ def allreduce_fine(t: dict, group=None) -> None:
 
 
 def combine(engine, catalog, group=None, stream=None) -> None:
-    """The whole combine for one rank's engine: round 1, prepare, round 2.
+    """The whole combine for one rank's engine: round 1, prepare, round 2
+    (and, in per-host mode, the same for the (site, host) rows).
     ``stream``: the torch stream wrapping the engine's stream (collectives
     are ordered after K2 on it)."""
     t = engine.device_tensors(catalog)
@@ -64,6 +65,44 @@ def combine(engine, catalog, group=None, stream=None) -> None:
     engine.prepare_median(catalog)
     with ctx:
         allreduce_fine(t, group)
+    if getattr(engine, "_hosts", False):
+        combine_hosts(engine, catalog, group, stream)
+
+
+def key_union(local: torch.Tensor, group=None) -> torch.Tensor:
+    """Sorted union of every rank's sorted int64 keys (variable lengths)."""
+    world = dist.get_world_size(group)
+    n = torch.tensor([local.numel()], dtype=torch.int64, device=local.device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    m = max(int(x.item()) for x in sizes)
+    pad = torch.full((max(m, 1),), -1, dtype=torch.int64, device=local.device)
+    pad[:local.numel()] = local
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    allk = torch.cat([p[:int(k.item())] for p, k in zip(parts, sizes)])
+    return torch.unique(allk, sorted=True)
+
+
+def combine_hosts(engine, catalog, group=None, stream=None) -> None:
+    """Per-host rows across ranks (gnetmon.h gnm_hosts_*): the union of the
+    ranks' (site, host) keys, then the two rounds of the exact median on
+    the union's rows. Keys are site << 32 | host (< 2^63: int64 order is
+    the key order)."""
+    local = engine.hosts_local_keys(catalog)
+    union = key_union(local, group)
+    t = engine.hosts_set_keys(union)
+    ctx = torch.cuda.stream(stream) if stream is not None else _nullctx()
+    with ctx:
+        dist.all_reduce(t["sums"], op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(t["coarse"], op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(t["min_bps"], op=dist.ReduceOp.MIN, group=group)
+        dist.all_reduce(t["max_bps"], op=dist.ReduceOp.MAX, group=group)
+    torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
+    engine.hosts_prepare_median()
+    with ctx:
+        dist.all_reduce(t["fine"], op=dist.ReduceOp.SUM, group=group)
+    torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
 
 
 class _nullctx:

@@ -747,6 +747,41 @@ class Engine:
             "fine": torch.as_tensor(_View(p["fine"][0], p["fine"][1], "<i4"), device=dev),
         }
 
+    # -- per-host rows across GPUs (gnetmon.h gnm_hosts_*) --------------------------
+    def _view(self, ptr, n, typestr):
+        import torch
+
+        class _V:
+            def __init__(self):
+                self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                                 "version": 3}
+        return torch.as_tensor(_V(), device=torch.device("cuda", self.device))
+
+    def hosts_local_keys(self, catalog: SiteCatalog):
+        """This context's distinct (site << 32 | host) keys, sorted: a zero-copy
+        int64 CUDA tensor (valid until finalize)."""
+        import torch
+        ptr, n = C.c_void_p(), C.c_uint64()
+        _check(lib.gnm_hosts_local_keys(self._h, catalog.handle, C.byref(ptr), C.byref(n)))
+        if n.value == 0:
+            return torch.empty(0, dtype=torch.int64, device=torch.device("cuda", self.device))
+        return self._view(ptr.value, n.value, "<i8")
+
+    def hosts_set_keys(self, keys) -> dict:
+        """Round 1 of the per-host combine: partials of the sorted key union
+        (an int64 CUDA tensor on this device) as zero-copy tensors."""
+        keys = keys.contiguous()
+        p = _lib.gnm_host_partials()
+        _check(lib.gnm_hosts_set_keys(self._h, keys.data_ptr() if keys.numel() else None, keys.numel(),
+                                      C.byref(p)))
+        n = max(p.n, 1)
+        return {"sums": self._view(p.sums, 3 * n, "<i8"), "min_bps": self._view(p.min, n, "<f8"),
+                "max_bps": self._view(p.max, n, "<f8"), "coarse": self._view(p.coarse, 157 * n, "<i4"),
+                "fine": self._view(p.fine, 64 * n, "<i4"), "n": p.n}
+
+    def hosts_prepare_median(self) -> None:
+        _check(lib.gnm_hosts_prepare_median(self._h))
+
     def classify(self, batch: FlowBatch, catalog: SiteCatalog,
                  params: Optional[FilterParams] = None, out=None):
         """Per-record class << 30 | site (gnm_classify)."""

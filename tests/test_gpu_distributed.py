@@ -75,7 +75,8 @@ def test_two_rank_combine_on_device_matches_single(engine, workload, n):
                                                       np.uint64))
 
 
-def test_bench_multi_rank_line():
+@pytest.mark.parametrize("extra", [[], ["--hosts"]])
+def test_bench_multi_rank_line(extra):
     """bench.py's N>1 path (index shards, the combine every step, barrier +
     max-over-ranks timing) under torchrun with two ranks; gloo and one
     device here (test hooks), NCCL on a multi-GPU box."""
@@ -87,7 +88,7 @@ def test_bench_multi_rank_line():
     out = subprocess.run(
         [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
          "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
-         "--records", "3000000", "--steps", "3", "--warmup", "3", "--e2e-steps", "1", "--no-cpu-baseline"],
+         "--records", "3000000", "--steps", "3", "--warmup", "3", "--e2e-steps", "1", "--no-cpu-baseline"] + extra,
         cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
@@ -95,3 +96,58 @@ def test_bench_multi_rank_line():
     d = lines[0]
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
     assert d["config"]["parallelism"] == "index shards x2"
+
+
+def _rank_hosts(rank, world, port, outdir, n, workload):
+    import torch
+    import torch.distributed as dist
+    from paper_1108_1785_b200 import Engine, FlowBatch, SiteCatalog, synth
+    from paper_1108_1785_b200 import distributed as D
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    w = synth.workload(workload)
+    cols = synth.generate(w, n)
+    cat = SiteCatalog()
+    w.sites.register(cat)
+    a, b = D.shard_range(n, rank, world)
+    eng = Engine(0)
+    eng.set_hosts(True)
+    stream = torch.cuda.ExternalStream(eng.stream_handle(), device="cuda:0")
+    for _ in range(2):
+        eng.accumulate(FlowBatch(*[c[a:b] for c in cols]).to_device(), cat)
+        torch.cuda.synchronize()
+        D.combine(eng, cat, stream=stream)  # site rows and, in per-host mode, host rows
+        res = eng.finalize(cat)
+    np.save(os.path.join(outdir, f"table{rank}.npy"), res.table)
+    np.save(os.path.join(outdir, f"hosts{rank}.npy"), res.host_table)
+    eng.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("workload,n", [("D1", 300_001), ("D3", 1_500_007)])
+def test_two_rank_host_rows_match_single(engine, workload, n):
+    """Per-host rows across ranks (gnm_hosts_*): the union of the ranks'
+    (site, host) keys and the two-round median on it give every rank the
+    single engine's rows bit-exactly."""
+    import torch.multiprocessing as mp
+    from paper_1108_1785_b200 import FlowBatch, SiteCatalog, synth
+
+    w = synth.workload(workload)
+    cols = synth.generate(w, n)
+    cat = SiteCatalog()
+    w.sites.register(cat)
+    engine.set_hosts(True)
+    try:
+        want = engine.aggregate(FlowBatch(*cols).to_device(), cat)
+    finally:
+        engine.set_hosts(False)
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_rank_hosts, args=(2, _free_port(), d, n, workload), nprocs=2, join=True)
+        for r in range(2):
+            np.testing.assert_array_equal(np.load(os.path.join(d, f"table{r}.npy")), want.table)
+            np.testing.assert_array_equal(np.load(os.path.join(d, f"hosts{r}.npy")), want.host_table,
+                                          err_msg=f"rank {r}")
