@@ -278,3 +278,25 @@ def test_gpu_host_results_c_abi_errors(hosts_engine):
     assert _lib.lib.gnm_host_count(h) == 3
     hosts_engine.reset()
     assert _lib.lib.gnm_host_count(h) == 0
+
+
+@pytest.mark.gpu
+def test_gpu_hosts_union_path_single_context(hosts_engine):
+    """The cross-context path with one context (union = its own keys, no
+    collective): gnm_hosts_local_keys -> set_keys -> prepare_median ->
+    finalize gives the same rows as the local path; histograms are refused
+    for union rows."""
+    w = synth.workload("D2")
+    cols = synth.generate(w, 300_000)
+    cat = SiteCatalog()
+    w.sites.register(cat)
+    want = hosts_engine.aggregate(FlowBatch(*cols).to_device(), cat).host_table
+    hosts_engine.accumulate(FlowBatch(*cols).to_device(), cat)
+    keys = hosts_engine.hosts_local_keys(cat)
+    t = hosts_engine.hosts_set_keys(keys.clone())
+    assert t["n"] == len(want)
+    hosts_engine.hosts_prepare_median()
+    res = hosts_engine.finalize(cat)
+    np.testing.assert_array_equal(res.host_table, want)
+    with pytest.raises(Exception):
+        hosts_engine.host_histogram_entries()

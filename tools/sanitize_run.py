@@ -2,7 +2,7 @@
 (tools/sanitize.sh): K1/K2/K3 on SoA host and AoS inputs with histograms and
 a fused window, hot-slot modes, per-host rows (both median paths: two-round
 and sorted), NetFlow decode (golden datagrams), FLOWARC1 decode and in-place
-analysis. Host numpy inputs only (no torch allocations in the trace)."""
+analysis. Host numpy inputs (torch only for the key union of the cross-context path)."""
 import os
 import sys
 
@@ -45,6 +45,13 @@ with Engine(0) as eng:
     rb = eng.aggregate(FlowBatch(*bcols), big)
     assert len(rb.host_table) > 100_000, len(rb.host_table)
     eng.host_histogram_entries()
+    # the cross-context union path with one context
+    eng.accumulate(FlowBatch(*bcols), big)
+    import torch
+    keys = eng.hosts_local_keys(big)
+    eng.hosts_set_keys(keys.clone())
+    eng.hosts_prepare_median()
+    eng.finalize(big)
     eng.set_hosts(False)
     z = golden_io.load("netflow")
     eng.decode_netflow(z["datagrams"], z["offsets"])
