@@ -206,6 +206,13 @@ int gnm_ctx_set_chunk_records(gnm_ctx* ctx, uint64_t records);
 #define GNM_HOT_AUTO 1
 #define GNM_HOT_FORCE 2
 int gnm_ctx_set_hot_mode(gnm_ctx* ctx, int mode);
+/* CUDA graphs (default on): a gnm_analyze / gnm_analyze_window call on a
+ * DEVICE batch that repeats the previous call's inputs (column pointers,
+ * size, registry and version, parameters, window, threshold, hot mode)
+ * replays one captured graph of the whole device phase instead of launching
+ * its kernels one by one. Results are identical; the batch's contents may
+ * change between calls. Not used with timing, per-host mode or histograms. */
+int gnm_ctx_set_graphs(gnm_ctx* ctx, int enable);
 /* Per-host mode (off by default): K2 also logs each Forward flow's host,
  * rate and micro-bps, and every finalize then builds the per-host rows,
  * sorted by (site, host) like the reference's std::map iteration. Only

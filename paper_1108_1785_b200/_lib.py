@@ -160,6 +160,7 @@ _SIGS = [
     ("gnm_ctx_set_chunk_records", C.c_int, [_P, C.c_uint64]),
     ("gnm_ctx_set_hot_mode", C.c_int, [_P, C.c_int]),
     ("gnm_ctx_set_hosts", C.c_int, [_P, C.c_int]),
+    ("gnm_ctx_set_graphs", C.c_int, [_P, C.c_int]),
     ("gnm_host_count", C.c_uint64, [_P]),
     ("gnm_host_results", C.c_int, [_P, _P, C.c_uint64, _P]),
     ("gnm_host_histogram_entries", C.c_int, [_P, _P, _P, _P, C.c_uint64, C.POINTER(C.c_uint64)]),

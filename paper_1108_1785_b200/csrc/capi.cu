@@ -108,6 +108,29 @@ struct gnm_ctx {
     gnm::HostRows hrows;
     gnm::HostLocal hlocal;   // hosts local phase done (gnm_hosts_local_keys)
     gnm::HostGlobal hglobal; // cross-context rows (gnm_hosts_set_keys)
+
+    // CUDA graph of a repeated device-batch analysis (analyze_graphed)
+    bool graphs = true;
+    struct GraphKey {
+        const void* cols[6];
+        uint64_t n;
+        const gnm_registry* reg;
+        uint64_t version;
+        gnm_filter_params params;
+        uint64_t win_lo, win_hi;
+        int windowed;
+        double threshold;
+        int hot_mode;
+        uint32_t n_sites;
+        uint64_t alloc_gen;
+        bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof o) == 0; }
+    } gkey{};
+    // Bumped whenever a buffer or baked-in size a captured graph refers to
+    // changes (table upload, partials, log, output staging).
+    uint64_t alloc_gen = 0;
+    bool gkey_valid = false;
+    cudaGraphExec_t gexec = nullptr;
+    uint64_t g_kernels = 0; // kernels per replay (launch accounting)
     bool prepared = false; // K3a + K2b ran (gnm_prepare_median) for this accumulation
     uint32_t* d_scratch = nullptr; // hot-site plan: counts, site->slot, slot->site, counter
     uint32_t partial_cap = 0;
@@ -212,6 +235,7 @@ void ensure_table(gnm_ctx* c, const gnm_registry* reg) {
     c->occ[0] = c->occ[1] = 0;
     c->reg = reg;
     c->reg_version = reg->r.version();
+    c->alloc_gen += 1;
 }
 
 // Partials sized for the registry's site count; all-zero (min=+inf) at rest.
@@ -253,12 +277,14 @@ void ensure_partials(gnm_ctx* c, uint32_t n_sites) {
         ck(gnm::launch_init_partials(c->P, c->stream), "init partials");
         c->kernel_launches += 1;
         c->partial_cap = cap;
+        c->alloc_gen += 1;
     }
     if (c->P.n_sites != n_sites) {
         // Tallies live after the last site row: move them (zero at rest).
         c->P.n_sites = n_sites;
         ck(cudaMemsetAsync(c->P.sums + static_cast<size_t>(n_sites) * 4, 0, 32, c->stream),
            "cudaMemsetAsync");
+        c->alloc_gen += 1;
         // The hot-plan layout depends on n_sites: start from zero counts.
         ck(cudaMemsetAsync(c->d_scratch, 0, gnm::plan_scratch_words(c->partial_cap) * 4, c->stream),
            "cudaMemsetAsync(scratch)");
@@ -278,6 +304,7 @@ void ensure_out(gnm_ctx* c, uint32_t n_sites) {
     ck(cudaMemset(c->d_out, 0, rows * sizeof(gnm_site_stats)), "cudaMemset(out)");
     ck(cudaMallocHost(&c->h_out, rows * sizeof(gnm_site_stats)), "cudaMallocHost(out)");
     c->out_cap_rows = rows;
+    c->alloc_gen += 1;
 }
 
 void ensure_stage(gnm_ctx* c, size_t bytes_per_slot, bool need_host) {
@@ -355,6 +382,7 @@ void grow_buf(gnm_ctx* c, T** buf, size_t* cap, size_t used, size_t need, const 
     }
     *buf = nb;
     *cap = ncap;
+    c->alloc_gen += 1;
 }
 
 void grow_u32(gnm_ctx* c, unsigned int** buf, size_t* cap, size_t used, size_t need, const char* what) {
@@ -606,12 +634,15 @@ void clear_log(gnm_ctx* c) {
     c->prepared = false;
 }
 
-int finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* r) {
+// phase: 1 = the device work (stream-ordered, capturable), 2 = the host
+// part (wait, copy the rows out, reset the accumulation), 3 = both.
+int finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* r, int phase = 3) {
     if (!r) return fail(GNM_ERR_INVALID_ARGUMENT, "null result");
     const uint32_t n_sites = static_cast<uint32_t>(reg->r.sites().size());
     if (r->sites_capacity < n_sites || (n_sites && !r->sites))
         return fail(GNM_ERR_CAPACITY, "result.sites holds " + std::to_string(r->sites_capacity) +
                                           " rows, registry has " + std::to_string(n_sites) + " sites");
+    if (phase & 1) {
     if (int e = begin_accumulate(c, reg)) return e; // no-op when already accumulating
     ensure_out(c, n_sites);
     EventPair ev;
@@ -662,6 +693,8 @@ int finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* r) {
         gnm::free_local(c->hlocal, c->stream);
         gnm::free_global(c->hglobal, c->stream);
     }
+    } // device phase
+    if (!(phase & 2)) return GNM_OK;
     clear_log(c);
     ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
     // K3b computed every field, avg included (rounded like the host's libgcc).
@@ -854,6 +887,7 @@ void gnm_ctx_destroy(gnm_ctx* c) {
             cudaEventDestroy(p.a);
             cudaEventDestroy(p.b);
         }
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     delete c;
@@ -1270,12 +1304,108 @@ int gnm_accumulate_window_aos(gnm_ctx* c, const gnm_registry* reg, const gnm_fil
     return guarded([&] { return accumulate_aos(c, reg, params, batch, &w); });
 }
 
+namespace {
+void drop_graph(gnm_ctx* c) {
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    c->gexec = nullptr;
+}
+
+// A device-batch analysis repeated with the same inputs (column pointers,
+// sizes, registry version, parameters, window) replays one CUDA graph of
+// its whole device phase (K1, K2, K3a, K2b, K3b, the resets and the row
+// copy-out): the second identical call captures it, later ones launch it.
+// Only the host part (wait, rows out) runs per call. Not for host batches,
+// per-host mode, histogram export or timing (their host-side work differs
+// per call), nor on the legacy default stream.
+int analyze_graphed(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* params,
+                    const gnm_batch_soa* b, gnm_result* r, const Window* win) {
+    gnm_ctx::GraphKey k;
+    std::memset(&k, 0, sizeof k);
+    const void* cols[6] = {b->src_addr, b->dst_addr, b->d_pkts, b->d_octets, b->start_ms, b->end_ms};
+    for (int i = 0; i < 6; ++i) k.cols[i] = cols[i];
+    k.n = b->n;
+    k.reg = reg;
+    k.version = reg->r.version();
+    if (params) k.params = *params;
+    else gnm_filter_params_default(&k.params);
+    k.windowed = win != nullptr;
+    k.win_lo = win ? win->lo : 0;
+    k.win_hi = win ? win->hi : 0;
+    k.threshold = r->threshold_bps;
+    k.hot_mode = c->hot_mode;
+    k.n_sites = static_cast<uint32_t>(reg->r.sites().size());
+    // The registry's table and partials for this call (a no-op when nothing
+    // changed; any reallocation or upload bumps alloc_gen and so the key).
+    if (int e = begin_accumulate(c, reg)) return e;
+    c->accumulating = false;
+    k.alloc_gen = c->alloc_gen;
+    const bool same = c->gkey_valid && k == c->gkey;
+    if (same && c->gexec) {
+        ck(cudaGraphLaunch(c->gexec, c->stream), "cudaGraphLaunch");
+        c->kernel_launches += c->g_kernels;
+        c->k2_launches += 1;
+        c->records = b->n;
+        return finalize(c, reg, r, 2);
+    }
+    if (!same) {
+        drop_graph(c);
+        c->gkey = k;
+        c->gkey_valid = true;
+        if (int e = accumulate_soa(c, reg, params, b, win)) return e;
+        return finalize(c, reg, r);
+    }
+    // Second identical call: capture the device phase, then launch it.
+    const uint64_t k0 = c->kernel_launches;
+    ck(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+    int e = GNM_OK;
+    try {
+        e = accumulate_soa(c, reg, params, b, win);
+        if (e == GNM_OK) e = finalize(c, reg, r, 1);
+    } catch (...) {
+        e = GNM_ERR_CUDA;
+    }
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+    cudaError_t ie = cudaErrorUnknown;
+    if (e == GNM_OK && ce == cudaSuccess && g && c->alloc_gen == k.alloc_gen)
+        ie = cudaGraphInstantiate(&c->gexec, g, 0);
+    if (g) cudaGraphDestroy(g);
+    clear_log(c); // the captured work has not run: start the accumulation over
+    c->accumulating = false;
+    if (ie != cudaSuccess) { // not capturable here: plain calls from now on
+        cudaGetLastError();
+        c->gexec = nullptr;
+        c->graphs = false;
+        c->kernel_launches = k0;
+        if (int e2 = accumulate_soa(c, reg, params, b, win)) return e2;
+        return finalize(c, reg, r);
+    }
+    c->g_kernels = c->kernel_launches - k0;
+    ck(cudaGraphLaunch(c->gexec, c->stream), "cudaGraphLaunch");
+    return finalize(c, reg, r, 2);
+}
+
+bool graph_eligible(const gnm_ctx* c, const gnm_batch_soa* b, const gnm_result* r) {
+    return c->graphs && !c->timing && !c->hosts && b && b->mem == GNM_MEM_DEVICE && b->n > 0 && r &&
+           !r->histograms && c->stream != nullptr;
+}
+} // namespace
+
+int gnm_ctx_set_graphs(gnm_ctx* c, int enable) {
+    if (!c) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx");
+    c->graphs = enable != 0;
+    c->gkey_valid = false;
+    drop_graph(c);
+    return GNM_OK;
+}
+
 int gnm_analyze_window(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* params,
                        const gnm_batch_soa* batch, gnm_result* result) {
     if (!c || !reg || !result) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx/registry/result");
     if (c->accumulating) return fail(GNM_ERR_INVALID_ARGUMENT, "an accumulation is in progress");
     const Window w{result->window_start_ms, result->window_end_ms};
     return guarded([&] {
+        if (graph_eligible(c, batch, result)) return analyze_graphed(c, reg, params, batch, result, &w);
         if (int e = accumulate_soa(c, reg, params, batch, &w)) return e;
         return finalize(c, reg, result);
     });
@@ -1286,6 +1416,7 @@ int gnm_analyze(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* pa
     if (!c || !reg) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx/registry");
     if (c->accumulating) return fail(GNM_ERR_INVALID_ARGUMENT, "an accumulation is in progress");
     return guarded([&] {
+        if (graph_eligible(c, batch, result)) return analyze_graphed(c, reg, params, batch, result, nullptr);
         if (int e = accumulate_soa(c, reg, params, batch)) return e;
         return finalize(c, reg, result);
     });

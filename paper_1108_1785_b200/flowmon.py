@@ -516,6 +516,10 @@ class Engine:
         m = {"off": _lib.HOT_OFF, "auto": _lib.HOT_AUTO, "force": _lib.HOT_FORCE}[mode]
         _check(lib.gnm_ctx_set_hot_mode(self._h, m))
 
+    def set_graphs(self, on: bool = True) -> None:
+        """Replay one CUDA graph for repeated device-batch analyses (default on)."""
+        _check(lib.gnm_ctx_set_graphs(self._h, 1 if on else 0))
+
     def set_hosts(self, on: bool = True) -> None:
         """Per-host mode (SiteResult::hosts, rate_engine.cpp:272-289): every
         later result carries ``host_table`` and ``sites[s].hosts``. Only

@@ -261,3 +261,44 @@ def test_window_fused_aos(engine, orc):
     got = engine.aggregate_window(FlowRecords(synth.to_aos(cols)), cat, lo, hi)
     m = _window_mask(cols, lo, hi)
     parity.assert_matches_oracle(got, parity.oracle_reference(orc, cat, tuple(np.ascontiguousarray(c[m]) for c in cols)))
+
+
+def test_graph_replay_matches_plain_calls(engine, orc):
+    """Repeated device-batch calls replay a captured CUDA graph: identical
+    results to graphs off, across in-place data changes, a registry switch
+    in between (partials / table / log reallocated), hot-mode changes and a
+    fused window."""
+    import torch
+    from paper_1108_1785_b200 import Engine
+    w = synth.workload("D2")
+    cols = synth.generate(w, 400_000)
+    cat = layout_catalog(w.sites)
+    dev = [torch.from_numpy(c.view(np.int32 if c.dtype.itemsize == 4 else np.int64).copy()).cuda() for c in cols]
+    batch = FlowBatch(*dev)
+    plain = Engine(0)
+    plain.set_graphs(False)
+    want = plain.aggregate(batch, cat)
+    for _ in range(4):  # plain, capture, replays
+        got = engine.aggregate(batch, cat)
+        np.testing.assert_array_equal(got.table, want.table)
+    # contents change in place: the replay reads the new data
+    dev[3].mul_(2)
+    want2 = plain.aggregate(batch, cat)
+    got2 = engine.aggregate(batch, cat)
+    np.testing.assert_array_equal(got2.table, want2.table)
+    assert not np.array_equal(got2.table, want.table)
+    # another registry (bigger) in between, then the first again
+    big = layout_catalog(synth.workload("D3").sites)
+    engine.aggregate(FlowBatch(*synth.generate(synth.workload("D3"), 300_000)).to_device(), big)
+    for _ in range(3):
+        np.testing.assert_array_equal(engine.aggregate(batch, cat).table, want2.table)
+    for mode in ("off", "force", "auto"):
+        engine.set_hot_mode(mode)
+        for _ in range(3):
+            np.testing.assert_array_equal(engine.aggregate(batch, cat).table, want2.table)
+    end = cols[5]
+    lo, hi = int(np.percentile(end, 25)), int(np.percentile(end, 75))
+    wantw = plain.aggregate_window(batch, cat, lo, hi)
+    for _ in range(3):
+        np.testing.assert_array_equal(engine.aggregate_window(batch, cat, lo, hi).table, wantw.table)
+    plain.close()

@@ -53,6 +53,11 @@ with Engine(0) as eng:
     eng.hosts_prepare_median()
     eng.finalize(big)
     eng.set_hosts(False)
+    # repeated device-batch calls: plain, capture, graph replays
+    import torch
+    dcols = [torch.from_numpy(c.view(np.int32 if c.dtype.itemsize == 4 else np.int64).copy()).cuda() for c in cols]
+    for _ in range(4):
+        eng.aggregate(FlowBatch(*dcols), cat)
     z = golden_io.load("netflow")
     eng.decode_netflow(z["datagrams"], z["offsets"])
     arc = make_archive(cols)
