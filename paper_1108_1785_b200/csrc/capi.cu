@@ -643,56 +643,56 @@ int finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* r, int phase = 3) 
         return fail(GNM_ERR_CAPACITY, "result.sites holds " + std::to_string(r->sites_capacity) +
                                           " rows, registry has " + std::to_string(n_sites) + " sites");
     if (phase & 1) {
-    if (int e = begin_accumulate(c, reg)) return e; // no-op when already accumulating
-    ensure_out(c, n_sites);
-    EventPair ev;
-    if (c->timing) {
-        ev = take_pair(c);
-        ck(cudaEventRecord(ev.a, c->stream), "cudaEventRecord");
-    }
-    const double thr = r->threshold_bps;
-    const bool export_hist = r->histograms != nullptr;
-    if (!c->hlocal.ready) gnm::free_hosts(c->hrows, c->stream); // else: gnm_hosts_local_keys built them
-    if (c->hosts && c->log_used >= (1ull << 32))
-        return fail(GNM_ERR_CAPACITY, "per-host mode holds < 2^32 log entries per finalize");
-    prepare_median(c);
-    ck(gnm::launch_k3b(c->device, c->P, thr, c->d_out, 1, c->stream), "K3b launch");
-    c->kernel_launches += 1;
-    if (c->timing) {
-        ck(cudaEventRecord(ev.b, c->stream), "cudaEventRecord");
-        c->k3_pairs.push_back(ev);
-    }
-    ck(cudaMemcpyAsync(c->h_out, c->d_out, (static_cast<size_t>(n_sites) + 1) * sizeof(gnm_site_stats),
-                       cudaMemcpyDeviceToHost, c->stream),
-       "cudaMemcpyAsync(D2H)");
-    if (export_hist) {
-        // RateHistogram::buckets_ per site, rebuilt exactly from the log.
-        const size_t bytes = static_cast<size_t>(n_sites) * gnm::kBuckets * 4;
-        uint32_t* dense = nullptr;
-        ck(cudaMallocAsync(reinterpret_cast<void**>(&dense), std::max<size_t>(bytes, 4), c->stream),
-           "cudaMallocAsync(hist export)");
-        ck(cudaMemsetAsync(dense, 0, bytes, c->stream), "cudaMemsetAsync(hist export)");
-        for (const auto& sl : c->slices) {
-            ck(gnm::launch_hist_from_log(c->device, slice_view(c, sl), n_sites, dense, c->stream), "hist export");
-            c->kernel_launches += 1;
+        if (int e = begin_accumulate(c, reg)) return e; // no-op when already accumulating
+        ensure_out(c, n_sites);
+        EventPair ev;
+        if (c->timing) {
+            ev = take_pair(c);
+            ck(cudaEventRecord(ev.a, c->stream), "cudaEventRecord");
         }
-        ck(cudaMemcpyAsync(r->histograms, dense, bytes, cudaMemcpyDeviceToHost, c->stream),
-           "cudaMemcpyAsync(D2H hist)");
-        ck(cudaFreeAsync(dense, c->stream), "cudaFreeAsync(hist export)");
-    }
-    if (c->hosts) {
-        // SiteResult::hosts: the per-host post-pass over the same log.
-        if (c->hglobal.prepared) { // rows of the cross-context union
-            ck(gnm::hosts_global_finish(c->device, c->hrows, c->hglobal, c->stream), "per-host rows (union)");
-            c->kernel_launches += 1;
-        } else {
-            if (!c->hlocal.ready) ck(build_hosts_local(c, reg), "per-host post-pass");
-            ck(gnm::finish_hosts(c->device, c->hrows, c->hlocal, c->stream), "per-host post-pass");
-            c->kernel_launches += 4;
+        const double thr = r->threshold_bps;
+        const bool export_hist = r->histograms != nullptr;
+        if (!c->hlocal.ready) gnm::free_hosts(c->hrows, c->stream); // else: gnm_hosts_local_keys built them
+        if (c->hosts && c->log_used >= (1ull << 32))
+            return fail(GNM_ERR_CAPACITY, "per-host mode holds < 2^32 log entries per finalize");
+        prepare_median(c);
+        ck(gnm::launch_k3b(c->device, c->P, thr, c->d_out, 1, c->stream), "K3b launch");
+        c->kernel_launches += 1;
+        if (c->timing) {
+            ck(cudaEventRecord(ev.b, c->stream), "cudaEventRecord");
+            c->k3_pairs.push_back(ev);
         }
-        gnm::free_local(c->hlocal, c->stream);
-        gnm::free_global(c->hglobal, c->stream);
-    }
+        ck(cudaMemcpyAsync(c->h_out, c->d_out, (static_cast<size_t>(n_sites) + 1) * sizeof(gnm_site_stats),
+                           cudaMemcpyDeviceToHost, c->stream),
+           "cudaMemcpyAsync(D2H)");
+        if (export_hist) {
+            // RateHistogram::buckets_ per site, rebuilt exactly from the log.
+            const size_t bytes = static_cast<size_t>(n_sites) * gnm::kBuckets * 4;
+            uint32_t* dense = nullptr;
+            ck(cudaMallocAsync(reinterpret_cast<void**>(&dense), std::max<size_t>(bytes, 4), c->stream),
+               "cudaMallocAsync(hist export)");
+            ck(cudaMemsetAsync(dense, 0, bytes, c->stream), "cudaMemsetAsync(hist export)");
+            for (const auto& sl : c->slices) {
+                ck(gnm::launch_hist_from_log(c->device, slice_view(c, sl), n_sites, dense, c->stream), "hist export");
+                c->kernel_launches += 1;
+            }
+            ck(cudaMemcpyAsync(r->histograms, dense, bytes, cudaMemcpyDeviceToHost, c->stream),
+               "cudaMemcpyAsync(D2H hist)");
+            ck(cudaFreeAsync(dense, c->stream), "cudaFreeAsync(hist export)");
+        }
+        if (c->hosts) {
+            // SiteResult::hosts: the per-host post-pass over the same log.
+            if (c->hglobal.prepared) { // rows of the cross-context union
+                ck(gnm::hosts_global_finish(c->device, c->hrows, c->hglobal, c->stream), "per-host rows (union)");
+                c->kernel_launches += 1;
+            } else {
+                if (!c->hlocal.ready) ck(build_hosts_local(c, reg), "per-host post-pass");
+                ck(gnm::finish_hosts(c->device, c->hrows, c->hlocal, c->stream), "per-host post-pass");
+                c->kernel_launches += 4;
+            }
+            gnm::free_local(c->hlocal, c->stream);
+            gnm::free_global(c->hglobal, c->stream);
+        }
     } // device phase
     if (!(phase & 2)) return GNM_OK;
     clear_log(c);
