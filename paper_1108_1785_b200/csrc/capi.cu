@@ -128,6 +128,7 @@ struct gnm_ctx {
     // Bumped whenever a buffer or baked-in size a captured graph refers to
     // changes (table upload, partials, log, output staging).
     uint64_t alloc_gen = 0;
+    bool capturing = false; // inside analyze_graphed's stream capture: no (re)allocation allowed
     bool gkey_valid = false;
     cudaGraphExec_t gexec = nullptr;
     uint64_t g_kernels = 0; // kernels per replay (launch accounting)
@@ -294,6 +295,7 @@ void ensure_partials(gnm_ctx* c, uint32_t n_sites) {
 void ensure_out(gnm_ctx* c, uint32_t n_sites) {
     const size_t rows = static_cast<size_t>(n_sites) + 1; // + tallies
     if (rows <= c->out_cap_rows) return;
+    if (c->capturing) throw CudaError("cudaMalloc(out): no allocation during graph capture");
     ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
     if (c->d_out) cudaFree(c->d_out);
     if (c->h_out) cudaFreeHost(c->h_out);
@@ -373,6 +375,7 @@ gnm::DevLog slice_view(const gnm_ctx* c, const gnm_ctx::LogSlice& sl) {
 template <typename T>
 void grow_buf(gnm_ctx* c, T** buf, size_t* cap, size_t used, size_t need, const char* what) {
     if (need <= *cap) return;
+    if (c->capturing) throw CudaError(std::string(what) + ": no allocation during graph capture");
     const size_t ncap = std::max(need, *cap + *cap / 2);
     T* nb = nullptr;
     ck(cudaMallocAsync(reinterpret_cast<void**>(&nb), ncap * sizeof(T), c->stream), what);
@@ -1358,12 +1361,14 @@ int analyze_graphed(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params
     const uint64_t k0 = c->kernel_launches;
     ck(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
     int e = GNM_OK;
+    c->capturing = true;
     try {
         e = accumulate_soa(c, reg, params, b, win);
         if (e == GNM_OK) e = finalize(c, reg, r, 1);
     } catch (...) {
         e = GNM_ERR_CUDA;
     }
+    c->capturing = false;
     cudaGraph_t g = nullptr;
     const cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
     cudaError_t ie = cudaErrorUnknown;
