@@ -123,6 +123,7 @@ struct gnm_ctx {
         int hot_mode;
         uint32_t n_sites;
         uint64_t alloc_gen;
+        int aos;
         bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof o) == 0; }
     } gkey{};
     // Bumped whenever a buffer or baked-in size a captured graph refers to
@@ -1321,12 +1322,21 @@ void drop_graph(gnm_ctx* c) {
 // per-host mode, histogram export or timing (their host-side work differs
 // per call), nor on the legacy default stream.
 int analyze_graphed(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* params,
-                    const gnm_batch_soa* b, gnm_result* r, const Window* win) {
+                    const gnm_batch_soa* b, const gnm_batch_aos* ba, gnm_result* r, const Window* win) {
     gnm_ctx::GraphKey k;
     std::memset(&k, 0, sizeof k);
-    const void* cols[6] = {b->src_addr, b->dst_addr, b->d_pkts, b->d_octets, b->start_ms, b->end_ms};
-    for (int i = 0; i < 6; ++i) k.cols[i] = cols[i];
-    k.n = b->n;
+    if (b) {
+        const void* cols[6] = {b->src_addr, b->dst_addr, b->d_pkts, b->d_octets, b->start_ms, b->end_ms};
+        for (int i = 0; i < 6; ++i) k.cols[i] = cols[i];
+        k.n = b->n;
+    } else {
+        k.cols[0] = ba->records;
+        k.n = ba->n;
+        k.aos = 1;
+    }
+    auto accumulate = [&]() {
+        return b ? accumulate_soa(c, reg, params, b, win) : accumulate_aos(c, reg, params, ba, win);
+    };
     k.reg = reg;
     k.version = reg->r.version();
     if (params) k.params = *params;
@@ -1347,14 +1357,14 @@ int analyze_graphed(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params
         ck(cudaGraphLaunch(c->gexec, c->stream), "cudaGraphLaunch");
         c->kernel_launches += c->g_kernels;
         c->k2_launches += 1;
-        c->records = b->n;
+        c->records = k.n;
         return finalize(c, reg, r, 2);
     }
     if (!same) {
         drop_graph(c);
         c->gkey = k;
         c->gkey_valid = true;
-        if (int e = accumulate_soa(c, reg, params, b, win)) return e;
+        if (int e = accumulate()) return e;
         return finalize(c, reg, r);
     }
     // Second identical call: capture the device phase, then launch it.
@@ -1363,7 +1373,7 @@ int analyze_graphed(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params
     int e = GNM_OK;
     c->capturing = true;
     try {
-        e = accumulate_soa(c, reg, params, b, win);
+        e = accumulate();
         if (e == GNM_OK) e = finalize(c, reg, r, 1);
     } catch (...) {
         e = GNM_ERR_CUDA;
@@ -1382,7 +1392,7 @@ int analyze_graphed(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params
         c->gexec = nullptr;
         c->graphs = false;
         c->kernel_launches = k0;
-        if (int e2 = accumulate_soa(c, reg, params, b, win)) return e2;
+        if (int e2 = accumulate()) return e2;
         return finalize(c, reg, r);
     }
     c->g_kernels = c->kernel_launches - k0;
@@ -1390,9 +1400,9 @@ int analyze_graphed(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params
     return finalize(c, reg, r, 2);
 }
 
-bool graph_eligible(const gnm_ctx* c, const gnm_batch_soa* b, const gnm_result* r) {
-    return c->graphs && !c->timing && !c->hosts && b && b->mem == GNM_MEM_DEVICE && b->n > 0 && r &&
-           !r->histograms && c->stream != nullptr;
+bool graph_eligible(const gnm_ctx* c, int mem, uint64_t n, const gnm_result* r) {
+    return c->graphs && !c->timing && !c->hosts && mem == GNM_MEM_DEVICE && n > 0 && r && !r->histograms &&
+           c->stream != nullptr;
 }
 } // namespace
 
@@ -1410,7 +1420,8 @@ int gnm_analyze_window(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_par
     if (c->accumulating) return fail(GNM_ERR_INVALID_ARGUMENT, "an accumulation is in progress");
     const Window w{result->window_start_ms, result->window_end_ms};
     return guarded([&] {
-        if (graph_eligible(c, batch, result)) return analyze_graphed(c, reg, params, batch, result, &w);
+        if (batch && graph_eligible(c, batch->mem, batch->n, result))
+            return analyze_graphed(c, reg, params, batch, nullptr, result, &w);
         if (int e = accumulate_soa(c, reg, params, batch, &w)) return e;
         return finalize(c, reg, result);
     });
@@ -1421,7 +1432,8 @@ int gnm_analyze(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* pa
     if (!c || !reg) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx/registry");
     if (c->accumulating) return fail(GNM_ERR_INVALID_ARGUMENT, "an accumulation is in progress");
     return guarded([&] {
-        if (graph_eligible(c, batch, result)) return analyze_graphed(c, reg, params, batch, result, nullptr);
+        if (batch && graph_eligible(c, batch->mem, batch->n, result))
+            return analyze_graphed(c, reg, params, batch, nullptr, result, nullptr);
         if (int e = accumulate_soa(c, reg, params, batch)) return e;
         return finalize(c, reg, result);
     });
@@ -1432,6 +1444,8 @@ int gnm_analyze_aos(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params
     if (!c || !reg) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx/registry");
     if (c->accumulating) return fail(GNM_ERR_INVALID_ARGUMENT, "an accumulation is in progress");
     return guarded([&] {
+        if (batch && batch->records && graph_eligible(c, batch->mem, batch->n, result))
+            return analyze_graphed(c, reg, params, nullptr, batch, result, nullptr);
         if (int e = accumulate_aos(c, reg, params, batch)) return e;
         return finalize(c, reg, result);
     });

@@ -3,10 +3,17 @@
 #include "registry.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cctype>
 #include <map>
 
 namespace gnm {
+
+uint64_t Registry::next_version() {
+    static std::atomic<uint64_t> counter{0};
+    return ++counter;
+}
+
 
 // parse_ipv4, site_catalog.cpp:10-40: exactly four dot-separated decimal
 // octets, each 1-3 digits and <= 255, nothing trailing.
@@ -114,7 +121,7 @@ int Registry::register_site(const std::string& name, const std::vector<Cidr>& ci
         entries_.emplace_back(p, id);
         index_.emplace(p >> 8, id);
     }
-    ++version_;
+    version_ = next_version();
     *out_id = id;
     return 0;
 }

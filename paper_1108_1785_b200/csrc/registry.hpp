@@ -101,6 +101,8 @@ public:
 
     const std::vector<Site>& sites() const { return sites_; }
     const std::vector<std::pair<uint32_t, uint32_t>>& entries() const { return entries_; }
+    // Unique across all registries of the process (a fresh registry at a
+    // recycled address never looks like one the device already holds).
     uint64_t version() const { return version_; }
 
     DeviceTable compile_device_table() const;
@@ -109,7 +111,8 @@ private:
     std::vector<Site> sites_;
     std::vector<std::pair<uint32_t, uint32_t>> entries_; // prefix24 -> site, insertion order
     std::unordered_map<uint32_t, uint32_t> index_;       // prefix24 >> 8 -> site
-    uint64_t version_ = 0;
+    uint64_t version_ = next_version();
+    static uint64_t next_version();
 };
 
 } // namespace gnm

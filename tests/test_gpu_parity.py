@@ -302,3 +302,36 @@ def test_graph_replay_matches_plain_calls(engine, orc):
     for _ in range(3):
         np.testing.assert_array_equal(engine.aggregate_window(batch, cat, lo, hi).table, wantw.table)
     plain.close()
+
+
+def test_graph_replay_aos(engine):
+    """Graph replay of repeated device AoS (64-byte FlowRecord) calls."""
+    import torch
+    from paper_1108_1785_b200 import Engine
+    w = synth.workload("D1")
+    cols = synth.generate(w, 200_000)
+    cat = layout_catalog(w.sites)
+    rows = torch.from_numpy(synth.to_aos(cols)).cuda()
+    plain = Engine(0)
+    plain.set_graphs(False)
+    want = plain.aggregate(FlowRecords(rows), cat)
+    for _ in range(4):
+        np.testing.assert_array_equal(engine.aggregate(FlowRecords(rows), cat).table, want.table)
+    plain.close()
+
+
+def test_fresh_registries_never_reuse_a_stale_device_table(engine):
+    """Registries created and dropped in a loop (their handles' addresses get
+    recycled): every call sees its own registry's table, because registry
+    versions are unique across the process."""
+    import gc
+    for i in range(24):
+        cat = SiteCatalog()
+        cat.register_site("only", [f"10.{i}.1.0/24"])
+        src = np.array([(10 << 24) | (i << 16) | (1 << 8) | 5, (10 << 24) | (((i + 1) % 24) << 16) | (1 << 8) | 5],
+                       np.uint32)
+        cols = parity.make_cols(src, np.full(2, 1, np.uint32), np.full(2, 50), np.full(2, 500_000), np.full(2, 1000))
+        got = engine.classify(FlowBatch(*cols), cat)
+        assert int(got[0]) == 0 and int(got[1]) >> 30 == 3, (i, got)
+        del cat
+        gc.collect()
