@@ -125,14 +125,20 @@ struct gnm_ctx {
         uint64_t alloc_gen;
         int aos;
         bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof o) == 0; }
-    } gkey{};
+    };
+    struct GraphEntry {
+        GraphKey key;
+        cudaGraphExec_t exec = nullptr;
+        uint64_t kernels = 0; // kernels per replay (launch accounting)
+        uint64_t last_use = 0;
+    };
+    std::vector<GraphEntry> graph_cache; // up to kGraphCache recent input sets
+    uint64_t graph_clock = 0;
     // Bumped whenever a buffer or baked-in size a captured graph refers to
     // changes (table upload, partials, log, output staging).
     uint64_t alloc_gen = 0;
     bool capturing = false; // inside analyze_graphed's stream capture: no (re)allocation allowed
-    bool gkey_valid = false;
-    cudaGraphExec_t gexec = nullptr;
-    uint64_t g_kernels = 0; // kernels per replay (launch accounting)
+
     bool prepared = false; // K3a + K2b ran (gnm_prepare_median) for this accumulation
     uint32_t* d_scratch = nullptr; // hot-site plan: counts, site->slot, slot->site, counter
     uint32_t partial_cap = 0;
@@ -891,7 +897,8 @@ void gnm_ctx_destroy(gnm_ctx* c) {
             cudaEventDestroy(p.a);
             cudaEventDestroy(p.b);
         }
-    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    for (auto& ge : c->graph_cache)
+        if (ge.exec) cudaGraphExecDestroy(ge.exec);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     delete c;
@@ -1309,18 +1316,22 @@ int gnm_accumulate_window_aos(gnm_ctx* c, const gnm_registry* reg, const gnm_fil
 }
 
 namespace {
-void drop_graph(gnm_ctx* c) {
-    if (c->gexec) cudaGraphExecDestroy(c->gexec);
-    c->gexec = nullptr;
+constexpr size_t kGraphCache = 32;
+
+void drop_graphs(gnm_ctx* c) {
+    for (auto& ge : c->graph_cache)
+        if (ge.exec) cudaGraphExecDestroy(ge.exec);
+    c->graph_cache.clear();
 }
 
 // A device-batch analysis repeated with the same inputs (column pointers,
-// sizes, registry version, parameters, window) replays one CUDA graph of
-// its whole device phase (K1, K2, K3a, K2b, K3b, the resets and the row
-// copy-out): the second identical call captures it, later ones launch it.
-// Only the host part (wait, rows out) runs per call. Not for host batches,
-// per-host mode, histogram export or timing (their host-side work differs
-// per call), nor on the legacy default stream.
+// sizes, registry version, parameters, window) replays a CUDA graph of its
+// whole device phase (K1, K2, K3a, K2b, K3b, the resets and the row
+// copy-out): the second call with a given input set captures it, later ones
+// launch it, for up to kGraphCache recent input sets (a ring of streaming
+// batches replays too). Only the host part (wait, rows out) runs per call.
+// Not for host batches, per-host mode, histogram export or timing (their
+// host-side work differs per call), nor on the legacy default stream.
 int analyze_graphed(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params* params,
                     const gnm_batch_soa* b, const gnm_batch_aos* ba, gnm_result* r, const Window* win) {
     gnm_ctx::GraphKey k;
@@ -1352,22 +1363,41 @@ int analyze_graphed(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params
     if (int e = begin_accumulate(c, reg)) return e;
     c->accumulating = false;
     k.alloc_gen = c->alloc_gen;
-    const bool same = c->gkey_valid && k == c->gkey;
-    if (same && c->gexec) {
-        ck(cudaGraphLaunch(c->gexec, c->stream), "cudaGraphLaunch");
-        c->kernel_launches += c->g_kernels;
+    // Entries of an older allocation generation can never match again.
+    for (size_t i = 0; i < c->graph_cache.size();) {
+        if (c->graph_cache[i].key.alloc_gen != k.alloc_gen) {
+            if (c->graph_cache[i].exec) cudaGraphExecDestroy(c->graph_cache[i].exec);
+            c->graph_cache.erase(c->graph_cache.begin() + static_cast<long>(i));
+        } else {
+            ++i;
+        }
+    }
+    gnm_ctx::GraphEntry* hit = nullptr;
+    for (auto& ge : c->graph_cache)
+        if (ge.key == k) hit = &ge;
+    if (hit && hit->exec) {
+        hit->last_use = ++c->graph_clock;
+        ck(cudaGraphLaunch(hit->exec, c->stream), "cudaGraphLaunch");
+        c->kernel_launches += hit->kernels;
         c->k2_launches += 1;
         c->records = k.n;
         return finalize(c, reg, r, 2);
     }
-    if (!same) {
-        drop_graph(c);
-        c->gkey = k;
-        c->gkey_valid = true;
+    if (!hit) { // first sighting: remember the input set, run the call plainly
+        if (c->graph_cache.size() >= kGraphCache) {
+            auto lru = std::min_element(c->graph_cache.begin(), c->graph_cache.end(),
+                                        [](const auto& x, const auto& y) { return x.last_use < y.last_use; });
+            if (lru->exec) cudaGraphExecDestroy(lru->exec);
+            c->graph_cache.erase(lru);
+        }
+        gnm_ctx::GraphEntry ge;
+        ge.key = k;
+        ge.last_use = ++c->graph_clock;
+        c->graph_cache.push_back(ge);
         if (int e = accumulate()) return e;
         return finalize(c, reg, r);
     }
-    // Second identical call: capture the device phase, then launch it.
+    // Second sighting: capture the device phase, then launch it.
     const uint64_t k0 = c->kernel_launches;
     ck(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
     int e = GNM_OK;
@@ -1381,22 +1411,25 @@ int analyze_graphed(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params
     c->capturing = false;
     cudaGraph_t g = nullptr;
     const cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+    cudaGraphExec_t exec = nullptr;
     cudaError_t ie = cudaErrorUnknown;
     if (e == GNM_OK && ce == cudaSuccess && g && c->alloc_gen == k.alloc_gen)
-        ie = cudaGraphInstantiate(&c->gexec, g, 0);
+        ie = cudaGraphInstantiate(&exec, g, 0);
     if (g) cudaGraphDestroy(g);
     clear_log(c); // the captured work has not run: start the accumulation over
     c->accumulating = false;
     if (ie != cudaSuccess) { // not capturable here: plain calls from now on
         cudaGetLastError();
-        c->gexec = nullptr;
         c->graphs = false;
+        drop_graphs(c);
         c->kernel_launches = k0;
         if (int e2 = accumulate()) return e2;
         return finalize(c, reg, r);
     }
-    c->g_kernels = c->kernel_launches - k0;
-    ck(cudaGraphLaunch(c->gexec, c->stream), "cudaGraphLaunch");
+    hit->exec = exec;
+    hit->kernels = c->kernel_launches - k0;
+    hit->last_use = ++c->graph_clock;
+    ck(cudaGraphLaunch(exec, c->stream), "cudaGraphLaunch");
     return finalize(c, reg, r, 2);
 }
 
@@ -1409,8 +1442,7 @@ bool graph_eligible(const gnm_ctx* c, int mem, uint64_t n, const gnm_result* r) 
 int gnm_ctx_set_graphs(gnm_ctx* c, int enable) {
     if (!c) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx");
     c->graphs = enable != 0;
-    c->gkey_valid = false;
-    drop_graph(c);
+    drop_graphs(c);
     return GNM_OK;
 }
 

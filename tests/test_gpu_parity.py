@@ -335,3 +335,25 @@ def test_fresh_registries_never_reuse_a_stale_device_table(engine):
         assert int(got[0]) == 0 and int(got[1]) >> 30 == 3, (i, got)
         del cat
         gc.collect()
+
+
+def test_graph_cache_ring_of_batches(engine):
+    """A ring of streaming batches (different buffers and windows, cycled)
+    replays one graph per input set: identical to plain calls."""
+    import torch
+    from paper_1108_1785_b200 import Engine
+    w = synth.workload("D5")
+    cat = layout_catalog(w.sites)
+    ring = []
+    for j in range(3):
+        cols = synth.generate(w, 150_000, index_offset=j * 150_000)
+        dev = [torch.from_numpy(c.view(np.int32 if c.dtype.itemsize == 4 else np.int64).copy()).cuda() for c in cols]
+        lo = int(np.percentile(cols[5], 5 + 10 * j))
+        ring.append((FlowBatch(*dev), lo, lo + 60_000_000))
+    plain = Engine(0)
+    plain.set_graphs(False)
+    want = [plain.aggregate_window(b, cat, lo, hi).table for b, lo, hi in ring]
+    for rep in range(4):
+        for (b, lo, hi), t in zip(ring, want):
+            np.testing.assert_array_equal(engine.aggregate_window(b, cat, lo, hi).table, t)
+    plain.close()
