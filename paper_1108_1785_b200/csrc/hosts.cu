@@ -150,6 +150,7 @@ __device__ __forceinline__ void fold(uint32_t slot, unsigned long long lo, uint3
 
 __global__ void __launch_bounds__(kInsBlock, 4) h_insert(DevLog L, const unsigned int* __restrict__ counts,
                                                          const uint32_t* __restrict__ off,
+                                                         const uint2* __restrict__ dir,
                                                          unsigned long long* keys, uint32_t mask, int shift,
                                                          unsigned long long* __restrict__ acc,
                                                          uint32_t* __restrict__ slot_of,
@@ -197,16 +198,33 @@ __global__ void __launch_bounds__(kInsBlock, 4) h_insert(DevLog L, const unsigne
             unsigned long long key[4], first[4];
             uint32_t h0[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) { // issue the four first probes
+            for (int q = 0; q < 4; ++q) { // dense ids, or issue the four first probes
                 const uint32_t site = L.buckets ? xs[q] : xs[q] >> kLogSiteShift;
                 key[q] = static_cast<unsigned long long>(site) << 32 | hs[q];
-                h0[q] = static_cast<uint32_t>((key[q] * 0x9E3779B97F4A7C15ull) >> shift) & mask;
+                if (dir) {
+                    // The host's /16 is in the registry directory (its /24 is
+                    // registered): id = rank of the /16 << 16 | its low 16
+                    // bits, bit-reversed so that the hosts of one /24 (one
+                    // site, often hot) land 256 entries apart instead of in
+                    // the same L2 sectors.
+                    const uint32_t d = hs[q] >> 16;
+                    const uint2 pr = __ldg(dir + (d >> 5));
+                    h0[q] = (pr.y + __popc(pr.x & ((1u << (d & 31u)) - 1u))) << 16 | __brev(hs[q] << 16);
+                } else {
+                    h0[q] = static_cast<uint32_t>((key[q] * 0x9E3779B97F4A7C15ull) >> shift) & mask;
+                }
                 first[q] = i + q < n ? keys[h0[q]] : 0ull;
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 if (i + q >= n) break;
-                const uint32_t slot = first[q] == key[q] ? h0[q] : insert_key(keys, mask, shift, key[q]);
+                uint32_t slot;
+                if (dir) { // mark the id used (every writer stores the same key)
+                    slot = h0[q];
+                    if (first[q] != key[q]) keys[slot] = key[q];
+                } else {
+                    slot = first[q] == key[q] ? h0[q] : insert_key(keys, mask, shift, key[q]);
+                }
                 slot_of[base + i + q] = slot;
                 bk[base + i + q] = L.buckets ? bs[q] : xs[q] & kBucketMask;
                 fold(slot, los[q], us[q], rts[q], t, acc);
@@ -532,7 +550,8 @@ cudaError_t finish_two_round(int device, HostRows& h, const unsigned long long* 
 } // namespace
 
 cudaError_t build_hosts_local(int device, const HostSlice* slices, int n_slices, const unsigned int* counts,
-                              size_t n_counts, uint64_t max_keys, HostRows& out, HostLocal& loc, cudaStream_t s) {
+                              size_t n_counts, uint64_t max_keys, const uint32_t* dir, uint32_t n16, HostRows& out,
+                              HostLocal& loc, cudaStream_t s) {
     free_hosts(out, s);
     free_local(loc, s);
     loc.ready = true;
@@ -558,9 +577,13 @@ cudaError_t build_hosts_local(int device, const HostSlice* slices, int n_slices,
     HCK(cudaFuncSetAttribute(h_insert, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kInsSmem)));
     int sms = 0;
     HCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    // H1: at least two slots per possible key.
+    // H1: dense ids when the registry's /16 blocks allow (every host lies in
+    // a registered /24, so rank-of-/16 << 16 | low 16 bits is unique and
+    // needs no probe), else an open-addressing table of at least two slots
+    // per possible key.
+    const bool dense = dir && n16 && (static_cast<uint64_t>(n16) << 16) <= (1ull << 24);
     const int tbits = std::max(10, bits_for(2 * std::max<uint64_t>(1, std::min(n, max_keys))));
-    const uint32_t cap = 1u << tbits;
+    const uint32_t cap = dense ? n16 << 16 : 1u << tbits;
     HCK(dalloc(&loc.table, cap, s)); // owned by `loc` (free_local)
     HCK(dalloc(&loc.acc, static_cast<size_t>(cap) * 5, s));
     loc.cap = cap;
@@ -574,7 +597,8 @@ cudaError_t build_hosts_local(int device, const HostSlice* slices, int n_slices,
         // Four CTAs per SM, fewer for small logs.
         const uint64_t items = static_cast<uint64_t>(sl.log.regions) * ((sl.log.warp_cap + kInsChunk - 1) / kInsChunk);
         const uint32_t g = std::min<uint32_t>(grid_for(device, items * 32, kInsBlock), 4 * sms);
-        h_insert<<<g, kInsBlock, kInsSmem, s>>>(sl.log, counts + sl.count_off, off + sl.count_off, loc.table,
+        h_insert<<<g, kInsBlock, kInsSmem, s>>>(sl.log, counts + sl.count_off, off + sl.count_off,
+                                                dense ? reinterpret_cast<const uint2*>(dir) : nullptr, loc.table,
                                                 cap - 1, 64 - tbits, loc.acc, out.row_of, out.bkt);
         HCK(cudaGetLastError());
     }
@@ -631,7 +655,8 @@ cudaError_t finish_hosts(int device, HostRows& out, HostLocal& loc, cudaStream_t
 cudaError_t build_hosts(int device, const HostSlice* slices, int n_slices, const unsigned int* counts,
                         size_t n_counts, uint64_t max_keys, HostRows& out, cudaStream_t s) {
     HostLocal loc;
-    const cudaError_t e = build_hosts_local(device, slices, n_slices, counts, n_counts, max_keys, out, loc, s);
+    const cudaError_t e =
+        build_hosts_local(device, slices, n_slices, counts, n_counts, max_keys, nullptr, 0, out, loc, s);
     if (e != cudaSuccess) {
         free_local(loc, s);
         return e;

@@ -66,8 +66,11 @@ struct HostGlobal {
 // Local phase (H0..H2): flat per-flow (slot, bucket), per-slot sums, the
 // sorted local keys; `out.n_rows` = local rows. Then either finish_hosts
 // (this context's rows) or the global combine below.
+// dir / n16: the device registry table's /16 directory and its non-empty
+// /16 count (dense host ids when n16 << 16 <= 2^24), or null / 0 (hashing).
 cudaError_t build_hosts_local(int device, const HostSlice* slices, int n_slices, const unsigned int* counts,
-                              size_t n_counts, uint64_t max_keys, HostRows& out, HostLocal& loc, cudaStream_t s);
+                              size_t n_counts, uint64_t max_keys, const uint32_t* dir, uint32_t n16, HostRows& out,
+                              HostLocal& loc, cudaStream_t s);
 cudaError_t finish_hosts(int device, HostRows& out, HostLocal& loc, cudaStream_t s);
 // Global combine: begin (map local rows into the union, fill sums/min/max
 // and coarse counts), [caller all-reduces], prepare (each row's median
