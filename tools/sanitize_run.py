@@ -45,6 +45,16 @@ with Engine(0) as eng:
     rb = eng.aggregate(FlowBatch(*bcols), big)
     assert len(rb.host_table) > 100_000, len(rb.host_table)
     eng.host_histogram_entries()
+    # > 256 non-empty /16 blocks: hashed host slots instead of dense ids
+    many = SiteCatalog()
+    for i in range(300):
+        many.register_site(f"m{i}", [f"{20 + i // 256}.{i % 256}.1.0/24"])
+    msrc = np.array([((20 + i // 256) << 24) | ((i % 256) << 16) | (1 << 8) | (j % 200)
+                     for i in range(300) for j in range(50)], np.uint32)
+    m = len(msrc)
+    mcols = (msrc, np.full(m, 1, np.uint32), np.full(m, 50, np.uint32), np.full(m, 500_000, np.uint32),
+             np.full(m, 1_000_000 - 2000, np.uint64), np.full(m, 1_000_000, np.uint64))
+    assert len(eng.aggregate(FlowBatch(*mcols), many).host_table) > 0
     # the cross-context union path with one context
     eng.accumulate(FlowBatch(*bcols), big)
     import torch
