@@ -647,12 +647,17 @@ __device__ __forceinline__ void run_scalar(const DevBatch& b, uint64_t first, ui
                                            const DevPartials& P, const HotSmem& h, Ctr& t,
                                            WarpQueue& wq, const DevLog& L) {
     constexpr bool kWin = kMode & kModeWindow, kHosts = kMode & kModeHosts;
+    // One round ahead: the next record's loads are in flight while this one
+    // is classified.
+    uint32_t nsrc = 0, ndst = 0, npkts = 0, noct = 0;
+    uint64_t ndur = 0, nend = 0;
+    if (first + lane < last) load_record<kLayout>(b, first + lane, nsrc, ndst, npkts, noct, ndur, nend);
     for (uint64_t base = first; base < last; base += stride) {
         const uint64_t i = base + lane;
-        uint32_t src = 0, dst = 0, pkts = 0, oct = 0;
-        uint64_t dur = 0, end = 0;
+        const uint32_t src = nsrc, dst = ndst, pkts = npkts, oct = noct;
+        const uint64_t dur = ndur, end = nend;
         const bool ok = i < last;
-        if (ok) load_record<kLayout>(b, i, src, dst, pkts, oct, dur, end);
+        if (i + stride < last) load_record<kLayout>(b, i + stride, nsrc, ndst, npkts, noct, ndur, nend);
         Ctr one;
         uint32_t host;
         const uint32_t code = stage_a<kSmem>(src, dst, pkts, oct, dur, p, gt, one, host, window_in<kWin>(end, p));
