@@ -10,10 +10,11 @@
 // bits and exact micro-bps; at finalize this post-pass turns the log into the
 // reference's rows without any per-host histogram storage:
 //   H0  flat offsets: exclusive scan of the per-warp log counts;
-//   H1  insert every (site, host) key into an open-addressing table (at most
-//       256 keys per registry /24 entry, so the table is sized by
-//       min(flows, 256 * entries)); accumulate the u128 micro-bps sum, min and
-//       max per slot (through a per-CTA shared table for the hot slots);
+//   H1  give every (site, host) key a slot: a dense id from the registry's
+//       /16 directory when its non-empty /16 blocks allow (a host lies in a
+//       registered /24), else an open-addressing table sized by
+//       min(flows, 256 * /24 entries); accumulate the u128 micro-bps sum, min
+//       and max per slot (through a per-CTA shared table for the hot slots);
 //       flatten (slot, bucket) per flow;
 //   H2  collect the distinct keys, radix-sort them: row = rank in (site,
 //       host) order, i.e. the std::map's iteration order; every flow's slot
@@ -28,7 +29,9 @@
 //   H5  per row: count, clamp into [min, max], avg as the host rounds it
 //       (stats_from, :242-253).
 // Histograms (dense or sparse) are built from the per-flow (row, bucket)
-// arrays only when asked for.
+// arrays only when asked for. Across contexts (gnm_hosts_*), H0..H2 run per
+// context, the rows become the union of every context's keys, and H3/H5 run
+// on partials the caller all-reduces (hosts_global_*).
 #include <cuda_runtime.h>
 
 #include <cub/device/device_radix_sort.cuh>
