@@ -1008,55 +1008,62 @@ __global__ void __launch_bounds__(kK2Block) k_classify(DevSoA b, const uint32_t*
 // inside it. The 157 counts are loaded in unrolled batches (independent
 // loads in flight) and kept in registers between the two passes.
 __global__ void __launch_bounds__(128) k3a_median_sb(DevPartials P) {
+    // Four lanes per site, each over ~40 of the 157 super-buckets (a site's
+    // counts are n_sites apart; neighbouring sites' are adjacent, so each
+    // load instruction stays coalesced across quads).
+    constexpr uint32_t kPart = (kCoarse + 3) / 4; // 40
     const uint32_t n = P.n_sites;
-    for (uint32_t site = blockIdx.x * blockDim.x + threadIdx.x; site < n; site += gridDim.x * blockDim.x) {
+    const uint32_t lane = threadIdx.x & 31u, part = lane & 3u;
+    const uint32_t stride = (gridDim.x * blockDim.x) >> 2;
+    for (uint32_t site0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 2;; site0 += stride) {
+        const bool in = site0 < n;
+        if (!__any_sync(0xFFFFFFFFu, in)) break; // warp-uniform: the quads shuffle below
+        const uint32_t site = in ? site0 : 0u;
+        const uint32_t sb0 = part * kPart;
         const unsigned int* col = P.coarse + site;
-        uint64_t cnt = 0;
-#pragma unroll 16
-        for (uint32_t sb = 0; sb < kCoarse; ++sb) cnt += __ldcg(col + static_cast<size_t>(sb) * n);
-        uint32_t msb = kLogSkip, rank = 0;
-        if (cnt) {
-            const uint64_t target = (cnt + 1) / 2;
-            uint64_t cum = 0;
-            for (uint32_t sb0 = 0; sb0 < kCoarse; sb0 += 8) {
-                uint32_t c[8];
+        uint32_t v[kPart];
+        uint64_t c = 0;
 #pragma unroll
-                for (uint32_t u = 0; u < 8; ++u)
-                    c[u] = sb0 + u < kCoarse ? __ldcg(col + static_cast<size_t>(sb0 + u) * n) : 0u;
-                uint64_t part = 0;
+        for (uint32_t i = 0; i < kPart; ++i) {
+            v[i] = (in && sb0 + i < kCoarse) ? __ldcg(col + static_cast<size_t>(sb0 + i) * n) : 0u;
+            c += v[i];
+        }
+        uint64_t pre = __shfl_up_sync(0xFFFFFFFFu, c, 1); // exclusive prefix within the quad
+        pre = part >= 1 ? pre : 0;
+        uint64_t p2 = __shfl_up_sync(0xFFFFFFFFu, pre + c, 2);
+        pre += part >= 2 ? p2 : 0;
+        const uint64_t tot = __shfl_sync(0xFFFFFFFFu, pre + c, (lane & ~3u) + 3u);
+        const uint64_t target = (tot + 1) / 2;
+        unsigned long long found = 0; // (msb + 1) << 32 | rank, from the part that holds the median
+        if (tot && pre < target && pre + c >= target) {
+            uint64_t cum = pre;
 #pragma unroll
-                for (uint32_t u = 0; u < 8; ++u) part += c[u];
-                if (cum + part < target) {
-                    cum += part;
-                    continue;
-                }
-#pragma unroll
-                for (uint32_t u = 0; u < 8; ++u) {
-                    if (cum + c[u] >= target) {
-                        msb = sb0 + u;
-                        rank = static_cast<uint32_t>(target - cum);
-                        break;
-                    }
-                    cum += c[u];
-                }
-                break;
+            for (uint32_t i = 0; i < kPart; ++i) {
+                if (!found && cum + v[i] >= target) found = static_cast<unsigned long long>(sb0 + i + 1) << 32 | (target - cum);
+                cum += v[i];
             }
         }
-        // Heavy sites (>= kHeavyMin flows) get one of kHeavy shared-memory
-        // fine rows in K2b: their median super-bucket draws thousands of
-        // same-address reductions otherwise.
-        uint32_t hidx = kHeavyNone;
-        if (cnt >= kHeavyMin) {
-            const uint32_t k = atomicAdd(P.heavy_next, 1u);
-            if (k < kHeavy) {
-                hidx = k;
-                P.heavy_next[1 + k] = site; // heavy row -> site, for K2b's flush
+        found = max(found, __shfl_xor_sync(0xFFFFFFFFu, found, 1));
+        found = max(found, __shfl_xor_sync(0xFFFFFFFFu, found, 2));
+        if (in && part == 0) {
+            const uint32_t msb = found ? static_cast<uint32_t>(found >> 32) - 1u : kLogSkip;
+            const uint32_t rank = static_cast<uint32_t>(found);
+            // Heavy sites (>= kHeavyMin flows) get one of kHeavy shared-memory
+            // fine rows in K2b: their median super-bucket draws thousands of
+            // same-address reductions otherwise.
+            uint32_t hidx = kHeavyNone;
+            if (tot >= kHeavyMin) {
+                const uint32_t k = atomicAdd(P.heavy_next, 1u);
+                if (k < kHeavy) {
+                    hidx = k;
+                    P.heavy_next[1 + k] = site; // heavy row -> site, for K2b's flush
+                }
             }
+            P.msb[site] = msb | hidx << 8;
+            P.map16[site] = static_cast<unsigned short>((msb & 0xFFu) | (hidx == kHeavyNone ? 0xFF00u : hidx << 8));
+            P.mrank[site] = rank;
+            P.cnt[site] = tot;
         }
-        P.msb[site] = msb | hidx << 8;
-        P.map16[site] = static_cast<unsigned short>((msb & 0xFFu) | (hidx == kHeavyNone ? 0xFF00u : hidx << 8));
-        P.mrank[site] = rank;
-        P.cnt[site] = cnt;
     }
 }
 
@@ -1448,7 +1455,7 @@ uint32_t small_grid(int device, uint64_t items, uint32_t block) {
 cudaError_t launch_k3a(int device, const DevPartials& P, cudaStream_t s) {
     if (P.n_sites == 0) return cudaSuccess;
     if (cudaError_t e = cudaMemsetAsync(P.heavy_next, 0, 4, s)) return e;
-    k3a_median_sb<<<small_grid(device, P.n_sites, 128), 128, 0, s>>>(P);
+    k3a_median_sb<<<small_grid(device, static_cast<uint64_t>(P.n_sites) * 4, 128), 128, 0, s>>>(P);
     return cudaGetLastError();
 }
 
