@@ -357,3 +357,18 @@ def test_graph_cache_ring_of_batches(engine):
         for (b, lo, hi), t in zip(ring, want):
             np.testing.assert_array_equal(engine.aggregate_window(b, cat, lo, hi).table, t)
     plain.close()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["D1", "D2", "D3"])
+def test_full_size_configs_bit_exact(engine, orc, name):
+    """BASELINE.json configs[0..2] at their full sizes (D1 100k records / 256
+    sites, D2 1M / 1k mixed prefixes, D3 100M / 10k Zipf sites): the whole
+    site table (counts, byte and u128 micro-bps sums, min / max / avg /
+    median) and the tallies equal the C oracle's bit for bit."""
+    w = synth.workload(name)
+    cols = synth.generate(w, w.n)
+    cat = layout_catalog(w.sites)
+    res = engine.aggregate(FlowBatch(*cols).to_device(), cat)
+    assert res.tallies.total() == w.n
+    parity.assert_matches_oracle(res, parity.oracle_reference(orc, cat, cols), check_hist=False)
