@@ -372,3 +372,25 @@ def test_full_size_configs_bit_exact(engine, orc, name):
     res = engine.aggregate(FlowBatch(*cols).to_device(), cat)
     assert res.tallies.total() == w.n
     parity.assert_matches_oracle(res, parity.oracle_reference(orc, cat, cols), check_hist=False)
+
+
+@pytest.mark.slow
+def test_d4_one_billion_records_chunked(engine, orc):
+    """BASELINE.json configs[3] (D4: 1B records with D3's distribution) on one
+    GPU through the split API: ten 100M-record index shards accumulated into
+    one context (ten K2 launches, one 1B-entry log), finalized once, equal
+    the C oracle run over the same shards bit for bit."""
+    w = synth.workload("D4")
+    cat = layout_catalog(w.sites)
+    p, s = cat.entries_arrays()
+    oc = orc.catalog(p, s)
+    acc = None
+    shard = w.n // 10
+    for k in range(10):
+        cols = synth.generate(w, shard, index_offset=k * shard)
+        engine.accumulate(FlowBatch(*cols).to_device(), cat)
+        acc = orc.aggregate(cols, oc, cat.site_count(), acc=acc)
+        del cols
+    res = engine.finalize(cat)
+    assert res.tallies.total() == w.n
+    parity.assert_matches_oracle(res, orc.finalize(acc), check_hist=False)
