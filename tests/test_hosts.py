@@ -300,3 +300,16 @@ def test_gpu_hosts_union_path_single_context(hosts_engine):
     np.testing.assert_array_equal(res.host_table, want)
     with pytest.raises(Exception):
         hosts_engine.host_histogram_entries()
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_gpu_hosts_full_size_d3(hosts_engine, orc):
+    """Per-host rows at D3's full size (100M records, 80k (site, host) rows)
+    equal the oracle's restatement bit for bit."""
+    w = synth.workload("D3")
+    cols = synth.generate(w, w.n)
+    cat = SiteCatalog()
+    w.sites.register(cat)
+    res = hosts_engine.aggregate(FlowBatch(*cols).to_device(), cat)
+    assert_hosts_match_oracle(res, oracle_hosts(orc, cat, cols))
