@@ -354,7 +354,11 @@ def main():
     from paper_1108_1785_b200 import distributed as D
 
     world, rank, local = dist_env()
-    if world > 1:
+    # GNM_BENCH_FORCE_DIST: test hook, the N>1 code path (process group, the
+    # combine every step, max over ranks) at world size 1 -- NCCL on the one
+    # GPU a test box has.
+    distributed = world > 1 or bool(os.environ.get("GNM_BENCH_FORCE_DIST"))
+    if distributed:
         # NCCL over NVLink; GNM_BENCH_BACKEND=gloo is a test hook for several
         # ranks on the one GPU a test box has (NCCL refuses shared devices).
         backend = os.environ.get("GNM_BENCH_BACKEND", "nccl")
@@ -396,7 +400,7 @@ def main():
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=f"cuda:{local}")
 
     def step(batch):
-        if world == 1:
+        if not distributed:
             return eng.aggregate(batch, cat)
         # K2 on this rank's shard, then the two-round exact-median combine
         # over NCCL (paper_1108_1785_b200.distributed): all-reduce of sums /
@@ -407,7 +411,7 @@ def main():
         return eng.finalize(cat)
 
     def barrier():
-        if world > 1:
+        if distributed:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -431,7 +435,7 @@ def main():
         barrier()
         launches = eng.timing()["kernel_launches"] - launches0
         ms = ev0.elapsed_time(ev1)
-        if world > 1:
+        if distributed:
             tt = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ms = float(tt.item())
@@ -539,7 +543,7 @@ def main():
     if rank == 0:
         print(json.dumps(line), flush=True)
     eng.close()
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
     return 0
 

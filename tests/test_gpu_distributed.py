@@ -23,7 +23,7 @@ def _free_port():
     return port
 
 
-def _rank(rank, world, port, outdir, n, workload):
+def _rank(rank, world, port, outdir, n, workload, backend="gloo"):
     import torch
     import torch.distributed as dist
     from paper_1108_1785_b200 import Engine, FlowBatch, SiteCatalog, synth
@@ -31,8 +31,11 @@ def _rank(rank, world, port, outdir, n, workload):
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    else:
+        dist.init_process_group(backend, rank=rank, world_size=world)
     w = synth.workload(workload)
     cols = synth.generate(w, n)
     cat = SiteCatalog()
@@ -98,6 +101,27 @@ def test_bench_multi_rank_line(extra):
     assert d["config"]["parallelism"] == "index shards x2"
 
 
+@pytest.mark.parametrize("extra", [[], ["--hosts"]])
+def test_bench_nccl_path_single_rank(extra):
+    """bench.py's N>1 code path over NCCL (the backend the 8-GPU run uses),
+    forced at world size 1 by the GNM_BENCH_FORCE_DIST test hook."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GNM_BENCH_FORCE_DIST="1")
+    env.pop("GNM_BENCH_BACKEND", None)
+    out = subprocess.run(
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+         "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "1",
+         "--records", "3000000", "--steps", "3", "--warmup", "3", "--e2e-steps", "1", "--no-cpu-baseline"] + extra,
+        cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    assert lines[0]["value"] > 0 and lines[0]["e2e"]["value"] > 0
+
+
 def _rank_hosts(rank, world, port, outdir, n, workload):
     import torch
     import torch.distributed as dist
@@ -126,6 +150,25 @@ def _rank_hosts(rank, world, port, outdir, n, workload):
     eng.close()
     dist.barrier()
     dist.destroy_process_group()
+
+
+def test_nccl_combine_single_rank(engine):
+    """The combine over NCCL itself (the backend bench.py uses at N>1): one
+    rank, so the all-reduces are identities, but every collective runs on
+    the engine's stream with the partials' real dtypes (int64 SUM, f64
+    MIN/MAX, int32 SUM) and the table must equal the plain call's."""
+    import torch.multiprocessing as mp
+    from paper_1108_1785_b200 import FlowBatch, SiteCatalog, synth
+
+    n, workload = 1_000_003, "D3"
+    w = synth.workload(workload)
+    cols = synth.generate(w, n)
+    cat = SiteCatalog()
+    w.sites.register(cat)
+    want = engine.aggregate(FlowBatch(*cols).to_device(), cat)
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_rank, args=(1, _free_port(), d, n, workload, "nccl"), nprocs=1, join=True)
+        np.testing.assert_array_equal(np.load(os.path.join(d, "table0.npy")), want.table)
 
 
 @pytest.mark.parametrize("workload,n", [("D1", 300_001), ("D3", 1_500_007)])
