@@ -447,7 +447,7 @@ void launch_k2_timed(gnm_ctx* c, const gnm::DevBatch& b, const gnm::DevParams& p
     bool hot = false;
     if (c->hot_mode != GNM_HOT_OFF) {
         cudaError_t e;
-        hot = gnm::plan_hot(c->device, b, c->table, p, c->P.n_sites, c->d_scratch, cold.grid,
+        hot = gnm::plan_hot(c->device, b, c->table, p, c->P.n_sites, c->d_scratch, c->P.mn, c->P.mx, cold.grid,
                             c->hot_mode == GNM_HOT_FORCE, c->stream, &c->kernel_launches, &e);
         ck(e, "hot-site plan");
     }

@@ -189,12 +189,24 @@ __device__ __forceinline__ HotSmem hot_smem(uint32_t table_words_in_smem) {
     return h;
 }
 
-__device__ __forceinline__ void hot_init(const HotSmem& h) {
+// The min/max caches start from the hot sites' global bounds, which K1
+// already pulled in from the sample's flows (k_sample): every value there is
+// a rate whose reduction was issued, so the cache invariant below holds, and
+// the CTA's first flows of a hot site no longer all win against +inf / 0.
+__device__ __forceinline__ void hot_init(const HotSmem& h, const DevHot& hot, const DevPartials& P) {
     for (uint32_t i = threadIdx.x; i < kHotStride; i += blockDim.x) {
 #pragma unroll
         for (int k = 0; k < 5; ++k) h.limb[k * kHotStride + i] = 0;
-        h.mn[i] = kMinInitBits;
-        h.mx[i] = kMaxInitBits;
+        unsigned long long mn = kMinInitBits, mx = kMaxInitBits;
+        if (i >= 1 && i <= hot.n_slots) {
+            const uint32_t site = __ldg(hot.hot_site + i); // unassigned slots: stale, unused
+            if (site < P.n_sites) {
+                mn = __ldcg(P.mn + site);
+                mx = __ldcg(P.mx + site);
+            }
+        }
+        h.mn[i] = mn;
+        h.mx[i] = mx;
     }
     for (uint32_t i = threadIdx.x; i < kCoarseSlots * kCoarse; i += blockDim.x) h.coarse[i] = 0;
 }
@@ -676,12 +688,13 @@ __device__ __forceinline__ void run_scalar(const DevBatch& b, uint64_t first, ui
 // warp's queue after them, the warp's log region.
 template <bool kSmem, bool kHot, bool kHosts>
 __device__ __forceinline__ void k2_prologue(const uint32_t* __restrict__ gt, uint32_t table_words,
-                                            const DevLog& L, HotSmem& h, WarpQueue& wq) {
+                                            const DevLog& L, const DevHot& hot, const DevPartials& P,
+                                            HotSmem& h, WarpQueue& wq) {
     load_table<kSmem>(gt, table_words);
     const uint32_t smem_words = kSmem ? table_words : 0u;
     if constexpr (kHot) {
         h = hot_smem(smem_words);
-        hot_init(h);
+        hot_init(h, hot, P);
     }
     const uint32_t warp = threadIdx.x >> 5;
     uint4* queues = reinterpret_cast<uint4*>(g_smem + smem_words + (kHot ? kHotBytes / 4 : 0u));
@@ -741,7 +754,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_soa(DevBatch b, const uint32_t
     constexpr bool kWin = kMode & kModeWindow, kHosts = kMode & kModeHosts;
     HotSmem h{};
     WarpQueue wq;
-    k2_prologue<kSmem, kHot, kHosts>(gt, table_words, L, h, wq);
+    k2_prologue<kSmem, kHot, kHosts>(gt, table_words, L, hot, P, h, wq);
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warp = threadIdx.x >> 5;
     const DevSoA& c = b.soa;
@@ -816,7 +829,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_gen(DevBatch b, const uint32_t
     constexpr bool kHosts = kMode & kModeHosts;
     HotSmem h{};
     WarpQueue wq;
-    k2_prologue<kSmem, kHot, kHosts>(gt, table_words, L, h, wq);
+    k2_prologue<kSmem, kHot, kHosts>(gt, table_words, L, hot, P, h, wq);
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t r0 = b.n * blockIdx.x / gridDim.x, r1 = b.n * (blockIdx.x + 1) / gridDim.x;
     Ctr t;
@@ -832,7 +845,9 @@ template <bool kSmem>
 __global__ void __launch_bounds__(kK2Block) k_sample(DevBatch b, const uint32_t* __restrict__ gt,
                                                       uint32_t table_words, DevParams p,
                                                       uint64_t chunk_stride, uint32_t chunk_len,
-                                                      uint32_t* __restrict__ cnt) {
+                                                      uint32_t* __restrict__ cnt,
+                                                      unsigned long long* __restrict__ mn,
+                                                      unsigned long long* __restrict__ mx) {
     load_table<kSmem>(gt, table_words);
     if constexpr (kSmem) __syncthreads();
     // blockIdx.y picks the chunk; blockIdx.x * blockDim.x the first record
@@ -850,7 +865,17 @@ __global__ void __launch_bounds__(kK2Block) k_sample(DevBatch b, const uint32_t*
             dur < static_cast<uint64_t>(p.min_duration1) || (p.windowed && !(end >= p.win_lo && end < p.win_hi)))
             continue;
         const uint32_t v = site_of_full<kSmem>(gt, src, dst);
-        if (v != kNone) atomicAdd(cnt + (v & p.site_mask), 1u);
+        if (v == kNone) continue;
+        const uint32_t site = v & p.site_mask;
+        atomicAdd(cnt + site, 1u);
+        // The sampled Forward flow's rate (flow_rate, rate_engine.cpp:88-94)
+        // into its site's min/max now; K2 reduces the same flow again, which
+        // min/max absorb. A read filters the reductions (a stale read only
+        // costs an extra one).
+        const unsigned long long rb = static_cast<unsigned long long>(
+            __double_as_longlong(__ddiv_rn(8000.0 * static_cast<double>(oct), __ull2double_rn(dur))));
+        if (rb < __ldcg(mn + site)) red_min(mn + site, rb);
+        if (rb > __ldcg(mx + site)) red_max(mx + site, rb);
     }
 }
 
@@ -1378,8 +1403,8 @@ LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool ho
 }
 
 bool plan_hot(int device, const DevBatch& b, const DevTable& t, const DevParams& p,
-              uint32_t n_sites, uint32_t* scratch, int k2_grid, bool force, cudaStream_t s,
-              uint64_t* launches, cudaError_t* err) {
+              uint32_t n_sites, uint32_t* scratch, unsigned long long* mn, unsigned long long* mx,
+              int k2_grid, bool force, cudaStream_t s, uint64_t* launches, cudaError_t* err) {
     (void)device;
     *err = cudaSuccess;
     if (!t.packed || n_sites == 0 || b.n == 0) return false;
@@ -1409,7 +1434,7 @@ bool plan_hot(int device, const DevBatch& b, const DevTable& t, const DevParams&
     // The sample is small: probe the table through L1 rather than copying
     // it into every CTA's shared memory.
     const dim3 sg((chunk_len + 255) / 256, nchunks);
-    k_sample<false><<<sg, 256, 0, s>>>(b, t.words, t.n_words, p, stride, chunk_len, cnt);
+    k_sample<false><<<sg, 256, 0, s>>>(b, t.words, t.n_words, p, stride, chunk_len, cnt, mn, mx);
     k_hot_select<<<1, kSelectBlock, 0, s>>>(cnt, n_sites, thr, site_slot, hot_site);
     const uint32_t span = t.n_words - t.node_begin;
     const uint32_t rg = std::max<uint32_t>(1, std::min<uint32_t>((span + 255) / 256, 1024));

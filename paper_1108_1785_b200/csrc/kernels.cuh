@@ -160,13 +160,15 @@ LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool ho
                     bool hosts = false);
 
 // K1 (optional, skewed batches): sample the batch, pick the hot sites and
-// write their slots into the table words. Returns false when the batch is
+// write their slots into the table words; the sampled Forward flows' rates
+// also go into the partials' min/max (`mn`, `mx`), which seed K2's hot-slot
+// caches. Returns false when the batch is
 // too small for block-private accumulation to pay; `scratch` holds
 // n_sites u32 counts (zero at rest), n_sites u32 site->slot and kHotStride
 // u32 slot->site.
 bool plan_hot(int device, const DevBatch& b, const DevTable& t, const DevParams& p,
-              uint32_t n_sites, uint32_t* scratch, int k2_grid, bool force, cudaStream_t s,
-              uint64_t* launches, cudaError_t* err);
+              uint32_t n_sites, uint32_t* scratch, unsigned long long* mn, unsigned long long* mx,
+              int k2_grid, bool force, cudaStream_t s, uint64_t* launches, cudaError_t* err);
 
 // Entries one warp region must hold for a launch of `cfg` over b (>= the
 // warp's records, rounded up to the 32-entry drain granularity).
