@@ -840,7 +840,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_gen(DevBatch b, const uint32_t
 
 // ---- K1: hot-site plan ------------------------------------------------------
 // Each block classifies one contiguous chunk of the batch and counts Forward
-// flows per site.
+// flows per site; their rates also seed the sites' min/max (see hot_init).
 template <bool kSmem>
 __global__ void __launch_bounds__(kK2Block) k_sample(DevBatch b, const uint32_t* __restrict__ gt,
                                                       uint32_t table_words, DevParams p,
