@@ -251,6 +251,42 @@ def test_window_fused_snapshot_bit_exact(engine, orc, on_device):
     parity.assert_matches_oracle(got, parity.oracle_reference(orc, cat, tuple(np.ascontiguousarray(c[m]) for c in cols)))
 
 
+@pytest.mark.parametrize("mode", ["force", "auto"])
+def test_sampled_min_max_respects_window(engine, orc, mode):
+    """K1 reduces its sampled flows' rates into the sites' min/max (they
+    seed K2's hot-slot caches): records the window drops carry the most
+    extreme rates of the batch here, so a sample that ignored the window
+    (or the class filter) would show up in min_bps / max_bps."""
+    w = synth.workload("D3")
+    cols = [c.copy() for c in synth.generate(w, 600_000)]
+    cat = layout_catalog(w.sites)
+    end = cols[5]
+    lo, hi = int(np.percentile(end, 20)), int(np.percentile(end, 80))
+    out = ~_window_mask(cols, lo, hi)
+    idx = np.flatnonzero(out)
+    # Outside the window: half very fast (4e9 octets in 1 s), half very slow
+    # (2048 octets over ~11 days), all Forward-shaped for the hot sites.
+    fast, slow = idx[0::2], idx[1::2]
+    cols[3][fast] = np.uint32(4_000_000_000)
+    cols[2][fast] = np.uint32(25)
+    cols[4][fast] = cols[5][fast] - np.uint64(1000)
+    cols[3][slow] = np.uint32(2048)
+    cols[2][slow] = np.uint32(20)
+    cols[4][slow] = cols[5][slow] - np.uint64(1_000_000_000)
+    batch = FlowBatch(*cols).to_device()
+    engine.set_hot_mode(mode)
+    try:
+        got = engine.aggregate_window(batch, cat, lo, hi)
+        full = engine.aggregate(batch, cat)
+    finally:
+        engine.set_hot_mode("auto")
+    m = ~out
+    parity.assert_matches_oracle(got, parity.oracle_reference(
+        orc, cat, tuple(np.ascontiguousarray(c[m]) for c in cols)))
+    # and the unwindowed call does see the extremes
+    parity.assert_matches_oracle(full, parity.oracle_reference(orc, cat, tuple(cols)))
+
+
 def test_window_fused_aos(engine, orc):
     sites, cols = parity.engine_stress_set(50_000, seed=31)
     cat = catalog_of(sites)
