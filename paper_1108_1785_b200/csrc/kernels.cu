@@ -371,6 +371,10 @@ __device__ __forceinline__ uint32_t accumulate(uint32_t code, uint32_t oct, uint
                                                FlowOut& fo) {
     uint32_t& bucket = fo.bucket;
     bucket = 0;
+    // flow_rate (rate_engine.cpp:88-94): exact product, one IEEE division.
+    // Issued before the lookup: it needs only the record, so its dependent
+    // DFMA chain overlaps the table loads (an Unmatched item wastes it).
+    const double rate = __ddiv_rn(8000.0 * static_cast<double>(oct), __ull2double_rn(dur));
     const uint32_t v = resolve<kSmem>(gt, code);
     if (v == kNone) {
         ++c.unm;
@@ -390,8 +394,6 @@ __device__ __forceinline__ uint32_t accumulate(uint32_t code, uint32_t oct, uint
         cmn = h.mn[slot];
         cmx = h.mx[slot];
     }
-    // flow_rate (rate_engine.cpp:88-94): exact product, one IEEE division.
-    const double rate = __ddiv_rn(8000.0 * static_cast<double>(oct), __ull2double_rn(dur));
     uint64_t lo, hi;
     ubps_of(oct, dur, rate, lo, hi);
     const unsigned long long rb = static_cast<unsigned long long>(__double_as_longlong(rate));
