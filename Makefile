@@ -3,7 +3,7 @@
 # /root/reference, i.e. only in the build container).
 #
 #   paper_1108_1785_b200/lib/libgnetmon.so   product: sm_100a kernels + C-ABI
-#   paper_1108_1785_b200/lib/libgnm_synth.so synthetic flow generator (bench/tests)
+#   workloads/lib/libgnm_synth.so            synthetic flow generator (bench/tests)
 #   oracle/lib/liborc.so                     C restatement (test infrastructure)
 #   oracle/_ref/libflowmon_ref.so            unmodified reference (test infrastructure)
 
@@ -16,14 +16,14 @@ SRCS := $(PKG)/csrc/capi.cu $(PKG)/csrc/kernels.cu $(PKG)/csrc/netflow.cu $(PKG)
 HDRS := include/gnetmon.h $(PKG)/csrc/kernels.cuh $(PKG)/csrc/netflow.cuh $(PKG)/csrc/hosts.cuh $(PKG)/csrc/registry.hpp
 
 .PHONY: all ref clean oracle ablation
-all: $(PKG)/lib/libgnetmon.so $(PKG)/lib/libgnm_synth.so oracle
+all: $(PKG)/lib/libgnetmon.so workloads/lib/libgnm_synth.so oracle
 
 $(PKG)/lib/libgnetmon.so: $(SRCS) $(HDRS)
 	@mkdir -p $(PKG)/lib
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) 2> $(PKG)/lib/ptxas.log || (cat $(PKG)/lib/ptxas.log; false)
 
-$(PKG)/lib/libgnm_synth.so: $(PKG)/csrc/synth.c
-	@mkdir -p $(PKG)/lib
+workloads/lib/libgnm_synth.so: workloads/synth.c
+	@mkdir -p workloads/lib
 	gcc -std=c11 -O2 -fPIC -shared -fopenmp -Wall -Wextra -o $@ $< -lm
 
 # Measurement build with the K2 ablation switches (tools/ablation.sh); never
@@ -40,5 +40,5 @@ ref:
 	$(MAKE) -C oracle ref
 
 clean:
-	rm -rf $(PKG)/lib
+	rm -rf $(PKG)/lib workloads/lib
 	$(MAKE) -C oracle clean

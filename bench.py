@@ -174,10 +174,11 @@ def pinned_columns(n: int):
 
 
 def reference_sample(w, n_sample: int):
-    from paper_1108_1785_b200 import synth
+    # `workloads` and `oracle` only: the reference arm never maps libgnetmon.so
+    import workloads
     from oracle import Reference
     R = Reference()
-    cols = synth.generate(w, n_sample)
+    cols = workloads.generate(w, n_sample)
     cat = R.catalog([[c] for c in w.sites.cidrs])
     rec = R.records(cols)
     return R, cat, rec
@@ -212,46 +213,91 @@ def time_reference(w, n_sample: int, reps: int):
     return res
 
 
+def workload_config(w, n: int, n_sites: int, world: int, args) -> dict:
+    """The `config` object both arms print (the GPU arm's workload; the
+    reference arm times bounded samples of it, stated in cpu_baseline)."""
+    return {"workload": f"{w.name}: {n} records/GPU, {n_sites} /24 sites, Zipf s={w.zipf_s}, "
+                        f"8 hosts/site, 40% forward",
+            "records_per_gpu": n, "sites": n_sites, "input": args.input,
+            "hosts": ("per-host rows built every step" if args.hosts
+                      else "site level only (gnm_ctx_set_hosts off)"),
+            "parallelism": f"index shards x{world}",
+            "l2": "inputs 3.2 GB/GPU > 126 MB L2; no flush needed" if n >= 10_000_000
+                  else "inputs may fit L2"}
+
+
+def self_launch(args) -> int:
+    """`bench.py --gpus N` (N > 1) outside torchrun: relaunch this script as N
+    ranks on this node (one per GPU, rendezvous on 127.0.0.1), exactly as the
+    driver's torchrun form does; rank 0 prints the line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 # ---- the reference arm -------------------------------------------------------
 
 def run_reference_arm(args):
-    if args.steps is None:
-        args.steps = 20  # each step is a 2M-record CPU sample (~0.6 s)
+    """The reference's own CPU path (unmodified flowmon::aggregate from
+    oracle/_ref) on this box's host cores, on the GPU arm's workload, metric
+    and config: every step is a bounded sample (the workload's first M
+    records, M sized from a warmed probe so the whole run stays within a few
+    minutes), at the fastest worker count. Rank 0 only."""
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
-    from paper_1108_1785_b200 import synth
-    w = synth.workload(args.workload)
+    import workloads
+    w = workloads.workload(args.workload)
+    n = args.records or w.n
     nproc = os.cpu_count() or 1
-    R, cat, rec = reference_sample(w, args.cpu_sample)
-    workers = reference_workers(args.cpu_sample, nproc)
-    # Pick the fastest worker count (the reference gets slower with more
-    # workers on shuffled data): one warm-up run first (page
-    # faults, allocator), then the median of two runs per worker count.
-    R.time_range(rec, cat, 0, args.cpu_sample, 1)
-    probe = {wk: statistics.median(R.time_range(rec, cat, 0, args.cpu_sample, wk) for _ in range(2))
+    steps = args.steps if args.steps is not None else 10
+    # Probe on a 2M-record prefix: warm-up (page faults, allocator), then the
+    # median of two runs per worker count (the reference gets slower with
+    # more workers on shuffled data, BASELINE.md §2).
+    n_probe = min(args.cpu_sample, n)
+    R, cat, rec = reference_sample(w, n_probe)
+    workers = reference_workers(n_probe, nproc)
+    R.time_range(rec, cat, 0, n_probe, 1)
+    probe = {wk: statistics.median(R.time_range(rec, cat, 0, n_probe, wk) for _ in range(2))
              for wk in workers}
     best = min(probe, key=probe.get)
+    rate = n_probe / (probe[best] / 1e3)
+    # Sample size: ~150 s of timed CPU work over warmup + steps, 2M..20M
+    # records (never more than the workload).
+    budget_s = float(os.environ.get("GNM_REF_BUDGET_S", "150"))
+    m = int(rate * budget_s / max(1, steps + args.warmup))
+    m = max(min(n_probe, n), min(n, 20_000_000, m))
+    if m != n_probe:
+        del rec
+        R, cat, rec = reference_sample(w, m)
+        if best not in reference_workers(m, nproc):
+            best = max(reference_workers(m, nproc))
     for _ in range(args.warmup):
-        R.time_range(rec, cat, 0, args.cpu_sample, best)
-    ts = [R.time_range(rec, cat, 0, args.cpu_sample, best) for _ in range(args.steps)]
+        R.time_range(rec, cat, 0, m, best)
+    ts = [R.time_range(rec, cat, 0, m, best) for _ in range(steps)]
     total_ms = sum(ts)
-    value = args.cpu_sample * len(ts) / (total_ms / 1e3)
+    value = m * len(ts) / (total_ms / 1e3)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "records/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
         "ms_per_step": total_ms / len(ts), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32/u64 int + f64", "data": "synthetic",
-        "config": {"workload": f"{args.workload}: sample of {args.cpu_sample} records "
-                               f"({w.sites.base.size} sites, zipf {w.zipf_s})",
-                   "parallelism": f"cpu threads={best}"},
+        "config": workload_config(w, n, len(w.sites.base), world, args),
         "cpu_baseline": {"value": value, "unit": "records/s", "cores": best, "kind": "reference",
-                         "sample": f"first {args.cpu_sample} records of {args.workload}; "
-                                   f"flowmon::aggregate(FilterParams{{}}, workers={best}, Hash); "
-                                   f"probe ms by workers {json.dumps({str(k): round(v, 1) for k, v in probe.items()})}; "
+                         "sample": f"each step: the first {m} of the workload's {n} records per GPU "
+                                   f"(hosts computed, as the reference always does); unmodified "
+                                   f"flowmon::aggregate(FilterParams{{}}, workers={best}, Hash) from "
+                                   f"oracle/_ref (-O3 -DNDEBUG); worker probe on {n_probe} records, ms by "
+                                   f"workers {json.dumps({str(k): round(v, 1) for k, v in probe.items()})}; "
                                    f"nproc={nproc}, cpu={cpu_model()}"},
         "e2e": {"value": value, "unit": "records/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "parallelism_note": f"cpu threads={best}",
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -341,6 +387,10 @@ def run_stream(args):
 
 def main():
     args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}")
     if args.steps is None and args.impl != "reference" and args.workload != "D5":
         args.steps = 100
     if args.impl == "reference":
@@ -358,6 +408,9 @@ def main():
     # combine every step, max over ranks) at world size 1 -- NCCL on the one
     # GPU a test box has.
     distributed = world > 1 or bool(os.environ.get("GNM_BENCH_FORCE_DIST"))
+    if local >= torch.cuda.device_count():
+        raise SystemExit(f"bench.py: rank {rank} needs cuda:{local}, "
+                         f"{torch.cuda.device_count()} device(s) visible")
     if distributed:
         # NCCL over NVLink; GNM_BENCH_BACKEND=gloo is a test hook for several
         # ranks on the one GPU a test box has (NCCL refuses shared devices).
@@ -499,13 +552,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u32/u64 int + f64", "data": "synthetic",
-        "config": {"workload": f"{w.name}: {n} records/GPU, {n_sites} /24 sites, Zipf s={w.zipf_s}, "
-                               f"8 hosts/site, 40% forward",
-                   "records_per_gpu": n, "sites": n_sites, "input": args.input,
-                   "hosts": (f"per-host rows built every step ({len(res.host_table)} rows)" if args.hosts
-                             else "site level only (gnm_ctx_set_hosts off)"), "parallelism": f"index shards x{world}",
-                   "l2": "inputs 3.2 GB/GPU > 126 MB L2; no flush needed" if n >= 10_000_000
-                         else "inputs may fit L2"},
+        "config": workload_config(w, n, n_sites, world, args),
         "e2e": {"value": e2e_value, "unit": "records/s",
                 "h2d_bytes_per_step": n * (ALG_BYTES_PER_RECORD if args.input == "soa" else 64),
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / e2e_steps,

@@ -292,6 +292,8 @@ int gnm_analyze_window(gnm_ctx* ctx, const gnm_registry* reg, const gnm_filter_p
                        const gnm_batch_soa* batch, gnm_result* result);
 int gnm_accumulate_aos(gnm_ctx* ctx, const gnm_registry* reg, const gnm_filter_params* params,
                        const gnm_batch_aos* batch);
+/* GNM_ERR_CAPACITY (after the rows are written) when one accumulation held
+ * 2^32 or more Forward flows: the u32 coarse counts could have wrapped. */
 int gnm_finalize(gnm_ctx* ctx, const gnm_registry* reg, gnm_result* result);
 /* Drop accumulated partials without producing a result. */
 int gnm_reset(gnm_ctx* ctx);

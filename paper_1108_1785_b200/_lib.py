@@ -16,7 +16,6 @@ LIB_DIR = os.path.join(_HERE, "lib")
 # GNM_LIB: measurement builds only (tools/ablation.sh); the product and the
 # tests load the in-tree library.
 LIB_PATH = os.environ.get("GNM_LIB") or os.path.join(LIB_DIR, "libgnetmon.so")
-SYNTH_PATH = os.path.join(LIB_DIR, "libgnm_synth.so")
 
 BUCKET_COUNT = 10001
 NO_SITE = 0xFFFFFFFF

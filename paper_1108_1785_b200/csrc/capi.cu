@@ -94,6 +94,7 @@ struct gnm_ctx {
     unsigned int* d_log = nullptr;
     unsigned int* d_logb = nullptr;
     size_t log_cap = 0, log_used = 0;
+    size_t logb_cap = 0; // d_logb grows only for wide registries: its own capacity
     bool log_wide = false;
     unsigned int* d_counts = nullptr;
     size_t counts_cap = 0, counts_used = 0;
@@ -410,12 +411,8 @@ gnm::DevLog reserve_log(gnm_ctx* c, const gnm::LaunchCfg& cfg, const gnm::DevBat
     const size_t need = static_cast<size_t>(sl.warp_cap) * sl.regions;
     const bool wide = c->P.n_sites >= gnm::kLogPackedSites;
     if (c->slices.empty()) c->log_wide = wide;
-    size_t bcap = c->log_cap;
     grow_u32(c, &c->d_log, &c->log_cap, c->log_used, c->log_used + need, "log");
-    if (wide) {
-        if (!c->d_logb) bcap = 0;
-        grow_u32(c, &c->d_logb, &bcap, c->log_used, c->log_cap, "log buckets");
-    }
+    if (wide) grow_u32(c, &c->d_logb, &c->logb_cap, c->log_used, c->log_cap, "log buckets");
     grow_u32(c, &c->d_counts, &c->counts_cap, c->counts_used, c->counts_used + sl.regions, "log counts");
     if (c->hosts && c->lhost_cap < c->log_cap) {
         const size_t used = c->log_used, want = c->log_cap;
@@ -598,6 +595,9 @@ int accumulate_aos(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params*
                    const gnm_batch_aos* b, const Window* win = nullptr) {
     if (!b) return fail(GNM_ERR_INVALID_ARGUMENT, "null batch");
     if (b->n && !b->records) return fail(GNM_ERR_INVALID_ARGUMENT, "null records");
+    // the AoS layouts read u32/u64 fields in place (FlowRecord is 8-byte aligned)
+    if (b->mem == GNM_MEM_DEVICE && reinterpret_cast<uintptr_t>(b->records) % 8)
+        return fail(GNM_ERR_INVALID_ARGUMENT, "device FlowRecord rows must be 8-byte aligned");
     if (c->prepared) return fail(GNM_ERR_INVALID_ARGUMENT, "gnm_prepare_median already ran; finalize first");
     if (int e = begin_accumulate(c, reg)) return e;
     gnm::DevParams p = dev_params(c, params);
@@ -716,6 +716,12 @@ int finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* r, int phase = 3) 
     r->tallies.administrative = t[2];
     r->tallies.unmatched = t[3];
     r->n_sites = n_sites;
+    c->accumulating = false;
+    // coarse counts are u32 per (super-bucket, site): with fewer than 2^32
+    // Forward flows per accumulation (all ranks) none of them can wrap
+    if (r->tallies.forward >> 32)
+        return fail(GNM_ERR_CAPACITY, "more than 2^32-1 Forward flows in one accumulation: "
+                                      "finalize at least every 4G Forward flows");
     if (c->timing) {
         c->tot_k2 += c->k2_pairs.size();
         c->acc_ms = drain_pairs(c, c->k2_pairs);

@@ -59,6 +59,7 @@ def combine(engine, catalog, group=None, stream=None) -> None:
     ``stream``: the torch stream wrapping the engine's stream (collectives
     are ordered after K2 on it)."""
     t = engine.device_tensors(catalog)
+    stream = _engine_stream(engine, t, stream)
     ctx = torch.cuda.stream(stream) if stream is not None else _nullctx()
     with ctx:
         allreduce_partials(t, group)
@@ -92,6 +93,7 @@ def combine_hosts(engine, catalog, group=None, stream=None) -> None:
     local = engine.hosts_local_keys(catalog)
     union = key_union(local, group)
     t = engine.hosts_set_keys(union)
+    stream = _engine_stream(engine, t, stream)
     ctx = torch.cuda.stream(stream) if stream is not None else _nullctx()
     with ctx:
         dist.all_reduce(t["sums"], op=dist.ReduceOp.SUM, group=group)
@@ -103,6 +105,16 @@ def combine_hosts(engine, catalog, group=None, stream=None) -> None:
     with ctx:
         dist.all_reduce(t["fine"], op=dist.ReduceOp.SUM, group=group)
     torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
+
+
+def _engine_stream(engine, t: dict, stream):
+    """The stream the collectives run on: the caller's, else -- for CUDA
+    partials -- the engine's own stream, so the all-reduces are ordered after
+    K2 and before K3a/K2b/K3b (the engine launches on a non-blocking stream
+    that torch's current stream does not order against)."""
+    if stream is not None or not t["sums"].is_cuda or not hasattr(engine, "stream_handle"):
+        return stream
+    return torch.cuda.ExternalStream(engine.stream_handle(), device=t["sums"].device)
 
 
 class _nullctx:
