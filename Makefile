@@ -38,7 +38,9 @@ oracle:
 
 ref:
 	$(MAKE) -C oracle ref
+	$(MAKE) -C integration all
 
 clean:
 	rm -rf $(PKG)/lib workloads/lib
 	$(MAKE) -C oracle clean
+	$(MAKE) -C integration clean

@@ -1,0 +1,285 @@
+// The drop-in C++ adapter: flowmon::aggregate and flowmon::aggregate_partitioned
+// with the reference's exact signatures (rate_engine.hpp:143-154), computed on
+// the B200 through the C-ABI (include/gnetmon.h, libgnetmon.so).
+//
+// Link-time substitution (the reference has no plugin mechanism, SURVEY.md
+// §8b): the reference's rate_engine.cpp is compiled with
+//   -Daggregate=cpu_aggregate -Daggregate_partitioned=cpu_aggregate_partitioned
+// so its CPU path stays callable under those names, and this file provides
+// the two symbols every caller binds -- monitor.cpp:118 (run_cycle),
+// toolkit.cpp:297 (run_bench), acceptance.cpp:220/351, engine_test.cpp. The
+// rest of rate_engine.cpp (RateHistogram, classify, flow_rate, bucket_index,
+// attribute) is the reference's own code.
+//
+// The whole AnalysisResult is produced, not just the site level: every
+// SiteResult with its RateStats and RateHistogram, and SiteResult::hosts with
+// each host's RateStats and RateHistogram (rate_engine.cpp:255-292), so the
+// reference's AnalysisResult::operator== (rate_engine.hpp:112-119) can judge
+// it against cpu_aggregate.
+//
+// RateHistogram keeps its state private (rate_engine.hpp:68-73); it is rebuilt
+// through its public add(): one add at the exact min rate carrying the whole
+// u128 micro-bps sum, one at the exact max, and the remaining count of every
+// bucket at a rate inside that bucket and inside [min, max]. count_,
+// sum_ubps_, min_bps_, max_bps_ and buckets_ then equal the GPU's exact
+// integers and doubles field for field.
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "flowmon/rate_engine.hpp"
+#include "flowmon/site_catalog.hpp"
+#include "gnetmon.h"
+
+namespace flowmon {
+
+namespace {
+
+using u128 = unsigned __int128;
+
+[[noreturn]] void gpu_fail(const char* what) {
+    throw std::runtime_error(std::string("flowmon GPU adapter: ") + what + ": " + gnm_last_error());
+}
+
+void check(int status, const char* what) {
+    if (status != GNM_OK) gpu_fail(what);
+}
+
+// One context per host thread (gnetmon.h: calls on a context are serialized;
+// the reference's callers are single-threaded per monitor).
+struct Engine {
+    gnm_ctx* ctx = nullptr;
+    gnm_registry* reg = nullptr;
+    // the catalog the registry was compiled from: its (prefix24, site) entries
+    // and sites, compared on every call (a rebuild only on change)
+    std::vector<std::pair<std::uint32_t, SiteId>> entries;
+    std::size_t n_sites = 0;
+
+    Engine() {
+        const char* dev = std::getenv("GNM_DEVICE");
+        check(gnm_ctx_create(dev ? std::atoi(dev) : 0, &ctx), "gnm_ctx_create");
+        check(gnm_ctx_set_hosts(ctx, 1), "gnm_ctx_set_hosts"); // SiteResult::hosts
+    }
+    ~Engine() {
+        gnm_registry_destroy(reg);
+        gnm_ctx_destroy(ctx);
+    }
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    // SiteCatalog -> gnm_registry, sites in registration order so SiteIds
+    // (dense registration indices, site_catalog.cpp:91) are identical.
+    void sync(const SiteCatalog& catalog) {
+        if (reg && n_sites == catalog.site_count() && entries == catalog.entries()) return;
+        gnm_registry* r = nullptr;
+        check(gnm_registry_create(&r), "gnm_registry_create");
+        std::vector<gnm_cidr> cidrs;
+        for (const SiteCatalog::Site& s : catalog.sites()) {
+            cidrs.clear();
+            for (const Cidr& c : s.cidrs) cidrs.push_back({c.addr, static_cast<std::int32_t>(c.prefix_len)});
+            std::uint32_t id = 0;
+            if (gnm_registry_register_site(r, s.name.c_str(), cidrs.data(), cidrs.size(), &id) != GNM_OK ||
+                id != s.id) {
+                gnm_registry_destroy(r);
+                gpu_fail("registry rebuild");
+            }
+        }
+        gnm_registry_destroy(reg);
+        reg = r;
+        entries = catalog.entries();
+        n_sites = catalog.site_count();
+    }
+};
+
+Engine& engine() {
+    thread_local Engine e;
+    return e;
+}
+
+struct BucketCount {
+    std::uint32_t bucket;
+    std::uint32_t count;
+};
+
+// RateHistogram with exactly these buckets (ascending, non-zero), count, u128
+// sum and bounds, through its public add() (see the file comment).
+RateHistogram rebuild_histogram(const std::vector<BucketCount>& buckets, std::uint64_t count, u128 sum,
+                                double min_bps, double max_bps) {
+    RateHistogram h;
+    if (count == 0) {
+        if (!buckets.empty()) throw std::runtime_error("flowmon GPU adapter: buckets without flows");
+        return h;
+    }
+    std::uint64_t total = 0;
+    for (const BucketCount& b : buckets) total += b.count;
+    const std::size_t bmin = bucket_index(min_bps), bmax = bucket_index(max_bps);
+    std::vector<BucketCount> rem = buckets;
+    auto take = [&](std::size_t k) {
+        for (BucketCount& b : rem)
+            if (b.bucket == k && b.count) {
+                --b.count;
+                return;
+            }
+        throw std::runtime_error("flowmon GPU adapter: min/max outside the histogram's buckets");
+    };
+    if (total != count || min_bps > max_bps)
+        throw std::runtime_error("flowmon GPU adapter: histogram inconsistent with its stats");
+    h.add(min_bps, sum);
+    take(bmin);
+    if (count > 1) {
+        h.add(max_bps, 0);
+        take(bmax);
+    }
+    for (const BucketCount& b : rem) {
+        double rate;
+        if (b.bucket == bmin) rate = min_bps;
+        else if (b.bucket == bmax) rate = max_bps;
+        else if (b.bucket + 1 < kBucketCount) rate = static_cast<double>(b.bucket) * kBucketWidthBps + kBucketWidthBps / 2;
+        else throw std::runtime_error("flowmon GPU adapter: overflow bucket above max");
+        // strictly between bmin and bmax: the midpoint lies inside (min, max)
+        for (std::uint32_t i = 0; i < b.count; ++i) h.add(rate, 0);
+    }
+    return h;
+}
+
+RateStats stats_of(std::uint64_t count, double min_bps, double max_bps, double avg_bps, double median_bps) {
+    RateStats s;
+    s.flow_count = count;
+    s.min_bps = min_bps;
+    s.max_bps = max_bps;
+    s.avg_bps = avg_bps;
+    s.median_bps = median_bps;
+    return s;
+}
+
+u128 join(std::uint64_t lo, std::uint64_t hi) { return static_cast<u128>(hi) << 64 | lo; }
+
+// The GPU's finalize (site rows, tallies, per-host rows and their sparse
+// histograms) -> AnalysisResult, in the reference's map order.
+AnalysisResult collect(Engine& e, const gnm_result& r, const std::vector<gnm_site_stats>& rows) {
+    AnalysisResult out;
+    out.window_start_ms = r.window_start_ms;
+    out.window_end_ms = r.window_end_ms;
+    out.tallies.forward = r.tallies.forward;
+    out.tallies.pure_ack = r.tallies.pure_ack;
+    out.tallies.administrative = r.tallies.administrative;
+    out.tallies.unmatched = r.tallies.unmatched;
+
+    const std::uint64_t nh = gnm_host_count(e.ctx);
+    std::vector<gnm_host_stats> hosts(nh);
+    if (nh) check(gnm_host_results(e.ctx, hosts.data(), nh, nullptr), "gnm_host_results");
+    std::uint64_t ne = 0;
+    check(gnm_host_histogram_entries(e.ctx, nullptr, nullptr, nullptr, 0, &ne), "gnm_host_histogram_entries");
+    std::vector<std::uint32_t> er(ne), eb(ne), ec(ne);
+    if (ne) check(gnm_host_histogram_entries(e.ctx, er.data(), eb.data(), ec.data(), ne, &ne),
+                  "gnm_host_histogram_entries");
+
+    std::vector<std::uint64_t> site_dense(kBucketCount, 0);
+    std::vector<BucketCount> hb, sb;
+    std::uint64_t ei = 0, covered = 0;
+    for (std::uint64_t i = 0; i < nh;) {
+        const std::uint32_t site = hosts[i].site;
+        if (site >= rows.size() || rows[site].flow_count == 0)
+            throw std::runtime_error("flowmon GPU adapter: host row of an empty or unknown site");
+        const gnm_site_stats& g = rows[site];
+        SiteResult& sr = out.sites[site];
+        std::uint64_t host_flows = 0;
+        for (; i < nh && hosts[i].site == site; ++i) {
+            const gnm_host_stats& h = hosts[i];
+            hb.clear();
+            for (; ei < ne && er[ei] == i; ++ei) {
+                hb.push_back({eb[ei], ec[ei]});
+                site_dense[eb[ei]] += ec[ei];
+            }
+            HostResult& hr = sr.hosts[h.host];
+            hr.stats = stats_of(h.flow_count, h.min_bps, h.max_bps, h.avg_bps, h.median_bps);
+            hr.histogram = rebuild_histogram(hb, h.flow_count, join(h.rate_ubps_lo, h.rate_ubps_hi), h.min_bps,
+                                             h.max_bps);
+            host_flows += h.flow_count;
+        }
+        if (host_flows != g.flow_count)
+            throw std::runtime_error("flowmon GPU adapter: host rows do not sum to the site's flows");
+        sb.clear();
+        for (std::size_t k = 0; k < kBucketCount; ++k)
+            if (site_dense[k]) {
+                if (site_dense[k] > UINT32_MAX) throw std::runtime_error("flowmon GPU adapter: bucket overflow");
+                sb.push_back({static_cast<std::uint32_t>(k), static_cast<std::uint32_t>(site_dense[k])});
+                site_dense[k] = 0;
+            }
+        sr.stats = stats_of(g.flow_count, g.min_bps, g.max_bps, g.avg_bps, g.median_bps);
+        sr.histogram = rebuild_histogram(sb, g.flow_count, join(g.rate_ubps_lo, g.rate_ubps_hi), g.min_bps,
+                                         g.max_bps);
+        ++covered;
+    }
+    if (ei != ne) throw std::runtime_error("flowmon GPU adapter: histogram entries past the last host row");
+    std::uint64_t present = 0;
+    for (const gnm_site_stats& g : rows) present += g.flow_count != 0;
+    if (present != covered) throw std::runtime_error("flowmon GPU adapter: site without host rows");
+    return out;
+}
+
+// Slices (the reference's run_partitioned, rate_engine.cpp:294-331) become
+// successive gnm_accumulate_aos calls into one accumulation; the GPU result
+// is identical for any split (exact integer reductions), as the reference's
+// is by its monoid contract.
+AnalysisResult run_gpu(std::span<const FlowRecord> view, const SiteCatalog& catalog, const FilterParams& params,
+                       const std::vector<std::size_t>& boundaries, std::uint64_t window_start_ms,
+                       std::uint64_t window_end_ms) {
+    static_assert(sizeof(FlowRecord) == GNM_FLOW_RECORD_BYTES, "FlowRecord is the 64-byte gnm_batch_aos row");
+    Engine& e = engine();
+    e.sync(catalog);
+    const gnm_filter_params p{params.ack_avg_size_max, params.min_packets, params.min_duration_ms,
+                              params.workers};
+    std::size_t prev = 0;
+    auto slice = [&](std::size_t end) {
+        if (end < prev || end > view.size()) {
+            gnm_reset(e.ctx);
+            throw std::out_of_range("aggregate_partitioned: boundaries must be sorted and within the view");
+        }
+        const gnm_batch_aos b{view.data() + prev, end - prev, GNM_MEM_HOST};
+        if (int st = gnm_accumulate_aos(e.ctx, e.reg, &p, &b)) {
+            gnm_reset(e.ctx);
+            check(st, "gnm_accumulate_aos");
+        }
+        prev = end;
+    };
+    for (std::size_t b : boundaries) slice(b);
+    slice(view.size());
+
+    std::vector<gnm_site_stats> rows(e.n_sites);
+    gnm_result r{};
+    r.window_start_ms = window_start_ms; // copied through, never a filter (rate_engine.cpp:257-258)
+    r.window_end_ms = window_end_ms;
+    r.threshold_bps = GNM_DEFAULT_WARN_THRESHOLD_BPS;
+    r.sites_capacity = static_cast<std::uint32_t>(rows.size());
+    r.sites = rows.data();
+    r.histograms = nullptr; // site histograms are the sums of the host histograms
+    check(gnm_finalize(e.ctx, e.reg, &r), "gnm_finalize");
+    return collect(e, r, rows);
+}
+
+} // namespace
+
+// rate_engine.cpp:335-347. `workers` and `mode` select nothing on the GPU:
+// the result is identical for every worker count and lookup mode, by the
+// reference's own contract (engine_test.cpp:344-360).
+AnalysisResult aggregate(std::span<const FlowRecord> view, const SiteCatalog& catalog, const FilterParams& params,
+                         unsigned /*workers*/, LookupMode /*mode*/, std::uint64_t window_start_ms,
+                         std::uint64_t window_end_ms) {
+    return run_gpu(view, catalog, params, {}, window_start_ms, window_end_ms);
+}
+
+// rate_engine.cpp:349-355 (the test hook over caller-chosen slices).
+AnalysisResult aggregate_partitioned(std::span<const FlowRecord> view, const SiteCatalog& catalog,
+                                     const FilterParams& params, const std::vector<std::size_t>& boundaries,
+                                     LookupMode /*mode*/, std::uint64_t window_start_ms,
+                                     std::uint64_t window_end_ms) {
+    return run_gpu(view, catalog, params, boundaries, window_start_ms, window_end_ms);
+}
+
+} // namespace flowmon
