@@ -10,10 +10,12 @@
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
-           -Xptxas -v -cudart static -Iinclude
+           -Xptxas -v -cudart static -Iinclude -ldl
 PKG := paper_1108_1785_b200
-SRCS := $(PKG)/csrc/capi.cu $(PKG)/csrc/kernels.cu $(PKG)/csrc/netflow.cu $(PKG)/csrc/hosts.cu $(PKG)/csrc/registry.cpp
-HDRS := include/gnetmon.h $(PKG)/csrc/kernels.cuh $(PKG)/csrc/netflow.cuh $(PKG)/csrc/hosts.cuh $(PKG)/csrc/registry.hpp
+SRCS := $(PKG)/csrc/capi.cu $(PKG)/csrc/kernels.cu $(PKG)/csrc/netflow.cu $(PKG)/csrc/hosts.cu $(PKG)/csrc/registry.cpp \
+        $(PKG)/csrc/comm.cpp
+HDRS := include/gnetmon.h $(PKG)/csrc/kernels.cuh $(PKG)/csrc/netflow.cuh $(PKG)/csrc/hosts.cuh $(PKG)/csrc/registry.hpp \
+        $(PKG)/csrc/comm.hpp
 
 .PHONY: all ref clean oracle ablation
 all: $(PKG)/lib/libgnetmon.so workloads/lib/libgnm_synth.so oracle

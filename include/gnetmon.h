@@ -50,7 +50,8 @@ typedef enum gnm_status {
     GNM_ERR_CAPACITY = 9,       /* caller buffer too small */
     GNM_ERR_BAD_MAGIC = 10,     /* ArchiveError::Kind::BadMagic          flow_store.hpp:24 */
     GNM_ERR_BAD_VERSION = 11,   /* ArchiveError::Kind::BadVersion */
-    GNM_ERR_TRUNCATED = 12      /* ArchiveError::Kind::TruncatedArchive (incl. trailing bytes) */
+    GNM_ERR_TRUNCATED = 12,     /* ArchiveError::Kind::TruncatedArchive (incl. trailing bytes) */
+    GNM_ERR_COMM = 13           /* NCCL / communicator failure (multi-GPU combine) */
 } gnm_status;
 
 /* FlowClass (rate_engine.hpp:31), same ordinal values. */
@@ -326,8 +327,64 @@ typedef struct gnm_partials {
 } gnm_partials;
 int gnm_get_partials(gnm_ctx* ctx, const gnm_registry* reg, gnm_partials* out);
 /* Round 2 of the median on this context's log (see gnm_partials); no further
- * gnm_accumulate until gnm_finalize or gnm_reset. */
+ * gnm_accumulate until gnm_finalize or gnm_reset. Not with a communicator
+ * (gnm_ctx_comm_init), whose finalize runs both rounds itself. */
 int gnm_prepare_median(gnm_ctx* ctx, const gnm_registry* reg);
+
+/* ---- Multi-GPU inside the library ---------------------------
+ * Records shard by index across the GPUs -- rank i of N takes
+ * [n*i/N, n*(i+1)/N), the reference's worker boundaries (rate_engine.cpp:
+ * 341-344) -- and the per-site partials combine in two rounds of NCCL
+ * all-reduces over NVLink (round 1: sums and coarse counts SUM, min MIN, max
+ * MAX, as one ncclGroupStart/End call; round 2: the median super-buckets'
+ * fine counts SUM), enqueued on the context's stream between K2 and K3b.
+ * With a communicator attached, gnm_finalize / gnm_analyze* run the combine
+ * themselves: every rank returns the same global result. In per-host mode
+ * the ranks' (site, host) keys are all-gathered into their sorted union
+ * first; the host rows are then global, and a rank's host histograms
+ * (gnm_host_results / gnm_host_histogram_entries) count that rank's own
+ * flows over the global rows (gnm_group_host_histogram_entries sums them).
+ * NCCL (libnccl.so.2) is loaded on first use. */
+
+#define GNM_COMM_ID_BYTES 128 /* sizeof(ncclUniqueId) */
+
+/* One process per GPU: rank 0 creates the id, the caller distributes it to
+ * every rank out of band, and each rank attaches its context (the calls
+ * block until all N ranks have joined). */
+int gnm_comm_unique_id(unsigned char out[GNM_COMM_ID_BYTES]);
+int gnm_ctx_comm_init(gnm_ctx* ctx, int nranks, int rank, const unsigned char id[GNM_COMM_ID_BYTES]);
+/* Detach (and destroy) the context's communicator. */
+int gnm_ctx_comm_destroy(gnm_ctx* ctx);
+/* Ranks in the context's communicator (1 without one). */
+int gnm_ctx_comm_size(gnm_ctx* ctx);
+
+/* One process driving N GPUs: one context per device and one NCCL clique
+ * (ncclCommInitAll). GNM_GROUP_LOOPBACK exchanges through host memory
+ * instead -- a test hook that runs the same orchestration with several
+ * ranks on one device (NCCL rejects two ranks on one GPU). */
+typedef struct gnm_group gnm_group;
+#define GNM_GROUP_NCCL 0
+#define GNM_GROUP_LOOPBACK 1
+int gnm_group_create(const int* devices, int n_devices, int kind, gnm_group** out);
+void gnm_group_destroy(gnm_group* group);
+int gnm_group_size(const gnm_group* group);
+/* Rank i's context (per-context settings: hosts mode, hot mode, chunking). */
+gnm_ctx* gnm_group_ctx(gnm_group* group, int rank);
+/* aggregate over the group's GPUs: shard i of the batch to rank i, every
+ * rank accumulates its shard and finalizes with the combine (one host
+ * thread per rank); `result` receives the global rows. Host or device
+ * batches (device batches must be readable from every rank's GPU). */
+int gnm_group_analyze(gnm_group* group, const gnm_registry* reg, const gnm_filter_params* params,
+                      const gnm_batch_soa* batch, gnm_result* result);
+int gnm_group_analyze_aos(gnm_group* group, const gnm_registry* reg, const gnm_filter_params* params,
+                          const gnm_batch_aos* batch, gnm_result* result);
+/* Per-host rows of the last group analysis (hosts mode on every rank's
+ * context): the global rows, and their histograms summed over the ranks as
+ * sparse (row, bucket, count) entries in (row, bucket) order. */
+uint64_t gnm_group_host_count(gnm_group* group);
+int gnm_group_host_results(gnm_group* group, gnm_host_stats* out, uint64_t capacity);
+int gnm_group_host_histogram_entries(gnm_group* group, uint32_t* rows, uint32_t* buckets, uint32_t* counts,
+                                     uint64_t capacity, uint64_t* n_entries);
 
 /* Per-record classification (classify/attribute, rate_engine.cpp:71-86,
  * 127-146): out[i] = class << 30 | (site & 0x3FFFFFFF), site = 0x3FFFFFFF

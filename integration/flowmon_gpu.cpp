@@ -52,8 +52,13 @@ void check(int status, const char* what) {
 
 // One context per host thread (gnetmon.h: calls on a context are serialized;
 // the reference's callers are single-threaded per monitor).
+// GNM_ADAPTER_DEVICES="0,1,2,3" shards every call across those GPUs
+// (gnm_group: the reference's worker boundaries, the combine over NCCL);
+// "loopback:0,0" runs the same multi-rank orchestration through host memory
+// (a test hook for one-GPU boxes). Default: one context on GNM_DEVICE or 0.
 struct Engine {
-    gnm_ctx* ctx = nullptr;
+    gnm_group* group = nullptr;
+    gnm_ctx* ctx = nullptr; // the only context, or rank 0 of the group
     gnm_registry* reg = nullptr;
     // the catalog the registry was compiled from: its (prefix24, site) entries
     // and sites, compared on every call (a rebuild only on change)
@@ -61,13 +66,38 @@ struct Engine {
     std::size_t n_sites = 0;
 
     Engine() {
-        const char* dev = std::getenv("GNM_DEVICE");
-        check(gnm_ctx_create(dev ? std::atoi(dev) : 0, &ctx), "gnm_ctx_create");
-        check(gnm_ctx_set_hosts(ctx, 1), "gnm_ctx_set_hosts"); // SiteResult::hosts
+        if (const char* spec = std::getenv("GNM_ADAPTER_DEVICES")) {
+            std::string s = spec;
+            int kind = GNM_GROUP_NCCL;
+            if (s.rfind("loopback:", 0) == 0) {
+                kind = GNM_GROUP_LOOPBACK;
+                s = s.substr(9);
+            }
+            std::vector<int> devs;
+            for (std::size_t a = 0; a < s.size();) {
+                const std::size_t b = std::min(s.find(',', a), s.size());
+                devs.push_back(std::stoi(s.substr(a, b - a)));
+                a = b + 1;
+            }
+            check(gnm_group_create(devs.data(), static_cast<int>(devs.size()), kind, &group), "gnm_group_create");
+            for (int i = 0; i < gnm_group_size(group); ++i)
+                check(gnm_ctx_set_hosts(gnm_group_ctx(group, i), 1), "gnm_ctx_set_hosts");
+            ctx = gnm_group_ctx(group, 0);
+        } else {
+            const char* dev = std::getenv("GNM_DEVICE");
+            check(gnm_ctx_create(dev ? std::atoi(dev) : 0, &ctx), "gnm_ctx_create");
+            check(gnm_ctx_set_hosts(ctx, 1), "gnm_ctx_set_hosts"); // SiteResult::hosts
+        }
     }
     ~Engine() {
         gnm_registry_destroy(reg);
-        gnm_ctx_destroy(ctx);
+        if (group) gnm_group_destroy(group);
+        else gnm_ctx_destroy(ctx);
+    }
+    int host_entries(std::uint32_t* rows, std::uint32_t* buckets, std::uint32_t* counts, std::uint64_t cap,
+                     std::uint64_t* n) {
+        return group ? gnm_group_host_histogram_entries(group, rows, buckets, counts, cap, n)
+                     : gnm_host_histogram_entries(ctx, rows, buckets, counts, cap, n);
     }
     Engine(const Engine&) = delete;
     Engine& operator=(const Engine&) = delete;
@@ -174,10 +204,9 @@ AnalysisResult collect(Engine& e, const gnm_result& r, const std::vector<gnm_sit
     std::vector<gnm_host_stats> hosts(nh);
     if (nh) check(gnm_host_results(e.ctx, hosts.data(), nh, nullptr), "gnm_host_results");
     std::uint64_t ne = 0;
-    check(gnm_host_histogram_entries(e.ctx, nullptr, nullptr, nullptr, 0, &ne), "gnm_host_histogram_entries");
+    check(e.host_entries(nullptr, nullptr, nullptr, 0, &ne), "host histogram entries");
     std::vector<std::uint32_t> er(ne), eb(ne), ec(ne);
-    if (ne) check(gnm_host_histogram_entries(e.ctx, er.data(), eb.data(), ec.data(), ne, &ne),
-                  "gnm_host_histogram_entries");
+    if (ne) check(e.host_entries(er.data(), eb.data(), ec.data(), ne, &ne), "host histogram entries");
 
     std::vector<std::uint64_t> site_dense(kBucketCount, 0);
     std::vector<BucketCount> hb, sb;
@@ -235,6 +264,23 @@ AnalysisResult run_gpu(std::span<const FlowRecord> view, const SiteCatalog& cata
     e.sync(catalog);
     const gnm_filter_params p{params.ack_avg_size_max, params.min_packets, params.min_duration_ms,
                               params.workers};
+    std::vector<gnm_site_stats> rows(e.n_sites);
+    gnm_result r{};
+    r.window_start_ms = window_start_ms; // copied through, never a filter (rate_engine.cpp:257-258)
+    r.window_end_ms = window_end_ms;
+    r.threshold_bps = GNM_DEFAULT_WARN_THRESHOLD_BPS;
+    r.sites_capacity = static_cast<std::uint32_t>(rows.size());
+    r.sites = rows.data();
+    r.histograms = nullptr; // site histograms are the sums of the host histograms
+    if (e.group) {
+        // shards across the group's GPUs by the reference's worker boundaries;
+        // caller slices need no separate pass (the result is partition-independent)
+        for (std::size_t b : boundaries)
+            if (b > view.size()) throw std::out_of_range("aggregate_partitioned: boundary past the view");
+        const gnm_batch_aos b{view.data(), view.size(), GNM_MEM_HOST};
+        check(gnm_group_analyze_aos(e.group, e.reg, &p, &b, &r), "gnm_group_analyze_aos");
+        return collect(e, r, rows);
+    }
     std::size_t prev = 0;
     auto slice = [&](std::size_t end) {
         if (end < prev || end > view.size()) {
@@ -250,15 +296,6 @@ AnalysisResult run_gpu(std::span<const FlowRecord> view, const SiteCatalog& cata
     };
     for (std::size_t b : boundaries) slice(b);
     slice(view.size());
-
-    std::vector<gnm_site_stats> rows(e.n_sites);
-    gnm_result r{};
-    r.window_start_ms = window_start_ms; // copied through, never a filter (rate_engine.cpp:257-258)
-    r.window_end_ms = window_end_ms;
-    r.threshold_bps = GNM_DEFAULT_WARN_THRESHOLD_BPS;
-    r.sites_capacity = static_cast<std::uint32_t>(rows.size());
-    r.sites = rows.data();
-    r.histograms = nullptr; // site histograms are the sums of the host histograms
     check(gnm_finalize(e.ctx, e.reg, &r), "gnm_finalize");
     return collect(e, r, rows);
 }

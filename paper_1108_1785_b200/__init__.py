@@ -6,13 +6,13 @@ the C-ABI in include/gnetmon.h. ``flowmon`` mirrors the reference C++ API.
 """
 from . import flowmon  # noqa: F401  (loads lib/libgnetmon.so; fails loudly if absent)
 from .flowmon import (AnalysisResult, ArchiveError, CatalogError, Cidr, ClassTallies, Engine, FilterParams,
-                      FlowBatch, FlowClass, FlowRecords, GnmError, LookupMode, RateStats,
+                      FlowBatch, FlowClass, FlowRecords, GnmError, Group, LookupMode, RateStats,
                       SiteCatalog, SiteResult, SiteWarning, WarningState, aggregate,
                       aggregate_partitioned, evaluate_warnings, format_ipv4, parse_ipv4)
 
 __all__ = [
     "AnalysisResult", "ArchiveError", "CatalogError", "Cidr", "ClassTallies", "Engine", "FilterParams",
-    "FlowBatch", "FlowClass", "FlowRecords", "GnmError", "LookupMode", "RateStats", "SiteCatalog",
+    "FlowBatch", "FlowClass", "FlowRecords", "GnmError", "Group", "LookupMode", "RateStats", "SiteCatalog",
     "SiteResult", "SiteWarning", "WarningState", "aggregate", "aggregate_partitioned",
     "evaluate_warnings", "format_ipv4", "parse_ipv4",
 ]

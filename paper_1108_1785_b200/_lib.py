@@ -35,6 +35,11 @@ ERR_CAPACITY = 9
 ERR_BAD_MAGIC = 10
 ERR_BAD_VERSION = 11
 ERR_TRUNCATED = 12
+ERR_COMM = 13
+
+COMM_ID_BYTES = 128
+GROUP_NCCL = 0
+GROUP_LOOPBACK = 1
 
 HOT_OFF = 0
 HOT_AUTO = 1
@@ -201,6 +206,21 @@ _SIGS = [
     ("gnm_evaluate_warnings", C.c_int,
      [C.POINTER(gnm_result), _P, C.c_double, C.POINTER(gnm_warning), C.c_size_t,
       C.POINTER(C.c_size_t)]),
+    ("gnm_comm_unique_id", C.c_int, [_P]),
+    ("gnm_ctx_comm_init", C.c_int, [_P, C.c_int, C.c_int, _P]),
+    ("gnm_ctx_comm_destroy", C.c_int, [_P]),
+    ("gnm_ctx_comm_size", C.c_int, [_P]),
+    ("gnm_group_create", C.c_int, [C.POINTER(C.c_int), C.c_int, C.c_int, C.POINTER(_P)]),
+    ("gnm_group_destroy", None, [_P]),
+    ("gnm_group_size", C.c_int, [_P]),
+    ("gnm_group_ctx", _P, [_P, C.c_int]),
+    ("gnm_group_analyze", C.c_int,
+     [_P, _P, C.POINTER(gnm_filter_params), C.POINTER(gnm_batch_soa), C.POINTER(gnm_result)]),
+    ("gnm_group_analyze_aos", C.c_int,
+     [_P, _P, C.POINTER(gnm_filter_params), C.POINTER(gnm_batch_aos), C.POINTER(gnm_result)]),
+    ("gnm_group_host_count", C.c_uint64, [_P]),
+    ("gnm_group_host_results", C.c_int, [_P, _P, C.c_uint64]),
+    ("gnm_group_host_histogram_entries", C.c_int, [_P, _P, _P, _P, C.c_uint64, C.POINTER(C.c_uint64)]),
 ]
 SYMBOLS = [s[0] for s in _SIGS]
 

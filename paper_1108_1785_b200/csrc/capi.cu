@@ -11,11 +11,14 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
+#include "comm.hpp"
 #include "gnetmon.h"
 #include "kernels.cuh"
 #include "hosts.cuh"
@@ -48,6 +51,8 @@ int guarded(F&& f) {
         return f();
     } catch (const CudaError& e) {
         return fail(GNM_ERR_CUDA, e.what());
+    } catch (const gnm::CommError& e) {
+        return fail(GNM_ERR_COMM, e.what());
     } catch (const std::bad_alloc&) {
         return fail(GNM_ERR_OUT_OF_MEMORY, "out of memory");
     } catch (const std::exception& e) {
@@ -170,6 +175,11 @@ struct gnm_ctx {
     uint64_t tot_finalizes = 0, tot_k2 = 0, k2_since_fin = 0;
     int occ[2] = {0, 0}; // K2 blocks/SM (cold, hot) for the current table size
     uint64_t k2_launches = 0, kernel_launches = 0, records = 0;
+
+    // multi-GPU: with a communicator, gnm_finalize runs the two-round
+    // combine across the ranks itself (gnm_ctx_comm_init / gnm_group_*)
+    std::unique_ptr<gnm::Comm> comm;
+    bool discard_hist_out = false; // group ranks > 0: join the histogram all-reduce, keep no copy
 };
 
 namespace {
@@ -645,6 +655,70 @@ void clear_log(gnm_ctx* c) {
     c->prepared = false;
 }
 
+// The multi-GPU combine of the site partials, stream-ordered
+// on the context's stream between K2 and K3b: round 1 (one grouped call:
+// sums and coarse counts SUM, min MIN, max MAX), K3a + K2b on this rank's
+// log against the global coarse counts, round 2 (fine counts SUM). Every
+// rank ends with the same global partials, so K3b's rows are identical.
+void combine_sites(gnm_ctx* c) {
+    gnm::Comm& m = *c->comm;
+    const size_t n = c->P.n_sites;
+    m.group_start();
+    m.all_reduce(c->P.sums, n * 4 + 4, gnm::DType::U64, gnm::RedOp::Sum, c->stream);
+    m.all_reduce(c->P.coarse, n * gnm::kCoarse, gnm::DType::U32, gnm::RedOp::Sum, c->stream);
+    m.all_reduce(c->P.mn, n, gnm::DType::F64, gnm::RedOp::Min, c->stream);
+    m.all_reduce(c->P.mx, n, gnm::DType::F64, gnm::RedOp::Max, c->stream);
+    m.group_end();
+    prepare_median(c);
+    m.all_reduce(c->P.fine, n * gnm::kFineW, gnm::DType::U32, gnm::RedOp::Sum, c->stream);
+}
+
+// Per-host rows across the ranks: every rank's sorted distinct (site, host)
+// keys are all-gathered (counts first, then the key lists padded to the
+// longest), their sorted union becomes the global rows, and the same two
+// rounds as the sites run over them. Synchronises the stream (the union's
+// size sizes the partials), so it is never captured in a graph.
+void combine_hosts(gnm_ctx* c, const gnm_registry* reg) {
+    gnm::Comm& m = *c->comm;
+    const int N = m.nranks();
+    if (!c->hlocal.ready) ck(build_hosts_local(c, reg), "per-host local phase");
+    const uint64_t nl = c->hrows.n_rows;
+    unsigned long long* d_cnt = nullptr;
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&d_cnt), 8 * (N + 1), c->stream), "cudaMallocAsync(key counts)");
+    ck(cudaMemcpyAsync(d_cnt + N, &nl, 8, cudaMemcpyHostToDevice, c->stream), "cudaMemcpyAsync(key count)");
+    m.all_gather(d_cnt + N, d_cnt, 8, c->stream);
+    std::vector<uint64_t> counts(N);
+    ck(cudaMemcpyAsync(counts.data(), d_cnt, 8 * N, cudaMemcpyDeviceToHost, c->stream), "D2H key counts");
+    ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+    ck(cudaFreeAsync(d_cnt, c->stream), "cudaFreeAsync");
+    const uint64_t maxn = std::max<uint64_t>(1, *std::max_element(counts.begin(), counts.end()));
+    unsigned long long *send = nullptr, *all = nullptr, *uni = nullptr;
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&send), 8 * maxn, c->stream), "cudaMallocAsync(keys)");
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&all), 8 * maxn * N, c->stream), "cudaMallocAsync(keys)");
+    ck(cudaMallocAsync(reinterpret_cast<void**>(&uni), 8 * maxn * N, c->stream), "cudaMallocAsync(keys)");
+    ck(cudaMemsetAsync(send, 0xFF, 8 * maxn, c->stream), "cudaMemsetAsync(keys)"); // padding sorts last
+    if (nl) ck(cudaMemcpyAsync(send, c->hlocal.hk_sorted, 8 * nl, cudaMemcpyDeviceToDevice, c->stream), "keys");
+    m.all_gather(send, all, 8 * maxn, c->stream);
+    uint64_t nu = 0;
+    ck(gnm::hosts_key_union(c->device, all, maxn * N, uni, &nu, c->stream), "per-host key union");
+    if (nu >= (1ull << 24)) throw std::runtime_error("the per-host key union holds at most 2^24 - 1 rows");
+    ck(gnm::hosts_global_begin(c->device, c->hrows, c->hlocal, uni, nu, c->hglobal, c->stream),
+       "per-host union partials");
+    c->kernel_launches += 4;
+    for (void* p : {static_cast<void*>(send), static_cast<void*>(all), static_cast<void*>(uni)})
+        ck(cudaFreeAsync(p, c->stream), "cudaFreeAsync");
+    gnm::HostGlobal& g = c->hglobal;
+    m.group_start();
+    m.all_reduce(g.sums, nu * 3, gnm::DType::U64, gnm::RedOp::Sum, c->stream);
+    m.all_reduce(g.min, nu, gnm::DType::F64, gnm::RedOp::Min, c->stream);
+    m.all_reduce(g.max, nu, gnm::DType::F64, gnm::RedOp::Max, c->stream);
+    m.all_reduce(g.coarse, nu * 157, gnm::DType::U32, gnm::RedOp::Sum, c->stream);
+    m.group_end();
+    ck(gnm::hosts_global_prepare(c->device, c->hrows, g, c->stream), "per-host round 2");
+    c->kernel_launches += 2;
+    m.all_reduce(g.fine, nu * 64, gnm::DType::U32, gnm::RedOp::Sum, c->stream);
+}
+
 // phase: 1 = the device work (stream-ordered, capturable), 2 = the host
 // part (wait, copy the rows out, reset the accumulation), 3 = both.
 int finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* r, int phase = 3) {
@@ -666,7 +740,8 @@ int finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* r, int phase = 3) 
         if (!c->hlocal.ready) gnm::free_hosts(c->hrows, c->stream); // else: gnm_hosts_local_keys built them
         if (c->hosts && c->log_used >= (1ull << 32))
             return fail(GNM_ERR_CAPACITY, "per-host mode holds < 2^32 log entries per finalize");
-        prepare_median(c);
+        if (c->comm) combine_sites(c);
+        else prepare_median(c);
         ck(gnm::launch_k3b(c->device, c->P, thr, c->d_out, 1, c->stream), "K3b launch");
         c->kernel_launches += 1;
         if (c->timing) {
@@ -687,12 +762,18 @@ int finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* r, int phase = 3) 
                 ck(gnm::launch_hist_from_log(c->device, slice_view(c, sl), n_sites, dense, c->stream), "hist export");
                 c->kernel_launches += 1;
             }
-            ck(cudaMemcpyAsync(r->histograms, dense, bytes, cudaMemcpyDeviceToHost, c->stream),
-               "cudaMemcpyAsync(D2H hist)");
+            // every rank rebuilt its own flows' buckets: sum them over the ranks
+            if (c->comm)
+                c->comm->all_reduce(dense, static_cast<size_t>(n_sites) * gnm::kBuckets, gnm::DType::U32,
+                                    gnm::RedOp::Sum, c->stream);
+            if (!c->discard_hist_out)
+                ck(cudaMemcpyAsync(r->histograms, dense, bytes, cudaMemcpyDeviceToHost, c->stream),
+                   "cudaMemcpyAsync(D2H hist)");
             ck(cudaFreeAsync(dense, c->stream), "cudaFreeAsync(hist export)");
         }
         if (c->hosts) {
             // SiteResult::hosts: the per-host post-pass over the same log.
+            if (c->comm && !c->hglobal.prepared) combine_hosts(c, reg);
             if (c->hglobal.prepared) { // rows of the cross-context union
                 ck(gnm::hosts_global_finish(c->device, c->hrows, c->hglobal, c->stream), "per-host rows (union)");
                 c->kernel_launches += 1;
@@ -954,7 +1035,6 @@ int gnm_host_results(gnm_ctx* c, gnm_host_stats* out, uint64_t capacity, uint32_
         if (n) ck(cudaMemcpyAsync(out, c->hrows.rows, n * sizeof(gnm_host_stats), cudaMemcpyDeviceToHost, c->stream),
                   "cudaMemcpyAsync(D2H host rows)");
         if (n && histograms) {
-            if (c->hrows.global) return fail(GNM_ERR_INVALID_ARGUMENT, "no histograms for cross-context rows");
             const size_t bytes = n * gnm::kBuckets * 4;
             uint32_t* dense = nullptr;
             ck(cudaMallocAsync(reinterpret_cast<void**>(&dense), bytes, c->stream), "cudaMallocAsync(host hist)");
@@ -975,7 +1055,6 @@ int gnm_host_histogram_entries(gnm_ctx* c, uint32_t* rows, uint32_t* buckets, ui
     if (!c || !n_entries) return fail(GNM_ERR_INVALID_ARGUMENT, "null argument");
     return guarded([&] {
         ck(cudaSetDevice(c->device), "cudaSetDevice");
-        if (c->hrows.global) return fail(GNM_ERR_INVALID_ARGUMENT, "no histograms for cross-context rows");
         uint64_t n = 0;
         ck(gnm::hosts_sparse(c->device, c->hrows, &n, c->stream), "host histogram entries");
         *n_entries = n;
@@ -1091,6 +1170,7 @@ int gnm_finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* result) {
 
 int gnm_prepare_median(gnm_ctx* c, const gnm_registry* reg) {
     if (!c || !reg) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx/registry");
+    if (c->comm) return fail(GNM_ERR_INVALID_ARGUMENT, "the context's communicator combines inside gnm_finalize");
     return guarded([&] {
         if (int e = begin_accumulate(c, reg)) return e;
         EventPair ev;
@@ -1442,7 +1522,7 @@ int analyze_graphed(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params
 
 bool graph_eligible(const gnm_ctx* c, int mem, uint64_t n, const gnm_result* r) {
     return c->graphs && !c->timing && !c->hosts && mem == GNM_MEM_DEVICE && n > 0 && r && !r->histograms &&
-           c->stream != nullptr;
+           c->stream != nullptr && (!c->comm || c->comm->capturable());
 }
 } // namespace
 
@@ -1596,6 +1676,240 @@ int gnm_evaluate_warnings(const gnm_result* r, gnm_warning_state* st, double thr
         if (n_out) *n_out = n;
         return static_cast<int>(GNM_OK);
     });
+}
+
+// ---- multi-GPU inside the library ---------------------------------------------
+
+int gnm_comm_unique_id(unsigned char out[GNM_COMM_ID_BYTES]) {
+    if (!out) return fail(GNM_ERR_INVALID_ARGUMENT, "null out");
+    return guarded([&] {
+        gnm::nccl_unique_id(out);
+        return static_cast<int>(GNM_OK);
+    });
+}
+
+int gnm_ctx_comm_init(gnm_ctx* c, int nranks, int rank, const unsigned char id[GNM_COMM_ID_BYTES]) {
+    if (!c || !id) return fail(GNM_ERR_INVALID_ARGUMENT, "null argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(GNM_ERR_INVALID_ARGUMENT, "bad rank / nranks");
+    if (c->accumulating) return fail(GNM_ERR_INVALID_ARGUMENT, "attach a communicator between accumulations");
+    return guarded([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        c->comm = gnm::nccl_comm(nranks, rank, id);
+        return static_cast<int>(GNM_OK);
+    });
+}
+
+int gnm_ctx_comm_destroy(gnm_ctx* c) {
+    if (!c) return fail(GNM_ERR_INVALID_ARGUMENT, "null ctx");
+    if (c->accumulating) return fail(GNM_ERR_INVALID_ARGUMENT, "detach a communicator between accumulations");
+    return guarded([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+        c->comm.reset();
+        return static_cast<int>(GNM_OK);
+    });
+}
+
+int gnm_ctx_comm_size(gnm_ctx* c) { return c && c->comm ? c->comm->nranks() : 1; }
+
+} // extern "C"
+
+struct gnm_group {
+    std::vector<gnm_ctx*> ctx;
+    int kind = GNM_GROUP_NCCL;
+};
+
+namespace {
+
+// One host thread per rank (each drives its own device and communicator,
+// as NCCL requires when one process owns several ranks): rank i runs `work`
+// on its context; the first failing rank's status and message are returned.
+template <typename F>
+int on_every_rank(gnm_group* g, F&& work) {
+    const int n = static_cast<int>(g->ctx.size());
+    std::vector<int> st(n, GNM_OK);
+    std::vector<std::string> msg(n);
+    auto body = [&](int i) {
+        st[i] = guarded([&] {
+            ck(cudaSetDevice(g->ctx[i]->device), "cudaSetDevice");
+            return work(i, g->ctx[i]);
+        });
+        if (st[i] != GNM_OK) msg[i] = g_last_error;
+    };
+    if (n == 1) {
+        body(0);
+    } else {
+        std::vector<std::thread> th;
+        for (int i = 0; i < n; ++i) th.emplace_back(body, i);
+        for (auto& t : th) t.join();
+    }
+    for (int i = 0; i < n; ++i)
+        if (st[i] != GNM_OK) return fail(st[i], "rank " + std::to_string(i) + ": " + msg[i]);
+    return GNM_OK;
+}
+
+// Shard i of n records over N ranks: the reference's worker boundaries.
+std::pair<uint64_t, uint64_t> shard(uint64_t n, int i, int N) {
+    const unsigned __int128 a = static_cast<unsigned __int128>(n) * i / N;
+    const unsigned __int128 b = static_cast<unsigned __int128>(n) * (i + 1) / N;
+    return {static_cast<uint64_t>(a), static_cast<uint64_t>(b)};
+}
+
+int group_analyze(gnm_group* g, const gnm_registry* reg, const gnm_filter_params* params, const gnm_batch_soa* b,
+                  const gnm_batch_aos* ba, gnm_result* r) {
+    if (!g || !reg || !r) return fail(GNM_ERR_INVALID_ARGUMENT, "null argument");
+    if (b) {
+        if (int e = check_soa(b)) return e;
+    } else {
+        if (!ba) return fail(GNM_ERR_INVALID_ARGUMENT, "null batch");
+        if (ba->n && !ba->records) return fail(GNM_ERR_INVALID_ARGUMENT, "null records");
+        if (ba->mem == GNM_MEM_DEVICE && reinterpret_cast<uintptr_t>(ba->records) % 8)
+            return fail(GNM_ERR_INVALID_ARGUMENT, "device FlowRecord rows must be 8-byte aligned");
+    }
+    const uint32_t n_sites = static_cast<uint32_t>(reg->r.sites().size());
+    if (r->sites_capacity < n_sites || (n_sites && !r->sites))
+        return fail(GNM_ERR_CAPACITY, "result.sites holds fewer rows than the registry has sites");
+    const int N = static_cast<int>(g->ctx.size());
+    for (gnm_ctx* c : g->ctx)
+        if (c->hosts != g->ctx[0]->hosts)
+            return fail(GNM_ERR_INVALID_ARGUMENT, "per-host mode must be alike on every rank");
+    std::vector<std::vector<gnm_site_stats>> rows(N);
+    std::vector<gnm_result> res(N, *r);
+    return on_every_rank(g, [&](int i, gnm_ctx* c) -> int {
+        const uint64_t n = b ? b->n : ba->n;
+        const auto [lo, hi] = shard(n, i, N);
+        if (i) { // the other ranks' rows stay internal; histograms: all-reduced, not copied out
+            rows[i].resize(n_sites);
+            res[i].sites = rows[i].data();
+        }
+        c->discard_hist_out = i != 0;
+        int e;
+        if (b) {
+            gnm_batch_soa s = *b;
+            s.src_addr += lo;
+            s.dst_addr += lo;
+            s.d_pkts += lo;
+            s.d_octets += lo;
+            s.start_ms += lo;
+            s.end_ms += lo;
+            s.n = hi - lo;
+            e = accumulate_soa(c, reg, params, &s);
+        } else {
+            gnm_batch_aos a = *ba;
+            a.records = static_cast<const unsigned char*>(ba->records) + lo * GNM_FLOW_RECORD_BYTES;
+            a.n = hi - lo;
+            e = accumulate_aos(c, reg, params, &a);
+        }
+        if (e) {
+            gnm_reset(c);
+            return e;
+        }
+        e = finalize(c, reg, &res[i]);
+        c->discard_hist_out = false;
+        if (!e && i == 0) *r = res[0];
+        return e;
+    });
+}
+
+} // namespace
+
+extern "C" {
+
+int gnm_group_create(const int* devices, int n, int kind, gnm_group** out) {
+    if (!devices || n < 1 || !out) return fail(GNM_ERR_INVALID_ARGUMENT, "bad group arguments");
+    if (kind != GNM_GROUP_NCCL && kind != GNM_GROUP_LOOPBACK) return fail(GNM_ERR_INVALID_ARGUMENT, "bad group kind");
+    *out = nullptr;
+    auto* g = new gnm_group();
+    g->kind = kind;
+    for (int i = 0; i < n; ++i) {
+        gnm_ctx* c = nullptr;
+        if (int e = gnm_ctx_create(devices[i], &c)) {
+            gnm_group_destroy(g);
+            return e;
+        }
+        g->ctx.push_back(c);
+    }
+    const int e = guarded([&] {
+        auto comms = kind == GNM_GROUP_NCCL ? gnm::nccl_clique(devices, n) : gnm::loopback_clique(n);
+        for (int i = 0; i < n; ++i) g->ctx[i]->comm = std::move(comms[i]);
+        return static_cast<int>(GNM_OK);
+    });
+    if (e) {
+        gnm_group_destroy(g);
+        return e;
+    }
+    *out = g;
+    return GNM_OK;
+}
+
+void gnm_group_destroy(gnm_group* g) {
+    if (!g) return;
+    for (gnm_ctx* c : g->ctx) gnm_ctx_destroy(c);
+    delete g;
+}
+
+int gnm_group_size(const gnm_group* g) { return g ? static_cast<int>(g->ctx.size()) : 0; }
+
+gnm_ctx* gnm_group_ctx(gnm_group* g, int rank) {
+    return g && rank >= 0 && rank < static_cast<int>(g->ctx.size()) ? g->ctx[rank] : nullptr;
+}
+
+int gnm_group_analyze(gnm_group* g, const gnm_registry* reg, const gnm_filter_params* params,
+                      const gnm_batch_soa* batch, gnm_result* result) {
+    if (!batch) return fail(GNM_ERR_INVALID_ARGUMENT, "null batch");
+    return group_analyze(g, reg, params, batch, nullptr, result);
+}
+
+int gnm_group_analyze_aos(gnm_group* g, const gnm_registry* reg, const gnm_filter_params* params,
+                          const gnm_batch_aos* batch, gnm_result* result) {
+    if (!batch) return fail(GNM_ERR_INVALID_ARGUMENT, "null batch");
+    return group_analyze(g, reg, params, nullptr, batch, result);
+}
+
+uint64_t gnm_group_host_count(gnm_group* g) { return g && !g->ctx.empty() ? gnm_host_count(g->ctx[0]) : 0; }
+
+int gnm_group_host_results(gnm_group* g, gnm_host_stats* out, uint64_t capacity) {
+    if (!g || g->ctx.empty()) return fail(GNM_ERR_INVALID_ARGUMENT, "null group");
+    return gnm_host_results(g->ctx[0], out, capacity, nullptr); // every rank holds the same global rows
+}
+
+int gnm_group_host_histogram_entries(gnm_group* g, uint32_t* rows, uint32_t* buckets, uint32_t* counts,
+                                     uint64_t capacity, uint64_t* n_entries) {
+    if (!g || g->ctx.empty() || !n_entries) return fail(GNM_ERR_INVALID_ARGUMENT, "null argument");
+    // Each rank's entries count its own flows over the global rows; the
+    // group's histograms are their sum, merged here in (row, bucket) order.
+    std::vector<uint64_t> keys;
+    std::vector<uint32_t> cnts;
+    for (gnm_ctx* c : g->ctx) {
+        uint64_t n = 0;
+        if (int e = gnm_host_histogram_entries(c, nullptr, nullptr, nullptr, 0, &n)) return e;
+        std::vector<uint32_t> r(n), b(n), k(n);
+        if (n)
+            if (int e = gnm_host_histogram_entries(c, r.data(), b.data(), k.data(), n, &n)) return e;
+        for (uint64_t i = 0; i < n; ++i) {
+            keys.push_back(static_cast<uint64_t>(r[i]) << 32 | b[i]);
+            cnts.push_back(k[i]);
+        }
+    }
+    std::vector<uint64_t> order(keys.size());
+    for (uint64_t i = 0; i < order.size(); ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](uint64_t x, uint64_t y) { return keys[x] < keys[y]; });
+    uint64_t m = 0;
+    for (uint64_t i = 0; i < order.size(); ++i) {
+        const uint64_t k = keys[order[i]];
+        const bool fresh = i == 0 || k != keys[order[i - 1]];
+        if (fresh) ++m;
+        if (!rows) continue;
+        if (m > capacity || !buckets || !counts) return fail(GNM_ERR_CAPACITY, "host histogram entries: capacity");
+        if (fresh) {
+            rows[m - 1] = static_cast<uint32_t>(k >> 32);
+            buckets[m - 1] = static_cast<uint32_t>(k);
+            counts[m - 1] = 0;
+        }
+        counts[m - 1] += cnts[order[i]];
+    }
+    *n_entries = m;
+    return GNM_OK;
 }
 
 } // extern "C"

@@ -37,6 +37,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_run_length_encode.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
 
 #include <algorithm>
 #include <cstdint>
@@ -793,9 +794,46 @@ cudaError_t hosts_global_prepare(int device, const HostRows& out, HostGlobal& g,
     return cudaGetLastError();
 }
 
+cudaError_t hosts_key_union(int device, const unsigned long long* all, uint64_t n, unsigned long long* out,
+                            uint64_t* n_out, cudaStream_t s) {
+    (void)device;
+    *n_out = 0;
+    if (n == 0) return cudaSuccess;
+    Scratch tmp_(s);
+    unsigned long long* sorted = nullptr;
+    uint64_t* d_n = nullptr;
+    HCK(tmp_.get(&sorted, n));
+    HCK(tmp_.get(&d_n, 1));
+    size_t tb = 0, tb2 = 0;
+    HCK(cub::DeviceRadixSort::SortKeys(nullptr, tb, all, sorted, n, 0, 64, s));
+    HCK(cub::DeviceSelect::Unique(nullptr, tb2, sorted, out, d_n, n, s));
+    unsigned char* tmp = nullptr;
+    HCK(tmp_.get(&tmp, std::max(tb, tb2)));
+    HCK(cub::DeviceRadixSort::SortKeys(tmp, tb, all, sorted, n, 0, 64, s));
+    HCK(cub::DeviceSelect::Unique(tmp, tb2, sorted, out, d_n, n, s));
+    uint64_t m = 0;
+    HCK(cudaMemcpyAsync(&m, d_n, 8, cudaMemcpyDeviceToHost, s));
+    HCK(cudaStreamSynchronize(s));
+    unsigned long long last = 0;
+    if (m) {
+        HCK(cudaMemcpyAsync(&last, out + m - 1, 8, cudaMemcpyDeviceToHost, s));
+        HCK(cudaStreamSynchronize(s));
+    }
+    *n_out = m - (m && last == kEmpty ? 1 : 0); // the all-gather's padding sorts last
+    return cudaSuccess;
+}
+
 cudaError_t hosts_global_finish(int device, HostRows& out, HostGlobal& g, cudaStream_t s) {
     if (out.rows) cudaFreeAsync(out.rows, s);
     out.rows = nullptr;
+    // row_of now holds global rows: any sorted / sparse form of the local
+    // rows is stale, and the (row, bucket) key width follows the union
+    for (void* p : {out.sorted, out.sp_keys, static_cast<void*>(out.sp_counts)})
+        if (p) cudaFreeAsync(p, s);
+    out.sorted = out.sp_keys = nullptr;
+    out.sp_counts = nullptr;
+    out.n_sparse = ~0ull;
+    out.key64 = kBucketBits + bits_for(std::max<uint64_t>(g.n, 1)) > 32;
     const uint32_t n = static_cast<uint32_t>(g.n);
     HCK(dalloc(&out.rows, std::max<uint32_t>(n, 1), s));
     if (n)

@@ -78,6 +78,10 @@ cudaError_t finish_hosts(int device, HostRows& out, HostLocal& loc, cudaStream_t
 // finish (rows of the union in out.rows).
 cudaError_t hosts_global_begin(int device, HostRows& out, const HostLocal& loc, const unsigned long long* keys,
                                uint64_t n, HostGlobal& g, cudaStream_t s);
+// Sorted union (duplicates and the kEmpty padding dropped) of n keys
+// all-gathered from every rank; out holds up to n keys. Synchronises s.
+cudaError_t hosts_key_union(int device, const unsigned long long* all, uint64_t n, unsigned long long* out,
+                            uint64_t* n_out, cudaStream_t s);
 cudaError_t hosts_global_prepare(int device, const HostRows& out, HostGlobal& g, cudaStream_t s);
 cudaError_t hosts_global_finish(int device, HostRows& out, HostGlobal& g, cudaStream_t s);
 void free_local(HostLocal& loc, cudaStream_t s);

@@ -481,10 +481,42 @@ class Engine:
         self.device = device
         self._hosts = False
 
+    @classmethod
+    def _borrow(cls, handle, device: int) -> "Engine":
+        """A non-owning Engine over a context owned elsewhere (a Group's rank)."""
+        e = cls.__new__(cls)
+        e._h = C.c_void_p(handle)
+        e.device = device
+        e._hosts = False
+        e._owned = False
+        return e
+
     def close(self):
         if getattr(self, "_h", None):
-            lib.gnm_ctx_destroy(self._h)
+            if getattr(self, "_owned", True):
+                lib.gnm_ctx_destroy(self._h)
             self._h = None
+
+    # ---- multi-GPU inside the library (gnetmon.h gnm_ctx_comm_*) -------------
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        """ncclGetUniqueId, for rank 0 to distribute (gnm_comm_unique_id)."""
+        buf = (C.c_ubyte * _lib.COMM_ID_BYTES)()
+        _check(lib.gnm_comm_unique_id(buf))
+        return bytes(buf)
+
+    def comm_init(self, nranks: int, rank: int, unique_id: bytes) -> None:
+        """Attach an NCCL communicator: from now on every finalize / aggregate
+        combines the ranks' partials itself (two rounds, on this context's
+        stream) and returns the global result. Blocks until all ranks join."""
+        buf = (C.c_ubyte * _lib.COMM_ID_BYTES).from_buffer_copy(unique_id)
+        _check(lib.gnm_ctx_comm_init(self._h, nranks, rank, buf))
+
+    def comm_destroy(self) -> None:
+        _check(lib.gnm_ctx_comm_destroy(self._h))
+
+    def comm_size(self) -> int:
+        return lib.gnm_ctx_comm_size(self._h)
 
     def __del__(self):
         self.close()
@@ -875,3 +907,73 @@ def evaluate_warnings(result: AnalysisResult, catalog: SiteCatalog, state: Warni
     _check(lib.gnm_evaluate_warnings(C.byref(r), state._h, threshold_bps, out, cap, C.byref(n)))
     return [SiteWarning(out[i].site, catalog.site(out[i].site), out[i].median_bps,
                         out[i].consecutive_bad_hours) for i in range(n.value)]
+
+
+class Group:
+    """One process driving several GPUs (gnetmon.h gnm_group_*): a context per
+    device and an NCCL clique; ``aggregate`` shards the batch by the
+    reference's worker boundaries n*i/N (rate_engine.cpp:341-344), every rank
+    accumulates its shard on its own host thread and the partials combine in
+    two rounds inside the library. ``kind="loopback"`` exchanges through host
+    memory instead (a test hook: several ranks on one GPU)."""
+
+    def __init__(self, devices, kind: str = "nccl"):
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        k = {"nccl": _lib.GROUP_NCCL, "loopback": _lib.GROUP_LOOPBACK}[kind]
+        _check(lib.gnm_group_create(devs, len(devices), k, C.byref(h)))
+        self._h = h
+        self.devices = list(devices)
+        self.engines = [Engine._borrow(lib.gnm_group_ctx(h, i), d) for i, d in enumerate(devices)]
+        self._hosts = False
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.gnm_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __len__(self):
+        return lib.gnm_group_size(self._h)
+
+    def set_hosts(self, on: bool = True) -> None:
+        for e in self.engines:
+            e.set_hosts(on)
+        self._hosts = bool(on)
+
+    def aggregate(self, view, catalog: SiteCatalog, params: Optional[FilterParams] = None,
+                  window_start_ms: int = 0, window_end_ms: int = 0,
+                  threshold_bps: float = kDefaultWarnThresholdBps, histograms: bool = False) -> AnalysisResult:
+        p = Engine._params(params)
+        b = view._c()
+        r, table, hist, n = self.engines[0]._result(catalog, window_start_ms, window_end_ms, threshold_bps,
+                                                    histograms)
+        fn = lib.gnm_group_analyze_aos if isinstance(view, FlowRecords) else lib.gnm_group_analyze
+        _check(fn(self._h, catalog.handle, C.byref(p), C.byref(b), C.byref(r)))
+        res = _build_result(r, table[:n], None if hist is None else hist[:n])
+        if self._hosts:
+            k = lib.gnm_group_host_count(self._h)
+            rows = np.empty(max(k, 1), _lib.HOST_STATS_DTYPE)
+            _check(lib.gnm_group_host_results(self._h, rows.ctypes.data, len(rows)))
+            res.host_table = rows[:k]
+            res.host_histograms = None
+        return res
+
+    def host_histogram_entries(self):
+        """The group's per-host histograms (summed over the ranks), sparse:
+        (row, bucket, count) in (row, bucket) order."""
+        n = C.c_uint64()
+        _check(lib.gnm_group_host_histogram_entries(self._h, None, None, None, 0, C.byref(n)))
+        rows, bks, cnt = (np.empty(max(n.value, 1), np.uint32) for _ in range(3))
+        _check(lib.gnm_group_host_histogram_entries(self._h, rows.ctypes.data, bks.ctypes.data, cnt.ctypes.data,
+                                                    len(rows), C.byref(n)))
+        k = n.value
+        return rows[:k], bks[:k], cnt[:k]

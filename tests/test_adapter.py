@@ -160,3 +160,22 @@ def test_adapter_equals_reference_d3_slice(tmp_path):
     d = _parity(tmp_path, [[c] for c in w.sites.cidrs], synth.generate(w, 10_000_000), "--repeat", 3,
                 "--cpu-workers", 1, timeout=1800)
     assert d["records"] == 10_000_000 and d["sites"] == 10_000 and d["host_rows"] > 70_000
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("devices", ["loopback:0,0", "loopback:0,0,0", "0"])
+def test_adapter_multi_gpu_group_equals_reference(tmp_path, devices):
+    """GNM_ADAPTER_DEVICES: the adapter shards every call across a gnm_group
+    (the reference's worker boundaries) and the combine -- sites, the host
+    key union and the ranks' summed host histograms -- runs in the library.
+    Loopback runs 2-3 ranks on the one test GPU; "0" is a one-device NCCL
+    clique. The reference's own suites and AnalysisResult::operator== judge it."""
+    env = {"GNM_ADAPTER_DEVICES": devices}
+    out = _run([_bin("engine_tests_gpu")], env=env)
+    assert out.returncode == 0, out.stdout[-4000:] + out.stderr[-2000:]
+    from paper_1108_1785_b200 import synth
+    w = synth.workload("D2")
+    rec, cat = _write_inputs(tmp_path, [[c] for c in w.sites.cidrs], synth.generate(w, 500_000))
+    out = _run([_bin("adapter_parity"), rec, cat, "--partitions", "2"], env=env)
+    d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert out.returncode == 0 and d["equal"], d
