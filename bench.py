@@ -221,7 +221,8 @@ def workload_config(w, n: int, n_sites: int, world: int, args) -> dict:
             "records_per_gpu": n, "sites": n_sites, "input": args.input,
             "hosts": ("per-host rows built every step" if args.hosts
                       else "site level only (gnm_ctx_set_hosts off)"),
-            "parallelism": f"index shards x{world}",
+            "parallelism": (f"index shards x{world}, in-library NCCL two-round combine" if world > 1
+                            else "1 GPU"),
             "l2": "inputs 3.2 GB/GPU > 126 MB L2; no flush needed" if n >= 10_000_000
                   else "inputs may fit L2"}
 
@@ -451,14 +452,22 @@ def main():
     if args.hosts:
         eng.set_hosts(True)  # N > 1: distributed.combine also merges the host rows
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=f"cuda:{local}")
+    # N > 1 over NCCL: the library's own communicator (gnm_ctx_comm_init; the
+    # unique id travels over the torch process group), so every step is one
+    # gnm_analyze call -- K2 on this rank's shard, round 1 (one grouped NCCL
+    # call: sums / coarse SUM, min MIN, max MAX), K3a+K2b, round 2 (fine SUM),
+    # K3b -- all on the engine stream and replayed as one CUDA graph. The
+    # gloo test hook (several ranks on one GPU) combines through
+    # torch.distributed instead (paper_1108_1785_b200.distributed).
+    in_library = distributed and os.environ.get("GNM_BENCH_BACKEND", "nccl") == "nccl"
+    if in_library:
+        uid = [Engine.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        eng.comm_init(world, rank, uid[0])
 
     def step(batch):
-        if not distributed:
+        if not distributed or in_library:
             return eng.aggregate(batch, cat)
-        # K2 on this rank's shard, then the two-round exact-median combine
-        # over NCCL (paper_1108_1785_b200.distributed): all-reduce of sums /
-        # min / max / coarse counts, K3a+K2b on this rank's log, all-reduce
-        # of the median super-buckets' fine counts, K3b.
         eng.accumulate(batch, cat)
         D.combine(eng, cat, stream=stream)
         return eng.finalize(cat)

@@ -455,12 +455,14 @@ void launch_k2_timed(gnm_ctx* c, const gnm::DevBatch& b, const gnm::DevParams& p
     if (c->hot_mode != GNM_HOT_OFF) {
         cudaError_t e;
         hot = gnm::plan_hot(c->device, b, c->table, p, c->P.n_sites, c->d_scratch, c->P.mn, c->P.mx, cold.grid,
-                            c->hot_mode == GNM_HOT_FORCE, c->stream, &c->kernel_launches, &e);
+                            c->hot_mode == GNM_HOT_FORCE, cold.table_in_smem, c->stream, &c->kernel_launches, &e);
         ck(e, "hot-site plan");
     }
     const gnm::LaunchCfg cfg =
         hot ? gnm::k2_config(c->device, b, c->table.n_words, true, c->occ, c->hosts) : cold;
-    gnm::DevHot h{c->d_scratch + gnm::plan_hot_site_offset(c->P.n_sites), hot ? gnm::kHotSlots : 0u};
+    gnm::DevHot h{c->d_scratch + gnm::plan_hot_site_offset(c->P.n_sites), hot ? gnm::kHotSlots : 0u,
+                  cold.table_in_smem ? c->d_scratch + gnm::plan_slot_offset(c->P.n_sites) : nullptr,
+                  c->table.node_begin, c->table.leaf_begin};
     if (c->timing) {
         ck(cudaEventRecord(pe.b, c->stream), "cudaEventRecord");
         c->plan_pairs.push_back(pe);

@@ -168,6 +168,41 @@ __device__ __forceinline__ void load_table(const uint32_t* __restrict__ gt, uint
     }
 }
 
+// A table word with this call's hot slot (k_table_slots' rewrite, done here
+// on the shared-memory copy): uniform nodes and leaf entries carry
+// slot << 20 | site.
+__device__ __forceinline__ uint32_t with_slot(uint32_t w, uint32_t j, const DevHot& hot) {
+    if (j < hot.node_begin) return w;
+    if (j < hot.leaf_begin) {
+        if (!(w & 0x80000000u)) return w;
+        const uint32_t site = w & 0xFFFFFu;
+        return 0x80000000u | __ldg(hot.site_slot + site) << 20 | site;
+    }
+    if (w == 0xFFFFFFFFu) return w;
+    const uint32_t site = w & 0xFFFFFu;
+    return __ldg(hot.site_slot + site) << 20 | site;
+}
+
+template <bool kSmem, bool kHot>
+__device__ __forceinline__ void load_table_slots(const uint32_t* __restrict__ gt, uint32_t words, const DevHot& hot) {
+    if constexpr (kSmem && kHot) {
+        if (hot.site_slot) {
+            const uint4* g4 = reinterpret_cast<const uint4*>(gt);
+            uint4* s4 = reinterpret_cast<uint4*>(g_smem);
+            for (uint32_t i = threadIdx.x; i < words / 4; i += blockDim.x) {
+                uint4 v = __ldg(g4 + i);
+                v.x = with_slot(v.x, 4 * i, hot);
+                v.y = with_slot(v.y, 4 * i + 1, hot);
+                v.z = with_slot(v.z, 4 * i + 2, hot);
+                v.w = with_slot(v.w, 4 * i + 3, hot);
+                s4[i] = v;
+            }
+            return;
+        }
+    }
+    load_table<kSmem>(gt, words);
+}
+
 // ---- block-private hot-site accumulators ---------------------------------
 // Per slot: octets as two 16-bit limbs, micro-bps (< 2^48) as three 16-bit
 // limbs, each summed into its own u32 by non-returning shared adds; min/max
@@ -692,7 +727,7 @@ template <bool kSmem, bool kHot, bool kHosts>
 __device__ __forceinline__ void k2_prologue(const uint32_t* __restrict__ gt, uint32_t table_words,
                                             const DevLog& L, const DevHot& hot, const DevPartials& P,
                                             HotSmem& h, WarpQueue& wq) {
-    load_table<kSmem>(gt, table_words);
+    load_table_slots<kSmem, kHot>(gt, table_words, hot);
     const uint32_t smem_words = kSmem ? table_words : 0u;
     if constexpr (kHot) {
         h = hot_smem(smem_words);
@@ -940,11 +975,19 @@ __global__ void __launch_bounds__(kSelectBlock) k_hot_select(uint32_t* __restric
     {
         // cut: the lowest bin b with suffix(b) <= kHotSlots; cut_a the same
         // for the kCoarseSlots slots that also keep coarse counts in smem.
+        // Warp-reduced first: one shared atomic per warp, not per bin.
         uint32_t suffix = threadIdx.x + 1 < kSelectBlock ? part[threadIdx.x + 1] : 0u;
+        uint32_t lc = 0xFFFFFFFFu, lca = 0xFFFFFFFFu;
         for (int k = kCountBins / kSelectBlock - 1; k >= 0; --k) {
             suffix += bins[i0 + k];
-            if (suffix <= kHotSlots) atomicMin(&cut, i0 + k);
-            if (suffix <= kCoarseSlots) atomicMin(&cut_a, i0 + k);
+            if (suffix <= kHotSlots) lc = i0 + k;
+            if (suffix <= kCoarseSlots) lca = i0 + k;
+        }
+        lc = __reduce_min_sync(0xFFFFFFFFu, lc);
+        lca = __reduce_min_sync(0xFFFFFFFFu, lca);
+        if (lane == 0) {
+            if (lc != 0xFFFFFFFFu) atomicMin(&cut, lc);
+            if (lca != 0xFFFFFFFFu) atomicMin(&cut_a, lca);
         }
     }
     __syncthreads();
@@ -961,17 +1004,33 @@ __global__ void __launch_bounds__(kSelectBlock) k_hot_select(uint32_t* __restric
     __syncthreads();
     if (threadIdx.x == 0) next_a = 0;
     __syncthreads();
-    for (uint32_t s4 = threadIdx.x * 4; s4 < n_sites; s4 += blockDim.x * 4) {
-        const uint4 c4 = *reinterpret_cast<const uint4*>(cnt + s4);
+    // Slot numbers by warp-aggregated allocation (ballot + one shared
+    // atomic per warp and class), so the hot sites never serialise on the
+    // two counters.
+    const uint32_t lt = (1u << lane) - 1u;
+    for (uint32_t s0 = warp * 128; s0 < n_sites; s0 += blockDim.x * 4) { // warp-uniform trip count
+        const uint32_t s4 = s0 + lane * 4;
+        uint4 c4 = make_uint4(0, 0, 0, 0);
+        if (s4 < n_sites) c4 = *reinterpret_cast<const uint4*>(cnt + s4);
         const uint32_t cs[4] = {c4.x, c4.y, c4.z, c4.w};
 #pragma unroll
         for (uint32_t q = 0; q < 4; ++q) {
             const uint32_t s = s4 + q;
-            if (s >= n_sites) break;
+            const bool in = s < n_sites;
+            const bool a = in && cs[q] >= ta, bclass = in && !a && cs[q] >= t;
+            const unsigned ma = __ballot_sync(0xFFFFFFFFu, a), mb = __ballot_sync(0xFFFFFFFFu, bclass);
+            uint32_t fa = 0, fb = 0;
+            if (lane == 0) {
+                if (ma) fa = atomicAdd(&next_a, __popc(ma));
+                if (mb) fb = atomicAdd(&next, __popc(mb));
+            }
+            fa = __shfl_sync(0xFFFFFFFFu, fa, 0);
+            fb = __shfl_sync(0xFFFFFFFFu, fb, 0);
+            if (!in) continue;
             cnt[s] = 0;
             uint32_t slot = 0;
-            if (cs[q] >= ta) slot = atomicAdd(&next_a, 1u) + 1;
-            else if (cs[q] >= t) slot = base_b + atomicAdd(&next, 1u) + 1;
+            if (a) slot = fa + __popc(ma & lt) + 1;
+            else if (bclass) slot = base_b + fb + __popc(mb & lt) + 1;
             if (slot) hot_site[slot] = s;
             site_slot[s] = slot;
         }
@@ -1406,7 +1465,8 @@ LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool ho
 
 bool plan_hot(int device, const DevBatch& b, const DevTable& t, const DevParams& p,
               uint32_t n_sites, uint32_t* scratch, unsigned long long* mn, unsigned long long* mx,
-              int k2_grid, bool force, cudaStream_t s, uint64_t* launches, cudaError_t* err) {
+              int k2_grid, bool force, bool table_in_smem, cudaStream_t s, uint64_t* launches,
+              cudaError_t* err) {
     (void)device;
     *err = cudaSuccess;
     if (!t.packed || n_sites == 0 || b.n == 0) return false;
@@ -1438,10 +1498,13 @@ bool plan_hot(int device, const DevBatch& b, const DevTable& t, const DevParams&
     const dim3 sg((chunk_len + 255) / 256, nchunks);
     k_sample<false><<<sg, 256, 0, s>>>(b, t.words, t.n_words, p, stride, chunk_len, cnt, mn, mx);
     k_hot_select<<<1, kSelectBlock, 0, s>>>(cnt, n_sites, thr, site_slot, hot_site);
-    const uint32_t span = t.n_words - t.node_begin;
-    const uint32_t rg = std::max<uint32_t>(1, std::min<uint32_t>((span + 255) / 256, 1024));
-    k_table_slots<<<rg, 256, 0, s>>>(t.words, t.node_begin, t.leaf_begin, t.n_words, site_slot);
-    *launches += 3;
+    *launches += 2;
+    if (!table_in_smem) { // K2 probes the global table: write the slots into it
+        const uint32_t span = t.n_words - t.node_begin;
+        const uint32_t rg = std::max<uint32_t>(1, std::min<uint32_t>((span + 255) / 256, 1024));
+        k_table_slots<<<rg, 256, 0, s>>>(t.words, t.node_begin, t.leaf_begin, t.n_words, site_slot);
+        *launches += 1;
+    }
     *err = cudaGetLastError();
     return *err == cudaSuccess;
 }

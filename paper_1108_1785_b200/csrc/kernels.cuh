@@ -115,6 +115,10 @@ struct DevLog {
 struct DevHot {
     const uint32_t* hot_site;
     uint32_t n_slots;
+    // With the table in shared memory, K2 applies the plan's slot numbers
+    // (site -> slot) while loading it (no k_table_slots pass); null otherwise.
+    const uint32_t* site_slot;
+    uint32_t node_begin, leaf_begin;
 };
 
 struct DevSoA {
@@ -168,7 +172,8 @@ LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool ho
 // u32 slot->site.
 bool plan_hot(int device, const DevBatch& b, const DevTable& t, const DevParams& p,
               uint32_t n_sites, uint32_t* scratch, unsigned long long* mn, unsigned long long* mx,
-              int k2_grid, bool force, cudaStream_t s, uint64_t* launches, cudaError_t* err);
+              int k2_grid, bool force, bool table_in_smem, cudaStream_t s, uint64_t* launches,
+              cudaError_t* err);
 
 // Entries one warp region must hold for a launch of `cfg` over b (>= the
 // warp's records, rounded up to the 32-entry drain granularity).

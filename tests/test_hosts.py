@@ -284,13 +284,15 @@ def test_gpu_host_results_c_abi_errors(hosts_engine):
 def test_gpu_hosts_union_path_single_context(hosts_engine):
     """The cross-context path with one context (union = its own keys, no
     collective): gnm_hosts_local_keys -> set_keys -> prepare_median ->
-    finalize gives the same rows as the local path; histograms are refused
-    for union rows."""
+    finalize gives the same rows as the local path; the histograms of union
+    rows count this context's own flows (here: all of them) over the union
+    rows, so they equal the local path's."""
     w = synth.workload("D2")
     cols = synth.generate(w, 300_000)
     cat = SiteCatalog()
     w.sites.register(cat)
     want = hosts_engine.aggregate(FlowBatch(*cols).to_device(), cat).host_table
+    want_e = hosts_engine.host_histogram_entries()
     hosts_engine.accumulate(FlowBatch(*cols).to_device(), cat)
     keys = hosts_engine.hosts_local_keys(cat)
     t = hosts_engine.hosts_set_keys(keys.clone())
@@ -298,8 +300,8 @@ def test_gpu_hosts_union_path_single_context(hosts_engine):
     hosts_engine.hosts_prepare_median()
     res = hosts_engine.finalize(cat)
     np.testing.assert_array_equal(res.host_table, want)
-    with pytest.raises(Exception):
-        hosts_engine.host_histogram_entries()
+    for x, y in zip(hosts_engine.host_histogram_entries(), want_e):
+        np.testing.assert_array_equal(x, y)
 
 
 @pytest.mark.gpu
