@@ -480,6 +480,8 @@ void launch_k2_timed(gnm_ctx* c, const gnm::DevBatch& b, const gnm::DevParams& p
     c->records += b.n;
 }
 
+constexpr uint64_t kMaxLaunchRecords = 1ull << 31;
+
 gnm::DevBatch soa_batch(const void* const* cols, uint64_t n) {
     gnm::DevBatch b{};
     b.aos = false;
@@ -593,8 +595,12 @@ int accumulate_soa(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params*
     apply_window(p, win);
     if (b->n == 0) return GNM_OK;
     if (b->mem == GNM_MEM_DEVICE) {
-        const void* cols[6] = {b->src_addr, b->dst_addr, b->d_pkts, b->d_octets, b->start_ms, b->end_ms};
-        launch_k2_timed(c, soa_batch(cols, b->n), p);
+        // K2 indexes 64-record tiles in 32 bits: launches of < 2^31 records
+        for (uint64_t o = 0; o < b->n; o += kMaxLaunchRecords) {
+            const void* cols[6] = {b->src_addr + o, b->dst_addr + o, b->d_pkts + o, b->d_octets + o,
+                                   b->start_ms + o, b->end_ms + o};
+            launch_k2_timed(c, soa_batch(cols, std::min<uint64_t>(kMaxLaunchRecords, b->n - o)), p);
+        }
     } else {
         const void* cols[6] = {b->src_addr, b->dst_addr, b->d_pkts, b->d_octets, b->start_ms, b->end_ms};
         const size_t widths[6] = {4, 4, 4, 4, 8, 8};
@@ -616,7 +622,10 @@ int accumulate_aos(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params*
     apply_window(p, win);
     if (b->n == 0) return GNM_OK;
     if (b->mem == GNM_MEM_DEVICE) {
-        launch_k2_timed(c, aos_batch(b->records, b->n), p);
+        for (uint64_t o = 0; o < b->n; o += kMaxLaunchRecords)
+            launch_k2_timed(c, aos_batch(static_cast<const unsigned char*>(b->records) + o * GNM_FLOW_RECORD_BYTES,
+                                         std::min<uint64_t>(kMaxLaunchRecords, b->n - o)),
+                            p);
     } else {
         const void* cols[1] = {b->records};
         const size_t widths[1] = {GNM_FLOW_RECORD_BYTES};

@@ -775,73 +775,102 @@ __device__ __forceinline__ void k2_epilogue(Ctr& t, WarpQueue& wq, uint32_t lane
     }
 }
 
-// Main variant: SoA columns, 16-byte aligned, n < 2^32. Persistent: one
-// 768-thread CTA per SM owns the contiguous 64-record tiles
-// [b*T/G, (b+1)*T/G) and walks them in rounds of kWarps tiles (warp w takes
-// tile t0 + r*kWarps + w), two records per lane per tile (one LDG.64 per u32
-// column, one LDG.128 per u64 column, non-allocating, evict-first),
-// software-pipelined: the next round's six loads are in flight while this
-// one is classified. Every kEpochRounds rounds the CTA meets at a barrier
-// and normalizes the hot limbs (hot_normalize). The last CTA also takes the
-// < 64-record remainder through the scalar path.
-template <bool kSmem, bool kHot, int kMode>
-__global__ void __launch_bounds__(kK2Block, 1) k2_soa(DevBatch b, const uint32_t* __restrict__ gt,
-                                                    uint32_t table_words, DevParams p,
-                                                    DevPartials P, DevHot hot, DevLog L) {
+// One 64-record tile in registers: two records per lane (x and y).
+struct TileRegs {
+    uint2 s, d, k, o;     // src, dst, d_pkts, d_octets of (x, y)
+    ulonglong2 ts, te;    // start_ms, end_ms of (x, y)
+};
+
+// Streaming loads that may allocate in L1: the 64-byte FlowRecord rows are
+// read with two loads into their first 32-byte sector (src/dst at 0,
+// pkts/octets at 16) and one into the second (start/end at 48), so the
+// second load of a sector must hit L1 rather than go back to L2.
+__device__ __forceinline__ uint2 ld_rec_u2(const void* p, uint64_t pol) {
+    uint2 r;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ ulonglong2 ld_rec_u64x2(const void* p, uint64_t pol) {
+    ulonglong2 r;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.u64 {%0,%1}, [%2], %3;" : "=l"(r.x), "=l"(r.y) : "l"(p), "l"(pol));
+    return r;
+}
+
+// Tile loads. kLayout 0 (aligned SoA): lane takes records 2*lane, 2*lane+1
+// of the tile (one LDG.64 per u32 column, one LDG.128 per u64 column,
+// non-allocating). kLayout 2 (16-byte aligned AoS, the reference's 64-byte
+// FlowRecord rows): lane takes records lane and 32+lane, three vector loads
+// each (src/dst, pkts/octets, start/end).
+template <int kLayout>
+__device__ __forceinline__ void load_tile(const DevBatch& b, uint32_t tile, uint32_t lane, uint64_t pol,
+                                          TileRegs& t) {
+    if constexpr (kLayout == 0) {
+        const DevSoA& c = b.soa;
+        const uint32_t g = tile * 32u + lane;
+        t.s = ld_stream_u2(reinterpret_cast<const uint2*>(c.src) + g, pol);
+        t.d = ld_stream_u2(reinterpret_cast<const uint2*>(c.dst) + g, pol);
+        t.k = ld_stream_u2(reinterpret_cast<const uint2*>(c.pkts) + g, pol);
+        t.o = ld_stream_u2(reinterpret_cast<const uint2*>(c.octets) + g, pol);
+        t.ts = ld_stream_u64x2(reinterpret_cast<const ulonglong2*>(c.start) + g, pol);
+        t.te = ld_stream_u64x2(reinterpret_cast<const ulonglong2*>(c.end) + g, pol);
+    } else {
+        const unsigned char* rx = static_cast<const unsigned char*>(b.rec) + (static_cast<size_t>(tile) * 64u + lane) * 64u;
+        const unsigned char* ry = rx + 32u * 64u;
+        const uint2 ax = ld_rec_u2(rx, pol), ay = ld_rec_u2(ry, pol);
+        const uint2 cx = ld_rec_u2(rx + 16, pol), cy = ld_rec_u2(ry + 16, pol);
+        const ulonglong2 ex = ld_rec_u64x2(rx + 48, pol), ey = ld_rec_u64x2(ry + 48, pol);
+        t.s = make_uint2(ax.x, ay.x);
+        t.d = make_uint2(ax.y, ay.y);
+        t.k = make_uint2(cx.x, cy.x);
+        t.o = make_uint2(cx.y, cy.y);
+        t.ts = make_ulonglong2(ex.x, ey.x);
+        t.te = make_ulonglong2(ex.y, ey.y);
+    }
+}
+
+// Main variants: aligned SoA columns (k2_soa) or aligned AoS rows (k2_aos),
+// n < 2^32. Persistent: one 768-thread CTA per SM owns the contiguous
+// 64-record tiles [b*T/G, (b+1)*T/G) and walks them in rounds of kWarps
+// tiles (warp w takes tile t0 + r*kWarps + w), two records per lane per tile
+// (load_tile), software-pipelined: the next round's loads are in flight
+// while this one is classified. Every kEpochRounds rounds the CTA meets at a
+// barrier and normalizes the hot limbs (hot_normalize). The last CTA also
+// takes the < 64-record remainder through the scalar path.
+template <int kLayout, bool kSmem, bool kHot, int kMode>
+__device__ __forceinline__ void k2_tiles(const DevBatch& b, const uint32_t* __restrict__ gt, uint32_t table_words,
+                                         const DevParams& p, const DevPartials& P, const DevHot& hot,
+                                         const DevLog& L) {
     constexpr bool kWin = kMode & kModeWindow, kHosts = kMode & kModeHosts;
     HotSmem h{};
     WarpQueue wq;
     k2_prologue<kSmem, kHot, kHosts>(gt, table_words, L, hot, P, h, wq);
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warp = threadIdx.x >> 5;
-    const DevSoA& c = b.soa;
-    const uint64_t tiles = c.n >> 6;
+    const uint64_t tiles = b.n >> 6;
     const uint32_t t0 = static_cast<uint32_t>(tiles * blockIdx.x / gridDim.x);
     const uint32_t t_end = static_cast<uint32_t>(tiles * (blockIdx.x + 1) / gridDim.x);
     const uint32_t rounds = (t_end - t0 + kWarps - 1) / kWarps; // CTA-uniform
-    const uint2* src2 = reinterpret_cast<const uint2*>(c.src) + lane;
-    const uint2* dst2 = reinterpret_cast<const uint2*>(c.dst) + lane;
-    const uint2* pkt2 = reinterpret_cast<const uint2*>(c.pkts) + lane;
-    const uint2* oct2 = reinterpret_cast<const uint2*>(c.octets) + lane;
-    const ulonglong2* st2 = reinterpret_cast<const ulonglong2*>(c.start) + lane;
-    const ulonglong2* en2 = reinterpret_cast<const ulonglong2*>(c.end) + lane;
     Ctr t;
     const uint64_t pol = evict_first_policy();
     uint32_t tile = t0 + warp;
-    uint2 s, d, k, o;
-    ulonglong2 ts, te;
-    if (tile < t_end) {
-        const uint32_t g = tile * 32u;
-        s = ld_stream_u2(src2 + g, pol);
-        d = ld_stream_u2(dst2 + g, pol);
-        k = ld_stream_u2(pkt2 + g, pol);
-        o = ld_stream_u2(oct2 + g, pol);
-        ts = ld_stream_u64x2(st2 + g, pol);
-        te = ld_stream_u64x2(en2 + g, pol);
-    }
+    TileRegs cur;
+    if (tile < t_end) load_tile<kLayout>(b, tile, lane, pol, cur);
     for (uint32_t r = 0; r < rounds; ++r) {
         const uint32_t next = tile + kWarps;
-        uint2 ns, nd, nk, no;
-        ulonglong2 nt, ne;
-        if (next < t_end) {
-            const uint32_t g = next * 32u;
-            ns = ld_stream_u2(src2 + g, pol);
-            nd = ld_stream_u2(dst2 + g, pol);
-            nk = ld_stream_u2(pkt2 + g, pol);
-            no = ld_stream_u2(oct2 + g, pol);
-            nt = ld_stream_u64x2(st2 + g, pol);
-            ne = ld_stream_u64x2(en2 + g, pol);
-        }
+        TileRegs nx;
+        if (next < t_end) load_tile<kLayout>(b, next, lane, pol, nx);
         if (tile < t_end) {
-            const uint64_t dx = te.x - ts.x, dy = te.y - ts.y;
+            const uint64_t dx = cur.te.x - cur.ts.x, dy = cur.te.y - cur.ts.y;
             uint32_t hx, hy;
-            const uint32_t cx = stage_a<kSmem>(s.x, d.x, k.x, o.x, dx, p, gt, t, hx, window_in<kWin>(te.x, p));
-            const uint32_t cy = stage_a<kSmem>(s.y, d.y, k.y, o.y, dy, p, gt, t, hy, window_in<kWin>(te.y, p));
-            push<kHosts>(cx, o.x, dx, wq, lane, hx);
-            push<kHosts>(cy, o.y, dy, wq, lane, hy);
+            const uint32_t cx = stage_a<kSmem>(cur.s.x, cur.d.x, cur.k.x, cur.o.x, dx, p, gt, t, hx,
+                                               window_in<kWin>(cur.te.x, p));
+            const uint32_t cy = stage_a<kSmem>(cur.s.y, cur.d.y, cur.k.y, cur.o.y, dy, p, gt, t, hy,
+                                               window_in<kWin>(cur.te.y, p));
+            push<kHosts>(cx, cur.o.x, dx, wq, lane, hx);
+            push<kHosts>(cy, cur.o.y, dy, wq, lane, hy);
             drain_full<kSmem, kHot, kHosts>(wq, lane, gt, p, P, h, t, L);
         }
-        s = ns, d = nd, k = nk, o = no, ts = nt, te = ne;
+        cur = nx;
         tile = next;
         if constexpr (kHot) {
             if ((r + 1) % kEpochRounds == 0 && r + 1 < rounds) {
@@ -852,8 +881,22 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_soa(DevBatch b, const uint32_t
         }
     }
     if (blockIdx.x == gridDim.x - 1 && warp == 0)
-        run_scalar<1, kSmem, kHot, kMode>(b, tiles << 6, c.n, 32, lane, gt, p, P, h, t, wq, L);
+        run_scalar<kLayout == 0 ? 1 : 2, kSmem, kHot, kMode>(b, tiles << 6, b.n, 32, lane, gt, p, P, h, t, wq, L);
     k2_epilogue<kSmem, kHot, kHosts>(t, wq, lane, gt, p, P, h, hot, L);
+}
+
+template <bool kSmem, bool kHot, int kMode>
+__global__ void __launch_bounds__(kK2Block, 1) k2_soa(DevBatch b, const uint32_t* __restrict__ gt,
+                                                    uint32_t table_words, DevParams p,
+                                                    DevPartials P, DevHot hot, DevLog L) {
+    k2_tiles<0, kSmem, kHot, kMode>(b, gt, table_words, p, P, hot, L);
+}
+
+template <bool kSmem, bool kHot, int kMode>
+__global__ void __launch_bounds__(kK2Block, 1) k2_aos(DevBatch b, const uint32_t* __restrict__ gt,
+                                                    uint32_t table_words, DevParams p,
+                                                    DevPartials P, DevHot hot, DevLog L) {
+    k2_tiles<2, kSmem, kHot, kMode>(b, gt, table_words, p, P, hot, L);
 }
 
 // Other layouts: unaligned SoA (1), AoS 64-byte rows with vector (2) or
@@ -1359,6 +1402,7 @@ cudaError_t allow_smem(K kernel) {
 template <int L, bool kS, bool kH, int kW>
 constexpr auto k2_kernel() {
     if constexpr (L == 0) return k2_soa<kS, kH, kW>;
+    else if constexpr (L == 2) return k2_aos<kS, kH, kW>;
     else return k2_gen<L, kS, kH, kW>;
 }
 
@@ -1451,7 +1495,7 @@ LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool ho
     const uint64_t per_block = static_cast<uint64_t>(c.block) * 16;
     const uint64_t want = (b.n + per_block - 1) / per_block;
     uint64_t grid;
-    if (k2_layout(b) == 0) {
+    if (k2_layout(b) == 0 || k2_layout(b) == 2) {
         grid = std::min(sms, want); // persistent, one CTA per SM
     } else {
         // k2_gen: < 2^16 records per CTA (the hot limbs' bound); beyond one
