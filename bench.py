@@ -70,6 +70,9 @@ def parse_args():
     ap.add_argument("--input", default="soa", choices=["soa", "aos"],
                     help="record layout handed to the API: SoA columns (default, the north star's "
                          "loader layout) or the reference's 64-byte FlowRecord rows (gnm_analyze_aos)")
+    ap.add_argument("--no-pageable", action="store_true", help="skip the pageable-host e2e leg")
+    ap.add_argument("--no-adapter", action="store_true",
+                    help="skip the C++ drop-in leg (integration/_build/adapter_bench)")
     ap.add_argument("--hosts", action="store_true",
                     help="per-host mode: every step also builds SiteResult::hosts")
     return ap.parse_args()
@@ -521,6 +524,19 @@ def main():
     clk = clocks.stop()
     e2e_steps = args.e2e_steps or max(3, args.steps // 2)
     e2e_ms, _, res_e2e, _ = timed(host_batch, e2e_steps, breakdown=False)
+    # The same call from PAGEABLE host memory (a std::vector<FlowRecord> or a
+    # plain numpy array, as the C++ adapter passes it): the loader stages
+    # through pinned slots with multi-threaded copies.
+    pg_ms = None
+    if not args.no_pageable:
+        if args.input == "aos":
+            pg_batch = FlowRecords(np.array(rows, copy=True))
+        else:
+            pg_batch = FlowBatch(*[np.array(v, copy=True) for v in host])
+        pg_steps = 3
+        pg_ms, _, res_pg, _ = timed(pg_batch, pg_steps, breakdown=False)
+        assert np.array_equal(res.table, res_pg.table), "device and pageable-host runs differ"
+        del pg_batch
 
     total = n * world
     value = total * args.steps / (ms / 1e3)
@@ -567,7 +583,11 @@ def main():
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / e2e_steps,
                 "source": f"pinned host {args.input.upper()}, chunked double-buffered H2D",
                 "h2d_gbs": h2d_bytes * e2e_steps / (e2e_ms / 1e3) / 1e9, "h2d_raw_copy_gbs": h2d_peak,
-                "frac_of_raw_copy": (h2d_bytes * e2e_steps / (e2e_ms / 1e3) / 1e9) / h2d_peak},
+                "frac_of_raw_copy": (h2d_bytes * e2e_steps / (e2e_ms / 1e3) / 1e9) / h2d_peak,
+                "pageable": None if pg_ms is None else {
+                    "value": total * 3 / (pg_ms / 1e3), "unit": "records/s", "ms_per_step": pg_ms / 3,
+                    "source": f"pageable host {args.input.upper()} (numpy, not pinned): multi-threaded "
+                              f"staging copies into the loader's pinned slots"}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_kind": peak_kind,
                      "traffic": traffic["bytes_per_launch"] if traffic else None,
@@ -581,6 +601,24 @@ def main():
         "breakdown_ms": {"k1_plan": plan_avg, "k2": k2_avg, "k3_finalize": k3_avg,
                          "step": ms / args.steps, "source": "per-kernel CUDA events, separate untimed pass"},
     }
+    if rank == 0 and world == 1 and not args.no_adapter and args.workload in ("D1", "D3"):
+        # The reference's own call, flowmon::aggregate from a pageable
+        # std::vector<FlowRecord>, served by the C++ adapter: the full
+        # AnalysisResult (hosts and histograms included) end to end.
+        exe = os.path.join(ROOT, "integration", "_build", "adapter_bench")
+        if os.path.exists(exe):
+            eng.close()
+            torch.cuda.empty_cache()
+            out = subprocess.run([exe, "--workload", args.workload, "--records", str(n), "--steps", "3",
+                                  "--warmup", "1"], capture_output=True, text=True, timeout=900)
+            lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+            if out.returncode == 0 and lines:
+                a = json.loads(lines[-1])
+                line["e2e"]["adapter"] = {"value": a["records_per_s"], "unit": "records/s",
+                                          "ms_per_step": a["ms_per_step"], "source": a["source"],
+                                          "host_rows": a["host_rows"]}
+            else:
+                line["e2e"]["adapter"] = {"value": None, "error": (out.stderr or out.stdout)[-300:]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             reps = 3

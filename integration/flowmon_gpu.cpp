@@ -23,10 +23,13 @@
 // bucket at a rate inside that bucket and inside [min, max]. count_,
 // sum_ubps_, min_bps_, max_bps_ and buckets_ then equal the GPU's exact
 // integers and doubles field for field.
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <mutex>
+#include <thread>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -208,24 +211,44 @@ AnalysisResult collect(Engine& e, const gnm_result& r, const std::vector<gnm_sit
     std::vector<std::uint32_t> er(ne), eb(ne), ec(ne);
     if (ne) check(e.host_entries(er.data(), eb.data(), ec.data(), ne, &ne), "host histogram entries");
 
-    std::vector<std::uint64_t> site_dense(kBucketCount, 0);
-    std::vector<BucketCount> hb, sb;
-    std::uint64_t ei = 0, covered = 0;
-    for (std::uint64_t i = 0; i < nh;) {
-        const std::uint32_t site = hosts[i].site;
-        if (site >= rows.size() || rows[site].flow_count == 0)
+    // Host rows arrive in (site, host) order: one group of rows per present
+    // site. Groups (and their histogram entries) are independent, so they
+    // are rebuilt on several host threads -- RateHistogram::add runs once
+    // per flow -- and moved into the ordered maps afterwards.
+    struct Group {
+        std::uint32_t site;
+        std::uint64_t row0, row1, e0, e1;
+    };
+    std::vector<Group> groups;
+    for (std::uint64_t i = 0, ei = 0; i < nh;) {
+        Group g{hosts[i].site, i, i, ei, ei};
+        if (g.site >= rows.size() || rows[g.site].flow_count == 0)
             throw std::runtime_error("flowmon GPU adapter: host row of an empty or unknown site");
-        const gnm_site_stats& g = rows[site];
-        SiteResult& sr = out.sites[site];
-        std::uint64_t host_flows = 0;
-        for (; i < nh && hosts[i].site == site; ++i) {
+        for (; i < nh && hosts[i].site == g.site; ++i)
+            for (; ei < ne && er[ei] == i; ++ei) {
+            }
+        g.row1 = i;
+        g.e1 = ei;
+        groups.push_back(g);
+    }
+    if (!groups.empty() && groups.back().e1 != ne)
+        throw std::runtime_error("flowmon GPU adapter: histogram entries past the last host row");
+    std::vector<SiteResult> built(groups.size());
+    auto build = [&](std::size_t gi) {
+        const Group& gr = groups[gi];
+        const gnm_site_stats& g = rows[gr.site];
+        SiteResult& sr = built[gi];
+        std::vector<std::uint64_t> site_dense(kBucketCount, 0);
+        std::vector<BucketCount> hb, sb;
+        std::uint64_t host_flows = 0, ei = gr.e0;
+        for (std::uint64_t i = gr.row0; i < gr.row1; ++i) {
             const gnm_host_stats& h = hosts[i];
             hb.clear();
-            for (; ei < ne && er[ei] == i; ++ei) {
+            for (; ei < gr.e1 && er[ei] == i; ++ei) {
                 hb.push_back({eb[ei], ec[ei]});
                 site_dense[eb[ei]] += ec[ei];
             }
-            HostResult& hr = sr.hosts[h.host];
+            HostResult& hr = sr.hosts.emplace_hint(sr.hosts.end(), h.host, HostResult{})->second;
             hr.stats = stats_of(h.flow_count, h.min_bps, h.max_bps, h.avg_bps, h.median_bps);
             hr.histogram = rebuild_histogram(hb, h.flow_count, join(h.rate_ubps_lo, h.rate_ubps_hi), h.min_bps,
                                              h.max_bps);
@@ -233,22 +256,39 @@ AnalysisResult collect(Engine& e, const gnm_result& r, const std::vector<gnm_sit
         }
         if (host_flows != g.flow_count)
             throw std::runtime_error("flowmon GPU adapter: host rows do not sum to the site's flows");
-        sb.clear();
         for (std::size_t k = 0; k < kBucketCount; ++k)
             if (site_dense[k]) {
                 if (site_dense[k] > UINT32_MAX) throw std::runtime_error("flowmon GPU adapter: bucket overflow");
                 sb.push_back({static_cast<std::uint32_t>(k), static_cast<std::uint32_t>(site_dense[k])});
-                site_dense[k] = 0;
             }
         sr.stats = stats_of(g.flow_count, g.min_bps, g.max_bps, g.avg_bps, g.median_bps);
         sr.histogram = rebuild_histogram(sb, g.flow_count, join(g.rate_ubps_lo, g.rate_ubps_hi), g.min_bps,
                                          g.max_bps);
-        ++covered;
+    };
+    const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 16u));
+    if (nt == 1 || groups.size() < 2 || r.tallies.forward < (1u << 16)) {
+        for (std::size_t gi = 0; gi < groups.size(); ++gi) build(gi);
+    } else {
+        std::atomic<std::size_t> next{0};
+        std::vector<std::exception_ptr> errs(nt);
+        std::vector<std::thread> th;
+        for (unsigned t = 0; t < nt; ++t)
+            th.emplace_back([&, t] {
+                try {
+                    for (std::size_t gi; (gi = next.fetch_add(1)) < groups.size();) build(gi);
+                } catch (...) {
+                    errs[t] = std::current_exception();
+                }
+            });
+        for (auto& x : th) x.join();
+        for (auto& ep : errs)
+            if (ep) std::rethrow_exception(ep);
     }
-    if (ei != ne) throw std::runtime_error("flowmon GPU adapter: histogram entries past the last host row");
+    for (std::size_t gi = 0; gi < groups.size(); ++gi)
+        out.sites.emplace_hint(out.sites.end(), groups[gi].site, std::move(built[gi]));
     std::uint64_t present = 0;
     for (const gnm_site_stats& g : rows) present += g.flow_count != 0;
-    if (present != covered) throw std::runtime_error("flowmon GPU adapter: site without host rows");
+    if (present != groups.size()) throw std::runtime_error("flowmon GPU adapter: site without host rows");
     return out;
 }
 

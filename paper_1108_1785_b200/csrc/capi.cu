@@ -504,6 +504,49 @@ gnm::DevBatch aos_batch(const void* rec, uint64_t n) {
 // with K2 on the compute stream, chunk by chunk (SURVEY.md §8 loader L1).
 // Columns already in pinned memory DMA straight from the caller's buffers;
 // pageable columns go through the context's pinned staging slots.
+// Pageable host input: the copy into the pinned staging slot is the
+// bottleneck of the loader (one core copies ~10 GB/s, PCIe takes ~55), so
+// a chunk's column pieces are copied by several host threads, each taking
+// an equal share of the concatenated bytes.
+struct CopySeg {
+    unsigned char* dst;
+    const unsigned char* src;
+    size_t bytes;
+};
+
+void staged_copy(const std::vector<CopySeg>& segs) {
+    static const unsigned kThreads = [] {
+        unsigned t = std::thread::hardware_concurrency() / 2;
+        if (const char* e = std::getenv("GNM_STAGE_THREADS")) t = static_cast<unsigned>(std::atoi(e));
+        return std::max(1u, std::min(t, 16u));
+    }();
+    constexpr size_t kMinPerThread = 8u << 20;
+    size_t total = 0;
+    for (const CopySeg& g : segs) total += g.bytes;
+    const unsigned nt = static_cast<unsigned>(std::min<size_t>(kThreads, std::max<size_t>(1, total / kMinPerThread)));
+    // bytes [a, b) of the concatenation
+    auto run = [&](size_t a, size_t b) {
+        size_t at = 0;
+        for (const CopySeg& g : segs) {
+            const size_t lo = std::max(a, at), hi = std::min(b, at + g.bytes);
+            if (lo < hi) std::memcpy(g.dst + (lo - at), g.src + (lo - at), hi - lo);
+            at += g.bytes;
+        }
+    };
+    if (nt <= 1) {
+        run(0, total);
+        return;
+    }
+    const size_t per = (total / nt + 4095) & ~size_t(4095);
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < nt; ++t) {
+        const size_t a = std::min(total, per * t), b = std::min(total, per * (t + 1));
+        if (a < b) th.emplace_back(run, a, b);
+    }
+    run(0, std::min(total, per));
+    for (auto& x : th) x.join();
+}
+
 void load_and_run(gnm_ctx* c, bool aos, const void* const* cols, const size_t* widths, int ncols,
                   uint64_t n, const gnm::DevParams& p, bool archive = false) {
     size_t rec_bytes = 0;
@@ -531,11 +574,13 @@ void load_and_run(gnm_ctx* c, bool aos, const void* const* cols, const size_t* w
             // The pinned slot is free once its previous H2D completed.
             ck(cudaEventSynchronize(c->ev_h2d[slot]), "cudaEventSynchronize");
             size_t hoff = 0;
+            std::vector<CopySeg> segs;
             for (int i = 0; i < ncols; ++i) {
-                std::memcpy(c->h_stage[slot] + hoff,
-                            static_cast<const unsigned char*>(cols[i]) + base * widths[i], m * widths[i]);
+                segs.push_back({c->h_stage[slot] + hoff, static_cast<const unsigned char*>(cols[i]) + base * widths[i],
+                                m * widths[i]});
                 hoff += m * widths[i];
             }
+            staged_copy(segs);
             ck(cudaMemcpyAsync(dslot, c->h_stage[slot], hoff, cudaMemcpyHostToDevice, c->copy_stream),
                "cudaMemcpyAsync(H2D)");
             for (int i = 0; i < ncols; ++i) {
