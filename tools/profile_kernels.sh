@@ -37,4 +37,15 @@ if has launches; then
       python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/launches_${TAG}.log 2>&1
   echo "launches exit $?"
 fi
+if has hlaunches; then
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file gpurun_out/hlaunches_${TAG}.csv \
+      python bench.py --hosts --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 --no-pageable --no-adapter \
+      > gpurun_out/hlaunches_${TAG}.log 2>&1
+  echo "hlaunches exit $?"
+fi
+if has hbench; then
+  python bench.py --hosts --no-cpu-baseline --no-pageable --no-adapter > gpurun_out/hbench_${TAG}.json 2>&1
+  echo "hbench exit $?"
+fi
 exit 0
