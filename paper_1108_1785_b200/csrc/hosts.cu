@@ -85,15 +85,21 @@ __device__ __forceinline__ uint32_t insert_key(unsigned long long* keys, uint32_
 // slot's L2 atomics, so each CTA folds flows into a shared table of kAgg
 // entries first (an entry belongs to the first slot hashed to it; a flow
 // whose entry is taken goes to L2 directly). An entry keeps micro-bps below
-// 2^48 as three 16-bit limbs in u32 counters (native shared atomics); the
-// thread whose add reaches kFlushAt moves the limbs to L2 with atomic
-// exchanges, so no counter can wrap. Per-entry f32 bounds (rounded outward)
-// filter the L2 min/max reductions: a stale bound only costs an extra one.
+// 2^48 as three 16-bit limbs in u32 counters (native, non-returning shared
+// atomics). A CTA takes a contiguous range of at most kInsItemsPerCta work
+// items of at most kInsChunk flows, i.e. fewer than 2^16 adds per limb, so
+// no counter can wrap and no add has to return its value. Per-entry f32
+// bounds (rounded outward) filter the L2 min/max reductions: a stale bound
+// only costs an extra one.
+// Dense ids: the slot is computed, not probed; whether it is occupied is
+// read back from its max-rate accumulator (every flow's rate is > 0), and
+// its key is rebuilt from the id in h_collect_dense -- no per-flow key
+// traffic at all.
 constexpr uint32_t kInsBlock = 256;
 constexpr uint32_t kAgg = 2048;
-constexpr uint32_t kFlushAt = 1u << 15;
-constexpr size_t kInsSmem = kAgg * (4 + 4 + 3 * 4 + 4 + 4); // 48 KB
+constexpr size_t kInsSmem = kAgg * (4 + 4 + 3 * 4 + 4); // 40 KB
 constexpr uint32_t kInsChunk = 2048;
+constexpr uint32_t kInsItemsPerCta = 31; // 31 * 2048 < 2^16
 
 __device__ __forceinline__ void red_u64(unsigned long long* p, unsigned long long v) {
     asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -106,7 +112,6 @@ struct AggSmem {
     float* mn; // >= the smallest rate this CTA reduced into L2 for the entry (+inf: none)
     float* mx; // <= the largest
     uint32_t* key;
-    uint32_t* cnt;
     uint32_t* limb; // [3][kAgg]
 };
 
@@ -139,10 +144,6 @@ __device__ __forceinline__ void fold(uint32_t slot, unsigned long long lo, uint3
             red_max_u64(a + 4, rate);
             atomicMax(reinterpret_cast<int*>(t.mx + e), __float_as_int(__double2float_rd(r)));
         }
-        if (atomicAdd(t.cnt + e, 1u) + 1u == kFlushAt) {
-            agg_flush(t, e, a);
-            atomicSub(t.cnt + e, kFlushAt);
-        }
     } else {
         red_u64(a + 0, lo & 0xFFFFFFFFull);
         red_u64(a + 1, lo >> 32);
@@ -152,6 +153,7 @@ __device__ __forceinline__ void fold(uint32_t slot, unsigned long long lo, uint3
     }
 }
 
+template <bool kDense>
 __global__ void __launch_bounds__(kInsBlock, 4) h_insert(DevLog L, const unsigned int* __restrict__ counts,
                                                          const uint32_t* __restrict__ off,
                                                          const uint2* __restrict__ dir,
@@ -164,22 +166,22 @@ __global__ void __launch_bounds__(kInsBlock, 4) h_insert(DevLog L, const unsigne
     t.mn = reinterpret_cast<float*>(h_smem);
     t.mx = t.mn + kAgg;
     t.key = reinterpret_cast<uint32_t*>(t.mx + kAgg);
-    t.cnt = t.key + kAgg;
-    t.limb = t.cnt + kAgg;
+    t.limb = t.key + kAgg;
     for (uint32_t i = threadIdx.x; i < kAgg; i += blockDim.x) {
         t.mn[i] = __int_as_float(0x7F800000); // +inf
         t.mx[i] = 0.0f;
         t.key[i] = 0xFFFFFFFFu;
-        t.cnt[i] = 0;
 #pragma unroll
         for (int f = 0; f < 3; ++f) t.limb[f * kAgg + i] = 0;
     }
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     const uint32_t chunks = (L.warp_cap + kInsChunk - 1) / kInsChunk;
     const uint32_t items = L.regions * chunks;
-    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < items; w += nwarps) {
+    // this CTA's contiguous item range (<= kInsItemsPerCta items, see above)
+    const uint32_t i0 = static_cast<uint32_t>(static_cast<uint64_t>(items) * blockIdx.x / gridDim.x);
+    const uint32_t i1 = static_cast<uint32_t>(static_cast<uint64_t>(items) * (blockIdx.x + 1) / gridDim.x);
+    for (uint32_t w = i0 + (threadIdx.x >> 5); w < i1; w += blockDim.x >> 5) {
         const uint32_t r = w / chunks;
         const uint32_t c0 = (w % chunks) * kInsChunk;
         const uint32_t n = min(counts[r], c0 + kInsChunk);
@@ -205,7 +207,7 @@ __global__ void __launch_bounds__(kInsBlock, 4) h_insert(DevLog L, const unsigne
             for (int q = 0; q < 4; ++q) { // dense ids, or issue the four first probes
                 const uint32_t site = L.buckets ? xs[q] : xs[q] >> kLogSiteShift;
                 key[q] = static_cast<unsigned long long>(site) << 32 | hs[q];
-                if (dir) {
+                if constexpr (kDense) {
                     // The host's /16 is in the registry directory (its /24 is
                     // registered): id = rank of the /16 << 16 | its low 16
                     // bits, bit-reversed so that the hosts of one /24 (one
@@ -214,18 +216,18 @@ __global__ void __launch_bounds__(kInsBlock, 4) h_insert(DevLog L, const unsigne
                     const uint32_t d = hs[q] >> 16;
                     const uint2 pr = __ldg(dir + (d >> 5));
                     h0[q] = (pr.y + __popc(pr.x & ((1u << (d & 31u)) - 1u))) << 16 | __brev(hs[q] << 16);
+                    first[q] = 0;
                 } else {
                     h0[q] = static_cast<uint32_t>((key[q] * 0x9E3779B97F4A7C15ull) >> shift) & mask;
+                    first[q] = i + q < n ? keys[h0[q]] : 0ull;
                 }
-                first[q] = i + q < n ? keys[h0[q]] : 0ull;
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 if (i + q >= n) break;
                 uint32_t slot;
-                if (dir) { // mark the id used (every writer stores the same key)
+                if constexpr (kDense) {
                     slot = h0[q];
-                    if (first[q] != key[q]) keys[slot] = key[q];
                 } else {
                     slot = first[q] == key[q] ? h0[q] : insert_key(keys, mask, shift, key[q]);
                 }
@@ -255,6 +257,50 @@ __global__ void __launch_bounds__(256) h_collect(const unsigned long long* __res
         const uint32_t s = base + threadIdx.x;
         const unsigned long long k = s < cap ? keys[s] : kEmpty;
         const bool occ = k != kEmpty;
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, occ);
+        uint32_t first = 0;
+        if (lane == 0 && m) first = atomicAdd(n_out, __popc(m));
+        first = __shfl_sync(0xFFFFFFFFu, first, 0);
+        if (occ) {
+            const uint32_t i = first + __popc(m & ((1u << lane) - 1u));
+            hk[i] = k;
+            hs[i] = s;
+        }
+    }
+}
+
+// Dense ids: the /16 block of each rank (the inverse of the directory's
+// rank-of-/16), for rebuilding a slot's host address.
+__global__ void h_prefix_of_rank(const uint2* __restrict__ dir, uint32_t* __restrict__ prefix) {
+    const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= 65536u) return;
+    const uint2 pr = __ldg(dir + (d >> 5));
+    if ((pr.x >> (d & 31u)) & 1u) prefix[pr.y + __popc(pr.x & ((1u << (d & 31u)) - 1u))] = d;
+}
+
+// H2a (dense ids): the occupied slots (max-rate accumulator set: every
+// Forward rate is > 0) and their keys rebuilt from the id: host = the /16 of
+// the rank | the un-reversed low 16 bits, site = the registry's /24 entry
+// (words: the device table, site values masked by site_mask).
+__global__ void __launch_bounds__(256) h_collect_dense(const unsigned long long* __restrict__ acc, uint32_t cap,
+                                                       const uint32_t* __restrict__ prefix,
+                                                       const uint32_t* __restrict__ words, uint32_t site_mask,
+                                                       unsigned long long* __restrict__ hk, uint32_t* __restrict__ hs,
+                                                       unsigned int* __restrict__ n_out) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint2* dir = reinterpret_cast<const uint2*>(words);
+    for (uint32_t base = blockIdx.x * blockDim.x; base < cap; base += gridDim.x * blockDim.x) {
+        const uint32_t s = base + threadIdx.x;
+        const bool occ = s < cap && acc[static_cast<size_t>(s) * 5 + 4] != 0ull;
+        unsigned long long k = 0;
+        if (occ) {
+            const uint32_t ip = __ldg(prefix + (s >> 16)) << 16 | (__brev(s & 0xFFFFu) >> 16);
+            const uint32_t d = ip >> 16;
+            const uint2 pr = __ldg(dir + (d >> 5));
+            const uint32_t node = __ldg(words + 4096u + pr.y + __popc(pr.x & ((1u << (d & 31u)) - 1u)));
+            const uint32_t v = (node & 0x80000000u) ? node & 0x7FFFFFFFu : __ldg(words + node + ((ip >> 8) & 0xFFu));
+            k = static_cast<unsigned long long>(v & site_mask) << 32 | ip;
+        }
         const unsigned m = __ballot_sync(0xFFFFFFFFu, occ);
         uint32_t first = 0;
         if (lane == 0 && m) first = atomicAdd(n_out, __popc(m));
@@ -554,8 +600,8 @@ cudaError_t finish_two_round(int device, HostRows& h, const unsigned long long* 
 } // namespace
 
 cudaError_t build_hosts_local(int device, const HostSlice* slices, int n_slices, const unsigned int* counts,
-                              size_t n_counts, uint64_t max_keys, const uint32_t* dir, uint32_t n16, HostRows& out,
-                              HostLocal& loc, cudaStream_t s) {
+                              size_t n_counts, uint64_t max_keys, const uint32_t* dir, uint32_t n16, bool packed,
+                              HostRows& out, HostLocal& loc, cudaStream_t s) {
     free_hosts(out, s);
     free_local(loc, s);
     loc.ready = true;
@@ -578,7 +624,8 @@ cudaError_t build_hosts_local(int device, const HostSlice* slices, int n_slices,
     HCK(cudaStreamSynchronize(s));
     const uint64_t n = h_scal[0];
     if (n == 0) return cudaSuccess;
-    HCK(cudaFuncSetAttribute(h_insert, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kInsSmem)));
+    HCK(cudaFuncSetAttribute(h_insert<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kInsSmem)));
+    HCK(cudaFuncSetAttribute(h_insert<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kInsSmem)));
     int sms = 0;
     HCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     // H1: dense ids when the registry's /16 blocks allow (every host lies in
@@ -594,16 +641,23 @@ cudaError_t build_hosts_local(int device, const HostSlice* slices, int n_slices,
     HCK(dalloc(&out.row_of, n, s)); // slots first, rows later; owned by `out`
     HCK(dalloc(&out.bkt, n, s));
     out.n_flows = n;
-    HCK(cudaMemsetAsync(loc.table, 0xFF, static_cast<size_t>(cap) * 8, s));
+    if (!dense) HCK(cudaMemsetAsync(loc.table, 0xFF, static_cast<size_t>(cap) * 8, s));
     HCK(cudaMemsetAsync(loc.acc, 0, static_cast<size_t>(cap) * 40, s));
     for (int i = 0; i < n_slices; ++i) {
         const HostSlice& sl = slices[i];
-        // Four CTAs per SM, fewer for small logs.
+        // At least four CTAs per SM, and enough CTAs that none takes more
+        // than kInsItemsPerCta items (the limbs' no-wrap bound).
         const uint64_t items = static_cast<uint64_t>(sl.log.regions) * ((sl.log.warp_cap + kInsChunk - 1) / kInsChunk);
-        const uint32_t g = std::min<uint32_t>(grid_for(device, items * 32, kInsBlock), 4 * sms);
-        h_insert<<<g, kInsBlock, kInsSmem, s>>>(sl.log, counts + sl.count_off, off + sl.count_off,
-                                                dense ? reinterpret_cast<const uint2*>(dir) : nullptr, loc.table,
-                                                cap - 1, 64 - tbits, loc.acc, out.row_of, out.bkt);
+        const uint64_t g = std::max<uint64_t>((items + kInsItemsPerCta - 1) / kInsItemsPerCta,
+                                              std::min<uint64_t>(items, 4ull * sms));
+        if (dense)
+            h_insert<true><<<static_cast<uint32_t>(g), kInsBlock, kInsSmem, s>>>(
+                sl.log, counts + sl.count_off, off + sl.count_off, reinterpret_cast<const uint2*>(dir), loc.table,
+                cap - 1, 64 - tbits, loc.acc, out.row_of, out.bkt);
+        else
+            h_insert<false><<<static_cast<uint32_t>(g), kInsBlock, kInsSmem, s>>>(
+                sl.log, counts + sl.count_off, off + sl.count_off, nullptr, loc.table, cap - 1, 64 - tbits, loc.acc,
+                out.row_of, out.bkt);
         HCK(cudaGetLastError());
     }
     // H2: distinct keys in (site, host) order -> rows.
@@ -612,8 +666,17 @@ cudaError_t build_hosts_local(int device, const HostSlice* slices, int n_slices,
     const uint64_t kcap = std::min<uint64_t>(n, cap);
     HCK(tmp_.get(&hk, kcap));
     HCK(tmp_.get(&hs, kcap));
-    h_collect<<<grid_for(device, cap, 256), 256, 0, s>>>(loc.table, cap, hk, hs,
-                                                        reinterpret_cast<unsigned int*>(scal + 1));
+    if (dense) {
+        uint32_t* prefix = nullptr;
+        HCK(tmp_.get(&prefix, n16));
+        h_prefix_of_rank<<<256, 256, 0, s>>>(reinterpret_cast<const uint2*>(dir), prefix);
+        h_collect_dense<<<grid_for(device, cap, 256), 256, 0, s>>>(loc.acc, cap, prefix, dir,
+                                                                  packed ? 0xFFFFFu : 0x7FFFFFFFu, hk, hs,
+                                                                  reinterpret_cast<unsigned int*>(scal + 1));
+    } else {
+        h_collect<<<grid_for(device, cap, 256), 256, 0, s>>>(loc.table, cap, hk, hs,
+                                                            reinterpret_cast<unsigned int*>(scal + 1));
+    }
     HCK(cudaGetLastError());
     HCK(cudaMemcpyAsync(h_scal + 1, scal + 1, 8, cudaMemcpyDeviceToHost, s));
     HCK(cudaStreamSynchronize(s));
@@ -660,7 +723,7 @@ cudaError_t build_hosts(int device, const HostSlice* slices, int n_slices, const
                         size_t n_counts, uint64_t max_keys, HostRows& out, cudaStream_t s) {
     HostLocal loc;
     const cudaError_t e =
-        build_hosts_local(device, slices, n_slices, counts, n_counts, max_keys, nullptr, 0, out, loc, s);
+        build_hosts_local(device, slices, n_slices, counts, n_counts, max_keys, nullptr, 0, true, out, loc, s);
     if (e != cudaSuccess) {
         free_local(loc, s);
         return e;
