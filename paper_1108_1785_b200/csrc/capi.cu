@@ -687,7 +687,8 @@ cudaError_t build_hosts_local(gnm_ctx* c, const gnm_registry* reg) {
     c->kernel_launches += 3 + hs.size(); // own kernels; cub scan/sorts not counted
     const uint32_t n16 = c->table.leaf_begin - c->table.node_begin; // one node per non-empty /16
     return gnm::build_hosts_local(c->device, hs.data(), static_cast<int>(hs.size()), c->d_counts, c->counts_used,
-                                  max_keys, c->table.words, n16, c->table.packed, c->hrows, c->hlocal, c->stream);
+                                  max_keys, static_cast<uint32_t>(reg->r.sites().size()), c->table.words, n16,
+                                  c->table.packed, c->hrows, c->hlocal, c->stream);
 }
 
 // Round 1 -> round 2 of the median: K3a finds every site's median

@@ -336,12 +336,22 @@ constexpr size_t kTwoRoundBytes = 64ull << 20;
 // Hot (row, super-bucket) pairs would serialise on one L2 counter, so each
 // CTA counts into a shared table first (first come, first served; a pair
 // whose entry is taken goes to L2 directly) and flushes it once.
-constexpr uint32_t kCoarseAgg = 4096;
+#ifndef GNM_HC_AGG_BITS
+#define GNM_HC_AGG_BITS 13
+#endif
+#ifndef GNM_HC_CTAS_PER_SM
+#define GNM_HC_CTAS_PER_SM 3
+#endif
+constexpr uint32_t kCoarseAggBits = GNM_HC_AGG_BITS;
+constexpr uint32_t kCoarseAgg = 1u << kCoarseAggBits;
+constexpr size_t kCoarseSmem = static_cast<size_t>(kCoarseAgg) * 8;
 // With `rank`, also turns every flow's slot into its row (in place).
 __global__ void __launch_bounds__(512) h_coarse(uint32_t* __restrict__ row, const uint32_t* __restrict__ bk,
                                                 uint32_t n, uint32_t n_rows, const unsigned long long* __restrict__ rank,
                                                 uint32_t* __restrict__ coarse) {
-    __shared__ uint32_t tkey[kCoarseAgg], tcnt[kCoarseAgg];
+    extern __shared__ uint32_t hc_smem[];
+    uint32_t* tkey = hc_smem;
+    uint32_t* tcnt = hc_smem + kCoarseAgg;
     for (uint32_t i = threadIdx.x; i < kCoarseAgg; i += blockDim.x) {
         tkey[i] = 0xFFFFFFFFu;
         tcnt[i] = 0;
@@ -351,7 +361,7 @@ __global__ void __launch_bounds__(512) h_coarse(uint32_t* __restrict__ row, cons
         const uint32_t r = rank ? static_cast<uint32_t>(rank[row[j]]) : row[j], sb = bk[j] >> 6;
         if (rank) row[j] = r;
         const uint32_t key = r << 8 | sb; // rows < 2^24 on this path (rows * 628 B <= 64 MB)
-        const uint32_t e = (key * 2654435761u) >> (32 - 12);
+        const uint32_t e = (key * 2654435761u) >> (32 - kCoarseAggBits);
         uint32_t cur = tkey[e];
         if (cur == 0xFFFFFFFFu) cur = atomicCAS(tkey + e, 0xFFFFFFFFu, key);
         if (cur == 0xFFFFFFFFu || cur == key)
@@ -590,7 +600,12 @@ cudaError_t finish_two_round(int device, HostRows& h, const unsigned long long* 
     HCK(tmp_.get(&fine, static_cast<size_t>(nr) * kFineH));
     HCK(cudaMemsetAsync(coarse, 0, static_cast<size_t>(nr) * kCoarseH * 4, s));
     HCK(cudaMemsetAsync(fine, 0, static_cast<size_t>(nr) * kFineH * 4, s));
-    h_coarse<<<grid_for(device, n, 512), 512, 0, s>>>(h.row_of, h.bkt, n, nr, rank, coarse);
+    HCK(cudaFuncSetAttribute(h_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kCoarseSmem)));
+    int sms = 0;
+    HCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    const uint32_t cg = static_cast<uint32_t>(std::max<uint64_t>(
+        1, std::min<uint64_t>((n + 511) / 512, static_cast<uint64_t>(sms) * GNM_HC_CTAS_PER_SM)));
+    h_coarse<<<cg, 512, kCoarseSmem, s>>>(h.row_of, h.bkt, n, nr, rank, coarse);
     h_msb<<<grid_for(device, nr, 128), 128, 0, s>>>(coarse, nr, msb, mrank, cnt);
     h_fine<<<grid_for(device, n, 256), 256, 0, s>>>(h.row_of, h.bkt, n, msb, fine);
     h_final2<<<grid_for(device, nr, 128), 128, 0, s>>>(acc, cnt, msb, mrank, fine, hk_sorted, hs_sorted, nr, h.rows);
@@ -600,8 +615,8 @@ cudaError_t finish_two_round(int device, HostRows& h, const unsigned long long* 
 } // namespace
 
 cudaError_t build_hosts_local(int device, const HostSlice* slices, int n_slices, const unsigned int* counts,
-                              size_t n_counts, uint64_t max_keys, const uint32_t* dir, uint32_t n16, bool packed,
-                              HostRows& out, HostLocal& loc, cudaStream_t s) {
+                              size_t n_counts, uint64_t max_keys, uint32_t n_sites, const uint32_t* dir, uint32_t n16,
+                              bool packed, HostRows& out, HostLocal& loc, cudaStream_t s) {
     free_hosts(out, s);
     free_local(loc, s);
     loc.ready = true;
@@ -684,10 +699,12 @@ cudaError_t build_hosts_local(int device, const HostSlice* slices, int n_slices,
     HCK(dalloc(&loc.hk_sorted, n_rows, s));
     HCK(dalloc(&loc.hs_sorted, n_rows, s));
     tb = 0;
-    HCK(cub::DeviceRadixSort::SortPairs(nullptr, tb, hk, loc.hk_sorted, hs, loc.hs_sorted, n_rows, 0, 64, s));
+    // keys are site << 32 | host: only the site's bits above the host sort
+    const int end_bit = 32 + std::max(1, bits_for(std::max<uint64_t>(n_sites, 1)));
+    HCK(cub::DeviceRadixSort::SortPairs(nullptr, tb, hk, loc.hk_sorted, hs, loc.hs_sorted, n_rows, 0, end_bit, s));
     unsigned char* tmp2 = nullptr;
     HCK(tmp_.get(&tmp2, tb));
-    HCK(cub::DeviceRadixSort::SortPairs(tmp2, tb, hk, loc.hk_sorted, hs, loc.hs_sorted, n_rows, 0, 64, s));
+    HCK(cub::DeviceRadixSort::SortPairs(tmp2, tb, hk, loc.hk_sorted, hs, loc.hs_sorted, n_rows, 0, end_bit, s));
     h_rank<<<grid_for(device, n_rows, 256), 256, 0, s>>>(loc.hs_sorted, n_rows, loc.table);
     HCK(cudaGetLastError());
     out.n_rows = n_rows;
@@ -723,7 +740,8 @@ cudaError_t build_hosts(int device, const HostSlice* slices, int n_slices, const
                         size_t n_counts, uint64_t max_keys, HostRows& out, cudaStream_t s) {
     HostLocal loc;
     const cudaError_t e =
-        build_hosts_local(device, slices, n_slices, counts, n_counts, max_keys, nullptr, 0, true, out, loc, s);
+        build_hosts_local(device, slices, n_slices, counts, n_counts, max_keys, 0xFFFFFFFFu, nullptr, 0, true, out,
+                          loc, s);
     if (e != cudaSuccess) {
         free_local(loc, s);
         return e;
@@ -841,7 +859,8 @@ cudaError_t hosts_global_begin(int device, HostRows& out, const HostLocal& loc, 
                                                          g.min, g.max);
         const uint32_t nf = static_cast<uint32_t>(out.n_flows);
         g_rows<<<grid_for(device, nf, 256), 256, 0, s>>>(out.row_of, nf, loc.table, g.local_to_global);
-        h_coarse<<<grid_for(device, nf, 512), 512, 0, s>>>(out.row_of, out.bkt, nf, static_cast<uint32_t>(n),
+        HCK(cudaFuncSetAttribute(h_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kCoarseSmem)));
+        h_coarse<<<grid_for(device, nf, 512), 512, kCoarseSmem, s>>>(out.row_of, out.bkt, nf, static_cast<uint32_t>(n),
                                                            nullptr, g.coarse);
         HCK(cudaGetLastError());
     }

@@ -69,8 +69,8 @@ struct HostGlobal {
 // dir / n16: the device registry table's /16 directory and its non-empty
 // /16 count (dense host ids when n16 << 16 <= 2^24), or null / 0 (hashing).
 cudaError_t build_hosts_local(int device, const HostSlice* slices, int n_slices, const unsigned int* counts,
-                              size_t n_counts, uint64_t max_keys, const uint32_t* dir, uint32_t n16, bool packed,
-                              HostRows& out, HostLocal& loc, cudaStream_t s);
+                              size_t n_counts, uint64_t max_keys, uint32_t n_sites, const uint32_t* dir, uint32_t n16,
+                              bool packed, HostRows& out, HostLocal& loc, cudaStream_t s);
 cudaError_t finish_hosts(int device, HostRows& out, HostLocal& loc, cudaStream_t s);
 // Global combine: begin (map local rows into the union, fill sums/min/max
 // and coarse counts), [caller all-reduces], prepare (each row's median
