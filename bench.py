@@ -224,8 +224,7 @@ def workload_config(w, n: int, n_sites: int, world: int, args) -> dict:
             "records_per_gpu": n, "sites": n_sites, "input": args.input,
             "hosts": ("per-host rows built every step" if args.hosts
                       else "site level only (gnm_ctx_set_hosts off)"),
-            "parallelism": (f"index shards x{world}, in-library NCCL two-round combine" if world > 1
-                            else "1 GPU"),
+            "parallelism": f"index shards x{world}",
             "l2": "inputs 3.2 GB/GPU > 126 MB L2; no flush needed" if n >= 10_000_000
                   else "inputs may fit L2"}
 
@@ -595,6 +594,9 @@ def main():
                      "kernel_ms": k2_avg, "alg_bytes_per_record": ALG_BYTES_PER_RECORD,
                      "physical_bytes_per_record": ALG_BYTES_PER_RECORD if args.input == "soa" else 64,
                      "frac_of_nominal_8tbs": achieved / NOMINAL_HBM_GBS},
+        "combine": (None if not distributed else
+                    "in-library NCCL two-round combine (gnm_ctx_comm_init), in the CUDA graph" if in_library
+                    else "torch.distributed (gloo test hook) two-round combine"),
         "gpu_launches": launches,
         "clocks": clk,
         "kernel_share": k2_avg / (ms / args.steps),

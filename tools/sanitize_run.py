@@ -73,4 +73,16 @@ with Engine(0) as eng:
     arc = make_archive(cols)
     eng.decode_archive(arc)
     eng.aggregate_archive(arc, cat)
+# in-library multi-rank combine: a loopback group (sites, per-host union,
+# histograms summed) and a world-size-1 NCCL communicator with graph replay
+from paper_1108_1785_b200 import Group
+with Group([0, 0], kind="loopback") as g:
+    g.aggregate(FlowBatch(*cols), cat, histograms=True)
+    g.set_hosts(True)
+    g.aggregate(FlowRecords(synth.to_aos(cols)), cat)
+    g.host_histogram_entries()
+with Engine(0) as e1:
+    e1.comm_init(1, 0, Engine.comm_unique_id())
+    for _ in range(3):
+        e1.aggregate(FlowBatch(*dcols), cat)
 print("sanitize run ok:", len(r.host_table), "host rows,", len(rb.host_table), "host rows (sorted path)")
