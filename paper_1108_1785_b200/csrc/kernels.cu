@@ -49,9 +49,6 @@ namespace {
 
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kDirWordsDev = 4096u; // registry.hpp kDirWords
-#ifndef GNM_K2_PINGPONG
-#define GNM_K2_PINGPONG 0
-#endif
 #ifndef GNM_K2_BLOCK
 #define GNM_K2_BLOCK 768
 #endif
@@ -856,42 +853,6 @@ __device__ __forceinline__ void k2_tiles(const DevBatch& b, const uint32_t* __re
     Ctr t;
     const uint64_t pol = evict_first_policy();
     uint32_t tile = t0 + warp;
-#if GNM_K2_PINGPONG
-    // Two register sets, two rounds in flight: set A holds even rounds, set
-    // B odd ones; each is refilled two rounds ahead right after use.
-    auto process = [&](const TileRegs& c) {
-        const uint64_t dx = c.te.x - c.ts.x, dy = c.te.y - c.ts.y;
-        uint32_t hx, hy;
-        const uint32_t cx = stage_a<kSmem>(c.s.x, c.d.x, c.k.x, c.o.x, dx, p, gt, t, hx, window_in<kWin>(c.te.x, p));
-        const uint32_t cy = stage_a<kSmem>(c.s.y, c.d.y, c.k.y, c.o.y, dy, p, gt, t, hy, window_in<kWin>(c.te.y, p));
-        push<kHosts>(cx, c.o.x, dx, wq, lane, hx);
-        push<kHosts>(cy, c.o.y, dy, wq, lane, hy);
-        drain_full<kSmem, kHot, kHosts>(wq, lane, gt, p, P, h, t, L);
-    };
-    auto epoch = [&](uint32_t r) {
-        if constexpr (kHot) {
-            if ((r + 1) % kEpochRounds == 0 && r + 1 < rounds) {
-                __syncthreads();
-                hot_normalize(h, hot, P);
-                __syncthreads();
-            }
-        }
-    };
-    TileRegs ra, rb;
-    if (tile < t_end) load_tile<kLayout>(b, tile, lane, pol, ra);
-    if (tile + kWarps < t_end) load_tile<kLayout>(b, tile + kWarps, lane, pol, rb);
-    for (uint32_t r = 0; r < rounds; r += 2) {
-        if (tile < t_end) process(ra);
-        if (tile + 2 * kWarps < t_end) load_tile<kLayout>(b, tile + 2 * kWarps, lane, pol, ra);
-        epoch(r);
-        if (r + 1 < rounds) {
-            if (tile + kWarps < t_end) process(rb);
-            if (tile + 3 * kWarps < t_end) load_tile<kLayout>(b, tile + 3 * kWarps, lane, pol, rb);
-            epoch(r + 1);
-        }
-        tile += 2 * kWarps;
-    }
-#else
     TileRegs cur;
     if (tile < t_end) load_tile<kLayout>(b, tile, lane, pol, cur);
     for (uint32_t r = 0; r < rounds; ++r) {
@@ -919,7 +880,6 @@ __device__ __forceinline__ void k2_tiles(const DevBatch& b, const uint32_t* __re
             }
         }
     }
-#endif
     if (blockIdx.x == gridDim.x - 1 && warp == 0)
         run_scalar<kLayout == 0 ? 1 : 2, kSmem, kHot, kMode>(b, tiles << 6, b.n, 32, lane, gt, p, P, h, t, wq, L);
     k2_epilogue<kSmem, kHot, kHosts>(t, wq, lane, gt, p, P, h, hot, L);
