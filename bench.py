@@ -71,6 +71,8 @@ def parse_args():
                     help="record layout handed to the API: SoA columns (default, the north star's "
                          "loader layout) or the reference's 64-byte FlowRecord rows (gnm_analyze_aos)")
     ap.add_argument("--no-pageable", action="store_true", help="skip the pageable-host e2e leg")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the secondary AoS / per-host device legs")
     ap.add_argument("--no-adapter", action="store_true",
                     help="skip the C++ drop-in leg (integration/_build/adapter_bench)")
     ap.add_argument("--hosts", action="store_true",
@@ -205,15 +207,29 @@ def reference_workers(n_sample: int, nproc: int) -> list[int]:
     return out or [1]
 
 
-def time_reference(w, n_sample: int, reps: int):
-    """Median ms per worker count for flowmon::aggregate on the sample."""
-    R, cat, rec = reference_sample(w, n_sample)
+def reference_plan(w, n: int, runs: int, budget_s: float, probe_records: int = 10_000_000):
+    """The reference's CPU timing setup on this box: the workload's first
+    records (up to all n), the fastest worker count probed at a
+    representative size (its per-call histogram allocation -- 40 KB per
+    (site, host) per worker -- dominates small samples, so the probe must not
+    be tiny), and the largest sample whose `runs` timed calls fit
+    `budget_s`. Returns (R, cat, rec, m, best_workers, probe_ms_by_workers)."""
     nproc = os.cpu_count() or 1
-    res = {}
-    for wk in reference_workers(n_sample, nproc):
-        ts = [R.time_range(rec, cat, 0, n_sample, wk) for _ in range(reps)]
-        res[wk] = statistics.median(ts)
-    return res
+    m_probe = min(n, probe_records)
+    R, cat, rec = reference_sample(w, m_probe)
+    workers = reference_workers(m_probe, nproc)
+    R.time_range(rec, cat, 0, m_probe, 1)  # warm-up: page faults, allocator
+    probe = {wk: R.time_range(rec, cat, 0, m_probe, wk) for wk in workers}
+    best = min(probe, key=probe.get)
+    per_record_ms = probe[best] / m_probe
+    m = int(budget_s * 1e3 / max(1, runs) / per_record_ms)
+    m = max(m_probe, min(n, m))
+    if m != m_probe:
+        del rec
+        R, cat, rec = reference_sample(w, m)
+        if best not in reference_workers(m, nproc):
+            best = max(reference_workers(m, nproc))
+    return R, cat, rec, m, best, probe
 
 
 def workload_config(w, n: int, n_sites: int, world: int, args) -> dict:
@@ -259,32 +275,17 @@ def run_reference_arm(args):
     n = args.records or w.n
     nproc = os.cpu_count() or 1
     steps = args.steps if args.steps is not None else 10
-    # Probe on a 2M-record prefix: warm-up (page faults, allocator), then the
-    # median of two runs per worker count (the reference gets slower with
-    # more workers on shuffled data).
-    n_probe = min(args.cpu_sample, n)
-    R, cat, rec = reference_sample(w, n_probe)
-    workers = reference_workers(n_probe, nproc)
-    R.time_range(rec, cat, 0, n_probe, 1)
-    probe = {wk: statistics.median(R.time_range(rec, cat, 0, n_probe, wk) for _ in range(2))
-             for wk in workers}
-    best = min(probe, key=probe.get)
-    rate = n_probe / (probe[best] / 1e3)
-    # Sample size: ~150 s of timed CPU work over warmup + steps, 2M..20M
-    # records (never more than the workload).
-    budget_s = float(os.environ.get("GNM_REF_BUDGET_S", "150"))
-    m = int(rate * budget_s / max(1, steps + args.warmup))
-    m = max(min(n_probe, n), min(n, 20_000_000, m))
-    if m != n_probe:
-        del rec
-        R, cat, rec = reference_sample(w, m)
-        if best not in reference_workers(m, nproc):
-            best = max(reference_workers(m, nproc))
+    # Each step is the workload's first m records (all n when ~300 s of CPU
+    # time allows), at the fastest worker count probed on 10M records.
+    budget_s = float(os.environ.get("GNM_REF_BUDGET_S", "300"))
+    R, cat, rec, m, best, probe = reference_plan(w, n, steps + args.warmup, budget_s,
+                                                 probe_records=min(args.cpu_sample * 5, n))
     for _ in range(args.warmup):
         R.time_range(rec, cat, 0, m, best)
     ts = [R.time_range(rec, cat, 0, m, best) for _ in range(steps)]
     total_ms = sum(ts)
     value = m * len(ts) / (total_ms / 1e3)
+    n_probe = min(args.cpu_sample * 5, n)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "records/s",
         "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
@@ -292,8 +293,9 @@ def run_reference_arm(args):
         "vs_baseline": None, "dtype": "u32/u64 int + f64", "data": "synthetic",
         "config": workload_config(w, n, len(w.sites.base), world, args),
         "cpu_baseline": {"value": value, "unit": "records/s", "cores": best, "kind": "reference",
-                         "sample": f"each step: the first {m} of the workload's {n} records per GPU "
-                                   f"(hosts computed, as the reference always does); unmodified "
+                         "sample": (f"each step: all {n} records of the workload" if m == n else
+                                    f"each step: the first {m} of the workload's {n} records per GPU")
+                                   + f" (hosts computed, as the reference always does); unmodified "
                                    f"flowmon::aggregate(FilterParams{{}}, workers={best}, Hash) from "
                                    f"oracle/_ref (-O3 -DNDEBUG); worker probe on {n_probe} records, ms by "
                                    f"workers {json.dumps({str(k): round(v, 1) for k, v in probe.items()})}; "
@@ -603,6 +605,38 @@ def main():
         "breakdown_ms": {"k1_plan": plan_avg, "k2": k2_avg, "k3_finalize": k3_avg,
                          "step": ms / args.steps, "source": "per-kernel CUDA events, separate untimed pass"},
     }
+    if rank == 0 and world == 1 and not args.no_extras and args.input == "soa" and not args.hosts:
+        # Secondary device-resident measurements of the same records, so the
+        # driver's own line carries them: the reference's 64-byte FlowRecord
+        # rows (k2_aos; roofline on their 64 B/record physical bytes) and
+        # per-host mode (SiteResult::hosts every step). Same timing rules.
+        sec = {}
+        try:
+            stage = np.empty(n * 64, np.uint8)  # pageable: no pinned memory left behind
+            synth._lib().gnm_synth_to_aos(n, *[c.ctypes.data for c in host], stage.ctypes.data)
+            rows_t = torch.from_numpy(stage).to(f"cuda:{local}")
+            del stage
+            torch.cuda.synchronize()
+            a_ms, _, a_res, a_per = timed(FlowRecords(rows_t), 20)
+            assert np.array_equal(a_res.table, res.table), "AoS and SoA results differ"
+            sec["aos_device"] = {
+                "value": total * 20 / (a_ms / 1e3), "unit": "records/s", "ms_per_step": a_ms / 20,
+                "k2_ms": a_per["k2"], "k2_kernel": "k2_aos",
+                "k2_frac_of_hbm_physical": n * 64 / (a_per["k2"] / 1e3) / 1e9 / peak,
+                "source": "64-byte FlowRecord rows resident in HBM (gnm_analyze_aos), 20 steps"}
+            del rows_t
+            torch.cuda.empty_cache()
+            eng.set_hosts(True)
+            h_ms, _, h_res, h_per = timed(dev_batch, 10)
+            eng.set_hosts(False)
+            assert np.array_equal(h_res.table, res.table), "hosts-mode site rows differ"
+            sec["hosts_device"] = {
+                "value": total * 10 / (h_ms / 1e3), "unit": "records/s", "ms_per_step": h_ms / 10,
+                "host_rows": len(h_res.host_table), "k2_ms": h_per["k2"],
+                "source": "per-host rows (SiteResult::hosts) built every step, SoA in HBM, 10 steps"}
+        except Exception as e:  # a secondary leg never voids the headline
+            sec["error"] = repr(e)[:300]
+        line["secondary"] = sec
     if rank == 0 and world == 1 and not args.no_adapter and args.workload in ("D1", "D3"):
         # The reference's own call, flowmon::aggregate from a pageable
         # std::vector<FlowRecord>, served by the C++ adapter: the full
@@ -610,7 +644,12 @@ def main():
         exe = os.path.join(ROOT, "integration", "_build", "adapter_bench")
         if os.path.exists(exe):
             eng.close()
+            host_t = host = host_batch = dev_batch = dev_t = srcs = flat = None  # noqa: F841 (release pinned inputs)
+            import gc
+            gc.collect()
             torch.cuda.empty_cache()
+            if hasattr(torch._C, "_host_emptyCache"):  # give the pinned host cache back first
+                torch._C._host_emptyCache()
             out = subprocess.run([exe, "--workload", args.workload, "--records", str(n), "--steps", "3",
                                   "--warmup", "1"], capture_output=True, text=True, timeout=900)
             lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
@@ -623,16 +662,16 @@ def main():
                 line["e2e"]["adapter"] = {"value": None, "error": (out.stderr or out.stdout)[-300:]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            reps = 3
-            t = time_reference(w, args.cpu_sample, reps)
-            best = min(t, key=t.get)
+            eng.close()
+            R, cat_r, rec, m, best, probe = reference_plan(w, n, 3, 30.0, probe_records=min(args.cpu_sample * 5 // 2, n))
+            ts = [R.time_range(rec, cat_r, 0, m, best) for _ in range(3)]
             line["cpu_baseline"] = {
-                "value": args.cpu_sample / (t[best] / 1e3), "unit": "records/s", "cores": best,
+                "value": m / (statistics.median(ts) / 1e3), "unit": "records/s", "cores": best,
                 "kind": "reference",
-                "sample": f"first {args.cpu_sample} records of {w.name}, unmodified flowmon::aggregate "
-                          f"(oracle/_ref, -O3), median of {reps}; ms by workers "
-                          f"{json.dumps({str(k): round(v, 1) for k, v in t.items()})}; "
-                          f"nproc={os.cpu_count()}, cpu={cpu_model()}"}
+                "sample": f"first {m} records of {w.name}, unmodified flowmon::aggregate (oracle/_ref, -O3), "
+                          f"median of 3 at workers={best}; probe ms by workers on {min(args.cpu_sample * 5 // 2, n)} records "
+                          f"{json.dumps({str(k): round(v, 1) for k, v in probe.items()})}; "
+                          f"nproc={os.cpu_count()}, cpu={cpu_model()}; the --impl reference arm times larger samples"}
         except ImportError as e:
             line["cpu_baseline"] = {"value": None, "unit": "records/s", "cores": 0,
                                     "kind": "reference", "sample": f"unavailable: {e}"}

@@ -72,4 +72,4 @@ def test_reference_arm_maps_no_product_library(ref):
     assert not any("libgnetmon" in m for m in maps), maps
     assert any(m.endswith("oracle/_ref/libflowmon_ref.so") for m in maps), maps
     assert line["config"]["records_per_gpu"] == 300000
-    assert "first" in line["cpu_baseline"]["sample"]
+    assert "each step" in line["cpu_baseline"]["sample"]
