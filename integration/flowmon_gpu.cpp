@@ -24,10 +24,13 @@
 // sum_ubps_, min_bps_, max_bps_ and buckets_ then equal the GPU's exact
 // integers and doubles field for field.
 #include <atomic>
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <stdexcept>
@@ -67,6 +70,7 @@ struct Engine {
     // and sites, compared on every call (a rebuild only on change)
     std::vector<std::pair<std::uint32_t, SiteId>> entries;
     std::size_t n_sites = 0;
+    std::vector<std::uint32_t> ent_r, ent_b, ent_c; // host histogram entries (reused)
 
     Engine() {
         if (const char* spec = std::getenv("GNM_ADAPTER_DEVICES")) {
@@ -134,6 +138,19 @@ Engine& engine() {
     return e;
 }
 
+// GNM_ADAPTER_PROFILE=1: per-call phase times on stderr (diagnosis only).
+struct PhaseClock {
+    bool on = std::getenv("GNM_ADAPTER_PROFILE") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[adapter] %-22s %8.2f ms\n", what,
+                     std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
 struct BucketCount {
     std::uint32_t bucket;
     std::uint32_t count;
@@ -194,7 +211,7 @@ u128 join(std::uint64_t lo, std::uint64_t hi) { return static_cast<u128>(hi) << 
 
 // The GPU's finalize (site rows, tallies, per-host rows and their sparse
 // histograms) -> AnalysisResult, in the reference's map order.
-AnalysisResult collect(Engine& e, const gnm_result& r, const std::vector<gnm_site_stats>& rows) {
+AnalysisResult collect(Engine& e, const gnm_result& r, const std::vector<gnm_site_stats>& rows, PhaseClock& clk) {
     AnalysisResult out;
     out.window_start_ms = r.window_start_ms;
     out.window_end_ms = r.window_end_ms;
@@ -207,9 +224,19 @@ AnalysisResult collect(Engine& e, const gnm_result& r, const std::vector<gnm_sit
     std::vector<gnm_host_stats> hosts(nh);
     if (nh) check(gnm_host_results(e.ctx, hosts.data(), nh, nullptr), "gnm_host_results");
     std::uint64_t ne = 0;
+    clk.mark("host rows");
     check(e.host_entries(nullptr, nullptr, nullptr, 0, &ne), "host histogram entries");
-    std::vector<std::uint32_t> er(ne), eb(ne), ec(ne);
-    if (ne) check(e.host_entries(er.data(), eb.data(), ec.data(), ne, &ne), "host histogram entries");
+    clk.mark("entries: sort + count");
+    // The engine's entry buffers persist across calls (grown, never shrunk):
+    // a fresh 100+ MB allocation per call would page-fault on first touch.
+    if (e.ent_r.size() < ne) {
+        e.ent_r.resize(ne);
+        e.ent_b.resize(ne);
+        e.ent_c.resize(ne);
+    }
+    std::uint32_t *er = e.ent_r.data(), *eb = e.ent_b.data(), *ec = e.ent_c.data();
+    if (ne) check(e.host_entries(er, eb, ec, ne, &ne), "host histogram entries");
+    clk.mark("entries: export");
 
     // Host rows arrive in (site, host) order: one group of rows per present
     // site. Groups (and their histogram entries) are independent, so they
@@ -284,8 +311,10 @@ AnalysisResult collect(Engine& e, const gnm_result& r, const std::vector<gnm_sit
         for (auto& ep : errs)
             if (ep) std::rethrow_exception(ep);
     }
+    clk.mark("rebuild histograms");
     for (std::size_t gi = 0; gi < groups.size(); ++gi)
         out.sites.emplace_hint(out.sites.end(), groups[gi].site, std::move(built[gi]));
+    clk.mark("maps");
     std::uint64_t present = 0;
     for (const gnm_site_stats& g : rows) present += g.flow_count != 0;
     if (present != groups.size()) throw std::runtime_error("flowmon GPU adapter: site without host rows");
@@ -300,8 +329,10 @@ AnalysisResult run_gpu(std::span<const FlowRecord> view, const SiteCatalog& cata
                        const std::vector<std::size_t>& boundaries, std::uint64_t window_start_ms,
                        std::uint64_t window_end_ms) {
     static_assert(sizeof(FlowRecord) == GNM_FLOW_RECORD_BYTES, "FlowRecord is the 64-byte gnm_batch_aos row");
+    PhaseClock clk;
     Engine& e = engine();
     e.sync(catalog);
+    clk.mark("registry");
     const gnm_filter_params p{params.ack_avg_size_max, params.min_packets, params.min_duration_ms,
                               params.workers};
     std::vector<gnm_site_stats> rows(e.n_sites);
@@ -319,7 +350,8 @@ AnalysisResult run_gpu(std::span<const FlowRecord> view, const SiteCatalog& cata
             if (b > view.size()) throw std::out_of_range("aggregate_partitioned: boundary past the view");
         const gnm_batch_aos b{view.data(), view.size(), GNM_MEM_HOST};
         check(gnm_group_analyze_aos(e.group, e.reg, &p, &b, &r), "gnm_group_analyze_aos");
-        return collect(e, r, rows);
+        clk.mark("gpu (group)");
+        return collect(e, r, rows, clk);
     }
     std::size_t prev = 0;
     auto slice = [&](std::size_t end) {
@@ -336,8 +368,10 @@ AnalysisResult run_gpu(std::span<const FlowRecord> view, const SiteCatalog& cata
     };
     for (std::size_t b : boundaries) slice(b);
     slice(view.size());
+    clk.mark("accumulate (H2D+K2)");
     check(gnm_finalize(e.ctx, e.reg, &r), "gnm_finalize");
-    return collect(e, r, rows);
+    clk.mark("finalize (K3+hosts)");
+    return collect(e, r, rows, clk);
 }
 
 } // namespace

@@ -547,6 +547,41 @@ void staged_copy(const std::vector<CopySeg>& segs) {
     for (auto& x : th) x.join();
 }
 
+// Large device -> pageable host copies (the per-host histogram entries can
+// be hundreds of MB): through the two pinned staging slots, each chunk's
+// host copy (several threads) overlapping the next chunk's DMA. Small or
+// pinned destinations go directly.
+void d2h_large(gnm_ctx* c, void* dst, const void* src, size_t bytes) {
+    constexpr size_t kChunk = 32u << 20;
+    if (bytes < 2 * kChunk || is_pinned(dst)) {
+        if (bytes) ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream), "cudaMemcpyAsync(D2H)");
+        ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+        return;
+    }
+    ensure_stage(c, std::max<size_t>(c->stage_bytes, kChunk), true);
+    const size_t chunk = std::min(c->h_stage_bytes, c->stage_bytes);
+    cudaEvent_t done[2] = {c->ev_h2d[0], c->ev_h2d[1]}; // idle outside the loader
+    auto* d = static_cast<unsigned char*>(dst);
+    const auto* sp = static_cast<const unsigned char*>(src);
+    size_t pending_off = 0, pending_len = 0;
+    int pending_slot = -1;
+    for (size_t off = 0, k = 0; off < bytes; off += chunk, ++k) {
+        const int slot = static_cast<int>(k & 1);
+        const size_t len = std::min(chunk, bytes - off);
+        ck(cudaMemcpyAsync(c->h_stage[slot], sp + off, len, cudaMemcpyDeviceToHost, c->stream), "D2H chunk");
+        ck(cudaEventRecord(done[slot], c->stream), "cudaEventRecord");
+        if (pending_slot >= 0) { // drain the previous chunk while this one is in flight
+            ck(cudaEventSynchronize(done[pending_slot]), "cudaEventSynchronize");
+            staged_copy({{d + pending_off, c->h_stage[pending_slot], pending_len}});
+        }
+        pending_slot = slot;
+        pending_off = off;
+        pending_len = len;
+    }
+    ck(cudaEventSynchronize(done[pending_slot]), "cudaEventSynchronize");
+    staged_copy({{d + pending_off, c->h_stage[pending_slot], pending_len}});
+}
+
 void load_and_run(gnm_ctx* c, bool aos, const void* const* cols, const size_t* widths, int ncols,
                   uint64_t n, const gnm::DevParams& p, bool archive = false) {
     size_t rec_bytes = 0;
@@ -1123,9 +1158,9 @@ int gnm_host_histogram_entries(gnm_ctx* c, uint32_t* rows, uint32_t* buckets, ui
         ck(cudaMallocAsync(reinterpret_cast<void**>(&d), n * 12, c->stream), "cudaMallocAsync(host entries)");
         ck(gnm::hosts_sparse_export(c->device, c->hrows, d, d + n, d + 2 * n, c->stream), "host entries export");
         c->kernel_launches += 1;
-        ck(cudaMemcpyAsync(rows, d, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H rows");
-        ck(cudaMemcpyAsync(buckets, d + n, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H buckets");
-        ck(cudaMemcpyAsync(counts, d + 2 * n, n * 4, cudaMemcpyDeviceToHost, c->stream), "D2H counts");
+        d2h_large(c, rows, d, n * 4);
+        d2h_large(c, buckets, d + n, n * 4);
+        d2h_large(c, counts, d + 2 * n, n * 4);
         ck(cudaFreeAsync(d, c->stream), "cudaFreeAsync(host entries)");
         ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
         return static_cast<int>(GNM_OK);
