@@ -1234,11 +1234,14 @@ __global__ void __launch_bounds__(512, 2) k2b_fine(DevPartials P, DevLog L) {
             msb = m & 0xFFu;
             hh = (m >> 8) == kHeavyNone ? 0xFFu : m >> 8;
         }
-        if ((bk >> 6) != msb) return;
-        if (hh != 0xFFu)
-            asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hf_base + (hh * kFineW + (bk & 63u)) * 4) : "memory");
-        else
-            red_add(P.fine + static_cast<size_t>(site) * kFineW + (bk & 63u), 1u);
+        // branch-free: both addresses computed, the two reductions predicated
+        const uint32_t hit = (bk >> 6) == msb;
+        const uint32_t heavy = hit & (hh != 0xFFu), light = hit & (hh == 0xFFu);
+        const uint32_t sa = hf_base + ((hh & 0xFFu) * kFineW + (bk & 63u)) * 4;
+        unsigned int* ga = P.fine + static_cast<size_t>(site) * kFineW + (bk & 63u);
+        asm volatile("{\n\t.reg .pred ph, pl;\n\tsetp.ne.u32 ph, %2, 0;\n\tsetp.ne.u32 pl, %3, 0;\n\t"
+                     "@ph red.shared.add.u32 [%0], 1;\n\t@pl red.relaxed.gpu.global.add.u32 [%1], 1;\n\t}"
+                     ::"r"(sa), "l"(ga), "r"(heavy), "r"(light) : "memory");
     };
     for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < items; w += nwarps) {
         const uint32_t r = w / chunks;
