@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define GNM_ABI_VERSION 3
+#define GNM_ABI_VERSION 4
 
 /* rate_engine.hpp:18-20 */
 #define GNM_BUCKET_COUNT 10001

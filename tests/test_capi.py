@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version_and_defaults():
-    assert _lib.lib.gnm_abi_version() == 3
+    assert _lib.lib.gnm_abi_version() == 4
     p = _lib.gnm_filter_params()
     _lib.lib.gnm_filter_params_default(C.byref(p))
     assert (p.ack_avg_size_max, p.min_packets, p.min_duration_ms, p.workers) == (96, 20, 100, 1)
@@ -130,3 +130,27 @@ def test_warning_rule_matches_oracle_random(orc):
                                                     streak))[0].tolist())
         assert got == want
         assert [st.streak(s) for s in range(n)] == streak.tolist()
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")
+def test_multi_gpu_group_fails_loudly_without_devices():
+    """gnm_group_create (one context per device + a communicator clique)
+    reports the missing device instead of falling back to the CPU."""
+    from paper_1108_1785_b200 import Group
+    for kind in ("nccl", "loopback"):
+        with pytest.raises(GnmError) as e:
+            Group([0, 0], kind=kind)
+        assert e.value.status == _lib.ERR_NO_DEVICE
+
+
+def test_multi_gpu_argument_validation():
+    L = _lib.lib
+    h = C.c_void_p()
+    devs = (C.c_int * 2)(0, 0)
+    assert L.gnm_group_create(devs, 0, _lib.GROUP_NCCL, C.byref(h)) == _lib.ERR_INVALID_ARGUMENT
+    assert L.gnm_group_create(devs, 2, 7, C.byref(h)) == _lib.ERR_INVALID_ARGUMENT
+    assert L.gnm_group_size(None) == 0 and L.gnm_group_ctx(None, 0) is None
+    assert L.gnm_group_host_count(None) == 0
+    assert L.gnm_ctx_comm_size(None) == 1
+    assert L.gnm_ctx_comm_init(None, 1, 0, None) == _lib.ERR_INVALID_ARGUMENT
+    assert L.gnm_group_analyze(None, None, None, None, None) == _lib.ERR_INVALID_ARGUMENT
