@@ -796,6 +796,41 @@ __device__ __forceinline__ ulonglong2 ld_rec_u64x2(const void* p, uint64_t pol) 
     return r;
 }
 
+// FLOWARC1 entries (layout 4) are only 4-byte aligned and big-endian: the
+// tile keeps the 8 raw words of each of its two records and swaps them only
+// when the tile is processed, so the loads stay in flight a whole round.
+struct TileRaw4 {
+    uint32_t x[8], y[8]; // be64 start, be64 end, src, dst, pkts, octets
+};
+template <int kLayout>
+struct TileOf {
+    using type = TileRegs;
+};
+template <>
+struct TileOf<4> {
+    using type = TileRaw4;
+};
+
+__device__ __forceinline__ uint64_t be64(uint32_t hi_word, uint32_t lo_word) {
+    return static_cast<uint64_t>(__byte_perm(hi_word, 0, 0x0123)) << 32 | __byte_perm(lo_word, 0, 0x0123);
+}
+
+template <int kLayout>
+__device__ __forceinline__ TileRegs unpack_tile(const typename TileOf<kLayout>::type& t) {
+    if constexpr (kLayout == 4) {
+        TileRegs r;
+        r.ts = make_ulonglong2(be64(t.x[0], t.x[1]), be64(t.y[0], t.y[1]));
+        r.te = make_ulonglong2(be64(t.x[2], t.x[3]), be64(t.y[2], t.y[3]));
+        r.s = make_uint2(__byte_perm(t.x[4], 0, 0x0123), __byte_perm(t.y[4], 0, 0x0123));
+        r.d = make_uint2(__byte_perm(t.x[5], 0, 0x0123), __byte_perm(t.y[5], 0, 0x0123));
+        r.k = make_uint2(__byte_perm(t.x[6], 0, 0x0123), __byte_perm(t.y[6], 0, 0x0123));
+        r.o = make_uint2(__byte_perm(t.x[7], 0, 0x0123), __byte_perm(t.y[7], 0, 0x0123));
+        return r;
+    } else {
+        return t;
+    }
+}
+
 // Tile loads. kLayout 0 (aligned SoA): lane takes records 2*lane, 2*lane+1
 // of the tile (one LDG.64 per u32 column, one LDG.128 per u64 column,
 // non-allocating). kLayout 2 (16-byte aligned AoS, the reference's 64-byte
@@ -803,8 +838,21 @@ __device__ __forceinline__ ulonglong2 ld_rec_u64x2(const void* p, uint64_t pol) 
 // each (src/dst, pkts/octets, start/end).
 template <int kLayout>
 __device__ __forceinline__ void load_tile(const DevBatch& b, uint32_t tile, uint32_t lane, uint64_t pol,
-                                          TileRegs& t) {
-    if constexpr (kLayout == 0) {
+                                          typename TileOf<kLayout>::type& t) {
+    if constexpr (kLayout == 4) {
+        // entry words at 0,4 (start) 8,12 (end) 16 (src) 20 (dst) 32 (pkts)
+        // 36 (octets) of the 64-byte entry (flow_store.cpp:158-162, netflow.cpp:52-75)
+        const uint32_t* wx = reinterpret_cast<const uint32_t*>(static_cast<const unsigned char*>(b.rec) +
+                                                                (static_cast<size_t>(tile) * 64u + lane) * 64u);
+        const uint32_t* wy = wx + 32u * 16u;
+        constexpr int kWord[8] = {0, 1, 2, 3, 4, 5, 8, 9};
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            t.x[q] = __ldg(wx + kWord[q]);
+            t.y[q] = __ldg(wy + kWord[q]);
+        }
+        (void)pol;
+    } else if constexpr (kLayout == 0) {
         const DevSoA& c = b.soa;
         const uint32_t g = tile * 32u + lane;
         t.s = ld_stream_u2(reinterpret_cast<const uint2*>(c.src) + g, pol);
@@ -853,13 +901,14 @@ __device__ __forceinline__ void k2_tiles(const DevBatch& b, const uint32_t* __re
     Ctr t;
     const uint64_t pol = evict_first_policy();
     uint32_t tile = t0 + warp;
-    TileRegs cur;
-    if (tile < t_end) load_tile<kLayout>(b, tile, lane, pol, cur);
+    typename TileOf<kLayout>::type raw;
+    if (tile < t_end) load_tile<kLayout>(b, tile, lane, pol, raw);
     for (uint32_t r = 0; r < rounds; ++r) {
         const uint32_t next = tile + kWarps;
-        TileRegs nx;
+        typename TileOf<kLayout>::type nx;
         if (next < t_end) load_tile<kLayout>(b, next, lane, pol, nx);
         if (tile < t_end) {
+            const TileRegs cur = unpack_tile<kLayout>(raw);
             const uint64_t dx = cur.te.x - cur.ts.x, dy = cur.te.y - cur.ts.y;
             uint32_t hx, hy;
             const uint32_t cx = stage_a<kSmem>(cur.s.x, cur.d.x, cur.k.x, cur.o.x, dx, p, gt, t, hx,
@@ -870,7 +919,7 @@ __device__ __forceinline__ void k2_tiles(const DevBatch& b, const uint32_t* __re
             push<kHosts>(cy, cur.o.y, dy, wq, lane, hy);
             drain_full<kSmem, kHot, kHosts>(wq, lane, gt, p, P, h, t, L);
         }
-        cur = nx;
+        raw = nx;
         tile = next;
         if constexpr (kHot) {
             if ((r + 1) % kEpochRounds == 0 && r + 1 < rounds) {
@@ -881,7 +930,8 @@ __device__ __forceinline__ void k2_tiles(const DevBatch& b, const uint32_t* __re
         }
     }
     if (blockIdx.x == gridDim.x - 1 && warp == 0)
-        run_scalar<kLayout == 0 ? 1 : 2, kSmem, kHot, kMode>(b, tiles << 6, b.n, 32, lane, gt, p, P, h, t, wq, L);
+        run_scalar<kLayout == 0 ? 1 : kLayout, kSmem, kHot, kMode>(b, tiles << 6, b.n, 32, lane, gt, p, P, h, t, wq,
+                                                                  L);
     k2_epilogue<kSmem, kHot, kHosts>(t, wq, lane, gt, p, P, h, hot, L);
 }
 
@@ -897,6 +947,14 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_aos(DevBatch b, const uint32_t
                                                     uint32_t table_words, DevParams p,
                                                     DevPartials P, DevHot hot, DevLog L) {
     k2_tiles<2, kSmem, kHot, kMode>(b, gt, table_words, p, P, hot, L);
+}
+
+// FLOWARC1 entries read in place (the archive's big-endian rows).
+template <bool kSmem, bool kHot, int kMode>
+__global__ void __launch_bounds__(kK2Block, 1) k2_arc(DevBatch b, const uint32_t* __restrict__ gt,
+                                                    uint32_t table_words, DevParams p,
+                                                    DevPartials P, DevHot hot, DevLog L) {
+    k2_tiles<4, kSmem, kHot, kMode>(b, gt, table_words, p, P, hot, L);
 }
 
 // Other layouts: unaligned SoA (1), AoS 64-byte rows with vector (2) or
@@ -1406,6 +1464,7 @@ template <int L, bool kS, bool kH, int kW>
 constexpr auto k2_kernel() {
     if constexpr (L == 0) return k2_soa<kS, kH, kW>;
     else if constexpr (L == 2) return k2_aos<kS, kH, kW>;
+    else if constexpr (L == 4) return k2_arc<kS, kH, kW>;
     else return k2_gen<L, kS, kH, kW>;
 }
 
@@ -1498,7 +1557,7 @@ LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool ho
     const uint64_t per_block = static_cast<uint64_t>(c.block) * 16;
     const uint64_t want = (b.n + per_block - 1) / per_block;
     uint64_t grid;
-    if (k2_layout(b) == 0 || k2_layout(b) == 2) {
+    if (k2_layout(b) == 0 || k2_layout(b) == 2 || k2_layout(b) == 4) {
         grid = std::min(sms, want); // persistent, one CTA per SM
     } else {
         // k2_gen: < 2^16 records per CTA (the hot limbs' bound); beyond one
