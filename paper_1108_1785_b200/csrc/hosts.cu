@@ -98,8 +98,11 @@ __device__ __forceinline__ uint32_t insert_key(unsigned long long* keys, uint32_
 constexpr uint32_t kInsBlock = 256;
 constexpr uint32_t kAgg = 2048;
 constexpr size_t kInsSmem = kAgg * (4 + 4 + 3 * 4 + 4); // 40 KB
-constexpr uint32_t kInsChunk = 2048;
-constexpr uint32_t kInsItemsPerCta = 31; // 31 * 2048 < 2^16
+#ifndef GNM_INS_CHUNK
+#define GNM_INS_CHUNK 512
+#endif
+constexpr uint32_t kInsChunk = GNM_INS_CHUNK;
+constexpr uint32_t kInsItemsPerCta = 65535u / kInsChunk; // items * chunk < 2^16 adds per limb
 
 __device__ __forceinline__ void red_u64(unsigned long long* p, unsigned long long v) {
     asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
