@@ -45,8 +45,15 @@ __device__ __forceinline__ uint32_t wrap_diff(uint32_t a, uint32_t b) {
 __device__ __forceinline__ uint32_t check_header(const uint8_t* p, uint64_t len, uint32_t& count) {
     count = 0;
     if (len < kHdr) return 2;
-    const uint32_t version = be16(p);
-    count = be16(p + 2);
+    uint32_t version;
+    if ((reinterpret_cast<uintptr_t>(p) & 3u) == 0) { // one word load instead of four byte loads
+        const uint32_t w = __byte_perm(__ldg(reinterpret_cast<const uint32_t*>(p)), 0, 0x0123);
+        version = w >> 16;
+        count = w & 0xFFFFu;
+    } else {
+        version = be16(p);
+        count = be16(p + 2);
+    }
     if (version != 5) return 1;
     if (count == 0 || count > kMaxRec) return 3;
     if (len != kHdr + static_cast<uint64_t>(kRec) * count) return 2;
@@ -81,7 +88,14 @@ __device__ __forceinline__ void load_raw_bytes(const uint8_t* q, uint4& w0, uint
 // word loads (13-word record stride: conflict-free), others use byte loads;
 // decode (byte permutes), resolve_times, accepted rows staged in shared
 // memory and written with coalesced 16-byte stores at their final offsets.
-constexpr uint32_t kNfWarps = 8, kNfPerWarp = 4, kNfTile = kNfWarps * kNfPerWarp; // 32 datagrams (<= 32)
+#ifndef GNM_NF_PER_WARP
+#define GNM_NF_PER_WARP 4
+#endif
+// kNfTile datagrams per tile, a multiple of 32 (warp 0 scans kNfPer per lane):
+// bigger tiles amortise the look-back's CTA-wide barrier over more datagrams.
+constexpr uint32_t kNfWarps = 8, kNfPerWarp = GNM_NF_PER_WARP, kNfTile = kNfWarps * kNfPerWarp;
+constexpr uint32_t kNfPer = kNfTile / 32;
+static_assert(kNfTile % 32 == 0, "tile = whole warps of datagrams");
 constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagPrefix = 2ull << 62, kValMask = (1ull << 62) - 1;
 
 __global__ void __launch_bounds__(kNfWarps * 32) nf_decode(const uint8_t* __restrict__ d,
@@ -138,14 +152,20 @@ __global__ void __launch_bounds__(kNfWarps * 32) nf_decode(const uint8_t* __rest
         }
         __syncthreads();
         if (warp == 0) {
-            const uint32_t v = lane < kNfTile ? s_cnt[lane] : 0u;
+            // lane l owns datagrams [l*kNfPer, (l+1)*kNfPer) of the tile
+            uint32_t vv[kNfPer], v = 0;
+#pragma unroll
+            for (uint32_t q = 0; q < kNfPer; ++q) {
+                vv[q] = s_cnt[lane * kNfPer + q];
+                v += vv[q];
+            }
             uint32_t incl = v;
 #pragma unroll
             for (uint32_t o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
                 if (lane >= o) incl += y;
             }
-            const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31); // lanes >= kNfTile add 0
+            const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
             unsigned long long prefix = 0;
             if (lane == 0) {
                 if (tile == 0) {
@@ -164,7 +184,12 @@ __global__ void __launch_bounds__(kNfWarps * 32) nf_decode(const uint8_t* __rest
                 }
             }
             prefix = __shfl_sync(0xFFFFFFFFu, prefix, 0);
-            if (lane < kNfTile) s_base[lane] = prefix + incl - v;
+            unsigned long long b = prefix + incl - v;
+#pragma unroll
+            for (uint32_t q = 0; q < kNfPer; ++q) {
+                s_base[lane * kNfPer + q] = b;
+                b += vv[q];
+            }
         }
         __syncthreads();
         for (uint32_t k = 0; k < kNfPerWarp; ++k) {
@@ -174,15 +199,30 @@ __global__ void __launch_bounds__(kNfWarps * 32) nf_decode(const uint8_t* __rest
             const uint8_t* p = d + off[i];
             uint32_t count;
             if (check_header(p, off[i + 1] - off[i], count) != 0) continue; // warp-uniform
-            const uint32_t uptime = be32(p + 4), secs = be32(p + 8), nsecs = be32(p + 12);
-            const uint64_t wall = static_cast<uint64_t>(secs) * 1000u + nsecs / 1000000u;
             const bool words = (reinterpret_cast<uintptr_t>(p) & 3u) == 0; // warp-uniform
+            uint32_t uptime, secs, nsecs;
+            if (words) {
+                const uint32_t* h = reinterpret_cast<const uint32_t*>(p);
+                uptime = __byte_perm(__ldg(h + 1), 0, 0x0123);
+                secs = __byte_perm(__ldg(h + 2), 0, 0x0123);
+                nsecs = __byte_perm(__ldg(h + 3), 0, 0x0123);
+            } else {
+                uptime = be32(p + 4), secs = be32(p + 8), nsecs = be32(p + 12);
+            }
+            const uint64_t wall = static_cast<uint64_t>(secs) * 1000u + nsecs / 1000000u;
             uint32_t* recw = s_rec[warp];
             if (words) { // coalesced word loads of the record area (an L2 hit) into a padded tile
                 const uint32_t* src = reinterpret_cast<const uint32_t*>(p + kHdr);
+                // word idx = 12 r + c; each step of 32 words is r += 2, c += 8
+                uint32_t r = lane / 12, c = lane - r * 12;
                 for (uint32_t idx = lane; idx < count * 12; idx += 32) {
-                    const uint32_t r = idx / 12;
-                    recw[r * 13 + (idx - r * 12)] = __ldg(src + idx);
+                    recw[r * 13 + c] = __ldg(src + idx);
+                    r += 2;
+                    c += 8;
+                    if (c >= 12) {
+                        c -= 12;
+                        ++r;
+                    }
                 }
                 __syncwarp();
             }
