@@ -8,8 +8,10 @@
 //
 //   adapter_parity RECORDS CATALOG [--workers W] [--cpu-workers W] [--partitions K]
 //                  [--params ACK,PKTS,DUR] [--window S,E] [--repeat R] [--seed S]
+//   adapter_parity --workload D1|D3 [--records N] [options]
 //
-// RECORDS: raw 64-byte FlowRecord rows; CATALOG: SiteCatalog::load text.
+// RECORDS: raw 64-byte FlowRecord rows; CATALOG: SiteCatalog::load text; or
+// a bench workload generated in process (workload_gen.hpp).
 // Prints one JSON line; exit status 0 iff every comparison held.
 #include <algorithm>
 #include <chrono>
@@ -24,6 +26,7 @@
 
 #include "flowmon/rate_engine.hpp"
 #include "flowmon/site_catalog.hpp"
+#include "workload_gen.hpp"
 
 namespace flowmon {
 // the reference's own aggregate, renamed at compile time (integration/Makefile)
@@ -91,6 +94,7 @@ int main(int argc, char** argv) {
         return 2;
     }
     unsigned workers = 1, cpu_workers = 1;
+    std::uint64_t gen_records = 0;
     int partitions = 0, repeat = 1;
     std::uint64_t ws = 0, we = 0, seed = 1;
     FilterParams params;
@@ -101,6 +105,7 @@ int main(int argc, char** argv) {
         else if (k == "--partitions") partitions = std::stoi(v);
         else if (k == "--repeat") repeat = std::max(1, std::stoi(v));
         else if (k == "--seed") seed = std::stoull(v);
+        else if (k == "--records") gen_records = std::stoull(v);
         else if (k == "--window") std::sscanf(v.c_str(), "%lu,%lu", &ws, &we);
         else if (k == "--params")
             std::sscanf(v.c_str(), "%u,%u,%u", &params.ack_avg_size_max, &params.min_packets,
@@ -111,16 +116,26 @@ int main(int argc, char** argv) {
         }
     }
 
-    std::ifstream f(argv[1], std::ios::binary | std::ios::ate);
-    if (!f) {
-        std::fprintf(stderr, "cannot open %s\n", argv[1]);
-        return 2;
+    std::vector<FlowRecord> records;
+    SiteCatalog catalog;
+    if (std::string(argv[1]) == "--workload") {
+        if (!gnm_workload::make(argv[2], gen_records, records, catalog)) {
+            std::fprintf(stderr, "unknown workload %s\n", argv[2]);
+            return 2;
+        }
+    } else {
+        std::ifstream f(argv[1], std::ios::binary | std::ios::ate);
+        if (!f) {
+            std::fprintf(stderr, "cannot open %s\n", argv[1]);
+            return 2;
+        }
+        const std::size_t bytes = static_cast<std::size_t>(f.tellg());
+        records.resize(bytes / sizeof(FlowRecord));
+        f.seekg(0);
+        f.read(reinterpret_cast<char*>(records.data()),
+               static_cast<std::streamsize>(records.size() * sizeof(FlowRecord)));
+        catalog = SiteCatalog::load_file(argv[2]);
     }
-    const std::size_t bytes = static_cast<std::size_t>(f.tellg());
-    std::vector<FlowRecord> records(bytes / sizeof(FlowRecord));
-    f.seekg(0);
-    f.read(reinterpret_cast<char*>(records.data()), static_cast<std::streamsize>(records.size() * sizeof(FlowRecord)));
-    const SiteCatalog catalog = SiteCatalog::load_file(argv[2]);
     const std::span<const FlowRecord> view(records);
 
     // GPU through the adapter: the first call builds and uploads the registry;

@@ -179,3 +179,15 @@ def test_adapter_multi_gpu_group_equals_reference(tmp_path, devices):
     out = _run([_bin("adapter_parity"), rec, cat, "--partitions", "2"], env=env)
     d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
     assert out.returncode == 0 and d["equal"], d
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_adapter_equals_reference_d3_full_size():
+    """All 100M records of D3 (BASELINE configs[2]), generated in the driver:
+    the adapter's full AnalysisResult (10k sites, 80k hosts, every
+    histogram) == the unmodified reference's on the same records."""
+    out = _run([_bin("adapter_parity"), "--workload", "D3", "--cpu-workers", "1"], timeout=1800)
+    d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert out.returncode == 0 and d["equal"], d
+    assert d["records"] == 100_000_000 and d["sites"] == 10_000 and d["host_rows"] == 80_000
