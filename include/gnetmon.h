@@ -373,7 +373,10 @@ gnm_ctx* gnm_group_ctx(gnm_group* group, int rank);
 /* aggregate over the group's GPUs: shard i of the batch to rank i, every
  * rank accumulates its shard and finalizes with the combine (one host
  * thread per rank); `result` receives the global rows. Host or device
- * batches (device batches must be readable from every rank's GPU). */
+ * batches (device batches must be readable from every rank's GPU). If a
+ * rank fails, the group's communicators are aborted (no rank is left
+ * blocked in a collective), the root cause is returned, and later calls on
+ * the group fail with GNM_ERR_COMM. */
 int gnm_group_analyze(gnm_group* group, const gnm_registry* reg, const gnm_filter_params* params,
                       const gnm_batch_soa* batch, gnm_result* result);
 int gnm_group_analyze_aos(gnm_group* group, const gnm_registry* reg, const gnm_filter_params* params,

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -1809,6 +1810,7 @@ int gnm_ctx_comm_size(gnm_ctx* c) { return c && c->comm ? c->comm->nranks() : 1;
 struct gnm_group {
     std::vector<gnm_ctx*> ctx;
     int kind = GNM_GROUP_NCCL;
+    bool broken = false; // a rank failed and the communicators were aborted
 };
 
 namespace {
@@ -1821,13 +1823,24 @@ int on_every_rank(gnm_group* g, F&& work) {
     const int n = static_cast<int>(g->ctx.size());
     std::vector<int> st(n, GNM_OK);
     std::vector<std::string> msg(n);
+    std::atomic<int> first_fail{-1}; // the root cause, not the ranks it aborted
     auto body = [&](int i) {
         st[i] = guarded([&] {
             ck(cudaSetDevice(g->ctx[i]->device), "cudaSetDevice");
             return work(i, g->ctx[i]);
         });
-        if (st[i] != GNM_OK) msg[i] = g_last_error;
+        if (st[i] != GNM_OK) {
+            msg[i] = g_last_error;
+            int none = -1;
+            first_fail.compare_exchange_strong(none, i);
+            // the other ranks may be blocked in (or about to enter) a
+            // collective this rank will never join: abort the clique
+            for (gnm_ctx* c : g->ctx)
+                if (c->comm) c->comm->abort();
+            g->broken = true;
+        }
     };
+    if (g->broken) return fail(GNM_ERR_COMM, "the group's communicators were aborted by an earlier failure");
     if (n == 1) {
         body(0);
     } else {
@@ -1835,8 +1848,7 @@ int on_every_rank(gnm_group* g, F&& work) {
         for (int i = 0; i < n; ++i) th.emplace_back(body, i);
         for (auto& t : th) t.join();
     }
-    for (int i = 0; i < n; ++i)
-        if (st[i] != GNM_OK) return fail(st[i], "rank " + std::to_string(i) + ": " + msg[i]);
+    if (const int i = first_fail.load(); i >= 0) return fail(st[i], "rank " + std::to_string(i) + ": " + msg[i]);
     return GNM_OK;
 }
 
@@ -1895,6 +1907,16 @@ int group_analyze(gnm_group* g, const gnm_registry* reg, const gnm_filter_params
         if (e) {
             gnm_reset(c);
             return e;
+        }
+        // test hook: one rank fails between its accumulation and the combine
+        // (the others must not hang in a collective it never joins)
+        static const int fail_rank = [] {
+            const char* v = std::getenv("GNM_TEST_FAIL_RANK");
+            return v ? std::atoi(v) : -1;
+        }();
+        if (i == fail_rank) {
+            gnm_reset(c);
+            return fail(GNM_ERR_INVALID_ARGUMENT, "injected failure (GNM_TEST_FAIL_RANK)");
         }
         e = finalize(c, reg, &res[i]);
         c->discard_hist_out = false;

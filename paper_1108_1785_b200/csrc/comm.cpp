@@ -6,6 +6,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <condition_variable>
 #include <cstring>
 #include <limits>
@@ -22,6 +23,7 @@ struct NcclApi {
     ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
@@ -50,6 +52,7 @@ const NcclApi& nccl() {
         sym(a.CommInitRank, "ncclCommInitRank");
         sym(a.CommInitAll, "ncclCommInitAll");
         sym(a.CommDestroy, "ncclCommDestroy");
+        sym(a.CommAbort, "ncclCommAbort");
         sym(a.AllReduce, "ncclAllReduce");
         sym(a.AllGather, "ncclAllGather");
         sym(a.GroupStart, "ncclGroupStart");
@@ -85,7 +88,10 @@ class NcclComm final : public Comm {
 public:
     NcclComm(ncclComm_t c, int n, int r) : comm_(c), n_(n), r_(r) {}
     ~NcclComm() override {
-        if (comm_) nccl().CommDestroy(comm_);
+        if (ncclComm_t c = comm_.load()) nccl().CommDestroy(c);
+    }
+    void abort() override { // may run on another rank's thread
+        if (ncclComm_t c = comm_.exchange(nullptr)) nccl().CommAbort(c);
     }
     int nranks() const override { return n_; }
     int rank() const override { return r_; }
@@ -93,15 +99,20 @@ public:
     void group_start() override { nck(nccl().GroupStart(), "ncclGroupStart"); }
     void group_end() override { nck(nccl().GroupEnd(), "ncclGroupEnd"); }
     void all_reduce(void* buf, size_t count, DType t, RedOp op, cudaStream_t s) override {
-        nck(nccl().AllReduce(buf, buf, count, nccl_type(t), nccl_op(op), comm_, s), "ncclAllReduce");
+        live();
+        nck(nccl().AllReduce(buf, buf, count, nccl_type(t), nccl_op(op), comm_.load(), s), "ncclAllReduce");
     }
     void all_gather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
-        nck(nccl().AllGather(send, recv, bytes, ncclUint8, comm_, s), "ncclAllGather");
+        live();
+        nck(nccl().AllGather(send, recv, bytes, ncclUint8, comm_.load(), s), "ncclAllGather");
+    }
+    void live() const {
+        if (!comm_) throw CommError("NCCL communicator was aborted");
     }
     bool capturable() const override { return true; }
 
 private:
-    ncclComm_t comm_;
+    std::atomic<ncclComm_t> comm_;
     int n_, r_;
 };
 
@@ -116,16 +127,25 @@ struct LoopShared {
     uint64_t gen = 0;
     std::vector<std::vector<unsigned char>> buf;
 
+    bool poisoned = false; // a rank aborted: every wait fails from now on
+
     void barrier() {
         std::unique_lock<std::mutex> l(m);
+        if (poisoned) throw CommError("loopback group aborted by another rank");
         const uint64_t g = gen;
         if (++arrived == n) {
             arrived = 0;
             ++gen;
             cv.notify_all();
         } else {
-            cv.wait(l, [&] { return gen != g; });
+            cv.wait(l, [&] { return gen != g || poisoned; });
+            if (gen == g) throw CommError("loopback group aborted by another rank");
         }
+    }
+    void poison() {
+        std::lock_guard<std::mutex> l(m);
+        poisoned = true;
+        cv.notify_all();
     }
 };
 
@@ -171,6 +191,7 @@ public:
         stage_out(recv, out, s);
     }
     bool capturable() const override { return false; }
+    void abort() override { S_->poison(); }
 
 private:
     void stage_in(const void* dev, size_t bytes, cudaStream_t s) {

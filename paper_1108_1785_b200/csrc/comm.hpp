@@ -49,6 +49,11 @@ public:
     virtual void all_gather(const void* send, void* recv, size_t bytes, cudaStream_t s) = 0;
     // True when the collectives may be captured into a CUDA graph.
     virtual bool capturable() const = 0;
+    // Abort every pending and future collective of this communicator (and,
+    // for a clique, let the other ranks' waits fail instead of hanging): one
+    // rank of a group failing must not leave the others blocked forever.
+    // The communicator is unusable afterwards.
+    virtual void abort() = 0;
 };
 
 constexpr size_t kUniqueIdBytes = 128; // sizeof(ncclUniqueId)

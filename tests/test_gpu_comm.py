@@ -153,3 +153,31 @@ def test_comm_rejects_manual_prepare(engine):
         with pytest.raises(GnmError):
             e.prepare_median(cat)
         e.reset()
+
+
+def test_failed_rank_aborts_the_group_instead_of_hanging():
+    """One loopback rank fails between its accumulation and the combine
+    (GNM_TEST_FAIL_RANK): the other rank's collective is aborted, the call
+    returns an error promptly, and the group refuses further work."""
+    import os
+    import subprocess
+    import sys
+    prog = (
+        "import sys; sys.path.insert(0, '.')\n"
+        "from paper_1108_1785_b200 import Group, GnmError, FlowBatch, SiteCatalog, synth\n"
+        "w = synth.workload('D1'); cat = SiteCatalog(); w.sites.register(cat)\n"
+        "b = FlowBatch(*synth.generate(w, 20000))\n"
+        "g = Group([0, 0], kind='loopback')\n"
+        "try:\n"
+        "    g.aggregate(b, cat); print('NO ERROR')\n"
+        "except GnmError as e:\n"
+        "    print('FIRST', e.status, str(e)[:120])\n"
+        "try:\n"
+        "    g.aggregate(b, cat); print('NO ERROR 2')\n"
+        "except GnmError as e:\n"
+        "    print('SECOND', e.status, str(e)[:120])\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", prog], cwd=root, capture_output=True, text=True, timeout=120,
+                         env=dict(os.environ, GNM_TEST_FAIL_RANK="1"))
+    assert "FIRST" in out.stdout and "injected failure" in out.stdout, out.stdout + out.stderr
+    assert "SECOND 13" in out.stdout, out.stdout + out.stderr
