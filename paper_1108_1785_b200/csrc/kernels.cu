@@ -409,7 +409,15 @@ __device__ __forceinline__ uint32_t accumulate(uint32_t code, uint32_t oct, uint
     // flow_rate (rate_engine.cpp:88-94): exact product, one IEEE division.
     // Issued before the lookup: it needs only the record, so its dependent
     // DFMA chain overlaps the table loads (an Unmatched item wastes it).
+#ifdef GNM_K2_ABLATION
+    // 5: a single-MUFU approximate rate instead of the IEEE division (wrong
+    // results; measures what the exact division costs)
+    const double rate = p.ablation == 5
+        ? static_cast<double>(__fdividef(8000.0f * static_cast<float>(oct), static_cast<float>(dur)))
+        : __ddiv_rn(8000.0 * static_cast<double>(oct), __ull2double_rn(dur));
+#else
     const double rate = __ddiv_rn(8000.0 * static_cast<double>(oct), __ull2double_rn(dur));
+#endif
     const uint32_t v = resolve<kSmem>(gt, code);
     if (v == kNone) {
         ++c.unm;
@@ -451,8 +459,15 @@ __device__ __forceinline__ uint32_t accumulate(uint32_t code, uint32_t oct, uint
     }
 #endif
     unsigned long long* s = P.sums + static_cast<size_t>(site) * 4;
+#ifdef GNM_K2_ABLATION
+    // 6: everything but min/max; 7: everything but the octet / micro-bps sums
+    const bool abl_nominmax = p.ablation == 6, abl_nosums = p.ablation == 7;
+#else
+    constexpr bool abl_nominmax = false, abl_nosums = false;
+#endif
     if (kHot && slot) {
         uint32_t* l = h.limb + slot;
+        if (!abl_nosums) {
         red_add_shared(l, oct & 0xFFFFu);
         red_add_shared(l + kHotStride, oct >> 16);
         if (hi == 0 && lo < (1ull << 48)) {
@@ -464,6 +479,7 @@ __device__ __forceinline__ uint32_t accumulate(uint32_t code, uint32_t oct, uint
             red_add(s + 2, lo >> 32);
             if (hi) red_add(s + 3, hi);
         }
+        }
         if (slot <= kCoarseSlots)
             red_add_shared(h.coarse + (slot - 1) * kCoarse + sb, 1u);
         else
@@ -472,22 +488,26 @@ __device__ __forceinline__ uint32_t accumulate(uint32_t code, uint32_t oct, uint
         // cache moves (shared atomics; rare after the first flows) only AFTER
         // the RED, so it only ever holds rates whose RED was issued: a stale
         // read costs an extra RED but never hides a winning update.
-        if (rb < cmn) {
+        if (rb < cmn && !abl_nominmax) {
             red_min(P.mn + site, rb);
             atomicMin(h.mn + slot, rb);
         }
-        if (rb > cmx) {
+        if (rb > cmx && !abl_nominmax) {
             red_max(P.mx + site, rb);
             atomicMax(h.mx + slot, rb);
         }
     } else {
         red_add(P.coarse + static_cast<size_t>(sb) * P.n_sites + site, 1u);
-        red_add(s + 0, static_cast<unsigned long long>(oct));
-        red_add(s + 1, lo & 0xFFFFFFFFull);
-        if (lo >> 32) red_add(s + 2, lo >> 32);
-        if (hi) red_add(s + 3, hi);
-        red_min(P.mn + site, rb);
-        red_max(P.mx + site, rb);
+        if (!abl_nosums) {
+            red_add(s + 0, static_cast<unsigned long long>(oct));
+            red_add(s + 1, lo & 0xFFFFFFFFull);
+            if (lo >> 32) red_add(s + 2, lo >> 32);
+            if (hi) red_add(s + 3, hi);
+        }
+        if (!abl_nominmax) {
+            red_min(P.mn + site, rb);
+            red_max(P.mx + site, rb);
+        }
     }
     return site;
 }

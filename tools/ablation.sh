@@ -4,6 +4,8 @@
 #   2 + queue/drain + /24 resolve, no per-flow arithmetic
 #   3 + all per-flow arithmetic, no reductions
 #   4 + the histogram RED only
+#   5 full kernel with an approximate (single-MUFU) rate: the cost of the IEEE division
+#   6 full kernel without min/max; 7 full kernel without the sums
 #   0 full kernel
 set -u
 mkdir -p gpurun_out
