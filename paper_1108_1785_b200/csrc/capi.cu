@@ -785,7 +785,18 @@ void combine_hosts(gnm_ctx* c, const gnm_registry* reg) {
     ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
     ck(cudaFreeAsync(d_cnt, c->stream), "cudaFreeAsync");
     const uint64_t maxn = std::max<uint64_t>(1, *std::max_element(counts.begin(), counts.end()));
-    unsigned long long *send = nullptr, *all = nullptr, *uni = nullptr;
+    // stream-ordered temporaries, released on every path
+    struct Temps {
+        cudaStream_t s;
+        unsigned long long *send = nullptr, *all = nullptr, *uni = nullptr;
+        ~Temps() {
+            for (void* p : {static_cast<void*>(send), static_cast<void*>(all), static_cast<void*>(uni)})
+                if (p) cudaFreeAsync(p, s);
+        }
+    } tmp{c->stream};
+    unsigned long long*& send = tmp.send;
+    unsigned long long*& all = tmp.all;
+    unsigned long long*& uni = tmp.uni;
     ck(cudaMallocAsync(reinterpret_cast<void**>(&send), 8 * maxn, c->stream), "cudaMallocAsync(keys)");
     ck(cudaMallocAsync(reinterpret_cast<void**>(&all), 8 * maxn * N, c->stream), "cudaMallocAsync(keys)");
     ck(cudaMallocAsync(reinterpret_cast<void**>(&uni), 8 * maxn * N, c->stream), "cudaMallocAsync(keys)");
@@ -798,8 +809,6 @@ void combine_hosts(gnm_ctx* c, const gnm_registry* reg) {
     ck(gnm::hosts_global_begin(c->device, c->hrows, c->hlocal, uni, nu, c->hglobal, c->stream),
        "per-host union partials");
     c->kernel_launches += 4;
-    for (void* p : {static_cast<void*>(send), static_cast<void*>(all), static_cast<void*>(uni)})
-        ck(cudaFreeAsync(p, c->stream), "cudaFreeAsync");
     gnm::HostGlobal& g = c->hglobal;
     m.group_start();
     m.all_reduce(g.sums, nu * 3, gnm::DType::U64, gnm::RedOp::Sum, c->stream);
@@ -1787,6 +1796,8 @@ int gnm_ctx_comm_init(gnm_ctx* c, int nranks, int rank, const unsigned char id[G
     if (c->accumulating) return fail(GNM_ERR_INVALID_ARGUMENT, "attach a communicator between accumulations");
     return guarded([&] {
         ck(cudaSetDevice(c->device), "cudaSetDevice");
+        ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+        drop_graphs(c); // graphs captured without the collectives must not replay
         c->comm = gnm::nccl_comm(nranks, rank, id);
         return static_cast<int>(GNM_OK);
     });
@@ -1798,6 +1809,7 @@ int gnm_ctx_comm_destroy(gnm_ctx* c) {
     return guarded([&] {
         ck(cudaSetDevice(c->device), "cudaSetDevice");
         ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+        drop_graphs(c); // their captured collectives refer to this communicator
         c->comm.reset();
         return static_cast<int>(GNM_OK);
     });
@@ -1886,7 +1898,6 @@ int group_analyze(gnm_group* g, const gnm_registry* reg, const gnm_filter_params
             rows[i].resize(n_sites);
             res[i].sites = rows[i].data();
         }
-        c->discard_hist_out = i != 0;
         int e;
         if (b) {
             gnm_batch_soa s = *b;
@@ -1918,7 +1929,13 @@ int group_analyze(gnm_group* g, const gnm_registry* reg, const gnm_filter_params
             gnm_reset(c);
             return fail(GNM_ERR_INVALID_ARGUMENT, "injected failure (GNM_TEST_FAIL_RANK)");
         }
-        e = finalize(c, reg, &res[i]);
+        c->discard_hist_out = i != 0;
+        try {
+            e = finalize(c, reg, &res[i]);
+        } catch (...) {
+            c->discard_hist_out = false;
+            throw;
+        }
         c->discard_hist_out = false;
         if (!e && i == 0) *r = res[0];
         return e;
