@@ -412,6 +412,10 @@ typedef struct gnm_timing {
     double total_finalize_ms;
     uint64_t total_finalizes;
     uint64_t total_k2_launches;
+    /* bytes the loader has copied host -> device since ctx creation (host
+     * batches; non-windowed SoA batches send a u32 duration in place of the
+     * two u64 timestamps: 20 bytes per record instead of 32) */
+    uint64_t h2d_bytes;
 } gnm_timing;
 int gnm_ctx_timing(gnm_ctx* ctx, gnm_timing* out);
 /* 1 = record CUDA events around every kernel (default 0); enabling resets

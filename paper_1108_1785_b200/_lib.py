@@ -103,7 +103,8 @@ class gnm_timing(C.Structure):
                 ("kernel_launches", C.c_uint64), ("records", C.c_uint64),
                 ("plan_ms", C.c_double), ("total_plan_ms", C.c_double),
                 ("total_accumulate_ms", C.c_double), ("total_finalize_ms", C.c_double),
-                ("total_finalizes", C.c_uint64), ("total_k2_launches", C.c_uint64)]
+                ("total_finalizes", C.c_uint64), ("total_k2_launches", C.c_uint64),
+                ("h2d_bytes", C.c_uint64)]
 
 
 class gnm_warning(C.Structure):

@@ -176,6 +176,8 @@ struct gnm_ctx {
     uint64_t tot_finalizes = 0, tot_k2 = 0, k2_since_fin = 0;
     int occ[2] = {0, 0}; // K2 blocks/SM (cold, hot) for the current table size
     uint64_t k2_launches = 0, kernel_launches = 0, records = 0;
+    uint64_t h2d_bytes = 0; // loader copies since creation (gnm_timing)
+    unsigned stage_share = 1; // contexts loading at once in this process (a group's size)
 
     // multi-GPU: with a communicator, gnm_finalize runs the two-round
     // combine across the ranks itself (gnm_ctx_comm_init / gnm_group_*)
@@ -505,6 +507,20 @@ gnm::DevBatch aos_batch(const void* rec, uint64_t n) {
 // with K2 on the compute stream, chunk by chunk (SURVEY.md §8 loader L1).
 // Columns already in pinned memory DMA straight from the caller's buffers;
 // pageable columns go through the context's pinned staging slots.
+// Host threads for the loader's staging work: the cores of this process's
+// share of the node -- hardware threads / the ranks torchrun put on it
+// (LOCAL_WORLD_SIZE) / the contexts of a group loading at once -- at most 16.
+// GNM_STAGE_THREADS overrides.
+unsigned stage_threads(const gnm_ctx* c) {
+    static const unsigned kNode = [] {
+        unsigned t = std::thread::hardware_concurrency();
+        if (const char* l = std::getenv("LOCAL_WORLD_SIZE")) t /= std::max(1, std::atoi(l));
+        return std::max(1u, t);
+    }();
+    if (const char* e = std::getenv("GNM_STAGE_THREADS")) return std::max(1, std::min(std::atoi(e), 16));
+    return std::max(1u, std::min(kNode / std::max(1u, c->stage_share), 16u));
+}
+
 // Pageable host input: the copy into the pinned staging slot is the
 // bottleneck of the loader (one core copies ~10 GB/s, PCIe takes ~55), so
 // a chunk's column pieces are copied by several host threads, each taking
@@ -515,12 +531,7 @@ struct CopySeg {
     size_t bytes;
 };
 
-void staged_copy(const std::vector<CopySeg>& segs) {
-    static const unsigned kThreads = [] {
-        unsigned t = std::thread::hardware_concurrency() / 2;
-        if (const char* e = std::getenv("GNM_STAGE_THREADS")) t = static_cast<unsigned>(std::atoi(e));
-        return std::max(1u, std::min(t, 16u));
-    }();
+void staged_copy(const std::vector<CopySeg>& segs, unsigned kThreads) {
     constexpr size_t kMinPerThread = 8u << 20;
     size_t total = 0;
     for (const CopySeg& g : segs) total += g.bytes;
@@ -573,18 +584,201 @@ void d2h_large(gnm_ctx* c, void* dst, const void* src, size_t bytes) {
         ck(cudaEventRecord(done[slot], c->stream), "cudaEventRecord");
         if (pending_slot >= 0) { // drain the previous chunk while this one is in flight
             ck(cudaEventSynchronize(done[pending_slot]), "cudaEventSynchronize");
-            staged_copy({{d + pending_off, c->h_stage[pending_slot], pending_len}});
+            staged_copy({{d + pending_off, c->h_stage[pending_slot], pending_len}}, stage_threads(c));
         }
         pending_slot = slot;
         pending_off = off;
         pending_len = len;
     }
     ck(cudaEventSynchronize(done[pending_slot]), "cudaEventSynchronize");
-    staged_copy({{d + pending_off, c->h_stage[pending_slot], pending_len}});
+    staged_copy({{d + pending_off, c->h_stage[pending_slot], pending_len}}, stage_threads(c));
+}
+
+// fn(t, nt) on nt host threads (the calling thread is t = 0).
+template <typename F>
+void parallel_for(unsigned nt, F&& fn) {
+    if (nt <= 1) {
+        fn(0u, 1u);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < nt; ++t) th.emplace_back([&, t] { fn(t, nt); });
+    fn(0u, nt);
+    for (auto& x : th) x.join();
+}
+
+// Host SoA batches analysed without a snapshot window need only
+// dur = end - start of the two u64 columns (reduce_slice, rate_engine.cpp:
+// 211-236 uses nothing else of them): the loader sends it as u32 (20 bytes
+// per record over PCIe instead of 32) and K2 reads it in place (layout 5).
+// Computed on host threads while the previous chunk's DMA runs; a chunk with
+// any duration >= 2^32 (e.g. end < start, which wraps) goes uncompacted.
+// Pageable input: the four u32 columns are staged in the same pass.
+void load_and_run(gnm_ctx* c, bool aos, const void* const* cols, const size_t* widths, int ncols,
+                  uint64_t n, const gnm::DevParams& p, bool archive);
+
+void load_and_run_compact(gnm_ctx* c, const gnm_batch_soa* b, const gnm::DevParams& p) {
+    const uint64_t n = b->n;
+    bool pinned = true;
+    const void* cols[6] = {b->src_addr, b->dst_addr, b->d_pkts, b->d_octets, b->start_ms, b->end_ms};
+    for (const void* q : cols) pinned = pinned && is_pinned(q);
+    if (pinned && stage_threads(c) < 8) { // too few cores to out-run the plain DMA of pinned columns
+        const size_t widths[6] = {4, 4, 4, 4, 8, 8};
+        load_and_run(c, false, cols, widths, 6, n, p, false);
+        return;
+    }
+    const uint64_t chunk = (std::max<uint64_t>(1024, std::min<uint64_t>(c->chunk, n)) + 3) & ~uint64_t(3);
+    const size_t col = chunk * 4; // one u32 column of a slot, 16-byte multiple
+    // device slot: src | dst | pkts | octets | dur32, or the 32-byte fallback
+    // layout src | dst | pkts | octets | start | end; host slot: the staged columns
+    ensure_stage(c, chunk * 32, true);
+    const unsigned nt = stage_threads(c);
+    for (uint64_t base = 0, k = 0; base < n; base += chunk, ++k) {
+        const int slot = static_cast<int>(k & 1);
+        const uint64_t m = std::min<uint64_t>(chunk, n - base);
+        ck(cudaStreamWaitEvent(c->copy_stream, c->ev_k2[slot], 0), "cudaStreamWaitEvent");
+        ck(cudaEventSynchronize(c->ev_h2d[slot]), "cudaEventSynchronize"); // the host slot is free
+        EventPair ev;
+        if (c->timing) {
+            ev = take_pair(c);
+            ck(cudaEventRecord(ev.a, c->copy_stream), "cudaEventRecord");
+        }
+        unsigned char* hs = c->h_stage[slot];
+        unsigned char* ds = c->d_stage[slot];
+        uint32_t* hdur = reinterpret_cast<uint32_t*>(hs + (pinned ? 0 : 4 * col));
+        const auto* st = b->start_ms + base;
+        const auto* en = b->end_ms + base;
+        std::atomic<bool> wide{false};
+        parallel_for(nt, [&](unsigned t, unsigned ntt) {
+            const uint64_t lo = m * t / ntt, hi = m * (t + 1) / ntt;
+            if (!pinned) // the four u32 columns into the pinned slot
+                for (int q = 0; q < 4; ++q)
+                    std::memcpy(hs + q * col + lo * 4, static_cast<const uint32_t*>(cols[q]) + base + lo,
+                                (hi - lo) * 4);
+            uint64_t over = 0;
+            for (uint64_t i = lo; i < hi; ++i) {
+                const uint64_t d = en[i] - st[i];
+                over |= d >> 32;
+                hdur[i] = static_cast<uint32_t>(d);
+            }
+            if (over) wide.store(true, std::memory_order_relaxed);
+        });
+        const void* dcols[6];
+        for (int q = 0; q < 4; ++q) {
+            dcols[q] = ds + q * col;
+            const void* from = pinned ? static_cast<const void*>(static_cast<const uint32_t*>(cols[q]) + base)
+                                      : static_cast<const void*>(hs + q * col);
+            ck(cudaMemcpyAsync(ds + q * col, from, m * 4, cudaMemcpyHostToDevice, c->copy_stream), "H2D");
+        }
+        c->h2d_bytes += m * (wide.load() ? 32 : 20);
+        gnm::DevBatch db;
+        if (!wide.load()) {
+            ck(cudaMemcpyAsync(ds + 4 * col, hdur, m * 4, cudaMemcpyHostToDevice, c->copy_stream), "H2D dur");
+            db = soa_batch(dcols, m);
+            db.soa.start = db.soa.end = nullptr;
+            db.soa.dur32 = reinterpret_cast<const uint32_t*>(ds + 4 * col);
+        } else { // a duration needs 64 bits: send start/end (8-byte columns after the u32 ones)
+            dcols[4] = ds + 4 * col;
+            dcols[5] = ds + 4 * col + chunk * 8;
+            ck(cudaMemcpyAsync(ds + 4 * col, st, m * 8, cudaMemcpyHostToDevice, c->copy_stream), "H2D start");
+            ck(cudaMemcpyAsync(ds + 4 * col + chunk * 8, en, m * 8, cudaMemcpyHostToDevice, c->copy_stream),
+               "H2D end");
+            db = soa_batch(dcols, m);
+        }
+        if (c->timing) {
+            ck(cudaEventRecord(ev.b, c->copy_stream), "cudaEventRecord");
+            c->h2d_pairs.push_back(ev);
+        }
+        ck(cudaEventRecord(c->ev_h2d[slot], c->copy_stream), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(c->stream, c->ev_h2d[slot], 0), "cudaStreamWaitEvent");
+        launch_k2_timed(c, db, p);
+        ck(cudaEventRecord(c->ev_k2[slot], c->stream), "cudaEventRecord");
+    }
+    ck(cudaStreamSynchronize(c->copy_stream), "cudaStreamSynchronize");
+}
+
+// The same compaction for host FlowRecord rows (the C++ drop-in's
+// std::vector): host threads gather src, dst, d_pkts, d_octets and the u32
+// duration of each 64-byte row (netflow.hpp:59-67) into the staging slot, so
+// 20 of the 64 bytes per record cross PCIe. Chunks with a duration >= 2^32
+// send their rows whole (layout 2).
+void load_and_run_compact_aos(gnm_ctx* c, const gnm_batch_aos* b, const gnm::DevParams& p) {
+    const uint64_t n = b->n;
+    const bool pinned = is_pinned(b->records);
+    const uint64_t chunk = (std::max<uint64_t>(1024, std::min<uint64_t>(c->chunk, n)) + 3) & ~uint64_t(3);
+    const size_t col = chunk * 4;
+    ensure_stage(c, chunk * GNM_FLOW_RECORD_BYTES, true);
+    const unsigned nt = stage_threads(c);
+    const auto* rows = static_cast<const unsigned char*>(b->records);
+    for (uint64_t base = 0, k = 0; base < n; base += chunk, ++k) {
+        const int slot = static_cast<int>(k & 1);
+        const uint64_t m = std::min<uint64_t>(chunk, n - base);
+        ck(cudaStreamWaitEvent(c->copy_stream, c->ev_k2[slot], 0), "cudaStreamWaitEvent");
+        ck(cudaEventSynchronize(c->ev_h2d[slot]), "cudaEventSynchronize");
+        EventPair ev;
+        if (c->timing) {
+            ev = take_pair(c);
+            ck(cudaEventRecord(ev.a, c->copy_stream), "cudaEventRecord");
+        }
+        unsigned char* hs = c->h_stage[slot];
+        unsigned char* ds = c->d_stage[slot];
+        auto* hsrc = reinterpret_cast<uint32_t*>(hs);
+        auto* hdst = reinterpret_cast<uint32_t*>(hs + col);
+        auto* hpk = reinterpret_cast<uint32_t*>(hs + 2 * col);
+        auto* hoc = reinterpret_cast<uint32_t*>(hs + 3 * col);
+        auto* hdu = reinterpret_cast<uint32_t*>(hs + 4 * col);
+        std::atomic<bool> wide{false};
+        parallel_for(nt, [&](unsigned t, unsigned ntt) {
+            const uint64_t lo = m * t / ntt, hi = m * (t + 1) / ntt;
+            uint64_t over = 0;
+            for (uint64_t i = lo; i < hi; ++i) {
+                const unsigned char* r = rows + (base + i) * GNM_FLOW_RECORD_BYTES;
+                uint32_t w[6];
+                uint64_t st, en;
+                std::memcpy(w, r, 24);
+                std::memcpy(&st, r + 48, 8);
+                std::memcpy(&en, r + 56, 8);
+                const uint64_t d = en - st;
+                over |= d >> 32;
+                hsrc[i] = w[0];
+                hdst[i] = w[1];
+                hpk[i] = w[4];
+                hoc[i] = w[5];
+                hdu[i] = static_cast<uint32_t>(d);
+            }
+            if (over) wide.store(true, std::memory_order_relaxed);
+        });
+        gnm::DevBatch db;
+        if (!wide.load()) {
+            for (int q = 0; q < 5; ++q)
+                ck(cudaMemcpyAsync(ds + q * col, hs + q * col, m * 4, cudaMemcpyHostToDevice, c->copy_stream),
+                   "H2D");
+            c->h2d_bytes += m * 20;
+            const void* dcols[6] = {ds, ds + col, ds + 2 * col, ds + 3 * col, nullptr, nullptr};
+            db = soa_batch(dcols, m);
+            db.soa.dur32 = reinterpret_cast<const uint32_t*>(ds + 4 * col);
+        } else { // a duration needs 64 bits: the rows go whole
+            ck(cudaMemcpyAsync(ds, rows + base * GNM_FLOW_RECORD_BYTES, m * GNM_FLOW_RECORD_BYTES,
+                               cudaMemcpyHostToDevice, c->copy_stream),
+               "H2D rows");
+            c->h2d_bytes += m * GNM_FLOW_RECORD_BYTES;
+            db = aos_batch(ds, m);
+        }
+        if (c->timing) {
+            ck(cudaEventRecord(ev.b, c->copy_stream), "cudaEventRecord");
+            c->h2d_pairs.push_back(ev);
+        }
+        ck(cudaEventRecord(c->ev_h2d[slot], c->copy_stream), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(c->stream, c->ev_h2d[slot], 0), "cudaStreamWaitEvent");
+        launch_k2_timed(c, db, p);
+        ck(cudaEventRecord(c->ev_k2[slot], c->stream), "cudaEventRecord");
+    }
+    ck(cudaStreamSynchronize(c->copy_stream), "cudaStreamSynchronize");
+    (void)pinned;
 }
 
 void load_and_run(gnm_ctx* c, bool aos, const void* const* cols, const size_t* widths, int ncols,
-                  uint64_t n, const gnm::DevParams& p, bool archive = false) {
+                  uint64_t n, const gnm::DevParams& p, bool archive) {
     size_t rec_bytes = 0;
     bool pinned = true;
     for (int i = 0; i < ncols; ++i) {
@@ -616,9 +810,10 @@ void load_and_run(gnm_ctx* c, bool aos, const void* const* cols, const size_t* w
                                 m * widths[i]});
                 hoff += m * widths[i];
             }
-            staged_copy(segs);
+            staged_copy(segs, stage_threads(c));
             ck(cudaMemcpyAsync(dslot, c->h_stage[slot], hoff, cudaMemcpyHostToDevice, c->copy_stream),
                "cudaMemcpyAsync(H2D)");
+            c->h2d_bytes += hoff;
             for (int i = 0; i < ncols; ++i) {
                 dcols[i] = dslot + off;
                 off += m * widths[i];
@@ -628,6 +823,7 @@ void load_and_run(gnm_ctx* c, bool aos, const void* const* cols, const size_t* w
                 ck(cudaMemcpyAsync(dslot + off, static_cast<const unsigned char*>(cols[i]) + base * widths[i],
                                    m * widths[i], cudaMemcpyHostToDevice, c->copy_stream),
                    "cudaMemcpyAsync(H2D)");
+                c->h2d_bytes += m * widths[i];
                 dcols[i] = dslot + off;
                 off += m * widths[i];
             }
@@ -683,9 +879,13 @@ int accumulate_soa(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params*
             launch_k2_timed(c, soa_batch(cols, std::min<uint64_t>(kMaxLaunchRecords, b->n - o)), p);
         }
     } else {
-        const void* cols[6] = {b->src_addr, b->dst_addr, b->d_pkts, b->d_octets, b->start_ms, b->end_ms};
-        const size_t widths[6] = {4, 4, 4, 4, 8, 8};
-        load_and_run(c, false, cols, widths, 6, b->n, p);
+        if (!p.windowed && !std::getenv("GNM_NO_COMPACT")) {
+            load_and_run_compact(c, b, p);
+        } else {
+            const void* cols[6] = {b->src_addr, b->dst_addr, b->d_pkts, b->d_octets, b->start_ms, b->end_ms};
+            const size_t widths[6] = {4, 4, 4, 4, 8, 8};
+            load_and_run(c, false, cols, widths, 6, b->n, p, false);
+        }
     }
     return GNM_OK;
 }
@@ -708,9 +908,15 @@ int accumulate_aos(gnm_ctx* c, const gnm_registry* reg, const gnm_filter_params*
                                          std::min<uint64_t>(kMaxLaunchRecords, b->n - o)),
                             p);
     } else {
-        const void* cols[1] = {b->records};
-        const size_t widths[1] = {GNM_FLOW_RECORD_BYTES};
-        load_and_run(c, true, cols, widths, 1, b->n, p);
+        // compaction pays when enough cores can gather the rows faster than
+        // PCIe moves them whole (pageable rows are copied by the CPU anyway)
+        if (!p.windowed && !std::getenv("GNM_NO_COMPACT") && (stage_threads(c) >= 8 || !is_pinned(b->records))) {
+            load_and_run_compact_aos(c, b, p);
+        } else {
+            const void* cols[1] = {b->records};
+            const size_t widths[1] = {GNM_FLOW_RECORD_BYTES};
+            load_and_run(c, true, cols, widths, 1, b->n, p, false);
+        }
     }
     return GNM_OK;
 }
@@ -1249,6 +1455,7 @@ int gnm_ctx_timing(gnm_ctx* c, gnm_timing* out) {
     out->total_finalize_ms = c->tot_fin_ms;
     out->total_finalizes = c->tot_finalizes;
     out->total_k2_launches = c->tot_k2;
+    out->h2d_bytes = c->h2d_bytes;
     return GNM_OK;
 }
 
@@ -1962,7 +2169,10 @@ int gnm_group_create(const int* devices, int n, int kind, gnm_group** out) {
     }
     const int e = guarded([&] {
         auto comms = kind == GNM_GROUP_NCCL ? gnm::nccl_clique(devices, n) : gnm::loopback_clique(n);
-        for (int i = 0; i < n; ++i) g->ctx[i]->comm = std::move(comms[i]);
+        for (int i = 0; i < n; ++i) {
+            g->ctx[i]->comm = std::move(comms[i]);
+            g->ctx[i]->stage_share = static_cast<unsigned>(n); // the ranks load at once
+        }
         return static_cast<int>(GNM_OK);
     });
     if (e) {

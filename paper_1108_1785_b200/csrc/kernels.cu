@@ -681,6 +681,11 @@ __device__ __forceinline__ void load_record(const DevBatch& b, uint64_t i, uint3
         src = c.src[i], dst = c.dst[i], pkts = c.pkts[i], oct = c.octets[i];
         end = c.end[i];
         dur = end - c.start[i];
+    } else if constexpr (kLayout == 5) { // compacted: only the duration (never windowed)
+        const DevSoA& c = b.soa;
+        src = c.src[i], dst = c.dst[i], pkts = c.pkts[i], oct = c.octets[i];
+        dur = c.dur32[i];
+        end = dur;
     } else if constexpr (kLayout == 2) {
         const unsigned char* r = static_cast<const unsigned char*>(b.rec) + i * 64;
         const uint2 a = __ldg(reinterpret_cast<const uint2*>(r));                 // src dst
@@ -872,6 +877,17 @@ __device__ __forceinline__ void load_tile(const DevBatch& b, uint32_t tile, uint
             t.y[q] = __ldg(wy + kWord[q]);
         }
         (void)pol;
+    } else if constexpr (kLayout == 5) {
+        // compacted SoA: the duration column replaces start/end (ts = 0, te = dur)
+        const DevSoA& c = b.soa;
+        const uint32_t g = tile * 32u + lane;
+        t.s = ld_stream_u2(reinterpret_cast<const uint2*>(c.src) + g, pol);
+        t.d = ld_stream_u2(reinterpret_cast<const uint2*>(c.dst) + g, pol);
+        t.k = ld_stream_u2(reinterpret_cast<const uint2*>(c.pkts) + g, pol);
+        t.o = ld_stream_u2(reinterpret_cast<const uint2*>(c.octets) + g, pol);
+        const uint2 du = ld_stream_u2(reinterpret_cast<const uint2*>(c.dur32) + g, pol);
+        t.ts = make_ulonglong2(0ull, 0ull);
+        t.te = make_ulonglong2(du.x, du.y);
     } else if constexpr (kLayout == 0) {
         const DevSoA& c = b.soa;
         const uint32_t g = tile * 32u + lane;
@@ -969,6 +985,14 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_aos(DevBatch b, const uint32_t
     k2_tiles<2, kSmem, kHot, kMode>(b, gt, table_words, p, P, hot, L);
 }
 
+// Loader-compacted SoA (u32 durations in place of start/end).
+template <bool kSmem, bool kHot, int kMode>
+__global__ void __launch_bounds__(kK2Block, 1) k2_dur(DevBatch b, const uint32_t* __restrict__ gt,
+                                                    uint32_t table_words, DevParams p,
+                                                    DevPartials P, DevHot hot, DevLog L) {
+    k2_tiles<5, kSmem, kHot, kMode>(b, gt, table_words, p, P, hot, L);
+}
+
 // FLOWARC1 entries read in place (the archive's big-endian rows).
 template <bool kSmem, bool kHot, int kMode>
 __global__ void __launch_bounds__(kK2Block, 1) k2_arc(DevBatch b, const uint32_t* __restrict__ gt,
@@ -1018,6 +1042,7 @@ __global__ void __launch_bounds__(kK2Block) k_sample(DevBatch b, const uint32_t*
         uint64_t dur, end;
         if (b.archive) load_record<4>(b, i, src, dst, pkts, oct, dur, end);
         else if (b.aos) load_record<3>(b, i, src, dst, pkts, oct, dur, end);
+        else if (b.soa.dur32) load_record<5>(b, i, src, dst, pkts, oct, dur, end);
         else load_record<1>(b, i, src, dst, pkts, oct, dur, end);
         if (static_cast<uint64_t>(oct) < p.ack_plus1 * pkts || pkts < p.min_packets1 ||
             dur < static_cast<uint64_t>(p.min_duration1) || (p.windowed && !(end >= p.win_lo && end < p.win_hi)))
@@ -1485,6 +1510,7 @@ constexpr auto k2_kernel() {
     if constexpr (L == 0) return k2_soa<kS, kH, kW>;
     else if constexpr (L == 2) return k2_aos<kS, kH, kW>;
     else if constexpr (L == 4) return k2_arc<kS, kH, kW>;
+    else if constexpr (L == 5) return k2_dur<kS, kH, kW>;
     else return k2_gen<L, kS, kH, kW>;
 }
 
@@ -1543,6 +1569,7 @@ int k2_layout(const DevBatch& b) {
     if (b.archive) return 4;
     if (b.aos) return (reinterpret_cast<uintptr_t>(b.rec) & 15u) == 0 ? 2 : 3;
     const DevSoA& c = b.soa;
+    if (c.dur32) return 5; // the loader's staging: 16-byte aligned columns
     const bool vec = ((reinterpret_cast<uintptr_t>(c.src) | reinterpret_cast<uintptr_t>(c.dst) |
                        reinterpret_cast<uintptr_t>(c.pkts) | reinterpret_cast<uintptr_t>(c.octets) |
                        reinterpret_cast<uintptr_t>(c.start) | reinterpret_cast<uintptr_t>(c.end)) &
@@ -1559,6 +1586,7 @@ cudaError_t init_kernel_attributes() {
     if ((e = allow_layout<2>())) return e;
     if ((e = allow_layout<3>())) return e;
     if ((e = allow_layout<4>())) return e;
+    if ((e = allow_layout<5>())) return e;
     if ((e = allow_smem(k_sample<true>))) return e;
     return allow_smem(k_classify<true>);
 }
@@ -1577,7 +1605,7 @@ LaunchCfg k2_config(int device, const DevBatch& b, uint32_t table_words, bool ho
     const uint64_t per_block = static_cast<uint64_t>(c.block) * 16;
     const uint64_t want = (b.n + per_block - 1) / per_block;
     uint64_t grid;
-    if (k2_layout(b) == 0 || k2_layout(b) == 2 || k2_layout(b) == 4) {
+    if (k2_layout(b) == 0 || k2_layout(b) == 2 || k2_layout(b) == 4 || k2_layout(b) == 5) {
         grid = std::min(sms, want); // persistent, one CTA per SM
     } else {
         // k2_gen: < 2^16 records per CTA (the hot limbs' bound); beyond one
@@ -1645,6 +1673,7 @@ cudaError_t launch_k2(const LaunchCfg& cfg, const DevBatch& b, const DevTable& t
     case 1: launch_k2_l<1>(cfg, b, t, p, P, hot, log, s); break;
     case 2: launch_k2_l<2>(cfg, b, t, p, P, hot, log, s); break;
     case 3: launch_k2_l<3>(cfg, b, t, p, P, hot, log, s); break;
+    case 5: launch_k2_l<5>(cfg, b, t, p, P, hot, log, s); break;
     default: launch_k2_l<4>(cfg, b, t, p, P, hot, log, s); break;
     }
     return cudaGetLastError();

@@ -129,6 +129,10 @@ struct DevSoA {
     const uint64_t* start;
     const uint64_t* end;
     uint64_t n;
+    // Loader-compacted batches (non-windowed host SoA input): the duration
+    // end - start as u32, computed on the host, in place of start/end (which
+    // are then null). K2 layout 5.
+    const uint32_t* dur32 = nullptr;
 };
 
 // A batch is SoA columns or 64-byte flowmon::FlowRecord AoS rows.

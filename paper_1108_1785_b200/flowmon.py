@@ -595,7 +595,7 @@ class Engine:
                 "plan_ms": t.plan_ms, "total_plan_ms": t.total_plan_ms,
                 "total_accumulate_ms": t.total_accumulate_ms,
                 "total_finalize_ms": t.total_finalize_ms, "total_finalizes": t.total_finalizes,
-                "total_k2_launches": t.total_k2_launches}
+                "total_k2_launches": t.total_k2_launches, "h2d_bytes": t.h2d_bytes}
 
     @staticmethod
     def _params(params: Optional[FilterParams]) -> gnm_filter_params:
