@@ -667,8 +667,8 @@ def main():
             torch.cuda.empty_cache()
             if hasattr(torch._C, "_host_emptyCache"):  # give the pinned host cache back first
                 torch._C._host_emptyCache()
-            out = subprocess.run([exe, "--workload", args.workload, "--records", str(n), "--steps", "3",
-                                  "--warmup", "1"], capture_output=True, text=True, timeout=900)
+            out = subprocess.run([exe, "--workload", args.workload, "--records", str(n), "--steps", "5",
+                                  "--warmup", "2"], capture_output=True, text=True, timeout=900)
             lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
             if out.returncode == 0 and lines:
                 a = json.loads(lines[-1])

@@ -8,6 +8,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
+#include <functional>
+#include <condition_variable>
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
@@ -73,6 +76,68 @@ struct gnm_warning_state {
 
 struct EventPair {
     cudaEvent_t a = nullptr, b = nullptr;
+};
+
+// Persistent host workers for the loader's staging work (parallel_for):
+// run(nt, fn) executes fn(t, nt) for t = 1..nt-1 on the workers and t = 0
+// on the caller, and returns when all are done.
+class WorkerPool {
+public:
+    explicit WorkerPool(unsigned n) {
+        for (unsigned i = 0; i < n; ++i) th_.emplace_back([this] { loop(); });
+    }
+    ~WorkerPool() {
+        {
+            std::lock_guard<std::mutex> l(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    size_t size() const { return th_.size(); }
+    template <typename F>
+    void run(unsigned nt, F& fn) {
+        {
+            std::lock_guard<std::mutex> l(m_);
+            job_ = [&fn](unsigned t, unsigned n) { fn(t, n); };
+            nt_ = nt;
+            next_ = 1;
+            done_ = 0;
+            ++gen_;
+        }
+        cv_.notify_all();
+        fn(0u, nt);
+        std::unique_lock<std::mutex> l(m_);
+        done_cv_.wait(l, [&] { return done_ == nt_ - 1; });
+        job_ = nullptr;
+    }
+
+private:
+    void loop() {
+        uint64_t seen = 0;
+        std::unique_lock<std::mutex> l(m_);
+        while (true) {
+            cv_.wait(l, [&] { return stop_ || (gen_ != seen && next_ < nt_); });
+            if (stop_) return;
+            seen = gen_;
+            while (next_ < nt_) {
+                const unsigned t = next_++;
+                auto job = job_;
+                const unsigned n = nt_;
+                l.unlock();
+                job(t, n);
+                l.lock();
+                if (++done_ == nt_ - 1) done_cv_.notify_one();
+            }
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex m_;
+    std::condition_variable cv_, done_cv_;
+    std::function<void(unsigned, unsigned)> job_;
+    unsigned nt_ = 0, next_ = 0, done_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
 };
 
 struct gnm_ctx {
@@ -178,6 +243,7 @@ struct gnm_ctx {
     uint64_t k2_launches = 0, kernel_launches = 0, records = 0;
     uint64_t h2d_bytes = 0; // loader copies since creation (gnm_timing)
     unsigned stage_share = 1; // contexts loading at once in this process (a group's size)
+    std::unique_ptr<WorkerPool> pool_workers; // the loader's host threads (parallel_for)
 
     // multi-GPU: with a communicator, gnm_finalize runs the two-round
     // combine across the ranks itself (gnm_ctx_comm_init / gnm_group_*)
@@ -594,17 +660,17 @@ void d2h_large(gnm_ctx* c, void* dst, const void* src, size_t bytes) {
     staged_copy({{d + pending_off, c->h_stage[pending_slot], pending_len}}, stage_threads(c));
 }
 
-// fn(t, nt) on nt host threads (the calling thread is t = 0).
+// fn(t, nt) on nt host threads (the calling thread is t = 0), on the
+// context's persistent worker pool: a loader chunk is a few milliseconds of
+// work, so spawning threads per chunk would cost a visible share of it.
 template <typename F>
-void parallel_for(unsigned nt, F&& fn) {
+void parallel_for(gnm_ctx* c, unsigned nt, F&& fn) {
     if (nt <= 1) {
         fn(0u, 1u);
         return;
     }
-    std::vector<std::thread> th;
-    for (unsigned t = 1; t < nt; ++t) th.emplace_back([&, t] { fn(t, nt); });
-    fn(0u, nt);
-    for (auto& x : th) x.join();
+    if (!c->pool_workers || c->pool_workers->size() + 1 < nt) c->pool_workers.reset(new WorkerPool(nt - 1));
+    c->pool_workers->run(nt, fn);
 }
 
 // Host SoA batches analysed without a snapshot window need only
@@ -649,7 +715,7 @@ void load_and_run_compact(gnm_ctx* c, const gnm_batch_soa* b, const gnm::DevPara
         const auto* st = b->start_ms + base;
         const auto* en = b->end_ms + base;
         std::atomic<bool> wide{false};
-        parallel_for(nt, [&](unsigned t, unsigned ntt) {
+        parallel_for(c, nt, [&](unsigned t, unsigned ntt) {
             const uint64_t lo = m * t / ntt, hi = m * (t + 1) / ntt;
             if (!pinned) // the four u32 columns into the pinned slot
                 for (int q = 0; q < 4; ++q)
@@ -728,7 +794,7 @@ void load_and_run_compact_aos(gnm_ctx* c, const gnm_batch_aos* b, const gnm::Dev
         auto* hoc = reinterpret_cast<uint32_t*>(hs + 3 * col);
         auto* hdu = reinterpret_cast<uint32_t*>(hs + 4 * col);
         std::atomic<bool> wide{false};
-        parallel_for(nt, [&](unsigned t, unsigned ntt) {
+        parallel_for(c, nt, [&](unsigned t, unsigned ntt) {
             const uint64_t lo = m * t / ntt, hi = m * (t + 1) / ntt;
             uint64_t over = 0;
             for (uint64_t i = lo; i < hi; ++i) {
