@@ -597,69 +597,6 @@ struct CopySeg {
     size_t bytes;
 };
 
-void staged_copy(const std::vector<CopySeg>& segs, unsigned kThreads) {
-    constexpr size_t kMinPerThread = 8u << 20;
-    size_t total = 0;
-    for (const CopySeg& g : segs) total += g.bytes;
-    const unsigned nt = static_cast<unsigned>(std::min<size_t>(kThreads, std::max<size_t>(1, total / kMinPerThread)));
-    // bytes [a, b) of the concatenation
-    auto run = [&](size_t a, size_t b) {
-        size_t at = 0;
-        for (const CopySeg& g : segs) {
-            const size_t lo = std::max(a, at), hi = std::min(b, at + g.bytes);
-            if (lo < hi) std::memcpy(g.dst + (lo - at), g.src + (lo - at), hi - lo);
-            at += g.bytes;
-        }
-    };
-    if (nt <= 1) {
-        run(0, total);
-        return;
-    }
-    const size_t per = (total / nt + 4095) & ~size_t(4095);
-    std::vector<std::thread> th;
-    for (unsigned t = 1; t < nt; ++t) {
-        const size_t a = std::min(total, per * t), b = std::min(total, per * (t + 1));
-        if (a < b) th.emplace_back(run, a, b);
-    }
-    run(0, std::min(total, per));
-    for (auto& x : th) x.join();
-}
-
-// Large device -> pageable host copies (the per-host histogram entries can
-// be hundreds of MB): through the two pinned staging slots, each chunk's
-// host copy (several threads) overlapping the next chunk's DMA. Small or
-// pinned destinations go directly.
-void d2h_large(gnm_ctx* c, void* dst, const void* src, size_t bytes) {
-    constexpr size_t kChunk = 32u << 20;
-    if (bytes < 2 * kChunk || is_pinned(dst)) {
-        if (bytes) ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream), "cudaMemcpyAsync(D2H)");
-        ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
-        return;
-    }
-    ensure_stage(c, std::max<size_t>(c->stage_bytes, kChunk), true);
-    const size_t chunk = std::min(c->h_stage_bytes, c->stage_bytes);
-    cudaEvent_t done[2] = {c->ev_h2d[0], c->ev_h2d[1]}; // idle outside the loader
-    auto* d = static_cast<unsigned char*>(dst);
-    const auto* sp = static_cast<const unsigned char*>(src);
-    size_t pending_off = 0, pending_len = 0;
-    int pending_slot = -1;
-    for (size_t off = 0, k = 0; off < bytes; off += chunk, ++k) {
-        const int slot = static_cast<int>(k & 1);
-        const size_t len = std::min(chunk, bytes - off);
-        ck(cudaMemcpyAsync(c->h_stage[slot], sp + off, len, cudaMemcpyDeviceToHost, c->stream), "D2H chunk");
-        ck(cudaEventRecord(done[slot], c->stream), "cudaEventRecord");
-        if (pending_slot >= 0) { // drain the previous chunk while this one is in flight
-            ck(cudaEventSynchronize(done[pending_slot]), "cudaEventSynchronize");
-            staged_copy({{d + pending_off, c->h_stage[pending_slot], pending_len}}, stage_threads(c));
-        }
-        pending_slot = slot;
-        pending_off = off;
-        pending_len = len;
-    }
-    ck(cudaEventSynchronize(done[pending_slot]), "cudaEventSynchronize");
-    staged_copy({{d + pending_off, c->h_stage[pending_slot], pending_len}}, stage_threads(c));
-}
-
 // fn(t, nt) on nt host threads (the calling thread is t = 0), on the
 // context's persistent worker pool: a loader chunk is a few milliseconds of
 // work, so spawning threads per chunk would cost a visible share of it.
@@ -672,6 +609,63 @@ void parallel_for(gnm_ctx* c, unsigned nt, F&& fn) {
     if (!c->pool_workers || c->pool_workers->size() + 1 < nt) c->pool_workers.reset(new WorkerPool(nt - 1));
     c->pool_workers->run(nt, fn);
 }
+
+void staged_copy(gnm_ctx* c, const std::vector<CopySeg>& segs, unsigned kThreads) {
+    constexpr size_t kMinPerThread = 256u << 10;
+    size_t total = 0;
+    for (const CopySeg& g : segs) total += g.bytes;
+    const unsigned nt = static_cast<unsigned>(std::min<size_t>(kThreads, std::max<size_t>(1, total / kMinPerThread)));
+    const size_t per = nt <= 1 ? total : (total / nt + 4095) & ~size_t(4095);
+    // bytes [a, b) of the concatenation
+    parallel_for(c, nt, [&](unsigned t, unsigned) {
+        const size_t a = std::min(total, per * t), b = std::min(total, per * (t + 1));
+        size_t at = 0;
+        for (const CopySeg& g : segs) {
+            const size_t lo = std::max(a, at), hi = std::min(b, at + g.bytes);
+            if (lo < hi) std::memcpy(g.dst + (lo - at), g.src + (lo - at), hi - lo);
+            at += g.bytes;
+        }
+    });
+}
+
+// Device -> pageable host copies of a megabyte or more (the per-host rows,
+// 64 B each; the per-host histogram entries, up to hundreds of MB): through
+// the two pinned staging slots, each chunk's host copy (several threads,
+// which also take the destination's first-touch page faults) overlapping the
+// next chunk's DMA; below 64 MB in one chunk, whose host copy is spread over
+// the threads. A direct pageable cudaMemcpy runs at ~22 GB/s. Small or
+// pinned destinations go directly.
+void d2h_large(gnm_ctx* c, void* dst, const void* src, size_t bytes) {
+    const size_t kChunk = bytes < (64u << 20) ? bytes : 32u << 20;
+    if (bytes < (1u << 20) || is_pinned(dst)) {
+        if (bytes) ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream), "cudaMemcpyAsync(D2H)");
+        ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
+        return;
+    }
+    ensure_stage(c, std::max<size_t>(c->stage_bytes, kChunk), true);
+    const size_t chunk = std::min({c->h_stage_bytes, c->stage_bytes, kChunk});
+    cudaEvent_t done[2] = {c->ev_h2d[0], c->ev_h2d[1]}; // idle outside the loader
+    auto* d = static_cast<unsigned char*>(dst);
+    const auto* sp = static_cast<const unsigned char*>(src);
+    size_t pending_off = 0, pending_len = 0;
+    int pending_slot = -1;
+    for (size_t off = 0, k = 0; off < bytes; off += chunk, ++k) {
+        const int slot = static_cast<int>(k & 1);
+        const size_t len = std::min(chunk, bytes - off);
+        ck(cudaMemcpyAsync(c->h_stage[slot], sp + off, len, cudaMemcpyDeviceToHost, c->stream), "D2H chunk");
+        ck(cudaEventRecord(done[slot], c->stream), "cudaEventRecord");
+        if (pending_slot >= 0) { // drain the previous chunk while this one is in flight
+            ck(cudaEventSynchronize(done[pending_slot]), "cudaEventSynchronize");
+            staged_copy(c, {{d + pending_off, c->h_stage[pending_slot], pending_len}}, stage_threads(c));
+        }
+        pending_slot = slot;
+        pending_off = off;
+        pending_len = len;
+    }
+    ck(cudaEventSynchronize(done[pending_slot]), "cudaEventSynchronize");
+    staged_copy(c, {{d + pending_off, c->h_stage[pending_slot], pending_len}}, stage_threads(c));
+}
+
 
 // Host SoA batches analysed without a snapshot window need only
 // dur = end - start of the two u64 columns (reduce_slice, rate_engine.cpp:
@@ -876,7 +870,7 @@ void load_and_run(gnm_ctx* c, bool aos, const void* const* cols, const size_t* w
                                 m * widths[i]});
                 hoff += m * widths[i];
             }
-            staged_copy(segs, stage_threads(c));
+            staged_copy(c, segs, stage_threads(c));
             ck(cudaMemcpyAsync(dslot, c->h_stage[slot], hoff, cudaMemcpyHostToDevice, c->copy_stream),
                "cudaMemcpyAsync(H2D)");
             c->h2d_bytes += hoff;
@@ -1406,8 +1400,7 @@ int gnm_host_results(gnm_ctx* c, gnm_host_stats* out, uint64_t capacity, uint32_
         return fail(GNM_ERR_CAPACITY, "host rows: capacity " + std::to_string(capacity) + " < " + std::to_string(n));
     return guarded([&] {
         ck(cudaSetDevice(c->device), "cudaSetDevice");
-        if (n) ck(cudaMemcpyAsync(out, c->hrows.rows, n * sizeof(gnm_host_stats), cudaMemcpyDeviceToHost, c->stream),
-                  "cudaMemcpyAsync(D2H host rows)");
+        d2h_large(c, out, c->hrows.rows, n * sizeof(gnm_host_stats));
         if (n && histograms) {
             const size_t bytes = n * gnm::kBuckets * 4;
             uint32_t* dense = nullptr;
@@ -1415,8 +1408,7 @@ int gnm_host_results(gnm_ctx* c, gnm_host_stats* out, uint64_t capacity, uint32_
             ck(cudaMemsetAsync(dense, 0, bytes, c->stream), "cudaMemsetAsync(host hist)");
             ck(gnm::hosts_histograms(c->device, c->hrows, dense, c->stream), "host histograms");
             c->kernel_launches += 1;
-            ck(cudaMemcpyAsync(histograms, dense, bytes, cudaMemcpyDeviceToHost, c->stream),
-               "cudaMemcpyAsync(D2H host hist)");
+            d2h_large(c, histograms, dense, bytes);
             ck(cudaFreeAsync(dense, c->stream), "cudaFreeAsync(host hist)");
         }
         ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");

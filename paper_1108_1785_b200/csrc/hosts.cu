@@ -58,9 +58,64 @@ int bits_for(uint64_t n) { // smallest b with 2^b >= n (n >= 1)
     return b;
 }
 
-__global__ void h_total(const unsigned int* counts, const uint32_t* off, size_t n,
-                        unsigned long long* total) {
-    *total = n ? static_cast<unsigned long long>(off[n - 1]) + counts[n - 1] : 0ull;
+// H0, one block: exclusive scans of the per-warp-region log counts (flow
+// offsets `off`) and of their H1 work items (non-empty chunks of kInsChunk
+// entries, `ioff`); out[0] = total flows, out[2 + k] = work items of slice k
+// (regions [slice_off[k], slice_off[k + 1]) ).
+constexpr uint32_t kOffBlock = 1024;
+template <uint32_t kChunk>
+__global__ void __launch_bounds__(kOffBlock) h_offsets(const unsigned int* __restrict__ counts, uint32_t n,
+                                                       uint32_t* __restrict__ off, uint32_t* __restrict__ ioff,
+                                                       const uint32_t* __restrict__ slice_off, uint32_t n_slices,
+                                                       unsigned long long* __restrict__ out) {
+    __shared__ unsigned long long wsum[kOffBlock / 32];
+    __shared__ uint32_t total_items;
+    const uint32_t t = threadIdx.x, lane = t & 31u, warp = t >> 5;
+    const uint32_t per = (n + kOffBlock - 1) / kOffBlock;
+    const uint32_t a = min(n, t * per), b = min(n, a + per);
+    uint32_t f = 0, it = 0;
+    for (uint32_t r = a; r < b; ++r) {
+        const uint32_t c = counts[r];
+        f += c;
+        it += (c + kChunk - 1) / kChunk;
+    }
+    // (flows, items) packed in one u64: flows < 2^32, items < 2^32
+    unsigned long long v = static_cast<unsigned long long>(it) << 32 | f, x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+        if (lane >= static_cast<uint32_t>(d)) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned long long w = wsum[lane];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, w, d);
+            if (lane >= static_cast<uint32_t>(d)) w += y;
+        }
+        wsum[lane] = w; // inclusive over warps
+        if (lane == 31) {
+            out[0] = static_cast<uint32_t>(w);
+            total_items = static_cast<uint32_t>(w >> 32);
+        }
+    }
+    __syncthreads();
+    unsigned long long e = x - v + (warp ? wsum[warp - 1] : 0ull); // exclusive prefix of this thread
+    uint32_t fo = static_cast<uint32_t>(e), io = static_cast<uint32_t>(e >> 32);
+    for (uint32_t r = a; r < b; ++r) {
+        const uint32_t c = counts[r];
+        off[r] = fo;
+        ioff[r] = io;
+        fo += c;
+        io += (c + kChunk - 1) / kChunk;
+    }
+    __syncthreads(); // ioff written by the block is visible to the block
+    for (uint32_t k = t; k < n_slices; k += kOffBlock) {
+        const uint32_t s0 = slice_off[k], s1 = k + 1 < n_slices ? slice_off[k + 1] : n;
+        out[2 + k] = (s1 < n ? ioff[s1] : total_items) - (s0 < n ? ioff[s0] : total_items);
+    }
 }
 
 __device__ __forceinline__ uint32_t insert_key(unsigned long long* keys, uint32_t mask, int shift,
@@ -77,27 +132,47 @@ __device__ __forceinline__ uint32_t insert_key(unsigned long long* keys, uint32_
     }
 }
 
-// H1, warp per work item (region, chunk of kInsChunk entries); each lane
-// takes 4 consecutive entries per step (LDG.128 on the u32 columns) and the
-// four table probes are issued before any is resolved.
+// H1, warp per work item (a non-empty chunk of kInsChunk entries of one
+// warp region, numbered by h_offsets); each lane takes 4 consecutive entries
+// per step (LDG.128 on the u32 columns) and the four table probes are issued
+// before any is resolved.
 // acc[slot] = {limb0, limb1, limb2, ~min bits, max bits} in L2 (zero at
 // start: the min is kept complemented). Heavy hosts would serialise on their
 // slot's L2 atomics, so each CTA folds flows into a shared table of kAgg
-// entries first (an entry belongs to the first slot hashed to it; a flow
-// whose entry is taken goes to L2 directly). An entry keeps micro-bps below
-// 2^48 as three 16-bit limbs in u32 counters (native, non-returning shared
-// atomics). A CTA takes a contiguous range of at most kInsItemsPerCta work
-// items of at most kInsChunk flows, i.e. fewer than 2^16 adds per limb, so
-// no counter can wrap and no add has to return its value. Per-entry f32
-// bounds (rounded outward) filter the L2 min/max reductions: a stale bound
-// only costs an extra one.
+// entries first (one CTA of 1024 threads per SM, 192 KB); a flow whose slot
+// has no entry goes to L2 directly. The table starts with the batch's hot
+// slots (h_hot_sample / h_hot_pick: per entry the most frequent sampled slot
+// hashing to it); an entry left empty goes to the first slot hashed to it.
+// An entry keeps micro-bps below 2^48 as three 16-bit limbs in u32 counters
+// (native, non-returning shared atomics). A CTA takes a contiguous range of
+// at most kInsItemsPerCta work items of at most kInsChunk flows, i.e. fewer
+// than 2^16 adds per limb, so no counter can wrap and no add has to return
+// its value. Per-entry f32 bounds (rounded outward) filter the L2 min/max
+// reductions: a stale bound only costs an extra one.
 // Dense ids: the slot is computed, not probed; whether it is occupied is
 // read back from its max-rate accumulator (every flow's rate is > 0), and
 // its key is rebuilt from the id in h_collect_dense -- no per-flow key
 // traffic at all.
-constexpr uint32_t kInsBlock = 256;
-constexpr uint32_t kAgg = 2048;
-constexpr size_t kInsSmem = kAgg * (4 + 4 + 3 * 4 + 4); // 40 KB
+#ifndef GNM_INS_BLOCK
+#define GNM_INS_BLOCK 1024
+#endif
+constexpr uint32_t kInsBlock = GNM_INS_BLOCK;
+#ifndef GNM_INS_AGG_BITS
+#define GNM_INS_AGG_BITS 13
+#endif
+constexpr uint32_t kAggBits = GNM_INS_AGG_BITS;
+constexpr uint32_t kAgg = 1u << kAggBits;
+// GNM_INS_EXACT: the entry keeps the exact min/max rate bits (u64, moved by
+// shared CAS loops, which fire only when the bound improves) and reduces them
+// into L2 once at the flush, instead of f32 filters that reduce every
+// improvement as it happens (~2 ln k reductions for k flows of the entry).
+#ifndef GNM_INS_EXACT
+#define GNM_INS_EXACT 0
+#endif
+constexpr size_t kInsSmem = kAgg * (GNM_INS_EXACT ? 8 + 8 + 3 * 4 + 4 : 4 + 4 + 3 * 4 + 4); // 192 KB at 8192
+#ifndef GNM_INS_CTAS_PER_SM
+#define GNM_INS_CTAS_PER_SM 1
+#endif
 #ifndef GNM_INS_CHUNK
 #define GNM_INS_CHUNK 512
 #endif
@@ -112,8 +187,13 @@ __device__ __forceinline__ void red_max_u64(unsigned long long* p, unsigned long
 }
 
 struct AggSmem {
+#if GNM_INS_EXACT
+    unsigned long long* nmn; // ~(smallest rate bits) of the entry's flows in this CTA (0: none)
+    unsigned long long* mx;  // largest rate bits (0: none)
+#else
     float* mn; // >= the smallest rate this CTA reduced into L2 for the entry (+inf: none)
     float* mx; // <= the largest
+#endif
     uint32_t* key;
     uint32_t* limb; // [3][kAgg]
 };
@@ -121,21 +201,34 @@ struct AggSmem {
 __device__ __forceinline__ void agg_flush(const AggSmem& t, uint32_t e, unsigned long long* a) {
     const uint32_t x0 = atomicExch(t.limb + e, 0u), x1 = atomicExch(t.limb + kAgg + e, 0u);
     const uint32_t x2 = atomicExch(t.limb + 2 * kAgg + e, 0u);
-    red_u64(a + 0, static_cast<unsigned long long>(x0) + (static_cast<unsigned long long>(x1) << 16));
+    if (x0 | x1) red_u64(a + 0, static_cast<unsigned long long>(x0) + (static_cast<unsigned long long>(x1) << 16));
     if (x2) red_u64(a + 1, x2);
+#if GNM_INS_EXACT
+    if (const unsigned long long m = t.mx[e]) {
+        red_max_u64(a + 3, t.nmn[e]);
+        red_max_u64(a + 4, m);
+    }
+#endif
 }
 
-// One flow's contribution (any lane, no warp-level grouping).
+__device__ __forceinline__ uint32_t agg_entry(uint32_t slot) { return (slot * 2654435761u) >> (32 - kAggBits); }
+
+// One flow's contribution (any lane, no warp-level grouping). An entry left
+// empty by the preload (h_hot_pick) goes to the first slot hashed to it.
 __device__ __forceinline__ void fold(uint32_t slot, unsigned long long lo, uint32_t hi, unsigned long long rate,
                                      const AggSmem& t, unsigned long long* acc) {
     unsigned long long* a = acc + static_cast<size_t>(slot) * 5;
-    const uint32_t e = (slot * 2654435761u) >> (32 - 11);
+    const uint32_t e = agg_entry(slot);
     uint32_t cur = t.key[e];
     if (cur == 0xFFFFFFFFu) cur = atomicCAS(t.key + e, 0xFFFFFFFFu, slot);
     if ((cur == 0xFFFFFFFFu || cur == slot) && hi == 0 && lo < (1ull << 48)) {
         atomicAdd(t.limb + e, static_cast<uint32_t>(lo) & 0xFFFFu);
         atomicAdd(t.limb + kAgg + e, static_cast<uint32_t>(lo) >> 16);
         atomicAdd(t.limb + 2 * kAgg + e, static_cast<uint32_t>(lo >> 32));
+#if GNM_INS_EXACT
+        if (~rate > t.nmn[e]) atomicMax(t.nmn + e, ~rate);
+        if (rate > t.mx[e]) atomicMax(t.mx + e, rate);
+#else
         // Bounds move by shared atomics on the f32 bits (positive floats
         // order as integers), only after their reduction was issued.
         const double r = __longlong_as_double(static_cast<long long>(rate));
@@ -147,6 +240,7 @@ __device__ __forceinline__ void fold(uint32_t slot, unsigned long long lo, uint3
             red_max_u64(a + 4, rate);
             atomicMax(reinterpret_cast<int*>(t.mx + e), __float_as_int(__double2float_rd(r)));
         }
+#endif
     } else {
         red_u64(a + 0, lo & 0xFFFFFFFFull);
         red_u64(a + 1, lo >> 32);
@@ -156,37 +250,98 @@ __device__ __forceinline__ void fold(uint32_t slot, unsigned long long lo, uint3
     }
 }
 
-template <bool kDense>
-__global__ void __launch_bounds__(kInsBlock, 4) h_insert(DevLog L, const unsigned int* __restrict__ counts,
-                                                         const uint32_t* __restrict__ off,
-                                                         const uint2* __restrict__ dir,
-                                                         unsigned long long* keys, uint32_t mask, int shift,
-                                                         unsigned long long* __restrict__ acc,
-                                                         uint32_t* __restrict__ slot_of,
-                                                         uint32_t* __restrict__ bk) {
+// Dense id of a host whose /16 is in the registry directory (its /24 is
+// registered): rank of the /16 << 16 | its low 16 bits, bit-reversed so
+// that the hosts of one /24 (one site, often hot) land 256 entries apart
+// instead of in the same L2 sectors.
+__device__ __forceinline__ uint32_t dense_id(uint32_t host, const uint2* __restrict__ dir) {
+    const uint32_t d = host >> 16;
+    const uint2 pr = __ldg(dir + (d >> 5));
+    return (pr.y + __popc(pr.x & ((1u << (d & 31u)) - 1u))) << 16 | __brev(host << 16);
+}
+
+// Hot-slot preload (dense ids). Which hosts are heavy is a property of the
+// batch, not of a CTA's share of it, so instead of first-come entries (most
+// taken by hosts a CTA sees once) every CTA's table starts with the same
+// set: the slots of a 1-in-kHotStride sample of the log, counted, and per
+// table entry the most frequent slot hashing to it.
+constexpr uint32_t kHotStride = 16;
+__global__ void h_hot_sample(DevLog L, const unsigned int* __restrict__ counts, const uint2* __restrict__ dir,
+                             uint32_t* __restrict__ cnt) {
+    const uint32_t per = (L.warp_cap + kHotStride - 1) / kHotStride;
+    const uint64_t total = static_cast<uint64_t>(L.regions) * per;
+    for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
+         w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t r = static_cast<uint32_t>(w / per), i = static_cast<uint32_t>(w % per) * kHotStride;
+        if (i < __ldg(counts + r))
+            atomicAdd(cnt + dense_id(L.hosts[static_cast<size_t>(r) * L.warp_cap + i], dir), 1u);
+    }
+}
+
+__global__ void h_hot_pick(const uint32_t* __restrict__ cnt, uint32_t cap, unsigned long long* __restrict__ table) {
+    for (uint32_t sl = blockIdx.x * blockDim.x + threadIdx.x; sl < cap; sl += gridDim.x * blockDim.x) {
+        const uint32_t c = cnt[sl];
+        if (c >= 2) atomicMax(table + agg_entry(sl), static_cast<unsigned long long>(c) << 32 | sl);
+    }
+}
+
+template <bool kDense, bool kPre>
+__global__ void __launch_bounds__(kInsBlock, GNM_INS_CTAS_PER_SM) h_insert(
+    DevLog L, const unsigned int* __restrict__ counts, const uint32_t* __restrict__ off,
+    const uint32_t* __restrict__ ioff, uint32_t items, const uint2* __restrict__ dir,
+    unsigned long long* keys, uint32_t mask, int shift, unsigned long long* __restrict__ acc,
+    uint32_t* __restrict__ slot_of, uint32_t* __restrict__ bk, const unsigned long long* __restrict__ hot) {
     extern __shared__ __align__(16) unsigned char h_smem[];
     AggSmem t;
+#if GNM_INS_EXACT
+    t.nmn = reinterpret_cast<unsigned long long*>(h_smem);
+    t.mx = t.nmn + kAgg;
+    t.key = reinterpret_cast<uint32_t*>(t.mx + kAgg);
+#else
     t.mn = reinterpret_cast<float*>(h_smem);
     t.mx = t.mn + kAgg;
     t.key = reinterpret_cast<uint32_t*>(t.mx + kAgg);
+#endif
     t.limb = t.key + kAgg;
     for (uint32_t i = threadIdx.x; i < kAgg; i += blockDim.x) {
+#if GNM_INS_EXACT
+        t.nmn[i] = 0;
+        t.mx[i] = 0;
+#else
         t.mn[i] = __int_as_float(0x7F800000); // +inf
         t.mx[i] = 0.0f;
-        t.key[i] = 0xFFFFFFFFu;
+#endif
+        if constexpr (kPre) {
+            const unsigned long long h = hot[i];
+            t.key[i] = h ? static_cast<uint32_t>(h) : 0xFFFFFFFFu;
+        } else {
+            t.key[i] = 0xFFFFFFFFu;
+        }
 #pragma unroll
         for (int f = 0; f < 3; ++f) t.limb[f * kAgg + i] = 0;
     }
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t chunks = (L.warp_cap + kInsChunk - 1) / kInsChunk;
-    const uint32_t items = L.regions * chunks;
-    // this CTA's contiguous item range (<= kInsItemsPerCta items, see above)
+    // this CTA's contiguous range of the slice's `items` work items (the
+    // non-empty chunks, numbered by ioff; <= kInsItemsPerCta, see above)
+    const uint32_t ibase = ioff[0];
     const uint32_t i0 = static_cast<uint32_t>(static_cast<uint64_t>(items) * blockIdx.x / gridDim.x);
     const uint32_t i1 = static_cast<uint32_t>(static_cast<uint64_t>(items) * (blockIdx.x + 1) / gridDim.x);
+    uint32_t r = 0;
+    {
+        // the region of this warp's first item: the last r with ioff[r] <= item
+        const uint32_t w0 = ibase + i0 + (threadIdx.x >> 5);
+        uint32_t lo = 0, hi = L.regions; // ioff[lo] <= w0 < ioff[hi] (ioff[regions] = end)
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(ioff + mid) <= w0) lo = mid;
+            else hi = mid;
+        }
+        r = lo;
+    }
     for (uint32_t w = i0 + (threadIdx.x >> 5); w < i1; w += blockDim.x >> 5) {
-        const uint32_t r = w / chunks;
-        const uint32_t c0 = (w % chunks) * kInsChunk;
+        while (r + 1 < L.regions && __ldg(ioff + r + 1) <= ibase + w) ++r;
+        const uint32_t c0 = (ibase + w - __ldg(ioff + r)) * kInsChunk;
         const uint32_t n = min(counts[r], c0 + kInsChunk);
         const uint32_t base = off[r];
         const size_t rb = static_cast<size_t>(r) * L.warp_cap;
@@ -211,14 +366,7 @@ __global__ void __launch_bounds__(kInsBlock, 4) h_insert(DevLog L, const unsigne
                 const uint32_t site = L.buckets ? xs[q] : xs[q] >> kLogSiteShift;
                 key[q] = static_cast<unsigned long long>(site) << 32 | hs[q];
                 if constexpr (kDense) {
-                    // The host's /16 is in the registry directory (its /24 is
-                    // registered): id = rank of the /16 << 16 | its low 16
-                    // bits, bit-reversed so that the hosts of one /24 (one
-                    // site, often hot) land 256 entries apart instead of in
-                    // the same L2 sectors.
-                    const uint32_t d = hs[q] >> 16;
-                    const uint2 pr = __ldg(dir + (d >> 5));
-                    h0[q] = (pr.y + __popc(pr.x & ((1u << (d & 31u)) - 1u))) << 16 | __brev(hs[q] << 16);
+                    h0[q] = dense_id(hs[q], dir);
                     first[q] = 0;
                 } else {
                     h0[q] = static_cast<uint32_t>((key[q] * 0x9E3779B97F4A7C15ull) >> shift) & mask;
@@ -349,6 +497,21 @@ constexpr uint32_t kCoarseAggBits = GNM_HC_AGG_BITS;
 constexpr uint32_t kCoarseAgg = 1u << kCoarseAggBits;
 constexpr size_t kCoarseSmem = static_cast<size_t>(kCoarseAgg) * 8;
 // With `rank`, also turns every flow's slot into its row (in place).
+// Each thread takes four consecutive flows per step (LDG.128 of the slot and
+// bucket columns) and issues their four rank gathers before using any: the
+// gathers are dependent, L2-latency-bound loads.
+__device__ __forceinline__ void coarse_one(uint32_t r, uint32_t sb, uint32_t n_rows, uint32_t* tkey, uint32_t* tcnt,
+                                           uint32_t* __restrict__ coarse) {
+    const uint32_t key = r << 8 | sb; // rows < 2^24 on this path (rows * 628 B <= 64 MB)
+    const uint32_t e = (key * 2654435761u) >> (32 - kCoarseAggBits);
+    uint32_t cur = tkey[e];
+    if (cur == 0xFFFFFFFFu) cur = atomicCAS(tkey + e, 0xFFFFFFFFu, key);
+    if (cur == 0xFFFFFFFFu || cur == key)
+        atomicAdd(tcnt + e, 1u);
+    else
+        atomicAdd(coarse + static_cast<size_t>(sb) * n_rows + r, 1u);
+}
+
 __global__ void __launch_bounds__(512) h_coarse(uint32_t* __restrict__ row, const uint32_t* __restrict__ bk,
                                                 uint32_t n, uint32_t n_rows, const unsigned long long* __restrict__ rank,
                                                 uint32_t* __restrict__ coarse) {
@@ -360,17 +523,25 @@ __global__ void __launch_bounds__(512) h_coarse(uint32_t* __restrict__ row, cons
         tcnt[i] = 0;
     }
     __syncthreads();
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-        const uint32_t r = rank ? static_cast<uint32_t>(rank[row[j]]) : row[j], sb = bk[j] >> 6;
+    const uint32_t n4 = n / 4; // row and bk are cudaMallocAsync bases: 16-byte aligned
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n4; j += gridDim.x * blockDim.x) {
+        uint4 rw = __ldcs(reinterpret_cast<const uint4*>(row) + j);
+        const uint4 bw = __ldcs(reinterpret_cast<const uint4*>(bk) + j);
+        if (rank) {
+            const unsigned long long a = rank[rw.x], b = rank[rw.y], c = rank[rw.z], d = rank[rw.w];
+            rw = make_uint4(static_cast<uint32_t>(a), static_cast<uint32_t>(b), static_cast<uint32_t>(c),
+                            static_cast<uint32_t>(d));
+            __stcs(reinterpret_cast<uint4*>(row) + j, rw);
+        }
+        coarse_one(rw.x, bw.x >> 6, n_rows, tkey, tcnt, coarse);
+        coarse_one(rw.y, bw.y >> 6, n_rows, tkey, tcnt, coarse);
+        coarse_one(rw.z, bw.z >> 6, n_rows, tkey, tcnt, coarse);
+        coarse_one(rw.w, bw.w >> 6, n_rows, tkey, tcnt, coarse);
+    }
+    for (uint32_t j = n4 * 4 + blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const uint32_t r = rank ? static_cast<uint32_t>(rank[row[j]]) : row[j];
         if (rank) row[j] = r;
-        const uint32_t key = r << 8 | sb; // rows < 2^24 on this path (rows * 628 B <= 64 MB)
-        const uint32_t e = (key * 2654435761u) >> (32 - kCoarseAggBits);
-        uint32_t cur = tkey[e];
-        if (cur == 0xFFFFFFFFu) cur = atomicCAS(tkey + e, 0xFFFFFFFFu, key);
-        if (cur == 0xFFFFFFFFu || cur == key)
-            atomicAdd(tcnt + e, 1u);
-        else
-            atomicAdd(coarse + static_cast<size_t>(sb) * n_rows + r, 1u);
+        coarse_one(r, bk[j] >> 6, n_rows, tkey, tcnt, coarse);
     }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < kCoarseAgg; i += blockDim.x)
@@ -399,23 +570,43 @@ __global__ void h_msb(const uint32_t* __restrict__ coarse, uint32_t n_rows, uint
     }
 }
 
+// Four consecutive flows per lane per step, their msb gathers issued
+// together; lanes carrying the same (row, bucket) add once.
 __global__ void __launch_bounds__(256) h_fine(const uint32_t* __restrict__ row, const uint32_t* __restrict__ bk,
                                               uint32_t n, const uint32_t* __restrict__ msb,
                                               uint32_t* __restrict__ fine) {
     const uint32_t lane = threadIdx.x & 31u;
-    for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+    const uint32_t n4 = (n + 3) / 4;
+    for (uint32_t base = blockIdx.x * blockDim.x; base < n4; base += gridDim.x * blockDim.x) {
         const uint32_t j = base + threadIdx.x;
-        bool hit = false;
-        uint32_t r = 0, b = 0;
-        if (j < n) {
-            r = row[j];
-            b = bk[j];
-            hit = (b >> 6) == __ldg(msb + r);
+        uint32_t rs[4] = {0, 0, 0, 0}, bs[4] = {0, 0, 0, 0}, ms[4];
+        bool in[4] = {false, false, false, false};
+        if (4 * j + 3 < n) {
+            const uint4 rw = __ldcs(reinterpret_cast<const uint4*>(row) + j);
+            const uint4 bw = __ldcs(reinterpret_cast<const uint4*>(bk) + j);
+            rs[0] = rw.x, rs[1] = rw.y, rs[2] = rw.z, rs[3] = rw.w;
+            bs[0] = bw.x, bs[1] = bw.y, bs[2] = bw.z, bs[3] = bw.w;
+            in[0] = in[1] = in[2] = in[3] = true;
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (4 * j + q < n) {
+                    rs[q] = row[4 * j + q];
+                    bs[q] = bk[4 * j + q];
+                    in[q] = true;
+                }
         }
-        const unsigned long long key = hit ? (static_cast<unsigned long long>(r) << 8 | (b & 63u)) : ~0ull;
-        const unsigned m = __match_any_sync(0xFFFFFFFFu, key);
-        if (hit && lane == static_cast<uint32_t>(__ffs(m) - 1))
-            atomicAdd(fine + static_cast<size_t>(r) * kFineH + (b & 63u), __popc(m));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ms[q] = in[q] ? __ldg(msb + rs[q]) : 0xFFFFFFFFu;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const bool hit = (bs[q] >> 6) == ms[q];
+            const unsigned long long key =
+                hit ? (static_cast<unsigned long long>(rs[q]) << 8 | (bs[q] & 63u)) : ~0ull;
+            const unsigned m = __match_any_sync(0xFFFFFFFFu, key);
+            if (hit && lane == static_cast<uint32_t>(__ffs(m) - 1))
+                atomicAdd(fine + static_cast<size_t>(rs[q]) * kFineH + (bs[q] & 63u), __popc(m));
+        }
     }
 }
 
@@ -594,6 +785,8 @@ cudaError_t finish_sorted(int device, HostRows& h, const unsigned long long* acc
 cudaError_t finish_two_round(int device, HostRows& h, const unsigned long long* rank, const unsigned long long* acc,
                              const unsigned long long* hk_sorted, const uint32_t* hs_sorted, cudaStream_t s) {
     Scratch tmp_(s);
+    if ((reinterpret_cast<uintptr_t>(h.row_of) | reinterpret_cast<uintptr_t>(h.bkt)) & 15u)
+        return cudaErrorMisalignedAddress; // h_coarse / h_fine read them as uint4
     const uint32_t n = static_cast<uint32_t>(h.n_flows), nr = static_cast<uint32_t>(h.n_rows);
     uint32_t *coarse = nullptr, *msb = nullptr, *mrank = nullptr, *cnt = nullptr, *fine = nullptr;
     HCK(tmp_.get(&coarse, static_cast<size_t>(nr) * kCoarseH));
@@ -610,7 +803,7 @@ cudaError_t finish_two_round(int device, HostRows& h, const unsigned long long* 
         1, std::min<uint64_t>((n + 511) / 512, static_cast<uint64_t>(sms) * GNM_HC_CTAS_PER_SM)));
     h_coarse<<<cg, 512, kCoarseSmem, s>>>(h.row_of, h.bkt, n, nr, rank, coarse);
     h_msb<<<grid_for(device, nr, 128), 128, 0, s>>>(coarse, nr, msb, mrank, cnt);
-    h_fine<<<grid_for(device, n, 256), 256, 0, s>>>(h.row_of, h.bkt, n, msb, fine);
+    h_fine<<<grid_for(device, (n + 3) / 4, 256), 256, 0, s>>>(h.row_of, h.bkt, n, msb, fine);
     h_final2<<<grid_for(device, nr, 128), 128, 0, s>>>(acc, cnt, msb, mrank, fine, hk_sorted, hs_sorted, nr, h.rows);
     return cudaGetLastError();
 }
@@ -625,25 +818,28 @@ cudaError_t build_hosts_local(int device, const HostSlice* slices, int n_slices,
     loc.ready = true;
     if (n_counts == 0) return cudaSuccess;
     Scratch tmp_(s);
-    // H0: flat offsets of every warp region's entries.
-    uint32_t* off = nullptr;
-    unsigned long long* scal = nullptr; // [0] total flows, [1] distinct keys
+    // H0: flat offsets of every warp region's entries, H1 work items per slice.
+    uint32_t *off = nullptr, *ioff = nullptr, *slice_off = nullptr;
+    unsigned long long* scal = nullptr; // [0] total flows, [1] distinct keys, [2 + k] items of slice k
     HCK(tmp_.get(&off, n_counts));
-    HCK(tmp_.get(&scal, 2));
-    size_t tb = 0;
-    HCK(cub::DeviceScan::ExclusiveSum(nullptr, tb, counts, off, n_counts, s));
-    unsigned char* tmp = nullptr;
-    HCK(tmp_.get(&tmp, tb));
-    HCK(cub::DeviceScan::ExclusiveSum(tmp, tb, counts, off, n_counts, s));
-    HCK(cudaMemsetAsync(scal, 0, 16, s));
-    h_total<<<1, 1, 0, s>>>(counts, off, n_counts, scal);
-    unsigned long long h_scal[2] = {0, 0};
-    HCK(cudaMemcpyAsync(h_scal, scal, 8, cudaMemcpyDeviceToHost, s));
+    HCK(tmp_.get(&ioff, n_counts));
+    HCK(tmp_.get(&slice_off, n_slices));
+    HCK(tmp_.get(&scal, 2 + n_slices));
+    std::vector<uint32_t> h_slice_off(n_slices);
+    for (int i = 0; i < n_slices; ++i) h_slice_off[i] = static_cast<uint32_t>(slices[i].count_off);
+    HCK(cudaMemcpyAsync(slice_off, h_slice_off.data(), n_slices * 4, cudaMemcpyHostToDevice, s));
+    HCK(cudaMemsetAsync(scal, 0, (2 + n_slices) * 8, s));
+    h_offsets<kInsChunk><<<1, kOffBlock, 0, s>>>(counts, static_cast<uint32_t>(n_counts), off, ioff, slice_off,
+                                                 static_cast<uint32_t>(n_slices), scal);
+    std::vector<unsigned long long> h_scal(2 + n_slices, 0);
+    HCK(cudaMemcpyAsync(h_scal.data(), scal, h_scal.size() * 8, cudaMemcpyDeviceToHost, s));
     HCK(cudaStreamSynchronize(s));
     const uint64_t n = h_scal[0];
     if (n == 0) return cudaSuccess;
-    HCK(cudaFuncSetAttribute(h_insert<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kInsSmem)));
-    HCK(cudaFuncSetAttribute(h_insert<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kInsSmem)));
+    HCK(cudaFuncSetAttribute(h_insert<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kInsSmem)));
+    HCK(cudaFuncSetAttribute(h_insert<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kInsSmem)));
     int sms = 0;
     HCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     // H1: dense ids when the registry's /16 blocks allow (every host lies in
@@ -661,21 +857,37 @@ cudaError_t build_hosts_local(int device, const HostSlice* slices, int n_slices,
     out.n_flows = n;
     if (!dense) HCK(cudaMemsetAsync(loc.table, 0xFF, static_cast<size_t>(cap) * 8, s));
     HCK(cudaMemsetAsync(loc.acc, 0, static_cast<size_t>(cap) * 40, s));
+    unsigned long long* hot = nullptr; // dense ids: the preloaded hot slots of every H1 table
+    if (dense) {
+        uint32_t* cnt = nullptr;
+        HCK(tmp_.get(&cnt, cap));
+        HCK(tmp_.get(&hot, kAgg));
+        HCK(cudaMemsetAsync(cnt, 0, static_cast<size_t>(cap) * 4, s));
+        HCK(cudaMemsetAsync(hot, 0, static_cast<size_t>(kAgg) * 8, s));
+        for (int i = 0; i < n_slices; ++i)
+            h_hot_sample<<<static_cast<uint32_t>(sms) * 8, 256, 0, s>>>(
+                slices[i].log, counts + slices[i].count_off, reinterpret_cast<const uint2*>(dir), cnt);
+        h_hot_pick<<<grid_for(device, cap, 256), 256, 0, s>>>(cnt, cap, hot);
+        HCK(cudaGetLastError());
+    }
     for (int i = 0; i < n_slices; ++i) {
         const HostSlice& sl = slices[i];
         // At least four CTAs per SM, and enough CTAs that none takes more
         // than kInsItemsPerCta items (the limbs' no-wrap bound).
-        const uint64_t items = static_cast<uint64_t>(sl.log.regions) * ((sl.log.warp_cap + kInsChunk - 1) / kInsChunk);
+        const uint64_t items = h_scal[2 + i];
+        if (items == 0) continue;
         const uint64_t g = std::max<uint64_t>((items + kInsItemsPerCta - 1) / kInsItemsPerCta,
-                                              std::min<uint64_t>(items, 4ull * sms));
+                                              std::min<uint64_t>(items, static_cast<uint64_t>(GNM_INS_CTAS_PER_SM) * sms));
         if (dense)
-            h_insert<true><<<static_cast<uint32_t>(g), kInsBlock, kInsSmem, s>>>(
-                sl.log, counts + sl.count_off, off + sl.count_off, reinterpret_cast<const uint2*>(dir), loc.table,
-                cap - 1, 64 - tbits, loc.acc, out.row_of, out.bkt);
+            h_insert<true, true><<<static_cast<uint32_t>(g), kInsBlock, kInsSmem, s>>>(
+                sl.log, counts + sl.count_off, off + sl.count_off, ioff + sl.count_off, static_cast<uint32_t>(items),
+                reinterpret_cast<const uint2*>(dir), loc.table,
+                cap - 1, 64 - tbits, loc.acc, out.row_of, out.bkt, hot);
         else
-            h_insert<false><<<static_cast<uint32_t>(g), kInsBlock, kInsSmem, s>>>(
-                sl.log, counts + sl.count_off, off + sl.count_off, nullptr, loc.table, cap - 1, 64 - tbits, loc.acc,
-                out.row_of, out.bkt);
+            h_insert<false, false><<<static_cast<uint32_t>(g), kInsBlock, kInsSmem, s>>>(
+                sl.log, counts + sl.count_off, off + sl.count_off, ioff + sl.count_off, static_cast<uint32_t>(items),
+                nullptr, loc.table, cap - 1, 64 - tbits, loc.acc,
+                out.row_of, out.bkt, nullptr);
         HCK(cudaGetLastError());
     }
     // H2: distinct keys in (site, host) order -> rows.
@@ -696,12 +908,12 @@ cudaError_t build_hosts_local(int device, const HostSlice* slices, int n_slices,
                                                             reinterpret_cast<unsigned int*>(scal + 1));
     }
     HCK(cudaGetLastError());
-    HCK(cudaMemcpyAsync(h_scal + 1, scal + 1, 8, cudaMemcpyDeviceToHost, s));
+    HCK(cudaMemcpyAsync(h_scal.data() + 1, scal + 1, 8, cudaMemcpyDeviceToHost, s));
     HCK(cudaStreamSynchronize(s));
     const uint32_t n_rows = static_cast<uint32_t>(h_scal[1]);
     HCK(dalloc(&loc.hk_sorted, n_rows, s));
     HCK(dalloc(&loc.hs_sorted, n_rows, s));
-    tb = 0;
+    size_t tb = 0;
     // keys are site << 32 | host: only the site's bits above the host sort
     const int end_bit = 32 + std::max(1, bits_for(std::max<uint64_t>(n_sites, 1)));
     HCK(cub::DeviceRadixSort::SortPairs(nullptr, tb, hk, loc.hk_sorted, hs, loc.hs_sorted, n_rows, 0, end_bit, s));
@@ -874,7 +1086,7 @@ cudaError_t hosts_global_begin(int device, HostRows& out, const HostLocal& loc, 
 cudaError_t hosts_global_prepare(int device, const HostRows& out, HostGlobal& g, cudaStream_t s) {
     const uint32_t n = static_cast<uint32_t>(g.n), nf = static_cast<uint32_t>(out.n_flows);
     if (n) h_msb<<<grid_for(device, n, 128), 128, 0, s>>>(g.coarse, n, g.msb, g.mrank, g.cnt);
-    if (nf) h_fine<<<grid_for(device, nf, 256), 256, 0, s>>>(out.row_of, out.bkt, nf, g.msb, g.fine);
+    if (nf) h_fine<<<grid_for(device, (nf + 3) / 4, 256), 256, 0, s>>>(out.row_of, out.bkt, nf, g.msb, g.fine);
     g.prepared = true;
     return cudaGetLastError();
 }

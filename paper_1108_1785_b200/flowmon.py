@@ -247,6 +247,22 @@ class SiteCatalog:
 
 # ---- record batches ------------------------------------------------------------
 
+def _pinned_rows(n: int) -> np.ndarray:
+    """n HOST_STATS_DTYPE rows in page-locked memory from torch's caching
+    host allocator (reused once an earlier result is dropped): the D2H of the
+    per-host rows then runs at the pinned rate instead of ~22 GB/s pageable
+    (80k rows: ~0.1 ms instead of ~0.23). Plain numpy when torch is absent."""
+    nbytes = n * _lib.HOST_STATS_DTYPE.itemsize
+    try:
+        import torch
+        if nbytes >= (1 << 20) and torch.cuda.is_available():
+            buf = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+            return buf.numpy().view(_lib.HOST_STATS_DTYPE)  # the array keeps `buf` alive
+    except ImportError:
+        pass
+    return np.empty(n, _lib.HOST_STATS_DTYPE)
+
+
 def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
@@ -563,7 +579,7 @@ class Engine:
         if not getattr(self, "_hosts", False):
             return res
         n = lib.gnm_host_count(self._h)
-        rows = np.empty(max(n, 1), _lib.HOST_STATS_DTYPE)
+        rows = _pinned_rows(max(n, 1))
         hist = np.empty((max(n, 1), BUCKET_COUNT), np.uint32) if histograms else None
         _check(lib.gnm_host_results(self._h, rows.ctypes.data, len(rows),
                                     hist.ctypes.data if hist is not None else None))
@@ -961,7 +977,7 @@ class Group:
         res = _build_result(r, table[:n], None if hist is None else hist[:n])
         if self._hosts:
             k = lib.gnm_group_host_count(self._h)
-            rows = np.empty(max(k, 1), _lib.HOST_STATS_DTYPE)
+            rows = _pinned_rows(max(k, 1))
             _check(lib.gnm_group_host_results(self._h, rows.ctypes.data, len(rows)))
             res.host_table = rows[:k]
             res.host_histograms = None

@@ -21,6 +21,16 @@ cap() { # name, kernel regex, bench args...
 has k2 && cap k2 k2_soa
 has hinsert && cap hinsert h_insert --hosts
 has aos && cap aos k2_gen --input aos
+if has hpost; then
+  # the per-host median passes (h_coarse, h_fine) of one step
+  timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:h_coarse|h_fine|h_collect" -s 9 -c 3 \
+      -f -o gpurun_out/hpost_${TAG} python bench.py --hosts --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 \
+      --no-pageable --no-adapter --no-extras > gpurun_out/hpost_${TAG}.log 2>&1
+  echo "hpost ncu exit $?"
+  ncu -i gpurun_out/hpost_${TAG}.ncu-rep --page source --csv --print-source=cuda,sass \
+      > gpurun_out/hpost_${TAG}_source.csv 2>/dev/null
+  ncu -i gpurun_out/hpost_${TAG}.ncu-rep --page details > gpurun_out/hpost_${TAG}_details.txt 2>/dev/null
+fi
 
 if has small; then
   # one capture each of the step's small kernels (K1 plan, finalize)
