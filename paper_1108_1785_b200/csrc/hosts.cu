@@ -263,19 +263,47 @@ __device__ __forceinline__ uint32_t dense_id(uint32_t host, const uint2* __restr
 // Hot-slot preload (dense ids). Which hosts are heavy is a property of the
 // batch, not of a CTA's share of it, so instead of first-come entries (most
 // taken by hosts a CTA sees once) every CTA's table starts with the same
-// set: the slots of a 1-in-kHotStride sample of the log, counted, and per
-// table entry the most frequent slot hashing to it.
-constexpr uint32_t kHotStride = 16;
-__global__ void h_hot_sample(DevLog L, const unsigned int* __restrict__ counts, const uint2* __restrict__ dir,
-                             uint32_t* __restrict__ cnt) {
-    const uint32_t per = (L.warp_cap + kHotStride - 1) / kHotStride;
-    const uint64_t total = static_cast<uint64_t>(L.regions) * per;
-    for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
-         w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint32_t r = static_cast<uint32_t>(w / per), i = static_cast<uint32_t>(w % per) * kHotStride;
-        if (i < __ldg(counts + r))
-            atomicAdd(cnt + dense_id(L.hosts[static_cast<size_t>(r) * L.warp_cap + i], dir), 1u);
+// set: the slots of a sample of the log, counted, and per table entry the
+// most frequent sampled slot hashing to it.
+// The sample is the first `take` entries of every warp region: K2's warps
+// log the flows of tiles spread over the whole batch, so the regions' heads
+// are a sample of the batch, read with coalesced loads. Heavy slots recur
+// within a CTA's regions, so each CTA counts them in a shared table first
+// (first come; a slot without an entry goes to L2 directly): plain
+// per-sample L2 atomics serialise on the hottest slots' counters.
+constexpr uint32_t kSampleAggBits = 12, kSampleAgg = 1u << kSampleAggBits;
+constexpr uint32_t kSampleHead = 512; // entries per region (one slice)
+__global__ void __launch_bounds__(1024) h_hot_sample(DevLog L, const unsigned int* __restrict__ counts,
+                                                     const uint2* __restrict__ dir, uint32_t take,
+                                                     uint32_t* __restrict__ cnt) {
+    __shared__ uint32_t skey[kSampleAgg], scnt[kSampleAgg];
+    for (uint32_t i = threadIdx.x; i < kSampleAgg; i += blockDim.x) {
+        skey[i] = 0xFFFFFFFFu;
+        scnt[i] = 0;
     }
+    __syncthreads();
+    const uint32_t r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31u;
+    if (r < L.regions) {
+        const uint32_t n = min(__ldg(counts + r), take);
+        const unsigned int* h = L.hosts + static_cast<size_t>(r) * L.warp_cap;
+        for (uint32_t i = lane * 4; i < n; i += 128) {
+            const uint4 x = __ldcs(reinterpret_cast<const uint4*>(h + i));
+            const uint32_t hs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (i + q >= n) break;
+                const uint32_t sl = dense_id(hs[q], dir);
+                const uint32_t e = (sl * 2654435761u) >> (32 - kSampleAggBits);
+                uint32_t cur = skey[e];
+                if (cur == 0xFFFFFFFFu) cur = atomicCAS(skey + e, 0xFFFFFFFFu, sl);
+                if (cur == 0xFFFFFFFFu || cur == sl) atomicAdd(scnt + e, 1u);
+                else atomicAdd(cnt + sl, 1u);
+            }
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < kSampleAgg; i += blockDim.x)
+        if (scnt[i]) atomicAdd(cnt + skey[i], scnt[i]);
 }
 
 __global__ void h_hot_pick(const uint32_t* __restrict__ cnt, uint32_t cap, unsigned long long* __restrict__ table) {
@@ -864,9 +892,10 @@ cudaError_t build_hosts_local(int device, const HostSlice* slices, int n_slices,
         HCK(tmp_.get(&hot, kAgg));
         HCK(cudaMemsetAsync(cnt, 0, static_cast<size_t>(cap) * 4, s));
         HCK(cudaMemsetAsync(hot, 0, static_cast<size_t>(kAgg) * 8, s));
+        const uint32_t take = std::max<uint32_t>(32, (kSampleHead / n_slices) & ~3u);
         for (int i = 0; i < n_slices; ++i)
-            h_hot_sample<<<static_cast<uint32_t>(sms) * 8, 256, 0, s>>>(
-                slices[i].log, counts + slices[i].count_off, reinterpret_cast<const uint2*>(dir), cnt);
+            h_hot_sample<<<(slices[i].log.regions + 31) / 32, 1024, 0, s>>>(
+                slices[i].log, counts + slices[i].count_off, reinterpret_cast<const uint2*>(dir), take, cnt);
         h_hot_pick<<<grid_for(device, cap, 256), 256, 0, s>>>(cnt, cap, hot);
         HCK(cudaGetLastError());
     }
