@@ -12,6 +12,7 @@
 #include <functional>
 #include <condition_variable>
 #include <atomic>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -79,8 +80,17 @@ struct EventPair {
 };
 
 // Persistent host workers for the loader's staging work (parallel_for):
-// run(nt, fn) executes fn(t, nt) for t = 1..nt-1 on the workers and t = 0
-// on the caller, and returns when all are done.
+// run(nt, fn) executes fn(t, nt) for t = 0..nt-1 and returns when all are
+// done; the caller takes t = 0 and then claims any task no worker has
+// started yet. A loader chunk is a millisecond or two of copying, and a
+// condition-variable wake-up costs tens to hundreds of microseconds, so an
+// idle worker spins on the run counter for kSpin before it sleeps.
+inline void cpu_relax() {
+#if defined(__x86_64__) || defined(__i386__)
+    __builtin_ia32_pause();
+#endif
+}
+
 class WorkerPool {
 public:
     explicit WorkerPool(unsigned n) {
@@ -89,7 +99,7 @@ public:
     ~WorkerPool() {
         {
             std::lock_guard<std::mutex> l(m_);
-            stop_ = true;
+            stop_.store(true);
         }
         cv_.notify_all();
         for (auto& t : th_) t.join();
@@ -97,47 +107,79 @@ public:
     size_t size() const { return th_.size(); }
     template <typename F>
     void run(unsigned nt, F& fn) {
-        {
-            std::lock_guard<std::mutex> l(m_);
-            job_ = [&fn](unsigned t, unsigned n) { fn(t, n); };
-            nt_ = nt;
-            next_ = 1;
-            done_ = 0;
-            ++gen_;
+        if (nt <= 1) {
+            fn(0u, 1u);
+            return;
         }
-        cv_.notify_all();
+        job_ = [&fn](unsigned t, unsigned n) { fn(t, n); };
+        done_.store(0);
+        // state = run id (24 bits) | nt (8 bits) | next task (32 bits); one
+        // fetch_add claims a task of exactly the run it belongs to
+        run_id_ = (run_id_ + 1) & 0xFFFFFFu;
+        state_.store(static_cast<uint64_t>(run_id_) << 40 | static_cast<uint64_t>(nt) << 32 | 1u);
+        if (sleepers_.load() > 0) {
+            std::lock_guard<std::mutex> l(m_);
+            cv_.notify_all();
+        }
         fn(0u, nt);
-        std::unique_lock<std::mutex> l(m_);
-        done_cv_.wait(l, [&] { return done_ == nt_ - 1; });
+        for (;;) { // help with tasks nobody has claimed
+            const uint64_t st = state_.fetch_add(1);
+            const unsigned t = static_cast<unsigned>(st);
+            if (t >= nt) break;
+            fn(t, nt);
+            done_.fetch_add(1);
+        }
+        for (unsigned k = 0; done_.load() != nt - 1; ++k) {
+            cpu_relax();
+            if (k > 4096) std::this_thread::yield();
+        }
         job_ = nullptr;
     }
 
 private:
+    static constexpr auto kSpin = std::chrono::microseconds(3000);
     void loop() {
-        uint64_t seen = 0;
-        std::unique_lock<std::mutex> l(m_);
-        while (true) {
-            cv_.wait(l, [&] { return stop_ || (gen_ != seen && next_ < nt_); });
-            if (stop_) return;
-            seen = gen_;
-            while (next_ < nt_) {
-                const unsigned t = next_++;
-                auto job = job_;
-                const unsigned n = nt_;
-                l.unlock();
-                job(t, n);
-                l.lock();
-                if (++done_ == nt_ - 1) done_cv_.notify_one();
+        uint32_t seen = 0;
+        for (;;) {
+            uint64_t st = state_.load();
+            if (static_cast<uint32_t>(st >> 40) == seen) {
+                const auto t0 = std::chrono::steady_clock::now();
+                for (unsigned k = 1;; ++k) {
+                    cpu_relax(); // leave the core's other hardware thread its issue slots
+                    st = state_.load();
+                    if (static_cast<uint32_t>(st >> 40) != seen || stop_.load()) break;
+                    if ((k & 1023u) == 0 && std::chrono::steady_clock::now() - t0 > kSpin) {
+                        std::unique_lock<std::mutex> l(m_);
+                        sleepers_.fetch_add(1);
+                        cv_.wait(l, [&] { return static_cast<uint32_t>(state_.load() >> 40) != seen || stop_.load(); });
+                        sleepers_.fetch_sub(1);
+                        st = state_.load();
+                        break;
+                    }
+                }
+            }
+            if (stop_.load()) return;
+            for (;;) {
+                // a claim belongs to the run it was taken from (a newer run's
+                // task is that run's to execute: its caller waits for it)
+                const uint64_t c = state_.fetch_add(1);
+                const unsigned t = static_cast<unsigned>(c), n = static_cast<unsigned>(c >> 32) & 0xFFu;
+                seen = static_cast<uint32_t>(c >> 40);
+                if (t >= n) break;
+                job_(t, n);
+                done_.fetch_add(1);
             }
         }
     }
     std::vector<std::thread> th_;
     std::mutex m_;
-    std::condition_variable cv_, done_cv_;
+    std::condition_variable cv_;
     std::function<void(unsigned, unsigned)> job_;
-    unsigned nt_ = 0, next_ = 0, done_ = 0;
-    uint64_t gen_ = 0;
-    bool stop_ = false;
+    std::atomic<uint64_t> state_{0};
+    std::atomic<unsigned> done_{0};
+    std::atomic<int> sleepers_{0};
+    std::atomic<bool> stop_{false};
+    uint32_t run_id_ = 0;
 };
 
 struct gnm_ctx {
