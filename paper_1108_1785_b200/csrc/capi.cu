@@ -652,8 +652,11 @@ void parallel_for(gnm_ctx* c, unsigned nt, F&& fn) {
     c->pool_workers->run(nt, fn);
 }
 
+#ifndef GNM_RESULT_COPY_THREADS
+#define GNM_RESULT_COPY_THREADS 4
+#endif
 void staged_copy(gnm_ctx* c, const std::vector<CopySeg>& segs, unsigned kThreads) {
-    constexpr size_t kMinPerThread = 256u << 10;
+    constexpr size_t kMinPerThread = 192u << 10;
     size_t total = 0;
     for (const CopySeg& g : segs) total += g.bytes;
     const unsigned nt = static_cast<unsigned>(std::min<size_t>(kThreads, std::max<size_t>(1, total / kMinPerThread)));
@@ -1200,7 +1203,14 @@ int finalize(gnm_ctx* c, const gnm_registry* reg, gnm_result* r, int phase = 3) 
     clear_log(c);
     ck(cudaStreamSynchronize(c->stream), "cudaStreamSynchronize");
     // K3b computed every field, avg included (rounded like the host's libgcc).
-    if (n_sites) std::memcpy(r->sites, c->h_out, static_cast<size_t>(n_sites) * sizeof(gnm_site_stats));
+    if (n_sites) {
+        // ~80 B per site: a 10k-site registry is 0.8 MB on every step's
+        // critical path, spread over a few pool threads
+        const size_t bytes = static_cast<size_t>(n_sites) * sizeof(gnm_site_stats);
+        staged_copy(c, {{reinterpret_cast<unsigned char*>(r->sites), reinterpret_cast<const unsigned char*>(c->h_out),
+                         bytes}},
+                    std::min<unsigned>(GNM_RESULT_COPY_THREADS, stage_threads(c)));
+    }
     const auto* t = reinterpret_cast<const uint64_t*>(c->h_out + n_sites);
     r->tallies.forward = t[0];
     r->tallies.pure_ack = t[1];
