@@ -94,7 +94,7 @@ inline void cpu_relax() {
 class WorkerPool {
 public:
     explicit WorkerPool(unsigned n) {
-        for (unsigned i = 0; i < n; ++i) th_.emplace_back([this] { loop(); });
+        for (unsigned i = 0; i < n; ++i) th_.emplace_back([this, i] { loop(i); });
     }
     ~WorkerPool() {
         {
@@ -115,6 +115,7 @@ public:
         done_.store(0);
         // state = run id (24 bits) | nt (8 bits) | next task (32 bits); one
         // fetch_add claims a task of exactly the run it belongs to
+        last_nt_.store(nt);
         run_id_ = (run_id_ + 1) & 0xFFFFFFu;
         state_.store(static_cast<uint64_t>(run_id_) << 40 | static_cast<uint64_t>(nt) << 32 | 1u);
         if (sleepers_.load() > 0) {
@@ -137,18 +138,26 @@ public:
     }
 
 private:
-    static constexpr auto kSpin = std::chrono::microseconds(3000);
-    void loop() {
+    // GNM_POOL_SPIN_US overrides the spin before sleeping (0: sleep at once)
+    const std::chrono::microseconds kSpin{[] {
+        const char* e = std::getenv("GNM_POOL_SPIN_US");
+        return e ? std::atol(e) : 3000L;
+    }()};
+    // Worker `index` spins only if the last run used that many threads: a
+    // small run (the result copy) leaves the rest of a loader-sized pool
+    // asleep instead of spinning on the cores the caller's host work needs.
+    void loop(unsigned index) {
         uint32_t seen = 0;
         for (;;) {
             uint64_t st = state_.load();
             if (static_cast<uint32_t>(st >> 40) == seen) {
+                const bool spin = index + 1 < last_nt_.load();
                 const auto t0 = std::chrono::steady_clock::now();
                 for (unsigned k = 1;; ++k) {
                     cpu_relax(); // leave the core's other hardware thread its issue slots
                     st = state_.load();
                     if (static_cast<uint32_t>(st >> 40) != seen || stop_.load()) break;
-                    if ((k & 1023u) == 0 && std::chrono::steady_clock::now() - t0 > kSpin) {
+                    if (!spin || ((k & 1023u) == 0 && std::chrono::steady_clock::now() - t0 > kSpin)) {
                         std::unique_lock<std::mutex> l(m_);
                         sleepers_.fetch_add(1);
                         cv_.wait(l, [&] { return static_cast<uint32_t>(state_.load() >> 40) != seen || stop_.load(); });
@@ -178,6 +187,7 @@ private:
     std::atomic<uint64_t> state_{0};
     std::atomic<unsigned> done_{0};
     std::atomic<int> sleepers_{0};
+    std::atomic<unsigned> last_nt_{0};
     std::atomic<bool> stop_{false};
     uint32_t run_id_ = 0;
 };
