@@ -41,6 +41,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "hosts.cuh"
@@ -498,12 +500,6 @@ __global__ void h_rank(const uint32_t* __restrict__ hs_sorted, uint32_t n, unsig
         keys[hs_sorted[i]] = i;
 }
 
-// Flat per-flow row ids in place of the slots.
-__global__ void h_to_rows(uint32_t* __restrict__ slot_row, uint32_t n, const unsigned long long* __restrict__ rank) {
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
-        slot_row[j] = static_cast<uint32_t>(rank[slot_row[j]]);
-}
-
 // ---- per-row exact lower median, two rounds (rows * 628 B L2-resident) -------
 // The sites' scheme (kernels.cuh): coarse counts per (super-bucket, row),
 // super-bucket-major; each row's median super-bucket and the median's rank
@@ -684,6 +680,18 @@ __global__ void h_keys(const uint32_t* __restrict__ row, const uint32_t* __restr
         sk[j] = static_cast<K>(row[j]) << kBucketBits | bk[j];
 }
 
+// h_to_rows + h_keys in one pass: every flow's slot becomes its row (in
+// place) and its (row, bucket) sort key is written.
+template <typename K>
+__global__ void h_rows_keys(uint32_t* __restrict__ row, const uint32_t* __restrict__ bk, uint32_t n,
+                            const unsigned long long* __restrict__ rank, K* __restrict__ sk) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const uint32_t r = static_cast<uint32_t>(rank[row[j]]);
+        row[j] = r;
+        sk[j] = static_cast<K>(r) << kBucketBits | bk[j];
+    }
+}
+
 // start[row] = first position of the row's run; start[n_rows] = n.
 template <typename K>
 __global__ void h_starts(const K* __restrict__ sk, uint32_t n, uint32_t n_rows, uint32_t* __restrict__ start) {
@@ -771,15 +779,19 @@ struct Scratch {
 };
 
 // h.sorted: every flow's (row, bucket) key in (row, bucket) order.
+// With `rank`, h.row_of still holds H1 slots and becomes rows on the way.
 template <typename K>
-cudaError_t sort_keys(int device, HostRows& h, cudaStream_t s) {
+cudaError_t sort_keys(int device, HostRows& h, cudaStream_t s, const unsigned long long* rank = nullptr) {
     Scratch tmp_(s);
     const uint32_t n = static_cast<uint32_t>(h.n_flows);
     K *sk = nullptr, *sk2 = nullptr;
     HCK(tmp_.get(&sk, n));
     HCK(dalloc(&sk2, n, s));
     h.sorted = sk2; // owned by `h` from here (free_hosts)
-    h_keys<K><<<grid_for(device, n, 256), 256, 0, s>>>(h.row_of, h.bkt, n, sk);
+    if (rank)
+        h_rows_keys<K><<<grid_for(device, n, 256), 256, 0, s>>>(h.row_of, h.bkt, n, rank, sk);
+    else
+        h_keys<K><<<grid_for(device, n, 256), 256, 0, s>>>(h.row_of, h.bkt, n, sk);
     HCK(cudaGetLastError());
     const int end_bit = static_cast<int>(kBucketBits) + std::max(1, bits_for(h.n_rows));
     size_t tb = 0;
@@ -795,10 +807,10 @@ cudaError_t ensure_sorted(int device, HostRows& h, cudaStream_t s) {
 }
 
 template <typename K>
-cudaError_t finish_sorted(int device, HostRows& h, const unsigned long long* acc, const unsigned long long* hk_sorted,
-                          const uint32_t* hs_sorted, cudaStream_t s) {
+cudaError_t finish_sorted(int device, HostRows& h, const unsigned long long* rank, const unsigned long long* acc,
+                          const unsigned long long* hk_sorted, const uint32_t* hs_sorted, cudaStream_t s) {
     Scratch tmp_(s);
-    HCK(ensure_sorted(device, h, s));
+    if (!h.sorted && h.n_flows) HCK(sort_keys<K>(device, h, s, rank));
     const uint32_t n = static_cast<uint32_t>(h.n_flows);
     uint32_t* start = nullptr;
     HCK(tmp_.get(&start, static_cast<size_t>(h.n_rows) + 1));
@@ -956,6 +968,20 @@ cudaError_t build_hosts_local(int device, const HostSlice* slices, int n_slices,
     return cudaSuccess;
 }
 
+// The median scheme for `rows` rows: the L2-resident two-round counts
+// (rows * 628 B <= 64 MB) or the sort. GNM_HOSTS_MEDIAN=sort|two forces one
+// (measurement; both are exact).
+static bool two_round_median(uint32_t rows) {
+    static const int force = [] {
+        const char* e = std::getenv("GNM_HOSTS_MEDIAN");
+        if (!e) return 0;
+        return std::strcmp(e, "sort") == 0 ? 1 : (std::strcmp(e, "two") == 0 ? 2 : 0);
+    }();
+    if (force == 1) return false;
+    if (force == 2) return rows < (1u << 24); // h_coarse's key packs the row in 24 bits
+    return static_cast<size_t>(rows) * kCoarseH * 4 <= kTwoRoundBytes;
+}
+
 cudaError_t finish_hosts(int device, HostRows& out, HostLocal& loc, cudaStream_t s) {
     cudaError_t e = cudaSuccess;
     if (out.n_flows) {
@@ -963,16 +989,13 @@ cudaError_t finish_hosts(int device, HostRows& out, HostLocal& loc, cudaStream_t
         e = dalloc(&out.rows, n_rows, s);
         // H3..H5: the exact lower median per row (slots become rows on the way).
         if (e == cudaSuccess) {
-            if (static_cast<size_t>(n_rows) * kCoarseH * 4 <= kTwoRoundBytes) {
+            if (two_round_median(n_rows)) {
                 e = finish_two_round(device, out, loc.table, loc.acc, loc.hk_sorted, loc.hs_sorted, s);
             } else {
-                h_to_rows<<<grid_for(device, out.n_flows, 256), 256, 0, s>>>(
-                    out.row_of, static_cast<uint32_t>(out.n_flows), loc.table);
-                e = cudaGetLastError();
-                if (e == cudaSuccess)
-                    e = out.key64 ? finish_sorted<unsigned long long>(device, out, loc.acc, loc.hk_sorted,
-                                                                      loc.hs_sorted, s)
-                                  : finish_sorted<uint32_t>(device, out, loc.acc, loc.hk_sorted, loc.hs_sorted, s);
+                e = out.key64 ? finish_sorted<unsigned long long>(device, out, loc.table, loc.acc, loc.hk_sorted,
+                                                                  loc.hs_sorted, s)
+                              : finish_sorted<uint32_t>(device, out, loc.table, loc.acc, loc.hk_sorted,
+                                                        loc.hs_sorted, s);
             }
         }
     }
