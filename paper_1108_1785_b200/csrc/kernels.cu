@@ -70,6 +70,11 @@ constexpr uint32_t kLimbFlush = 1u << 28;
 constexpr uint32_t kQueue = 96; // per-warp queue capacity: < 32 left + 2 x 32 pushed
 // The top kCoarseSlots hot slots also keep their coarse counts in shared memory.
 constexpr uint32_t kCoarseSlots = 32;
+// Hot slots 1..kTopReplicas all belong to the most sampled site (a power of 2).
+#ifndef GNM_TOP_REPLICAS
+#define GNM_TOP_REPLICAS 4
+#endif
+constexpr uint32_t kTopReplicas = GNM_TOP_REPLICAS;
 // K2b's shared-memory fine rows for the heaviest sites.
 constexpr uint32_t kHeavy = 64;
 constexpr uint32_t kHeavyNone = 0xFFFFFFu;
@@ -431,7 +436,8 @@ __device__ __forceinline__ uint32_t accumulate(uint32_t code, uint32_t oct, uint
         return site;
     }
 #endif
-    const uint32_t slot = kHot ? (v >> 20) & 0x7FFu : 0u;
+    uint32_t slot = kHot ? (v >> 20) & 0x7FFu : 0u;
+    if (kHot && slot == 1u) slot += threadIdx.x & (kTopReplicas - 1); // the top site's replicas (k_hot_select)
     unsigned long long cmn = 0, cmx = ~0ull;
     if (kHot && slot) { // issued early: the latency hides behind the division
         cmn = h.mn[slot];
@@ -1074,16 +1080,27 @@ __global__ void __launch_bounds__(kSelectBlock) k_hot_select(uint32_t* __restric
     __shared__ uint32_t bins[kCountBins];
     __shared__ uint32_t part[kSelectBlock];
     __shared__ uint32_t cut, cut_a, next, next_a;
+    __shared__ unsigned long long top; // count << 32 | site of the most sampled site
     for (uint32_t i = threadIdx.x; i < kCountBins; i += blockDim.x) bins[i] = 0;
-    if (threadIdx.x == 0) next = 0;
+    if (threadIdx.x == 0) {
+        next = 0;
+        top = 0;
+    }
     __syncthreads();
+    unsigned long long best = 0;
     for (uint32_t s4 = threadIdx.x * 4; s4 < n_sites; s4 += blockDim.x * 4) { // 16-byte loads
         const uint4 c4 = *reinterpret_cast<const uint4*>(cnt + s4);
         const uint32_t cs[4] = {c4.x, c4.y, c4.z, c4.w};
 #pragma unroll
         for (uint32_t q = 0; q < 4; ++q)
-            if (s4 + q < n_sites && cs[q] >= thr) atomicAdd(&bins[min(cs[q], kCountBins - 1)], 1u);
+            if (s4 + q < n_sites && cs[q] >= thr) {
+                atomicAdd(&bins[min(cs[q], kCountBins - 1)], 1u);
+                best = max(best, static_cast<unsigned long long>(cs[q]) << 32 | (s4 + q));
+            }
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xFFFFFFFFu, best, o));
+    if ((threadIdx.x & 31u) == 0 && best) atomicMax(&top, best);
     __syncthreads();
     // Suffix sums over the bins: thread i owns bins [4i, 4i+4).
     const uint32_t i0 = threadIdx.x * (kCountBins / kSelectBlock);
@@ -1126,8 +1143,8 @@ __global__ void __launch_bounds__(kSelectBlock) k_hot_select(uint32_t* __restric
         uint32_t lc = 0xFFFFFFFFu, lca = 0xFFFFFFFFu;
         for (int k = kCountBins / kSelectBlock - 1; k >= 0; --k) {
             suffix += bins[i0 + k];
-            if (suffix <= kHotSlots) lc = i0 + k;
-            if (suffix <= kCoarseSlots) lca = i0 + k;
+            if (suffix <= kHotSlots - (kTopReplicas - 1)) lc = i0 + k;
+            if (suffix <= kCoarseSlots - (kTopReplicas - 1)) lca = i0 + k;
         }
         lc = __reduce_min_sync(0xFFFFFFFFu, lc);
         lca = __reduce_min_sync(0xFFFFFFFFu, lca);
@@ -1139,6 +1156,12 @@ __global__ void __launch_bounds__(kSelectBlock) k_hot_select(uint32_t* __restric
     __syncthreads();
     const uint32_t t = max(max(cut, thr), 1u);
     const uint32_t ta = max(cut_a, t);
+    // Slots 1..kTopReplicas: the most sampled site (~10% of a Zipf batch's
+    // Forward flows), one replica per lane & (kTopReplicas - 1) in K2, so its
+    // flows in one drain do not all add to the same shared-memory words.
+    // Reserved (unassigned) when no site is hot.
+    const uint32_t top_cnt = static_cast<uint32_t>(top >> 32);
+    const uint32_t top_site = top_cnt >= t ? static_cast<uint32_t>(top) : 0xFFFFFFFFu;
     // Slots 1..n_a: the top sites (count >= ta); the rest follow them.
     uint32_t n_a = 0;
     for (uint32_t b = threadIdx.x; b < kCountBins; b += blockDim.x)
@@ -1146,7 +1169,8 @@ __global__ void __launch_bounds__(kSelectBlock) k_hot_select(uint32_t* __restric
     n_a = __reduce_add_sync(0xFFFFFFFFu, n_a);
     if ((threadIdx.x & 31u) == 0 && n_a) atomicAdd(&next_a, n_a);
     __syncthreads();
-    const uint32_t base_b = next_a;
+    const uint32_t base_b = next_a - (top_site != 0xFFFFFFFFu && top_cnt >= ta ? 1u : 0u) + kTopReplicas;
+    if (threadIdx.x < kTopReplicas && top_site != 0xFFFFFFFFu) hot_site[1 + threadIdx.x] = top_site;
     __syncthreads();
     if (threadIdx.x == 0) next_a = 0;
     __syncthreads();
@@ -1163,7 +1187,8 @@ __global__ void __launch_bounds__(kSelectBlock) k_hot_select(uint32_t* __restric
         for (uint32_t q = 0; q < 4; ++q) {
             const uint32_t s = s4 + q;
             const bool in = s < n_sites;
-            const bool a = in && cs[q] >= ta, bclass = in && !a && cs[q] >= t;
+            const bool is_top = s == top_site;
+            const bool a = in && !is_top && cs[q] >= ta, bclass = in && !is_top && !a && cs[q] >= t;
             const unsigned ma = __ballot_sync(0xFFFFFFFFu, a), mb = __ballot_sync(0xFFFFFFFFu, bclass);
             uint32_t fa = 0, fb = 0;
             if (lane == 0) {
@@ -1175,9 +1200,10 @@ __global__ void __launch_bounds__(kSelectBlock) k_hot_select(uint32_t* __restric
             if (!in) continue;
             cnt[s] = 0;
             uint32_t slot = 0;
-            if (a) slot = fa + __popc(ma & lt) + 1;
+            if (a) slot = kTopReplicas + fa + __popc(ma & lt) + 1;
             else if (bclass) slot = base_b + fb + __popc(mb & lt) + 1;
             if (slot) hot_site[slot] = s;
+            if (is_top) slot = 1;
             site_slot[s] = slot;
         }
     }
@@ -1624,9 +1650,12 @@ bool plan_hot(int device, const DevBatch& b, const DevTable& t, const DevParams&
     (void)device;
     *err = cudaSuccess;
     if (!t.packed || n_sites == 0 || b.n == 0) return false;
-    // Sample 1/64 of the batch (at most 256k records) in 16..256 contiguous
+    // Sample 1/64 of the batch (at most GNM_K1_SAMPLE records) in 16..256 contiguous
     // chunks of about 1024 records (one CTA each).
-    uint64_t sample = std::min<uint64_t>(262144, b.n / 64);
+#ifndef GNM_K1_SAMPLE
+#define GNM_K1_SAMPLE 262144
+#endif
+    uint64_t sample = std::min<uint64_t>(GNM_K1_SAMPLE, b.n / 64);
     const uint32_t chunks = static_cast<uint32_t>(std::min<uint64_t>(256, std::max<uint64_t>(16, sample / 1024)));
     uint32_t chunk_len = static_cast<uint32_t>(sample / chunks);
     uint32_t thr;
