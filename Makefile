@@ -15,7 +15,7 @@ PKG := paper_1108_1785_b200
 SRCS := $(PKG)/csrc/capi.cu $(PKG)/csrc/kernels.cu $(PKG)/csrc/netflow.cu $(PKG)/csrc/hosts.cu $(PKG)/csrc/registry.cpp \
         $(PKG)/csrc/comm.cpp
 HDRS := include/gnetmon.h $(PKG)/csrc/kernels.cuh $(PKG)/csrc/netflow.cuh $(PKG)/csrc/hosts.cuh $(PKG)/csrc/registry.hpp \
-        $(PKG)/csrc/comm.hpp
+        $(PKG)/csrc/comm.hpp $(PKG)/csrc/rate.cuh
 
 .PHONY: all ref clean oracle ablation
 all: $(PKG)/lib/libgnetmon.so workloads/lib/libgnm_synth.so oracle

@@ -222,12 +222,11 @@ struct gnm_ctx {
     unsigned int* d_counts = nullptr;
     size_t counts_cap = 0, counts_used = 0;
     std::vector<LogSlice> slices;
-    // hosts mode (gnm_ctx_set_hosts): per-entry host, rate bits, micro-bps
+    // hosts mode (gnm_ctx_set_hosts): per-entry host, octets, duration
     bool hosts = false;
     unsigned int* d_lhost = nullptr;
-    unsigned long long* d_lrate = nullptr;
-    unsigned long long* d_llo = nullptr;
-    unsigned int* d_lhi = nullptr;
+    unsigned int* d_loct = nullptr;
+    unsigned long long* d_ldur = nullptr;
     size_t lhost_cap = 0;
     gnm::HostRows hrows;
     gnm::HostLocal hlocal;   // hosts local phase done (gnm_hosts_local_keys)
@@ -504,9 +503,8 @@ gnm::DevLog slice_view(const gnm_ctx* c, const gnm_ctx::LogSlice& sl) {
     lg.warp_cap = sl.warp_cap;
     lg.regions = sl.regions;
     lg.hosts = c->hosts ? c->d_lhost + sl.entry_off : nullptr;
-    lg.rates = c->hosts ? c->d_lrate + sl.entry_off : nullptr;
-    lg.ulo = c->hosts ? c->d_llo + sl.entry_off : nullptr;
-    lg.uhi = c->hosts ? c->d_lhi + sl.entry_off : nullptr;
+    lg.octs = c->hosts ? c->d_loct + sl.entry_off : nullptr;
+    lg.durs = c->hosts ? c->d_ldur + sl.entry_off : nullptr;
     return lg;
 }
 
@@ -550,11 +548,9 @@ gnm::DevLog reserve_log(gnm_ctx* c, const gnm::LaunchCfg& cfg, const gnm::DevBat
         size_t k = c->lhost_cap;
         grow_buf(c, &c->d_lhost, &k, used, want, "log hosts");
         k = c->lhost_cap;
-        grow_buf(c, &c->d_lrate, &k, used, want, "log rates");
+        grow_buf(c, &c->d_loct, &k, used, want, "log octets");
         k = c->lhost_cap;
-        grow_buf(c, &c->d_llo, &k, used, want, "log micro-bps");
-        k = c->lhost_cap;
-        grow_buf(c, &c->d_lhi, &k, used, want, "log micro-bps");
+        grow_buf(c, &c->d_ldur, &k, used, want, "log durations");
         c->lhost_cap = k;
     }
     c->log_used += need;
@@ -1394,9 +1390,8 @@ void gnm_ctx_destroy(gnm_ctx* c) {
     cudaFree(c->d_logb);
     cudaFree(c->d_counts);
     cudaFree(c->d_lhost);
-    cudaFree(c->d_lrate);
-    cudaFree(c->d_llo);
-    cudaFree(c->d_lhi);
+    cudaFree(c->d_loct);
+    cudaFree(c->d_ldur);
     gnm::free_hosts(c->hrows, c->stream);
     gnm::free_local(c->hlocal, c->stream);
     gnm::free_global(c->hglobal, c->stream);

@@ -46,6 +46,7 @@
 #include <vector>
 
 #include "hosts.cuh"
+#include "rate.cuh"
 
 namespace gnm {
 namespace {
@@ -380,15 +381,26 @@ __global__ void __launch_bounds__(kInsBlock, GNM_INS_CTAS_PER_SM) h_insert(
             const uint4 x = __ldcs(reinterpret_cast<const uint4*>(L.entries + pos));
             const uint4 hst = __ldcs(reinterpret_cast<const uint4*>(L.hosts + pos));
             const uint4 bb = L.buckets ? __ldcs(reinterpret_cast<const uint4*>(L.buckets + pos)) : make_uint4(0, 0, 0, 0);
-            const uint4 uh = __ldcs(reinterpret_cast<const uint4*>(L.uhi + pos));
-            const ulonglong2 lo01 = __ldcs(reinterpret_cast<const ulonglong2*>(L.ulo + pos));
-            const ulonglong2 lo23 = __ldcs(reinterpret_cast<const ulonglong2*>(L.ulo + pos + 2));
-            const ulonglong2 rt01 = __ldcs(reinterpret_cast<const ulonglong2*>(L.rates + pos));
-            const ulonglong2 rt23 = __ldcs(reinterpret_cast<const ulonglong2*>(L.rates + pos + 2));
+            const uint4 oc = __ldcs(reinterpret_cast<const uint4*>(L.octs + pos));
+            const ulonglong2 du01 = __ldcs(reinterpret_cast<const ulonglong2*>(L.durs + pos));
+            const ulonglong2 du23 = __ldcs(reinterpret_cast<const ulonglong2*>(L.durs + pos + 2));
             const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, hs[4] = {hst.x, hst.y, hst.z, hst.w};
-            const uint32_t bs[4] = {bb.x, bb.y, bb.z, bb.w}, us[4] = {uh.x, uh.y, uh.z, uh.w};
-            const unsigned long long los[4] = {lo01.x, lo01.y, lo23.x, lo23.y};
-            const unsigned long long rts[4] = {rt01.x, rt01.y, rt23.x, rt23.y};
+            const uint32_t bs[4] = {bb.x, bb.y, bb.z, bb.w};
+            // flow_rate and rate_ubps_of again (rate.cuh: the same arithmetic
+            // as K2, so the same bits), from the logged octets and duration
+            const uint32_t os[4] = {oc.x, oc.y, oc.z, oc.w};
+            const unsigned long long ds[4] = {du01.x, du01.y, du23.x, du23.y};
+            unsigned long long los[4], rts[4];
+            uint32_t us[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double rate = flow_rate_dev(os[q], ds[q]);
+                uint64_t lo, hi;
+                ubps_of(os[q], ds[q], rate, lo, hi);
+                los[q] = lo;
+                us[q] = static_cast<uint32_t>(hi);
+                rts[q] = static_cast<unsigned long long>(__double_as_longlong(rate));
+            }
             unsigned long long key[4], first[4];
             uint32_t h0[4];
 #pragma unroll

@@ -43,6 +43,7 @@
 #include <algorithm>
 
 #include "kernels.cuh"
+#include "rate.cuh"
 
 namespace gnm {
 namespace {
@@ -252,42 +253,7 @@ __device__ __forceinline__ void hot_init(const HotSmem& h, const DevHot& hot, co
 }
 
 // ---- per-flow arithmetic -----------------------------------------------------
-// Exact micro-bps of one flow, rate_ubps_of (rate_engine.cpp:100-107):
-// X = floor(octets * 8e9 / dur) as a 128-bit value (hi is non-zero only
-// when dur is a few ms and octets are huge).
-//
-// Fast path: the f64 rate (one IEEE division, needed for min/max anyway) is
-// within 2^-52 relative of 8000*oct/dur (2^-53 more when double(dur) rounds),
-// so y = rate * 1e6 is within 3*X*2^-53 of X; below rate 1e9 (X < 2^50)
-// that is < 0.375, and q = rint(y) satisfies |q - X| < 0.875. Hence
-// floor(X) is q or q - 1, decided by the sign of the exact residual
-// p - q*dur (|residual| < dur, so its 64-bit wrapped value is exact).
-// Everything else takes the exact integer division.
-__device__ __noinline__ uint4 ubps_slow(uint32_t oct, uint64_t dur) {
-    if (oct <= 2305843009u) {
-        const uint64_t q = static_cast<uint64_t>(oct) * 8000000000ull / dur;
-        return make_uint4(static_cast<uint32_t>(q), static_cast<uint32_t>(q >> 32), 0u, 0u);
-    }
-    const unsigned __int128 q = static_cast<unsigned __int128>(oct) * 8000000000ull / dur;
-    const uint64_t lo = static_cast<uint64_t>(q), hi = static_cast<uint64_t>(q >> 64);
-    return make_uint4(static_cast<uint32_t>(lo), static_cast<uint32_t>(lo >> 32),
-                      static_cast<uint32_t>(hi), static_cast<uint32_t>(hi >> 32));
-}
-
-__device__ __forceinline__ void ubps_of(uint32_t oct, uint64_t dur, double rate, uint64_t& lo,
-                                        uint64_t& hi) {
-    if (oct <= 2305843009u && rate < 1.0e9) {
-        const uint64_t pp = static_cast<uint64_t>(oct) * 8000000000ull;
-        const uint64_t q = __double2ull_rn(__dmul_rn(rate, 1.0e6));
-        const int64_t r = static_cast<int64_t>(pp - q * dur);
-        lo = r < 0 ? q - 1 : q;
-        hi = 0;
-        return;
-    }
-    const uint4 s = ubps_slow(oct, dur);
-    lo = static_cast<uint64_t>(s.y) << 32 | s.x;
-    hi = static_cast<uint64_t>(s.w) << 32 | s.z;
-}
+// flow_rate_dev / ubps_of / ubps_slow: rate.cuh (shared with hosts.cu).
 
 // bucket_index (rate_engine.cpp:119-125) from the exact quotient:
 // floor(RN(RN(8000*oct/dur)/1e4)) == floor(4*oct/(5*dur)) for every u32 oct
@@ -396,12 +362,14 @@ __device__ __forceinline__ uint32_t resolve(const uint32_t* __restrict__ gt, uin
 // Returns the site (kNone: Unmatched at /24) and the bucket.
 // K2 compile-time modes (kMode bits).
 constexpr int kModeWindow = 1; // FlowStore::snapshot window fused (DevParams::windowed)
-constexpr int kModeHosts = 2;  // hosts mode: log host, rate, micro-bps per Forward flow
+constexpr int kModeHosts = 2;  // hosts mode: log host, octets, duration per Forward flow
 
 struct FlowOut {
     uint32_t bucket = 0;
     unsigned long long rate_bits = 0;
     uint64_t lo = 0, hi = 0;
+    uint32_t oct = 0; // hosts mode: what H1 recomputes the rate and micro-bps from
+    uint64_t dur = 0;
 };
 
 template <bool kSmem, bool kHot>
@@ -411,6 +379,8 @@ __device__ __forceinline__ uint32_t accumulate(uint32_t code, uint32_t oct, uint
                                                FlowOut& fo) {
     uint32_t& bucket = fo.bucket;
     bucket = 0;
+    fo.oct = oct;
+    fo.dur = dur;
     // flow_rate (rate_engine.cpp:88-94): exact product, one IEEE division.
     // Issued before the lookup: it needs only the record, so its dependent
     // DFMA chain overlaps the table loads (an Unmatched item wastes it).
@@ -419,9 +389,9 @@ __device__ __forceinline__ uint32_t accumulate(uint32_t code, uint32_t oct, uint
     // results; measures what the exact division costs)
     const double rate = p.ablation == 5
         ? static_cast<double>(__fdividef(8000.0f * static_cast<float>(oct), static_cast<float>(dur)))
-        : __ddiv_rn(8000.0 * static_cast<double>(oct), __ull2double_rn(dur));
+        : flow_rate_dev(oct, dur);
 #else
-    const double rate = __ddiv_rn(8000.0 * static_cast<double>(oct), __ull2double_rn(dur));
+    const double rate = flow_rate_dev(oct, dur);
 #endif
     const uint32_t v = resolve<kSmem>(gt, code);
     if (v == kNone) {
@@ -563,12 +533,11 @@ __device__ __forceinline__ void log_entry(WarpQueue& wq, uint32_t lane, uint32_t
         } else {
             __stcs(wq.log + i, site << kLogSiteShift | fo.bucket);
         }
-        if constexpr (kHosts) { // the flow's host, rate and exact micro-bps
+        if constexpr (kHosts) { // the flow's host, octets and duration (H1 recomputes rate and micro-bps)
             const size_t j = wq.region_off + i;
             __stcs(L.hosts + j, host);
-            __stcs(L.rates + j, fo.rate_bits);
-            __stcs(L.ulo + j, static_cast<unsigned long long>(fo.lo));
-            __stcs(L.uhi + j, static_cast<unsigned int>(fo.hi));
+            __stcs(L.octs + j, fo.oct);
+            __stcs(L.durs + j, static_cast<unsigned long long>(fo.dur));
         }
     }
     wq.pos += __popc(m);
@@ -794,9 +763,8 @@ __device__ __forceinline__ void k2_epilogue(Ctr& t, WarpQueue& wq, uint32_t lane
         if constexpr (kHosts) {
             const size_t j = wq.region_off + i;
             L.hosts[j] = 0;
-            L.rates[j] = 0;
-            L.ulo[j] = 0;
-            L.uhi[j] = 0;
+            L.octs[j] = 0;
+            L.durs[j] = 1; // never read (past the count); a valid duration all the same
         }
     }
     flush_tallies(t, P.sums + static_cast<size_t>(P.n_sites) * 4);

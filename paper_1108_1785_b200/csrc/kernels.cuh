@@ -103,12 +103,12 @@ struct DevLog {
     uint32_t warp_cap;
     uint32_t regions;
     // Hosts mode (gnm_ctx_set_hosts), else null: per entry the matched host
-    // IP, the f64 rate bits and the exact micro-bps (lo, hi); indexed like
-    // `entries` from this slice's base.
+    // IP, the flow's octets and duration (H1 recomputes the f64 rate and the
+    // exact micro-bps from them: 16 bytes per flow instead of 24); indexed
+    // like `entries` from this slice's base.
     unsigned int* hosts;
-    unsigned long long* rates;
-    unsigned long long* ulo;
-    unsigned int* uhi;
+    unsigned int* octs;
+    unsigned long long* durs;
 };
 
 // Per-call hot-site plan: slot -> site (slots 1..n_slots), 0 slots = off.
