@@ -40,6 +40,7 @@
 #include <cub/device/device_select.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -60,6 +61,10 @@ int bits_for(uint64_t n) { // smallest b with 2^b >= n (n >= 1)
     while ((1ull << b) < n) ++b;
     return b;
 }
+
+// The post-pass kernels' dynamic shared-memory limits, set once per device
+// (cudaFuncSetAttribute costs host time on every call otherwise).
+cudaError_t hosts_attributes(int device);
 
 // H0, one block: exclusive scans of the per-warp-region log counts (flow
 // offsets `off`) and of their H1 work items (non-empty chunks of kInsChunk
@@ -848,7 +853,7 @@ cudaError_t finish_two_round(int device, HostRows& h, const unsigned long long* 
     HCK(tmp_.get(&fine, static_cast<size_t>(nr) * kFineH));
     HCK(cudaMemsetAsync(coarse, 0, static_cast<size_t>(nr) * kCoarseH * 4, s));
     HCK(cudaMemsetAsync(fine, 0, static_cast<size_t>(nr) * kFineH * 4, s));
-    HCK(cudaFuncSetAttribute(h_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kCoarseSmem)));
+    HCK(hosts_attributes(device));
     int sms = 0;
     HCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     const uint32_t cg = static_cast<uint32_t>(std::max<uint64_t>(
@@ -858,6 +863,19 @@ cudaError_t finish_two_round(int device, HostRows& h, const unsigned long long* 
     h_fine<<<grid_for(device, (n + 3) / 4, 256), 256, 0, s>>>(h.row_of, h.bkt, n, msb, fine);
     h_final2<<<grid_for(device, nr, 128), 128, 0, s>>>(acc, cnt, msb, mrank, fine, hk_sorted, hs_sorted, nr, h.rows);
     return cudaGetLastError();
+}
+
+cudaError_t hosts_attributes(int device) {
+    static std::atomic<uint64_t> done{0}; // one bit per device ordinal (< 64)
+    const uint64_t bit = device >= 0 && device < 64 ? 1ull << device : 0ull;
+    if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+    HCK(cudaFuncSetAttribute(h_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kCoarseSmem)));
+    HCK(cudaFuncSetAttribute(h_insert<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kInsSmem)));
+    HCK(cudaFuncSetAttribute(h_insert<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kInsSmem)));
+    done.fetch_or(bit, std::memory_order_release);
+    return cudaSuccess;
 }
 
 } // namespace
@@ -888,10 +906,7 @@ cudaError_t build_hosts_local(int device, const HostSlice* slices, int n_slices,
     HCK(cudaStreamSynchronize(s));
     const uint64_t n = h_scal[0];
     if (n == 0) return cudaSuccess;
-    HCK(cudaFuncSetAttribute(h_insert<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kInsSmem)));
-    HCK(cudaFuncSetAttribute(h_insert<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kInsSmem)));
+    HCK(hosts_attributes(device));
     int sms = 0;
     HCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     // H1: dense ids when the registry's /16 blocks allow (every host lies in
@@ -1138,7 +1153,7 @@ cudaError_t hosts_global_begin(int device, HostRows& out, const HostLocal& loc, 
                                                          g.min, g.max);
         const uint32_t nf = static_cast<uint32_t>(out.n_flows);
         g_rows<<<grid_for(device, nf, 256), 256, 0, s>>>(out.row_of, nf, loc.table, g.local_to_global);
-        HCK(cudaFuncSetAttribute(h_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kCoarseSmem)));
+        HCK(hosts_attributes(device));
         h_coarse<<<grid_for(device, nf, 512), 512, kCoarseSmem, s>>>(out.row_of, out.bkt, nf, static_cast<uint32_t>(n),
                                                            nullptr, g.coarse);
         HCK(cudaGetLastError());
