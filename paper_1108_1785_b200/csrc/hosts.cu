@@ -6,9 +6,10 @@
 // stats_from(hist) (finalize, rate_engine.cpp:272-289). Paths are relative to
 // /root/reference/proj/core/src.
 //
-// Here K2 (hosts mode) logs each Forward flow's site, bucket, host, f64 rate
-// bits and exact micro-bps; at finalize this post-pass turns the log into the
-// reference's rows without any per-host histogram storage:
+// Here K2 (hosts mode) logs each Forward flow's site, bucket, host, octets
+// and duration (H1 recomputes the f64 rate and exact micro-bps, rate.cuh);
+// at finalize this post-pass turns the log into the reference's rows without
+// any per-host histogram storage:
 //   H0  flat offsets: exclusive scan of the per-warp log counts;
 //   H1  give every (site, host) key a slot: a dense id from the registry's
 //       /16 directory when its non-empty /16 blocks allow (a host lies in a
