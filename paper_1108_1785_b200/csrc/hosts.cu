@@ -554,7 +554,11 @@ __device__ __forceinline__ void coarse_one(uint32_t r, uint32_t sb, uint32_t n_r
         atomicAdd(coarse + static_cast<size_t>(sb) * n_rows + r, 1u);
 }
 
-__global__ void __launch_bounds__(512) h_coarse(uint32_t* __restrict__ row, const uint32_t* __restrict__ bk,
+// kPack (local two-round path, rows < 2^18): instead of writing every
+// flow's row over its slot, write row << 14 | bucket over its bucket, so
+// h_fine (and any histogram export) reads one u32 column per flow, not two.
+template <bool kPack>
+__global__ void __launch_bounds__(512) h_coarse(uint32_t* __restrict__ row, uint32_t* __restrict__ bk,
                                                 uint32_t n, uint32_t n_rows, const unsigned long long* __restrict__ rank,
                                                 uint32_t* __restrict__ coarse) {
     extern __shared__ uint32_t hc_smem[];
@@ -573,7 +577,12 @@ __global__ void __launch_bounds__(512) h_coarse(uint32_t* __restrict__ row, cons
             const unsigned long long a = rank[rw.x], b = rank[rw.y], c = rank[rw.z], d = rank[rw.w];
             rw = make_uint4(static_cast<uint32_t>(a), static_cast<uint32_t>(b), static_cast<uint32_t>(c),
                             static_cast<uint32_t>(d));
-            __stcs(reinterpret_cast<uint4*>(row) + j, rw);
+            if constexpr (kPack)
+                __stcs(reinterpret_cast<uint4*>(bk) + j,
+                       make_uint4(rw.x << kBucketBits | bw.x, rw.y << kBucketBits | bw.y, rw.z << kBucketBits | bw.z,
+                                  rw.w << kBucketBits | bw.w));
+            else
+                __stcs(reinterpret_cast<uint4*>(row) + j, rw);
         }
         coarse_one(rw.x, bw.x >> 6, n_rows, tkey, tcnt, coarse);
         coarse_one(rw.y, bw.y >> 6, n_rows, tkey, tcnt, coarse);
@@ -582,8 +591,12 @@ __global__ void __launch_bounds__(512) h_coarse(uint32_t* __restrict__ row, cons
     }
     for (uint32_t j = n4 * 4 + blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
         const uint32_t r = rank ? static_cast<uint32_t>(rank[row[j]]) : row[j];
-        if (rank) row[j] = r;
-        coarse_one(r, bk[j] >> 6, n_rows, tkey, tcnt, coarse);
+        const uint32_t b = bk[j];
+        if (rank) {
+            if constexpr (kPack) bk[j] = r << kBucketBits | b;
+            else row[j] = r;
+        }
+        coarse_one(r, b >> 6, n_rows, tkey, tcnt, coarse);
     }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < kCoarseAgg; i += blockDim.x)
@@ -614,6 +627,7 @@ __global__ void h_msb(const uint32_t* __restrict__ coarse, uint32_t n_rows, uint
 
 // Four consecutive flows per lane per step, their msb gathers issued
 // together; lanes carrying the same (row, bucket) add once.
+template <bool kPacked> // bk holds row << 14 | bucket (row unused)
 __global__ void __launch_bounds__(256) h_fine(const uint32_t* __restrict__ row, const uint32_t* __restrict__ bk,
                                               uint32_t n, const uint32_t* __restrict__ msb,
                                               uint32_t* __restrict__ fine) {
@@ -624,19 +638,28 @@ __global__ void __launch_bounds__(256) h_fine(const uint32_t* __restrict__ row, 
         uint32_t rs[4] = {0, 0, 0, 0}, bs[4] = {0, 0, 0, 0}, ms[4];
         bool in[4] = {false, false, false, false};
         if (4 * j + 3 < n) {
-            const uint4 rw = __ldcs(reinterpret_cast<const uint4*>(row) + j);
             const uint4 bw = __ldcs(reinterpret_cast<const uint4*>(bk) + j);
-            rs[0] = rw.x, rs[1] = rw.y, rs[2] = rw.z, rs[3] = rw.w;
             bs[0] = bw.x, bs[1] = bw.y, bs[2] = bw.z, bs[3] = bw.w;
+            if constexpr (!kPacked) {
+                const uint4 rw = __ldcs(reinterpret_cast<const uint4*>(row) + j);
+                rs[0] = rw.x, rs[1] = rw.y, rs[2] = rw.z, rs[3] = rw.w;
+            }
             in[0] = in[1] = in[2] = in[3] = true;
         } else {
 #pragma unroll
             for (int q = 0; q < 4; ++q)
                 if (4 * j + q < n) {
-                    rs[q] = row[4 * j + q];
+                    if constexpr (!kPacked) rs[q] = row[4 * j + q];
                     bs[q] = bk[4 * j + q];
                     in[q] = true;
                 }
+        }
+        if constexpr (kPacked) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                rs[q] = bs[q] >> kBucketBits;
+                bs[q] &= kBucketMask;
+            }
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) ms[q] = in[q] ? __ldg(msb + rs[q]) : 0xFFFFFFFFu;
@@ -693,9 +716,9 @@ __global__ void h_final2(const unsigned long long* __restrict__ acc, const uint3
 // ---- per-row median from sorted (row, bucket) keys (many rows) -------------------
 template <typename K>
 __global__ void h_keys(const uint32_t* __restrict__ row, const uint32_t* __restrict__ bk, uint32_t n,
-                       K* __restrict__ sk) {
+                       K* __restrict__ sk, bool packed) {
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
-        sk[j] = static_cast<K>(row[j]) << kBucketBits | bk[j];
+        sk[j] = packed ? static_cast<K>(bk[j]) : static_cast<K>(row[j]) << kBucketBits | bk[j];
 }
 
 // h_to_rows + h_keys in one pass: every flow's slot becomes its row (in
@@ -754,10 +777,13 @@ __global__ void h_final(const unsigned long long* __restrict__ acc, const uint32
 }
 
 __global__ void h_hist(const uint32_t* __restrict__ row, const uint32_t* __restrict__ bk, uint64_t n,
-                       uint32_t* __restrict__ dense) {
+                       uint32_t* __restrict__ dense, bool packed) {
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-        atomicAdd(dense + static_cast<size_t>(row[i]) * kBuckets + bk[i], 1u);
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t b = bk[i];
+        const uint32_t r = packed ? b >> kBucketBits : row[i];
+        atomicAdd(dense + static_cast<size_t>(r) * kBuckets + (b & kBucketMask), 1u);
+    }
 }
 
 uint32_t grid_for(int device, uint64_t n, uint32_t block) {
@@ -809,7 +835,7 @@ cudaError_t sort_keys(int device, HostRows& h, cudaStream_t s, const unsigned lo
     if (rank)
         h_rows_keys<K><<<grid_for(device, n, 256), 256, 0, s>>>(h.row_of, h.bkt, n, rank, sk);
     else
-        h_keys<K><<<grid_for(device, n, 256), 256, 0, s>>>(h.row_of, h.bkt, n, sk);
+        h_keys<K><<<grid_for(device, n, 256), 256, 0, s>>>(h.row_of, h.bkt, n, sk, h.packed);
     HCK(cudaGetLastError());
     const int end_bit = static_cast<int>(kBucketBits) + std::max(1, bits_for(h.n_rows));
     size_t tb = 0;
@@ -859,9 +885,14 @@ cudaError_t finish_two_round(int device, HostRows& h, const unsigned long long* 
     HCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     const uint32_t cg = static_cast<uint32_t>(std::max<uint64_t>(
         1, std::min<uint64_t>((n + 511) / 512, static_cast<uint64_t>(sms) * GNM_HC_CTAS_PER_SM)));
-    h_coarse<<<cg, 512, kCoarseSmem, s>>>(h.row_of, h.bkt, n, nr, rank, coarse);
+    // rows < 2^18 here (rows * 628 B <= 64 MB): pack them into the bucket column
+    const bool pack = rank && nr < (1u << (32 - kBucketBits));
+    if (pack) h_coarse<true><<<cg, 512, kCoarseSmem, s>>>(h.row_of, h.bkt, n, nr, rank, coarse);
+    else h_coarse<false><<<cg, 512, kCoarseSmem, s>>>(h.row_of, h.bkt, n, nr, rank, coarse);
+    h.packed = pack;
     h_msb<<<grid_for(device, nr, 128), 128, 0, s>>>(coarse, nr, msb, mrank, cnt);
-    h_fine<<<grid_for(device, (n + 3) / 4, 256), 256, 0, s>>>(h.row_of, h.bkt, n, msb, fine);
+    if (pack) h_fine<true><<<grid_for(device, (n + 3) / 4, 256), 256, 0, s>>>(h.row_of, h.bkt, n, msb, fine);
+    else h_fine<false><<<grid_for(device, (n + 3) / 4, 256), 256, 0, s>>>(h.row_of, h.bkt, n, msb, fine);
     h_final2<<<grid_for(device, nr, 128), 128, 0, s>>>(acc, cnt, msb, mrank, fine, hk_sorted, hs_sorted, nr, h.rows);
     return cudaGetLastError();
 }
@@ -870,7 +901,8 @@ cudaError_t hosts_attributes(int device) {
     static std::atomic<uint64_t> done{0}; // one bit per device ordinal (< 64)
     const uint64_t bit = device >= 0 && device < 64 ? 1ull << device : 0ull;
     if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
-    HCK(cudaFuncSetAttribute(h_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kCoarseSmem)));
+    HCK(cudaFuncSetAttribute(h_coarse<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kCoarseSmem)));
+    HCK(cudaFuncSetAttribute(h_coarse<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kCoarseSmem)));
     HCK(cudaFuncSetAttribute(h_insert<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(kInsSmem)));
     HCK(cudaFuncSetAttribute(h_insert<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1155,7 +1187,7 @@ cudaError_t hosts_global_begin(int device, HostRows& out, const HostLocal& loc, 
         const uint32_t nf = static_cast<uint32_t>(out.n_flows);
         g_rows<<<grid_for(device, nf, 256), 256, 0, s>>>(out.row_of, nf, loc.table, g.local_to_global);
         HCK(hosts_attributes(device));
-        h_coarse<<<grid_for(device, nf, 512), 512, kCoarseSmem, s>>>(out.row_of, out.bkt, nf, static_cast<uint32_t>(n),
+        h_coarse<false><<<grid_for(device, nf, 512), 512, kCoarseSmem, s>>>(out.row_of, out.bkt, nf, static_cast<uint32_t>(n),
                                                            nullptr, g.coarse);
         HCK(cudaGetLastError());
     }
@@ -1166,7 +1198,7 @@ cudaError_t hosts_global_begin(int device, HostRows& out, const HostLocal& loc, 
 cudaError_t hosts_global_prepare(int device, const HostRows& out, HostGlobal& g, cudaStream_t s) {
     const uint32_t n = static_cast<uint32_t>(g.n), nf = static_cast<uint32_t>(out.n_flows);
     if (n) h_msb<<<grid_for(device, n, 128), 128, 0, s>>>(g.coarse, n, g.msb, g.mrank, g.cnt);
-    if (nf) h_fine<<<grid_for(device, (nf + 3) / 4, 256), 256, 0, s>>>(out.row_of, out.bkt, nf, g.msb, g.fine);
+    if (nf) h_fine<false><<<grid_for(device, (nf + 3) / 4, 256), 256, 0, s>>>(out.row_of, out.bkt, nf, g.msb, g.fine);
     g.prepared = true;
     return cudaGetLastError();
 }
@@ -1238,7 +1270,7 @@ void free_global(HostGlobal& g, cudaStream_t s) {
 
 cudaError_t hosts_histograms(int device, const HostRows& h, uint32_t* dense, cudaStream_t s) {
     if (h.n_flows == 0) return cudaSuccess;
-    h_hist<<<grid_for(device, h.n_flows, 256), 256, 0, s>>>(h.row_of, h.bkt, h.n_flows, dense);
+    h_hist<<<grid_for(device, h.n_flows, 256), 256, 0, s>>>(h.row_of, h.bkt, h.n_flows, dense, h.packed);
     return cudaGetLastError();
 }
 

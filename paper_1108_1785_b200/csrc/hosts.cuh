@@ -22,8 +22,9 @@ struct HostSlice {
 struct HostRows {
     gnm_host_stats* rows = nullptr;
     uint64_t n_rows = 0;
-    uint32_t* row_of = nullptr; // per flow: its row
-    uint32_t* bkt = nullptr;    // per flow: its bucket
+    uint32_t* row_of = nullptr; // per flow: its row (stale H1 slots when `packed`)
+    uint32_t* bkt = nullptr;    // per flow: its bucket, or row << 14 | bucket when `packed`
+    bool packed = false;        // the local two-round median packed the rows into bkt (rows < 2^18)
     uint64_t n_flows = 0;
     void* sorted = nullptr;     // (row << 14 | bucket) keys in order, u32 or u64 per key64; on demand
     bool key64 = false;
