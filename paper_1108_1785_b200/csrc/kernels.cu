@@ -789,6 +789,13 @@ __device__ __forceinline__ uint2 ld_rec_u2(const void* p, uint64_t pol) {
     asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(pol));
     return r;
 }
+__device__ __forceinline__ uint4 ld_rec_u4(const void* p, uint64_t pol) {
+    uint4 r;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(pol));
+    return r;
+}
 __device__ __forceinline__ ulonglong2 ld_rec_u64x2(const void* p, uint64_t pol) {
     ulonglong2 r;
     asm volatile("ld.global.nc.L2::cache_hint.v2.u64 {%0,%1}, [%2], %3;" : "=l"(r.x), "=l"(r.y) : "l"(p), "l"(pol));
@@ -841,16 +848,31 @@ __device__ __forceinline__ void load_tile(const DevBatch& b, uint32_t tile, uint
     if constexpr (kLayout == 4) {
         // entry words at 0,4 (start) 8,12 (end) 16 (src) 20 (dst) 32 (pkts)
         // 36 (octets) of the 64-byte entry (flow_store.cpp:158-162, netflow.cpp:52-75)
-        const uint32_t* wx = reinterpret_cast<const uint32_t*>(static_cast<const unsigned char*>(b.rec) +
-                                                                (static_cast<size_t>(tile) * 64u + lane) * 64u);
-        const uint32_t* wy = wx + 32u * 16u;
-        constexpr int kWord[8] = {0, 1, 2, 3, 4, 5, 8, 9};
+        if ((reinterpret_cast<uintptr_t>(b.rec) & 15u) == 4u) {
+            // The usual case (a 16-byte-aligned archive: entries at 20 + 64*i):
+            // the 16-byte vectors at entry - 4, + 12, + 28 hold entry words
+            // (-1, 0, 1, 2), (3, 4, 5, 6), (7, 8, 9, 10) -- three LDG.128 per
+            // record instead of eight LDG.32 (the -4 of entry 0 is the header).
+            const uint4* vx = reinterpret_cast<const uint4*>(static_cast<const unsigned char*>(b.rec) - 4 +
+                                                             (static_cast<size_t>(tile) * 64u + lane) * 64u);
+            const uint4* vy = vx + 32u * 4u;
+            const uint4 a0 = ld_rec_u4(vx, pol), a1 = ld_rec_u4(vx + 1, pol), a2 = ld_rec_u4(vx + 2, pol);
+            const uint4 b0 = ld_rec_u4(vy, pol), b1 = ld_rec_u4(vy + 1, pol), b2 = ld_rec_u4(vy + 2, pol);
+            t.x[0] = a0.y, t.x[1] = a0.z, t.x[2] = a0.w, t.x[3] = a1.x;
+            t.x[4] = a1.y, t.x[5] = a1.z, t.x[6] = a2.y, t.x[7] = a2.z;
+            t.y[0] = b0.y, t.y[1] = b0.z, t.y[2] = b0.w, t.y[3] = b1.x;
+            t.y[4] = b1.y, t.y[5] = b1.z, t.y[6] = b2.y, t.y[7] = b2.z;
+        } else {
+            const uint32_t* wx = reinterpret_cast<const uint32_t*>(static_cast<const unsigned char*>(b.rec) +
+                                                                    (static_cast<size_t>(tile) * 64u + lane) * 64u);
+            const uint32_t* wy = wx + 32u * 16u;
+            constexpr int kWord[8] = {0, 1, 2, 3, 4, 5, 8, 9};
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            t.x[q] = __ldg(wx + kWord[q]);
-            t.y[q] = __ldg(wy + kWord[q]);
+            for (int q = 0; q < 8; ++q) {
+                t.x[q] = __ldg(wx + kWord[q]);
+                t.y[q] = __ldg(wy + kWord[q]);
+            }
         }
-        (void)pol;
     } else if constexpr (kLayout == 5) {
         // compacted SoA: the duration column replaces start/end (ts = 0, te = dur)
         const DevSoA& c = b.soa;
