@@ -73,6 +73,9 @@ with Engine(0) as eng:
     arc = make_archive(cols)
     eng.decode_archive(arc)
     eng.aggregate_archive(arc, cat)
+    # the archive resident in HBM: k2_arc's 16-byte vector loads (entry - 4 reads the header)
+    import torch
+    eng.aggregate_archive(torch.from_numpy(np.frombuffer(arc, np.uint8).copy()).cuda(), cat)
 # in-library multi-rank combine: a loopback group (sites, per-host union,
 # histograms summed) and a world-size-1 NCCL communicator with graph replay
 from paper_1108_1785_b200 import Group
