@@ -1324,8 +1324,17 @@ __global__ void __launch_bounds__(128) k3a_median_sb(DevPartials P) {
 // (median super-bucket | heavy row << 8) in shared memory (small
 // registries), else read from L2/L1.
 constexpr uint32_t kMapSites = 12288; // 24 KB of static shared memory
+// Three 512-thread CTAs per SM with four 16-byte log vectors in flight per
+// lane (40 registers) measured ahead of two CTAs with eight (finalize 0.082
+// -> 0.080 ms, profiles/round2/ab_k2b_occupancy.txt).
+#ifndef GNM_K2B_CTAS
+#define GNM_K2B_CTAS 3
+#endif
+#ifndef GNM_K2B_V
+#define GNM_K2B_V 4
+#endif
 template <bool kMap, bool kWide>
-__global__ void __launch_bounds__(512, 2) k2b_fine(DevPartials P, DevLog L) {
+__global__ void __launch_bounds__(512, GNM_K2B_CTAS) k2b_fine(DevPartials P, DevLog L) {
     __shared__ uint32_t hf[kHeavy * kFineW];
     __shared__ uint4 map4[kMap ? kMapSites / 8 : 1];
     const uint16_t* map = reinterpret_cast<const uint16_t*>(map4);
@@ -1339,7 +1348,7 @@ __global__ void __launch_bounds__(512, 2) k2b_fine(DevPartials P, DevLog L) {
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     const uint32_t chunks = (L.warp_cap + kLogChunk - 1) / kLogChunk;
     const uint32_t items = L.regions * chunks;
-    constexpr uint32_t kV = kWide ? 4 : 8; // LDG.128 per lane in flight
+    constexpr uint32_t kV = kWide ? 4 : GNM_K2B_V; // LDG.128 per lane in flight
     // One log entry: skip unless in its site's median super-bucket; heavy
     // sites count in shared memory, the rest in L2.
     auto one = [&](uint32_t site, uint32_t bk) {
@@ -1725,8 +1734,8 @@ cudaError_t launch_k3a(int device, const DevPartials& P, cudaStream_t s) {
 
 cudaError_t launch_k2b(int device, const DevPartials& P, const DevLog& log, cudaStream_t s) {
     if (log.regions == 0) return cudaSuccess;
-    // Persistent: two CTAs per SM, so the heavy rows flush rarely.
-    const uint32_t grid = static_cast<uint32_t>(sm_count(device)) * 2;
+    // Persistent: GNM_K2B_CTAS CTAs per SM, so the heavy rows flush rarely.
+    const uint32_t grid = static_cast<uint32_t>(sm_count(device)) * GNM_K2B_CTAS;
     const bool wide = log.buckets != nullptr;
     if (P.n_sites <= kMapSites) {
         if (wide) k2b_fine<true, true><<<grid, 512, 0, s>>>(P, log);
